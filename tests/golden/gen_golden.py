@@ -1,0 +1,157 @@
+"""Generate golden vectors for the PPLL hot path FROM THE REFERENCE ITSELF.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/gen_golden.py
+
+It imports ``locopipe`` from ``/root/reference/pkg/src`` and drives its public
+API (``build_modules``, ``local_loss_and_update``, ``run_deterministic``,
+``run_epoch``) on fixed seeds, then writes small ``.npz`` fixtures next to this
+script.  Nothing at test time reads /root/reference: the fixtures travel.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+import locopipe as lp  # noqa: E402
+
+# (name, dims, s, d_prime, interval, seed, batch, steps, aux_hidden_width)
+CASES = [
+    ("mlp_s1", (48, 32, 10), 1, 0, 1, 7, 8, 4, None),
+    ("mlp_s2", (48, 40, 32, 24, 10), 2, 2, 3, 42, 16, 5, None),
+    ("mlp_s4", (96, 64, 64, 48, 40, 10), 4, 2, 3, 42, 16, 5, None),
+    ("mlp_s3_wide_aux", (40, 36, 28, 20, 10), 3, 1, 1, 5, 12, 4, 24),
+    ("mlp_s4_odd", (33, 17, 29, 13, 21, 7), 4, 3, 2, 11, 9, 6, None),
+]
+
+HYPER = dict(lr0=0.05, lr_min=0.001, momentum=0.9, weight_decay=1e-4)
+
+
+def make(dims, s, d_prime, interval, seed, total_steps, aux_hidden_width):
+    spec = lp.NetworkSpec(tuple(dims))
+    plan = lp.partition(spec, s)
+    hyper = lp.Hyperparams(total_steps=total_steps, seed=seed,
+                           aux_hidden_width=aux_hidden_width, **HYPER)
+    return plan, lp.build_modules(spec, plan, d_prime, interval, hyper)
+
+
+def flat(mod):
+    return np.concatenate([p.data.ravel() for p in mod.parameters()])
+
+
+def flat_m(mod):
+    return np.concatenate([mod.optimizer.buffer_for(p).ravel()
+                           for p in mod.parameters()])
+
+
+def gen_case(name, dims, s, d_prime, interval, seed, B, steps, ahw):
+    plan, mods = make(dims, s, d_prime, interval, seed, steps, ahw)
+    rng = np.random.default_rng(1000 + seed)
+    xs = rng.standard_normal((steps, B, dims[0]))
+    ys = rng.integers(0, dims[-1], size=(steps, B))
+    out = {
+        "dims": np.array(dims), "s": s, "d_prime": d_prime, "interval": interval,
+        "seed": seed, "batch": B, "steps": steps,
+        "aux_hidden_width": -1 if ahw is None else ahw,
+        "boundaries": np.array(plan.boundaries),
+        "assigned_aux_depth": np.array([m.assigned_aux_depth for m in mods]),
+        "xs": xs, "ys": ys,
+    }
+    for j, m in enumerate(mods):
+        out[f"init_{j}"] = flat(m)
+        out[f"shapes_{j}"] = np.array([list(p.shape) + [0] * (2 - len(p.shape))
+                                       for p in m.parameters()])
+    losses = np.zeros((s, steps))
+    for t in range(steps):
+        h = lp.Tensor(xs[t])
+        for j, m in enumerate(mods):
+            loss, h = lp.local_loss_and_update(m, h, ys[t])
+            losses[j, t] = loss
+            if t == 0:
+                out[f"xout0_{j}"] = h.data.copy()
+        # logits of the final stage after the step are not needed; x_out is
+    out["losses"] = losses
+    for j, m in enumerate(mods):
+        out[f"final_{j}"] = flat(m)
+        out[f"mom_{j}"] = flat_m(m)
+        out[f"step_count_{j}"] = m.optimizer.step_count
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    return losses
+
+
+def gen_threaded_equivalence():
+    """threaded PPLL (run_epoch) == sequential loop, on the reference."""
+    dims = (24, 20, 16, 12, 6)
+    data_rng = np.random.default_rng(5)
+    data = [(data_rng.standard_normal((6, 24)), data_rng.integers(0, 6, 6))
+            for _ in range(7)]
+    _, mods = make(dims, 3, 2, 1, 3, 20, None)
+    m = lp.run_epoch(lp.RunMode.PPLL, mods, iter(data), lp.RunConfig(buffer_capacity=2))
+    out = {"xs": np.stack([d[0] for d in data]), "ys": np.stack([d[1] for d in data]),
+           "losses": np.array(m.loss_history)}
+    for j, mod in enumerate(mods):
+        out[f"final_{j}"] = flat(mod)
+    np.savez_compressed(os.path.join(HERE, "threaded_ppll.npz"), **out)
+
+
+def gen_traces():
+    """Deterministic round-robin integer bookkeeping (runtime.py:475-533)."""
+    traces = []
+    for s, n, M in [(2, 4, 1), (2, 7, 2), (3, 5, 1), (3, 9, 3), (4, 6, 2),
+                    (4, 1, 1), (5, 12, 2), (1, 5, 2), (4, 0, 2)]:
+        dims = (4,) + (5,) * s + (2,)
+        _, mods = make(dims, s, 1, 1, 0, 64, None)
+        rng = np.random.default_rng(s * 100 + n)
+        data = [(rng.standard_normal((3, 4)), rng.integers(0, 2, 3)) for _ in range(n)]
+        m = lp.run_deterministic(lp.RunMode.PPLL, mods, iter(data),
+                                 lp.RunConfig(buffer_capacity=M))
+        traces.append({
+            "s": s, "n": n, "M": M, "wall_time": m.wall_time,
+            "busy_time": m.busy_time, "batches_processed": m.batches_processed,
+            "staleness": {str(k): v for k, v in sorted(m.staleness.items())},
+            "high_water": m.buffer_high_water, "n_batches": m.n_batches,
+        })
+    with open(os.path.join(HERE, "roundrobin_traces.json"), "w") as f:
+        json.dump(traces, f, indent=1, sort_keys=True)
+
+
+def gen_full_m():
+    """The CIFAR-shaped MLP analog (SURVEY §8 'M'): losses + param checksums."""
+    dims = (3072, 1024, 1024, 1024, 1024, 10)
+    steps, B = 3, 128
+    plan, mods = make(dims, 4, 2, 3, 42, 100, None)
+    rng = np.random.default_rng(0)
+    xs = rng.standard_normal((steps, B, 3072))
+    ys = rng.integers(0, 10, size=(steps, B))
+    losses = np.zeros((4, steps))
+    for t in range(steps):
+        h = lp.Tensor(xs[t])
+        for j, m in enumerate(mods):
+            loss, h = lp.local_loss_and_update(m, h, ys[t])
+            losses[j, t] = loss
+    out = {"losses": losses, "data_seed": 0, "steps": steps, "batch": B,
+           "boundaries": np.array(plan.boundaries)}
+    for j, m in enumerate(mods):
+        f = flat(m)
+        out[f"sum_{j}"] = f.sum()
+        out[f"abssum_{j}"] = np.abs(f).sum()
+        out[f"sq_{j}"] = (f * f).sum()
+        out[f"head_{j}"] = f[:256]
+        out[f"tail_{j}"] = f[-256:]
+    np.savez_compressed(os.path.join(HERE, "full_m.npz"), **out)
+
+
+if __name__ == "__main__":
+    for case in CASES:
+        print(case[0], gen_case(*case)[:, -1])
+    gen_threaded_equivalence()
+    gen_traces()
+    gen_full_m()
+    print("ok")
