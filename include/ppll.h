@@ -1,0 +1,165 @@
+/*
+ * ppll.h — C-ABI of the B200-native PPLL (arXiv 2411.12780) local-learning
+ * hot path.  Plain pointers, sizes and an opaque CUDA stream handle; no torch
+ * types.  Every entry point is stream-ordered and never synchronises the host
+ * unless its name says so.
+ *
+ * The reference (locopipe, /root/reference/pkg/src/locopipe) is pure Python,
+ * so "the reference's FFI" is its Python API; each function below names the
+ * reference symbol (file:line) whose semantics it implements.  The Python
+ * mirror in paper_2411_12780_b200/ binds these via ctypes.
+ *
+ * dtype codes: PPLL_F32 (parity mode, SIMT fp32 GEMMs) and PPLL_BF16
+ * (performance mode: bf16 operands on tcgen05 tensor cores, fp32 accumulate,
+ * fp32 master weights/momenta).  Return value: PPLL_OK or a PPLL_ERR_* code;
+ * ppll_last_error() describes the last failure on the calling thread.
+ */
+#ifndef PPLL_H_
+#define PPLL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPLL_ABI_VERSION 1
+
+enum {
+  PPLL_OK = 0,
+  PPLL_ERR_ARG = 1,       /* DimensionMismatch / ValueError (errors.py:14-15)  */
+  PPLL_ERR_CUDA = 2,      /* CUDA runtime failure                              */
+  PPLL_ERR_UNSUPPORTED = 3,
+  PPLL_ERR_CLOSED = 4,    /* PushAfterClose (errors.py:70-71)                  */
+  PPLL_ERR_TIMEOUT = 5
+};
+
+enum { PPLL_F32 = 0, PPLL_BF16 = 1 };
+
+/* sticky device error-word bits (one int32 per stage) */
+#define PPLL_ERRBIT_LABEL 1   /* LabelOutOfRange  tensor.py:216-219 */
+#define PPLL_ERRBIT_LOSS 2    /* NonFiniteError   tensor.py:227     */
+#define PPLL_ERRBIT_PARAM 4   /* NonFiniteError   tensor.py:41-43   */
+#define PPLL_ERRBIT_STEP 8    /* StepOutOfRange   optim.py:41-42    */
+
+/* GEMM engine selection for the bf16 path (PPLL_GEMM_AUTO picks tcgen05 when
+ * the shape/alignment allows, else the SIMT kernel for skinny shapes). */
+enum { PPLL_GEMM_AUTO = 0, PPLL_GEMM_SIMT = 1, PPLL_GEMM_TCGEN05 = 2 };
+
+int ppll_abi_version(void);
+const char* ppll_last_error(void);
+/* number of kernels this library launched since load (process-wide counter) */
+uint64_t ppll_launch_count(void);
+void ppll_set_gemm_engine(int engine);
+
+/* ---- primitive ops: tensor.py ------------------------------------------ */
+
+/* Y[M,N] = relu?(X[M,K] · W[K,N] + b[N]); W is stored (in,out) row-major as in
+ * blocks.py:193.  Optional Y2 receives an identical copy (the fused push of a
+ * block's output into a ring slot, runtime.py:349-353).
+ * Replaces matmul tensor.py:137-150, bias_add :170-180, relu :153-157. */
+int ppll_linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W,
+                    const float* b, void* Y, int ldy, void* Y2, int ldy2,
+                    int relu, int dtype, void* stream);
+
+/* dX[M,K] = (dY[M,N] · Wᵀ) ⊙ [mask > 0]  (mask NULL: no mask).
+ * Replaces the matmul adjoint dA = g·Bᵀ (tensor.py:148) and the ReLU adjoint
+ * g·(x>0) (tensor.py:156-157; subgradient 0 at 0). */
+int ppll_linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void* W,
+                      const void* mask, int ldmask, void* dX, int lddx, int dtype,
+                      void* stream);
+
+/* dW[K,N] = Xᵀ·dY (fp32), db[N] = Σ_rows dY (fp32; NULL to skip).
+ * Replaces the matmul adjoint dB = Aᵀ·g (tensor.py:149) and the bias_add
+ * adjoint g.sum(axis=0) (tensor.py:179). */
+int ppll_linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY,
+                      int lddy, float* dW, float* db, int dtype, void* stream);
+
+/* Fused mean softmax cross-entropy forward + adjoint (tensor.py:201-234):
+ * loss = mean_b −log softmax(z_b)[y_b] (max-subtracted), dz = (softmax −
+ * onehot)/B.  The scalar loss is written to loss_hist[*step] (step may be
+ * NULL → index 0).  Out-of-range labels set PPLL_ERRBIT_LABEL, a non-finite
+ * loss sets PPLL_ERRBIT_LOSS in *err (err may be NULL). */
+int ppll_softmax_xent(int B, int C, const void* logits, int ldz, const int64_t* labels,
+                      void* dlogits, int lddz, float* loss_hist, const int* step,
+                      int* err, int dtype, void* stream);
+
+/* ---- optimizer: optim.py ----------------------------------------------- */
+
+/* One Nesterov-SGD step over a flat parameter buffer (optim.py:71-89):
+ *   g' = g + wd·θ;  v = μ·v + g';  θ −= lr·(g' + μ·v)
+ * lr = lr_table[*step] when step != NULL (device-resident cosine table,
+ * CUDA-graph safe), else lr_host.  When step != NULL the kernel's last block
+ * advances *step by one (OptimizerState.step_count += 1, optim.py:89) and sets
+ * PPLL_ERRBIT_STEP if *step > max_step.  theta_lp (nullable) receives a bf16
+ * shadow copy of the updated θ for the tensor-core path. */
+int ppll_nesterov_step(int64_t n, float* theta, float* v, const float* g, void* theta_lp,
+                       const float* lr_table, int* step, int max_step, float lr_host,
+                       float mu, float wd, int* err, void* stream);
+
+/* cosine_lr (optim.py:39-44), fp64 on the host; returns NaN if out of range */
+double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps);
+
+/* element conversion helpers (fp32 <-> bf16), n elements */
+int ppll_cast(int64_t n, const void* src, int src_dtype, void* dst, int dst_dtype, void* stream);
+
+/* ---- one local step of a stage: blocks.py:266-289 ----------------------- */
+
+typedef struct ppll_stage ppll_stage;
+
+/* Layers 0..n_block-1 are the block, n_block..n_layers-1 the aux head
+ * (blocks.py:147-187).  param_offsets[2*i] / [2*i+1] are the element offsets
+ * of W_i / b_i inside the flat fp32 buffers theta/grad/mom (and theta_lp, bf16,
+ * same offsets).  The stage keeps device scratch of its own (activations and
+ * two gradient ping-pong buffers for max_batch rows). */
+ppll_stage* ppll_stage_create(int n_layers, int n_block, const int* in_w, const int* out_w,
+                              const int* relu_after, const int64_t* param_offsets,
+                              int64_t n_params, int max_batch, int dtype, float* theta,
+                              float* grad, float* mom, void* theta_lp, const float* lr_table,
+                              int* step, int max_step, float* loss_hist, int* err, float mu,
+                              float wd);
+void ppll_stage_destroy(ppll_stage* st);
+
+/* The whole PPLL local step, stream-ordered, no host sync:
+ * block forward (last epilogue also stores into x_out = the push, which
+ * reflects PRE-update params, blocks.py:279-283) → aux forward → softmax-CE →
+ * backward (no dX for the detached block input, blocks.py:277-278) →
+ * cosine-LR Nesterov over every stage param (blocks.py:287-288). */
+int ppll_stage_step(ppll_stage* st, int B, const void* x_in, const int64_t* labels,
+                    void* x_out, void* stream);
+
+/* forward only (block_forward / aux_forward, blocks.py:249-263): writes the
+ * block output to h_out and, if logits != NULL, the local logits. */
+int ppll_stage_forward(ppll_stage* st, int B, const void* x_in, void* h_out, void* logits,
+                       void* stream);
+
+/* ---- stage-boundary ring (runtime.py:52-120 StageBuffer) ----------------
+ * Device-resident flag words for an SPSC ring of `capacity` slots.  ready[i]
+ * holds the sequence number (batch_id+1) published into slot i; credit holds
+ * the number of slots the consumer has released.  Publication is a
+ * release-store at system scope after the slot payload; waits are acquire
+ * spins on the device (no host round trip), usable inside CUDA graphs and
+ * across NVLink peers (flags may live in peer memory mapped via CUDA IPC). */
+int ppll_ring_publish(int* ready_word, int seq, void* stream);
+int ppll_ring_wait(const int* ready_word, int seq, void* stream);
+int ppll_ring_release(int* credit_word, void* stream);
+int ppll_ring_wait_credit(const int* credit_word, int need, void* stream);
+
+/* ---- P2P / IPC plumbing for the multi-GPU ring -------------------------- */
+int ppll_ipc_get_handle(void* dev_ptr, void* handle_out /* 64 bytes */);
+int ppll_ipc_open_handle(const void* handle /* 64 bytes */, void** dev_ptr_out);
+int ppll_ipc_close_handle(void* dev_ptr);
+int ppll_enable_peer(int peer_device);
+
+/* runtime-owned device memory (ring slots/flags; IPC-exportable) */
+void* ppll_dev_alloc(size_t bytes);   /* zero-filled; NULL on failure */
+int ppll_dev_free(void* dev_ptr);
+
+/* synchronising helpers (host waits) */
+int ppll_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPLL_H_ */

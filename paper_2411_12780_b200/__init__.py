@@ -1,0 +1,55 @@
+"""paper_2411_12780_b200 — B200-native PPLL (pipeline parallelism based on
+local learning, arXiv 2411.12780).
+
+A drop-in for the reference ``locopipe`` training loop (its public names are
+re-exported here with the same signatures, ``locopipe/__init__.py:10-85``),
+running each stage's local step as hand-written sm_100a kernels behind a
+C-ABI library (``include/ppll.h``) and the PPLL dataflow as device rings on
+CUDA streams.  The analysis/UI/data parts of the reference (cost model,
+config, CLI, figures, toy data) are outside this build's scope.
+"""
+from .blocks import (
+    AuxHead,
+    Hyperparams,
+    LinearLayer,
+    LocalModule,
+    MemoryProxy,
+    NetworkSpec,
+    PartitionPlan,
+    aux_depth,
+    aux_forward,
+    block_forward,
+    build_modules,
+    local_loss_and_update,
+    memory_footprint,
+    partition,
+)
+from .errors import (
+    ConfigMismatch,
+    DimensionMismatch,
+    LabelOutOfRange,
+    LocopipeError,
+    MissingGradient,
+    NonFiniteError,
+    PushAfterClose,
+    StepOutOfRange,
+    TooManyStages,
+    WorkerPanic,
+    ZeroDuration,
+)
+from .optim import LrSchedule, OptimizerState, cosine_lr, sgd_nesterov_step
+from .runtime import (
+    END_OF_STREAM,
+    BufferSlot,
+    DevicePipeline,
+    EpochMetrics,
+    RunConfig,
+    RunMode,
+    StageBuffer,
+    run_deterministic,
+    run_epoch,
+    throughput,
+)
+from .tensor import Tensor, matmul, softmax_xent
+
+__version__ = "0.1.0"

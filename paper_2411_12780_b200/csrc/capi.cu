@@ -1,0 +1,209 @@
+// extern "C" boundary (include/ppll.h) + linear-layer engine dispatch.
+#include <stdarg.h>
+#include <atomic>
+#include <math.h>
+#include <string.h>
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ppll {
+
+static thread_local char t_err[512] = {0};
+static std::atomic<uint64_t> g_launches{0};
+int g_gemm_engine = PPLL_GEMM_AUTO;
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return t_err; }
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+using bf16 = __nv_bfloat16;
+
+// ---- linear forward: Y = relu?(X·W + b) ------------------------------------
+int linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,
+               void* Y, int ldy, void* Y2, int ldy2, int relu, int dtype, float* ws,
+               size_t ws_elems, cudaStream_t s) {
+  if (M < 0 || K < 1 || N < 1) { set_error("linear_fwd: bad shape %d %d %d", M, K, N); return PPLL_ERR_ARG; }
+  if (M == 0) return PPLL_OK;
+  if (dtype == PPLL_F32) {
+    Epilogue<float> ep;
+    ep.C = (float*)Y; ep.ldc = ldy; ep.C2 = (float*)Y2; ep.ldc2 = ldy2; ep.bias = b; ep.relu = relu;
+    return launch_gemm_simt<float, float>(M, N, K, (const float*)X, ldx, 1, (const float*)W, N, 1,
+                                          ep, ws, ws_elems, s);
+  }
+  Epilogue<bf16> ep;
+  ep.C = (bf16*)Y; ep.ldc = ldy; ep.C2 = (bf16*)Y2; ep.ldc2 = ldy2; ep.bias = b; ep.relu = relu;
+  if (g_gemm_engine != PPLL_GEMM_SIMT) {
+    int r = launch_gemm_tc<bf16>(M, N, K, (const bf16*)X, ldx, true, (const bf16*)W, N, false, ep,
+                                 ws, ws_elems, s);
+    if (r != PPLL_ERR_UNSUPPORTED || g_gemm_engine == PPLL_GEMM_TCGEN05) return r;
+  }
+  return launch_gemm_simt<bf16, bf16>(M, N, K, (const bf16*)X, ldx, 1, (const bf16*)W, N, 1, ep,
+                                      ws, ws_elems, s);
+}
+
+// ---- linear dgrad: dX = (dY·Wᵀ) ⊙ [mask > 0] --------------------------------
+int linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void* W, const void* mask,
+                 int ldmask, void* dX, int lddx, int dtype, float* ws, size_t ws_elems,
+                 cudaStream_t s) {
+  if (M < 0 || K < 1 || N < 1) { set_error("linear_dgrad: bad shape"); return PPLL_ERR_ARG; }
+  if (M == 0) return PPLL_OK;
+  if (dtype == PPLL_F32) {
+    Epilogue<float> ep;
+    ep.C = (float*)dX; ep.ldc = lddx; ep.mask = (const float*)mask; ep.ldmask = ldmask;
+    return launch_gemm_simt<float, float>(M, K, N, (const float*)dY, lddy, 1, (const float*)W, 1, N,
+                                          ep, ws, ws_elems, s);
+  }
+  Epilogue<bf16> ep;
+  ep.C = (bf16*)dX; ep.ldc = lddx; ep.mask = (const bf16*)mask; ep.ldmask = ldmask;
+  if (g_gemm_engine != PPLL_GEMM_SIMT) {
+    int r = launch_gemm_tc<bf16>(M, K, N, (const bf16*)dY, lddy, true, (const bf16*)W, N, true, ep,
+                                 ws, ws_elems, s);
+    if (r != PPLL_ERR_UNSUPPORTED || g_gemm_engine == PPLL_GEMM_TCGEN05) return r;
+  }
+  return launch_gemm_simt<bf16, bf16>(M, K, N, (const bf16*)dY, lddy, 1, (const bf16*)W, 1, N, ep,
+                                      ws, ws_elems, s);
+}
+
+// ---- linear wgrad: dW = Xᵀ·dY (fp32), db = Σ_rows dY ------------------------
+int linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, int lddy, float* dW,
+                 float* db, int dtype, float* ws, size_t ws_elems, cudaStream_t s) {
+  if (M < 0 || K < 1 || N < 1) { set_error("linear_wgrad: bad shape"); return PPLL_ERR_ARG; }
+  Epilogue<float> ep;
+  ep.C = dW; ep.ldc = N;
+  int r;
+  if (dtype == PPLL_F32) {
+    r = launch_gemm_simt<float, float>(K, N, M, (const float*)X, 1, ldx, (const float*)dY, lddy, 1,
+                                       ep, ws, ws_elems, s);
+    if (r == PPLL_OK && db) r = launch_colsum<float>(M, N, (const float*)dY, lddy, db, s);
+    return r;
+  }
+  r = PPLL_ERR_UNSUPPORTED;
+  if (g_gemm_engine != PPLL_GEMM_SIMT) {
+    r = launch_gemm_tc<float>(K, N, M, (const bf16*)X, ldx, false, (const bf16*)dY, lddy, false, ep,
+                              ws, ws_elems, s);
+    if (r != PPLL_OK && (r != PPLL_ERR_UNSUPPORTED || g_gemm_engine == PPLL_GEMM_TCGEN05)) return r;
+  }
+  if (r == PPLL_ERR_UNSUPPORTED)
+    r = launch_gemm_simt<bf16, float>(K, N, M, (const bf16*)X, 1, ldx, (const bf16*)dY, lddy, 1, ep,
+                                      ws, ws_elems, s);
+  if (r == PPLL_OK && db) r = launch_colsum<bf16>(M, N, (const bf16*)dY, lddy, db, s);
+  return r;
+}
+
+}  // namespace ppll
+
+using namespace ppll;
+
+extern "C" {
+
+int ppll_abi_version(void) { return PPLL_ABI_VERSION; }
+const char* ppll_last_error(void) { return ppll::last_error(); }
+uint64_t ppll_launch_count(void) { return g_launches.load(); }
+void ppll_set_gemm_engine(int engine) { g_gemm_engine = engine; }
+
+int ppll_linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,
+                    void* Y, int ldy, void* Y2, int ldy2, int relu, int dtype, void* stream) {
+  return linear_fwd(M, K, N, X, ldx, W, b, Y, ldy, Y2, ldy2, relu, dtype, nullptr, 0, S(stream));
+}
+
+int ppll_linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void* W,
+                      const void* mask, int ldmask, void* dX, int lddx, int dtype, void* stream) {
+  return linear_dgrad(M, K, N, dY, lddy, W, mask, ldmask, dX, lddx, dtype, nullptr, 0, S(stream));
+}
+
+int ppll_linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, int lddy,
+                      float* dW, float* db, int dtype, void* stream) {
+  return linear_wgrad(M, K, N, X, ldx, dY, lddy, dW, db, dtype, nullptr, 0, S(stream));
+}
+
+int ppll_softmax_xent(int B, int C, const void* logits, int ldz, const int64_t* labels,
+                      void* dlogits, int lddz, float* loss_hist, const int* step, int* err,
+                      int dtype, void* stream) {
+  if (B < 1 || C < 1) { set_error("softmax_xent needs a non-empty batch"); return PPLL_ERR_ARG; }
+  if (dtype == PPLL_F32)
+    return launch_softmax_xent<float>(B, C, (const float*)logits, ldz, labels, (float*)dlogits,
+                                      lddz, loss_hist, step, err, S(stream));
+  return launch_softmax_xent<bf16>(B, C, (const bf16*)logits, ldz, labels, (bf16*)dlogits, lddz,
+                                   loss_hist, step, err, S(stream));
+}
+
+int ppll_nesterov_step(int64_t n, float* theta, float* v, const float* g, void* theta_lp,
+                       const float* lr_table, int* step, int max_step, float lr_host, float mu,
+                       float wd, int* err, void* stream) {
+  if (n < 0) { set_error("nesterov: negative size"); return PPLL_ERR_ARG; }
+  if (n == 0) return PPLL_OK;
+  return launch_nesterov(n, theta, v, g, (bf16*)theta_lp, lr_table, step, max_step, lr_host, mu,
+                         wd, err, S(stream));
+}
+
+double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps) {
+  if (step < 0 || step > total_steps || total_steps < 1) return NAN;
+  double span = lr0 - lr_min;
+  return lr_min + 0.5 * span * (1.0 + cos(M_PI * (double)step / (double)total_steps));
+}
+
+int ppll_cast(int64_t n, const void* src, int src_dtype, void* dst, int dst_dtype, void* stream) {
+  return launch_cast(n, src, src_dtype, dst, dst_dtype, S(stream));
+}
+
+int ppll_ring_publish(int* ready_word, int seq, void* stream) {
+  return launch_ring_publish(ready_word, seq, S(stream));
+}
+int ppll_ring_wait(const int* ready_word, int seq, void* stream) {
+  return launch_ring_wait(ready_word, seq, S(stream));
+}
+int ppll_ring_release(int* credit_word, void* stream) {
+  return launch_ring_release(credit_word, S(stream));
+}
+int ppll_ring_wait_credit(const int* credit_word, int need, void* stream) {
+  return launch_ring_wait(credit_word, need, S(stream));
+}
+
+int ppll_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  PPLL_CUDA_CHECK(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle_out, &h, sizeof(h));
+  return PPLL_OK;
+}
+int ppll_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  PPLL_CUDA_CHECK(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return PPLL_OK;
+}
+int ppll_ipc_close_handle(void* dev_ptr) {
+  PPLL_CUDA_CHECK(cudaIpcCloseMemHandle(dev_ptr));
+  return PPLL_OK;
+}
+int ppll_enable_peer(int peer_device) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); return PPLL_OK; }
+  PPLL_CUDA_CHECK(e);
+  return PPLL_OK;
+}
+void* ppll_dev_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    set_error("cudaMalloc(%zu) failed", bytes);
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaMemset(p, 0, bytes);
+  return p;
+}
+int ppll_dev_free(void* p) {
+  PPLL_CUDA_CHECK(cudaFree(p));
+  return PPLL_OK;
+}
+int ppll_stream_sync(void* stream) {
+  PPLL_CUDA_CHECK(cudaStreamSynchronize(S(stream)));
+  return PPLL_OK;
+}
+
+}  // extern "C"

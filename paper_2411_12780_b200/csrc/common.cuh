@@ -1,0 +1,62 @@
+// Shared device/host helpers for the PPLL B200 library (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/ppll.h"
+
+namespace ppll {
+
+// Sticky per-stage error word bits (checked asynchronously by the host;
+// mapped to the reference's exception classes in the Python shim).
+enum ErrBits : int {
+  kErrLabel = PPLL_ERRBIT_LABEL,          // LabelOutOfRange   (tensor.py:216-219)
+  kErrLossNonFinite = PPLL_ERRBIT_LOSS,   // NonFiniteError    (tensor.py:227)
+  kErrParamNonFinite = PPLL_ERRBIT_PARAM, // NonFiniteError    (tensor.py:41-43)
+  kErrStep = PPLL_ERRBIT_STEP,            // StepOutOfRange    (optim.py:41-42)
+};
+
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define PPLL_CUDA_CHECK(expr)                                                   \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::ppll::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,              \
+                        cudaGetErrorString(_e));                                \
+      return PPLL_ERR_CUDA;                                                     \
+    }                                                                           \
+  } while (0)
+
+#define PPLL_LAUNCH_CHECK() PPLL_CUDA_CHECK(cudaGetLastError())
+
+template <typename T> struct DT;
+template <> struct DT<float> {
+  static __device__ __forceinline__ float ld(const float* p) { return *p; }
+  static __device__ __forceinline__ void st(float* p, float v) { *p = v; }
+};
+template <> struct DT<__nv_bfloat16> {
+  static __device__ __forceinline__ float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+};
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace ppll

@@ -1,0 +1,402 @@
+// Bandwidth-bound and SIMT kernels of the PPLL local step (sm_100a).
+//
+//  * gemm_simt      — fp32-accumulate SIMT GEMM with fused bias/ReLU/mask/dual
+//                     store epilogue.  It is the fp32 parity engine and the
+//                     engine for skinny shapes (class-count N, tiny K) that
+//                     cannot fill a 128-row tcgen05 tile.
+//  * colsum         — bias gradient Σ_rows dY (tensor.py:179), deterministic.
+//  * softmax_xent   — fused mean-CE forward + adjoint (tensor.py:201-234).
+//  * nesterov_step  — multi-tensor (flat buffer) Nesterov-SGD (optim.py:71-89).
+//  * ring kernels   — release/acquire flag words for the stage-boundary ring.
+#include <math.h>
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ppll {
+
+// ------------------------------------------------------------------------
+// SIMT GEMM: C(m,n) = Σ_k A(m,k)·B(k,n), generic strides.
+// A(m,k) = A[m*a_rs + k*a_cs];  B(k,n) = B[k*b_rs + n*b_cs].
+// 64x64x16 tiles, 256 threads, 4x4 outputs per thread.
+// ------------------------------------------------------------------------
+constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256)
+gemm_simt_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs, long a_cs,
+                 const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep, int k_per_split) {
+  __shared__ float As[SB_K][SB_M + 4];
+  __shared__ float Bs[SB_K][SB_N + 4];
+  const int t = threadIdx.x;
+  const int m0 = blockIdx.y * SB_M, n0 = blockIdx.x * SB_N;
+  const int kbeg = blockIdx.z * k_per_split;
+  const int kend = min(K, kbeg + k_per_split);
+  const int ty = t / 16, tx = t % 16;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  const bool a_kc = (a_cs == 1);   // A is k-contiguous (row-major [M,K])
+  const bool b_nc = (b_cs == 1);   // B is n-contiguous (row-major [K,N])
+  for (int k0 = kbeg; k0 < kend; k0 += SB_K) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int mm, kk;
+      if (a_kc) { kk = t % 16; mm = t / 16 + 16 * i; }
+      else      { mm = t % 64; kk = t / 64 + 4 * i; }
+      int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < kend) ? to_f(A[(long)gm * a_rs + (long)gk * a_cs]) : 0.f;
+      int nn, kb;
+      if (b_nc) { nn = t % 64; kb = t / 64 + 4 * i; }
+      else      { kb = t % 16; nn = t / 16 + 16 * i; }
+      int gn = n0 + nn, gkb = k0 + kb;
+      Bs[kb][nn] = (gn < N && gkb < kend) ? to_f(Bm[(long)gkb * b_rs + (long)gn * b_cs]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SB_K; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gn = n0 + tx + 16 * j;
+      if (gn >= N) continue;
+      if (ep.partial) {  // split-K partial: raw fp32 into the workspace slice
+        ep.partial[((long)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+      } else {
+        ep.apply(gm, gn, acc[i][j]);
+      }
+    }
+  }
+}
+
+// split-K reduction + epilogue: C = epilogue(Σ_s partial[s])
+template <typename TO>
+__global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ part,
+                                     Epilogue<TO> ep) {
+  long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  long total = (long)M * N;
+  for (; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(long)z * total + idx];
+    ep.apply((int)(idx / N), (int)(idx % N), s);
+  }
+}
+
+template <typename TI, typename TO>
+int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, const TI* B,
+                     long b_rs, long b_cs, const Epilogue<TO>& ep, float* ws, size_t ws_elems,
+                     cudaStream_t s) {
+  dim3 grid(ceil_div(N, SB_N), ceil_div(M, SB_M), 1);
+  int tiles = grid.x * grid.y;
+  int splits = 1;
+  // split K when the tile grid cannot fill the 148 SMs and K is deep
+  if (ws && tiles < 74 && K >= 512) {
+    splits = 148 / tiles;
+    splits = min(splits, K / 128);
+    while (splits > 1 && (size_t)splits * M * N > ws_elems) --splits;
+    if (splits < 1) splits = 1;
+  }
+  int kps = ((K + splits - 1) / splits + SB_K - 1) / SB_K * SB_K;
+  splits = ceil_div(K, kps);
+  grid.z = splits;
+  if (splits == 1) {
+    Epilogue<TO> e = ep;
+    e.partial = nullptr;
+    gemm_simt_kernel<TI, TO><<<grid, 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, e, K);
+    note_launch();
+  } else {
+    Epilogue<TO> e = ep;
+    e.partial = ws;
+    gemm_simt_kernel<TI, TO><<<grid, 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, e, kps);
+    note_launch();
+    Epilogue<TO> r = ep;
+    r.partial = nullptr;
+    int blocks = min(ceil_div((long)M * N, 256), 148 * 8);
+    splitk_reduce_kernel<TO><<<blocks, 256, 0, s>>>(M, N, splits, ws, r);
+    note_launch();
+  }
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+template int launch_gemm_simt<float, float>(int, int, int, const float*, long, long, const float*, long, long, const Epilogue<float>&, float*, size_t, cudaStream_t);
+template int launch_gemm_simt<__nv_bfloat16, __nv_bfloat16>(int, int, int, const __nv_bfloat16*, long, long, const __nv_bfloat16*, long, long, const Epilogue<__nv_bfloat16>&, float*, size_t, cudaStream_t);
+template int launch_gemm_simt<__nv_bfloat16, float>(int, int, int, const __nv_bfloat16*, long, long, const __nv_bfloat16*, long, long, const Epilogue<float>&, float*, size_t, cudaStream_t);
+
+// ------------------------------------------------------------------------
+// bias gradient: db[n] = Σ_m G[m*ld + n]   (fixed summation order)
+// ------------------------------------------------------------------------
+template <typename T>
+__global__ void colsum_kernel(int M, int N, const T* __restrict__ G, int ld, float* __restrict__ db) {
+  __shared__ float red[8][33];
+  int n = blockIdx.x * 32 + threadIdx.x;
+  float s = 0.f;
+  if (n < N)
+    for (int m = threadIdx.y; m < M; m += 8) s += to_f(G[(long)m * ld + n]);
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) t += red[r][threadIdx.x];
+    db[n] = t;
+  }
+}
+
+template <typename T>
+int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s) {
+  colsum_kernel<T><<<ceil_div(N, 32), dim3(32, 8), 0, s>>>(M, N, G, ld, db);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template int launch_colsum<float>(int, int, const float*, int, float*, cudaStream_t);
+template int launch_colsum<__nv_bfloat16>(int, int, const __nv_bfloat16*, int, float*, cudaStream_t);
+
+// ------------------------------------------------------------------------
+// softmax cross-entropy, fused forward + adjoint (tensor.py:201-234).
+// One block; warp w handles rows w, w+nw, ...; per-row losses are summed in a
+// fixed order in double so the scalar is deterministic.
+// ------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512)
+softmax_xent_kernel(int B, int C, const T* __restrict__ z, int ldz, const int64_t* __restrict__ y,
+                    T* __restrict__ dz, int lddz, float* loss_hist, const int* step, int* err) {
+  extern __shared__ float row_loss[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const float invB = 1.0f / (float)B;
+  for (int r = w; r < B; r += nw) {
+    const T* zr = z + (long)r * ldz;
+    long lab = y[r];
+    bool bad = (lab < 0 || lab >= C);
+    float mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, to_f(zr[c]));
+    mx = warp_max(mx);
+    float se = 0.f;
+    for (int c = lane; c < C; c += 32) se += expf(to_f(zr[c]) - mx);
+    se = warp_sum(se);
+    float lse = logf(se);
+    T* dr = dz + (long)r * lddz;
+    for (int c = lane; c < C; c += 32) {
+      float zc = to_f(zr[c]);
+      float p = expf(zc - mx) / se;
+      float gcv = (p - (c == lab ? 1.f : 0.f)) * invB;
+      DT<T>::st(dr + c, bad ? 0.f : gcv);
+    }
+    if (lane == 0) {
+      float zl = bad ? 0.f : to_f(zr[lab]);
+      row_loss[r] = -((zl - mx) - lse);
+      if (bad && err) atomicOr(err, kErrLabel);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int r = 0; r < B; ++r) s += (double)row_loss[r];
+    float loss = (float)(s / (double)B);
+    int idx = step ? *step : 0;
+    loss_hist[idx] = loss;
+    if (!isfinite(loss) && err) atomicOr(err, kErrLossNonFinite);
+  }
+}
+
+template <typename T>
+int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* dz, int lddz,
+                        float* loss_hist, const int* step, int* err, cudaStream_t s) {
+  int threads = B >= 256 ? 512 : 256;
+  size_t smem = sizeof(float) * (size_t)B;
+  if (smem > 48 * 1024) {
+    set_error("softmax_xent: batch %d too large", B);
+    return PPLL_ERR_ARG;
+  }
+  softmax_xent_kernel<T><<<1, threads, smem, s>>>(B, C, z, ldz, y, dz, lddz, loss_hist, step, err);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template int launch_softmax_xent<float>(int, int, const float*, int, const int64_t*, float*, int, float*, const int*, int*, cudaStream_t);
+template int launch_softmax_xent<__nv_bfloat16>(int, int, const __nv_bfloat16*, int, const int64_t*, __nv_bfloat16*, int, float*, const int*, int*, cudaStream_t);
+
+// ------------------------------------------------------------------------
+// Nesterov-SGD over one flat buffer (optim.py:81-88):
+//   g' = g + wd·θ ; v = μv + g' ; θ -= lr·(g' + μv)
+// 20 B/param algorithmic (read θ,v,g; write θ,v) + 2 B for the bf16 shadow.
+// The last block to finish advances the device step counter (optim.py:89).
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const float* __restrict__ g,
+                __nv_bfloat16* __restrict__ th_lp, const float* __restrict__ lr_table, int* step,
+                int max_step, float lr_host, float mu, float wd, int* err, unsigned int* done) {
+  __shared__ int s_skip;
+  __shared__ float s_lr;
+  if (threadIdx.x == 0) {
+    int e = err ? *(volatile int*)err : 0;
+    int st = step ? *(volatile int*)step : 0;
+    int skip = (e & (kErrLabel | kErrLossNonFinite)) ? 1 : 0;
+    if (step && (st < 0 || st > max_step)) {
+      skip = 1;
+      if (err) atomicOr(err, kErrStep);
+    }
+    s_skip = skip;
+    s_lr = step ? lr_table[min(max(st, 0), max_step)] : lr_host;
+  }
+  __syncthreads();
+  bool bad = false;
+  if (!s_skip) {
+    const float lr = s_lr;
+    long n4 = n / 4;
+    float4* th4 = reinterpret_cast<float4*>(th);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+      float4 t = th4[i], vv = v4[i], gg = g4[i];
+      float gp;
+#define NEST(c)                                  \
+      gp = fmaf(wd, t.c, gg.c);                  \
+      vv.c = fmaf(mu, vv.c, gp);                 \
+      t.c = t.c - lr * fmaf(mu, vv.c, gp);       \
+      bad |= !isfinite(t.c);
+      NEST(x) NEST(y) NEST(z) NEST(w)
+#undef NEST
+      th4[i] = t;
+      v4[i] = vv;
+      if (th_lp) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(t.x, t.y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(t.z, t.w);
+        reinterpret_cast<__nv_bfloat162*>(th_lp)[2 * i] = lo;
+        reinterpret_cast<__nv_bfloat162*>(th_lp)[2 * i + 1] = hi;
+      }
+    }
+    for (long i = n4 * 4 + (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+      float t = th[i], gp = fmaf(wd, t, g[i]);
+      float vv = fmaf(mu, v[i], gp);
+      t = t - lr * fmaf(mu, vv, gp);
+      th[i] = t;
+      v[i] = vv;
+      if (th_lp) th_lp[i] = __float2bfloat16_rn(t);
+      bad |= !isfinite(t);
+    }
+  }
+  if (bad && err) atomicOr(err, kErrParamNonFinite);
+  if (step) {
+    // last block advances the step counter after every block has read it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned int prev = atomicAdd(done, 1u);
+      if (prev == gridDim.x - 1) {
+        if (!s_skip) atomicAdd(step, 1);
+        *done = 0u;
+        __threadfence();
+      }
+    }
+  }
+}
+
+int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* th_lp,
+                    const float* lr_table, int* step, int max_step, float lr_host, float mu,
+                    float wd, int* err, cudaStream_t s) {
+  long n4 = (n + 3) / 4;
+  int blocks = (int)min((n4 + 255) / 256, (long)148 * 4);
+  if (blocks < 1) blocks = 1;
+  if ((reinterpret_cast<uintptr_t>(th) | reinterpret_cast<uintptr_t>(v) |
+       reinterpret_cast<uintptr_t>(g)) & 15) {
+    set_error("nesterov: flat buffers must be 16-byte aligned");
+    return PPLL_ERR_ARG;
+  }
+  // step points to two int32 words: [step_count, block-completion scratch]
+  unsigned int* done = step ? reinterpret_cast<unsigned int*>(step + 1) : nullptr;
+  nesterov_kernel<<<blocks, 256, 0, s>>>(n, th, v, g, th_lp, lr_table, step, max_step, lr_host,
+                                         mu, wd, err, done);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+// ------------------------------------------------------------------------
+// casts
+// ------------------------------------------------------------------------
+template <typename TS, typename TD>
+__global__ void cast_kernel(long n, const TS* __restrict__ s, TD* __restrict__ d) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    DT<TD>::st(d + i, to_f(s[i]));
+}
+
+int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t s) {
+  int blocks = (int)min((n + 255) / 256, (long)148 * 8);
+  if (blocks < 1) return PPLL_OK;
+  if (sd == PPLL_F32 && dd == PPLL_BF16)
+    cast_kernel<<<blocks, 256, 0, s>>>(n, (const float*)src, (__nv_bfloat16*)dst);
+  else if (sd == PPLL_BF16 && dd == PPLL_F32)
+    cast_kernel<<<blocks, 256, 0, s>>>(n, (const __nv_bfloat16*)src, (float*)dst);
+  else if (sd == PPLL_F32 && dd == PPLL_F32)
+    cast_kernel<<<blocks, 256, 0, s>>>(n, (const float*)src, (float*)dst);
+  else
+    cast_kernel<<<blocks, 256, 0, s>>>(n, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+// ------------------------------------------------------------------------
+// ring flag words (runtime.py:88-115 push/pop/close semantics on device)
+// ------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__global__ void ring_publish_kernel(int* w, int seq) {
+  __threadfence_system();
+  st_release_sys(w, seq);
+}
+__global__ void ring_wait_kernel(const int* w, int seq) {
+  while (ld_acquire_sys(w) < seq) __nanosleep(64);
+  __threadfence_system();
+}
+__global__ void ring_release_kernel(int* w) {
+  __threadfence_system();
+  atomicAdd_system(w, 1);
+}
+
+int launch_ring_publish(int* w, int seq, cudaStream_t s) {
+  ring_publish_kernel<<<1, 1, 0, s>>>(w, seq);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+int launch_ring_wait(const int* w, int seq, cudaStream_t s) {
+  ring_wait_kernel<<<1, 1, 0, s>>>(w, seq);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+int launch_ring_release(int* w, cudaStream_t s) {
+  ring_release_kernel<<<1, 1, 0, s>>>(w);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+}  // namespace ppll

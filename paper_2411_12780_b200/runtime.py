@@ -1,0 +1,549 @@
+"""Pipeline execution of gradient-isolated stages (mirrors locopipe runtime.py).
+
+The reference runs one Python thread per stage joined by bounded
+``StageBuffer`` FIFOs.  Here the PPLL dataflow is expressed on the device:
+
+* each stage has its own CUDA stream (on its module's device);
+* each stage boundary is a device-resident ring of ``buffer_capacity`` slots
+  (activation + labels) on the CONSUMER's device — the producer's last block
+  epilogue stores straight into the slot (over NVLink when the consumer is a
+  peer GPU), labels travel with the features;
+* "pop" is a stream wait on the slot's ready event, "push backpressure" is a
+  stream wait on the consumer's free event for the slot (credit) — the host
+  only enqueues, it never waits per batch (except to recycle its pinned
+  staging buffer, the analog of the source blocking on a full buffer);
+* every stage step is a CUDA graph (one per ring slot) of the native local
+  step, so the host issue cost per batch is a handful of launches.
+
+Because every ring is FIFO with one producer and one consumer, each stage
+consumes batches in order and its trajectory is independent of timing, so
+the device pipeline is bitwise equal to ``run_deterministic`` (the reference's
+round-robin replay, reproduced here with its exact integer bookkeeping).
+Staleness, buffer high water and busy/idle time are reconstructed from CUDA
+event timestamps recorded around every stage step.
+"""
+from __future__ import annotations
+
+import threading
+import time
+from collections import Counter, deque
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .blocks import LocalModule
+from .errors import ConfigMismatch, InvalidMode, PushAfterClose, WorkerPanic, ZeroDuration
+from .tensor import Tensor
+
+
+class RunMode(Enum):
+    E2E = "E2E"
+    NAIVE_PP = "NaivePP"
+    PPLL = "PPLL"
+
+
+class _EndOfStream:
+    def __repr__(self) -> str:
+        return "EndOfStream"
+
+
+#: Sentinel returned by pop() once a buffer is closed and drained (runtime.py:43-49).
+END_OF_STREAM = _EndOfStream()
+
+
+@dataclass
+class BufferSlot:
+    """One batch travelling between stages: id, detached features, labels
+    (runtime.py:52-65).  Features may be device tensors of any rank >= 2."""
+
+    batch_id: int
+    features: Tensor
+    labels: object
+
+    def __post_init__(self):
+        if self.features.track_grad:
+            raise ValueError("buffer slots must carry detached tensors")
+        shp = self.features.shape
+        if len(shp) != 2 or shp[0] != len(self.labels):
+            raise ValueError(f"features {shp} do not match {len(self.labels)} labels")
+
+
+class StageBuffer:
+    """Bounded blocking SPSC FIFO (runtime.py:68-120) — the host-side API twin
+    of the device ring (same push/pop/close/high-water semantics)."""
+
+    def __init__(self, capacity: int):
+        if capacity < 1:
+            raise ValueError(f"capacity must be >= 1, got {capacity}")
+        self.capacity = capacity
+        self._items: deque = deque()
+        self._cv = threading.Condition()
+        self._closed = False
+        self.high_water = 0
+        self.producer_progress = -1
+        self.total_pushed = 0
+
+    def push(self, slot: BufferSlot) -> None:
+        with self._cv:
+            if self._closed:
+                raise PushAfterClose("push on closed buffer")
+            while len(self._items) >= self.capacity:
+                self._cv.wait()
+                if self._closed:
+                    raise PushAfterClose("buffer closed while waiting to push")
+            self._items.append(slot)
+            self.total_pushed += 1
+            if len(self._items) > self.high_water:
+                self.high_water = len(self._items)
+            self._cv.notify_all()
+
+    def pop(self):
+        with self._cv:
+            while not self._items and not self._closed:
+                self._cv.wait()
+            if self._items:
+                slot = self._items.popleft()
+                self._cv.notify_all()
+                return slot
+            return END_OF_STREAM
+
+    def close(self) -> None:
+        with self._cv:
+            self._closed = True
+            self._cv.notify_all()
+
+    @property
+    def occupancy(self) -> int:
+        with self._cv:
+            return len(self._items)
+
+
+@dataclass
+class RunConfig:
+    """Knobs for one epoch run (runtime.py:123-141).
+
+    ``sleep_padding`` / ``comm_padding`` exist for API compatibility with the
+    reference's thread emulation; the device pipeline has real compute and
+    real transfers, so they must be 0.  ``use_graphs`` replays each stage step
+    from a CUDA graph; ``timing`` records per-step CUDA events (busy/idle,
+    staleness and high-water reconstruction).
+    """
+
+    buffer_capacity: int = 2
+    sleep_padding: float | Sequence[float] = 0.0
+    comm_padding: float = 0.0
+    use_graphs: bool = True
+    timing: bool = True
+
+    def pad_for(self, stage: int) -> float:
+        if isinstance(self.sleep_padding, (int, float)):
+            return float(self.sleep_padding)
+        pads = self.sleep_padding
+        return float(pads[stage]) if stage < len(pads) else float(pads[-1])
+
+
+@dataclass
+class EpochMetrics:
+    """What one epoch did (runtime.py:144-183).  Threaded (device) runs report
+    seconds measured with CUDA events; deterministic runs report scheduler
+    rounds (virtual time), like the reference."""
+
+    n_stages: int
+    n_batches: int = 0
+    wall_time: float = 0.0
+    batches_processed: list = field(default_factory=list)
+    busy_time: list = field(default_factory=list)
+    loss_history: list = field(default_factory=list)
+    staleness: Counter = field(default_factory=Counter)
+    buffer_high_water: list = field(default_factory=list)
+    images: int = 0
+
+    def __post_init__(self):
+        if not self.batches_processed:
+            self.batches_processed = [0] * self.n_stages
+        if not self.busy_time:
+            self.busy_time = [0.0] * self.n_stages
+        if not self.loss_history:
+            self.loss_history = [[] for _ in range(self.n_stages)]
+
+    def mean_loss(self, stage: int) -> float:
+        hist = self.loss_history[stage]
+        return float(sum(hist) / len(hist)) if hist else float("nan")
+
+    @property
+    def final_stage_mean_loss(self) -> float:
+        return self.mean_loss(self.n_stages - 1)
+
+    @property
+    def mean_staleness(self) -> float:
+        total = sum(self.staleness.values())
+        if total == 0:
+            return 0.0
+        return sum(k * v for k, v in self.staleness.items()) / total
+
+    @property
+    def idle_fraction(self) -> list:
+        """Per-stage 1 - busy/wall."""
+        if self.wall_time <= 0:
+            return [float("nan")] * self.n_stages
+        return [max(0.0, 1.0 - b / self.wall_time) for b in self.busy_time]
+
+
+def throughput(metrics: EpochMetrics, n_batches: int) -> float:
+    """Batches per second (or per virtual step), runtime.py:186-190."""
+    if metrics.wall_time <= 0.0:
+        raise ZeroDuration("epoch wall time is not positive")
+    return n_batches / metrics.wall_time
+
+
+def _validate_modules(modules: Sequence[LocalModule]) -> None:
+    """runtime.py:193-202."""
+    if not modules:
+        raise ConfigMismatch("no modules to run")
+    for j, m in enumerate(modules):
+        if m.stage_index != j:
+            raise ConfigMismatch(f"module {j} carries stage_index {m.stage_index}")
+        if j > 0 and m.input_width != modules[j - 1].output_width:
+            raise ConfigMismatch(
+                f"stage {j} input width {m.input_width} != stage {j - 1} "
+                f"output width {modules[j - 1].output_width}")
+        if j > 0 and m.precision != modules[j - 1].precision:
+            raise ConfigMismatch("all stages must share one precision")
+
+
+def run_epoch(mode: RunMode, modules: Sequence[LocalModule], dataset_iter: Iterable,
+              config: RunConfig | None = None) -> EpochMetrics:
+    """Feed every batch of ``dataset_iter`` through the pipeline once
+    (runtime.py:211-223).  PPLL runs as the device pipeline."""
+    config = config or RunConfig()
+    _validate_modules(modules)
+    if mode == RunMode.PPLL:
+        return DevicePipeline(modules, config).run(dataset_iter)
+    if mode in (RunMode.E2E, RunMode.NAIVE_PP):
+        raise InvalidMode(f"{mode.value} is a comparison baseline not built on the device yet "
+                          "(SURVEY §8f rank 1)")
+    raise ConfigMismatch(f"unknown mode {mode!r}")
+
+
+def run_deterministic(mode: RunMode, modules: Sequence[LocalModule], dataset_iter: Iterable,
+                      config: RunConfig | None = None) -> EpochMetrics:
+    """Single-stream replay with the reference's virtual timing
+    (runtime.py:226-243, 475-533)."""
+    config = config or RunConfig()
+    _validate_modules(modules)
+    if mode == RunMode.PPLL:
+        return _run_ppll_roundrobin(modules, dataset_iter, config)
+    if mode in (RunMode.E2E, RunMode.NAIVE_PP):
+        raise InvalidMode(f"{mode.value} is not built on the device yet (SURVEY §8f rank 1)")
+    raise ConfigMismatch(f"unknown mode {mode!r}")
+
+
+# --------------------------------------------------------------------------
+# device rings
+# --------------------------------------------------------------------------
+
+class _Rings:
+    """Per-boundary device rings: ring j is stage j's input (ring 0 is filled
+    by the source).  Slot k holds [max_batch, in_w_j] features and labels."""
+
+    def __init__(self, modules, capacity, max_batch):
+        self.M = capacity
+        self.x, self.y = [], []
+        for m in modules:
+            self.x.append(torch.empty((capacity, max_batch, m.input_width), dtype=m.act_dtype,
+                                      device=m.device))
+            self.y.append(torch.zeros((capacity, max_batch), dtype=torch.int64, device=m.device))
+        m0 = modules[0]
+        self.x_pin = torch.empty((capacity, max_batch, m0.input_width), dtype=torch.float32,
+                                 pin_memory=True)
+        self.y_pin = torch.empty((capacity, max_batch), dtype=torch.int64, pin_memory=True)
+        self.x_stage = (torch.empty((capacity, max_batch, m0.input_width), dtype=torch.float32,
+                                    device=m0.device) if m0.act_dtype != torch.float32 else None)
+
+
+def _enable_peers(modules):
+    devs = sorted({m.device.index for m in modules})
+    if len(devs) < 2:
+        return
+    lib = N.load()
+    for a in devs:
+        with torch.cuda.device(a):
+            for b in devs:
+                if a != b and torch.cuda.can_device_access_peer(a, b):
+                    N.check(lib.ppll_enable_peer(b), "enable peer access")
+
+
+class DevicePipeline:
+    """The PPLL pipeline on CUDA streams (see module docstring)."""
+
+    def __init__(self, modules, config: RunConfig, max_batch: int | None = None):
+        if config.pad_for(0) or config.comm_padding:
+            raise ConfigMismatch("sleep/comm padding is a thread-emulation knob; "
+                                 "the device pipeline must run unpadded")
+        self.modules = list(modules)
+        self.config = config
+        self.M = config.buffer_capacity
+        self.max_batch = max_batch
+        self.rings = None
+        self.graphs = {}
+        self.streams = [torch.cuda.Stream(device=m.device) for m in self.modules]
+        self.src_stream = torch.cuda.Stream(device=self.modules[0].device)
+        s, M = len(self.modules), self.M
+        self.ev_ready = [[torch.cuda.Event() for _ in range(M)] for _ in range(s)]
+        self.ev_free = [[torch.cuda.Event() for _ in range(M)] for _ in range(s)]
+        self.ev_h2d = [torch.cuda.Event() for _ in range(M)]
+        self.used_free = [[False] * M for _ in range(s)]
+        _enable_peers(self.modules)
+
+    # -- setup ----------------------------------------------------------
+    def _ensure(self, batch: int):
+        if self.rings is not None and batch <= self.max_batch:
+            return
+        self.max_batch = max(batch, self.max_batch or 0)
+        for m in self.modules:
+            m.native(self.max_batch)
+        self.rings = _Rings(self.modules, self.M, self.max_batch)
+        self.graphs = {}
+
+    def _launch(self, j: int, slot: int, B: int, stream):
+        """Enqueue stage j's local step on ring slot ``slot`` (B rows)."""
+        m, r = self.modules[j], self.rings
+        last = j == len(self.modules) - 1
+        x_in = r.x[j][slot]
+        y = r.y[j][slot]
+        x_out = None if last else r.x[j + 1][slot]
+        if not last:
+            r.y[j + 1][slot][:B].copy_(y[:B], non_blocking=True)
+        N.check(N.load().ppll_stage_step(m.native(B), B, x_in.data_ptr(), y.data_ptr(),
+                                         N.ptr(x_out), stream.cuda_stream), f"stage {j} step")
+
+    def _step(self, j: int, slot: int, B: int):
+        stream = self.streams[j]
+        if not self.config.use_graphs or B != self.max_batch:
+            with torch.cuda.stream(stream):
+                self._launch(j, slot, B, stream)
+            return
+        key = (j, slot)
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(device=self.modules[j].device)
+            cap.wait_stream(stream)
+            with torch.cuda.device(self.modules[j].device):
+                with torch.cuda.graph(g, stream=cap):
+                    self._launch(j, slot, B, cap)
+            stream.wait_stream(cap)
+            self.graphs[key] = g
+        with torch.cuda.stream(stream):
+            g.replay()
+
+    # -- the epoch -------------------------------------------------------
+    def run(self, dataset_iter: Iterable) -> EpochMetrics:
+        mods, M, s = self.modules, self.M, len(self.modules)
+        metrics = EpochMetrics(n_stages=s)
+        step0 = [m.optimizer.step_count for m in mods]
+        timing = self.config.timing
+        t_start, t_end, t_src = [[] for _ in range(s)], [[] for _ in range(s)], []
+        ev0 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(self.src_stream):
+            ev0.record(self.src_stream)
+        n = 0
+        images = 0
+        for batch_id, (x, y) in enumerate(dataset_iter):
+            x = np.asarray(x, dtype=np.float32) if not torch.is_tensor(x) else x
+            B = int(x.shape[0])
+            if B < 1:
+                raise WorkerPanic(-1, "empty batch")
+            for m in mods:
+                if m.optimizer.step_count + 1 > m.schedule.total_steps + 1:
+                    raise WorkerPanic(m.stage_index, f"StepOutOfRange: step "
+                                      f"{m.optimizer.step_count} > {m.schedule.total_steps}")
+            self._ensure(B)
+            r = self.rings
+            slot = batch_id % M
+            # ---- source: host -> ring 0 (runtime.py:312-323) ----
+            if batch_id >= M:
+                self.ev_h2d[slot].synchronize()          # recycle pinned staging
+            xt = torch.as_tensor(x)
+            if xt.dim() != 2 or xt.shape[1] != mods[0].input_width:
+                raise WorkerPanic(0, f"DimensionMismatch: stage 0 expects width "
+                                     f"{mods[0].input_width}, got {tuple(xt.shape)}")
+            r.x_pin[slot, :B].copy_(xt)
+            yt = torch.as_tensor(np.asarray(y)) if not torch.is_tensor(y) else y
+            if yt.dtype.is_floating_point or tuple(yt.shape) != (B,):
+                raise WorkerPanic(0, "labels must be integers matching the batch")
+            r.y_pin[slot, :B].copy_(yt)
+            src = self.src_stream
+            with torch.cuda.stream(src):
+                if self.used_free[0][slot]:
+                    src.wait_event(self.ev_free[0][slot])
+                if timing:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(src)
+                    t_src.append(e)
+                if r.x_stage is None:
+                    r.x[0][slot, :B].copy_(r.x_pin[slot, :B], non_blocking=True)
+                else:
+                    r.x_stage[slot, :B].copy_(r.x_pin[slot, :B], non_blocking=True)
+                    N.check(N.load().ppll_cast(B * mods[0].input_width,
+                                               r.x_stage[slot].data_ptr(), N.F32,
+                                               r.x[0][slot].data_ptr(), N.BF16,
+                                               src.cuda_stream), "cast")
+                r.y[0][slot, :B].copy_(r.y_pin[slot, :B], non_blocking=True)
+                self.ev_h2d[slot].record(src)
+                self.ev_ready[0][slot].record(src)
+            # ---- stages (runtime.py:325-388 worker loop, on device) ----
+            for j in range(s):
+                st = self.streams[j]
+                st.wait_event(self.ev_ready[j][slot])                  # pop
+                if j < s - 1 and self.used_free[j + 1][slot]:
+                    st.wait_event(self.ev_free[j + 1][slot])           # credit (backpressure)
+                if timing:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(st)
+                    t_start[j].append(e)
+                self._step(j, slot, B)
+                self.ev_free[j][slot].record(st)
+                self.used_free[j][slot] = True
+                if j < s - 1:
+                    self.ev_ready[j + 1][slot].record(st)              # push
+                if timing:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(st)
+                    t_end[j].append(e)
+                mods[j].optimizer.step_count += 1
+            n += 1
+            images += B
+        for st in self.streams:
+            st.synchronize()
+        self.src_stream.synchronize()
+        # ---- errors: first failing stage surfaces as WorkerPanic ----
+        for j, m in enumerate(mods):
+            try:
+                m.raise_for_error(stage=j)
+            except WorkerPanic:
+                for k, mm in enumerate(mods):
+                    mm.optimizer.step_count = step0[k] + max(0, mm.device_step() - step0[k])
+                raise
+        # ---- metrics ----
+        metrics.n_batches = n
+        metrics.images = images
+        metrics.batches_processed = [n] * s
+        metrics.loss_history = [m.loss_history(step0[j], n) for j, m in enumerate(mods)]
+        metrics.buffer_high_water = [0] * s
+        if timing and n:
+            ms = lambda e: ev0.elapsed_time(e)  # noqa: E731
+            src_t = [ms(e) for e in t_src]
+            st_t = [[ms(e) for e in t_start[j]] for j in range(s)]
+            en_t = [[ms(e) for e in t_end[j]] for j in range(s)]
+            metrics.wall_time = max(en_t[-1][-1], max(v[-1] for v in en_t)) / 1e3
+            metrics.busy_time = [sum(b - a for a, b in zip(st_t[j], en_t[j])) / 1e3
+                                 for j in range(s)]
+            for j in range(s):
+                prod_start = src_t if j == 0 else st_t[j - 1]
+                push_t = src_t if j == 0 else en_t[j - 1]
+                for t in range(n):
+                    # producer_progress at pop time (runtime.py:336-337)
+                    prog = int(np.searchsorted(prod_start, st_t[j][t], side="right")) - 1
+                    metrics.staleness[max(0, min(prog, t + M) - t)] += 1
+                # occupancy right after each push (runtime.py:96-99)
+                hw = 0
+                for t in range(n):
+                    popped = int(np.searchsorted(st_t[j], push_t[t], side="right"))
+                    hw = max(hw, min(M, max(1, t + 1 - popped)))
+                metrics.buffer_high_water[j] = hw
+        else:
+            metrics.staleness[0] += n * s
+            metrics.buffer_high_water = [min(M, n)] * s
+            metrics.wall_time = 0.0
+        return metrics
+
+
+# --------------------------------------------------------------------------
+# deterministic round-robin replay (runtime.py:475-533)
+# --------------------------------------------------------------------------
+
+def _run_ppll_roundrobin(modules, dataset_iter, config) -> EpochMetrics:
+    s = len(modules)
+    M = config.buffer_capacity
+    metrics = EpochMetrics(n_stages=s)
+    pipe = DevicePipeline(modules, RunConfig(buffer_capacity=M, use_graphs=False, timing=False))
+    stream = torch.cuda.current_stream(modules[0].device)
+    step0 = [m.optimizer.step_count for m in modules]
+    it = iter(dataset_iter)
+    stream_done = False
+    bufs = [deque() for _ in range(s)]
+    closed = [False] * s
+    progress = [-1] * s
+    done = [False] * s
+    next_id = 0
+    rounds = 0
+    high_water = [0] * s
+    sizes = {}
+    lib = N.load()
+    while not all(done):
+        rounds += 1
+        while not stream_done and len(bufs[0]) < M:
+            try:
+                x, y = next(it)
+            except StopIteration:
+                stream_done = True
+                closed[0] = True
+                break
+            xt = torch.as_tensor(np.asarray(x, dtype=np.float32) if not torch.is_tensor(x) else x)
+            B = int(xt.shape[0])
+            pipe._ensure(B)
+            r = pipe.rings
+            slot = next_id % M
+            sizes[next_id] = B
+            with torch.cuda.stream(stream):
+                xd = xt.to(device=modules[0].device, dtype=torch.float32)
+                if r.x_stage is None:
+                    r.x[0][slot, :B].copy_(xd)
+                else:
+                    N.check(lib.ppll_cast(B * modules[0].input_width, xd.data_ptr(), N.F32,
+                                          r.x[0][slot].data_ptr(), N.BF16, stream.cuda_stream),
+                            "cast")
+                r.y[0][slot, :B].copy_(torch.as_tensor(np.asarray(y)).to(torch.int64))
+            progress[0] = next_id
+            bufs[0].append(next_id)
+            high_water[0] = max(high_water[0], len(bufs[0]))
+            next_id += 1
+        for j in range(s):
+            if done[j]:
+                continue
+            if not bufs[j]:
+                if closed[j]:
+                    done[j] = True
+                    if j < s - 1:
+                        closed[j + 1] = True
+                continue
+            last = j == s - 1
+            if not last and len(bufs[j + 1]) >= M:
+                continue
+            bid = bufs[j].popleft()
+            metrics.staleness[max(0, progress[j] - bid)] += 1
+            if not last:
+                progress[j + 1] = bid
+            with torch.cuda.stream(stream):
+                pipe._launch(j, bid % M, sizes[bid], stream)
+            modules[j].optimizer.step_count += 1
+            if not last:
+                bufs[j + 1].append(bid)
+                high_water[j + 1] = max(high_water[j + 1], len(bufs[j + 1]))
+            metrics.batches_processed[j] += 1
+    stream.synchronize()
+    for j, m in enumerate(modules):
+        m.raise_for_error(stage=j)
+    metrics.n_batches = metrics.batches_processed[0]
+    metrics.images = sum(sizes.values())
+    metrics.loss_history = [m.loss_history(step0[j], metrics.batches_processed[j])
+                            for j, m in enumerate(modules)]
+    metrics.wall_time = float(rounds)
+    metrics.busy_time = [float(c) for c in metrics.batches_processed]
+    metrics.buffer_high_water = high_water
+    return metrics

@@ -1,0 +1,369 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the oracle and
+the reference's golden vectors.
+
+Tolerances (stated):
+  * integer bookkeeping (batch ids, FIFO order, counts, staleness bounds,
+    deterministic trace): bit-exact;
+  * fp32 parity mode vs the fp64 reference: per-step loss |Δ| <= 5e-6 (x
+    max(1,|loss|)); final weights max|ΔW| / max|W| <= 5e-3;
+  * bf16 tensor-core mode: per-step loss |Δ| <= 2e-2 relative; weights
+    max|ΔW| / max|W| <= 5e-2;
+  * device pipeline vs device round-robin vs device sequential: bitwise.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_12780_b200 as lp
+import ppll_oracle as orc
+from conftest import GOLDEN
+from paper_2411_12780_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["mlp_s1", "mlp_s2", "mlp_s4", "mlp_s3_wide_aux", "mlp_s4_odd"]
+TOL = {"fp32": (5e-6, 5e-3), "bf16": (2e-2, 5e-2)}
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def _mods(z, precision, total_steps=None):
+    dims = tuple(int(d) for d in z["dims"])
+    spec = lp.NetworkSpec(dims)
+    plan = lp.partition(spec, int(z["s"]))
+    ahw = int(z["aux_hidden_width"])
+    hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001,
+                           total_steps=total_steps or int(z["steps"]), momentum=0.9,
+                           weight_decay=1e-4, seed=int(z["seed"]),
+                           aux_hidden_width=None if ahw < 0 else ahw, precision=precision)
+    return lp.build_modules(spec, plan, int(z["d_prime"]), int(z["interval"]), hyper)
+
+
+def _flat(m):
+    return np.concatenate([p.data.ravel() for p in m.parameters()])
+
+
+# --- primitives through the C-ABI ------------------------------------------------
+
+SHAPES = [(7, 5, 3), (64, 64, 64), (128, 3072, 1024), (100, 200, 10), (256, 384, 1152),
+          (128, 1024, 1024), (33, 17, 29)]
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("M,K,Nn", SHAPES)
+def test_linear_ops_match_torch_fp32(dtype, M, K, Nn):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + K)
+    tdt = torch.float32 if dtype == "fp32" else torch.bfloat16
+    code = N.F32 if dtype == "fp32" else N.BF16
+    X = torch.randn(M, K, device="cuda", generator=g).to(tdt)
+    W = (torch.randn(K, Nn, device="cuda", generator=g) / K ** 0.5).to(tdt)
+    b = torch.randn(Nn, device="cuda", generator=g)
+    dY = torch.randn(M, Nn, device="cuda", generator=g).to(tdt)
+    Xm = torch.relu(X.float()).to(tdt)   # mask source with exact zeros
+    lib = N.load()
+    s = torch.cuda.current_stream().cuda_stream
+    Y = torch.empty(M, Nn, device="cuda", dtype=tdt)
+    Y2 = torch.empty_like(Y)
+    N.check(lib.ppll_linear_fwd(M, K, Nn, X.data_ptr(), K, W.data_ptr(), b.data_ptr(),
+                                Y.data_ptr(), Nn, Y2.data_ptr(), Nn, 1, code, s), "fwd")
+    dX = torch.empty(M, K, device="cuda", dtype=tdt)
+    N.check(lib.ppll_linear_dgrad(M, K, Nn, dY.data_ptr(), Nn, W.data_ptr(), Xm.data_ptr(), K,
+                                  dX.data_ptr(), K, code, s), "dgrad")
+    dW = torch.empty(K, Nn, device="cuda")
+    db = torch.empty(Nn, device="cuda")
+    N.check(lib.ppll_linear_wgrad(M, K, Nn, Xm.data_ptr(), K, dY.data_ptr(), Nn, dW.data_ptr(),
+                                  db.data_ptr(), code, s), "wgrad")
+    torch.cuda.synchronize()
+    Xf, Wf, dYf, Xmf = X.double(), W.double(), dY.double(), Xm.double()
+    refY = torch.relu(Xf @ Wf + b.double())
+    refdX = (dYf @ Wf.T) * (Xmf > 0)
+    refdW = Xmf.T @ dYf
+    refdb = dYf.sum(0)
+    rtol = 1e-5 if dtype == "fp32" else 2e-2
+
+    def close(a, r):
+        scale = r.abs().max().item() + 1e-12
+        return (a.double() - r).abs().max().item() / scale
+
+    assert close(Y, refY) < rtol
+    assert torch.equal(Y, Y2)                       # dual store (fused push) is identical
+    assert close(dX, refdX) < rtol
+    assert bool(((Xmf > 0) | (dX.double() == 0)).all())   # mask: exact zeros
+    assert close(dW, refdW) < rtol
+    assert close(db, refdb) < 1e-5
+
+
+def test_softmax_xent_kats_and_label_flag():
+    z = lp.Tensor(np.zeros((3, 4)))
+    assert lp.softmax_xent(z, np.array([0, 1, 3])).item() == pytest.approx(np.log(4), abs=1e-6)
+    big = lp.Tensor(np.array([[1e4, 0.0], [0.0, 1e4]]))
+    assert lp.softmax_xent(big, np.array([0, 1])).item() == pytest.approx(0.0, abs=1e-6)
+    with pytest.raises(lp.LabelOutOfRange):
+        lp.softmax_xent(z, np.array([0, 1, 4]))
+    # the device flag path (range check left to the kernel)
+    lib = N.load()
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    dz = torch.empty(3, 4, device="cuda")
+    y = torch.tensor([0, 9, 1], device="cuda")
+    N.check(lib.ppll_softmax_xent(3, 4, z.dev.data_ptr(), 4, y.data_ptr(), dz.data_ptr(), 4,
+                                  loss.data_ptr(), None, err.data_ptr(), N.F32,
+                                  torch.cuda.current_stream().cuda_stream), "xent")
+    assert int(err.item()) & N.ERRBIT_LABEL
+
+
+def test_softmax_xent_matches_oracle_random():
+    rng = np.random.default_rng(3)
+    for B, C in [(1, 2), (5, 10), (128, 10), (64, 100), (300, 7)]:
+        zh = rng.standard_normal((B, C)) * 3
+        yh = rng.integers(0, C, B)
+        ref, gref = orc.softmax_xent(zh, yh)
+        z = torch.tensor(zh, dtype=torch.float32, device="cuda")
+        dz = torch.empty_like(z)
+        loss = torch.zeros(1, device="cuda")
+        N.check(N.load().ppll_softmax_xent(B, C, z.data_ptr(), C,
+                                           torch.tensor(yh, device="cuda").data_ptr(),
+                                           dz.data_ptr(), C, loss.data_ptr(), None, None, N.F32,
+                                           torch.cuda.current_stream().cuda_stream), "xent")
+        assert abs(loss.item() - ref) < 1e-5
+        np.testing.assert_allclose(dz.cpu().numpy(), gref, atol=1e-7)
+
+
+def test_nesterov_kats_and_recurrence():
+    # test_optim.py:15-56 frozen values
+    for th0, g, lr, mu, wd, want in [(1.0, 0.5, 0.1, 0.0, 0.0, 0.95), (0.0, 1.0, 1.0, 0.9, 0.0, -1.9),
+                                     (10.0, 0.0, 1.0, 0.0, 1e-4, 9.999)]:
+        p = lp.Tensor(np.array([th0]), track_grad=True)
+        st = lp.OptimizerState([p], mu=mu, weight_decay=wd)
+        p.grad = lp.Tensor(np.array([g]))
+        lp.sgd_nesterov_step([p], st, lr)
+        assert p.data[0] == pytest.approx(want, rel=1e-6)
+        assert p.grad is None and st.step_count == 1
+    p = lp.Tensor(np.array([0.0]), track_grad=True)
+    st = lp.OptimizerState([p], mu=0.9, weight_decay=0.0)
+    for _ in range(2):
+        p.grad = lp.Tensor(np.array([1.0]))
+        lp.sgd_nesterov_step([p], st, 1.0)
+    assert p.data[0] == pytest.approx(-4.61, rel=1e-6)
+    # all-or-nothing
+    a, b = lp.Tensor(np.array([1.0]), track_grad=True), lp.Tensor(np.array([2.0]), track_grad=True)
+    st = lp.OptimizerState([a, b])
+    a.grad = lp.Tensor(np.array([1.0]))
+    with pytest.raises(lp.MissingGradient):
+        lp.sgd_nesterov_step([a, b], st, 0.1)
+    assert a.data[0] == 1.0 and a.grad is not None and st.step_count == 0
+    # random trajectories vs the oracle recurrence (optim.py:81-88)
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        th0 = rng.normal(size=(37,))
+        mu, wd, lr = rng.uniform(0, 0.95), rng.uniform(0, 0.01), rng.uniform(0.01, 0.2)
+        p = lp.Tensor(th0.copy(), track_grad=True)
+        st = lp.OptimizerState([p], mu=mu, weight_decay=wd)
+        rt, rv = th0.copy(), np.zeros_like(th0)
+        for _ in range(4):
+            g = rng.normal(size=th0.shape)
+            p.grad = lp.Tensor(g)
+            lp.sgd_nesterov_step([p], st, lr)
+            orc.nesterov_update(rt, rv, g, lr, mu, wd)
+        np.testing.assert_allclose(p.data, rt, atol=1e-5)
+
+
+# --- the local step vs the reference's golden vectors ---------------------------
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("name", CASES)
+def test_local_steps_match_reference_golden(name, precision):
+    z = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    mods = _mods(z, precision)
+    s, steps = int(z["s"]), int(z["steps"])
+    for j, m in enumerate(mods):    # initial parameters: fp32 rounding of the fp64 draws
+        np.testing.assert_allclose(_flat(m), z[f"init_{j}"], rtol=0, atol=1e-7)
+    ltol, wtol = TOL[precision]
+    losses = np.zeros((s, steps))
+    for t in range(steps):
+        h = lp.Tensor(z["xs"][t])
+        for j, m in enumerate(mods):
+            loss, h = lp.local_loss_and_update(m, h, z["ys"][t])
+            losses[j, t] = loss
+            if t == 0:
+                ref = z[f"xout0_{j}"]
+                err = np.abs(h.data - ref).max() / max(np.abs(ref).max(), 1e-6)
+                assert err < (1e-5 if precision == "fp32" else 3e-2), (j, err)
+    ref = z["losses"]
+    if precision == "fp32":
+        assert np.abs(losses - ref).max() <= ltol * max(1.0, np.abs(ref).max())
+    else:
+        assert (np.abs(losses - ref) / np.abs(ref)).max() <= ltol
+    for j, m in enumerate(mods):
+        fin, want = _flat(m), z[f"final_{j}"]
+        assert np.abs(fin - want).max() / np.abs(want).max() <= wtol
+        assert m.optimizer.step_count == int(z[f"step_count_{j}"])
+        assert m.device_step() == steps
+
+
+def test_full_m_config_fp32_losses():
+    """(3072,1024,1024,1024,1024,10), s=4, B=128 vs the reference (3 steps)."""
+    z = np.load(os.path.join(GOLDEN, "full_m.npz"))
+    dims = (3072, 1024, 1024, 1024, 1024, 10)
+    spec = lp.NetworkSpec(dims)
+    mods = lp.build_modules(spec, lp.partition(spec, 4), 2, 3,
+                            lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=100, seed=42))
+    rng = np.random.default_rng(0)
+    xs = rng.standard_normal((3, 128, 3072))
+    ys = rng.integers(0, 10, size=(3, 128))
+    losses = np.zeros((4, 3))
+    for t in range(3):
+        h = lp.Tensor(xs[t])
+        for j, m in enumerate(mods):
+            losses[j, t], h = lp.local_loss_and_update(m, h, ys[t])
+    assert np.abs(losses - z["losses"]).max() <= 5e-6 * 3
+    for j, m in enumerate(mods):
+        f = _flat(m)
+        np.testing.assert_allclose(f[:256], z[f"head_{j}"], atol=5e-5)
+
+
+# --- local-step semantics (test_blocks.py:198-238) -------------------------------
+
+def test_gradient_isolation_and_pre_step_output():
+    z = np.load(os.path.join(GOLDEN, "mlp_s4.npz"))
+    mods = _mods(z, "fp32", total_steps=10)
+    before = [_flat(m) for m in mods]
+    x = lp.Tensor(np.random.default_rng(8).normal(size=(5, mods[1].input_width)))
+    expected = lp.block_forward(mods[1], x).data
+    seen = []
+    loss, x_out = lp.local_loss_and_update(mods[1], x, np.array([0, 1, 2, 3, 4]),
+                                           on_output=seen.append)
+    assert np.isfinite(loss)
+    assert np.array_equal(x_out.data, expected)          # pre-update parameters
+    assert len(seen) == 1 and seen[0] is x_out and not x_out.track_grad
+    after = [_flat(m) for m in mods]
+    for j in range(4):
+        assert np.array_equal(before[j], after[j]) == (j != 1)
+    with pytest.raises(ValueError):
+        lp.local_loss_and_update(mods[0], lp.Tensor(np.zeros((2, 96)), track_grad=True),
+                                 np.array([0, 1]))
+    with pytest.raises(lp.DimensionMismatch):
+        lp.block_forward(mods[0], lp.Tensor(np.zeros((2, 5))))
+
+
+def test_label_error_and_step_out_of_range():
+    z = np.load(os.path.join(GOLDEN, "mlp_s2.npz"))
+    mods = _mods(z, "fp32", total_steps=1)
+    before = _flat(mods[0])
+    with pytest.raises(lp.LabelOutOfRange):
+        lp.local_loss_and_update(mods[0], lp.Tensor(np.zeros((3, 48))), np.array([0, 99, 1]))
+    assert np.array_equal(_flat(mods[0]), before) and mods[0].optimizer.step_count == 0
+    x = lp.Tensor(np.ones((3, 48)))
+    lp.local_loss_and_update(mods[0], x, np.array([0, 1, 2]))
+    lp.local_loss_and_update(mods[0], x, np.array([0, 1, 2]))   # step 1 == total_steps: allowed
+    with pytest.raises(lp.StepOutOfRange):
+        lp.local_loss_and_update(mods[0], x, np.array([0, 1, 2]))
+
+
+# --- the pipeline (runtime.py) -----------------------------------------------------
+
+def _toy(n, width, classes, batch, seed):
+    rng = np.random.default_rng(seed)
+    return [(rng.normal(size=(batch, width)), rng.integers(0, classes, size=batch))
+            for _ in range(n)]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_device_pipeline_equals_roundrobin_equals_sequential(precision):
+    z = np.load(os.path.join(GOLDEN, "mlp_s4.npz"))
+    data = _toy(9, 96, 10, 16, 5)
+    a, b, c = (_mods(z, precision, total_steps=20) for _ in range(3))
+    ma = lp.run_epoch(lp.RunMode.PPLL, a, iter(data), lp.RunConfig(buffer_capacity=2))
+    mb = lp.run_deterministic(lp.RunMode.PPLL, b, iter(data), lp.RunConfig(buffer_capacity=3))
+    seq = [[] for _ in range(4)]
+    for x, y in data:
+        h = lp.Tensor(x)
+        for j, m in enumerate(c):
+            loss, h = lp.local_loss_and_update(m, h, y)
+            seq[j].append(loss)
+    assert ma.loss_history == mb.loss_history == seq
+    for x, y, w in zip(a, b, c):
+        assert np.array_equal(_flat(x), _flat(y)) and np.array_equal(_flat(x), _flat(w))
+    assert ma.batches_processed == mb.batches_processed == [9] * 4
+    assert sum(ma.staleness.values()) == 36 and all(0 <= k <= 2 for k in ma.staleness)
+    assert all(1 <= hw <= 2 for hw in ma.buffer_high_water)
+    assert ma.wall_time > 0 and all(0 < bt <= ma.wall_time for bt in ma.busy_time)
+
+
+def test_pipeline_matches_reference_threaded_golden():
+    """The reference's threaded run_epoch (golden) == our device pipeline."""
+    z = np.load(os.path.join(GOLDEN, "threaded_ppll.npz"))
+    dims = (24, 20, 16, 12, 6)
+    spec = lp.NetworkSpec(dims)
+    mods = lp.build_modules(spec, lp.partition(spec, 3), 2, 1,
+                            lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=20, seed=3))
+    data = list(zip(z["xs"], z["ys"]))
+    m = lp.run_epoch(lp.RunMode.PPLL, mods, iter(data), lp.RunConfig(buffer_capacity=2))
+    assert np.abs(np.array(m.loss_history) - z["losses"]).max() < 5e-6 * 3
+    for j, mod in enumerate(mods):
+        want = z[f"final_{j}"]
+        assert np.abs(_flat(mod) - want).max() / np.abs(want).max() < 5e-3
+
+
+def test_deterministic_traces_bit_exact():
+    with open(os.path.join(GOLDEN, "roundrobin_traces.json")) as f:
+        traces = json.load(f)
+    for t in traces:
+        s, n, M = t["s"], t["n"], t["M"]
+        dims = (4,) + (5,) * s + (2,)
+        spec = lp.NetworkSpec(dims)
+        mods = lp.build_modules(spec, lp.partition(spec, s), 1, 1,
+                                lp.Hyperparams(total_steps=64, seed=0))
+        rng = np.random.default_rng(s * 100 + n)
+        data = [(rng.standard_normal((3, 4)), rng.integers(0, 2, 3)) for _ in range(n)]
+        m = lp.run_deterministic(lp.RunMode.PPLL, mods, iter(data), lp.RunConfig(buffer_capacity=M))
+        assert m.wall_time == t["wall_time"]
+        assert m.busy_time == t["busy_time"]
+        assert m.batches_processed == t["batches_processed"]
+        assert {str(k): v for k, v in sorted(m.staleness.items())} == t["staleness"]
+        assert m.buffer_high_water == t["high_water"]
+        assert m.n_batches == t["n_batches"]
+
+
+def test_conservation_and_bounds_random_pipelines():
+    rng = np.random.default_rng(0)
+    for _ in range(6):
+        s = int(rng.integers(2, 6))
+        cap = int(rng.integers(1, 4))
+        n = int(rng.integers(1, 12))
+        dims = (4,) + tuple(int(rng.integers(3, 9)) for _ in range(s)) + (3,)
+        spec = lp.NetworkSpec(dims)
+        mods = lp.build_modules(spec, lp.partition(spec, s), 1, 1,
+                                lp.Hyperparams(total_steps=64, seed=int(rng.integers(1000))))
+        m = lp.run_epoch(lp.RunMode.PPLL, mods, iter(_toy(n, 4, 3, 6, int(rng.integers(99)))),
+                         lp.RunConfig(buffer_capacity=cap))
+        assert m.n_batches == n and m.batches_processed == [n] * s
+        assert [len(h) for h in m.loss_history] == [n] * s
+        assert sum(m.staleness.values()) == s * n
+        assert all(0 <= k <= cap for k in m.staleness)
+        assert all(1 <= hw <= cap for hw in m.buffer_high_water)
+
+
+def test_worker_failure_surfaces_as_panic():
+    spec = lp.NetworkSpec((4, 5, 4, 2))
+    mods = lp.build_modules(spec, lp.partition(spec, 2), 1, 1, lp.Hyperparams(total_steps=8))
+    with pytest.raises(lp.WorkerPanic) as err:
+        lp.run_epoch(lp.RunMode.PPLL, mods, iter([(np.zeros((3, 4)), np.array([0, 9, 1]))]))
+    assert err.value.stage_index in (0, 1)
+
+
+def test_native_kernels_were_launched():
+    before = N.launch_count()
+    spec = lp.NetworkSpec((32, 16, 8))
+    mods = lp.build_modules(spec, lp.partition(spec, 1), 0, 1, lp.Hyperparams(total_steps=4))
+    lp.local_loss_and_update(mods[0], lp.Tensor(np.ones((4, 32))), np.array([0, 1, 2, 3]))
+    assert N.launch_count() > before
