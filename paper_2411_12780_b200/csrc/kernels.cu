@@ -136,6 +136,20 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
   return PPLL_OK;
 }
 
+template <typename TO>
+int launch_splitk_reduce(int M, int N, int splits, const float* ws, const Epilogue<TO>& ep,
+                         cudaStream_t s) {
+  Epilogue<TO> r = ep;
+  r.partial = nullptr;
+  int blocks = min(ceil_div((long)M * N, 256), 148 * 8);
+  splitk_reduce_kernel<TO><<<blocks, 256, 0, s>>>(M, N, splits, ws, r);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template int launch_splitk_reduce<float>(int, int, int, const float*, const Epilogue<float>&, cudaStream_t);
+template int launch_splitk_reduce<__nv_bfloat16>(int, int, int, const float*, const Epilogue<__nv_bfloat16>&, cudaStream_t);
+
 template int launch_gemm_simt<float, float>(int, int, int, const float*, long, long, const float*, long, long, const Epilogue<float>&, float*, size_t, cudaStream_t);
 template int launch_gemm_simt<__nv_bfloat16, __nv_bfloat16>(int, int, int, const __nv_bfloat16*, long, long, const __nv_bfloat16*, long, long, const Epilogue<__nv_bfloat16>&, float*, size_t, cudaStream_t);
 template int launch_gemm_simt<__nv_bfloat16, float>(int, int, int, const __nv_bfloat16*, long, long, const __nv_bfloat16*, long, long, const Epilogue<float>&, float*, size_t, cudaStream_t);

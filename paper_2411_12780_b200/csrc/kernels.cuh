@@ -41,6 +41,10 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
                    const __nv_bfloat16* B, long ldb, bool b_kmajor, const Epilogue<TO>& ep,
                    float* ws, size_t ws_elems, cudaStream_t s);
 
+template <typename TO>
+int launch_splitk_reduce(int M, int N, int splits, const float* ws, const Epilogue<TO>& ep,
+                         cudaStream_t s);
+
 template <typename T>
 int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s);
 

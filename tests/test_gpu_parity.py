@@ -367,3 +367,19 @@ def test_native_kernels_were_launched():
     mods = lp.build_modules(spec, lp.partition(spec, 1), 0, 1, lp.Hyperparams(total_steps=4))
     lp.local_loss_and_update(mods[0], lp.Tensor(np.ones((4, 32))), np.array([0, 1, 2, 3]))
     assert N.launch_count() > before
+
+
+# --- the tcgen05 engine specifically ---------------------------------------------
+
+TC_SHAPES = [(128, 64, 64), (128, 3072, 1024), (256, 384, 1152), (100, 200, 96),
+             (8320, 384, 1536), (130, 1024, 264), (1024, 1024, 1024)]
+
+
+@pytest.mark.parametrize("M,K,Nn", TC_SHAPES)
+def test_tcgen05_engine_matches_torch(M, K, Nn):
+    lib = N.load()
+    lib.ppll_set_gemm_engine(N.GEMM_TCGEN05)
+    try:
+        test_linear_ops_match_torch_fp32("bf16", M, K, Nn)
+    finally:
+        lib.ppll_set_gemm_engine(N.GEMM_AUTO)
