@@ -189,18 +189,22 @@ def dominant_kernel_roofline(mods, B, hbm, stream_dev):
     g = torch.zeros_like(f["grad"])
     th, v = f["theta"].clone(), f["mom"].clone()
     lp_buf = f["theta_lp"].clone() if f["theta_lp"] is not None else None
-    R = 50
+    R = 20
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=stream_dev)   # 256 MB > L2
     for _ in range(3):
         lib.ppll_nesterov_step(n, th.data_ptr(), v.data_ptr(), g.data_ptr(), N.ptr(lp_buf),
                                None, None, 0, 0.0, 0.9, 1e-4, None, st.cuda_stream)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
+    times = []
     for _ in range(R):
+        flush.zero_()                      # evict the operands from L2 between launches
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
         lib.ppll_nesterov_step(n, th.data_ptr(), v.data_ptr(), g.data_ptr(), N.ptr(lp_buf),
                                None, None, 0, 0.0, 0.9, 1e-4, None, st.cuda_stream)
-    b.record(st)
-    b.synchronize()
-    dt = a.elapsed_time(b) / R * 1e-3
+        b.record(st)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    dt = statistics.median(times) * 1e-3
     per_param = 20 + (2 if lp_buf is not None else 0)
     bytes_ = n * per_param
     return {"kernel": "nesterov_kernel (fused Nesterov-SGD, largest stage)",
@@ -213,7 +217,7 @@ def dominant_kernel_roofline(mods, B, hbm, stream_dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="mlp_m", choices=sorted(WORKLOADS))

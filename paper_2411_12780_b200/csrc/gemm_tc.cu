@@ -3,22 +3,25 @@
 //
 //   C[M,N] = Σ_k A(m,k)·B(k,n)   bf16 operands, fp32 accumulation in TMEM.
 //
-// One CTA computes a 128 x BN tile (UMMA M=128, N=BN, K=16 per instruction,
-// cta_group::1).  Warp roles (192 threads):
+// Persistent kernel: one CTA per SM walks a static schedule of work items
+// (128 x BN output tiles, optionally split along K).  Warp roles (192 thr):
 //   warp 0      TMA producer (one elected lane): A/B k-blocks of 64 into a
-//               kStages-deep smem ring, mbarrier full/empty handshake;
+//               kStages-deep shared-memory ring (mbarrier full/empty);
 //   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x
-//               tcgen05.mma per k-block, tcgen05.commit frees the smem slot;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (one accumulator row per
-//               thread), fused bias / ReLU / ReLU-mask / dual store (the ring
-//               push) or raw fp32 split-K partials.
-// Operand layouts (all 128-byte swizzled, TMA box inner extent 64 elements):
-//   K-major  (A: X[M,K], dY[M,N];  B: W[K_in,N_out] seen as N x K in dgrad):
-//            box {64 (K), rows}; UMMA desc SBO = 1024 B, K advance +32 B.
-//   MN-major (A: Xᵀ in wgrad;  B: W in fwd, dY in wgrad):
-//            boxes {64 (MN), 64 (K)} stacked along MN every 8 KB;
-//            UMMA desc LBO = 8 KB (MN chunk stride), SBO = 1024 B (8-row K
-//            group stride), K advance +2048 B (16 rows of 128 B).
+//               tcgen05.mma (M=128, N=BN, K=16) per k-block, tcgen05.commit
+//               frees the smem slot; accumulators are DOUBLE-BUFFERED in
+//               TMEM (2 x BN columns) so tile i+1's MMAs overlap tile i's
+//               epilogue;
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (row per thread) → smem
+//               transpose → column-per-lane coalesced stores with the fused
+//               bias / ReLU / ReLU-mask / dual store (the ring push), or
+//               fp32 split-K partials; the last CTA to finish a split tile
+//               (atomic ticket) reduces the partials in fixed order and runs
+//               the epilogue — deterministic, no extra launch.
+// Operand layouts (128-byte swizzled, TMA box inner extent 64 elements):
+//   K-major  box {64 (K), rows};  UMMA desc SBO = 1024 B, K step +32 B.
+//   MN-major boxes {64 (MN), 64 (K)} every 8 KB along MN;  UMMA desc
+//            LBO = 8 KB (MN-chunk stride), SBO = 1024 B, K step +2048 B.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -30,11 +33,12 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+constexpr int kNumSMs = 148;
+constexpr int kTickets = 4096;   // split-K tile tickets kept at the end of the workspace
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -42,6 +46,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -53,7 +60,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
                                             int x, int y) {
   asm volatile(
@@ -62,7 +68,6 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
-
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
@@ -72,7 +77,6 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
-
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -81,14 +85,12 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
       : "memory");
 }
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -102,36 +104,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void epi_bar() {   // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 
 template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;     // BN * 128 B
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN >= 256) ? 4 : 6;
-  static constexpr int TOTAL = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
+  static constexpr int EPI = 4 * 32 * 33 * 4;     // per-warp 32x33 fp32 transpose tiles
+  static constexpr int TOTAL = STAGES * STAGE + EPI + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
+};
+
+struct Sched {
+  int mt, nt, tiles, splits, kps, items;
 };
 
 template <typename TO, bool A_K, bool B_K, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               int M, int N, int K, int k_per_split, Epilogue<TO> ep) {
+               int M, int N, int K, Sched sc, Epilogue<TO> ep, float* part, int* tickets) {
   using L = Smem<BN>;
   constexpr int S = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGE);
+  float* epi_smem = reinterpret_cast<float*>(smem + S * L::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGE + L::EPI);
   uint64_t* empty = full + S;
-  uint64_t* tmem_full = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + S;      // [2]
+  uint64_t* tempty = tfull + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int kbeg = blockIdx.z * k_per_split;
-  const int kend = min(K, kbeg + k_per_split);
-  const int nkb = (kend - kbeg + BK - 1) / BK;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -140,14 +149,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(L::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -158,75 +170,128 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   if (warp == 0) {
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % S;
-        const uint32_t round = kb / S;
-        mbar_wait(&empty[st], (round & 1) ^ 1);
-        uint8_t* sa = smem + st * L::STAGE;
-        uint8_t* sb = sa + L::A_BYTES;
-        const int k0 = kbeg + kb * BK;
-        mbar_expect_tx(&full[st], L::STAGE);
-        if (A_K) {
-          tma_load_2d(&map_a, &full[st], sa, k0, m0);
-        } else {
+      int kb_total = 0;
+      for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+        const int tile = w % sc.tiles, z = w / sc.tiles;
+        const int m0 = (tile % sc.mt) * BM, n0 = (tile / sc.mt) * BN;
+        const int kbeg = z * sc.kps, kend = min(K, kbeg + sc.kps);
+        for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb_total) {
+          const int st = kb_total % S;
+          mbar_wait(&empty[st], ((kb_total / S) & 1) ^ 1);
+          uint8_t* sa = smem + st * L::STAGE;
+          uint8_t* sb = sa + L::A_BYTES;
+          mbar_expect_tx(&full[st], L::STAGE);
+          if (A_K) {
+            tma_load_2d(&map_a, &full[st], sa, k0, m0);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BM / 64; ++i) tma_load_2d(&map_a, &full[st], sa + i * 8192, m0 + 64 * i, k0);
-        }
-        if (B_K) {
-          tma_load_2d(&map_b, &full[st], sb, k0, n0);
-        } else {
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_2d(&map_a, &full[st], sa + i * 8192, m0 + 64 * i, k0);
+          }
+          if (B_K) {
+            tma_load_2d(&map_b, &full[st], sb, k0, n0);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i) tma_load_2d(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0);
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------- MMA issuer ---------------------------
-    // instruction descriptor: D=f32, A=B=bf16, majors, N>>3, M>>4
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_K ? 0u : 1u) << 15) |
                            ((B_K ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb % S;
-        const uint32_t round = kb / S;
-        mbar_wait(&full[st], round & 1);
+      int kb_total = 0, it = 0;
+      for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
+        const int z = w / sc.tiles;
+        const int kbeg = z * sc.kps, kend = min(K, kbeg + sc.kps);
+        const int acc = it & 1;
+        const uint32_t dtm = tmem + (uint32_t)(acc * BN);
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = smem_u32(smem + st * L::STAGE);
-        const uint32_t sb = sa + L::A_BYTES;
+        int first = 1;
+        for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb_total) {
+          const int st = kb_total % S;
+          mbar_wait(&full[st], (kb_total / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + st * L::STAGE);
+          const uint32_t sb = sa + L::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = A_K ? make_desc(sa + k * 32, 16, 1024) : make_desc(sa + k * 2048, 8192, 1024);
-          const uint64_t bd = B_K ? make_desc(sb + k * 32, 16, 1024) : make_desc(sb + k * 2048, 8192, 1024);
-          mma_bf16(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_K ? make_desc(sa + k * 32, 16, 1024)
+                                    : make_desc(sa + k * 2048, 8192, 1024);
+            const uint64_t bd = B_K ? make_desc(sb + k * 32, 16, 1024)
+                                    : make_desc(sb + k * 2048, 8192, 1024);
+            mma_bf16(dtm, ad, bd, idesc, first ? 0u : 1u);
+            first = 0;
+          }
+          mma_commit(&empty[st]);
         }
-        mma_commit(&empty[st]);
+        mma_commit(&tfull[acc]);
       }
-      mma_commit(tmem_full);
     }
     __syncwarp();
   } else {
     // ------------------------- epilogue -----------------------------
-    const int q = warp & 3;                 // TMEM lane quadrant of this warp
-    const int row = m0 + q * 32 + lane;
-    if (lane == 0) mbar_wait(tmem_full, 0);
-    __syncwarp();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;                    // TMEM lane quadrant of this warp
+    float* tile_s = epi_smem + (warp - 2) * (32 * 33);
+    int it = 0;
+    for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
+      const int tile = w % sc.tiles, z = w / sc.tiles;
+      const int m0 = (tile % sc.mt) * BM, n0 = (tile / sc.mt) * BN;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int rbase = m0 + q * 32;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
-      if (row < M) {
-        const int nb = n0 + c;
-        if (ep.partial) {
-          float* dst = ep.partial + ((long)blockIdx.z * M + row) * N + nb;
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < N) dst[i] = __uint_as_float(r[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (nb + i < N) ep.apply(row, nb + i, __uint_as_float(r[i]));
+        for (int i = 0; i < 32; ++i) tile_s[lane * 33 + i] = __uint_as_float(r[i]);
+        __syncwarp();
+        const int col = n0 + c + lane;
+        if (col < N) {
+          if (sc.splits > 1) {
+            float* dst = part + ((long)z * M) * N + col;
+            for (int rr = 0; rr < 32 && rbase + rr < M; ++rr)
+              dst[(long)(rbase + rr) * N] = tile_s[rr * 33 + lane];
+          } else {
+            for (int rr = 0; rr < 32 && rbase + rr < M; ++rr)
+              ep.apply(rbase + rr, col, tile_s[rr * 33 + lane]);
+          }
+        }
+        __syncwarp();
+      }
+      // accumulator buffer drained: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (sc.splits > 1) {
+        // deterministic split-K fix-up by the last CTA of this tile
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 64) {
+          int old = atomicAdd(&tickets[tile], 1);
+          *s_last = (old == sc.splits - 1);
+        }
+        epi_bar();
+        if (*s_last) {
+          __threadfence();
+          for (int c = 0; c < BN; c += 32) {
+            const int col = n0 + c + lane;
+            if (col >= N) continue;
+            for (int rr = 0; rr < 32 && rbase + rr < M; ++rr) {
+              const long off = (long)(rbase + rr) * N + col;
+              float s = 0.f;
+              for (int zz = 0; zz < sc.splits; ++zz) s += __ldcg(part + (long)zz * M * N + off);
+              ep.apply(rbase + rr, col, s);
+            }
+          }
+          if (threadIdx.x == 64) tickets[tile] = 0;   // re-arm for the next launch
         }
       }
     }
@@ -236,7 +301,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+                 "r"(L::TMEM_COLS));
   }
 }
 
@@ -273,8 +338,8 @@ static bool make_map(CUtensorMap* map, const void* ptr, long inner, long outer, 
 }
 
 template <typename TO, bool A_K, bool B_K, int BN>
-static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits,
-               int kps, const Epilogue<TO>& ep, cudaStream_t s) {
+static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const Sched& sc,
+               const Epilogue<TO>& ep, float* part, int* tickets, cudaStream_t s) {
   auto kern = gemm_tc_kernel<TO, A_K, B_K, BN>;
   constexpr int smem = Smem<BN>::TOTAL;
   static bool attr_set = false;
@@ -282,8 +347,8 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
     PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  dim3 grid(ceil_div(N, BN), ceil_div(M, BM), splits);
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, M, N, K, kps, ep);
+  const int grid = sc.items < kNumSMs ? sc.items : kNumSMs;
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, M, N, K, sc, ep, part, tickets);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -291,51 +356,75 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
 
 template <typename TO, bool A_K, bool B_K>
 static int dispatch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
-                       int splits, int kps, const Epilogue<TO>& ep, cudaStream_t s) {
-  if (bn == 256) return run<TO, A_K, B_K, 256>(ma, mb, M, N, K, splits, kps, ep, s);
-  if (bn == 128) return run<TO, A_K, B_K, 128>(ma, mb, M, N, K, splits, kps, ep, s);
-  return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, splits, kps, ep, s);
+                       const Sched& sc, const Epilogue<TO>& ep, float* part, int* tickets,
+                       cudaStream_t s) {
+  switch (bn) {
+    case 256: return run<TO, A_K, B_K, 256>(ma, mb, M, N, K, sc, ep, part, tickets, s);
+    case 192: return run<TO, A_K, B_K, 192>(ma, mb, M, N, K, sc, ep, part, tickets, s);
+    case 128: return run<TO, A_K, B_K, 128>(ma, mb, M, N, K, sc, ep, part, tickets, s);
+    default: return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, sc, ep, part, tickets, s);
+  }
 }
 
 }  // namespace tc
+
+// workspace layout: [partials ... | kTickets ints (zeroed once, re-armed by the kernel)]
+size_t gemm_tc_ticket_offset(size_t ws_elems) {
+  return ws_elems >= (size_t)tc::kTickets ? ws_elems - tc::kTickets : 0;
+}
 
 template <typename TO>
 int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_kmajor,
                    const __nv_bfloat16* B, long ldb, bool b_kmajor, const Epilogue<TO>& ep,
                    float* ws, size_t ws_elems, cudaStream_t s) {
   using namespace tc;
-  // shapes the tensor-core tile cannot use efficiently go to the SIMT engine
+  // shapes a 128-row tensor-core tile cannot use efficiently go to the SIMT engine
   if (N < 32 || K < 16 || M < 1) return PPLL_ERR_UNSUPPORTED;
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15) || (lda * 2) % 16 || (ldb * 2) % 16)
     return PPLL_ERR_UNSUPPORTED;
-  // tile width: widest that still gives >= ~1 wave of CTAs
   const int mt = ceil_div(M, BM);
-  int bn = 256;
-  while (bn > 64 && (long)mt * ceil_div(N, bn) < 120) bn >>= 1;
-  const int tiles = mt * ceil_div(N, bn);
+  // tile width: minimise (waves x per-tile cost), per-tile cost ~ BN + 32
+  int bn = 64;
+  long best = -1;
+  const int cands[4] = {256, 192, 128, 64};
+  for (int i = 0; i < 4; ++i) {
+    const int c = cands[i];
+    if (c > 64 && !b_kmajor && c % 64) continue;
+    const long tiles = (long)mt * ceil_div(N, c);
+    const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (c + 32);
+    if (best < 0 || cost < best) { best = cost; bn = c; }
+  }
+  Sched sc;
+  sc.mt = mt;
+  sc.nt = ceil_div(N, bn);
+  sc.tiles = sc.mt * sc.nt;
   int splits = 1;
-  if (ws && tiles < 100 && K >= 4 * BK) {
-    splits = min(148 / tiles, K / (2 * BK));
-    while (splits > 1 && (size_t)splits * M * N > ws_elems) --splits;
+  float* part = nullptr;
+  int* tickets = nullptr;
+  const size_t tick_off = gemm_tc_ticket_offset(ws_elems);
+  if (ws && tick_off > 0 && sc.tiles <= kTickets && sc.tiles * 2 <= kNumSMs && K >= 8 * BK) {
+    splits = kNumSMs / sc.tiles;
+    if (splits > K / (4 * BK)) splits = K / (4 * BK);
+    while (splits > 1 && (size_t)splits * M * N > tick_off) --splits;
     if (splits < 1) splits = 1;
   }
-  int kps = ceil_div(ceil_div(K, splits), BK) * BK;
-  splits = ceil_div(K, kps);
-
+  sc.kps = ceil_div(ceil_div(K, splits), BK) * BK;
+  sc.splits = ceil_div(K, sc.kps);
+  sc.items = sc.tiles * sc.splits;
+  if (sc.splits > 1) {
+    part = ws;
+    tickets = reinterpret_cast<int*>(ws + tick_off);
+  }
   CUtensorMap ma, mb;
   bool ok = a_kmajor ? make_map(&ma, A, K, M, lda, BM) : make_map(&ma, A, M, K, lda, 64);
   ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, bn) : make_map(&mb, B, N, K, ldb, 64));
   if (!ok) return PPLL_ERR_UNSUPPORTED;
-
   Epilogue<TO> e = ep;
-  e.partial = splits > 1 ? ws : nullptr;
-  int r;
-  if (a_kmajor && !b_kmajor) r = dispatch_bn<TO, true, false>(bn, ma, mb, M, N, K, splits, kps, e, s);
-  else if (a_kmajor && b_kmajor) r = dispatch_bn<TO, true, true>(bn, ma, mb, M, N, K, splits, kps, e, s);
-  else if (!a_kmajor && !b_kmajor) r = dispatch_bn<TO, false, false>(bn, ma, mb, M, N, K, splits, kps, e, s);
-  else r = dispatch_bn<TO, false, true>(bn, ma, mb, M, N, K, splits, kps, e, s);
-  if (r || splits == 1) return r;
-  return launch_splitk_reduce<TO>(M, N, splits, ws, ep, s);
+  e.partial = nullptr;
+  if (a_kmajor && !b_kmajor) return dispatch_bn<TO, true, false>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
+  if (a_kmajor && b_kmajor) return dispatch_bn<TO, true, true>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
+  if (!a_kmajor && !b_kmajor) return dispatch_bn<TO, false, false>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
+  return dispatch_bn<TO, false, true>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
 }
 
 template int launch_gemm_tc<float>(int, int, int, const __nv_bfloat16*, long, bool, const __nv_bfloat16*, long, bool, const Epilogue<float>&, float*, size_t, cudaStream_t);

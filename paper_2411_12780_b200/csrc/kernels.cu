@@ -99,10 +99,78 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __re
   }
 }
 
+// Skinny shapes (classifier N <= 32, or reduction K <= 32): the 64x64 tile
+// would idle most of its lanes, so use
+//  * row-warp: one warp per output row, lanes split K, NP accumulators,
+//    butterfly reduction (A k-contiguous, N <= 32);
+//  * dot: one thread per output element, the coalesced operand dimension
+//    mapped to the fastest thread index.
+template <typename TI, typename TO, int NP>
+__global__ void __launch_bounds__(256)
+gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
+                    const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep) {
+  const int lane = threadIdx.x & 31;
+  const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (m >= M) return;
+  float acc[NP];
+#pragma unroll
+  for (int n = 0; n < NP; ++n) acc[n] = 0.f;
+  const TI* ar = A + (long)m * a_rs;
+  for (int k = lane; k < K; k += 32) {
+    const float a = to_f(ar[k]);
+    const TI* br = Bm + (long)k * b_rs;
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+      if (n < N) acc[n] = fmaf(a, to_f(br[(long)n * b_cs]), acc[n]);
+  }
+#pragma unroll
+  for (int n = 0; n < NP; ++n) acc[n] = warp_sum(acc[n]);
+#pragma unroll
+  for (int n = 0; n < NP; ++n)
+    if (n < N && lane == n) ep.apply(m, n, acc[n]);
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256)
+gemm_dot_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs, long a_cs,
+                const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep, int m_fast) {
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long)M * N) return;
+  const int m = m_fast ? (int)(idx % M) : (int)(idx / N);
+  const int n = m_fast ? (int)(idx / M) : (int)(idx % N);
+  const TI* ar = A + (long)m * a_rs;
+  const TI* bc = Bm + (long)n * b_cs;
+  float acc = 0.f;
+  for (int k = 0; k < K; ++k) acc = fmaf(to_f(ar[(long)k * a_cs]), to_f(bc[(long)k * b_rs]), acc);
+  ep.apply(m, n, acc);
+}
+
 template <typename TI, typename TO>
 int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, const TI* B,
                      long b_rs, long b_cs, const Epilogue<TO>& ep, float* ws, size_t ws_elems,
                      cudaStream_t s) {
+  if (N <= 32 && a_cs == 1 && K >= 64) {
+    Epilogue<TO> e = ep;
+    e.partial = nullptr;
+    if (N <= 16)
+      gemm_rowwarp_kernel<TI, TO, 16><<<ceil_div(M, 8), 256, 0, s>>>(M, N, K, A, a_rs, B, b_rs, b_cs, e);
+    else
+      gemm_rowwarp_kernel<TI, TO, 32><<<ceil_div(M, 8), 256, 0, s>>>(M, N, K, A, a_rs, B, b_rs, b_cs, e);
+    note_launch();
+    PPLL_LAUNCH_CHECK();
+    return PPLL_OK;
+  }
+  if (N <= 32 || K <= 32) {
+    Epilogue<TO> e = ep;
+    e.partial = nullptr;
+    // fastest thread index along the dimension whose operand (or output) is contiguous
+    const int m_fast = (b_cs != 1 && a_rs == 1) ? 1 : 0;
+    gemm_dot_kernel<TI, TO><<<ceil_div((long)M * N, 256), 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B,
+                                                                         b_rs, b_cs, e, m_fast);
+    note_launch();
+    PPLL_LAUNCH_CHECK();
+    return PPLL_OK;
+  }
   dim3 grid(ceil_div(N, SB_N), ceil_div(M, SB_M), 1);
   int tiles = grid.x * grid.y;
   int splits = 1;
@@ -190,7 +258,7 @@ template int launch_colsum<__nv_bfloat16>(int, int, const __nv_bfloat16*, int, f
 // fixed order in double so the scalar is deterministic.
 // ------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 softmax_xent_kernel(int B, int C, const T* __restrict__ z, int ldz, const int64_t* __restrict__ y,
                     T* __restrict__ dz, int lddz, float* loss_hist, const int* step, int* err) {
   extern __shared__ float row_loss[];
@@ -198,43 +266,48 @@ softmax_xent_kernel(int B, int C, const T* __restrict__ z, int ldz, const int64_
   const float invB = 1.0f / (float)B;
   for (int r = w; r < B; r += nw) {
     const T* zr = z + (long)r * ldz;
-    long lab = y[r];
-    bool bad = (lab < 0 || lab >= C);
+    const long lab = y[r];
+    const bool bad = (lab < 0 || lab >= C);
     float mx = -INFINITY;
     for (int c = lane; c < C; c += 32) mx = fmaxf(mx, to_f(zr[c]));
     mx = warp_max(mx);
-    float se = 0.f;
-    for (int c = lane; c < C; c += 32) se += expf(to_f(zr[c]) - mx);
+    float se = 0.f, zl = 0.f;
+    for (int c = lane; c < C; c += 32) {
+      const float v = to_f(zr[c]);
+      se += __expf(v - mx);
+      if (c == lab) zl = v;
+    }
     se = warp_sum(se);
-    float lse = logf(se);
+    zl = warp_sum(zl);
+    const float inv = 1.0f / se;
     T* dr = dz + (long)r * lddz;
     for (int c = lane; c < C; c += 32) {
-      float zc = to_f(zr[c]);
-      float p = expf(zc - mx) / se;
-      float gcv = (p - (c == lab ? 1.f : 0.f)) * invB;
-      DT<T>::st(dr + c, bad ? 0.f : gcv);
+      const float p = __expf(to_f(zr[c]) - mx) * inv;
+      DT<T>::st(dr + c, bad ? 0.f : (p - (c == lab ? 1.f : 0.f)) * invB);
     }
     if (lane == 0) {
-      float zl = bad ? 0.f : to_f(zr[lab]);
-      row_loss[r] = -((zl - mx) - lse);
+      row_loss[r] = bad ? 0.f : -((zl - mx) - logf(se));
       if (bad && err) atomicOr(err, kErrLabel);
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (w == 0) {   // fixed-order reduction: lane-strided partials, then a fixed tree
     double s = 0.0;
-    for (int r = 0; r < B; ++r) s += (double)row_loss[r];
-    float loss = (float)(s / (double)B);
-    int idx = step ? *step : 0;
-    loss_hist[idx] = loss;
-    if (!isfinite(loss) && err) atomicOr(err, kErrLossNonFinite);
+    for (int r = lane; r < B; r += 32) s += (double)row_loss[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const float loss = (float)(s / (double)B);
+      loss_hist[step ? *step : 0] = loss;
+      if (!isfinite(loss) && err) atomicOr(err, kErrLossNonFinite);
+    }
   }
 }
 
 template <typename T>
 int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* dz, int lddz,
                         float* loss_hist, const int* step, int* err, cudaStream_t s) {
-  int threads = B >= 256 ? 512 : 256;
+  int threads = B >= 32 ? 1024 : 32 * B;
   size_t smem = sizeof(float) * (size_t)B;
   if (smem > 48 * 1024) {
     set_error("softmax_xent: batch %d too large", B);

@@ -107,6 +107,8 @@ ppll_stage* ppll_stage_create(int n_layers, int n_block, const int* in_w, const 
     ppll_stage_destroy(st);
     return nullptr;
   }
+  // split-K tickets live at the end of the workspace and must start at zero
+  cudaMemset(st->ws, 0, st->ws_elems * sizeof(float));
   return st;
 }
 
