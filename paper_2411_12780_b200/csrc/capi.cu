@@ -24,20 +24,31 @@ void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_re
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 using bf16 = __nv_bfloat16;
 
-// ---- linear forward: Y = relu?(X·W + b) ------------------------------------
-int linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,
-               void* Y, int ldy, void* Y2, int ldy2, int relu, int dtype, float* ws,
-               size_t ws_elems, cudaStream_t s) {
+template <typename TO>
+static Epilogue<TO> make_ep(const LinOpts& o, void* C, long ldc, int ncols) {
+  Epilogue<TO> e;
+  e.C = (TO*)C; e.ldc = ldc;
+  e.C2 = (TO*)o.C2; e.ldc2 = o.ldc2;
+  e.bias = o.bias; e.act = o.act;
+  e.mask = (const TO*)o.mask; e.ldmask = o.ldmask;
+  e.mask_mode = o.mask ? (o.mask_mode ? o.mask_mode : (int)kMaskRelu) : (int)kMaskNone;
+  e.res = (const TO*)o.res; e.ldres = o.ldres;
+  e.pre = (TO*)o.pre; e.ldpre = o.ldpre;
+  epilogue_finalize(e, ncols);
+  return e;
+}
+
+// ---- linear forward: Y = act(X·W + b [+ R]) ----------------------------------
+int gemm_fwd(int M, int K, int N, const void* X, long ldx, const void* W, const LinOpts& o,
+             void* Y, long ldy, int dtype, float* ws, size_t ws_elems, cudaStream_t s) {
   if (M < 0 || K < 1 || N < 1) { set_error("linear_fwd: bad shape %d %d %d", M, K, N); return PPLL_ERR_ARG; }
   if (M == 0) return PPLL_OK;
   if (dtype == PPLL_F32) {
-    Epilogue<float> ep;
-    ep.C = (float*)Y; ep.ldc = ldy; ep.C2 = (float*)Y2; ep.ldc2 = ldy2; ep.bias = b; ep.relu = relu;
+    auto ep = make_ep<float>(o, Y, ldy, N);
     return launch_gemm_simt<float, float>(M, N, K, (const float*)X, ldx, 1, (const float*)W, N, 1,
                                           ep, ws, ws_elems, s);
   }
-  Epilogue<bf16> ep;
-  ep.C = (bf16*)Y; ep.ldc = ldy; ep.C2 = (bf16*)Y2; ep.ldc2 = ldy2; ep.bias = b; ep.relu = relu;
+  auto ep = make_ep<bf16>(o, Y, ldy, N);
   if (g_gemm_engine != PPLL_GEMM_SIMT) {
     int r = launch_gemm_tc<bf16>(M, N, K, (const bf16*)X, ldx, true, (const bf16*)W, N, false, ep,
                                  ws, ws_elems, s);
@@ -47,20 +58,17 @@ int linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const
                                       ws, ws_elems, s);
 }
 
-// ---- linear dgrad: dX = (dY·Wᵀ) ⊙ [mask > 0] --------------------------------
-int linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void* W, const void* mask,
-                 int ldmask, void* dX, int lddx, int dtype, float* ws, size_t ws_elems,
-                 cudaStream_t s) {
+// ---- linear dgrad: dX = (dY·Wᵀ) ⊙ mask-function ------------------------------
+int gemm_dgrad(int M, int K, int N, const void* dY, long lddy, const void* W, const LinOpts& o,
+               void* dX, long lddx, int dtype, float* ws, size_t ws_elems, cudaStream_t s) {
   if (M < 0 || K < 1 || N < 1) { set_error("linear_dgrad: bad shape"); return PPLL_ERR_ARG; }
   if (M == 0) return PPLL_OK;
   if (dtype == PPLL_F32) {
-    Epilogue<float> ep;
-    ep.C = (float*)dX; ep.ldc = lddx; ep.mask = (const float*)mask; ep.ldmask = ldmask;
+    auto ep = make_ep<float>(o, dX, lddx, K);
     return launch_gemm_simt<float, float>(M, K, N, (const float*)dY, lddy, 1, (const float*)W, 1, N,
                                           ep, ws, ws_elems, s);
   }
-  Epilogue<bf16> ep;
-  ep.C = (bf16*)dX; ep.ldc = lddx; ep.mask = (const bf16*)mask; ep.ldmask = ldmask;
+  auto ep = make_ep<bf16>(o, dX, lddx, K);
   if (g_gemm_engine != PPLL_GEMM_SIMT) {
     int r = launch_gemm_tc<bf16>(M, K, N, (const bf16*)dY, lddy, true, (const bf16*)W, N, true, ep,
                                  ws, ws_elems, s);
@@ -70,12 +78,29 @@ int linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void* W, c
                                       ws, ws_elems, s);
 }
 
+int linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,
+               void* Y, int ldy, void* Y2, int ldy2, int relu, int dtype, float* ws,
+               size_t ws_elems, cudaStream_t s) {
+  LinOpts o;
+  o.bias = b; o.act = relu ? kActRelu : kActNone; o.C2 = Y2; o.ldc2 = ldy2;
+  return gemm_fwd(M, K, N, X, ldx, W, o, Y, ldy, dtype, ws, ws_elems, s);
+}
+
+int linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void* W, const void* mask,
+                 int ldmask, void* dX, int lddx, int dtype, float* ws, size_t ws_elems,
+                 cudaStream_t s) {
+  LinOpts o;
+  o.mask = mask; o.ldmask = ldmask; o.mask_mode = mask ? kMaskRelu : kMaskNone;
+  return gemm_dgrad(M, K, N, dY, lddy, W, o, dX, lddx, dtype, ws, ws_elems, s);
+}
+
 // ---- linear wgrad: dW = Xᵀ·dY (fp32), db = Σ_rows dY ------------------------
 int linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, int lddy, float* dW,
                  float* db, int dtype, float* ws, size_t ws_elems, cudaStream_t s) {
   if (M < 0 || K < 1 || N < 1) { set_error("linear_wgrad: bad shape"); return PPLL_ERR_ARG; }
   Epilogue<float> ep;
   ep.C = dW; ep.ldc = N;
+  epilogue_finalize(ep, N);
   int r;
   if (dtype == PPLL_F32) {
     r = launch_gemm_simt<float, float>(K, N, M, (const float*)X, 1, ldx, (const float*)dY, lddy, 1,

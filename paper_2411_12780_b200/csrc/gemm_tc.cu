@@ -12,12 +12,12 @@
 //               frees the smem slot; accumulators are DOUBLE-BUFFERED in
 //               TMEM (2 x BN columns) so tile i+1's MMAs overlap tile i's
 //               epilogue;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (row per thread) → smem
-//               transpose → column-per-lane coalesced stores with the fused
-//               bias / ReLU / ReLU-mask / dual store (the ring push), or
-//               fp32 split-K partials; the last CTA to finish a split tile
-//               (atomic ticket) reduces the partials in fixed order and runs
-//               the epilogue — deterministic, no extra launch.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (one accumulator row per
+//               thread) → fused bias / residual / pre-activation store /
+//               ReLU|GELU / ReLU-mask|GELU-gradient / dual store (the ring
+//               push), 32-column row segments moved as 16-B vectors; or fp32
+//               split-K partials reduced afterwards in fixed split order
+//               (deterministic) by splitk_reduce_kernel with the same epilogue.
 // Operand layouts (128-byte swizzled, TMA box inner extent 64 elements):
 //   K-major  box {64 (K), rows};  UMMA desc SBO = 1024 B, K step +32 B.
 //   MN-major boxes {64 (MN), 64 (K)} every 8 KB along MN;  UMMA desc
@@ -34,7 +34,6 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 constexpr int kNumSMs = 148;
-constexpr int kTickets = 4096;   // split-K tile tickets kept at the end of the workspace
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -104,9 +103,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void epi_bar() {   // the 4 epilogue warps only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-}
 
 template <int BN>
 struct Smem {
@@ -114,7 +110,7 @@ struct Smem {
   static constexpr int B_BYTES = BN * BK * 2;     // BN * 128 B
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
-  static constexpr int EPI = 4 * 32 * 33 * 4;     // per-warp 32x33 fp32 transpose tiles
+  static constexpr int EPI = 0;
   static constexpr int TOTAL = STAGES * STAGE + EPI + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
@@ -126,19 +122,17 @@ struct Sched {
 template <typename TO, bool A_K, bool B_K, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               int M, int N, int K, Sched sc, Epilogue<TO> ep, float* part, int* tickets) {
+               int M, int N, int K, Sched sc, Epilogue<TO> ep, float* part) {
   using L = Smem<BN>;
   constexpr int S = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
-  float* epi_smem = reinterpret_cast<float*>(smem + S * L::STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGE + L::EPI);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;      // [2]
   uint64_t* tempty = tfull + 2;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
@@ -236,8 +230,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     __syncwarp();
   } else {
     // ------------------------- epilogue -----------------------------
+    // thread = one accumulator row; 32-column segments move as 16-B vectors
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
-    float* tile_s = epi_smem + (warp - 2) * (32 * 33);
     int it = 0;
     for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
       const int tile = w % sc.tiles, z = w / sc.tiles;
@@ -245,55 +239,26 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int rbase = m0 + q * 32;
+      const int row = m0 + q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < BN && n0 + c < N; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
+        float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) tile_s[lane * 33 + i] = __uint_as_float(r[i]);
-        __syncwarp();
-        const int col = n0 + c + lane;
-        if (col < N) {
-          if (sc.splits > 1) {
-            float* dst = part + ((long)z * M) * N + col;
-            for (int rr = 0; rr < 32 && rbase + rr < M; ++rr)
-              dst[(long)(rbase + rr) * N] = tile_s[rr * 33 + lane];
-          } else {
-            for (int rr = 0; rr < 32 && rbase + rr < M; ++rr)
-              ep.apply(rbase + rr, col, tile_s[rr * 33 + lane]);
-          }
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (row < M) {
+          if (sc.splits > 1)
+            st_row32<float>(part + ((long)z * M + row) * N + n0 + c, (N % 4) == 0,
+                            min(32, N - n0 - c), v);
+          else
+            ep.apply_row32(row, n0 + c, v);
         }
-        __syncwarp();
       }
       // accumulator buffer drained: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (sc.splits > 1) {
-        // deterministic split-K fix-up by the last CTA of this tile
-        __threadfence();
-        epi_bar();
-        if (threadIdx.x == 64) {
-          int old = atomicAdd(&tickets[tile], 1);
-          *s_last = (old == sc.splits - 1);
-        }
-        epi_bar();
-        if (*s_last) {
-          __threadfence();
-          for (int c = 0; c < BN; c += 32) {
-            const int col = n0 + c + lane;
-            if (col >= N) continue;
-            for (int rr = 0; rr < 32 && rbase + rr < M; ++rr) {
-              const long off = (long)(rbase + rr) * N + col;
-              float s = 0.f;
-              for (int zz = 0; zz < sc.splits; ++zz) s += __ldcg(part + (long)zz * M * N + off);
-              ep.apply(rbase + rr, col, s);
-            }
-          }
-          if (threadIdx.x == 64) tickets[tile] = 0;   // re-arm for the next launch
-        }
-      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -339,7 +304,7 @@ static bool make_map(CUtensorMap* map, const void* ptr, long inner, long outer, 
 
 template <typename TO, bool A_K, bool B_K, int BN>
 static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const Sched& sc,
-               const Epilogue<TO>& ep, float* part, int* tickets, cudaStream_t s) {
+               const Epilogue<TO>& ep, float* part, cudaStream_t s) {
   auto kern = gemm_tc_kernel<TO, A_K, B_K, BN>;
   constexpr int smem = Smem<BN>::TOTAL;
   static bool attr_set = false;
@@ -348,7 +313,7 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
     attr_set = true;
   }
   const int grid = sc.items < kNumSMs ? sc.items : kNumSMs;
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, M, N, K, sc, ep, part, tickets);
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, M, N, K, sc, ep, part);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -356,22 +321,16 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
 
 template <typename TO, bool A_K, bool B_K>
 static int dispatch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
-                       const Sched& sc, const Epilogue<TO>& ep, float* part, int* tickets,
-                       cudaStream_t s) {
+                       const Sched& sc, const Epilogue<TO>& ep, float* part, cudaStream_t s) {
   switch (bn) {
-    case 256: return run<TO, A_K, B_K, 256>(ma, mb, M, N, K, sc, ep, part, tickets, s);
-    case 192: return run<TO, A_K, B_K, 192>(ma, mb, M, N, K, sc, ep, part, tickets, s);
-    case 128: return run<TO, A_K, B_K, 128>(ma, mb, M, N, K, sc, ep, part, tickets, s);
-    default: return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, sc, ep, part, tickets, s);
+    case 256: return run<TO, A_K, B_K, 256>(ma, mb, M, N, K, sc, ep, part, s);
+    case 192: return run<TO, A_K, B_K, 192>(ma, mb, M, N, K, sc, ep, part, s);
+    case 128: return run<TO, A_K, B_K, 128>(ma, mb, M, N, K, sc, ep, part, s);
+    default: return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, sc, ep, part, s);
   }
 }
 
 }  // namespace tc
-
-// workspace layout: [partials ... | kTickets ints (zeroed once, re-armed by the kernel)]
-size_t gemm_tc_ticket_offset(size_t ws_elems) {
-  return ws_elems >= (size_t)tc::kTickets ? ws_elems - tc::kTickets : 0;
-}
 
 template <typename TO>
 int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_kmajor,
@@ -389,7 +348,6 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   const int cands[4] = {256, 192, 128, 64};
   for (int i = 0; i < 4; ++i) {
     const int c = cands[i];
-    if (c > 64 && !b_kmajor && c % 64) continue;
     const long tiles = (long)mt * ceil_div(N, c);
     const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (c + 32);
     if (best < 0 || cost < best) { best = cost; bn = c; }
@@ -399,32 +357,30 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   sc.nt = ceil_div(N, bn);
   sc.tiles = sc.mt * sc.nt;
   int splits = 1;
-  float* part = nullptr;
-  int* tickets = nullptr;
-  const size_t tick_off = gemm_tc_ticket_offset(ws_elems);
-  if (ws && tick_off > 0 && sc.tiles <= kTickets && sc.tiles * 2 <= kNumSMs && K >= 8 * BK) {
+  if (ws && sc.tiles * 2 <= kNumSMs && K >= 8 * BK) {
     splits = kNumSMs / sc.tiles;
     if (splits > K / (4 * BK)) splits = K / (4 * BK);
-    while (splits > 1 && (size_t)splits * M * N > tick_off) --splits;
+    while (splits > 1 && (size_t)splits * M * N > ws_elems) --splits;
     if (splits < 1) splits = 1;
   }
   sc.kps = ceil_div(ceil_div(K, splits), BK) * BK;
   sc.splits = ceil_div(K, sc.kps);
   sc.items = sc.tiles * sc.splits;
-  if (sc.splits > 1) {
-    part = ws;
-    tickets = reinterpret_cast<int*>(ws + tick_off);
-  }
   CUtensorMap ma, mb;
   bool ok = a_kmajor ? make_map(&ma, A, K, M, lda, BM) : make_map(&ma, A, M, K, lda, 64);
   ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, bn) : make_map(&mb, B, N, K, ldb, 64));
   if (!ok) return PPLL_ERR_UNSUPPORTED;
   Epilogue<TO> e = ep;
   e.partial = nullptr;
-  if (a_kmajor && !b_kmajor) return dispatch_bn<TO, true, false>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
-  if (a_kmajor && b_kmajor) return dispatch_bn<TO, true, true>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
-  if (!a_kmajor && !b_kmajor) return dispatch_bn<TO, false, false>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
-  return dispatch_bn<TO, false, true>(bn, ma, mb, M, N, K, sc, e, part, tickets, s);
+  float* part = sc.splits > 1 ? ws : nullptr;
+  int r;
+  if (a_kmajor && !b_kmajor) r = dispatch_bn<TO, true, false>(bn, ma, mb, M, N, K, sc, e, part, s);
+  else if (a_kmajor && b_kmajor) r = dispatch_bn<TO, true, true>(bn, ma, mb, M, N, K, sc, e, part, s);
+  else if (!a_kmajor && !b_kmajor) r = dispatch_bn<TO, false, false>(bn, ma, mb, M, N, K, sc, e, part, s);
+  else r = dispatch_bn<TO, false, true>(bn, ma, mb, M, N, K, sc, e, part, s);
+  if (r || sc.splits == 1) return r;
+  // deterministic split-K reduction (fixed split order) + the fused epilogue
+  return launch_splitk_reduce<TO>(M, N, sc.splits, ws, ep, s);
 }
 
 template int launch_gemm_tc<float>(int, int, int, const __nv_bfloat16*, long, bool, const __nv_bfloat16*, long, bool, const Epilogue<float>&, float*, size_t, cudaStream_t);

@@ -6,7 +6,91 @@ namespace ppll {
 
 void note_launch(int n = 1);
 
-// GEMM epilogue: v -> (+bias[n]) -> relu? -> ⊙[mask>0] -> C (and C2).
+enum Act : int { kActNone = 0, kActRelu = 1, kActGelu = 2 };
+enum MaskMode : int { kMaskNone = 0, kMaskRelu = 1, kMaskGeluGrad = 2 };
+
+__device__ __forceinline__ float gelu_f(float x) {        // exact (erf) GELU
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {   // d/dx gelu(x)
+  const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+  const float pdf = 0.3989422804014327f * __expf(-0.5f * x * x);
+  return cdf + x * pdf;
+}
+
+template <typename T>
+__device__ __forceinline__ void ld_row32(const T* p, bool vec, int valid, float (&o)[32]);
+template <>
+__device__ __forceinline__ void ld_row32<float>(const float* p, bool vec, int valid, float (&o)[32]) {
+  if (vec && valid == 32) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 q = reinterpret_cast<const float4*>(p)[i];
+      o[4 * i] = q.x; o[4 * i + 1] = q.y; o[4 * i + 2] = q.z; o[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = i < valid ? p[i] : 0.f;
+  }
+}
+template <>
+__device__ __forceinline__ void ld_row32<__nv_bfloat16>(const __nv_bfloat16* p, bool vec, int valid,
+                                                        float (&o)[32]) {
+  if (vec && valid == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 q = reinterpret_cast<const uint4*>(p)[i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        o[8 * i + 2 * j] = f.x;
+        o[8 * i + 2 * j + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = i < valid ? __bfloat162float(p[i]) : 0.f;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st_row32(T* p, bool vec, int valid, const float (&v)[32]);
+template <>
+__device__ __forceinline__ void st_row32<float>(float* p, bool vec, int valid, const float (&v)[32]) {
+  if (vec && valid == 32) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      reinterpret_cast<float4*>(p)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) p[i] = v[i];
+  }
+}
+template <>
+__device__ __forceinline__ void st_row32<__nv_bfloat16>(__nv_bfloat16* p, bool vec, int valid,
+                                                        const float (&v)[32]) {
+  if (vec && valid == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 q;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+      reinterpret_cast<uint4*>(p)[i] = q;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) p[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+// GEMM epilogue:
+//   v -> (+bias[n]) -> (+R[m,n]) -> [store pre-activation P] -> act (ReLU|GELU)
+//     -> ReLU mask (v·[mask>0]) | GELU gradient (v·gelu'(mask)) -> C (and C2)
+// `vec` = every pointer 16-B aligned and every leading dimension a multiple of
+// 16 B, so 32-column row segments move as 16-B vectors.
 template <typename TO>
 struct Epilogue {
   TO* C = nullptr;
@@ -14,19 +98,81 @@ struct Epilogue {
   TO* C2 = nullptr;       // optional dual store (fused ring push)
   long ldc2 = 0;
   const float* bias = nullptr;
-  int relu = 0;
+  int act = kActNone;
   const TO* mask = nullptr;
   long ldmask = 0;
+  int mask_mode = kMaskNone;
+  const TO* res = nullptr;   // residual added before the activation
+  long ldres = 0;
+  TO* pre = nullptr;         // pre-activation store (GELU backward)
+  long ldpre = 0;
+  int ncols = 0;             // N (for row-segment bounds)
+  int vec = 0;
   float* partial = nullptr;  // split-K workspace (internal)
 
+  __device__ __forceinline__ float act_f(float v) const {
+    if (act == kActRelu) return fmaxf(v, 0.f);
+    if (act == kActGelu) return gelu_f(v);
+    return v;
+  }
   __device__ __forceinline__ void apply(int m, int n, float v) const {
     if (bias) v += bias[n];
-    if (relu) v = fmaxf(v, 0.f);
-    if (mask) v = (to_f(mask[(long)m * ldmask + n]) > 0.f) ? v : 0.f;
+    if (res) v += to_f(res[(long)m * ldres + n]);
+    if (pre) DT<TO>::st(pre + (long)m * ldpre + n, v);
+    v = act_f(v);
+    if (mask_mode == kMaskRelu) v = (to_f(mask[(long)m * ldmask + n]) > 0.f) ? v : 0.f;
+    else if (mask_mode == kMaskGeluGrad) v *= gelu_grad_f(to_f(mask[(long)m * ldmask + n]));
     DT<TO>::st(C + (long)m * ldc + n, v);
     if (C2) DT<TO>::st(C2 + (long)m * ldc2 + n, v);
   }
+  // 32 consecutive columns n0..n0+31 of row m (n0 % 32 == 0)
+  __device__ __forceinline__ void apply_row32(int m, int n0, float (&v)[32]) const {
+    const int valid = min(32, ncols - n0);
+    const bool vv = vec != 0;
+    if (bias) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += (i < valid) ? __ldg(bias + n0 + i) : 0.f;
+    }
+    if (res) {
+      float r[32];
+      ld_row32<TO>(res + (long)m * ldres + n0, vv, valid, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += r[i];
+    }
+    if (pre) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, v);
+    if (act != kActNone) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i]);
+    }
+    if (mask_mode != kMaskNone) {
+      float k[32];
+      ld_row32<TO>(mask + (long)m * ldmask + n0, vv, valid, k);
+      if (mask_mode == kMaskRelu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(k[i]);
+      }
+    }
+    st_row32<TO>(C + (long)m * ldc + n0, vv, valid, v);
+    if (C2) st_row32<TO>(C2 + (long)m * ldc2 + n0, vv, valid, v);
+  }
 };
+
+// host: decide the vector flag from pointer alignment and leading dimensions
+template <typename TO>
+inline void epilogue_finalize(Epilogue<TO>& e, int ncols) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  auto ldok = [](long ld) { return (ld * (long)sizeof(TO)) % 16 == 0; };
+  e.ncols = ncols;
+  bool v = al(e.C) && ldok(e.ldc);
+  if (e.C2) v = v && al(e.C2) && ldok(e.ldc2);
+  if (e.mask) v = v && al(e.mask) && ldok(e.ldmask);
+  if (e.res) v = v && al(e.res) && ldok(e.ldres);
+  if (e.pre) v = v && al(e.pre) && ldok(e.ldpre);
+  e.vec = v ? 1 : 0;
+}
 
 template <typename TI, typename TO>
 int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, const TI* B,
@@ -60,6 +206,25 @@ int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t
 int launch_ring_publish(int* w, int seq, cudaStream_t s);
 int launch_ring_wait(const int* w, int seq, cudaStream_t s);
 int launch_ring_release(int* w, cudaStream_t s);
+
+// Host-side description of a fused linear epilogue (see Epilogue).
+struct LinOpts {
+  const float* bias = nullptr;
+  int act = kActNone;
+  const void* mask = nullptr;
+  long ldmask = 0;
+  int mask_mode = kMaskNone;
+  const void* res = nullptr;
+  long ldres = 0;
+  void* pre = nullptr;
+  long ldpre = 0;
+  void* C2 = nullptr;
+  long ldc2 = 0;
+};
+int gemm_fwd(int M, int K, int N, const void* X, long ldx, const void* W, const LinOpts& o,
+             void* Y, long ldy, int dtype, float* ws, size_t ws_elems, cudaStream_t s);
+int gemm_dgrad(int M, int K, int N, const void* dY, long lddy, const void* W, const LinOpts& o,
+               void* dX, long lddx, int dtype, float* ws, size_t ws_elems, cudaStream_t s);
 
 // linear-layer ops used by both the C-ABI and the stage runtime
 int linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,
