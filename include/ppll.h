@@ -134,6 +134,29 @@ int ppll_stage_step(ppll_stage* st, int B, const void* x_in, const int64_t* labe
 int ppll_stage_forward(ppll_stage* st, int B, const void* x_in, void* h_out, void* logits,
                        void* stream);
 
+/* ---- one local step of a ViT stage (same step semantics, blocks.py:266-289,
+ * applied to pre-LN transformer blocks; no reference implementation exists —
+ * parity is pinned to oracle/vit_oracle.py) -------------------------------
+ * cfg[12] = {max_batch, tokens, dim, heads, mlp, classes, n_block_layers,
+ *            n_aux_layers, has_patch_embed, img_channels, img_size, patch}
+ * offsets = [wpe, bpe, cls, pos] (stage 0; ignored otherwise)
+ *         + 12 per transformer layer (ln1_g, ln1_b, wqkv, bqkv, wo, bo, ln2_g,
+ *           ln2_b, w1, b1, w2, b2), block layers then aux layers
+ *         + [lnf_g, lnf_b, wh, bh] (aux head, or the task head on the final stage)
+ * Activations are [batch*tokens, dim] row-major; stage 0 takes images
+ * [batch, C, H, W] in the activation dtype. */
+typedef struct ppll_vit_stage ppll_vit_stage;
+ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, int64_t n_params,
+                                      int dtype, float* theta, float* grad, float* mom,
+                                      void* theta_lp, const float* lr_table, int* step,
+                                      int max_step, float* loss_hist, int* err, float mu,
+                                      float wd);
+void ppll_vit_stage_destroy(ppll_vit_stage* st);
+int ppll_vit_stage_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
+                        void* x_out, void* stream);
+int ppll_vit_stage_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_out,
+                           void* logits, void* stream);
+
 /* ---- stage-boundary ring (runtime.py:52-120 StageBuffer) ----------------
  * Device-resident flag words for an SPSC ring of `capacity` slots.  ready[i]
  * holds the sequence number (batch_id+1) published into slot i; credit holds

@@ -51,5 +51,6 @@ from .runtime import (
     throughput,
 )
 from .tensor import Tensor, matmul, softmax_xent
+from .vit import VitLocalModule, VitSpec, balanced_depths, build_vit_modules
 
 __version__ = "0.1.0"

@@ -239,6 +239,32 @@ class LocalModule:
         except Exception:
             pass
 
+    # -- generic stage interface used by the runtime ------------------------
+    @property
+    def in_shape(self) -> tuple:
+        return (self.input_width,)
+
+    @property
+    def out_shape(self) -> tuple:
+        return (self.output_width,)
+
+    @property
+    def in_features(self) -> int:
+        return int(np.prod(self.in_shape))
+
+    @property
+    def out_features(self) -> int:
+        return int(np.prod(self.out_shape))
+
+    def launch_step(self, B, x_ptr, y_ptr, out_ptr, stream) -> None:
+        """Enqueue one local step (``ppll_stage_step``) on ``stream``."""
+        N.check(N.load().ppll_stage_step(self.native(B), B, x_ptr, y_ptr, out_ptr, stream),
+                f"stage {self.stage_index} step")
+
+    def launch_forward(self, B, x_ptr, h_ptr, logits_ptr, stream) -> None:
+        N.check(N.load().ppll_stage_forward(self.native(B), B, x_ptr, h_ptr, logits_ptr, stream),
+                f"stage {self.stage_index} forward")
+
     def error_word(self) -> int:
         """Sticky device error bits (synchronises this module's device)."""
         return int(self._flat["state"][2].item())
@@ -370,27 +396,30 @@ def _materialise(j, host, n_block, assigned, hidden, hyper, device):
 # --------------------------------------------------------------------------
 
 def _as_input(module: LocalModule, x: Tensor) -> torch.Tensor:
+    """[B, *in_shape] (or [B, in_features]) device tensor in the stage dtype,
+    flattened to [B, in_features]."""
     t = x.dev
-    if t.dim() != 2 or t.shape[1] != module.input_width:
+    ok = t.dim() >= 2 and (tuple(t.shape[1:]) == tuple(module.in_shape) or
+                           (t.dim() == 2 and t.shape[1] == module.in_features))
+    if not ok:
         raise DimensionMismatch(
-            f"stage {module.stage_index} expects width {module.input_width}, got {x.shape}")
+            f"stage {module.stage_index} expects width {module.in_shape}, got {x.shape}")
     require_cuda(t, f"stage {module.stage_index}")
     if t.device != module.device or t.dtype != module.act_dtype:
         t = t.to(device=module.device, dtype=module.act_dtype)
-    return t.contiguous()
+    return t.reshape(t.shape[0], module.in_features).contiguous()
 
 
 def _forward(module: LocalModule, x: Tensor, want_logits: bool):
     xin = _as_input(module, x)
     B = xin.shape[0]
-    h = torch.empty((B, module.output_width), dtype=module.act_dtype, device=module.device)
+    h = torch.empty((B,) + tuple(module.out_shape), dtype=module.act_dtype, device=module.device)
     logits = None
     if want_logits:
         logits = torch.empty((B, module.num_classes), dtype=module.act_dtype, device=module.device)
     if B:
         st = torch.cuda.current_stream(module.device).cuda_stream
-        N.check(N.load().ppll_stage_forward(module.native(B), B, xin.data_ptr(), h.data_ptr(),
-                                            N.ptr(logits), st), "stage forward")
+        module.launch_forward(B, xin.data_ptr(), h.data_ptr(), N.ptr(logits), st)
     return h, logits
 
 
@@ -448,19 +477,17 @@ def local_loss_and_update(module: LocalModule, x_in: Tensor, labels,
     if B < 1:
         raise DimensionMismatch("softmax_xent needs a non-empty batch")
     step = module.optimizer.step_count
-    x_out = torch.empty((B, module.output_width), dtype=module.act_dtype, device=module.device)
+    x_out = torch.empty((B,) + tuple(module.out_shape), dtype=module.act_dtype,
+                        device=module.device)
     st = torch.cuda.current_stream(module.device).cuda_stream
-    lib = N.load()
     if step > module.schedule.total_steps:
         # reference order: forward + push happen, then cosine_lr raises (blocks.py:280-287)
-        N.check(lib.ppll_stage_forward(module.native(B), B, xin.data_ptr(), x_out.data_ptr(),
-                                       None, st), "stage forward")
+        module.launch_forward(B, xin.data_ptr(), x_out.data_ptr(), None, st)
         out = Tensor(x_out)
         if on_output is not None:
             on_output(out)
         raise StepOutOfRange(f"step {step} outside [0, {module.schedule.total_steps}]")
-    N.check(lib.ppll_stage_step(module.native(B), B, xin.data_ptr(), y.data_ptr(),
-                                x_out.data_ptr(), st), "stage step")
+    module.launch_step(B, xin.data_ptr(), y.data_ptr(), x_out.data_ptr(), st)
     out = Tensor(x_out)
     if on_output is not None:
         on_output(out)

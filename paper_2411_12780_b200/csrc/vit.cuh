@@ -1,0 +1,34 @@
+// ViT kernel launchers (vit_kernels.cu), used by the ViT stage executor.
+#pragma once
+#include "common.cuh"
+
+namespace ppll {
+
+constexpr float kLnEps = 1e-5f;
+
+template <typename T>
+int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const float* b, T* y,
+                  long ldy, float* mean, float* rstd, cudaStream_t s);
+// dx may be null (only gamma/beta gradients wanted); part/dg/db may be null
+template <typename T>
+int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
+                  const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
+                  float* part, float* dg, float* db, cudaStream_t s);
+int ln_bwd_blocks(int M);
+template <typename T>
+int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse, cudaStream_t s);
+template <typename T>
+int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, const T* dout,
+                    const float* lse, T* dqkv, cudaStream_t s);
+template <typename T>
+int launch_patchify(int B, int C, int HW, int p, const T* img, T* out, cudaStream_t s);
+template <typename T>
+int launch_embed(int B, int P, int D, const T* tok, const float* cls, const float* pos, T* x,
+                 cudaStream_t s);
+template <typename T>
+int launch_embed_bwd(int B, int P, int D, const T* dx, T* dtok, float* dcls, float* dpos,
+                     cudaStream_t s);
+template <typename T>
+int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s);
+
+}  // namespace ppll

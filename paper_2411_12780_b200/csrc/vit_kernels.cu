@@ -1,0 +1,501 @@
+// Bandwidth-bound / small-sequence kernels of the ViT local step (sm_100a):
+// LayerNorm fwd/bwd (+ deterministic gamma/beta reductions), multi-head
+// self-attention fwd/bwd for short sequences (T <= 160, head_dim 64), patch
+// extraction and token-embedding assembly.  fp32 math, T in {float, bf16}.
+// The GEMM-shaped work of the layer (QKV, projection, MLP) runs on the
+// tcgen05 engine (gemm_tc.cu); see vit_stage.cu for the step schedule.
+#include <math.h>
+#include "common.cuh"
+#include "kernels.cuh"
+#include "vit.cuh"
+
+namespace ppll {
+
+// ---------------------------------------------------------------------------
+// LayerNorm forward: one warp per row, D <= 1024 (D % 32 == 0).
+// y = (x - mean) * rstd * g + b ; stores mean/rstd for the backward.
+// ---------------------------------------------------------------------------
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256)
+ln_fwd_kernel(int M, int D, const T* __restrict__ x, long ldx, const float* __restrict__ g,
+              const float* __restrict__ b, T* __restrict__ y, long ldy, float* __restrict__ mean,
+              float* __restrict__ rstd) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const T* xr = x + (long)row * ldx;
+  float v[VPL];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < D ? to_f(xr[c]) : 0.f;
+    s += v[i];
+  }
+  const float mu = warp_sum(s) / (float)D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    const float d = c < D ? v[i] - mu : 0.f;
+    q += d * d;
+  }
+  const float rs = rsqrtf(warp_sum(q) / (float)D + kLnEps);
+  T* yr = y + (long)row * ldy;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < D) DT<T>::st(yr + c, (v[i] - mu) * rs * g[c] + b[c]);
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm backward: warp per row; dx = rstd·(dxh − mean(dxh) − xh·mean(dxh·xh))
+// (+ dres, the residual-stream gradient, fused).  Per-block partial sums of
+// dg = Σ dy·xh and db = Σ dy go to part[block][2][D] (fixed order).
+// ---------------------------------------------------------------------------
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256)
+ln_bwd_kernel(int M, int D, const T* __restrict__ dy, long lddy, const T* __restrict__ x, long ldx,
+              const float* __restrict__ mean, const float* __restrict__ rstd,
+              const float* __restrict__ g, const T* __restrict__ dres, long ldres,
+              T* __restrict__ dx, long lddx, float* __restrict__ part, int rows_per_block) {
+  __shared__ float red[2][32 * VPL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float pg[VPL], pb[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) pg[i] = pb[i] = 0.f;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(M, r0 + rows_per_block);
+  for (int row = r0 + w; row < r1; row += 8) {
+    const T* dyr = dy + (long)row * lddy;
+    const T* xr = x + (long)row * ldx;
+    const float mu = mean[row], rs = rstd[row];
+    float xh[VPL], dxh[VPL];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < D) {
+        const float d = to_f(dyr[c]);
+        xh[i] = (to_f(xr[c]) - mu) * rs;
+        dxh[i] = d * g[c];
+        pg[i] += d * xh[i];
+        pb[i] += d;
+      } else {
+        xh[i] = dxh[i] = 0.f;
+      }
+      s1 += dxh[i];
+      s2 += dxh[i] * xh[i];
+    }
+    s1 = warp_sum(s1) / (float)D;
+    s2 = warp_sum(s2) / (float)D;
+    if (dx) {
+      T* dxr = dx + (long)row * lddx;
+      const T* rr = dres ? dres + (long)row * ldres : nullptr;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < D) {
+          float o = rs * (dxh[i] - s1 - xh[i] * s2);
+          if (rr) o += to_f(rr[c]);
+          DT<T>::st(dxr + c, o);
+        }
+      }
+    }
+  }
+  if (part) {
+    // warps accumulate in a fixed order (warp 0, 1, ..., 7): deterministic
+    for (int k = 0; k < 8; ++k) {
+      if (w == k) {
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int c = lane + 32 * i;
+          red[0][c] = (k == 0 ? 0.f : red[0][c]) + pg[i];
+          red[1][c] = (k == 0 ? 0.f : red[1][c]) + pb[i];
+        }
+      }
+      __syncthreads();
+    }
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      part[((long)blockIdx.x * 2 + 0) * D + c] = red[0][c];
+      part[((long)blockIdx.x * 2 + 1) * D + c] = red[1][c];
+    }
+  }
+}
+
+__global__ void ln_param_reduce_kernel(int nblk, int D, const float* __restrict__ part,
+                                       float* __restrict__ dg, float* __restrict__ db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= D) return;
+  float a = 0.f, b = 0.f;
+  for (int k = 0; k < nblk; ++k) {
+    a += part[((long)k * 2 + 0) * D + c];
+    b += part[((long)k * 2 + 1) * D + c];
+  }
+  dg[c] = a;
+  db[c] = b;
+}
+
+template <typename T>
+int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const float* b, T* y,
+                  long ldy, float* mean, float* rstd, cudaStream_t s) {
+  if (D % 32 || D > 1024) { set_error("layernorm: D=%d unsupported", D); return PPLL_ERR_ARG; }
+  const int blocks = ceil_div(M, 8);
+  if (D <= 384)
+    ln_fwd_kernel<T, 12><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+  else if (D <= 768)
+    ln_fwd_kernel<T, 24><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+  else
+    ln_fwd_kernel<T, 32><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : 148 * 2; }
+
+template <typename T>
+int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
+                  const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
+                  float* part, float* dg, float* db, cudaStream_t s) {
+  if (D % 32 || D > 1024) { set_error("layernorm: D=%d unsupported", D); return PPLL_ERR_ARG; }
+  const int nblk = ln_bwd_blocks(M);
+  const int rpb = ceil_div(M, nblk);
+  if (D <= 384)
+    ln_bwd_kernel<T, 12><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+  else if (D <= 768)
+    ln_bwd_kernel<T, 24><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+  else
+    ln_bwd_kernel<T, 32><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  if (part && dg) {
+    ln_param_reduce_kernel<<<ceil_div(D, 128), 128, 0, s>>>(nblk, D, part, dg, db);
+    note_launch();
+    PPLL_LAUNCH_CHECK();
+  }
+  return PPLL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-head self-attention, short sequences: one CTA per (batch, head),
+// Q/K/V/S resident in shared memory, fp32 math.
+// qkv rows: [q (H*dh) | k | v], row b*T + t; o rows: b*T + t, head h at h*dh.
+// ---------------------------------------------------------------------------
+constexpr int kDh = 64;
+constexpr int kLd = kDh + 1;
+
+__host__ __device__ inline size_t attn_fwd_smem(int T) {
+  return sizeof(float) * (3 * (size_t)T * kLd + (size_t)T * (T + 1));
+}
+__host__ __device__ inline size_t attn_bwd_smem(int T) {
+  return sizeof(float) * (4 * (size_t)T * kLd + (size_t)T * (T + 1) + (size_t)T);
+}
+
+template <typename T>
+__device__ __forceinline__ void load_head(float* dst, const T* src, int Tn, long ld, int col0) {
+  for (int idx = threadIdx.x; idx < Tn * kDh; idx += blockDim.x) {
+    const int t = idx / kDh, d = idx % kDh;
+    dst[t * kLd + d] = to_f(src[(long)t * ld + col0 + d]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+attn_fwd_kernel(int Tn, int H, const T* __restrict__ qkv, T* __restrict__ o, float* __restrict__ lse,
+                float scale) {
+  extern __shared__ float sm[];
+  float* Q = sm;
+  float* Kk = Q + Tn * kLd;
+  float* V = Kk + Tn * kLd;
+  float* S = V + Tn * kLd;
+  const int b = blockIdx.x / H, h = blockIdx.x % H;
+  const int D = H * kDh;
+  const long ld = 3L * D;
+  const T* base = qkv + (long)b * Tn * ld;
+  load_head(Q, base, Tn, ld, h * kDh);
+  load_head(Kk, base, Tn, ld, D + h * kDh);
+  load_head(V, base, Tn, ld, 2 * D + h * kDh);
+  __syncthreads();
+  const int ldS = Tn + 1;
+  for (int idx = threadIdx.x; idx < Tn * Tn; idx += blockDim.x) {
+    const int i = idx / Tn, j = idx % Tn;
+    const float* qi = Q + i * kLd;
+    const float* kj = Kk + j * kLd;
+    float acc = 0.f;
+#pragma unroll 16
+    for (int d = 0; d < kDh; ++d) acc = fmaf(qi[d], kj[d], acc);
+    S[i * ldS + j] = acc * scale;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = w; i < Tn; i += nw) {
+    float* si = S + i * ldS;
+    float mx = -INFINITY;
+    for (int j = lane; j < Tn; j += 32) mx = fmaxf(mx, si[j]);
+    mx = warp_max(mx);
+    float se = 0.f;
+    for (int j = lane; j < Tn; j += 32) {
+      const float e = __expf(si[j] - mx);
+      si[j] = e;
+      se += e;
+    }
+    se = warp_sum(se);
+    const float inv = 1.f / se;
+    for (int j = lane; j < Tn; j += 32) si[j] *= inv;
+    if (lane == 0) lse[(long)blockIdx.x * Tn + i] = mx + logf(se);
+  }
+  __syncthreads();
+  T* ob = o + (long)b * Tn * D + h * kDh;
+  for (int idx = threadIdx.x; idx < Tn * kDh; idx += blockDim.x) {
+    const int i = idx / kDh, d = idx % kDh;
+    const float* pi = S + i * ldS;
+    float acc = 0.f;
+    for (int j = 0; j < Tn; ++j) acc = fmaf(pi[j], V[j * kLd + d], acc);
+    DT<T>::st(ob + (long)i * D + d, acc);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+attn_bwd_kernel(int Tn, int H, const T* __restrict__ qkv, const T* __restrict__ o,
+                const T* __restrict__ dout, const float* __restrict__ lse, T* __restrict__ dqkv,
+                float scale) {
+  extern __shared__ float sm[];
+  float* Q = sm;
+  float* Kk = Q + Tn * kLd;
+  float* V = Kk + Tn * kLd;
+  float* dO = V + Tn * kLd;
+  float* S = dO + Tn * kLd;
+  float* Di = S + Tn * (Tn + 1);
+  const int b = blockIdx.x / H, h = blockIdx.x % H;
+  const int D = H * kDh;
+  const long ld = 3L * D;
+  const T* base = qkv + (long)b * Tn * ld;
+  load_head(Q, base, Tn, ld, h * kDh);
+  load_head(Kk, base, Tn, ld, D + h * kDh);
+  load_head(V, base, Tn, ld, 2 * D + h * kDh);
+  load_head(dO, dout + (long)b * Tn * D, Tn, D, h * kDh);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // D_i = rowsum(dO ⊙ O)
+  const T* ob = o + (long)b * Tn * D + h * kDh;
+  __syncthreads();
+  for (int i = w; i < Tn; i += nw) {
+    float acc = 0.f;
+    for (int d = lane; d < kDh; d += 32) acc += dO[i * kLd + d] * to_f(ob[(long)i * D + d]);
+    acc = warp_sum(acc);
+    if (lane == 0) Di[i] = acc;
+  }
+  // P = exp(scale·QKᵀ − lse)
+  const int ldS = Tn + 1;
+  const float* lrow = lse + (long)blockIdx.x * Tn;
+  for (int idx = threadIdx.x; idx < Tn * Tn; idx += blockDim.x) {
+    const int i = idx / Tn, j = idx % Tn;
+    const float* qi = Q + i * kLd;
+    const float* kj = Kk + j * kLd;
+    float acc = 0.f;
+#pragma unroll 16
+    for (int d = 0; d < kDh; ++d) acc = fmaf(qi[d], kj[d], acc);
+    S[i * ldS + j] = __expf(acc * scale - lrow[i]);
+  }
+  __syncthreads();
+  T* dq = dqkv + (long)b * Tn * ld + h * kDh;
+  T* dk = dq + D;
+  T* dv = dq + 2 * D;
+  // dV = Pᵀ dO
+  for (int idx = threadIdx.x; idx < Tn * kDh; idx += blockDim.x) {
+    const int j = idx / kDh, d = idx % kDh;
+    float acc = 0.f;
+    for (int i = 0; i < Tn; ++i) acc = fmaf(S[i * ldS + j], dO[i * kLd + d], acc);
+    DT<T>::st(dv + (long)j * ld + d, acc);
+  }
+  __syncthreads();
+  // dS = P ⊙ (dO Vᵀ − D_i), in place
+  for (int idx = threadIdx.x; idx < Tn * Tn; idx += blockDim.x) {
+    const int i = idx / Tn, j = idx % Tn;
+    const float* gi = dO + i * kLd;
+    const float* vj = V + j * kLd;
+    float acc = 0.f;
+#pragma unroll 16
+    for (int d = 0; d < kDh; ++d) acc = fmaf(gi[d], vj[d], acc);
+    S[i * ldS + j] = S[i * ldS + j] * (acc - Di[i]);
+  }
+  __syncthreads();
+  // dQ = scale · dS K ; dK = scale · dSᵀ Q
+  for (int idx = threadIdx.x; idx < Tn * kDh; idx += blockDim.x) {
+    const int i = idx / kDh, d = idx % kDh;
+    float aq = 0.f, ak = 0.f;
+    for (int j = 0; j < Tn; ++j) {
+      aq = fmaf(S[i * ldS + j], Kk[j * kLd + d], aq);
+      ak = fmaf(S[j * ldS + i], Q[j * kLd + d], ak);
+    }
+    DT<T>::st(dq + (long)i * ld + d, aq * scale);
+    DT<T>::st(dk + (long)i * ld + d, ak * scale);
+  }
+}
+
+template <typename T>
+int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse, cudaStream_t s) {
+  if (dh != kDh) { set_error("attention: head_dim %d unsupported (64)", dh); return PPLL_ERR_ARG; }
+  const size_t smem = attn_fwd_smem(Tn);
+  if (smem > 220 * 1024) { set_error("attention: T=%d too long", Tn); return PPLL_ERR_ARG; }
+  static bool set = false;
+  if (!set) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_kernel<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    set = true;
+  }
+  attn_fwd_kernel<T><<<B * H, 256, smem, s>>>(Tn, H, qkv, o, lse, 1.0f / sqrtf((float)dh));
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+template <typename T>
+int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, const T* dout,
+                    const float* lse, T* dqkv, cudaStream_t s) {
+  if (dh != kDh) { set_error("attention: head_dim %d unsupported (64)", dh); return PPLL_ERR_ARG; }
+  const size_t smem = attn_bwd_smem(Tn);
+  if (smem > 220 * 1024) { set_error("attention: T=%d too long", Tn); return PPLL_ERR_ARG; }
+  static bool set = false;
+  if (!set) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_kernel<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    set = true;
+  }
+  attn_bwd_kernel<T><<<B * H, 256, smem, s>>>(Tn, H, qkv, o, dout, lse, dqkv,
+                                              1.0f / sqrtf((float)dh));
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// patches + token assembly
+// ---------------------------------------------------------------------------
+// img [B, C, HW, HW] -> out [B*P, C*p*p], inner order (c, py, px), patches row-major
+template <typename T>
+__global__ void patchify_kernel(int B, int C, int HW, int p, const T* __restrict__ img,
+                                T* __restrict__ out) {
+  const int np = HW / p, P = np * np, pd = C * p * p;
+  const long total = (long)B * P * pd;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    const int e = (int)(idx % pd);
+    const long bp = idx / pd;
+    const int pi = (int)(bp % P), b = (int)(bp / P);
+    const int c = e / (p * p), r = e % (p * p), py = r / p, px = r % p;
+    const int yy = (pi / np) * p + py, xx = (pi % np) * p + px;
+    out[idx] = img[(((long)b * C + c) * HW + yy) * HW + xx];
+  }
+}
+
+// x[b,0,:] = cls + pos[0]; x[b,1+i,:] = tok[b,i,:] + pos[1+i]
+template <typename T>
+__global__ void embed_kernel(int B, int P, int D, const T* __restrict__ tok,
+                             const float* __restrict__ cls, const float* __restrict__ pos,
+                             T* __restrict__ x) {
+  const int Tn = P + 1;
+  const long total = (long)B * Tn * D;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    const int d = (int)(idx % D);
+    const long bt = idx / D;
+    const int t = (int)(bt % Tn), b = (int)(bt / Tn);
+    const float v = t == 0 ? cls[d] : to_f(tok[((long)b * P + t - 1) * D + d]);
+    DT<T>::st(x + idx, v + pos[(long)t * D + d]);
+  }
+}
+
+// dtok[b,i,:] = dx[b,1+i,:]; dcls = Σ_b dx[b,0,:]; dpos[t,:] = Σ_b dx[b,t,:]
+template <typename T>
+__global__ void embed_bwd_kernel(int B, int P, int D, const T* __restrict__ dx, T* __restrict__ dtok,
+                                 float* __restrict__ dcls, float* __restrict__ dpos) {
+  const int Tn = P + 1;
+  const long nt = (long)Tn * D;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < nt;
+       idx += (long)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / D), d = (int)(idx % D);
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) {
+      const float v = to_f(dx[((long)b * Tn + t) * D + d]);
+      s += v;
+      if (t > 0) DT<T>::st(dtok + ((long)b * P + t - 1) * D + d, v);
+    }
+    dpos[idx] = s;
+    if (t == 0) dcls[d] = s;
+  }
+}
+
+// dx = 0 except the cls rows: dx[b,0,:] = dcls_rows[b,:] (head backward)
+template <typename T>
+__global__ void scatter_cls_kernel(int B, int Tn, int D, const T* __restrict__ dz,
+                                   T* __restrict__ dx) {
+  const long total = (long)B * Tn * D;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    const int d = (int)(idx % D);
+    const long bt = idx / D;
+    const int t = (int)(bt % Tn), b = (int)(bt / Tn);
+    DT<T>::st(dx + idx, t == 0 ? to_f(dz[(long)b * D + d]) : 0.f);
+  }
+}
+
+static int grid_for(long n) { return (int)min((n + 255) / 256, (long)148 * 16); }
+
+template <typename T>
+int launch_patchify(int B, int C, int HW, int p, const T* img, T* out, cudaStream_t s) {
+  const long n = (long)B * (HW / p) * (HW / p) * C * p * p;
+  patchify_kernel<T><<<grid_for(n), 256, 0, s>>>(B, C, HW, p, img, out);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template <typename T>
+int launch_embed(int B, int P, int D, const T* tok, const float* cls, const float* pos, T* x,
+                 cudaStream_t s) {
+  embed_kernel<T><<<grid_for((long)B * (P + 1) * D), 256, 0, s>>>(B, P, D, tok, cls, pos, x);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template <typename T>
+int launch_embed_bwd(int B, int P, int D, const T* dx, T* dtok, float* dcls, float* dpos,
+                     cudaStream_t s) {
+  embed_bwd_kernel<T><<<grid_for((long)(P + 1) * D), 256, 0, s>>>(B, P, D, dx, dtok, dcls, dpos);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template <typename T>
+int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s) {
+  scatter_cls_kernel<T><<<grid_for((long)B * Tn * D), 256, 0, s>>>(B, Tn, D, dz, dx);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+#define INST(T)                                                                                  \
+  template int launch_ln_fwd<T>(int, int, const T*, long, const float*, const float*, T*, long,  \
+                                float*, float*, cudaStream_t);                                   \
+  template int launch_ln_bwd<T>(int, int, const T*, long, const T*, long, const float*,          \
+                                const float*, const float*, const T*, long, T*, long, float*,    \
+                                float*, float*, cudaStream_t);                                   \
+  template int launch_attn_fwd<T>(int, int, int, int, const T*, T*, float*, cudaStream_t);      \
+  template int launch_attn_bwd<T>(int, int, int, int, const T*, const T*, const T*,             \
+                                  const float*, T*, cudaStream_t);                               \
+  template int launch_patchify<T>(int, int, int, int, const T*, T*, cudaStream_t);              \
+  template int launch_embed<T>(int, int, int, const T*, const float*, const float*, T*,          \
+                               cudaStream_t);                                                    \
+  template int launch_embed_bwd<T>(int, int, int, const T*, T*, float*, float*, cudaStream_t);  \
+  template int launch_scatter_cls<T>(int, int, int, const T*, T*, cudaStream_t);
+INST(float)
+INST(__nv_bfloat16)
+#undef INST
+
+}  // namespace ppll

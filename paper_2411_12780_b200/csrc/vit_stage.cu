@@ -1,0 +1,341 @@
+// Native executor of one ViT local-learning stage (the PPLL local step,
+// blocks.py:266-289 semantics, applied to pre-LN transformer blocks):
+//
+//   [patchify → patch GEMM → +cls/+pos]            (stage 0 only)
+//   block layers   : LN1 → QKV GEMM → MHSA → proj GEMM(+res) → LN2 →
+//                    FC1 GEMM(+GELU, pre-act kept) → FC2 GEMM(+res)
+//                    (the last block layer's FC2 epilogue dual-stores x_out,
+//                     i.e. the push, with PRE-update parameters)
+//   aux layers     : same layer type, N_l = aux_depth(l, d', n) of them
+//   head           : LN on the cls rows → classifier GEMM → softmax-CE
+//   backward       : reverse of the above; no gradient into the detached
+//                    stage input (the first LN1 backward only produces its
+//                    gamma/beta gradients)
+//   update         : one Nesterov launch over the flat parameter buffer.
+//
+// Every tensor is [rows, features] row-major with rows = batch·tokens; the
+// per-layer activations needed by the backward are kept in a workspace sized
+// once for max_batch.
+#include <vector>
+#include "common.cuh"
+#include "kernels.cuh"
+#include "vit.cuh"
+
+namespace {
+enum { kLn1g, kLn1b, kWqkv, kBqkv, kWo, kBo, kLn2g, kLn2b, kW1, kB1, kW2, kB2, kLayerParams };
+struct LayerBufs {
+  char *xn1, *qkv, *o, *x1, *xn2, *u, *h, *x2;
+  float *mean1, *rstd1, *mean2, *rstd2, *lse;
+};
+}  // namespace
+
+struct ppll_vit_stage {
+  int Bmax, T, D, H, F, C, n_block, n_aux, has_patch, img_c, img_hw, patch;
+  int dtype;
+  size_t esz;
+  std::vector<int64_t> off;          // [patch 4][12 per layer][head 4]
+  int64_t n_params;
+  float *theta, *grad, *mom;
+  void* theta_lp;
+  const float* lr_table;
+  int* step;
+  int max_step;
+  float* loss_hist;
+  int* err;
+  float mu, wd;
+  std::vector<LayerBufs> L;
+  char *patches = nullptr, *tok = nullptr, *x0 = nullptr;
+  char *zc = nullptr, *logits = nullptr, *dlog = nullptr, *dz = nullptr, *dzc = nullptr;
+  float *meanf = nullptr, *rstdf = nullptr;
+  char *dxa = nullptr, *dxb = nullptr, *dxc = nullptr, *dbig = nullptr, *dxn = nullptr,
+       *dqkv = nullptr, *dO = nullptr, *dtok = nullptr;
+  float* ln_part = nullptr;
+  float* ws = nullptr;
+  size_t ws_elems = 0;
+  std::vector<void*> allocs;
+
+  int layers() const { return n_block + n_aux; }
+  int64_t po(int layer, int k) const { return off[4 + layer * kLayerParams + k]; }
+  int64_t ho(int k) const { return off[4 + layers() * kLayerParams + k]; }
+  const void* W(int64_t o) const {
+    return dtype == PPLL_F32 ? (const void*)(theta + o)
+                             : (const void*)(reinterpret_cast<const __nv_bfloat16*>(theta_lp) + o);
+  }
+  const float* P(int64_t o) const { return theta + o; }
+  float* G(int64_t o) const { return grad + o; }
+  char* alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, (bytes + 255) / 256 * 256) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return reinterpret_cast<char*>(p);
+  }
+};
+
+using namespace ppll;
+
+template <typename TT>
+static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out, bool head,
+                       cudaStream_t s) {
+  const int T = st->T, D = st->D, F = st->F, H = st->H;
+  const int M = B * T;
+  const TT* xcur = reinterpret_cast<const TT*>(x_in);
+  int r;
+  if (st->has_patch) {
+    const int P = T - 1, pd = st->img_c * st->patch * st->patch;
+    r = launch_patchify<TT>(B, st->img_c, st->img_hw, st->patch, (const TT*)x_in, (TT*)st->patches, s);
+    if (r) return r;
+    LinOpts o;
+    o.bias = st->P(st->off[1]);
+    r = gemm_fwd(B * P, pd, D, st->patches, pd, st->W(st->off[0]), o, st->tok, D, st->dtype, st->ws,
+                 st->ws_elems, s);
+    if (r) return r;
+    r = launch_embed<TT>(B, P, D, (const TT*)st->tok, st->P(st->off[2]), st->P(st->off[3]),
+                         (TT*)st->x0, s);
+    if (r) return r;
+    xcur = (const TT*)st->x0;
+  }
+  for (int l = 0; l < st->layers(); ++l) {
+    LayerBufs& b = st->L[l];
+    r = launch_ln_fwd<TT>(M, D, xcur, D, st->P(st->po(l, kLn1g)), st->P(st->po(l, kLn1b)),
+                          (TT*)b.xn1, D, b.mean1, b.rstd1, s);
+    if (r) return r;
+    LinOpts o1;
+    o1.bias = st->P(st->po(l, kBqkv));
+    r = gemm_fwd(M, D, 3 * D, b.xn1, D, st->W(st->po(l, kWqkv)), o1, b.qkv, 3 * D, st->dtype,
+                 st->ws, st->ws_elems, s);
+    if (r) return r;
+    r = launch_attn_fwd<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
+    if (r) return r;
+    LinOpts o2;
+    o2.bias = st->P(st->po(l, kBo));
+    o2.res = xcur;
+    o2.ldres = D;
+    r = gemm_fwd(M, D, D, b.o, D, st->W(st->po(l, kWo)), o2, b.x1, D, st->dtype, st->ws,
+                 st->ws_elems, s);
+    if (r) return r;
+    r = launch_ln_fwd<TT>(M, D, (const TT*)b.x1, D, st->P(st->po(l, kLn2g)),
+                          st->P(st->po(l, kLn2b)), (TT*)b.xn2, D, b.mean2, b.rstd2, s);
+    if (r) return r;
+    LinOpts o3;
+    o3.bias = st->P(st->po(l, kB1));
+    o3.act = kActGelu;
+    o3.pre = b.u;
+    o3.ldpre = F;
+    r = gemm_fwd(M, D, F, b.xn2, D, st->W(st->po(l, kW1)), o3, b.h, F, st->dtype, st->ws,
+                 st->ws_elems, s);
+    if (r) return r;
+    LinOpts o4;
+    o4.bias = st->P(st->po(l, kB2));
+    o4.res = b.x1;
+    o4.ldres = D;
+    if (l == st->n_block - 1 && x_out) {   // fused push of the block output
+      o4.C2 = x_out;
+      o4.ldc2 = D;
+    }
+    r = gemm_fwd(M, F, D, b.h, F, st->W(st->po(l, kW2)), o4, b.x2, D, st->dtype, st->ws,
+                 st->ws_elems, s);
+    if (r) return r;
+    xcur = (const TT*)b.x2;
+  }
+  if (!head) return PPLL_OK;
+  // head: LayerNorm on the cls rows (row stride T·D) + classifier
+  r = launch_ln_fwd<TT>(B, D, xcur, (long)T * D, st->P(st->ho(0)), st->P(st->ho(1)), (TT*)st->zc,
+                        D, st->meanf, st->rstdf, s);
+  if (r) return r;
+  LinOpts oh;
+  oh.bias = st->P(st->ho(3));
+  return gemm_fwd(B, D, st->C, st->zc, D, st->W(st->ho(2)), oh, st->logits, st->C, st->dtype,
+                  st->ws, st->ws_elems, s);
+}
+
+template <typename TT>
+static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
+                    void* x_out, cudaStream_t s) {
+  const int T = st->T, D = st->D, F = st->F, H = st->H, C = st->C;
+  const int M = B * T;
+  int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
+  if (r) return r;
+  r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
+                              st->loss_hist, st->step, st->err, s);
+  if (r) return r;
+  const TT* xlast = (const TT*)st->L[st->layers() - 1].x2;
+  // ---- head backward ----
+  r = linear_wgrad(B, D, C, st->zc, D, st->dlog, C, st->G(st->ho(2)), st->G(st->ho(3)), st->dtype,
+                   st->ws, st->ws_elems, s);
+  if (r) return r;
+  LinOpts none;
+  r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
+                 st->ws_elems, s);
+  if (r) return r;
+  r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, (long)T * D, st->meanf, st->rstdf,
+                        st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, st->ln_part,
+                        st->G(st->ho(0)), st->G(st->ho(1)), s);
+  if (r) return r;
+  r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)st->dxa, s);
+  if (r) return r;
+  // ---- layers, last first ----
+  char* dx2 = st->dxa;   // gradient w.r.t. the current layer's output
+  char* dx1 = st->dxb;
+  char* dxn_out = st->dxc;
+  for (int l = st->layers() - 1; l >= 0; --l) {
+    LayerBufs& b = st->L[l];
+    const void* xin_l = l > 0 ? (const void*)st->L[l - 1].x2
+                              : (st->has_patch ? (const void*)st->x0 : x_in);
+    r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), st->G(st->po(l, kB2)),
+                     st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+    LinOpts og;
+    og.mask = b.u;
+    og.ldmask = F;
+    og.mask_mode = kMaskGeluGrad;
+    r = gemm_dgrad(M, F, D, dx2, D, st->W(st->po(l, kW2)), og, st->dbig, F, st->dtype, st->ws,
+                   st->ws_elems, s);
+    if (r) return r;
+    r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
+                     st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+    r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
+                   st->ws, st->ws_elems, s);
+    if (r) return r;
+    r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
+                          st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, st->ln_part,
+                          st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s);
+    if (r) return r;
+    r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), st->G(st->po(l, kBo)),
+                     st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+    r = gemm_dgrad(M, D, D, dx1, D, st->W(st->po(l, kWo)), none, st->dO, D, st->dtype, st->ws,
+                   st->ws_elems, s);
+    if (r) return r;
+    r = launch_attn_bwd<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
+                            b.lse, (TT*)st->dqkv, s);
+    if (r) return r;
+    r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)),
+                     st->G(st->po(l, kBqkv)), st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+    r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
+                   st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+    // no gradient into the detached stage input (blocks.py:277-278)
+    const bool need_dx = l > 0 || st->has_patch;
+    r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
+                          st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
+                          need_dx ? (TT*)dxn_out : nullptr, D, st->ln_part,
+                          st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s);
+    if (r) return r;
+    char* t = dx2;
+    dx2 = dxn_out;
+    dxn_out = t;
+  }
+  if (st->has_patch) {
+    const int P = T - 1, pd = st->img_c * st->patch * st->patch;
+    r = launch_embed_bwd<TT>(B, P, D, (const TT*)dx2, (TT*)st->dtok, st->G(st->off[2]),
+                             st->G(st->off[3]), s);
+    if (r) return r;
+    r = linear_wgrad(B * P, pd, D, st->patches, pd, st->dtok, D, st->G(st->off[0]),
+                     st->G(st->off[1]), st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+  }
+  return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
+                         reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
+                         st->max_step, 0.f, st->mu, st->wd, st->err, s);
+}
+
+extern "C" {
+
+ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, int64_t n_params,
+                                      int dtype, float* theta, float* grad, float* mom,
+                                      void* theta_lp, const float* lr_table, int* step,
+                                      int max_step, float* loss_hist, int* err, float mu, float wd) {
+  ppll_vit_stage* st = new ppll_vit_stage();
+  st->Bmax = cfg[0]; st->T = cfg[1]; st->D = cfg[2]; st->H = cfg[3]; st->F = cfg[4];
+  st->C = cfg[5]; st->n_block = cfg[6]; st->n_aux = cfg[7]; st->has_patch = cfg[8];
+  st->img_c = cfg[9]; st->img_hw = cfg[10]; st->patch = cfg[11];
+  if (st->Bmax < 1 || st->T < 1 || st->D % 32 || st->D % st->H || st->D / st->H != 64 ||
+      st->n_block < 1 || (dtype != PPLL_F32 && dtype != PPLL_BF16) ||
+      (dtype == PPLL_BF16 && !theta_lp)) {
+    set_error("ppll_vit_stage_create: unsupported configuration (D=%d H=%d)", st->D, st->H);
+    delete st;
+    return nullptr;
+  }
+  st->dtype = dtype;
+  st->esz = dtype == PPLL_F32 ? 4 : 2;
+  st->off.assign(offsets, offsets + 4 + (st->n_block + st->n_aux) * kLayerParams + 4);
+  st->n_params = n_params;
+  st->theta = theta; st->grad = grad; st->mom = mom; st->theta_lp = theta_lp;
+  st->lr_table = lr_table; st->step = step; st->max_step = max_step;
+  st->loss_hist = loss_hist; st->err = err; st->mu = mu; st->wd = wd;
+  const size_t M = (size_t)st->Bmax * st->T, D = st->D, F = st->F, e = st->esz;
+  bool ok = true;
+  auto A = [&](size_t bytes) { char* p = st->alloc(bytes); ok = ok && p; return p; };
+  for (int l = 0; l < st->layers(); ++l) {
+    LayerBufs b;
+    b.xn1 = A(M * D * e); b.qkv = A(M * 3 * D * e); b.o = A(M * D * e); b.x1 = A(M * D * e);
+    b.xn2 = A(M * D * e); b.u = A(M * F * e); b.h = A(M * F * e); b.x2 = A(M * D * e);
+    b.mean1 = (float*)A(M * 4); b.rstd1 = (float*)A(M * 4);
+    b.mean2 = (float*)A(M * 4); b.rstd2 = (float*)A(M * 4);
+    b.lse = (float*)A((size_t)st->Bmax * st->H * st->T * 4);
+    st->L.push_back(b);
+  }
+  if (st->has_patch) {
+    const size_t P = st->T - 1, pd = (size_t)st->img_c * st->patch * st->patch;
+    st->patches = A(st->Bmax * P * pd * e);
+    st->tok = A(st->Bmax * P * D * e);
+    st->x0 = A(M * D * e);
+    st->dtok = A(st->Bmax * P * D * e);
+  }
+  st->zc = A(st->Bmax * D * e);
+  st->logits = A((size_t)st->Bmax * st->C * e);
+  st->dlog = A((size_t)st->Bmax * st->C * e);
+  st->dz = A(st->Bmax * D * e);
+  st->dzc = A(st->Bmax * D * e);
+  st->meanf = (float*)A(st->Bmax * 4);
+  st->rstdf = (float*)A(st->Bmax * 4);
+  st->dxa = A(M * D * e); st->dxb = A(M * D * e); st->dxc = A(M * D * e);
+  st->dbig = A(M * F * e); st->dxn = A(M * D * e); st->dqkv = A(M * 3 * D * e);
+  st->dO = A(M * D * e);
+  st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 2 * D * 4);
+  // split-K workspace: 16 partial copies of the largest weight gradient
+  st->ws_elems = 16 * (size_t)D * (F > 3 * D ? F : 3 * D);
+  st->ws = (float*)A(st->ws_elems * 4);
+  if (!ok) {
+    set_error("ppll_vit_stage_create: out of device memory");
+    ppll_vit_stage_destroy(st);
+    return nullptr;
+  }
+  return st;
+}
+
+void ppll_vit_stage_destroy(ppll_vit_stage* st) {
+  if (!st) return;
+  for (void* p : st->allocs) cudaFree(p);
+  delete st;
+}
+
+int ppll_vit_stage_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
+                        void* x_out, void* stream) {
+  if (!st || B < 1 || B > st->Bmax || !x_in || !labels) {
+    set_error("ppll_vit_stage_step: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (st->dtype == PPLL_F32) return vit_step<float>(st, B, x_in, labels, x_out, s);
+  return vit_step<__nv_bfloat16>(st, B, x_in, labels, x_out, s);
+}
+
+int ppll_vit_stage_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_out,
+                           void* logits, void* stream) {
+  if (!st || B < 1 || B > st->Bmax) {
+    set_error("ppll_vit_stage_forward: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int r = st->dtype == PPLL_F32 ? vit_forward<float>(st, B, x_in, h_out, logits != nullptr, s)
+                                : vit_forward<__nv_bfloat16>(st, B, x_in, h_out, logits != nullptr, s);
+  if (r || !logits) return r;
+  PPLL_CUDA_CHECK(cudaMemcpyAsync(logits, st->logits, (size_t)B * st->C * st->esz,
+                                  cudaMemcpyDeviceToDevice, s));
+  return PPLL_OK;
+}
+
+}  // extern "C"

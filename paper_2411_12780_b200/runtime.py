@@ -207,7 +207,7 @@ def _validate_modules(modules: Sequence[LocalModule]) -> None:
     for j, m in enumerate(modules):
         if m.stage_index != j:
             raise ConfigMismatch(f"module {j} carries stage_index {m.stage_index}")
-        if j > 0 and m.input_width != modules[j - 1].output_width:
+        if j > 0 and m.in_features != modules[j - 1].out_features:
             raise ConfigMismatch(
                 f"stage {j} input width {m.input_width} != stage {j - 1} "
                 f"output width {modules[j - 1].output_width}")
@@ -254,14 +254,14 @@ class _Rings:
         self.M = capacity
         self.x, self.y = [], []
         for m in modules:
-            self.x.append(torch.empty((capacity, max_batch, m.input_width), dtype=m.act_dtype,
+            self.x.append(torch.empty((capacity, max_batch, m.in_features), dtype=m.act_dtype,
                                       device=m.device))
             self.y.append(torch.zeros((capacity, max_batch), dtype=torch.int64, device=m.device))
         m0 = modules[0]
-        self.x_pin = torch.empty((capacity, max_batch, m0.input_width), dtype=torch.float32,
+        self.x_pin = torch.empty((capacity, max_batch, m0.in_features), dtype=torch.float32,
                                  pin_memory=True)
         self.y_pin = torch.empty((capacity, max_batch), dtype=torch.int64, pin_memory=True)
-        self.x_stage = (torch.empty((capacity, max_batch, m0.input_width), dtype=torch.float32,
+        self.x_stage = (torch.empty((capacity, max_batch, m0.in_features), dtype=torch.float32,
                                     device=m0.device) if m0.act_dtype != torch.float32 else None)
 
 
@@ -318,8 +318,7 @@ class DevicePipeline:
         x_out = None if last else r.x[j + 1][slot]
         if not last:
             r.y[j + 1][slot][:B].copy_(y[:B], non_blocking=True)
-        N.check(N.load().ppll_stage_step(m.native(B), B, x_in.data_ptr(), y.data_ptr(),
-                                         N.ptr(x_out), stream.cuda_stream), f"stage {j} step")
+        m.launch_step(B, x_in.data_ptr(), y.data_ptr(), N.ptr(x_out), stream.cuda_stream)
 
     def _step(self, j: int, slot: int, B: int):
         stream = self.streams[j]
@@ -368,9 +367,11 @@ class DevicePipeline:
             slot = batch_id % M
             # ---- source: host -> ring 0 (runtime.py:312-323) ----
             xt = torch.as_tensor(x)
-            if xt.dim() != 2 or xt.shape[1] != mods[0].input_width:
+            if xt.dim() >= 2 and xt[0].numel() == mods[0].in_features:
+                xt = xt.reshape(B, mods[0].in_features)
+            else:
                 raise WorkerPanic(0, f"DimensionMismatch: stage 0 expects width "
-                                     f"{mods[0].input_width}, got {tuple(xt.shape)}")
+                                     f"{mods[0].in_shape}, got {tuple(xt.shape)}")
             yt = torch.as_tensor(np.asarray(y)) if not torch.is_tensor(y) else y
             if yt.dtype.is_floating_point or tuple(yt.shape) != (B,):
                 raise WorkerPanic(0, "labels must be integers matching the batch")
@@ -396,7 +397,7 @@ class DevicePipeline:
                     if not resident:
                         r.x_stage[slot, :B].copy_(x_src, non_blocking=True)
                         x_src = r.x_stage[slot, :B]
-                    N.check(N.load().ppll_cast(B * mods[0].input_width, x_src.data_ptr(),
+                    N.check(N.load().ppll_cast(B * mods[0].in_features, x_src.data_ptr(),
                                                N.F32, r.x[0][slot].data_ptr(), N.BF16,
                                                src.cuda_stream), "cast")
                 r.y[0][slot, :B].copy_(y_src, non_blocking=True)
@@ -502,6 +503,7 @@ def _run_ppll_roundrobin(modules, dataset_iter, config) -> EpochMetrics:
                 break
             xt = torch.as_tensor(np.asarray(x, dtype=np.float32) if not torch.is_tensor(x) else x)
             B = int(xt.shape[0])
+            xt = xt.reshape(B, -1)
             pipe._ensure(B)
             r = pipe.rings
             slot = next_id % M
@@ -511,7 +513,7 @@ def _run_ppll_roundrobin(modules, dataset_iter, config) -> EpochMetrics:
                 if r.x_stage is None:
                     r.x[0][slot, :B].copy_(xd)
                 else:
-                    N.check(lib.ppll_cast(B * modules[0].input_width, xd.data_ptr(), N.F32,
+                    N.check(lib.ppll_cast(B * modules[0].in_features, xd.data_ptr(), N.F32,
                                           r.x[0][slot].data_ptr(), N.BF16, stream.cuda_stream),
                             "cast")
                 r.y[0][slot, :B].copy_(torch.as_tensor(np.asarray(y)).to(torch.int64))
