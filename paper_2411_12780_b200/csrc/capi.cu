@@ -105,7 +105,7 @@ int linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, in
   if (dtype == PPLL_F32) {
     r = launch_gemm_simt<float, float>(K, N, M, (const float*)X, 1, ldx, (const float*)dY, lddy, 1,
                                        ep, ws, ws_elems, s);
-    if (r == PPLL_OK && db) r = launch_colsum<float>(M, N, (const float*)dY, lddy, db, s);
+    if (r == PPLL_OK && db) r = launch_colsum<float>(M, N, (const float*)dY, lddy, db, s, ws, ws_elems);
     return r;
   }
   r = PPLL_ERR_UNSUPPORTED;
@@ -117,7 +117,7 @@ int linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, in
   if (r == PPLL_ERR_UNSUPPORTED)
     r = launch_gemm_simt<bf16, float>(K, N, M, (const bf16*)X, 1, ldx, (const bf16*)dY, lddy, 1, ep,
                                       ws, ws_elems, s);
-  if (r == PPLL_OK && db) r = launch_colsum<bf16>(M, N, (const bf16*)dY, lddy, db, s);
+  if (r == PPLL_OK && db) r = launch_colsum<bf16>(M, N, (const bf16*)dY, lddy, db, s, ws, ws_elems);
   return r;
 }
 

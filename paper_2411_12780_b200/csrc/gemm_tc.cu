@@ -342,27 +342,38 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15) || (lda * 2) % 16 || (ldb * 2) % 16)
     return PPLL_ERR_UNSUPPORTED;
   const int mt = ceil_div(M, BM);
-  // tile width: minimise (waves x per-tile cost), per-tile cost ~ BN + 32
-  int bn = 64;
-  long best = -1;
+  // Pick (tile width, K splits) with a small cost model (seconds):
+  //   MMA    : waves x 128·BN·K/splits MACs at the per-SM tcgen05 rate
+  //   epilog : 128·BN·bytes per item at ~150 GB/s per SM (one exposed, the
+  //            rest overlap the next item's MMAs through the TMEM double buffer)
+  //   split-K: partial write + read + reduce launch
+  const double mac_rate = 1.5e15 / 2 / kNumSMs;          // MAC/s per SM (bf16, sustained)
+  const double out_b = (double)sizeof(TO);
+  int bn = 64, splits = 1;
+  double best = -1;
   const int cands[4] = {256, 192, 128, 64};
   for (int i = 0; i < 4; ++i) {
     const int c = cands[i];
     const long tiles = (long)mt * ceil_div(N, c);
-    const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (c + 32);
-    if (best < 0 || cost < best) { best = cost; bn = c; }
+    int sp = 1;
+    if (ws && tiles * 2 <= kNumSMs && K >= 8 * BK) {
+      sp = (int)(kNumSMs / tiles);
+      if (sp > K / (4 * BK)) sp = K / (4 * BK);
+      while (sp > 1 && (size_t)sp * M * N > ws_elems) --sp;
+      if (sp < 1) sp = 1;
+    }
+    const long items = tiles * sp;
+    const double waves = (double)((items + kNumSMs - 1) / kNumSMs);
+    const double t_mma = 128.0 * c * (double)ceil_div(K, sp) / mac_rate;
+    const double t_epi = 128.0 * c * (sp > 1 ? 4.0 : out_b) / 150e9;
+    double cost = waves * (t_mma > t_epi ? t_mma : t_epi) + t_epi;
+    if (sp > 1) cost += (double)(sp + 1) * M * N * 4 / 5e12 + 2e-6;
+    if (best < 0 || cost < best) { best = cost; bn = c; splits = sp; }
   }
   Sched sc;
   sc.mt = mt;
   sc.nt = ceil_div(N, bn);
   sc.tiles = sc.mt * sc.nt;
-  int splits = 1;
-  if (ws && sc.tiles * 2 <= kNumSMs && K >= 8 * BK) {
-    splits = kNumSMs / sc.tiles;
-    if (splits > K / (4 * BK)) splits = K / (4 * BK);
-    while (splits > 1 && (size_t)splits * M * N > ws_elems) --splits;
-    if (splits < 1) splits = 1;
-  }
   sc.kps = ceil_div(ceil_div(K, splits), BK) * BK;
   sc.splits = ceil_div(K, sc.kps);
   sc.items = sc.tiles * sc.splits;

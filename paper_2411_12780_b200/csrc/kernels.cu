@@ -225,32 +225,55 @@ template int launch_gemm_simt<__nv_bfloat16, float>(int, int, int, const __nv_bf
 // ------------------------------------------------------------------------
 // bias gradient: db[n] = Σ_m G[m*ld + n]   (fixed summation order)
 // ------------------------------------------------------------------------
+// Pass 1: block (32 cols x 8 row lanes) sums rows [chunk*rpc, (chunk+1)*rpc)
+// of 32 columns; the 8 lanes combine in a fixed order -> out[chunk][n].
+// Pass 2 (only when several chunks): out[n] = Σ_chunk part[chunk][n] in order.
 template <typename T>
-__global__ void colsum_kernel(int M, int N, const T* __restrict__ G, int ld, float* __restrict__ db) {
+__global__ void colsum_kernel(int M, int N, const T* __restrict__ G, long ld, int rpc,
+                              float* __restrict__ out) {
   __shared__ float red[8][33];
-  int n = blockIdx.x * 32 + threadIdx.x;
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * rpc, r1 = min(M, r0 + rpc);
   float s = 0.f;
-  if (n < N)
-    for (int m = threadIdx.y; m < M; m += 8) s += to_f(G[(long)m * ld + n]);
+  if (n < N) {
+#pragma unroll 4
+    for (int m = r0 + threadIdx.y; m < r1; m += 8) s += to_f(G[(long)m * ld + n]);
+  }
   red[threadIdx.y][threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.y == 0 && n < N) {
     float t = 0.f;
 #pragma unroll
     for (int r = 0; r < 8; ++r) t += red[r][threadIdx.x];
-    db[n] = t;
+    out[(long)blockIdx.y * N + n] = t;
   }
 }
 
 template <typename T>
-int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s) {
-  colsum_kernel<T><<<ceil_div(N, 32), dim3(32, 8), 0, s>>>(M, N, G, ld, db);
-  note_launch();
+int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s, float* ws,
+                  size_t ws_elems) {
+  int chunks = 1;
+  if (ws && M > 512) {
+    chunks = min(ceil_div(M, 64), 256);
+    while (chunks > 1 && (size_t)chunks * N > ws_elems) chunks /= 2;
+  }
+  const int rpc = ceil_div(M, chunks);
+  chunks = ceil_div(M, rpc);
+  if (chunks <= 1) {
+    colsum_kernel<T><<<dim3(ceil_div(N, 32), 1), dim3(32, 8), 0, s>>>(M, N, G, ld, M, db);
+    note_launch();
+  } else {
+    colsum_kernel<T><<<dim3(ceil_div(N, 32), chunks), dim3(32, 8), 0, s>>>(M, N, G, ld, rpc, ws);
+    note_launch();
+    colsum_kernel<float><<<dim3(ceil_div(N, 32), 1), dim3(32, 8), 0, s>>>(chunks, N, ws, N,
+                                                                           chunks, db);
+    note_launch();
+  }
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
-template int launch_colsum<float>(int, int, const float*, int, float*, cudaStream_t);
-template int launch_colsum<__nv_bfloat16>(int, int, const __nv_bfloat16*, int, float*, cudaStream_t);
+template int launch_colsum<float>(int, int, const float*, int, float*, cudaStream_t, float*, size_t);
+template int launch_colsum<__nv_bfloat16>(int, int, const __nv_bfloat16*, int, float*, cudaStream_t, float*, size_t);
 
 // ------------------------------------------------------------------------
 // softmax cross-entropy, fused forward + adjoint (tensor.py:201-234).

@@ -192,7 +192,8 @@ int launch_splitk_reduce(int M, int N, int splits, const float* ws, const Epilog
                          cudaStream_t s);
 
 template <typename T>
-int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s);
+int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s, float* ws = nullptr,
+                  size_t ws_elems = 0);
 
 template <typename T>
 int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* dz, int lddz,

@@ -128,17 +128,25 @@ ln_bwd_kernel(int M, int D, const T* __restrict__ dy, long lddy, const T* __rest
   }
 }
 
+// part is [nblk][2D]; block (32 cols x 8 lanes), fixed-order combination
 __global__ void ln_param_reduce_kernel(int nblk, int D, const float* __restrict__ part,
                                        float* __restrict__ dg, float* __restrict__ db) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= D) return;
-  float a = 0.f, b = 0.f;
-  for (int k = 0; k < nblk; ++k) {
-    a += part[((long)k * 2 + 0) * D + c];
-    b += part[((long)k * 2 + 1) * D + c];
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;   // column of the [nblk, 2D] matrix
+  float s = 0.f;
+  if (c < 2 * D) {
+#pragma unroll 4
+    for (int k = threadIdx.y; k < nblk; k += 8) s += part[(long)k * 2 * D + c];
   }
-  dg[c] = a;
-  db[c] = b;
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < 2 * D) {
+    float t = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) t += red[r][threadIdx.x];
+    if (c < D) dg[c] = t;
+    else db[c - D] = t;
+  }
 }
 
 template <typename T>
@@ -175,7 +183,7 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
   note_launch();
   PPLL_LAUNCH_CHECK();
   if (part && dg) {
-    ln_param_reduce_kernel<<<ceil_div(D, 128), 128, 0, s>>>(nblk, D, part, dg, db);
+    ln_param_reduce_kernel<<<ceil_div(2 * D, 32), dim3(32, 8), 0, s>>>(nblk, D, part, dg, db);
     note_launch();
     PPLL_LAUNCH_CHECK();
   }
