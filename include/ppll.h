@@ -52,6 +52,8 @@ const char* ppll_last_error(void);
 /* number of kernels this library launched since load (process-wide counter) */
 uint64_t ppll_launch_count(void);
 void ppll_set_gemm_engine(int engine);
+/* ViT attention engine: 0 = tcgen05 when supported (bf16, T <= 128), 1 = SIMT */
+void ppll_set_attn_engine(int engine);
 
 /* ---- primitive ops: tensor.py ------------------------------------------ */
 

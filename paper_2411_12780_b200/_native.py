@@ -26,6 +26,7 @@ SIGNATURES = {
     "ppll_last_error": (C.c_char_p, []),
     "ppll_launch_count": (_u64, []),
     "ppll_set_gemm_engine": (None, [_i]),
+    "ppll_set_attn_engine": (None, [_i]),
     "ppll_linear_fwd": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _vp]),
     "ppll_linear_dgrad": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _i, _i, _vp]),
     "ppll_linear_wgrad": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _i, _vp]),

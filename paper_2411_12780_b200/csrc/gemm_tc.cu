@@ -364,7 +364,11 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
     }
     const long items = tiles * sp;
     const double waves = (double)((items + kNumSMs - 1) / kNumSMs);
-    const double t_mma = 128.0 * c * (double)ceil_div(K, sp) / mac_rate;
+    // per K=16 step: max(tensor floor 128·N/256 cycles, smem operand read (A 4 KB + B N·32 B) at
+    // 128 B/cycle) — narrow tiles are bound by re-reading A from shared memory
+    const double cyc16 = fmax(c / 2.0, (4096.0 + 32.0 * c) / 128.0);
+    const double t_mma = (double)ceil_div(K, 16 * sp) * cyc16 / 1.9e9;
+    (void)mac_rate;
     const double t_epi = 128.0 * c * (sp > 1 ? 4.0 : out_b) / 150e9;
     double cost = waves * (t_mma > t_epi ? t_mma : t_epi) + t_epi;
     if (sp > 1) cost += (double)(sp + 1) * M * N * 4 / 5e12 + 2e-6;

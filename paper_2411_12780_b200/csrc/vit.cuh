@@ -20,6 +20,15 @@ int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse
 template <typename T>
 int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, const T* dout,
                     const float* lse, T* dqkv, cudaStream_t s);
+// tcgen05 attention (attn_tc.cu): bf16, head_dim 64, T <= 128
+bool attn_tc_supported(int Tn, int dh);
+int launch_attn_tc_fwd(int B, int Tn, int H, const __nv_bfloat16* qkv, __nv_bfloat16* o,
+                       float* lse, cudaStream_t s);
+int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __nv_bfloat16* o,
+                       const __nv_bfloat16* dout, const float* lse, __nv_bfloat16* dqkv,
+                       cudaStream_t s);
+extern int g_attn_engine;   // 0 auto (tcgen05 when supported), 1 SIMT
+
 template <typename T>
 int launch_patchify(int B, int C, int HW, int p, const T* img, T* out, cudaStream_t s);
 template <typename T>

@@ -16,6 +16,7 @@
 // Every tensor is [rows, features] row-major with rows = batch·tokens; the
 // per-layer activations needed by the backward are kept in a workspace sized
 // once for max_batch.
+#include <type_traits>
 #include <vector>
 #include "common.cuh"
 #include "kernels.cuh"
@@ -73,6 +74,26 @@ struct ppll_vit_stage {
 
 using namespace ppll;
 
+// attention engine: tcgen05 for bf16 with T <= 128, SIMT kernels otherwise
+template <typename TT>
+static int attn_fwd_any(int B, int T, int H, int dh, const TT* qkv, TT* o, float* lse,
+                        cudaStream_t s) {
+  if constexpr (std::is_same<TT, __nv_bfloat16>::value) {
+    if (g_attn_engine == 0 && attn_tc_supported(T, dh))
+      return launch_attn_tc_fwd(B, T, H, qkv, o, lse, s);
+  }
+  return launch_attn_fwd<TT>(B, T, H, dh, qkv, o, lse, s);
+}
+template <typename TT>
+static int attn_bwd_any(int B, int T, int H, int dh, const TT* qkv, const TT* o, const TT* dout,
+                        const float* lse, TT* dqkv, cudaStream_t s) {
+  if constexpr (std::is_same<TT, __nv_bfloat16>::value) {
+    if (g_attn_engine == 0 && attn_tc_supported(T, dh))
+      return launch_attn_tc_bwd(B, T, H, qkv, o, dout, lse, dqkv, s);
+  }
+  return launch_attn_bwd<TT>(B, T, H, dh, qkv, o, dout, lse, dqkv, s);
+}
+
 template <typename TT>
 static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out, bool head,
                        cudaStream_t s) {
@@ -104,7 +125,7 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     r = gemm_fwd(M, D, 3 * D, b.xn1, D, st->W(st->po(l, kWqkv)), o1, b.qkv, 3 * D, st->dtype,
                  st->ws, st->ws_elems, s);
     if (r) return r;
-    r = launch_attn_fwd<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
+    r = attn_fwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
     if (r) return r;
     LinOpts o2;
     o2.bias = st->P(st->po(l, kBo));
@@ -207,7 +228,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     r = gemm_dgrad(M, D, D, dx1, D, st->W(st->po(l, kWo)), none, st->dO, D, st->dtype, st->ws,
                    st->ws_elems, s);
     if (r) return r;
-    r = launch_attn_bwd<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
+    r = attn_bwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
                             b.lse, (TT*)st->dqkv, s);
     if (r) return r;
     r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)),

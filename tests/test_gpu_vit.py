@@ -107,3 +107,55 @@ def test_vit_pipeline_bitwise_equals_roundrobin(precision):
     for x, z in zip(a, b):
         assert np.array_equal(_flat(x), _flat(z))
     assert ma.batches_processed == [7, 7, 7]
+
+
+FULL = dict(image=32, channels=3, patch=4, dim=384, heads=6, mlp=1536, depth=2, classes=10)
+
+
+def test_tcgen05_attention_matches_simt_attention():
+    """The tcgen05 attention (bf16, T=65) against the SIMT attention kernels:
+    same stage, same data, engine switched through the C-ABI."""
+    from paper_2411_12780_b200 import _native as N
+    lib = N.load()
+    spec = lp.VitSpec(**FULL)
+    rng = np.random.default_rng(4)
+    img = rng.standard_normal((6, 3, 32, 32))
+    y = rng.integers(0, 10, 6)
+    outs = []
+    for engine in (0, 1):
+        lib.ppll_set_attn_engine(engine)
+        try:
+            hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=4, seed=9, precision="bf16")
+            mods = lp.build_vit_modules(spec, [1, 1], 1, 3, hyper)
+            losses, xs = [], []
+            h = lp.Tensor(img)
+            for m in mods:
+                loss, h = lp.local_loss_and_update(m, h, y)
+                losses.append(loss)
+                xs.append(h.data)
+            outs.append((losses, xs, [_flat(m) for m in mods]))
+        finally:
+            lib.ppll_set_attn_engine(0)
+    (l0, x0, p0), (l1, x1, p1) = outs
+    np.testing.assert_allclose(l0, l1, rtol=1e-2)
+    for a, b in zip(x0, x1):
+        assert np.abs(a - b).max() / np.abs(b).max() < 2e-2
+    for a, b in zip(p0, p1):
+        assert np.abs(a - b).max() / np.abs(b).max() < 2e-2
+
+
+def test_vit_s_geometry_bf16_vs_oracle():
+    spec, mods, stages = _pair(FULL, [1, 1], 1, 3, "bf16", 2)
+    rng = np.random.default_rng(2)
+    img = rng.standard_normal((4, 3, 32, 32))
+    y = rng.integers(0, 10, 4)
+    h, hr = lp.Tensor(img), img
+    for m, st in zip(mods, stages):
+        loss, h = lp.local_loss_and_update(m, h, y)
+        ref, hr, _ = vo.local_step(st, hr, y, 0.05, 0.001, 2, 0.9, 1e-4)
+        assert abs(loss - ref) <= 3e-2 * abs(ref)
+        assert np.abs(h.data - hr).max() / np.abs(hr).max() <= 5e-2
+        hr = h.data
+    for m, st in zip(mods, stages):
+        a, b = _flat(m), _flat_o(st)
+        assert np.abs(a - b).max() / np.abs(b).max() <= 5e-2
