@@ -4,7 +4,7 @@
 //   C[M,N] = Σ_k A(m,k)·B(k,n)   bf16 operands, fp32 accumulation in TMEM.
 //
 // Persistent kernel: one CTA per SM walks a static schedule of work items
-// (128 x BN output tiles, optionally split along K).  Warp roles (192 thr):
+// (128 x BN output tiles, optionally split along K).  Warp roles (320 thr):
 //   warp 0      TMA producer (one elected lane): A/B k-blocks of 64 into a
 //               kStages-deep shared-memory ring (mbarrier full/empty);
 //   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x
@@ -12,7 +12,8 @@
 //               frees the smem slot; accumulators are DOUBLE-BUFFERED in
 //               TMEM (2 x BN columns) so tile i+1's MMAs overlap tile i's
 //               epilogue;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (one accumulator row per
+//   warps 2..9  epilogue (two warps per TMEM lane quadrant, alternating
+//               32-column chunks): tcgen05.ld 32x32b.x32 (one accumulator row per
 //               thread) → fused bias / residual / pre-activation store /
 //               ReLU|GELU / ReLU-mask|GELU-gradient / dual store (the ring
 //               push), 32-column row segments moved as 16-B vectors; or fp32
@@ -32,7 +33,8 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kNumSMs = 148;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -145,7 +147,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -231,7 +233,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   } else {
     // ------------------------- epilogue -----------------------------
     // thread = one accumulator row; 32-column segments move as 16-B vectors
+    // two warps per TMEM lane quadrant, alternating 32-column chunks
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
+    const int half = (warp - 2) >> 2;
     int it = 0;
     for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
       const int tile = w % sc.tiles, z = w / sc.tiles;
@@ -241,7 +245,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = m0 + q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN && n0 + c < N; c += 32) {
+      for (int c = 32 * half; c < BN && n0 + c < N; c += 64) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
         float v[32];

@@ -165,7 +165,8 @@ int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const floa
   return PPLL_OK;
 }
 
-int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : 148 * 2; }
+// ~2 rows per warp: enough rows in flight to cover DRAM latency, few partials
+int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : min(ceil_div(M, 16), 148 * 4); }
 
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
