@@ -112,7 +112,7 @@ struct Smem {
   static constexpr int B_BYTES = BN * BK * 2;     // BN * 128 B
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
-  static constexpr int EPI = 0;
+  static constexpr int EPI = 2 * BN * 4;          // bias slice per accumulator buffer
   static constexpr int TOTAL = STAGES * STAGE + EPI + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
@@ -130,6 +130,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
+  float* bias_s = reinterpret_cast<float*>(smem + S * L::STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGE + L::EPI);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;      // [2]
@@ -241,22 +242,33 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const int tile = w % sc.tiles, z = w / sc.tiles;
       const int m0 = (tile % sc.mt) * BM, n0 = (tile / sc.mt) * BN;
       const int acc = it & 1;
+      const bool split = sc.splits > 1;
+      float* bs = bias_s + acc * BN;
+      if (!split && ep.bias) {
+        // stage this tile's bias slice in shared memory (epilogue warps only)
+        const int t = threadIdx.x - 64;
+        if (t < BN) bs[t] = (n0 + t < N) ? __ldg(ep.bias + n0 + t) : 0.f;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = m0 + q * 32 + lane;
+      const bool live = row < M;
 #pragma unroll 1
       for (int c = 32 * half; c < BN && n0 + c < N; c += 64) {
+        float ra[32], ka[32];
+        if (!split && live) ep.load_aux32(row, n0 + c, ra, ka);   // overlaps the TMEM load
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (row < M) {
-          if (sc.splits > 1)
+        if (live) {
+          if (split)
             st_row32<float>(part + ((long)z * M + row) * N + n0 + c, (N % 4) == 0,
                             min(32, N - n0 - c), v);
           else
-            ep.apply_row32(row, n0 + c, v);
+            ep.finish_row32(row, n0 + c, v, ra, ka, bs + c);
         }
       }
       // accumulator buffer drained: hand it back to the MMA warp

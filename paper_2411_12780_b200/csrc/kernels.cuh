@@ -125,6 +125,42 @@ struct Epilogue {
     DT<TO>::st(C + (long)m * ldc + n, v);
     if (C2) DT<TO>::st(C2 + (long)m * ldc2 + n, v);
   }
+  // Split form used by the tensor-core epilogue: issue the residual / mask row
+  // loads first (they overlap the TMEM load), then finish with the bias taken
+  // from a shared-memory copy of the tile's bias slice.
+  __device__ __forceinline__ void load_aux32(int m, int n0, float (&r)[32], float (&k)[32]) const {
+    const int valid = min(32, ncols - n0);
+    if (res) ld_row32<TO>(res + (long)m * ldres + n0, vec != 0, valid, r);
+    if (mask_mode != kMaskNone) ld_row32<TO>(mask + (long)m * ldmask + n0, vec != 0, valid, k);
+  }
+  __device__ __forceinline__ void finish_row32(int m, int n0, float (&v)[32], const float (&r)[32],
+                                               const float (&k)[32], const float* bias_s) const {
+    const int valid = min(32, ncols - n0);
+    const bool vv = vec != 0;
+    if (bias) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += bias_s[i];
+    }
+    if (res) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += r[i];
+    }
+    if (pre) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, v);
+    if (act != kActNone) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i]);
+    }
+    if (mask_mode == kMaskRelu) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
+    } else if (mask_mode == kMaskGeluGrad) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(k[i]);
+    }
+    st_row32<TO>(C + (long)m * ldc + n0, vv, valid, v);
+    if (C2) st_row32<TO>(C2 + (long)m * ldc2 + n0, vv, valid, v);
+  }
+
   // 32 consecutive columns n0..n0+31 of row m (n0 % 32 == 0)
   __device__ __forceinline__ void apply_row32(int m, int n0, float (&v)[32]) const {
     const int valid = min(32, ncols - n0);
