@@ -9,11 +9,14 @@ constexpr float kLnEps = 1e-5f;
 template <typename T>
 int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const float* b, T* y,
                   long ldy, float* mean, float* rstd, cudaStream_t s);
-// dx may be null (only gamma/beta gradients wanted); part/dg/db may be null
+// dx may be null (only gamma/beta gradients wanted); part/dg/db may be null;
+// dxsum (nullable) receives Σ_rows of the dx output — the bias gradient of the
+// layer that produced dy's residual stream, fused (needs D % 128 == 0).
+// part must hold ln_bwd_blocks(M) * 3 * D floats.
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
                   const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
-                  float* part, float* dg, float* db, cudaStream_t s);
+                  float* part, float* dg, float* db, cudaStream_t s, float* dxsum = nullptr);
 int ln_bwd_blocks(int M);
 template <typename T>
 int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse, cudaStream_t s);

@@ -12,6 +12,176 @@
 namespace ppll {
 
 // ---------------------------------------------------------------------------
+// 16-B vector row-segment helpers (N elements, 16-B aligned)
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void ldv(const __nv_bfloat16* p, float* o) {
+#pragma unroll
+  for (int i = 0; i < N / 8; ++i) {
+    const uint4 q = reinterpret_cast<const uint4*>(p)[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      o[8 * i + 2 * j] = f.x;
+      o[8 * i + 2 * j + 1] = f.y;
+    }
+  }
+}
+template <int N>
+__device__ __forceinline__ void ldv(const float* p, float* o) {
+#pragma unroll
+  for (int i = 0; i < N / 4; ++i) {
+    const float4 q = reinterpret_cast<const float4*>(p)[i];
+    o[4 * i] = q.x; o[4 * i + 1] = q.y; o[4 * i + 2] = q.z; o[4 * i + 3] = q.w;
+  }
+}
+template <int N>
+__device__ __forceinline__ void stv(__nv_bfloat16* p, const float* v) {
+#pragma unroll
+  for (int i = 0; i < N / 8; ++i) {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+    reinterpret_cast<uint4*>(p)[i] = q;
+  }
+}
+template <int N>
+__device__ __forceinline__ void stv(float* p, const float* v) {
+#pragma unroll
+  for (int i = 0; i < N / 4; ++i)
+    reinterpret_cast<float4*>(p)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+__device__ __forceinline__ float half_sum(float v) {   // reduce over the 16 lanes of a half-warp
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised LayerNorm (D = 16·EPL, EPL % 8 == 0): a half-warp per row, each
+// lane owns EPL contiguous features moved as 16-B vectors.
+// ---------------------------------------------------------------------------
+template <typename T, int EPL>
+__global__ void __launch_bounds__(256)
+ln_fwd_vkernel(int M, const T* __restrict__ x, long ldx, const float* __restrict__ g,
+               const float* __restrict__ b, T* __restrict__ y, long ldy, float* __restrict__ mean,
+               float* __restrict__ rstd) {
+  constexpr int D = 16 * EPL;
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + (lane >> 4);
+  const bool live = row < M;
+  const int c0 = hl * EPL;
+  float v[EPL];
+  if (live) ldv<EPL>(x + (long)row * ldx + c0, v);
+  else {
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) v[i] = 0.f;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) s += v[i];
+  const float mu = half_sum(s) * (1.f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) {
+    const float d = v[i] - mu;
+    q += d * d;
+  }
+  const float rs = rsqrtf(half_sum(q) * (1.f / D) + kLnEps);
+  if (!live) return;
+  float gg[EPL], bb[EPL];
+  ldv<EPL>(g + c0, gg);
+  ldv<EPL>(b + c0, bb);
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) v[i] = (v[i] - mu) * rs * gg[i] + bb[i];
+  stv<EPL>(y + (long)row * ldy + c0, v);
+  if (hl == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// backward; per-block column partials part[block][NS][D] with NS = 2 (dgamma,
+// dbeta) or 3 (+ Σ rows of the dx output: the next bias gradient, fused)
+template <typename T, int EPL, int NS>
+__global__ void __launch_bounds__(256)
+ln_bwd_vkernel(int M, const T* __restrict__ dy, long lddy, const T* __restrict__ x, long ldx,
+               const float* __restrict__ mean, const float* __restrict__ rstd,
+               const float* __restrict__ g, const T* __restrict__ dres, long ldres,
+               T* __restrict__ dx, long lddx, float* __restrict__ part, int rows_per_block) {
+  constexpr int D = 16 * EPL;
+  __shared__ float red[NS][D];
+  const int lane = threadIdx.x & 31, hl = lane & 15, w = threadIdx.x >> 5;
+  const int c0 = hl * EPL;
+  float gg[EPL];
+  ldv<EPL>(g + c0, gg);
+  float acc[NS][EPL];
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[k][i] = 0.f;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(M, r0 + rows_per_block);
+  for (int base = r0 + 2 * w; base < r1; base += 16) {
+    const int row = base + (lane >> 4);
+    const bool live = row < r1;
+    float d[EPL], xh[EPL];
+    float mu = 0.f, rs = 0.f;
+    if (live) {
+      ldv<EPL>(dy + (long)row * lddy + c0, d);
+      ldv<EPL>(x + (long)row * ldx + c0, xh);
+      mu = mean[row];
+      rs = rstd[row];
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) d[i] = xh[i] = 0.f;
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      xh[i] = (xh[i] - mu) * rs;
+      acc[0][i] += d[i] * xh[i];
+      acc[1][i] += d[i];
+      const float dxh = d[i] * gg[i];
+      s1 += dxh;
+      s2 += dxh * xh[i];
+    }
+    s1 = half_sum(s1) * (1.f / D);
+    s2 = half_sum(s2) * (1.f / D);
+    if (live) {
+      float o[EPL];
+      if (dres) ldv<EPL>(dres + (long)row * ldres + c0, o);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const float t = rs * (d[i] * gg[i] - s1 - xh[i] * s2);
+        o[i] = dres ? o[i] + t : t;
+        if (NS == 3) acc[2][i] += o[i];
+      }
+      if (dx) stv<EPL>(dx + (long)row * lddx + c0, o);
+    }
+  }
+  if (!part) return;
+  // the two half-warps own the same columns; then warps combine in fixed order
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) acc[k][i] += __shfl_xor_sync(0xffffffffu, acc[k][i], 16);
+  for (int k8 = 0; k8 < 8; ++k8) {
+    if (w == k8 && lane < 16) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) red[k][c0 + i] = (k8 == 0 ? 0.f : red[k][c0 + i]) + acc[k][i];
+    }
+    __syncthreads();
+  }
+  for (int c = threadIdx.x; c < NS * D; c += blockDim.x)
+    part[(long)blockIdx.x * NS * D + c] = (&red[0][0])[c];
+}
+
+// ---------------------------------------------------------------------------
 // LayerNorm forward: one warp per row, D <= 1024 (D % 32 == 0).
 // y = (x - mean) * rstd * g + b ; stores mean/rstd for the backward.
 // ---------------------------------------------------------------------------
@@ -128,38 +298,55 @@ ln_bwd_kernel(int M, int D, const T* __restrict__ dy, long lddy, const T* __rest
   }
 }
 
-// part is [nblk][2D]; block (32 cols x 8 lanes), fixed-order combination
-__global__ void ln_param_reduce_kernel(int nblk, int D, const float* __restrict__ part,
-                                       float* __restrict__ dg, float* __restrict__ db) {
+// part is [nblk][NS·D]; block (32 cols x 8 lanes), fixed-order combination;
+// stat k of column c goes to out[k][c] (dgamma, dbeta, Σ dx)
+__global__ void ln_param_reduce_kernel(int nblk, int D, int NS, const float* __restrict__ part,
+                                       float* __restrict__ o0, float* __restrict__ o1,
+                                       float* __restrict__ o2) {
   __shared__ float red[8][33];
-  const int c = blockIdx.x * 32 + threadIdx.x;   // column of the [nblk, 2D] matrix
+  const int c = blockIdx.x * 32 + threadIdx.x;   // column of the [nblk, NS·D] matrix
   float s = 0.f;
-  if (c < 2 * D) {
+  if (c < NS * D) {
 #pragma unroll 4
-    for (int k = threadIdx.y; k < nblk; k += 8) s += part[(long)k * 2 * D + c];
+    for (int k = threadIdx.y; k < nblk; k += 8) s += part[(long)k * NS * D + c];
   }
   red[threadIdx.y][threadIdx.x] = s;
   __syncthreads();
-  if (threadIdx.y == 0 && c < 2 * D) {
+  if (threadIdx.y == 0 && c < NS * D) {
     float t = 0.f;
 #pragma unroll
     for (int r = 0; r < 8; ++r) t += red[r][threadIdx.x];
-    if (c < D) dg[c] = t;
-    else db[c - D] = t;
+    const int k = c / D, cc = c % D;
+    float* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
+    if (o) o[cc] = t;
   }
 }
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+template <typename T>
+static bool vec_ok(int D, long ld) { return D % 128 == 0 && D <= 1024 && (ld * (long)sizeof(T)) % 16 == 0; }
 
 template <typename T>
 int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const float* b, T* y,
                   long ldy, float* mean, float* rstd, cudaStream_t s) {
   if (D % 32 || D > 1024) { set_error("layernorm: D=%d unsupported", D); return PPLL_ERR_ARG; }
-  const int blocks = ceil_div(M, 8);
-  if (D <= 384)
-    ln_fwd_kernel<T, 12><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
-  else if (D <= 768)
-    ln_fwd_kernel<T, 24><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
-  else
-    ln_fwd_kernel<T, 32><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+  if (vec_ok<T>(D, ldx) && vec_ok<T>(D, ldy) && aligned16(x) && aligned16(y) && aligned16(g) &&
+      aligned16(b)) {
+    const int blocks = ceil_div(M, 16);     // 8 warps x 2 rows
+    switch (D / 16) {
+#define LNF(E) case E: ln_fwd_vkernel<T, E><<<blocks, 256, 0, s>>>(M, x, ldx, g, b, y, ldy, mean, rstd); break;
+      LNF(8) LNF(16) LNF(24) LNF(32) LNF(40) LNF(48) LNF(56) LNF(64)
+#undef LNF
+    }
+  } else {
+    const int blocks = ceil_div(M, 8);
+    if (D <= 384)
+      ln_fwd_kernel<T, 12><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+    else if (D <= 768)
+      ln_fwd_kernel<T, 24><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+    else
+      ln_fwd_kernel<T, 32><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+  }
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -171,23 +358,48 @@ int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : min(ceil_div(M,
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
                   const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
-                  float* part, float* dg, float* db, cudaStream_t s) {
+                  float* part, float* dg, float* db, cudaStream_t s, float* dxsum) {
   if (D % 32 || D > 1024) { set_error("layernorm: D=%d unsupported", D); return PPLL_ERR_ARG; }
   const int nblk = ln_bwd_blocks(M);
   const int rpb = ceil_div(M, nblk);
-  if (D <= 384)
-    ln_bwd_kernel<T, 12><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
-  else if (D <= 768)
-    ln_bwd_kernel<T, 24><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
-  else
-    ln_bwd_kernel<T, 32><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+  const bool vec = D <= 512 && vec_ok<T>(D, lddy) && vec_ok<T>(D, ldx) && (!dres || vec_ok<T>(D, ldres)) &&
+                   (!dx || vec_ok<T>(D, lddx)) && aligned16(dy) && aligned16(x) &&
+                   (!dres || aligned16(dres)) && (!dx || aligned16(dx)) && aligned16(g);
+  int NS = 2;
+  if (vec) {
+    NS = dxsum ? 3 : 2;
+    if (NS == 3) {
+      switch (D / 16) {
+#define LNB(E) case E: ln_bwd_vkernel<T, E, 3><<<nblk, 256, 0, s>>>(M, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb); break;
+        LNB(8) LNB(16) LNB(24) LNB(32)
+#undef LNB
+      }
+    } else {
+      switch (D / 16) {
+#define LNB(E) case E: ln_bwd_vkernel<T, E, 2><<<nblk, 256, 0, s>>>(M, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb); break;
+        LNB(8) LNB(16) LNB(24) LNB(32)
+#undef LNB
+      }
+    }
+  } else {
+    if (dxsum && !dx) { set_error("layernorm: bias sum needs the dx output"); return PPLL_ERR_ARG; }
+    if (D <= 384)
+      ln_bwd_kernel<T, 12><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+    else if (D <= 768)
+      ln_bwd_kernel<T, 24><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+    else
+      ln_bwd_kernel<T, 32><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+  }
   note_launch();
   PPLL_LAUNCH_CHECK();
-  if (part && dg) {
-    ln_param_reduce_kernel<<<ceil_div(2 * D, 32), dim3(32, 8), 0, s>>>(nblk, D, part, dg, db);
+  if (part && (dg || (vec && dxsum))) {
+    ln_param_reduce_kernel<<<ceil_div(NS * D, 32), dim3(32, 8), 0, s>>>(nblk, D, NS, part, dg, db,
+                                                                        vec ? dxsum : nullptr);
     note_launch();
     PPLL_LAUNCH_CHECK();
   }
+  if (!vec && dxsum)   // wide rows: the bias sum as a separate column reduction
+    return launch_colsum<T>(M, D, dx, (int)lddx, dxsum, s, nullptr, 0);
   return PPLL_OK;
 }
 
@@ -494,7 +706,7 @@ int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s)
                                 float*, float*, cudaStream_t);                                   \
   template int launch_ln_bwd<T>(int, int, const T*, long, const T*, long, const float*,          \
                                 const float*, const float*, const T*, long, T*, long, float*,    \
-                                float*, float*, cudaStream_t);                                   \
+                                float*, float*, cudaStream_t, float*);                           \
   template int launch_attn_fwd<T>(int, int, int, int, const T*, T*, float*, cudaStream_t);      \
   template int launch_attn_bwd<T>(int, int, int, int, const T*, const T*, const T*,             \
                                   const float*, T*, cudaStream_t);                               \

@@ -202,8 +202,17 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     LayerBufs& b = st->L[l];
     const void* xin_l = l > 0 ? (const void*)st->L[l - 1].x2
                               : (st->has_patch ? (const void*)st->x0 : x_in);
-    r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), st->G(st->po(l, kB2)),
-                     st->dtype, st->ws, st->ws_elems, s);
+    const bool top = l == st->layers() - 1;
+    // db2 = Σ rows of dx2: for the top layer only the cls rows are non-zero
+    // (Σ of dz over the batch); below, the LN1 backward of layer l+1 already
+    // produced it as a fused output
+    if (top) {
+      r = launch_colsum<TT>(B, D, (const TT*)st->dzc, D, st->G(st->po(l, kB2)), s, st->ws,
+                            st->ws_elems);
+      if (r) return r;
+    }
+    r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, st->ws,
+                     st->ws_elems, s);
     if (r) return r;
     LinOpts og;
     og.mask = b.u;
@@ -218,12 +227,14 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
                    st->ws, st->ws_elems, s);
     if (r) return r;
+    // LN2 backward (+ residual) -> dx1, with dbo = Σ rows dx1 fused
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
                           st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, st->ln_part,
-                          st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s);
+                          st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s,
+                          st->G(st->po(l, kBo)));
     if (r) return r;
-    r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), st->G(st->po(l, kBo)),
-                     st->dtype, st->ws, st->ws_elems, s);
+    r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, st->ws,
+                     st->ws_elems, s);
     if (r) return r;
     r = gemm_dgrad(M, D, D, dx1, D, st->W(st->po(l, kWo)), none, st->dO, D, st->dtype, st->ws,
                    st->ws_elems, s);
@@ -237,12 +248,15 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
                    st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
-    // no gradient into the detached stage input (blocks.py:277-278)
+    // LN1 backward (+ residual) -> gradient of the layer input; no gradient
+    // into the detached stage input (blocks.py:277-278).  Its row sum is the
+    // bias gradient db2 of the layer below (fused).
     const bool need_dx = l > 0 || st->has_patch;
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
                           st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
                           need_dx ? (TT*)dxn_out : nullptr, D, st->ln_part,
-                          st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s);
+                          st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s,
+                          l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr);
     if (r) return r;
     char* t = dx2;
     dx2 = dxn_out;
@@ -315,7 +329,7 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
   st->dxa = A(M * D * e); st->dxb = A(M * D * e); st->dxc = A(M * D * e);
   st->dbig = A(M * F * e); st->dxn = A(M * D * e); st->dqkv = A(M * 3 * D * e);
   st->dO = A(M * D * e);
-  st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 2 * D * 4);
+  st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 3 * D * 4);
   // split-K workspace: 16 partial copies of the largest weight gradient
   st->ws_elems = 16 * (size_t)D * (F > 3 * D ? F : 3 * D);
   st->ws = (float*)A(st->ws_elems * 4);
