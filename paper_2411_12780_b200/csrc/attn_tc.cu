@@ -125,6 +125,56 @@ __device__ __forceinline__ void store_chunk16(uint8_t* buf, int r, int c16, cons
   }
 }
 
+// Warp transpose-reduce of 64 per-lane values: after 5 halving rounds lane L
+// holds the warp-wide sums of columns col_of_lane(L) and col_of_lane(L) + 1.
+__device__ __forceinline__ int col_of_lane(int L) {
+  return ((L >> 4) & 1) * 32 + ((L >> 3) & 1) * 16 + ((L >> 2) & 1) * 8 + ((L >> 1) & 1) * 4 +
+         (L & 1) * 2;
+}
+__device__ __forceinline__ float2 warp_colsum64(const float (&v)[64], int lane) {
+  float a[32];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float keep = hi ? v[j + 32] : v[j], send = hi ? v[j] : v[j + 32];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  float b[16];
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float keep = hi ? a[j + 16] : a[j], send = hi ? a[j] : a[j + 16];
+      b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  float c[8];
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float keep = hi ? b[j + 8] : b[j], send = hi ? b[j] : b[j + 8];
+      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  float d[4];
+  {
+    const bool hi = lane & 2;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float keep = hi ? c[j + 4] : c[j], send = hi ? c[j] : c[j + 4];
+      d[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+  }
+  const bool hi = lane & 1;
+  const float k0 = hi ? d[2] : d[0], s0 = hi ? d[0] : d[2];
+  const float k1 = hi ? d[3] : d[1], s1 = hi ? d[1] : d[3];
+  return make_float2(k0 + __shfl_xor_sync(0xffffffffu, s0, 1),
+                     k1 + __shfl_xor_sync(0xffffffffu, s1, 1));
+}
+
 struct Maps {
   CUtensorMap qkv128;   // box {64, 128} over [tokens, 3D]
   CUtensorMap qkvK;     // box {64, NK}
@@ -243,7 +293,8 @@ __global__ void __launch_bounds__(128, 1)
 attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                    const __grid_constant__ CUtensorMap mdo, int Tn, int H, int NK,
                    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                   const float* __restrict__ lse, __nv_bfloat16* __restrict__ dqkv, float scale) {
+                   const float* __restrict__ lse, __nv_bfloat16* __restrict__ dqkv, float scale,
+                   float* __restrict__ bias_part) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base0 = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + ((1024 - (base0 & 1023)) & 1023);
@@ -353,17 +404,34 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     const uint32_t col = part == 0 ? 0u : (part == 1 ? 64u : 128u);
 #pragma unroll
     for (int c = 0; c < 64; c += 16) ld16(lane_base + col + c, v + c);
+    const float sc = part == 0 ? 1.f : scale;
+    const int off = part == 0 ? 2 * D : (part == 1 ? D : 0);
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = r < Tn ? v[i] * sc : 0.f;
     if (r < Tn) {
-      const float sc = part == 0 ? 1.f : scale;
-      const int off = part == 0 ? 2 * D : (part == 1 ? D : 0);
       __nv_bfloat16* dst = dqkv + (long)(row0 + r) * ld + off + h * kDh;
       float v32[32];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v32[i] = v[32 * hh + i] * sc;
+        for (int i = 0; i < 32; ++i) v32[i] = v[32 * hh + i];
         st_row32<__nv_bfloat16>(dst + 32 * hh, true, 32, v32);
       }
+    }
+    if (bias_part) {
+      // fused bias gradient: Σ over this image's rows of the 64 columns, as a
+      // warp transpose-reduce (lane keeps 2 columns) then a fixed-order sum of
+      // the 4 warps; partial row b of a [batch, 3D] matrix
+      float2 cs = warp_colsum64(v, r & 31);
+      float* red = reinterpret_cast<float*>(sP);
+      const int cb = col_of_lane(r & 31);
+      red[warp * 64 + cb] = cs.x;
+      red[warp * 64 + cb + 1] = cs.y;
+      __syncthreads();
+      if (tid < 64)
+        bias_part[(long)b * ld + off + h * kDh + tid] =
+            ((red[tid] + red[64 + tid]) + red[128 + tid]) + red[192 + tid];
+      __syncthreads();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -432,7 +500,7 @@ int launch_attn_tc_fwd(int B, int Tn, int H, const __nv_bfloat16* qkv, __nv_bflo
 
 int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __nv_bfloat16* o,
                        const __nv_bfloat16* dout, const float* lse, __nv_bfloat16* dqkv,
-                       cudaStream_t s) {
+                       cudaStream_t s, float* bias_part) {
   using namespace atc;
   const int D = H * kDh, NK = (Tn + 15) / 16 * 16;
   CUtensorMap mq, mk, md;
@@ -449,7 +517,7 @@ int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __n
     set = true;
   }
   attn_tc_bwd_kernel<<<B * H, 128, kBwdSmem, s>>>(mq, mk, md, Tn, H, NK, o, dout, lse, dqkv,
-                                                  1.0f / sqrtf((float)kDh));
+                                                  1.0f / sqrtf((float)kDh), bias_part);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

@@ -140,9 +140,16 @@ gemm_dot_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs, long a
   const int n = m_fast ? (int)(idx / M) : (int)(idx % N);
   const TI* ar = A + (long)m * a_rs;
   const TI* bc = Bm + (long)n * b_cs;
-  float acc = 0.f;
-  for (int k = 0; k < K; ++k) acc = fmaf(to_f(ar[(long)k * a_cs]), to_f(bc[(long)k * b_rs]), acc);
-  ep.apply(m, n, acc);
+  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;   // 4 independent chains (ILP)
+  int k = 0;
+  for (; k + 4 <= K; k += 4) {
+    acc0 = fmaf(to_f(ar[(long)k * a_cs]), to_f(bc[(long)k * b_rs]), acc0);
+    acc1 = fmaf(to_f(ar[(long)(k + 1) * a_cs]), to_f(bc[(long)(k + 1) * b_rs]), acc1);
+    acc2 = fmaf(to_f(ar[(long)(k + 2) * a_cs]), to_f(bc[(long)(k + 2) * b_rs]), acc2);
+    acc3 = fmaf(to_f(ar[(long)(k + 3) * a_cs]), to_f(bc[(long)(k + 3) * b_rs]), acc3);
+  }
+  for (; k < K; ++k) acc0 = fmaf(to_f(ar[(long)k * a_cs]), to_f(bc[(long)k * b_rs]), acc0);
+  ep.apply(m, n, (acc0 + acc1) + (acc2 + acc3));
 }
 
 template <typename TI, typename TO>
@@ -163,8 +170,9 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
   if (N <= 32 || K <= 32) {
     Epilogue<TO> e = ep;
     e.partial = nullptr;
-    // fastest thread index along the dimension whose operand (or output) is contiguous
-    const int m_fast = (b_cs != 1 && a_rs == 1) ? 1 : 0;
+    // fastest thread index along the dimension whose streamed operand is contiguous:
+    // m when A is m-contiguous and N is small (its B element is then a warp broadcast)
+    const int m_fast = (a_rs == 1 && (b_cs != 1 || N <= 32)) ? 1 : 0;
     gemm_dot_kernel<TI, TO><<<ceil_div((long)M * N, 256), 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B,
                                                                          b_rs, b_cs, e, m_fast);
     note_launch();

@@ -27,9 +27,10 @@ int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, cons
 bool attn_tc_supported(int Tn, int dh);
 int launch_attn_tc_fwd(int B, int Tn, int H, const __nv_bfloat16* qkv, __nv_bfloat16* o,
                        float* lse, cudaStream_t s);
+// bias_part (nullable): [B, 3D] per-image column sums of dqkv (fused bias grad)
 int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __nv_bfloat16* o,
                        const __nv_bfloat16* dout, const float* lse, __nv_bfloat16* dqkv,
-                       cudaStream_t s);
+                       cudaStream_t s, float* bias_part = nullptr);
 extern int g_attn_engine;   // 0 auto (tcgen05 when supported), 1 SIMT
 
 template <typename T>

@@ -300,22 +300,22 @@ ln_bwd_kernel(int M, int D, const T* __restrict__ dy, long lddy, const T* __rest
 
 // part is [nblk][NS·D]; block (32 cols x 8 lanes), fixed-order combination;
 // stat k of column c goes to out[k][c] (dgamma, dbeta, Σ dx)
-__global__ void ln_param_reduce_kernel(int nblk, int D, int NS, const float* __restrict__ part,
-                                       float* __restrict__ o0, float* __restrict__ o1,
-                                       float* __restrict__ o2) {
-  __shared__ float red[8][33];
+__global__ void __launch_bounds__(1024)
+ln_param_reduce_kernel(int nblk, int D, int NS, const float* __restrict__ part,
+                       float* __restrict__ o0, float* __restrict__ o1, float* __restrict__ o2) {
+  __shared__ float red[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x;   // column of the [nblk, NS·D] matrix
   float s = 0.f;
   if (c < NS * D) {
 #pragma unroll 4
-    for (int k = threadIdx.y; k < nblk; k += 8) s += part[(long)k * NS * D + c];
+    for (int k = threadIdx.y; k < nblk; k += 32) s += part[(long)k * NS * D + c];
   }
   red[threadIdx.y][threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.y == 0 && c < NS * D) {
     float t = 0.f;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) t += red[r][threadIdx.x];
+    for (int r = 0; r < 32; ++r) t += red[r][threadIdx.x];
     const int k = c / D, cc = c % D;
     float* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
     if (o) o[cc] = t;
@@ -353,7 +353,7 @@ int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const floa
 }
 
 // ~2 rows per warp: enough rows in flight to cover DRAM latency, few partials
-int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : min(ceil_div(M, 16), 148 * 4); }
+int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : min(ceil_div(M, 16), 148 * 2); }
 
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
@@ -393,7 +393,7 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
   note_launch();
   PPLL_LAUNCH_CHECK();
   if (part && (dg || (vec && dxsum))) {
-    ln_param_reduce_kernel<<<ceil_div(NS * D, 32), dim3(32, 8), 0, s>>>(nblk, D, NS, part, dg, db,
+    ln_param_reduce_kernel<<<ceil_div(NS * D, 32), dim3(32, 32), 0, s>>>(nblk, D, NS, part, dg, db,
                                                                         vec ? dxsum : nullptr);
     note_launch();
     PPLL_LAUNCH_CHECK();

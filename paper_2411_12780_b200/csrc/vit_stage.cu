@@ -51,6 +51,7 @@ struct ppll_vit_stage {
   char *dxa = nullptr, *dxb = nullptr, *dxc = nullptr, *dbig = nullptr, *dxn = nullptr,
        *dqkv = nullptr, *dO = nullptr, *dtok = nullptr;
   float* ln_part = nullptr;
+  float* attn_bpart = nullptr;
   float* ws = nullptr;
   size_t ws_elems = 0;
   std::vector<void*> allocs;
@@ -84,14 +85,23 @@ static int attn_fwd_any(int B, int T, int H, int dh, const TT* qkv, TT* o, float
   }
   return launch_attn_fwd<TT>(B, T, H, dh, qkv, o, lse, s);
 }
+// also produces dbqkv = Σ rows of dqkv (fused into the tcgen05 kernel, or a
+// separate column reduction for the SIMT kernels)
 template <typename TT>
 static int attn_bwd_any(int B, int T, int H, int dh, const TT* qkv, const TT* o, const TT* dout,
-                        const float* lse, TT* dqkv, cudaStream_t s) {
+                        const float* lse, TT* dqkv, float* dbqkv, float* bpart, float* ws,
+                        size_t ws_elems, cudaStream_t s) {
+  const int D3 = 3 * H * dh;
   if constexpr (std::is_same<TT, __nv_bfloat16>::value) {
-    if (g_attn_engine == 0 && attn_tc_supported(T, dh))
-      return launch_attn_tc_bwd(B, T, H, qkv, o, dout, lse, dqkv, s);
+    if (g_attn_engine == 0 && attn_tc_supported(T, dh)) {
+      int r = launch_attn_tc_bwd(B, T, H, qkv, o, dout, lse, dqkv, s, bpart);
+      if (r) return r;
+      return launch_colsum<float>(B, D3, bpart, D3, dbqkv, s, ws, ws_elems);
+    }
   }
-  return launch_attn_bwd<TT>(B, T, H, dh, qkv, o, dout, lse, dqkv, s);
+  int r = launch_attn_bwd<TT>(B, T, H, dh, qkv, o, dout, lse, dqkv, s);
+  if (r) return r;
+  return launch_colsum<TT>(B * T, D3, dqkv, D3, dbqkv, s, ws, ws_elems);
 }
 
 template <typename TT>
@@ -240,10 +250,11 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
                    st->ws_elems, s);
     if (r) return r;
     r = attn_bwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
-                            b.lse, (TT*)st->dqkv, s);
+                         b.lse, (TT*)st->dqkv, st->G(st->po(l, kBqkv)), st->attn_bpart, st->ws,
+                         st->ws_elems, s);
     if (r) return r;
-    r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)),
-                     st->G(st->po(l, kBqkv)), st->dtype, st->ws, st->ws_elems, s);
+    r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)), nullptr,
+                     st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
     r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
                    st->dtype, st->ws, st->ws_elems, s);
@@ -330,6 +341,7 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
   st->dbig = A(M * F * e); st->dxn = A(M * D * e); st->dqkv = A(M * 3 * D * e);
   st->dO = A(M * D * e);
   st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 3 * D * 4);
+  st->attn_bpart = (float*)A((size_t)st->Bmax * 3 * D * 4);
   // split-K workspace: 16 partial copies of the largest weight gradient
   st->ws_elems = 16 * (size_t)D * (F > 3 * D ? F : 3 * D);
   st->ws = (float*)A(st->ws_elems * 4);
