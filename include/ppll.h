@@ -177,6 +177,10 @@ int ppll_ipc_open_handle(const void* handle /* 64 bytes */, void** dev_ptr_out);
 int ppll_ipc_close_handle(void* dev_ptr);
 int ppll_enable_peer(int peer_device);
 
+/* stream-ordered byte copy between any two device pointers (incl. IPC-mapped
+ * peer memory): the labels travelling with a pushed batch (runtime.py:353) */
+int ppll_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
 /* runtime-owned device memory (ring slots/flags; IPC-exportable) */
 void* ppll_dev_alloc(size_t bytes);   /* zero-filled; NULL on failure */
 int ppll_dev_free(void* dev_ptr);

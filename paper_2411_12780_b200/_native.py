@@ -51,6 +51,7 @@ SIGNATURES = {
     "ppll_ipc_open_handle": (_i, [_vp, _vp]),
     "ppll_ipc_close_handle": (_i, [_vp]),
     "ppll_enable_peer": (_i, [_i]),
+    "ppll_copy_async": (_i, [_vp, _vp, C.c_size_t, _vp]),
     "ppll_dev_alloc": (_vp, [C.c_size_t]),
     "ppll_dev_free": (_i, [_vp]),
     "ppll_stream_sync": (_i, [_vp]),

@@ -309,13 +309,16 @@ def _init_layer_host(rng, fan_in, fan_out):
 
 
 def build_modules(spec: NetworkSpec, plan: PartitionPlan, d_prime: int, n: int,
-                  hyper: Hyperparams, devices: Sequence | None = None) -> list:
+                  hyper: Hyperparams, devices: Sequence | None = None,
+                  only: Sequence[int] | None = None) -> list:
     """One LocalModule per stage of ``plan`` (blocks.py:198-237).
 
     Initial values are drawn on the host with the reference's generator and
     draw order (``default_rng(seed + j)``, block layers then aux layers, W
     before b) and uploaded once; ``devices[j]`` places stage j (default: the
-    current CUDA device for every stage).
+    current CUDA device for every stage).  ``only`` builds just those stage
+    indices (one process per GPU: each rank builds its own stages; a stage's
+    init does not depend on the others, blocks.py:202-204).
     """
     if plan.boundaries[-1][1] != spec.n_layers:
         raise ConfigMismatch("partition plan does not cover the network")
@@ -324,6 +327,8 @@ def build_modules(spec: NetworkSpec, plan: PartitionPlan, d_prime: int, n: int,
     last_stage = plan.n_stages - 1
     modules = []
     for j, (start, end) in enumerate(plan.boundaries):
+        if only is not None and j not in only:
+            continue
         device = torch.device(devices[j]) if devices is not None else default_device()
         if isinstance(device, torch.device) and device.type == "cuda" and device.index is None:
             device = torch.device("cuda", torch.cuda.current_device())

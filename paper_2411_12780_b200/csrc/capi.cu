@@ -226,6 +226,11 @@ int ppll_dev_free(void* p) {
   PPLL_CUDA_CHECK(cudaFree(p));
   return PPLL_OK;
 }
+int ppll_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return PPLL_OK;
+  PPLL_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, S(stream)));
+  return PPLL_OK;
+}
 int ppll_stream_sync(void* stream) {
   PPLL_CUDA_CHECK(cudaStreamSynchronize(S(stream)));
   return PPLL_OK;

@@ -188,7 +188,8 @@ class VitLocalModule(LocalModule):
 
 
 def build_vit_modules(spec: VitSpec, depths: Sequence[int], d_prime: int, n: int,
-                      hyper: Hyperparams, devices: Sequence | None = None) -> list:
+                      hyper: Hyperparams, devices: Sequence | None = None,
+                      only: Sequence[int] | None = None) -> list:
     """One VitLocalModule per block (``depths[j]`` transformer layers each).
 
     Init mirrors blocks.py:198-237: ``default_rng(seed + j)`` per stage; linear
@@ -201,6 +202,8 @@ def build_vit_modules(spec: VitSpec, depths: Sequence[int], d_prime: int, n: int
     s = len(depths)
     mods = []
     for j, dj in enumerate(depths):
+        if only is not None and j not in only:
+            continue
         device = torch.device(devices[j]) if devices is not None else default_device()
         if device.type == "cuda" and device.index is None:
             device = torch.device("cuda", torch.cuda.current_device())
