@@ -212,6 +212,120 @@ def build(wl, precision, device, total_steps):
                                 wl["interval"], hyper, devices=[device] * wl["s"])
 
 
+def sharded_stages(wl, world):
+    """Stage count at N GPUs: the configured s, or N when N exceeds it (the
+    paper's LPP: one block per GPU; ViT-S depth 8 on 8 GPUs = 1 layer/block)."""
+    return max(wl["s"], world)
+
+
+def run_sharded(args, wl, rank, world, local, dev):
+    """N > 1: stages sharded over ranks (stage j on rank floor(j·N/s)),
+    cross-GPU boundaries are CUDA-IPC rings written by the producer's epilogue
+    over NVLink; device-timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2411_12780_b200 as lp
+    from paper_2411_12780_b200 import _native as N
+    from paper_2411_12780_b200.distributed import (DistributedPipeline, gather_metrics,
+                                                   stage_placement)
+    s = sharded_stages(wl, world)
+    placement = stage_placement(s, world)
+    mine = [j for j in range(s) if placement[j] == rank]
+    B = wl["batch"]
+    total = args.warmup + 2 * args.steps + 16
+    hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=total, seed=42,
+                           precision=args.precision)
+    if wl["kind"] == "mlp":
+        spec = lp.NetworkSpec(wl["dims"])
+        s = min(s, spec.n_layers)
+        placement = stage_placement(s, world)
+        mine = [j for j in range(s) if placement[j] == rank]
+        mods = lp.build_modules(spec, lp.partition(spec, s), wl["d_prime"], wl["interval"],
+                                hyper, devices=[dev] * s, only=mine)
+    else:
+        spec = lp.VitSpec(**wl["spec"])
+        mods = lp.build_vit_modules(spec, lp.balanced_depths(spec.depth, s), wl["d_prime"],
+                                    wl["interval"], hyper, devices=[dev] * s, only=mine)
+    pipe = DistributedPipeline(mods, placement, rank, None, capacity=args.capacity, max_batch=B,
+                               use_graphs=not args.no_graphs)
+    in_shape = None
+    if rank == placement[0]:
+        in_shape = tuple(mods[0].in_shape)
+    shapes = [None] * world
+    dist.all_gather_object(shapes, in_shape)
+    in_shape = next(x for x in shapes if x is not None)
+    n_cls = spec.classes if wl["kind"] == "vit" else wl["dims"][-1]
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    pool = None
+    if rank == placement[0]:
+        pool = (torch.randn((64, B) + in_shape, device=dev, generator=gen),
+                torch.randint(0, n_cls, (64, B), device=dev, generator=gen))
+
+    def batches(k, off=0):
+        if pool is None:
+            return None
+        return ((pool[0][(off + i) % 64], pool[1][(off + i) % 64]) for i in range(k))
+
+    pipe.run(batches(args.warmup), args.warmup, B)
+    launches0 = N.launch_count() + pipe.replayed_kernels
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        res = pipe.run(batches(args.steps, 11), args.steps, B)
+    launches = N.launch_count() + pipe.replayed_kernels - launches0
+    met = gather_metrics(res, s, args.steps, args.steps * B, None)
+    errs = [None] * world
+    dist.all_gather_object(errs, res["errors"])
+    value = met.images / met.wall_time
+    idle = met.idle_fraction
+    # e2e: host numpy batches through the same sharded pipeline (rank 0 H2D)
+    rng = np.random.default_rng(7)
+    host = [(rng.standard_normal((B,) + in_shape).astype(np.float32),
+             rng.integers(0, n_cls, B)) for _ in range(8)]
+    e2e_steps = max(10, args.steps // 2)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    r2 = pipe.run((host[i % 8] for i in range(e2e_steps)) if rank == placement[0] else None,
+                  e2e_steps, B)
+    m2 = gather_metrics(r2, s, e2e_steps, e2e_steps * B, None)
+    e2e_dt = time.perf_counter() - t0
+    dts = [None] * world
+    dist.all_gather_object(dts, e2e_dt)
+    e2e_dt = max(dts)
+    launch_counts = [None] * world
+    dist.all_gather_object(launch_counts, launches)
+    if rank == 0:
+        line = {
+            "metric": "images/sec training (device-timed) at 1/2/4/8 B200; pipeline idle fraction",
+            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * met.wall_time / args.steps,
+            "higher_is_better": True, "scaling": "strong" if s == wl["s"] else "weak",
+            "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (seeded N(0,1) CIFAR-shaped inputs, uniform labels; "
+                    "random-init weights drawn like the reference)",
+            "config": cfg_dict(wl, args) | {
+                "stages": s, "placement": f"stage->rank {placement}",
+                "parallelism": f"pp{world} (PPLL stages sharded over GPUs; CUDA-IPC rings, "
+                               f"producer epilogue stores over NVLink)"},
+            "idle_fraction": {"per_stage": [round(x, 4) for x in idle],
+                              "mean": round(sum(idle) / len(idle), 4)},
+            "e2e": {"value": e2e_steps * B / e2e_dt, "unit": "images/s",
+                    "h2d_bytes_per_step": B * int(np.prod(in_shape)) * 4 + B * 8,
+                    "d2h_bytes_per_step": 4 * s,
+                    "api": "DistributedPipeline.run on host numpy batches (rank 0 H2D)"},
+            "roofline": None, "cpu_baseline": None,
+            "gpu_launches": int(sum(launch_counts)),
+            "clocks": clk.summary(),
+            "stage_errors": errs,
+            "final_losses": [h[-1] if h else None for h in met.loss_history],
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    pipe.close()
+    dist.destroy_process_group()
+
+
 def _time_kernel(fn, dev, reps=20):
     """Median CUDA-event duration of fn() on torch's current stream, L2
     flushed (256 MB write) before every launch."""
@@ -294,6 +408,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PPLL_BENCH_SHARE_GPU") == "1":   # test hook: all ranks on cuda:0
+        local = 0
 
     if args.impl == "reference":
         run_reference_arm(args, wl, rank)
@@ -307,7 +423,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # control plane only (IPC handles, metrics); the data path is P2P
+        dist.init_process_group("gloo")
+        return run_sharded(args, wl, rank, world, local, dev)
     hbm, tf_burst, tf_sus, peak_kind = peaks()
     B = wl["batch"]
     total = args.warmup + 3 * args.steps + 64

@@ -161,6 +161,8 @@ class DistributedPipeline:
         self.x_peer, self.y_peer, self.ready_peer, self.credit_peer = {}, {}, {}, {}
         self.ev_ready, self.ev_free = {}, {}
         self.graphs = {}
+        self.graph_kernels = {}
+        self.replayed_kernels = 0      # kernels launched through graph replays
         self._setup()
 
     # -- setup ---------------------------------------------------------------
@@ -247,12 +249,15 @@ class DistributedPipeline:
             g = torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream(device=self.device)
             cap.wait_stream(stream)
+            n0 = N.launch_count()
             with torch.cuda.graph(g, stream=cap):
                 self._launch(p, slot, B, cap)
+            self.graph_kernels[key] = N.launch_count() - n0
             stream.wait_stream(cap)
             self.graphs[key] = g
         with torch.cuda.stream(stream):
             g.replay()
+        self.replayed_kernels += self.graph_kernels[key]
 
     # -- the epoch -------------------------------------------------------------
     def run(self, batches: Iterable | None, n_batches: int, batch_size: int) -> dict:
