@@ -305,7 +305,7 @@ def run_sharded(args, wl, rank, world, local, dev):
             "data": "synthetic (seeded N(0,1) CIFAR-shaped inputs, uniform labels; "
                     "random-init weights drawn like the reference)",
             "config": cfg_dict(wl, args) | {
-                "stages": s, "placement": f"stage->rank {placement}",
+                "global_batch": B, "stages": s, "placement": f"stage->rank {placement}",
                 "parallelism": f"pp{world} (PPLL stages sharded over GPUs; CUDA-IPC rings, "
                                f"producer epilogue stores over NVLink)"},
             "idle_fraction": {"per_stage": [round(x, 4) for x in idle],
