@@ -80,9 +80,8 @@ def test_split_and_geometry():
 
 def test_local_step_update():
     st = ro.build_resnet_stages(SPEC, 2, d_prime=1, n_int=1, seed=3)[1]
-    c, h = 16, 2
     rng = np.random.default_rng(0)
-    x = rng.standard_normal((2, 4, 4, 8))
+    x = rng.standard_normal((2, 8, 8, 4))      # output of [stem, block0]: 4 ch at 8x8
     y = np.array([1, 4])
     before = [p.copy() for p in st.params()]
     _, _, _, grads = ro.local_grads(st, x, y)
