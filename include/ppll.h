@@ -159,6 +159,28 @@ int ppll_vit_stage_step(ppll_vit_stage* st, int B, const void* x_in, const int64
 int ppll_vit_stage_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_out,
                            void* logits, void* stream);
 
+/* ---- one local step of a ResNet stage (CIFAR basic blocks, NHWC; no
+ * reference implementation — parity pinned to oracle/resnet_oracle.py) ----
+ * cfg[8]  = {max_batch, img_channels, img_size, classes, has_stem, n_blocks,
+ *            n_aux_convs, stem_cout}
+ * geo     = 4 ints per block {cin, cout, stride, h_in}; out_geo = {C, H} of
+ *           the stage output (aux convs and the head run at this size)
+ * offsets = stem {w, bn_g, bn_b} (ignored without stem) + 9 per block
+ *           {w1, g1, b1, w2, g2, b2, ws, gs, bs} (-1 without a shortcut conv)
+ *           + 3 per aux conv {w, g, b} + head {w, b}.  Conv weights are
+ *           [round_up(k·k·Cin, 8), Cout] row-major (tap-major rows). */
+typedef struct ppll_resnet_stage ppll_resnet_stage;
+ppll_resnet_stage* ppll_resnet_stage_create(const int* cfg, const int* geo, const int* out_geo,
+                                            const int64_t* offsets, int64_t n_params, int dtype,
+                                            float* theta, float* grad, float* mom, void* theta_lp,
+                                            const float* lr_table, int* step, int max_step,
+                                            float* loss_hist, int* err, float mu, float wd);
+void ppll_resnet_stage_destroy(ppll_resnet_stage* st);
+int ppll_resnet_stage_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_t* labels,
+                           void* x_out, void* stream);
+int ppll_resnet_stage_forward(ppll_resnet_stage* st, int B, const void* x_in, void* h_out,
+                              void* logits, void* stream);
+
 /* ---- stage-boundary ring (runtime.py:52-120 StageBuffer) ----------------
  * Device-resident flag words for an SPSC ring of `capacity` slots.  ready[i]
  * holds the sequence number (batch_id+1) published into slot i; credit holds

@@ -52,5 +52,6 @@ from .runtime import (
 )
 from .tensor import Tensor, matmul, softmax_xent
 from .vit import VitLocalModule, VitSpec, balanced_depths, build_vit_modules
+from .resnet import ResLocalModule, ResNetSpec, build_resnet_modules, resnet_split
 
 __version__ = "0.1.0"

@@ -109,7 +109,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
-  static constexpr int B_BYTES = BN * BK * 2;     // BN * 128 B
+  static constexpr int B_BYTES = (BN < 64 ? 64 : BN) * BK * 2;  // MN-major boxes are 64 wide
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
   static constexpr int EPI = 2 * BN * 4;          // bias slice per accumulator buffer
@@ -177,7 +177,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
           mbar_wait(&empty[st], ((kb_total / S) & 1) ^ 1);
           uint8_t* sa = smem + st * L::STAGE;
           uint8_t* sb = sa + L::A_BYTES;
-          mbar_expect_tx(&full[st], L::STAGE);
+          mbar_expect_tx(&full[st], L::A_BYTES + (B_K ? BN * BK * 2 : L::B_BYTES));
           if (A_K) {
             tma_load_2d(&map_a, &full[st], sa, k0, m0);
           } else {
@@ -189,7 +189,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             tma_load_2d(&map_b, &full[st], sb, k0, n0);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
+            for (int i = 0; i < (BN + 63) / 64; ++i)
               tma_load_2d(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0);
           }
         }
@@ -342,7 +342,9 @@ static int dispatch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int
     case 256: return run<TO, A_K, B_K, 256>(ma, mb, M, N, K, sc, ep, part, s);
     case 192: return run<TO, A_K, B_K, 192>(ma, mb, M, N, K, sc, ep, part, s);
     case 128: return run<TO, A_K, B_K, 128>(ma, mb, M, N, K, sc, ep, part, s);
-    default: return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, sc, ep, part, s);
+    case 64: return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, sc, ep, part, s);
+    case 32: return run<TO, A_K, B_K, 32>(ma, mb, M, N, K, sc, ep, part, s);
+    default: return run<TO, A_K, B_K, 16>(ma, mb, M, N, K, sc, ep, part, s);
   }
 }
 
@@ -354,7 +356,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
                    float* ws, size_t ws_elems, cudaStream_t s) {
   using namespace tc;
   // shapes a 128-row tensor-core tile cannot use efficiently go to the SIMT engine
-  if (N < 32 || K < 16 || M < 1) return PPLL_ERR_UNSUPPORTED;
+  if (N < 16 || K < 16 || M < 1) return PPLL_ERR_UNSUPPORTED;
   if (((uintptr_t)A & 15) || ((uintptr_t)B & 15) || (lda * 2) % 16 || (ldb * 2) % 16)
     return PPLL_ERR_UNSUPPORTED;
   const int mt = ceil_div(M, BM);
@@ -367,9 +369,10 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   const double out_b = (double)sizeof(TO);
   int bn = 64, splits = 1;
   double best = -1;
-  const int cands[4] = {256, 192, 128, 64};
-  for (int i = 0; i < 4; ++i) {
+  const int cands[6] = {256, 192, 128, 64, 32, 16};
+  for (int i = 0; i < 6; ++i) {
     const int c = cands[i];
+    if (c < 64 && N > c) continue;       // narrow tiles only as the single column tile
     const long tiles = (long)mt * ceil_div(N, c);
     int sp = 1;
     if (ws && tiles * 2 <= kNumSMs && K >= 8 * BK) {

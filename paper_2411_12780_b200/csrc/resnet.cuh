@@ -1,0 +1,33 @@
+// ResNet kernel launchers (resnet_kernels.cu), used by the ResNet stage executor.
+#pragma once
+#include "common.cuh"
+
+namespace ppll {
+
+constexpr float kBnEps = 1e-5f;
+
+template <typename T>
+int launch_im2col(int N, int H, int W, int C, int k, int stride, int Kp, const T* x, T* col,
+                  cudaStream_t s);
+template <typename T>
+int launch_col2im(int N, int H, int W, int C, int k, int stride, int Kp, const T* dcol,
+                  const T* dres, const T* mask, T* dx, cudaStream_t s);
+int bn_chunks(int P);   // part buffers hold bn_chunks(P) * 3 * C floats
+template <typename T>
+int launch_bn_stats(int P, int C, const T* z, float* part, float* mean, float* rstd,
+                    cudaStream_t s);
+template <typename T>
+int launch_bn_apply(long P, int C, const T* z, const float* mean, const float* rstd, const float* g,
+                    const float* b, const T* z2, const float* mean2, const float* rstd2,
+                    const float* g2, const float* b2, const T* res, int relu, T* y, cudaStream_t s);
+template <typename T>
+int launch_relu_mask(long n, const T* dout, const T* out, T* dy, cudaStream_t s);
+template <typename T>
+int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, const float* rstd,
+                  const float* g, float* part, float* dg, float* db, T* dz, cudaStream_t s);
+template <typename T>
+int launch_gap(int N, int HW, int C, const T* x, T* out, cudaStream_t s);
+template <typename T>
+int launch_gap_bwd(int N, int HW, int C, const T* dp, T* dx, cudaStream_t s);
+
+}  // namespace ppll

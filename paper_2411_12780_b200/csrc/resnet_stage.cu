@@ -1,0 +1,397 @@
+// Native executor of one ResNet local-learning stage (the PPLL local step,
+// blocks.py:266-289 semantics, applied to CIFAR basic blocks; parity vs
+// oracle/resnet_oracle.py):
+//
+//   [stem conv3x3 + BN + ReLU]                         (stage 0 only)
+//   blocks : conv3x3(stride) → BN → ReLU → conv3x3 → BN  (+ shortcut: identity
+//            or conv1x1(stride) → BN) → add → ReLU; the last block's apply
+//            kernel also stores the push (x_out, PRE-update parameters)
+//   aux    : N_l × [conv3x3 → BN → ReLU] at the boundary resolution
+//   head   : global average pool → linear → softmax-CE
+//   backward in reverse (no gradient into the detached stage input), then one
+//   Nesterov launch over the flat parameter buffer.
+//
+// NHWC activations; a convolution is im2col (kept for the weight gradient) ·
+// W[k·k·Cin(padded to Kp), Cout] on the tcgen05 GEMM engine; its input
+// gradient is (dZ · Wᵀ) → col2im.  BatchNorm uses batch statistics (training
+// mode) with deterministic Welford / fixed-order reductions.
+#include <algorithm>
+#include <vector>
+#include "common.cuh"
+#include "kernels.cuh"
+#include "resnet.cuh"
+
+namespace {
+struct ConvBN {            // conv (+ its BN) activations kept for the backward
+  int cin, cout, k, stride, h_in, h_out, kp;
+  char *col, *z;
+  float *mean, *rstd;
+};
+struct Block {
+  ConvBN c1, c2;
+  bool has_sc;
+  ConvBN sc;
+  char *a1, *out;
+  int64_t off[9];          // w1 g1 b1 w2 g2 b2 ws gs bs
+};
+struct Aux {
+  ConvBN c;
+  char* out;
+  int64_t off[3];
+};
+}  // namespace
+
+struct ppll_resnet_stage {
+  int Bmax, img_c, img_hw, classes, has_stem, n_blk, n_aux, dtype;
+  size_t esz;
+  int64_t n_params;
+  float *theta, *grad, *mom;
+  void* theta_lp;
+  const float* lr_table;
+  int* step;
+  int max_step;
+  float* loss_hist;
+  int* err;
+  float mu, wd;
+  ConvBN stem;
+  char* stem_out = nullptr;
+  int64_t stem_off[3];
+  std::vector<Block> blocks;
+  std::vector<Aux> aux;
+  int64_t head_off[2];
+  int c_out = 0, h_out = 0;
+  char *pooled = nullptr, *logits = nullptr, *dlog = nullptr, *dp = nullptr;
+  char *dsum = nullptr, *dz = nullptr, *dy = nullptr, *dcol = nullptr, *dxa = nullptr,
+       *dxb = nullptr, *dtmp = nullptr;
+  float* bn_part = nullptr;
+  float* ws = nullptr;
+  size_t ws_elems = 0;
+  std::vector<void*> allocs;
+
+  char* alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, (bytes + 255) / 256 * 256) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return reinterpret_cast<char*>(p);
+  }
+  const void* W(int64_t o) const {
+    return dtype == PPLL_F32 ? (const void*)(theta + o)
+                             : (const void*)(reinterpret_cast<const __nv_bfloat16*>(theta_lp) + o);
+  }
+  const float* P(int64_t o) const { return theta + o; }
+  float* G(int64_t o) const { return grad + o; }
+};
+
+using namespace ppll;
+
+static int kp_of(int k, int cin) { return (k * k * cin + 7) / 8 * 8; }
+
+static bool make_conv(ppll_resnet_stage* st, ConvBN& c, int cin, int cout, int k, int stride,
+                      int h_in) {
+  c.cin = cin; c.cout = cout; c.k = k; c.stride = stride; c.h_in = h_in;
+  c.h_out = (h_in + 2 * ((k - 1) / 2) - k) / stride + 1;
+  c.kp = kp_of(k, cin);
+  const size_t P = (size_t)st->Bmax * c.h_out * c.h_out;
+  c.col = st->alloc(P * c.kp * st->esz);
+  c.z = st->alloc(P * cout * st->esz);
+  c.mean = (float*)st->alloc(cout * 4);
+  c.rstd = (float*)st->alloc(cout * 4);
+  return c.col && c.z && c.mean && c.rstd;
+}
+
+// conv (im2col · W) → BN statistics; returns z in c.z
+template <typename TT>
+static int conv_bn_fwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* x, int64_t w_off,
+                       cudaStream_t s) {
+  const int P = B * c.h_out * c.h_out;
+  int r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)x,
+                            (TT*)c.col, s);
+  if (r) return r;
+  LinOpts o;
+  r = gemm_fwd(P, c.kp, c.cout, c.col, c.kp, st->W(w_off), o, c.z, c.cout, st->dtype, st->ws,
+               st->ws_elems, s);
+  if (r) return r;
+  return launch_bn_stats<TT>(P, c.cout, (const TT*)c.z, st->bn_part, c.mean, c.rstd, s);
+}
+
+// given dy (gradient w.r.t. the BN output, ReLU already applied): BN backward,
+// weight gradient, and (if dx) the input gradient col2im(dZ·Wᵀ) (+dres, ⊙mask)
+template <typename TT>
+static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, int64_t w_off,
+                       int64_t g_off, int64_t b_off, void* dx, const void* dres,
+                       const void* mask, cudaStream_t s) {
+  const int P = B * c.h_out * c.h_out;
+  int r = launch_bn_bwd<TT>(P, c.cout, (const TT*)dy, (const TT*)c.z, c.mean, c.rstd,
+                            st->P(g_off), st->bn_part, st->G(g_off), st->G(b_off), (TT*)st->dz, s);
+  if (r) return r;
+  r = linear_wgrad(P, c.kp, c.cout, c.col, c.kp, st->dz, c.cout, st->G(w_off), nullptr,
+                   st->dtype, st->ws, st->ws_elems, s);
+  if (r || !dx) return r;
+  LinOpts none;
+  r = gemm_dgrad(P, c.kp, c.cout, st->dz, c.cout, st->W(w_off), none, st->dcol, c.kp, st->dtype,
+                 st->ws, st->ws_elems, s);
+  if (r) return r;
+  return launch_col2im<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)st->dcol,
+                           (const TT*)dres, (const TT*)mask, (TT*)dx, s);
+}
+
+template <typename TT>
+static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_out, bool head,
+                       cudaStream_t s) {
+  const void* x = x_in;
+  int r;
+  if (st->has_stem) {
+    ConvBN& c = st->stem;
+    r = conv_bn_fwd<TT>(st, c, B, x, st->stem_off[0], s);
+    if (r) return r;
+    r = launch_bn_apply<TT>((long)B * c.h_out * c.h_out, c.cout, (const TT*)c.z, c.mean, c.rstd,
+                            st->P(st->stem_off[1]), st->P(st->stem_off[2]), nullptr, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, 1, (TT*)st->stem_out, s);
+    if (r) return r;
+    x = st->stem_out;
+  }
+  for (size_t i = 0; i < st->blocks.size(); ++i) {
+    Block& b = st->blocks[i];
+    const long P = (long)B * b.c1.h_out * b.c1.h_out;
+    r = conv_bn_fwd<TT>(st, b.c1, B, x, b.off[0], s);
+    if (r) return r;
+    r = launch_bn_apply<TT>(P, b.c1.cout, (const TT*)b.c1.z, b.c1.mean, b.c1.rstd, st->P(b.off[1]),
+                            st->P(b.off[2]), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            1, (TT*)b.a1, s);
+    if (r) return r;
+    r = conv_bn_fwd<TT>(st, b.c2, B, b.a1, b.off[3], s);
+    if (r) return r;
+    if (b.has_sc) {
+      r = conv_bn_fwd<TT>(st, b.sc, B, x, b.off[6], s);
+      if (r) return r;
+      r = launch_bn_apply<TT>(P, b.c2.cout, (const TT*)b.c2.z, b.c2.mean, b.c2.rstd,
+                              st->P(b.off[4]), st->P(b.off[5]), (const TT*)b.sc.z, b.sc.mean,
+                              b.sc.rstd, st->P(b.off[7]), st->P(b.off[8]), nullptr, 1,
+                              (TT*)b.out, s);
+    } else {
+      r = launch_bn_apply<TT>(P, b.c2.cout, (const TT*)b.c2.z, b.c2.mean, b.c2.rstd,
+                              st->P(b.off[4]), st->P(b.off[5]), nullptr, nullptr, nullptr, nullptr,
+                              nullptr, (const TT*)x, 1, (TT*)b.out, s);
+    }
+    if (r) return r;
+    x = b.out;
+  }
+  const long Pout = (long)B * st->h_out * st->h_out;
+  if (x_out)   // the push: the block output (pre-update parameters)
+    PPLL_CUDA_CHECK(cudaMemcpyAsync(x_out, x, Pout * st->c_out * st->esz, cudaMemcpyDeviceToDevice, s));
+  if (!head) return PPLL_OK;
+  for (auto& a : st->aux) {
+    r = conv_bn_fwd<TT>(st, a.c, B, x, a.off[0], s);
+    if (r) return r;
+    r = launch_bn_apply<TT>(Pout, a.c.cout, (const TT*)a.c.z, a.c.mean, a.c.rstd, st->P(a.off[1]),
+                            st->P(a.off[2]), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            1, (TT*)a.out, s);
+    if (r) return r;
+    x = a.out;
+  }
+  r = launch_gap<TT>(B, st->h_out * st->h_out, st->c_out, (const TT*)x, (TT*)st->pooled, s);
+  if (r) return r;
+  LinOpts oh;
+  oh.bias = st->P(st->head_off[1]);
+  return gemm_fwd(B, st->c_out, st->classes, st->pooled, st->c_out, st->W(st->head_off[0]), oh,
+                  st->logits, st->classes, st->dtype, st->ws, st->ws_elems, s);
+}
+
+template <typename TT>
+static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_t* labels,
+                    void* x_out, cudaStream_t s) {
+  int r = res_forward<TT>(st, B, x_in, x_out, true, s);
+  if (r) return r;
+  const int C = st->c_out, HW = st->h_out * st->h_out;
+  r = launch_softmax_xent<TT>(B, st->classes, (const TT*)st->logits, st->classes, labels,
+                              (TT*)st->dlog, st->classes, st->loss_hist, st->step, st->err, s);
+  if (r) return r;
+  // head
+  r = linear_wgrad(B, C, st->classes, st->pooled, C, st->dlog, st->classes, st->G(st->head_off[0]),
+                   st->G(st->head_off[1]), st->dtype, st->ws, st->ws_elems, s);
+  if (r) return r;
+  LinOpts none;
+  r = gemm_dgrad(B, C, st->classes, st->dlog, st->classes, st->W(st->head_off[0]), none, st->dp,
+                 C, st->dtype, st->ws, st->ws_elems, s);
+  if (r) return r;
+  char* dx = st->dxa;
+  char* dx_next = st->dxb;
+  r = launch_gap_bwd<TT>(B, HW, C, (const TT*)st->dp, (TT*)dx, s);
+  if (r) return r;
+  // aux layers, last first (gradient w.r.t. each aux conv-BN-ReLU output)
+  for (int i = (int)st->aux.size() - 1; i >= 0; --i) {
+    Aux& a = st->aux[i];
+    r = launch_relu_mask<TT>((long)B * HW * C, (const TT*)dx, (const TT*)a.out, (TT*)st->dy, s);
+    if (r) return r;
+    r = conv_bn_bwd<TT>(st, a.c, B, st->dy, a.off[0], a.off[1], a.off[2], dx_next, nullptr, nullptr,
+                        s);
+    if (r) return r;
+    char* t = dx; dx = dx_next; dx_next = t;
+  }
+  // blocks, last first
+  for (int i = (int)st->blocks.size() - 1; i >= 0; --i) {
+    Block& b = st->blocks[i];
+    const long P = (long)B * b.c1.h_out * b.c1.h_out;
+    const bool need_dx = i > 0 || st->has_stem;
+    r = launch_relu_mask<TT>(P * b.c2.cout, (const TT*)dx, (const TT*)b.out, (TT*)st->dsum, s);
+    if (r) return r;
+    // conv2: input gradient masked by the ReLU that produced a1 -> dy
+    r = conv_bn_bwd<TT>(st, b.c2, B, st->dsum, b.off[3], b.off[4], b.off[5], st->dy, nullptr, b.a1,
+                        s);
+    if (r) return r;
+    const void* dres = nullptr;
+    if (b.has_sc) {
+      r = conv_bn_bwd<TT>(st, b.sc, B, st->dsum, b.off[6], b.off[7], b.off[8],
+                          need_dx ? st->dtmp : nullptr, nullptr, nullptr, s);
+      if (r) return r;
+      dres = st->dtmp;
+    } else {
+      dres = st->dsum;
+    }
+    // conv1 (+ shortcut / identity gradient) -> gradient of the block input
+    r = conv_bn_bwd<TT>(st, b.c1, B, st->dy, b.off[0], b.off[1], b.off[2],
+                        need_dx ? dx_next : nullptr, dres, nullptr, s);
+    if (r) return r;
+    char* t = dx; dx = dx_next; dx_next = t;
+  }
+  if (st->has_stem) {
+    ConvBN& c = st->stem;
+    const long P = (long)B * c.h_out * c.h_out;
+    r = launch_relu_mask<TT>(P * c.cout, (const TT*)dx, (const TT*)st->stem_out, (TT*)st->dy, s);
+    if (r) return r;
+    r = conv_bn_bwd<TT>(st, c, B, st->dy, st->stem_off[0], st->stem_off[1], st->stem_off[2],
+                        nullptr, nullptr, nullptr, s);
+    if (r) return r;
+  }
+  return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
+                         reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
+                         st->max_step, 0.f, st->mu, st->wd, st->err, s);
+}
+
+extern "C" {
+
+// cfg = {max_batch, img_channels, img_size, classes, has_stem, n_blocks, n_aux, stem_cout}
+// geo = 4 ints per block {cin, cout, stride, h_in}; out_geo = {C_out, H_out}
+// offsets = stem(3) + 9 per block (ws/gs/bs = -1 without shortcut) + 3 per aux + head(2)
+ppll_resnet_stage* ppll_resnet_stage_create(const int* cfg, const int* geo, const int* out_geo,
+                                            const int64_t* offsets, int64_t n_params, int dtype,
+                                            float* theta, float* grad, float* mom, void* theta_lp,
+                                            const float* lr_table, int* step, int max_step,
+                                            float* loss_hist, int* err, float mu, float wd) {
+  ppll_resnet_stage* st = new ppll_resnet_stage();
+  st->Bmax = cfg[0]; st->img_c = cfg[1]; st->img_hw = cfg[2]; st->classes = cfg[3];
+  st->has_stem = cfg[4]; st->n_blk = cfg[5]; st->n_aux = cfg[6];
+  const int stem_cout = cfg[7];
+  st->dtype = dtype;
+  st->esz = dtype == PPLL_F32 ? 4 : 2;
+  st->n_params = n_params;
+  st->theta = theta; st->grad = grad; st->mom = mom; st->theta_lp = theta_lp;
+  st->lr_table = lr_table; st->step = step; st->max_step = max_step;
+  st->loss_hist = loss_hist; st->err = err; st->mu = mu; st->wd = wd;
+  st->c_out = out_geo[0]; st->h_out = out_geo[1];
+  if ((dtype != PPLL_F32 && dtype != PPLL_BF16) || (dtype == PPLL_BF16 && !theta_lp) ||
+      st->Bmax < 1 || (!st->has_stem && st->n_blk < 1)) {
+    set_error("ppll_resnet_stage_create: invalid configuration");
+    delete st;
+    return nullptr;
+  }
+  bool ok = true;
+  int o = 0;
+  size_t maxPC = 0, maxPK = 0, maxC = 16;
+  auto track = [&](const ConvBN& c) {
+    const size_t P = (size_t)st->Bmax * c.h_out * c.h_out;
+    const size_t Pin = (size_t)st->Bmax * c.h_in * c.h_in;
+    maxPC = std::max(maxPC, std::max(P * c.cout, Pin * c.cin));
+    maxPK = std::max(maxPK, P * c.kp);
+    maxC = std::max(maxC, (size_t)c.cout);
+  };
+  if (st->has_stem) {
+    ok = ok && make_conv(st, st->stem, st->img_c, stem_cout, 3, 1, st->img_hw);
+    st->stem_out = st->alloc((size_t)st->Bmax * st->img_hw * st->img_hw * stem_cout * st->esz);
+    ok = ok && st->stem_out;
+    track(st->stem);
+  }
+  for (int i = 0; i < 3; ++i) st->stem_off[i] = offsets[o++];
+  for (int i = 0; i < st->n_blk; ++i) {
+    Block b{};
+    const int cin = geo[4 * i], cout = geo[4 * i + 1], stride = geo[4 * i + 2], h = geo[4 * i + 3];
+    ok = ok && make_conv(st, b.c1, cin, cout, 3, stride, h);
+    ok = ok && make_conv(st, b.c2, cout, cout, 3, 1, b.c1.h_out);
+    b.has_sc = stride != 1 || cin != cout;
+    if (b.has_sc) ok = ok && make_conv(st, b.sc, cin, cout, 1, stride, h);
+    const size_t P = (size_t)st->Bmax * b.c1.h_out * b.c1.h_out;
+    b.a1 = st->alloc(P * cout * st->esz);
+    b.out = st->alloc(P * cout * st->esz);
+    ok = ok && b.a1 && b.out;
+    for (int k = 0; k < 9; ++k) b.off[k] = offsets[o++];
+    track(b.c1); track(b.c2);
+    if (b.has_sc) track(b.sc);
+    st->blocks.push_back(b);
+  }
+  for (int i = 0; i < st->n_aux; ++i) {
+    Aux a{};
+    ok = ok && make_conv(st, a.c, st->c_out, st->c_out, 3, 1, st->h_out);
+    a.out = st->alloc((size_t)st->Bmax * st->h_out * st->h_out * st->c_out * st->esz);
+    ok = ok && a.out;
+    for (int k = 0; k < 3; ++k) a.off[k] = offsets[o++];
+    track(a.c);
+    st->aux.push_back(a);
+  }
+  st->head_off[0] = offsets[o++];
+  st->head_off[1] = offsets[o++];
+  const size_t e = st->esz;
+  st->pooled = st->alloc((size_t)st->Bmax * st->c_out * e);
+  st->logits = st->alloc((size_t)st->Bmax * st->classes * e);
+  st->dlog = st->alloc((size_t)st->Bmax * st->classes * e);
+  st->dp = st->alloc((size_t)st->Bmax * st->c_out * e);
+  st->dsum = st->alloc(maxPC * e); st->dz = st->alloc(maxPC * e); st->dy = st->alloc(maxPC * e);
+  st->dxa = st->alloc(maxPC * e); st->dxb = st->alloc(maxPC * e); st->dtmp = st->alloc(maxPC * e);
+  st->dcol = st->alloc(maxPK * e);
+  st->bn_part = (float*)st->alloc((size_t)256 * 3 * maxC * 4);     // bn_chunks() <= 256
+  // split-K partials of the largest weight gradient ([9·C, C]) for up to 160 splits
+  st->ws_elems = std::max((size_t)1 << 22, (size_t)160 * 9 * maxC * maxC);
+  st->ws = (float*)st->alloc(st->ws_elems * 4);
+  ok = ok && st->pooled && st->logits && st->dlog && st->dp && st->dsum && st->dz && st->dy &&
+       st->dxa && st->dxb && st->dtmp && st->dcol && st->bn_part && st->ws;
+  if (!ok) {
+    set_error("ppll_resnet_stage_create: out of device memory");
+    ppll_resnet_stage_destroy(st);
+    return nullptr;
+  }
+  return st;
+}
+
+void ppll_resnet_stage_destroy(ppll_resnet_stage* st) {
+  if (!st) return;
+  for (void* p : st->allocs) cudaFree(p);
+  delete st;
+}
+
+int ppll_resnet_stage_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_t* labels,
+                           void* x_out, void* stream) {
+  if (!st || B < 1 || B > st->Bmax || !x_in || !labels) {
+    set_error("ppll_resnet_stage_step: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (st->dtype == PPLL_F32) return res_step<float>(st, B, x_in, labels, x_out, s);
+  return res_step<__nv_bfloat16>(st, B, x_in, labels, x_out, s);
+}
+
+int ppll_resnet_stage_forward(ppll_resnet_stage* st, int B, const void* x_in, void* h_out,
+                              void* logits, void* stream) {
+  if (!st || B < 1 || B > st->Bmax) {
+    set_error("ppll_resnet_stage_forward: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int r = st->dtype == PPLL_F32
+              ? res_forward<float>(st, B, x_in, h_out, logits != nullptr, s)
+              : res_forward<__nv_bfloat16>(st, B, x_in, h_out, logits != nullptr, s);
+  if (r || !logits) return r;
+  PPLL_CUDA_CHECK(cudaMemcpyAsync(logits, st->logits, (size_t)B * st->classes * st->esz,
+                                  cudaMemcpyDeviceToDevice, s));
+  return PPLL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+"""GPU parity of the ResNet local step (native ``ppll_resnet_stage_step``)
+against the float64 CPU restatement ``oracle/resnet_oracle.py`` (pinned to
+torch autograd in tests/test_resnet_oracle.py).
+
+Tolerances: fp32 parity mode — per-step loss |Δ| <= 2e-4·max(1,|loss|),
+x_out max|Δ|/max|ref| <= 2e-4, weights max|ΔW|/max|W| <= 2e-3; bf16 mode
+— loss 5e-2 relative, x_out 8e-2, weights 8e-2 (BatchNorm over bf16
+activations).  Pipeline vs round-robin: bitwise."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_12780_b200 as lp
+import resnet_oracle as ro
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(n=1, image=8, channels=3, widths=(16, 32, 64), classes=5)
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _pair(kw, s, d_prime, n, precision, steps, seed=7):
+    hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=steps, seed=seed, precision=precision)
+    mods = lp.build_resnet_modules(lp.ResNetSpec(**kw), s, d_prime, n, hyper)
+    stages = ro.build_resnet_stages(ro.ResNetSpec(**kw), s, d_prime, n, seed)
+    return mods, stages
+
+
+def _flat(m):
+    return np.concatenate([p.data.ravel() for p in m.parameters()])
+
+
+def _flat_o(st):
+    return np.concatenate([p.ravel() for p in st.params()])
+
+
+def test_init_matches_oracle():
+    mods, stages = _pair(SMALL, 3, 1, 2, "fp32", 4)
+    assert [m.n_aux_convs for m in mods] == [len(s.aux) for s in stages]
+    for m, st in zip(mods, stages):
+        np.testing.assert_allclose(_flat(m), _flat_o(st), rtol=0, atol=1e-7)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_resnet_local_steps_match_oracle(precision):
+    steps = 3
+    mods, stages = _pair(SMALL, 3, 1, 2, precision, steps)
+    rng = np.random.default_rng(0)
+    B = 8
+    ltol, xtol, wtol = (2e-4, 2e-4, 2e-3) if precision == "fp32" else (5e-2, 8e-2, 8e-2)
+    for t in range(steps):
+        img = rng.standard_normal((B, 8, 8, 3))
+        y = rng.integers(0, 5, B)
+        h, hr = lp.Tensor(img), img
+        for j, (m, st) in enumerate(zip(mods, stages)):
+            loss, h = lp.local_loss_and_update(m, h, y)
+            ref, hr, _ = ro.local_step(st, hr, y, 0.05, 0.001, steps, 0.9, 1e-4)
+            assert abs(loss - ref) <= ltol * max(1.0, abs(ref)), (t, j, loss, ref)
+            hd = h.data.reshape(hr.shape)
+            assert np.abs(hd - hr).max() / np.abs(hr).max() <= xtol, (t, j)
+            hr = hd if precision == "bf16" else hr
+    for m, st in zip(mods, stages):
+        a, b = _flat(m), _flat_o(st)
+        assert np.abs(a - b).max() / np.abs(b).max() <= wtol
+
+
+def test_resnet32_geometry_one_step_fp32():
+    """ResNet-32 split into 4 stages, batch 4, one step of every stage."""
+    kw = dict(n=5, image=32, channels=3, widths=(16, 32, 64), classes=10)
+    mods, stages = _pair(kw, 4, 2, 3, "fp32", 2)
+    assert [len(m.block_ids) for m in mods] == [3, 4, 4, 4]
+    rng = np.random.default_rng(1)
+    img = rng.standard_normal((4, 32, 32, 3))
+    y = np.array([3, 7, 1, 0])
+    h, hr = lp.Tensor(img), img
+    for m, st in zip(mods, stages):
+        loss, h = lp.local_loss_and_update(m, h, y)
+        ref, hr, _ = ro.local_step(st, hr, y, 0.05, 0.001, 2, 0.9, 1e-4)
+        assert abs(loss - ref) <= 2e-4 * max(1.0, abs(ref))
+        assert np.abs(h.data.reshape(hr.shape) - hr).max() / np.abs(hr).max() <= 2e-4
+    for m, st in zip(mods, stages):
+        a, b = _flat(m), _flat_o(st)
+        assert np.abs(a - b).max() / np.abs(b).max() <= 2e-3
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_resnet_pipeline_bitwise_equals_roundrobin(precision):
+    hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=20, seed=3, precision=precision)
+    a = lp.build_resnet_modules(lp.ResNetSpec(**SMALL), 3, 1, 2, hyper)
+    b = lp.build_resnet_modules(lp.ResNetSpec(**SMALL), 3, 1, 2, hyper)
+    rng = np.random.default_rng(5)
+    data = [(rng.standard_normal((6, 8, 8, 3)), rng.integers(0, 5, 6)) for _ in range(6)]
+    ma = lp.run_epoch(lp.RunMode.PPLL, a, iter(data), lp.RunConfig(buffer_capacity=2))
+    mb = lp.run_deterministic(lp.RunMode.PPLL, b, iter(data), lp.RunConfig(buffer_capacity=2))
+    assert ma.loss_history == mb.loss_history
+    for x, z in zip(a, b):
+        assert np.array_equal(_flat(x), _flat(z))
