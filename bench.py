@@ -45,6 +45,14 @@ WORKLOADS = {
     "vit_s": dict(kind="vit", spec=dict(image=32, channels=3, patch=4, dim=384, heads=6,
                                         mlp=1536, depth=8, classes=10),
                   s=4, d_prime=1, interval=3, batch=128, ref_batch=4),
+    # configs[0]: ResNet-32 / 4 blocks, CIFAR-shaped, batch 128
+    "resnet32": dict(kind="resnet", spec=dict(n=5, image=32, channels=3, widths=(16, 32, 64),
+                                              classes=10),
+                     s=4, d_prime=1, interval=3, batch=128, ref_batch=8, data_shape="CIFAR-10"),
+    # configs[2]: ResNet-110 / 8 blocks, SVHN-shaped, batch 256
+    "resnet110": dict(kind="resnet", spec=dict(n=18, image=32, channels=3, widths=(16, 32, 64),
+                                               classes=10),
+                      s=8, d_prime=1, interval=3, batch=256, ref_batch=4, data_shape="SVHN"),
     "mlp_m": dict(kind="mlp", dims=(3072, 1024, 1024, 1024, 1024, 10), s=4, d_prime=2,
                   interval=3, batch=128, ref_batch=128),
 }
@@ -106,6 +114,12 @@ class ClockSampler:
 
 
 def describe(wl, name):
+    if wl["kind"] == "resnet":
+        sp = wl["spec"]
+        return (f"{name}: PPLL ResNet-{6 * sp['n'] + 2} (CIFAR basic blocks 16/32/64, option-B "
+                f"shortcut, train-mode BN), {wl['s']} gradient-isolated blocks, aux = "
+                f"aux_depth(l,{wl['d_prime']},{wl['interval']}) conv3x3-BN-ReLU + GAP + linear, "
+                f"{wl['data_shape']}-shaped {sp['image']}x{sp['image']}x3 NHWC, batch {wl['batch']}")
     if wl["kind"] == "vit":
         sp = wl["spec"]
         return (f"{name}: PPLL ViT-small/{sp['patch']} depth {sp['depth']} D={sp['dim']} "
@@ -147,6 +161,17 @@ def cpu_reference(wl, n_batches, warmup=1, time_budget=None, batch=None):
 
         def step(x, y):
             orc.sequential_ppll(stages, [(x, y)], 0.05, 0.001, 10 ** 6, 0.9, 1e-4)
+    elif wl["kind"] == "resnet":
+        import resnet_oracle as ro
+        spec = ro.ResNetSpec(**wl["spec"])
+        stages = ro.build_resnet_stages(spec, wl["s"], wl["d_prime"], wl["interval"], 42)
+        data = [(rng.standard_normal((B, spec.image, spec.image, spec.channels)),
+                 rng.integers(0, spec.classes, B)) for _ in range(4)]
+
+        def step(x, y):
+            h = x
+            for st in stages:
+                _, h, _ = ro.local_step(st, h, y, 0.05, 0.001, 10 ** 6, 0.9, 1e-4)
     else:
         import vit_oracle as vo
         spec = vo.VitSpec(**wl["spec"])
@@ -207,6 +232,9 @@ def build(wl, precision, device, total_steps):
         spec = lp.NetworkSpec(wl["dims"])
         return lp.build_modules(spec, lp.partition(spec, wl["s"]), wl["d_prime"],
                                 wl["interval"], hyper, devices=[device] * wl["s"])
+    if wl["kind"] == "resnet":
+        return lp.build_resnet_modules(lp.ResNetSpec(**wl["spec"]), wl["s"], wl["d_prime"],
+                                       wl["interval"], hyper, devices=[device] * wl["s"])
     spec = lp.VitSpec(**wl["spec"])
     return lp.build_vit_modules(spec, lp.balanced_depths(spec.depth, wl["s"]), wl["d_prime"],
                                 wl["interval"], hyper, devices=[device] * wl["s"])
@@ -242,6 +270,10 @@ def run_sharded(args, wl, rank, world, local, dev):
         mine = [j for j in range(s) if placement[j] == rank]
         mods = lp.build_modules(spec, lp.partition(spec, s), wl["d_prime"], wl["interval"],
                                 hyper, devices=[dev] * s, only=mine)
+    elif wl["kind"] == "resnet":
+        spec = lp.ResNetSpec(**wl["spec"])
+        mods = lp.build_resnet_modules(spec, s, wl["d_prime"], wl["interval"], hyper,
+                                       devices=[dev] * s, only=mine)
     else:
         spec = lp.VitSpec(**wl["spec"])
         mods = lp.build_vit_modules(spec, lp.balanced_depths(spec.depth, s), wl["d_prime"],
@@ -254,7 +286,7 @@ def run_sharded(args, wl, rank, world, local, dev):
     shapes = [None] * world
     dist.all_gather_object(shapes, in_shape)
     in_shape = next(x for x in shapes if x is not None)
-    n_cls = spec.classes if wl["kind"] == "vit" else wl["dims"][-1]
+    n_cls = wl["dims"][-1] if wl["kind"] == "mlp" else spec.classes
     gen = torch.Generator(device=dev).manual_seed(1234)
     pool = None
     if rank == placement[0]:
