@@ -113,11 +113,78 @@ __global__ void col2im_kernel(int N, int H, int W, int C, int k, int stride, int
   }
 }
 
+// bf16, C % 8 == 0: one thread per (pixel, 8-channel group), 16-B gathers
+__device__ __forceinline__ void acc8(float* a, uint4 q) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __bfloat1622float2(h[j]);
+    a[2 * j] += f.x;
+    a[2 * j + 1] += f.y;
+  }
+}
+__global__ void col2im_vec_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo,
+                                  int Kp, const __nv_bfloat16* __restrict__ dcol,
+                                  const __nv_bfloat16* __restrict__ dres,
+                                  const __nv_bfloat16* __restrict__ mask,
+                                  __nv_bfloat16* __restrict__ dx) {
+  const int p = (k - 1) / 2, C8 = C / 8;
+  const long total = (long)N * H * W * C8;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(idx % C8);
+    const long q = idx / C8;
+    const int w = (int)(q % W), h = (int)((q / W) % H), n = (int)(q / ((long)W * H));
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < k; ++r) {
+      const int hh = h + p - r;
+      if (hh < 0 || hh % stride) continue;
+      const int ho = hh / stride;
+      if (ho >= Ho) continue;
+      for (int s2 = 0; s2 < k; ++s2) {
+        const int ww = w + p - s2;
+        if (ww < 0 || ww % stride) continue;
+        const int wo = ww / stride;
+        if (wo >= Wo) continue;
+        acc8(a, *reinterpret_cast<const uint4*>(
+                    dcol + (((long)n * Ho + ho) * Wo + wo) * Kp + (r * k + s2) * C + c8 * 8));
+      }
+    }
+    const long o = q * C + c8 * 8;
+    if (dres) acc8(a, *reinterpret_cast<const uint4*>(dres + o));
+    if (mask) {
+      const uint4 mq = *reinterpret_cast<const uint4*>(mask + o);
+      const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mq);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(mh[j]);
+        if (!(f.x > 0.f)) a[2 * j] = 0.f;
+        if (!(f.y > 0.f)) a[2 * j + 1] = 0.f;
+      }
+    }
+    uint4 out;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) oh[j] = __floats2bfloat162_rn(a[2 * j], a[2 * j + 1]);
+    *reinterpret_cast<uint4*>(dx + o) = out;
+  }
+}
+
 template <typename T>
 int launch_col2im(int N, int H, int W, int C, int k, int stride, int Kp, const T* dcol,
                   const T* dres, const T* mask, T* dx, cudaStream_t s) {
   const int p = (k - 1) / 2;
   const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
+  if constexpr (sizeof(T) == 2) {
+    if (C % 8 == 0 && Kp % 8 == 0) {
+      col2im_vec_kernel<<<grid_for((long)N * H * W * C / 8), 256, 0, s>>>(
+          N, H, W, C, k, stride, Ho, Wo, Kp, (const __nv_bfloat16*)dcol,
+          (const __nv_bfloat16*)dres, (const __nv_bfloat16*)mask, (__nv_bfloat16*)dx);
+      note_launch();
+      PPLL_LAUNCH_CHECK();
+      return PPLL_OK;
+    }
+  }
   col2im_kernel<T><<<grid_for((long)N * H * W * C), 256, 0, s>>>(N, H, W, C, k, stride, Ho, Wo,
                                                                   Kp, dcol, dres, mask, dx);
   note_launch();
@@ -165,17 +232,31 @@ __global__ void bn_stats_part_kernel(int P, int C, const T* __restrict__ z, int 
   }
 }
 
+// one warp per channel: lanes merge strided chunks, then a butterfly whose
+// every merge is ordered (lower lane first) — identical on all lanes, and
+// deterministic
 __global__ void bn_stats_final_kernel(int chunks, int C, const float* __restrict__ part,
                                       float* __restrict__ mean, float* __restrict__ rstd) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= C) return;
   Welford t = {0.f, 0.f, 0.f};
-  for (int k = 0; k < chunks; ++k) {
+  for (int k = lane; k < chunks; k += 32) {
     const float* o = part + ((long)k * C + c) * 3;
     t = wf_merge(t, Welford{o[0], o[1], o[2]});
   }
-  mean[c] = t.mean;
-  rstd[c] = rsqrtf(t.m2 / fmaxf(t.n, 1.f) + kBnEps);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Welford u;
+    u.n = __shfl_xor_sync(0xffffffffu, t.n, off);
+    u.mean = __shfl_xor_sync(0xffffffffu, t.mean, off);
+    u.m2 = __shfl_xor_sync(0xffffffffu, t.m2, off);
+    t = (lane & off) ? wf_merge(u, t) : wf_merge(t, u);
+  }
+  if (lane == 0) {
+    mean[c] = t.mean;
+    rstd[c] = rsqrtf(t.m2 / fmaxf(t.n, 1.f) + kBnEps);
+  }
 }
 
 int bn_chunks(int P) { return max(1, min(ceil_div(P, 256), 256)); }
@@ -187,7 +268,7 @@ int launch_bn_stats(int P, int C, const T* z, float* part, float* mean, float* r
   const int rpc = ceil_div(P, chunks);
   bn_stats_part_kernel<T><<<dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s>>>(P, C, z, rpc, part);
   note_launch();
-  bn_stats_final_kernel<<<ceil_div(C, 128), 128, 0, s>>>(chunks, C, part, mean, rstd);
+  bn_stats_final_kernel<<<ceil_div(C, 8), 256, 0, s>>>(chunks, C, part, mean, rstd);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -272,17 +353,23 @@ __global__ void bn_bwd_part_kernel(int P, int C, const T* __restrict__ dy, const
   }
 }
 
+// one warp per channel: lane-strided partial sums, fixed butterfly
 __global__ void bn_bwd_final_kernel(int chunks, int C, const float* __restrict__ part,
                                     float* __restrict__ dg, float* __restrict__ db) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= C) return;
   float a = 0.f, b = 0.f;
-  for (int k = 0; k < chunks; ++k) {
+  for (int k = lane; k < chunks; k += 32) {
     a += part[((long)k * 2 + 0) * C + c];
     b += part[((long)k * 2 + 1) * C + c];
   }
-  dg[c] = a;
-  db[c] = b;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    dg[c] = a;
+    db[c] = b;
+  }
 }
 
 // dz = g·rstd/P · (P·dy − db − xhat·dg)
@@ -309,7 +396,7 @@ int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, cons
   bn_bwd_part_kernel<T><<<dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s>>>(P, C, dy, z, mean,
                                                                               rstd, rpc, part);
   note_launch();
-  bn_bwd_final_kernel<<<ceil_div(C, 128), 128, 0, s>>>(chunks, C, part, dg, db);
+  bn_bwd_final_kernel<<<ceil_div(C, 8), 256, 0, s>>>(chunks, C, part, dg, db);
   note_launch();
   const long total = (long)P * C;
   bn_bwd_dx_kernel<T><<<grid_for(total), 256, 0, s>>>(total, C, 1.f / (float)P, dy, z, mean, rstd,
