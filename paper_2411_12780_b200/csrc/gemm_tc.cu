@@ -34,7 +34,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kNumSMs = 148;
 
@@ -248,8 +248,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       float* bs = bias_s + acc * BN;
       if (!split && ep.bias) {
         // stage this tile's bias slice in shared memory (epilogue warps only)
-        const int t = threadIdx.x - 64;
-        if (t < BN) bs[t] = (n0 + t < N) ? __ldg(ep.bias + n0 + t) : 0.f;
+        for (int t = threadIdx.x - 64; t < BN; t += 32 * kEpiWarps)
+          bs[t] = (n0 + t < N) ? __ldg(ep.bias + n0 + t) : 0.f;
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -257,7 +257,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const int row = m0 + q * 32 + lane;
       const bool live = row < M;
 #pragma unroll 1
-      for (int c = 32 * half; c < BN && n0 + c < N; c += 64) {
+      for (int c = 32 * half; c < BN && n0 + c < N; c += 32 * (kEpiWarps / 4)) {
         float ra[32], ka[32];
         if (!split && live && !sc.probe) ep.load_aux32(row, n0 + c, ra, ka);   // overlaps the TMEM load
         uint32_t r[32];
@@ -387,9 +387,10 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
     }
     const long items = tiles * sp;
     const double waves = (double)((items + kNumSMs - 1) / kNumSMs);
-    // per K=16 step: max(tensor floor 128·N/256 cycles, smem operand read (A 4 KB + B N·32 B) at
-    // 128 B/cycle) — narrow tiles are bound by re-reading A from shared memory
-    const double cyc16 = fmax(c / 2.0, (4096.0 + 32.0 * c) / 128.0);
+    // per K=16 step: max(tensor floor 128·N/256 cycles, operand bytes (A 4 KB + B N·32 B)
+    // streamed L2 -> smem at ~80 B/cycle/SM (measured: 128-wide tiles reach ~55 % of the
+    // tensor peak, 256-wide ~82 %) — narrow tiles re-read A and are bandwidth bound
+    const double cyc16 = fmax(c / 2.0, (4096.0 + 32.0 * c) / 80.0);
     const double t_mma = (double)ceil_div(K, 16 * sp) * cyc16 / 1.9e9;
     (void)mac_rate;
     const double t_epi = 128.0 * c * (sp > 1 ? 4.0 : out_b) / 150e9;
