@@ -16,7 +16,8 @@
 //               32-column chunks): tcgen05.ld 32x32b.x32 (one accumulator row per
 //               thread) → fused bias / residual / pre-activation store /
 //               ReLU|GELU / ReLU-mask|GELU-gradient / dual store (the ring
-//               push), 32-column row segments moved as 16-B vectors; or fp32
+//               push); each warp's 32x32 block is transposed through a 2-KB
+//               smem buffer so stores cover 8 rows x 64 B (full sectors); or fp32
 //               split-K partials reduced afterwards in fixed split order
 //               (deterministic) by splitk_reduce_kernel with the same epilogue.
 // Operand layouts (128-byte swizzled, TMA box inner extent 64 elements):
@@ -114,7 +115,8 @@ struct Smem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
   static constexpr int EPI = 2 * BN * 4;          // bias slice per accumulator buffer
-  static constexpr int TOTAL = STAGES * STAGE + EPI + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STG = kEpiWarps * 2048;    // per-warp store-transpose buffers
+  static constexpr int TOTAL = STAGES * STAGE + EPI + STG + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
 
@@ -133,7 +135,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   const uint32_t base = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
   float* bias_s = reinterpret_cast<float*>(smem + S * L::STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGE + L::EPI);
+  uint8_t* stg_all = smem + S * L::STAGE + L::EPI;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + L::STG);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;      // [2]
   uint64_t* tempty = tfull + 2;     // [2]
@@ -239,6 +242,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // two warps per TMEM lane quadrant, alternating 32-column chunks
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int half = (warp - 2) >> 2;
+    uint8_t* stg = stg_all + (warp - 2) * 2048;
     int it = 0;
     for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
       const int tile = w % sc.tiles, z = w / sc.tiles;
@@ -265,15 +269,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (live) {
-          if (split)
-            st_row32<float>(part + ((long)z * M + row) * N + n0 + c, (N % 4) == 0,
-                            min(32, N - n0 - c), v);
-          else if (!sc.probe)
-            ep.finish_row32(row, n0 + c, v, ra, ka, bs + c);
-          else if (v[0] == 12345.f)   // keep the TMEM load live in probe mode
-            ep.C[0] = v[1];
-        }
+        if (split)
+          warp_store_block32<float>(part + (long)z * M * N, N, nullptr, 0, m0 + q * 32, M, n0 + c,
+                                    N, (N % 4) == 0, v, stg, lane);
+        else if (!sc.probe)
+          ep.finish_block32(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c, stg, lane);
+        else if (live && v[0] == 12345.f)   // keep the TMEM load live in probe mode
+          ep.C[0] = v[1];
       }
       // accumulator buffer drained: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -86,6 +86,64 @@ __device__ __forceinline__ void st_row32<__nv_bfloat16>(__nv_bfloat16* p, bool v
   }
 }
 
+// Coalesced store of a warp's 32x32 output block (thread = one row, 32
+// consecutive columns in registers, as tcgen05.ld 32x32b delivers them).
+// The block is transposed through a 2-KB per-warp shared-memory buffer (rows
+// of 64 B, 16-B chunks XOR-swizzled by (row>>1)&3 so both the row-wise writes
+// and the column-wise reads are bank-conflict free), then each store
+// instruction covers 8 rows x 64 contiguous bytes (full 32-B sectors) instead
+// of 32 rows x 16 B.  fp32 goes in two 16-column halves.  Up to two outputs
+// (the dual store of the ring push) share one transpose.
+template <typename TO>
+__device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, long ld2, int row0,
+                                                   int M, int n0, int N, bool vec,
+                                                   const float (&v)[32], uint8_t* stg, int lane) {
+  constexpr int kEl = 16 / (int)sizeof(TO);          // elements per 16-B chunk
+  constexpr int kPasses = sizeof(TO) == 4 ? 2 : 1;   // 64-B row slices per 32 columns
+  constexpr int kCols = 32 / kPasses;                // columns per pass
+#pragma unroll
+  for (int p = 0; p < kPasses; ++p) {
+    // write: this lane's row, 4 chunks of 16 B
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 q;
+      if constexpr (sizeof(TO) == 4) {
+        q = make_uint4(__float_as_uint(v[p * kCols + 4 * j]), __float_as_uint(v[p * kCols + 4 * j + 1]),
+                       __float_as_uint(v[p * kCols + 4 * j + 2]), __float_as_uint(v[p * kCols + 4 * j + 3]));
+      } else {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          h[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+      }
+      const int sj = j ^ ((lane >> 1) & 3);
+      *reinterpret_cast<uint4*>(stg + lane * 64 + sj * 16) = q;
+    }
+    __syncwarp();
+    // read: 8 rows x 4 chunks per instruction, 4 instructions
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = i * 8 + (lane >> 2), c = lane & 3;
+      const uint4 q = *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
+      const int row = row0 + r;
+      const int col = n0 + p * kCols + c * kEl;
+      if (row < M && col < N) {
+        if (vec && col + kEl <= N) {
+          *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
+          if (out2) *reinterpret_cast<uint4*>(out2 + (long)row * ld2 + col) = q;
+        } else {
+          const TO* e = reinterpret_cast<const TO*>(&q);
+          for (int t = 0; t < kEl && col + t < N; ++t) {
+            out[(long)row * ld + col + t] = e[t];
+            if (out2) out2[(long)row * ld2 + col + t] = e[t];
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // GEMM epilogue:
 //   v -> (+bias[n]) -> (+R[m,n]) -> [store pre-activation P] -> act (ReLU|GELU)
 //     -> ReLU mask (v·[mask>0]) | GELU gradient (v·gelu'(mask)) -> C (and C2)
@@ -159,6 +217,36 @@ struct Epilogue {
     }
     st_row32<TO>(C + (long)m * ldc + n0, vv, valid, v);
     if (C2) st_row32<TO>(C2 + (long)m * ldc2 + n0, vv, valid, v);
+  }
+  // Warp-cooperative form of finish_row32 for a 32-row x 32-column block
+  // (rows row0..row0+31, one per lane; rows >= M are computed but not stored):
+  // every store goes through warp_store_block32.
+  __device__ __forceinline__ void finish_block32(int row0, int M, int n0, float (&v)[32],
+                                                 const float (&r)[32], const float (&k)[32],
+                                                 const float* bias_s, uint8_t* stg,
+                                                 int lane) const {
+    const bool vv = vec != 0;
+    if (bias) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += bias_s[i];
+    }
+    if (res) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += r[i];
+    }
+    if (pre) warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, v, stg, lane);
+    if (act != kActNone) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i]);
+    }
+    if (mask_mode == kMaskRelu) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
+    } else if (mask_mode == kMaskGeluGrad) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(k[i]);
+    }
+    warp_store_block32<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane);
   }
 
   // 32 consecutive columns n0..n0+31 of row m (n0 % 32 == 0)
