@@ -293,6 +293,197 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// Cluster split-K (one output tile per cluster, one K slice per CTA).
+// The CS CTAs of a thread-block cluster each accumulate a K slice of the
+// same 128 x BN tile in TMEM; the partial is dumped into the CTA's own
+// (now idle) operand ring as fp32 [128][BN] (16-B chunks XOR-swizzled by
+// row), the cluster synchronises once, and CTA r reduces rows
+// [r·R, r·R + R) over all CS partials through distributed shared memory in
+// fixed rank order (deterministic) and stores them with coalesced 16-B
+// vectors.  Replaces the fp32 HBM workspace + splitk_reduce pass for the
+// weight-gradient GEMMs (long K = tokens, small M x N).  Plain epilogue.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+  return v;
+}
+
+template <typename TO, bool A_K, bool B_K, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
+                       const __grid_constant__ CUtensorMap map_b, int M, int N, int K, int mt,
+                       int kps, TO* __restrict__ C, long ldc, int vec) {
+  using L = Smem<BN>;
+  constexpr int S = L::STAGES;
+  static_assert(S * L::STAGE >= BM * BN * 4, "reduction buffer must fit in the operand ring");
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGE + L::EPI + L::STG);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
+  float* red = reinterpret_cast<float*>(smem);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int CS = (int)cluster_nctarank(), rank = (int)cluster_ctarank();
+  const int tile = blockIdx.x / CS;
+  const int m0 = (tile % mt) * BM, n0 = (tile / mt) * BN;
+  const int kbeg = rank * kps, kend = min(K, kbeg + kps);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  constexpr uint32_t kCols = BN < 32 ? 32 : BN;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int kb = 0;
+      for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb) {
+        const int st = kb % S;
+        mbar_wait(&empty[st], ((kb / S) & 1) ^ 1);
+        uint8_t* sa = smem + st * L::STAGE;
+        uint8_t* sb = sa + L::A_BYTES;
+        mbar_expect_tx(&full[st], L::A_BYTES + (B_K ? BN * BK * 2 : L::B_BYTES));
+        if (A_K) {
+          tma_load_2d(&map_a, &full[st], sa, k0, m0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < BM / 64; ++i)
+            tma_load_2d(&map_a, &full[st], sa + i * 8192, m0 + 64 * i, k0);
+        }
+        if (B_K) {
+          tma_load_2d(&map_b, &full[st], sb, k0, n0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < (BN + 63) / 64; ++i)
+            tma_load_2d(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_K ? 0u : 1u) << 15) |
+                           ((B_K ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    if (lane == 0) {
+      int kb = 0, first = 1;
+      for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb) {
+        const int st = kb % S;
+        mbar_wait(&full[st], (kb / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(smem + st * L::STAGE);
+        const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = A_K ? make_desc(sa + k * 32, 16, 1024)
+                                  : make_desc(sa + k * 2048, 8192, 1024);
+          const uint64_t bd = B_K ? make_desc(sb + k * 32, 16, 1024)
+                                  : make_desc(sb + k * 2048, 8192, 1024);
+          mma_bf16(tmem, ad, bd, idesc, first ? 0u : 1u);
+          first = 0;
+        }
+        mma_commit(&empty[st]);
+      }
+      mma_commit(&tfull[0]);
+    }
+    __syncwarp();
+  } else {
+    // all MMAs retired => every operand slot has been consumed: the ring is
+    // free and becomes this CTA's fp32 partial tile
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    mbar_wait(&tfull[0], 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int r = q * 32 + lane;
+    float* row = red + (long)r * BN;
+#pragma unroll 1
+    for (int c = 32 * half; c < BN; c += 64) {
+      uint32_t v[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int ch = (c >> 2) + j;                       // 16-B chunk index in the row
+        const int sw = (ch & ~7) | ((ch ^ r) & 7);
+        *reinterpret_cast<uint4*>(row + 4 * sw) = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  // ---- distributed reduction: this CTA owns rows [rank·R, rank·R + R) ----
+  {
+    const int R = (BM + CS - 1) / CS;
+    const int r0 = rank * R, r1 = min(BM, r0 + R);
+    constexpr int C4 = BN / 4;
+    const uint32_t red_addr = smem_u32(red);
+    for (int idx = threadIdx.x; idx < (r1 - r0) * C4; idx += kThreads) {
+      const int r = r0 + idx / C4, ch = idx % C4;
+      const int sw = (ch & ~7) | ((ch ^ r) & 7);
+      const uint32_t a = red_addr + (uint32_t)((r * BN + 4 * sw) * 4);
+      float4 acc = ld_dsmem_f4(a, 0);
+      for (int src = 1; src < CS; ++src) {
+        const float4 t = ld_dsmem_f4(a, (uint32_t)src);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      const int grow = m0 + r, gcol = n0 + 4 * ch;
+      if (grow < M && gcol < N) {
+        TO* dst = C + (long)grow * ldc + gcol;
+        const float e[4] = {acc.x, acc.y, acc.z, acc.w};
+        if (vec && gcol + 4 <= N) {
+          if constexpr (sizeof(TO) == 4) {
+            *reinterpret_cast<float4*>(dst) = acc;
+          } else {
+            __nv_bfloat162 h[2] = {__floats2bfloat162_rn(acc.x, acc.y), __floats2bfloat162_rn(acc.z, acc.w)};
+            *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<uint2*>(h);
+          }
+        } else {
+          for (int t = 0; t < 4 && gcol + t < N; ++t) DT<TO>::st(dst + t, e[t]);
+        }
+      }
+    }
+  }
+  cluster_sync_all();   // peers may still be reading this CTA's partial until here
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -354,6 +545,98 @@ static int dispatch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int
   }
 }
 
+
+// ---- cluster split-K launcher ----------------------------------------------
+template <typename TO, bool A_K, bool B_K, int BN>
+static cudaLaunchConfig_t cluster_cfg(int grid, int cs, cudaStream_t s, cudaLaunchAttribute* at) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Smem<BN>::TOTAL;
+  cfg.stream = s;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+template <typename TO, bool A_K, bool B_K, int BN>
+static bool cluster_attr_init() {
+  static bool done = false, ok = false;
+  if (!done) {
+    done = true;
+    ok = cudaFuncSetAttribute(gemm_tc_cluster_kernel<TO, A_K, B_K, BN>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL) ==
+         cudaSuccess;
+  }
+  return ok;
+}
+// how many clusters of `cs` CTAs fit on the GPU at once (GPC packing), cached
+template <typename TO, bool A_K, bool B_K, int BN>
+static int cluster_capacity(int cs) {
+  static int cap[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  if (cs < 1 || cs > 8) return 0;
+  if (cap[cs] < 0) {
+    cap[cs] = 0;
+    if (cluster_attr_init<TO, A_K, B_K, BN>()) {
+      cudaLaunchAttribute at[1];
+      cudaLaunchConfig_t cfg = cluster_cfg<TO, A_K, B_K, BN>(cs * kNumSMs, cs, 0, at);
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_cluster_kernel<TO, A_K, B_K, BN>, &cfg) ==
+          cudaSuccess)
+        cap[cs] = n;
+      else
+        cudaGetLastError();
+    }
+  }
+  return cap[cs];
+}
+template <typename TO, bool A_K, bool B_K, int BN>
+static int run_cluster(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int mt,
+                       int tiles, int cs, int kps, TO* C, long ldc, int vec, cudaStream_t s) {
+  if (!cluster_attr_init<TO, A_K, B_K, BN>()) {
+    set_error("gemm_tc_cluster_kernel: smem attribute");
+    return PPLL_ERR_CUDA;
+  }
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = cluster_cfg<TO, A_K, B_K, BN>(tiles * cs, cs, s, at);
+  PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_cluster_kernel<TO, A_K, B_K, BN>, ma, mb, M, N,
+                                     K, mt, kps, C, ldc, vec));
+  note_launch();
+  return PPLL_OK;
+}
+template <typename TO, bool A_K, bool B_K>
+static int cluster_capacity_bn(int bn, int cs) {
+  switch (bn) {
+    case 256: return cluster_capacity<TO, A_K, B_K, 256>(cs);
+    case 128: return cluster_capacity<TO, A_K, B_K, 128>(cs);
+    default: return cluster_capacity<TO, A_K, B_K, 64>(cs);
+  }
+}
+template <typename TO, bool A_K, bool B_K>
+static int dispatch_cluster(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
+                            int K, int mt, int tiles, int cs, int kps, TO* C, long ldc, int vec,
+                            cudaStream_t s) {
+  switch (bn) {
+    case 256: return run_cluster<TO, A_K, B_K, 256>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
+    case 128: return run_cluster<TO, A_K, B_K, 128>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
+    default: return run_cluster<TO, A_K, B_K, 64>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
+  }
+}
+template <typename TO>
+static int capacity_any(bool ak, bool bk, int bn, int cs) {
+  if (ak && !bk) return cluster_capacity_bn<TO, true, false>(bn, cs);
+  if (ak && bk) return cluster_capacity_bn<TO, true, true>(bn, cs);
+  if (!ak && !bk) return cluster_capacity_bn<TO, false, false>(bn, cs);
+  return cluster_capacity_bn<TO, false, true>(bn, cs);
+}
+
+// per-k-block (BK=64) mainloop cycles of a 128 x c tile: max(tensor floor,
+// operand bytes (A 4 KB + B c·32 B per K=16) streamed L2 -> smem at ~80 B/cycle/SM)
+static inline double kblock_cycles(int c) { return 4.0 * fmax(c / 2.0, (4096.0 + 32.0 * c) / 80.0); }
+
 }  // namespace tc
 
 template <typename TO>
@@ -400,11 +683,42 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
     if (sp > 1) cost += (double)(sp + 1) * M * N * 4 / 5e12 + 2e-6;
     if (best < 0 || cost < best) { best = cost; bn = c; splits = sp; }
   }
+  // Cluster split-K (plain epilogue only): one tile per cluster of cs CTAs,
+  // partials reduced through DSMEM.  Cost: waves over the GPC-packed cluster
+  // capacity x (K/cs mainloop + partial dump + distributed reduction).
+  static const int force_cl = getenv("PPLL_GEMM_CLUSTER") ? atoi(getenv("PPLL_GEMM_CLUSTER")) : -1;
+  const bool plain = !ep.bias && ep.act == kActNone && ep.mask_mode == kMaskNone && !ep.res &&
+                     !ep.pre && !ep.C2;
+  int cl_bn = 0, cl_cs = 0;
+  if (plain && force_cl != 0 && K >= 8 * BK) {
+    double cl_best = -1;
+    const int cb[3] = {256, 128, 64};
+    for (int i = 0; i < 3; ++i) {
+      const int c = cb[i];
+      if (c > 64 && N <= c / 2) continue;
+      const long tiles = (long)mt * ceil_div(N, c);
+      for (int cs = 2; cs <= 8; ++cs) {
+        if (K < cs * 4 * BK) break;
+        const int cap = capacity_any<TO>(a_kmajor, b_kmajor, c, cs);
+        if (cap <= 0) continue;
+        const double waves = (double)((tiles + cap - 1) / cap);
+        const double kb = (double)ceil_div(K, cs * BK);
+        const double t_red = 128.0 * c * 4 / 64.0 + 128.0 * c * 4 / 128.0;   // cycles
+        const double cost = waves * ((kb * kblock_cycles(c) + t_red) / 1.9e9 + 1.5e-6);
+        if (cl_best < 0 || cost < cl_best) { cl_best = cost; cl_bn = c; cl_cs = cs; }
+      }
+    }
+    if (cl_bn && (force_cl == 1 || cl_best < best)) {
+      bn = cl_bn;
+    } else {
+      cl_bn = 0;
+    }
+  }
   Sched sc;
   sc.mt = mt;
   sc.nt = ceil_div(N, bn);
   sc.tiles = sc.mt * sc.nt;
-  sc.kps = ceil_div(ceil_div(K, splits), BK) * BK;
+  sc.kps = ceil_div(ceil_div(K, cl_bn ? cl_cs : splits), BK) * BK;
   sc.splits = ceil_div(K, sc.kps);
   sc.items = sc.tiles * sc.splits;
   static const int probe = getenv("PPLL_GEMM_PROBE") ? atoi(getenv("PPLL_GEMM_PROBE")) : 0;
@@ -413,6 +727,17 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   bool ok = a_kmajor ? make_map(&ma, A, K, M, lda, BM) : make_map(&ma, A, M, K, lda, 64);
   ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, bn) : make_map(&mb, B, N, K, ldb, 64));
   if (!ok) return PPLL_ERR_UNSUPPORTED;
+  if (cl_bn) {
+    const int cs = sc.splits;   // every CTA of the cluster owns >= 1 k-block
+    Epilogue<TO> e = ep;
+    if (a_kmajor && !b_kmajor)
+      return dispatch_cluster<TO, true, false>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
+    if (a_kmajor && b_kmajor)
+      return dispatch_cluster<TO, true, true>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
+    if (!a_kmajor && !b_kmajor)
+      return dispatch_cluster<TO, false, false>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
+    return dispatch_cluster<TO, false, true>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
+  }
   Epilogue<TO> e = ep;
   e.partial = nullptr;
   float* part = sc.splits > 1 ? ws : nullptr;

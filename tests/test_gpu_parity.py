@@ -372,7 +372,9 @@ def test_native_kernels_were_launched():
 # --- the tcgen05 engine specifically ---------------------------------------------
 
 TC_SHAPES = [(128, 64, 64), (128, 3072, 1024), (256, 384, 1152), (100, 200, 96),
-             (8320, 384, 1536), (130, 1024, 264), (1024, 1024, 1024)]
+             (8320, 384, 1536), (130, 1024, 264), (1024, 1024, 1024),
+             # long reductions: the weight gradient takes the cluster split-K path
+             (8320, 1536, 384), (3000, 136, 72), (4736, 768, 3072)]
 
 
 @pytest.mark.parametrize("M,K,Nn", TC_SHAPES)
@@ -383,3 +385,24 @@ def test_tcgen05_engine_matches_torch(M, K, Nn):
         test_linear_ops_match_torch_fp32("bf16", M, K, Nn)
     finally:
         lib.ppll_set_gemm_engine(N.GEMM_AUTO)
+
+
+@pytest.mark.parametrize("M,K,Nn", [(8320, 384, 1536), (3000, 136, 72), (131072, 144, 16)])
+def test_wgrad_split_reduction_is_deterministic(M, K, Nn):
+    """Split-K weight gradients (cluster DSMEM or workspace reduction) sum the
+    K slices in a fixed order: two runs are bitwise identical."""
+    g = torch.Generator(device="cuda").manual_seed(M + K + Nn)
+    X = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    dY = torch.randn(M, Nn, device="cuda", generator=g).bfloat16()
+    lib = N.load()
+    s = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for _ in range(2):
+        dW = torch.full((K, Nn), float("nan"), device="cuda")
+        N.check(lib.ppll_linear_wgrad(M, K, Nn, X.data_ptr(), K, dY.data_ptr(), Nn,
+                                      dW.data_ptr(), None, N.BF16, s), "wgrad")
+        outs.append(dW)
+    torch.cuda.synchronize()
+    ref = X.double().T @ dY.double()
+    assert torch.equal(outs[0], outs[1])
+    assert (outs[0].double() - ref).abs().max().item() / ref.abs().max().item() < 1e-2
