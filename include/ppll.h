@@ -78,6 +78,21 @@ int ppll_linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void*
 int ppll_linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY,
                       int lddy, float* dW, float* db, int dtype, void* stream);
 
+/* Extended fused epilogues (the transformer-layer forms; same engines):
+ *   fwd:   Y = act(X·W + b [+ R]);  act 0 none, 1 ReLU, 2 GELU(erf),
+ *          3 GELU with P <- gelu'(pre-activation);  for act 0..2 P (optional)
+ *          receives the pre-activation.  Y2 (optional) is an identical copy.
+ *   dgrad: dX = (dY·Wᵀ) ∘ f(mask);  mask_mode 1 [mask>0], 2 gelu'(mask),
+ *          3 mask (a stored derivative).
+ * Replace the same tensor.py:137-180 ops plus the extension families' GELU /
+ * residual fusions (no reference counterpart). */
+int ppll_linear_fwd_ex(int M, int K, int N, const void* X, int ldx, const void* W,
+                       const float* b, const void* R, int ldr, int act, void* P, int ldp,
+                       void* Y, int ldy, void* Y2, int ldy2, int dtype, void* stream);
+int ppll_linear_dgrad_ex(int M, int K, int N, const void* dY, int lddy, const void* W,
+                         const void* mask, int ldmask, int mask_mode, void* dX, int lddx,
+                         int dtype, void* stream);
+
 /* Fused mean softmax cross-entropy forward + adjoint (tensor.py:201-234):
  * loss = mean_b −log softmax(z_b)[y_b] (max-subtracted), dz = (softmax −
  * onehot)/B.  The scalar loss is written to loss_hist[*step] (step may be

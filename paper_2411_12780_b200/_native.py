@@ -28,6 +28,9 @@ SIGNATURES = {
     "ppll_set_gemm_engine": (None, [_i]),
     "ppll_set_attn_engine": (None, [_i]),
     "ppll_linear_fwd": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _vp]),
+    "ppll_linear_fwd_ex": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _i, _vp, _i,
+                                _vp, _i, _i, _vp]),
+    "ppll_linear_dgrad_ex": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _i, _i, _vp, _i, _i, _vp]),
     "ppll_linear_dgrad": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _i, _i, _vp]),
     "ppll_linear_wgrad": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _i, _vp]),
     "ppll_softmax_xent": (_i, [_i, _i, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp]),

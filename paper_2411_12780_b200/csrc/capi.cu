@@ -142,6 +142,28 @@ int ppll_linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void*
   return linear_dgrad(M, K, N, dY, lddy, W, mask, ldmask, dX, lddx, dtype, nullptr, 0, S(stream));
 }
 
+int ppll_linear_fwd_ex(int M, int K, int N, const void* X, int ldx, const void* W,
+                       const float* b, const void* R, int ldr, int act, void* P, int ldp,
+                       void* Y, int ldy, void* Y2, int ldy2, int dtype, void* stream) {
+  if (act < kActNone || act > kActGeluD) { set_error("linear_fwd_ex: bad act %d", act); return PPLL_ERR_ARG; }
+  LinOpts o;
+  o.bias = b; o.res = R; o.ldres = ldr; o.act = act; o.pre = P; o.ldpre = ldp;
+  o.C2 = Y2; o.ldc2 = ldy2;
+  return gemm_fwd(M, K, N, X, ldx, W, o, Y, ldy, dtype, nullptr, 0, S(stream));
+}
+
+int ppll_linear_dgrad_ex(int M, int K, int N, const void* dY, int lddy, const void* W,
+                         const void* mask, int ldmask, int mask_mode, void* dX, int lddx,
+                         int dtype, void* stream) {
+  if (mask_mode < kMaskNone || mask_mode > kMaskMul || (mask_mode != kMaskNone && !mask)) {
+    set_error("linear_dgrad_ex: bad mask mode %d", mask_mode);
+    return PPLL_ERR_ARG;
+  }
+  LinOpts o;
+  o.mask = mask; o.ldmask = ldmask; o.mask_mode = mask ? mask_mode : kMaskNone;
+  return gemm_dgrad(M, K, N, dY, lddy, W, o, dX, lddx, dtype, nullptr, 0, S(stream));
+}
+
 int ppll_linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, int lddy,
                       float* dW, float* db, int dtype, void* stream) {
   return linear_wgrad(M, K, N, X, ldx, dY, lddy, dW, db, dtype, nullptr, 0, S(stream));

@@ -6,16 +6,99 @@ namespace ppll {
 
 void note_launch(int n = 1);
 
-enum Act : int { kActNone = 0, kActRelu = 1, kActGelu = 2 };
-enum MaskMode : int { kMaskNone = 0, kMaskRelu = 1, kMaskGeluGrad = 2 };
+// kActGeluD: GELU whose `pre` output receives gelu'(pre-activation) instead of
+// the pre-activation itself, so the backward multiplies (kMaskMul) instead of
+// re-evaluating erf/exp in the dgrad epilogue.
+enum Act : int { kActNone = 0, kActRelu = 1, kActGelu = 2, kActGeluD = 3 };
+enum MaskMode : int { kMaskNone = 0, kMaskRelu = 1, kMaskGeluGrad = 2, kMaskMul = 3 };
 
+// Exact-erf GELU and its derivative sharing one exponential:
+//   erf(z) = 1 - t·P(t)·e^{-z²}, t = 1/(1 + p|z|)   (Abramowitz-Stegun 7.1.26,
+//   |error| <= 1.5e-7, i.e. fp32-level for the GELU),  z = x/√2,
+//   gelu = x·Φ(x),  gelu' = Φ(x) + x·φ(x),  φ(x) = e^{-z²}/√(2π).
+// Two MUFU ops (rcp, ex2; approx.ftz: ~1 ulp, no range fix-ups) + 13 FP ops.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void gelu_both(float x, float& g, float& d) {
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x), 1.f));
+  float p = fmaf(t, 1.061405429f, -1.453152027f);
+  p = fmaf(t, p, 1.421413741f);
+  p = fmaf(t, p, -0.284496736f);
+  p = fmaf(t, p, 0.254829592f);
+  p *= t;
+  const float e = ex2_approx(x * x * -0.72134752044448170f);   // e^{-x²/2}
+  const float h = 0.5f * fmaf(-p, e, 1.f);                       // erf(|z|)/2
+  const float cdf = x >= 0.f ? 0.5f + h : 0.5f - h;
+  g = x * cdf;
+  d = fmaf(x, 0.3989422804014327f * e, cdf);
+}
+
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: two lanes per
+// instruction) for the epilogue's per-element math.
+struct f2 { float x, y; };
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+  f2 r;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 r;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ f2 splat2(float c) { return f2{c, c}; }
+// gelu_both on two elements: the polynomial and the products run packed,
+// rcp / ex2 stay scalar MUFU ops.
+__device__ __forceinline__ void gelu_both2(float& x0, float& x1, float& d0, float& d1) {
+  const f2 x{x0, x1};
+  const f2 ax{fabsf(x0), fabsf(x1)};
+  const f2 den = ffma2(splat2(0.3275911f * 0.70710678118654752f), ax, splat2(1.f));
+  const f2 t{rcp_approx(den.x), rcp_approx(den.y)};
+  f2 p = ffma2(t, splat2(1.061405429f), splat2(-1.453152027f));
+  p = ffma2(t, p, splat2(1.421413741f));
+  p = ffma2(t, p, splat2(-0.284496736f));
+  p = ffma2(t, p, splat2(0.254829592f));
+  p = fmul2(p, t);
+  const f2 q = fmul2(fmul2(x, x), splat2(-0.72134752044448170f));
+  const f2 e{ex2_approx(q.x), ex2_approx(q.y)};
+  const f2 h = ffma2(fmul2(p, e), splat2(-0.5f), splat2(0.5f));      // erf(|z|)/2
+  const f2 hs{copysignf(h.x, x0), copysignf(h.y, x1)};
+  const f2 cdf = fadd2(hs, splat2(0.5f));
+  const f2 g = fmul2(x, cdf);
+  const f2 d = ffma2(x, fmul2(e, splat2(0.3989422804014327f)), cdf);
+  x0 = g.x; x1 = g.y; d0 = d.x; d1 = d.y;
+}
 __device__ __forceinline__ float gelu_f(float x) {        // exact (erf) GELU
-  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+  float g, d;
+  gelu_both(x, g, d);
+  return g;
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {   // d/dx gelu(x)
-  const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
-  const float pdf = 0.3989422804014327f * __expf(-0.5f * x * x);
-  return cdf + x * pdf;
+  float g, d;
+  gelu_both(x, g, d);
+  return d;
 }
 
 template <typename T>
@@ -146,7 +229,8 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
 
 // GEMM epilogue:
 //   v -> (+bias[n]) -> (+R[m,n]) -> [store pre-activation P] -> act (ReLU|GELU)
-//     -> ReLU mask (v·[mask>0]) | GELU gradient (v·gelu'(mask)) -> C (and C2)
+//     -> ReLU mask (v·[mask>0]) | GELU gradient (v·gelu'(mask)) | v·mask -> C (and C2)
+//   (act GeluD: P receives gelu'(pre-activation) instead)
 // `vec` = every pointer 16-B aligned and every leading dimension a multiple of
 // 16 B, so 32-column row segments move as 16-B vectors.
 template <typename TO>
@@ -170,16 +254,17 @@ struct Epilogue {
 
   __device__ __forceinline__ float act_f(float v) const {
     if (act == kActRelu) return fmaxf(v, 0.f);
-    if (act == kActGelu) return gelu_f(v);
+    if (act == kActGelu || act == kActGeluD) return gelu_f(v);
     return v;
   }
   __device__ __forceinline__ void apply(int m, int n, float v) const {
     if (bias) v += bias[n];
     if (res) v += to_f(res[(long)m * ldres + n]);
-    if (pre) DT<TO>::st(pre + (long)m * ldpre + n, v);
+    if (pre) DT<TO>::st(pre + (long)m * ldpre + n, act == kActGeluD ? gelu_grad_f(v) : v);
     v = act_f(v);
     if (mask_mode == kMaskRelu) v = (to_f(mask[(long)m * ldmask + n]) > 0.f) ? v : 0.f;
     else if (mask_mode == kMaskGeluGrad) v *= gelu_grad_f(to_f(mask[(long)m * ldmask + n]));
+    else if (mask_mode == kMaskMul) v *= to_f(mask[(long)m * ldmask + n]);
     DT<TO>::st(C + (long)m * ldc + n, v);
     if (C2) DT<TO>::st(C2 + (long)m * ldc2 + n, v);
   }
@@ -191,61 +276,68 @@ struct Epilogue {
     if (res) ld_row32<TO>(res + (long)m * ldres + n0, vec != 0, valid, r);
     if (mask_mode != kMaskNone) ld_row32<TO>(mask + (long)m * ldmask + n0, vec != 0, valid, k);
   }
-  __device__ __forceinline__ void finish_row32(int m, int n0, float (&v)[32], const float (&r)[32],
-                                               const float (&k)[32], const float* bias_s) const {
-    const int valid = min(32, ncols - n0);
-    const bool vv = vec != 0;
-    if (bias) {
+  // activation (with the GeluD derivative written into d) and mask, in place
+  // activation (with the GeluD derivative written into d) and mask, in place.
+  // One GELU evaluation per element: on v (act GELU/GeluD) or on the mask
+  // (GELU-gradient mask); the two are never combined (host-checked).
+  __device__ __forceinline__ void act_mask32(float (&v)[32], const float (&k)[32],
+                                             float (&d)[32]) const {
+    const bool ga = act == kActGelu || act == kActGeluD;
+    if (ga) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += bias_s[i];
-    }
-    if (res) {
+      for (int i = 0; i < 32; i += 2) gelu_both2(v[i], v[i + 1], d[i], d[i + 1]);
+    } else if (mask_mode == kMaskGeluGrad) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += r[i];
-    }
-    if (pre) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, v);
-    if (act != kActNone) {
+      for (int i = 0; i < 32; i += 2) {
+        float g0 = k[i], g1 = k[i + 1];
+        gelu_both2(g0, g1, d[i], d[i + 1]);
+        const f2 r = fmul2(f2{v[i], v[i + 1]}, f2{d[i], d[i + 1]});
+        v[i] = r.x; v[i + 1] = r.y;
+      }
+    } else if (act == kActRelu) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i]);
+      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
     }
     if (mask_mode == kMaskRelu) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
-    } else if (mask_mode == kMaskGeluGrad) {
+    } else if (mask_mode == kMaskMul) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(k[i]);
+      for (int i = 0; i < 32; i += 2) {
+        const f2 r = fmul2(f2{v[i], v[i + 1]}, f2{k[i], k[i + 1]});
+        v[i] = r.x; v[i + 1] = r.y;
+      }
     }
-    st_row32<TO>(C + (long)m * ldc + n0, vv, valid, v);
-    if (C2) st_row32<TO>(C2 + (long)m * ldc2 + n0, vv, valid, v);
   }
-  // Warp-cooperative form of finish_row32 for a 32-row x 32-column block
-  // (rows row0..row0+31, one per lane; rows >= M are computed but not stored):
-  // every store goes through warp_store_block32.
+  // Warp-cooperative epilogue of a 32-row x 32-column block (rows
+  // row0..row0+31, one per lane; rows >= M are computed but not stored):
+  // every store goes through warp_store_block32.  `r` (the residual) is dead
+  // after the add and is reused for the GeluD derivative.
   __device__ __forceinline__ void finish_block32(int row0, int M, int n0, float (&v)[32],
-                                                 const float (&r)[32], const float (&k)[32],
+                                                 float (&r)[32], const float (&k)[32],
                                                  const float* bias_s, uint8_t* stg,
                                                  int lane) const {
     const bool vv = vec != 0;
     if (bias) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += bias_s[i];
+      for (int i = 0; i < 32; i += 2) {
+        const float2 bb = *reinterpret_cast<const float2*>(bias_s + i);
+        const f2 t = fadd2(f2{v[i], v[i + 1]}, f2{bb.x, bb.y});
+        v[i] = t.x; v[i + 1] = t.y;
+      }
     }
     if (res) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += r[i];
+      for (int i = 0; i < 32; i += 2) {
+        const f2 t = fadd2(f2{v[i], v[i + 1]}, f2{r[i], r[i + 1]});
+        v[i] = t.x; v[i + 1] = t.y;
+      }
     }
-    if (pre) warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, v, stg, lane);
-    if (act != kActNone) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i]);
-    }
-    if (mask_mode == kMaskRelu) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
-    } else if (mask_mode == kMaskGeluGrad) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(k[i]);
-    }
+    if (pre && act != kActGeluD)
+      warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, v, stg, lane);
+    act_mask32(v, k, r);
+    if (pre && act == kActGeluD)
+      warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg, lane);
     warp_store_block32<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane);
   }
 
@@ -263,22 +355,11 @@ struct Epilogue {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] += r[i];
     }
-    if (pre) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, v);
-    if (act != kActNone) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i]);
-    }
-    if (mask_mode != kMaskNone) {
-      float k[32];
-      ld_row32<TO>(mask + (long)m * ldmask + n0, vv, valid, k);
-      if (mask_mode == kMaskRelu) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(k[i]);
-      }
-    }
+    if (pre && act != kActGeluD) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, v);
+    float k[32], d[32];
+    if (mask_mode != kMaskNone) ld_row32<TO>(mask + (long)m * ldmask + n0, vv, valid, k);
+    act_mask32(v, k, d);
+    if (pre && act == kActGeluD) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, d);
     st_row32<TO>(C + (long)m * ldc + n0, vv, valid, v);
     if (C2) st_row32<TO>(C2 + (long)m * ldc2 + n0, vv, valid, v);
   }

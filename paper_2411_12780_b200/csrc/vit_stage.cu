@@ -149,7 +149,7 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     if (r) return r;
     LinOpts o3;
     o3.bias = st->P(st->po(l, kB1));
-    o3.act = kActGelu;
+    o3.act = kActGeluD;   // b.u <- gelu'(pre-activation)
     o3.pre = b.u;
     o3.ldpre = F;
     r = gemm_fwd(M, D, F, b.xn2, D, st->W(st->po(l, kW1)), o3, b.h, F, st->dtype, st->ws,
@@ -227,7 +227,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     LinOpts og;
     og.mask = b.u;
     og.ldmask = F;
-    og.mask_mode = kMaskGeluGrad;
+    og.mask_mode = kMaskMul;
     r = gemm_dgrad(M, F, D, dx2, D, st->W(st->po(l, kW2)), og, st->dbig, F, st->dtype, st->ws,
                    st->ws_elems, s);
     if (r) return r;

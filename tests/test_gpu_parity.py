@@ -406,3 +406,54 @@ def test_wgrad_split_reduction_is_deterministic(M, K, Nn):
     ref = X.double().T @ dY.double()
     assert torch.equal(outs[0], outs[1])
     assert (outs[0].double() - ref).abs().max().item() / ref.abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("engine", ["tcgen05", "simt"])
+@pytest.mark.parametrize("M,K,Nn", [(1040, 384, 1536), (200, 96, 136)])
+def test_gelu_epilogues_match_torch(engine, M, K, Nn):
+    """Transformer-layer epilogues: residual, GELU(erf), pre-activation /
+    GELU-derivative stores, GELU-gradient and stored-derivative masks."""
+    g = torch.Generator(device="cuda").manual_seed(M + Nn)
+    X = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(K, Nn, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    b = torch.randn(Nn, device="cuda", generator=g)
+    R = torch.randn(M, Nn, device="cuda", generator=g).bfloat16()
+    dY = torch.randn(M, Nn, device="cuda", generator=g).bfloat16()
+    Mk = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    lib = N.load()
+    lib.ppll_set_gemm_engine(N.GEMM_TCGEN05 if engine == "tcgen05" else N.GEMM_SIMT)
+    s = torch.cuda.current_stream().cuda_stream
+    try:
+        outs = {}
+        for act in (2, 3):
+            Y = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+            P = torch.empty_like(Y)
+            N.check(lib.ppll_linear_fwd_ex(M, K, Nn, X.data_ptr(), K, W.data_ptr(), b.data_ptr(),
+                                           R.data_ptr(), Nn, act, P.data_ptr(), Nn, Y.data_ptr(),
+                                           Nn, None, 0, N.BF16, s), "fwd_ex")
+            outs[act] = (Y, P)
+        dX = {}
+        for mode in (2, 3):
+            d = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
+            N.check(lib.ppll_linear_dgrad_ex(M, K, Nn, dY.data_ptr(), Nn, W.data_ptr(),
+                                             Mk.data_ptr(), K, mode, d.data_ptr(), K, N.BF16, s),
+                    "dgrad_ex")
+            dX[mode] = d
+        torch.cuda.synchronize()
+    finally:
+        lib.ppll_set_gemm_engine(N.GEMM_AUTO)
+    u = X.double() @ W.double() + b.double() + R.double()
+    gelu = torch.nn.functional.gelu(u)
+    cdf = 0.5 * (1 + torch.erf(u / 2 ** 0.5))
+    dgelu = cdf + u * torch.exp(-0.5 * u * u) / (2 * torch.pi) ** 0.5
+
+    def rel(a, r):
+        return (a.double() - r).abs().max().item() / (r.abs().max().item() + 1e-12)
+
+    assert rel(outs[2][0], gelu) < 1e-2 and rel(outs[2][1], u) < 1e-2
+    assert rel(outs[3][0], gelu) < 1e-2 and rel(outs[3][1], dgelu) < 1e-2
+    mk = Mk.double()
+    dmk = 0.5 * (1 + torch.erf(mk / 2 ** 0.5)) + mk * torch.exp(-0.5 * mk * mk) / (2 * torch.pi) ** 0.5
+    base = dY.double() @ W.double().T
+    assert rel(dX[2], base * dmk) < 1e-2
+    assert rel(dX[3], base * mk) < 1e-2

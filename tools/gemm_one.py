@@ -1,6 +1,8 @@
 """Run one linear-layer GEMM shape through the C-ABI (for ncu captures / probes).
 
-usage: python tools/gemm_one.py M K N [fwd|dgrad|wgrad] [iters]
+usage: python tools/gemm_one.py M K N [fwd|fwdgelu|dgrad|dgradmul|wgrad] [iters]
+  fwdgelu : bias + GELU, gelu'(pre-activation) stored (the ViT FC1 forward)
+  dgradmul: dX = (dY·Wᵀ) ∘ mask (the ViT FC2 dgrad with the stored derivative)
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -22,6 +24,15 @@ dW = torch.empty(K, Nn, device="cuda")
 if op == "fwd":
     fn = lambda: lib.ppll_linear_fwd(M, K, Nn, X.data_ptr(), K, W.data_ptr(), b.data_ptr(),
                                      Y.data_ptr(), Nn, None, 0, 1, N.BF16, s)
+elif op == "fwdgelu":
+    P = torch.empty_like(Y)
+    fn = lambda: lib.ppll_linear_fwd_ex(M, K, Nn, X.data_ptr(), K, W.data_ptr(), b.data_ptr(),
+                                        None, 0, 3, P.data_ptr(), Nn, Y.data_ptr(), Nn, None, 0,
+                                        N.BF16, s)
+elif op == "dgradmul":
+    Mk = torch.rand(M, K, device="cuda").bfloat16()
+    fn = lambda: lib.ppll_linear_dgrad_ex(M, K, Nn, dY.data_ptr(), Nn, W.data_ptr(),
+                                          Mk.data_ptr(), K, 3, dX.data_ptr(), K, N.BF16, s)
 elif op == "dgrad":
     fn = lambda: lib.ppll_linear_dgrad(M, K, Nn, dY.data_ptr(), Nn, W.data_ptr(), None, 0,
                                        dX.data_ptr(), K, N.BF16, s)

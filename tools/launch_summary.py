@@ -2,6 +2,7 @@
 import collections, csv, sys
 
 def main(path, top=25):
+    top = int(top)
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
