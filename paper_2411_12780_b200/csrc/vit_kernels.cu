@@ -104,16 +104,40 @@ ln_fwd_vkernel(int M, const T* __restrict__ x, long ldx, const float* __restrict
 }
 
 // backward; per-block column partials part[block][NS][D] with NS = 2 (dgamma,
-// dbeta) or 3 (+ Σ rows of the dx output: the next bias gradient, fused)
-template <typename T, int EPL, int NS>
-__global__ void __launch_bounds__(256)
-ln_bwd_vkernel(int M, const T* __restrict__ dy, long lddy, const T* __restrict__ x, long ldx,
-               const float* __restrict__ mean, const float* __restrict__ rstd,
-               const float* __restrict__ g, const T* __restrict__ dres, long ldres,
-               T* __restrict__ dx, long lddx, float* __restrict__ part, int rows_per_block) {
-  constexpr int D = 16 * EPL;
+// dbeta) or 3 (+ Σ rows of the dx output: the next bias gradient, fused).
+// Persistent (one 256-thread block per SM, half-warp per row, rows strided by
+// the grid) and software-pipelined: the next row's dy / x / residual vectors
+// are in flight while the current row is reduced, so every SM keeps ~32 rows
+// (~70 KB) of loads outstanding.
+template <int N>
+__device__ __forceinline__ void ldq(const __nv_bfloat16* p, uint4 (&q)[N / 8]) {
+#pragma unroll
+  for (int i = 0; i < N / 8; ++i) q[i] = reinterpret_cast<const uint4*>(p)[i];
+}
+template <int N>
+__device__ __forceinline__ void unq(const uint4 (&q)[N / 8], float* o) {
+#pragma unroll
+  for (int i = 0; i < N / 8; ++i) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[i]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      o[8 * i + 2 * j] = f.x;
+      o[8 * i + 2 * j + 1] = f.y;
+    }
+  }
+}
+template <int EPL, int NS, int LPR>
+__global__ void __launch_bounds__(256, 1)
+ln_bwd_vkernel(int M, const __nv_bfloat16* __restrict__ dy, long lddy,
+               const __nv_bfloat16* __restrict__ x, long ldx, const float* __restrict__ mean,
+               const float* __restrict__ rstd, const float* __restrict__ g,
+               const __nv_bfloat16* __restrict__ dres, long ldres, __nv_bfloat16* __restrict__ dx,
+               long lddx, float* __restrict__ part) {
+  // LPR lanes per row (16: two rows per warp; 32: one row per warp)
+  constexpr int D = LPR * EPL, NQ = EPL / 8, RPW = 32 / LPR, RPB = 8 * RPW;
   __shared__ float red[NS][D];
-  const int lane = threadIdx.x & 31, hl = lane & 15, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, hl = lane & (LPR - 1), w = threadIdx.x >> 5;
   const int c0 = hl * EPL;
   float gg[EPL];
   ldv<EPL>(g + c0, gg);
@@ -122,54 +146,77 @@ ln_bwd_vkernel(int M, const T* __restrict__ dy, long lddy, const T* __restrict__
   for (int k = 0; k < NS; ++k)
 #pragma unroll
     for (int i = 0; i < EPL; ++i) acc[k][i] = 0.f;
-  const int r0 = blockIdx.x * rows_per_block;
-  const int r1 = min(M, r0 + rows_per_block);
-  for (int base = r0 + 2 * w; base < r1; base += 16) {
-    const int row = base + (lane >> 4);
-    const bool live = row < r1;
-    float d[EPL], xh[EPL];
-    float mu = 0.f, rs = 0.f;
+  const int stride = gridDim.x * RPB;
+  int row = blockIdx.x * RPB + RPW * w + (LPR == 16 ? (lane >> 4) : 0);
+  uint4 qd[NQ], qx[NQ], qr[NQ];
+  float mu = 0.f, rs = 0.f;
+  if (row < M) {
+    ldq<EPL>(dy + (long)row * lddy + c0, qd);
+    ldq<EPL>(x + (long)row * ldx + c0, qx);
+    if (dres) ldq<EPL>(dres + (long)row * ldres + c0, qr);
+    mu = mean[row];
+    rs = rstd[row];
+  }
+  // every half-warp runs the same trip count (shuffles stay converged)
+  const int trips = (M + stride - 1) / stride;
+  for (int it = 0; it < trips; ++it) {
+    const bool live = row < M;
+    float d[EPL], xh[EPL], o[EPL];
     if (live) {
-      ldv<EPL>(dy + (long)row * lddy + c0, d);
-      ldv<EPL>(x + (long)row * ldx + c0, xh);
-      mu = mean[row];
-      rs = rstd[row];
+      unq<EPL>(qd, d);
+      unq<EPL>(qx, xh);
+      if (dres) unq<EPL>(qr, o);
     } else {
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) d[i] = xh[i] = 0.f;
+      for (int i = 0; i < EPL; ++i) d[i] = xh[i] = o[i] = 0.f;
+    }
+    const float cmu = mu, crs = rs;
+    const int crow = row;
+    row += stride;
+    if (row < M) {   // prefetch the next row
+      ldq<EPL>(dy + (long)row * lddy + c0, qd);
+      ldq<EPL>(x + (long)row * ldx + c0, qx);
+      if (dres) ldq<EPL>(dres + (long)row * ldres + c0, qr);
+      mu = mean[row];
+      rs = rstd[row];
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
-      xh[i] = (xh[i] - mu) * rs;
+      xh[i] = (xh[i] - cmu) * crs;
       acc[0][i] += d[i] * xh[i];
       acc[1][i] += d[i];
       const float dxh = d[i] * gg[i];
       s1 += dxh;
       s2 += dxh * xh[i];
     }
-    s1 = half_sum(s1) * (1.f / D);
-    s2 = half_sum(s2) * (1.f / D);
+    if (LPR == 16) {
+      s1 = half_sum(s1) * (1.f / D);
+      s2 = half_sum(s2) * (1.f / D);
+    } else {
+      s1 = warp_sum(s1) * (1.f / D);
+      s2 = warp_sum(s2) * (1.f / D);
+    }
     if (live) {
-      float o[EPL];
-      if (dres) ldv<EPL>(dres + (long)row * ldres + c0, o);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
-        const float t = rs * (d[i] * gg[i] - s1 - xh[i] * s2);
+        const float t = crs * (d[i] * gg[i] - s1 - xh[i] * s2);
         o[i] = dres ? o[i] + t : t;
         if (NS == 3) acc[2][i] += o[i];
       }
-      if (dx) stv<EPL>(dx + (long)row * lddx + c0, o);
+      if (dx) stv<EPL>(dx + (long)crow * lddx + c0, o);
     }
   }
   if (!part) return;
   // the two half-warps own the same columns; then warps combine in fixed order
+  if (LPR == 16) {
 #pragma unroll
-  for (int k = 0; k < NS; ++k)
+    for (int k = 0; k < NS; ++k)
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) acc[k][i] += __shfl_xor_sync(0xffffffffu, acc[k][i], 16);
+      for (int i = 0; i < EPL; ++i) acc[k][i] += __shfl_xor_sync(0xffffffffu, acc[k][i], 16);
+  }
   for (int k8 = 0; k8 < 8; ++k8) {
-    if (w == k8 && lane < 16) {
+    if (w == k8 && lane < LPR) {
 #pragma unroll
       for (int k = 0; k < NS; ++k)
 #pragma unroll
@@ -353,34 +400,45 @@ int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const floa
 }
 
 // ~2 rows per warp: enough rows in flight to cover DRAM latency, few partials
+// vector path: persistent, one block per SM (16 rows per block per trip);
+// scalar path: ~2 rows per warp
 int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : min(ceil_div(M, 16), 148 * 2); }
+static int ln_bwd_vblocks(int M, int rpb) { return min(ceil_div(M, rpb), 148); }
 
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
                   const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
                   float* part, float* dg, float* db, cudaStream_t s, float* dxsum) {
   if (D % 32 || D > 1024) { set_error("layernorm: D=%d unsupported", D); return PPLL_ERR_ARG; }
-  const int nblk = ln_bwd_blocks(M);
+  int nblk = ln_bwd_blocks(M);
   const int rpb = ceil_div(M, nblk);
-  const bool vec = D <= 512 && vec_ok<T>(D, lddy) && vec_ok<T>(D, ldx) && (!dres || vec_ok<T>(D, ldres)) &&
+  const bool vec = sizeof(T) == 2 && (D == 128 || D == 256 || D == 384 || D == 512 || D == 768) &&
+                   vec_ok<T>(D, lddy) && vec_ok<T>(D, ldx) && (!dres || vec_ok<T>(D, ldres)) &&
                    (!dx || vec_ok<T>(D, lddx)) && aligned16(dy) && aligned16(x) &&
                    (!dres || aligned16(dres)) && (!dx || aligned16(dx)) && aligned16(g);
   int NS = 2;
   if (vec) {
     NS = dxsum ? 3 : 2;
-    if (NS == 3) {
-      switch (D / 16) {
-#define LNB(E) case E: ln_bwd_vkernel<T, E, 3><<<nblk, 256, 0, s>>>(M, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb); break;
-        LNB(8) LNB(16) LNB(24) LNB(32)
-#undef LNB
-      }
-    } else {
-      switch (D / 16) {
-#define LNB(E) case E: ln_bwd_vkernel<T, E, 2><<<nblk, 256, 0, s>>>(M, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb); break;
-        LNB(8) LNB(16) LNB(24) LNB(32)
-#undef LNB
-      }
+    nblk = ln_bwd_vblocks(M, D == 768 || D == 512 ? 8 : 16);
+    using B16 = __nv_bfloat16;
+    const B16 *dyb = (const B16*)dy, *xb = (const B16*)x, *rb = (const B16*)dres;
+    B16* dxb = (B16*)dx;
+#define LNB(E, NSV, L) ln_bwd_vkernel<E, NSV, L><<<nblk, 256, 0, s>>>(M, dyb, lddy, xb, ldx, mean, rstd, g, rb, ldres, dxb, lddx, part)
+#define LNB_ALL(NSV)                          \
+    switch (D) {                              \
+      case 128: LNB(8, NSV, 16); break;       \
+      case 256: LNB(16, NSV, 16); break;      \
+      case 384: LNB(24, NSV, 16); break;      \
+      case 512: LNB(16, NSV, 32); break;      \
+      default: LNB(24, NSV, 32); break;       \
     }
+    if (NS == 3) {
+      LNB_ALL(3)
+    } else {
+      LNB_ALL(2)
+    }
+#undef LNB_ALL
+#undef LNB
   } else {
     if (dxsum && !dx) { set_error("layernorm: bias sum needs the dx output"); return PPLL_ERR_ARG; }
     if (D <= 384)
