@@ -182,18 +182,22 @@ struct Maps {
 };
 
 // ------------------------------------------------------------------ forward
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128, 4)
 attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                    int Tn, int H, int NK, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
                    float scale) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base0 = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + ((1024 - (base0 & 1023)) & 1023);
+  // ~53 KB and 128 TMEM columns so four CTAs share an SM: P's first 64-key
+  // atom overwrites Q (dead once S = Q·Kᵀ has retired), K and V hold only
+  // their NK rows, and O = P·V reuses the S columns after they are read.
+  const int kbytes = (NK * 128 + 1023) & ~1023;
   uint8_t* sQ = sm;                 // 16 KB
-  uint8_t* sK = sQ + 16384;         // NK*128 B (<= 16 KB)
-  uint8_t* sV = sK + 16384;
-  uint8_t* sP = sV + 16384;         // 32 KB
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 32768);   // [0]=tma [1]=mma
+  uint8_t* sP = sm;                 // 32 KB: [Q | keys 64..127 atom]
+  uint8_t* sK = sm + 32768;         // NK*128 B (<= 16 KB)
+  uint8_t* sV = sK + kbytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + kbytes);   // [0]=tma [1]=mma
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int b = blockIdx.x / H, h = blockIdx.x % H;
@@ -205,7 +209,7 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
         smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -262,14 +266,14 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t id = idesc(128, kDh, false, true);
     const uint32_t ap = smem_u32(sP), av = smem_u32(sV);
-    for (int j = 0; j < NK / 16; ++j) mma(tm + 128, kmaj_keys(ap, j), mnmaj_tile(av, j), id, j > 0);
+    for (int j = 0; j < NK / 16; ++j) mma(tm, kmaj_keys(ap, j), mnmaj_tile(av, j), id, j > 0);
     commit(&bar[1]);
   }
   mbar_wait(&bar[1], 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   float ov[64];
 #pragma unroll
-  for (int c = 0; c < 64; c += 16) ld16(lane_base + 128 + c, ov + c);
+  for (int c = 0; c < 64; c += 16) ld16(lane_base + c, ov + c);
   if (live) {
     float v32[32];
     __nv_bfloat16* dst = o + (long)(row0 + r) * D + h * kDh;
@@ -284,12 +288,12 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
   }
 }
 
 // ----------------------------------------------------------------- backward
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128, 2)
 attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                    const __grid_constant__ CUtensorMap mdo, int Tn, int H, int NK,
                    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
@@ -298,12 +302,16 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base0 = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + ((1024 - (base0 & 1023)) & 1023);
+  // ~107 KB so two CTAs share an SM: K holds only its NK rows, and V (dead
+  // once dP = dO·Vᵀ has retired) lives in dS's second 64-key atom, which is
+  // written only after that MMA completes.
+  const int kbytes = (NK * 128 + 1023) & ~1023;
   uint8_t* sQ = sm;                 // 16 KB (128 q rows)
   uint8_t* sK = sQ + 16384;         // NK rows
-  uint8_t* sV = sK + 16384;
-  uint8_t* sdO = sV + 16384;        // 16 KB
+  uint8_t* sdO = sK + kbytes;       // 16 KB
   uint8_t* sP = sdO + 16384;        // 32 KB
   uint8_t* sdS = sP + 32768;        // 32 KB
+  uint8_t* sV = sdS + 16384;        // NK rows, aliases dS keys 64..127
   uint64_t* bar = reinterpret_cast<uint64_t*>(sdS + 32768);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -466,8 +474,10 @@ static bool map2d(CUtensorMap* m, const void* ptr, long inner, long outer, long 
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int kFwdSmem = 16384 * 3 + 32768 + 1024 + 64;
-constexpr int kBwdSmem = 16384 * 4 + 32768 * 2 + 1024 + 64;
+constexpr int kFwdSmem = 16384 * 2 + 32768 + 1024 + 64;   // upper bound (NK = 128)
+inline int fwd_smem(int NK) { return 32768 + 2 * ((NK * 128 + 1023) & ~1023) + 1024 + 64; }
+constexpr int kBwdSmem = 16384 * 3 + 32768 * 2 + 1024 + 64;   // upper bound (NK = 128)
+inline int bwd_smem(int NK) { return 16384 * 2 + ((NK * 128 + 1023) & ~1023) + 32768 * 2 + 1024 + 64; }
 
 }  // namespace atc
 
@@ -491,7 +501,7 @@ int launch_attn_tc_fwd(int B, int Tn, int H, const __nv_bfloat16* qkv, __nv_bflo
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem));
     set = true;
   }
-  attn_tc_fwd_kernel<<<B * H, 128, kFwdSmem, s>>>(mq, mk, Tn, H, NK, o, lse,
+  attn_tc_fwd_kernel<<<B * H, 128, fwd_smem(NK), s>>>(mq, mk, Tn, H, NK, o, lse,
                                                   1.0f / sqrtf((float)kDh));
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -516,7 +526,7 @@ int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __n
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
     set = true;
   }
-  attn_tc_bwd_kernel<<<B * H, 128, kBwdSmem, s>>>(mq, mk, md, Tn, H, NK, o, dout, lse, dqkv,
+  attn_tc_bwd_kernel<<<B * H, 128, bwd_smem(NK), s>>>(mq, mk, md, Tn, H, NK, o, dout, lse, dqkv,
                                                   1.0f / sqrtf((float)kDh), bias_part);
   note_launch();
   PPLL_LAUNCH_CHECK();
