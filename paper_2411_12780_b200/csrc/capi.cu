@@ -65,17 +65,29 @@ int gemm_dgrad(int M, int K, int N, const void* dY, long lddy, const void* W, co
   if (M == 0) return PPLL_OK;
   if (dtype == PPLL_F32) {
     auto ep = make_ep<float>(o, dX, lddx, K);
-    return launch_gemm_simt<float, float>(M, K, N, (const float*)dY, lddy, 1, (const float*)W, 1, N,
-                                          ep, ws, ws_elems, s);
+    int r = launch_gemm_simt<float, float>(M, K, N, (const float*)dY, lddy, 1, (const float*)W, 1,
+                                           N, ep, ws, ws_elems, s);
+    if (r == PPLL_OK && o.db) r = launch_colsum<float>(M, K, (const float*)dX, (int)lddx, o.db, s, ws, ws_elems);
+    return r;
   }
   auto ep = make_ep<bf16>(o, dX, lddx, K);
   if (g_gemm_engine != PPLL_GEMM_SIMT) {
+    const bool fuse_cs = o.db && o.cs_ws && o.cs_ws_elems >= (size_t)ceil_div(M, 32) * K;
+    if (fuse_cs) ep.cs_part = o.cs_ws;
     int r = launch_gemm_tc<bf16>(M, K, N, (const bf16*)dY, lddy, true, (const bf16*)W, N, true, ep,
                                  ws, ws_elems, s);
+    if (r == PPLL_OK && o.db) {
+      if (fuse_cs)   // Σ over the row-block partials (fixed order)
+        return launch_colsum<float>(ceil_div(M, 32), K, o.cs_ws, K, o.db, s, ws, ws_elems);
+      return launch_colsum<bf16>(M, K, (const bf16*)dX, (int)lddx, o.db, s, ws, ws_elems);
+    }
     if (r != PPLL_ERR_UNSUPPORTED || g_gemm_engine == PPLL_GEMM_TCGEN05) return r;
+    ep.cs_part = nullptr;
   }
-  return launch_gemm_simt<bf16, bf16>(M, K, N, (const bf16*)dY, lddy, 1, (const bf16*)W, 1, N, ep,
-                                      ws, ws_elems, s);
+  int r = launch_gemm_simt<bf16, bf16>(M, K, N, (const bf16*)dY, lddy, 1, (const bf16*)W, 1, N, ep,
+                                       ws, ws_elems, s);
+  if (r == PPLL_OK && o.db) r = launch_colsum<bf16>(M, K, (const bf16*)dX, (int)lddx, o.db, s, ws, ws_elems);
+  return r;
 }
 
 int linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,

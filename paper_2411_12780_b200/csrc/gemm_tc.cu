@@ -664,7 +664,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
     if (c < 64 && N > c) continue;       // narrow tiles only as the single column tile
     const long tiles = (long)mt * ceil_div(N, c);
     int sp = 1;
-    if (ws && tiles * 2 <= kNumSMs && K >= 8 * BK) {
+    if (ws && !ep.cs_part && tiles * 2 <= kNumSMs && K >= 8 * BK) {
       sp = (int)(kNumSMs / tiles);
       if (sp > K / (4 * BK)) sp = K / (4 * BK);
       while (sp > 1 && (size_t)sp * M * N > ws_elems) --sp;

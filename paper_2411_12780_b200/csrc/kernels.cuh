@@ -177,10 +177,14 @@ __device__ __forceinline__ void st_row32<__nv_bfloat16>(__nv_bfloat16* p, bool v
 // instruction covers 8 rows x 64 contiguous bytes (full 32-B sectors) instead
 // of 32 rows x 16 B.  fp32 goes in two 16-column halves.  Up to two outputs
 // (the dual store of the ring push) share one transpose.
+// `csum` (optional): this 32-row block's column sums of the stored (rounded)
+// values, rows >= M excluded, written as one partial row csum[n0 .. n0+31]
+// (a fused bias-gradient Σ_rows; reduced over the row blocks afterwards).
 template <typename TO>
 __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, long ld2, int row0,
                                                    int M, int n0, int N, bool vec,
-                                                   const float (&v)[32], uint8_t* stg, int lane) {
+                                                   const float (&v)[32], uint8_t* stg, int lane,
+                                                   float* csum = nullptr) {
   constexpr int kEl = 16 / (int)sizeof(TO);          // elements per 16-B chunk
   constexpr int kPasses = sizeof(TO) == 4 ? 2 : 1;   // 64-B row slices per 32 columns
   constexpr int kCols = 32 / kPasses;                // columns per pass
@@ -204,12 +208,20 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
     }
     __syncwarp();
     // read: 8 rows x 4 chunks per instruction, 4 instructions
+    float cs[kEl];
+#pragma unroll
+    for (int e = 0; e < kEl; ++e) cs[e] = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int r = i * 8 + (lane >> 2), c = lane & 3;
       const uint4 q = *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
       const int row = row0 + r;
       const int col = n0 + p * kCols + c * kEl;
+      if (csum && row < M) {
+        const TO* e = reinterpret_cast<const TO*>(&q);
+#pragma unroll
+        for (int t = 0; t < kEl; ++t) cs[t] += to_f(e[t]);
+      }
       if (row < M && col < N) {
         if (vec && col + kEl <= N) {
           *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
@@ -221,6 +233,19 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
             if (out2) out2[(long)row * ld2 + col + t] = e[t];
           }
         }
+      }
+    }
+    if (csum) {   // lanes with equal (lane & 3) hold the same columns
+#pragma unroll
+      for (int t = 0; t < kEl; ++t) {
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 4);
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 8);
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 16);
+      }
+      const int col = n0 + p * kCols + (lane & 3) * kEl;
+      if (lane < 4) {
+        for (int t = 0; t < kEl; ++t)
+          if (col + t < N) csum[col + t] = cs[t];
       }
     }
     __syncwarp();
@@ -251,6 +276,7 @@ struct Epilogue {
   int ncols = 0;             // N (for row-segment bounds)
   int vec = 0;
   float* partial = nullptr;  // split-K workspace (internal)
+  float* cs_part = nullptr;  // fused column sums: [ceil(M/32)][ncols] partial rows (or null)
 
   __device__ __forceinline__ float act_f(float v) const {
     if (act == kActRelu) return fmaxf(v, 0.f);
@@ -338,7 +364,8 @@ struct Epilogue {
     act_mask32(v, k, r);
     if (pre && act == kActGeluD)
       warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg, lane);
-    warp_store_block32<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane);
+    warp_store_block32<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane,
+                           cs_part ? cs_part + (long)(row0 >> 5) * ncols : nullptr);
   }
 
   // 32 consecutive columns n0..n0+31 of row m (n0 % 32 == 0)
@@ -426,6 +453,11 @@ struct LinOpts {
   long ldpre = 0;
   void* C2 = nullptr;
   long ldc2 = 0;
+  // fused bias gradient db = Σ_rows(output) (tcgen05 engine: per-32-row-block
+  // column partials in cs_ws [ceil(M/32) x ncols], then one small reduction)
+  float* db = nullptr;
+  float* cs_ws = nullptr;
+  size_t cs_ws_elems = 0;
 };
 int gemm_fwd(int M, int K, int N, const void* X, long ldx, const void* W, const LinOpts& o,
              void* Y, long ldy, int dtype, float* ws, size_t ws_elems, cudaStream_t s);

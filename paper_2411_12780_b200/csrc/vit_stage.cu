@@ -51,6 +51,8 @@ struct ppll_vit_stage {
   char *dxa = nullptr, *dxb = nullptr, *dxc = nullptr, *dbig = nullptr, *dxn = nullptr,
        *dqkv = nullptr, *dO = nullptr, *dtok = nullptr;
   float* ln_part = nullptr;
+  float* cs_part = nullptr;       // fused bias-gradient column partials [ceil(M/32), F]
+  size_t cs_part_elems = 0;
   float* attn_bpart = nullptr;
   float* ws = nullptr;
   size_t ws_elems = 0;
@@ -228,10 +230,13 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     og.mask = b.u;
     og.ldmask = F;
     og.mask_mode = kMaskMul;
+    og.db = st->G(st->po(l, kB1));      // db1 = Σ rows dU, fused into this epilogue
+    og.cs_ws = st->cs_part;
+    og.cs_ws_elems = st->cs_part_elems;
     r = gemm_dgrad(M, F, D, dx2, D, st->W(st->po(l, kW2)), og, st->dbig, F, st->dtype, st->ws,
                    st->ws_elems, s);
     if (r) return r;
-    r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
+    r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), nullptr,
                      st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
     r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
@@ -341,6 +346,8 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
   st->dbig = A(M * F * e); st->dxn = A(M * D * e); st->dqkv = A(M * 3 * D * e);
   st->dO = A(M * D * e);
   st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 3 * D * 4);
+  st->cs_part_elems = (size_t)ceil_div((long)M, 32) * st->F;
+  st->cs_part = (float*)A(st->cs_part_elems * 4);
   st->attn_bpart = (float*)A((size_t)st->Bmax * 3 * D * 4);
   // split-K workspace: 16 partial copies of the largest weight gradient
   st->ws_elems = 16 * (size_t)D * (F > 3 * D ? F : 3 * D);
