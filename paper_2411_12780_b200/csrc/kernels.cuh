@@ -235,7 +235,7 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
         }
       }
     }
-    if (csum) {   // lanes with equal (lane & 3) hold the same columns
+    if (csum && row0 < M) {   // lanes with equal (lane & 3) hold the same columns
 #pragma unroll
       for (int t = 0; t < kEl; ++t) {
         cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 4);

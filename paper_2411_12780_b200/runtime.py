@@ -258,11 +258,18 @@ class _Rings:
                                       device=m.device))
             self.y.append(torch.zeros((capacity, max_batch), dtype=torch.int64, device=m.device))
         m0 = modules[0]
-        self.x_pin = torch.empty((capacity, max_batch, m0.in_features), dtype=torch.float32,
+        # host-input staging, decoupled from the ring capacity M: P pinned
+        # slots + P device fp32 slots, so host->device copies run up to P
+        # batches ahead of the ring's credits (the ring itself still holds
+        # exactly M slots: backpressure semantics unchanged)
+        self.P = max(8, 2 * capacity)
+        self.cast = m0.act_dtype != torch.float32
+        self.x_pin = torch.empty((self.P, max_batch, m0.in_features), dtype=torch.float32,
                                  pin_memory=True)
-        self.y_pin = torch.empty((capacity, max_batch), dtype=torch.int64, pin_memory=True)
-        self.x_stage = (torch.empty((capacity, max_batch, m0.in_features), dtype=torch.float32,
-                                    device=m0.device) if m0.act_dtype != torch.float32 else None)
+        self.y_pin = torch.empty((self.P, max_batch), dtype=torch.int64, pin_memory=True)
+        self.x_stage = torch.empty((self.P, max_batch, m0.in_features), dtype=torch.float32,
+                                   device=m0.device)
+        self.y_stage = torch.empty((self.P, max_batch), dtype=torch.int64, device=m0.device)
 
 
 def _enable_peers(modules):
@@ -292,10 +299,11 @@ class DevicePipeline:
         self.graphs = {}
         self.streams = [torch.cuda.Stream(device=m.device) for m in self.modules]
         self.src_stream = torch.cuda.Stream(device=self.modules[0].device)
+        self.h2d_stream = torch.cuda.Stream(device=self.modules[0].device)
         s, M = len(self.modules), self.M
         self.ev_ready = [[torch.cuda.Event() for _ in range(M)] for _ in range(s)]
         self.ev_free = [[torch.cuda.Event() for _ in range(M)] for _ in range(s)]
-        self.ev_h2d = [torch.cuda.Event() for _ in range(M)]
+        self.ev_h2d, self.ev_cast = [], []     # per staging slot (sized in _ensure)
         self.used_free = [[False] * M for _ in range(s)]
         _enable_peers(self.modules)
 
@@ -308,6 +316,9 @@ class DevicePipeline:
             m.native(self.max_batch)
         self.rings = _Rings(self.modules, self.M, self.max_batch)
         self.graphs = {}
+        self.ev_h2d = [torch.cuda.Event() for _ in range(self.rings.P)]
+        self.ev_cast = [torch.cuda.Event() for _ in range(self.rings.P)]
+        self.used_stage = [False] * self.rings.P
 
     def _launch(self, j: int, slot: int, B: int, stream):
         """Enqueue stage j's local step on ring slot ``slot`` (B rows)."""
@@ -375,33 +386,45 @@ class DevicePipeline:
             yt = torch.as_tensor(np.asarray(y)) if not torch.is_tensor(y) else y
             if yt.dtype.is_floating_point or tuple(yt.shape) != (B,):
                 raise WorkerPanic(0, "labels must be integers matching the batch")
-            if not resident:
-                if batch_id >= M:
-                    self.ev_h2d[slot].synchronize()      # recycle pinned staging
-                r.x_pin[slot, :B].copy_(xt)
-                r.y_pin[slot, :B].copy_(yt)
-                x_src, y_src = r.x_pin[slot, :B], r.y_pin[slot, :B]
-            else:                                        # inputs already in HBM
-                x_src, y_src = xt, yt
             src = self.src_stream
+            if not resident:
+                ps = batch_id % r.P
+                if self.used_stage[ps]:
+                    self.ev_h2d[ps].synchronize()        # recycle pinned staging
+                r.x_pin[ps, :B].copy_(xt)
+                r.y_pin[ps, :B].copy_(yt)
+                h2d = self.h2d_stream
+                with torch.cuda.stream(h2d):
+                    if self.used_stage[ps]:
+                        h2d.wait_event(self.ev_cast[ps])  # device staging slot consumed
+                    r.x_stage[ps, :B].copy_(r.x_pin[ps, :B], non_blocking=True)
+                    r.y_stage[ps, :B].copy_(r.y_pin[ps, :B], non_blocking=True)
+                    self.ev_h2d[ps].record(h2d)
+                self.used_stage[ps] = True
+                x_src, y_src = r.x_stage[ps, :B], r.y_stage[ps, :B]
+            else:                                        # inputs already in HBM
+                ps = None
+                x_src, y_src = xt, yt
             with torch.cuda.stream(src):
+                if ps is not None:
+                    src.wait_event(self.ev_h2d[ps])
                 if self.used_free[0][slot]:
                     src.wait_event(self.ev_free[0][slot])
                 if timing:
                     e = torch.cuda.Event(enable_timing=True)
                     e.record(src)
                     t_src.append(e)
-                if r.x_stage is None:
+                if not r.cast:
                     r.x[0][slot, :B].copy_(x_src, non_blocking=True)
                 else:
-                    if not resident:
-                        r.x_stage[slot, :B].copy_(x_src, non_blocking=True)
-                        x_src = r.x_stage[slot, :B]
+                    if x_src.dtype != torch.float32:
+                        x_src = x_src.float()
                     N.check(N.load().ppll_cast(B * mods[0].in_features, x_src.data_ptr(),
                                                N.F32, r.x[0][slot].data_ptr(), N.BF16,
                                                src.cuda_stream), "cast")
                 r.y[0][slot, :B].copy_(y_src, non_blocking=True)
-                self.ev_h2d[slot].record(src)
+                if ps is not None:
+                    self.ev_cast[ps].record(src)
                 self.ev_ready[0][slot].record(src)
             # ---- stages (runtime.py:325-388 worker loop, on device) ----
             for j in range(s):
@@ -428,6 +451,7 @@ class DevicePipeline:
         for st in self.streams:
             st.synchronize()
         self.src_stream.synchronize()
+        self.h2d_stream.synchronize()
         # ---- errors: first failing stage surfaces as WorkerPanic ----
         for j, m in enumerate(mods):
             try:
@@ -510,7 +534,7 @@ def _run_ppll_roundrobin(modules, dataset_iter, config) -> EpochMetrics:
             sizes[next_id] = B
             with torch.cuda.stream(stream):
                 xd = xt.to(device=modules[0].device, dtype=torch.float32)
-                if r.x_stage is None:
+                if not r.cast:
                     r.x[0][slot, :B].copy_(xd)
                 else:
                     N.check(lib.ppll_cast(B * modules[0].in_features, xd.data_ptr(), N.F32,
