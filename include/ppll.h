@@ -151,6 +151,16 @@ int ppll_stage_step(ppll_stage* st, int B, const void* x_in, const int64_t* labe
 int ppll_stage_forward(ppll_stage* st, int B, const void* x_in, void* h_out, void* logits,
                        void* stream);
 
+/* The paper's comparison baselines, E2E and naive PP (runtime.py:248-284,
+ * 294-408 with ppll=False, 423-465): block-only forward keeping activations;
+ * block backward from dLoss/d(block output) g_out (or, final stage, from the
+ * task loss on the block output when labels != NULL; loss recorded like a
+ * local step), writing dLoss/d(block input) into g_in (NULL: untracked
+ * input), then the Nesterov step over the block parameters only. */
+int ppll_stage_block_forward(ppll_stage* st, int B, const void* x_in, void* h_out, void* stream);
+int ppll_stage_block_backward(ppll_stage* st, int B, const void* x_in, const void* g_out,
+                              const int64_t* labels, void* g_in, void* stream);
+
 /* ---- one local step of a ViT stage (same step semantics, blocks.py:266-289,
  * applied to pre-LN transformer blocks; no reference implementation exists —
  * parity is pinned to oracle/vit_oracle.py) -------------------------------

@@ -216,6 +216,32 @@ def sequential_ppll(stages, batches, lr0, lr_min, total_steps, mu, wd):
     return losses
 
 
+def e2e_step(stages, x, y, lr0, lr_min, total_steps, mu, wd):
+    """The paper's baselines E2E (runtime.py:248-284) and naive PP
+    (runtime.py:359-382, 423-465), which compute the same numbers: block
+    forward through every stage, the task loss on the final stage's output
+    (no aux heads), backward through all blocks with the boundary gradients
+    flowing stage to stage (no dX into the network input), then the
+    cosine-LR Nesterov step over each stage's BLOCK parameters only; every
+    stage's step_count advances.  Returns the loss."""
+    h = np.asarray(x, dtype=np.float64)
+    acts = []
+    for st in stages:
+        h, a = _forward(st.block, h)
+        acts.append(a)
+    loss, g = softmax_xent(h, y)
+    grads = [None] * len(stages)
+    for j in reversed(range(len(stages))):
+        grads[j], g = _backward(stages[j].block, acts[j], g, first_input_detached=(j == 0))
+    for j, st in enumerate(stages):
+        lr = cosine_lr(st.step_count, lr0, lr_min, total_steps)
+        nb = 2 * len(st.block)
+        for p, v, gg in zip(st.params()[:nb], st.momenta[:nb], grads[j]):
+            nesterov_update(p, v, gg, lr, mu, wd)
+        st.step_count += 1
+    return loss
+
+
 # --------------------------------------------------------------------------
 # deterministic round-robin scheduler bookkeeping (runtime.py:475-533)
 # --------------------------------------------------------------------------

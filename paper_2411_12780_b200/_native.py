@@ -41,6 +41,8 @@ SIGNATURES = {
                                 _vp, _vp, _i, _vp, _vp, _f, _f]),
     "ppll_stage_destroy": (None, [_vp]),
     "ppll_stage_step": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "ppll_stage_block_forward": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "ppll_stage_block_backward": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp]),
     "ppll_stage_forward": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ppll_vit_stage_create": (_vp, [_vp, _vp, _i64, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _f, _f]),
     "ppll_vit_stage_destroy": (None, [_vp]),

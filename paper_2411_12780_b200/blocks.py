@@ -265,6 +265,18 @@ class LocalModule:
         N.check(N.load().ppll_stage_forward(self.native(B), B, x_ptr, h_ptr, logits_ptr, stream),
                 f"stage {self.stage_index} forward")
 
+    # -- the E2E / naive-PP baselines (runtime.py:248-284, 359-382) ---------
+    supports_e2e = True
+
+    def launch_block_forward(self, B, x_ptr, h_ptr, stream) -> None:
+        N.check(N.load().ppll_stage_block_forward(self.native(B), B, x_ptr, h_ptr, stream),
+                f"stage {self.stage_index} block forward")
+
+    def launch_block_backward(self, B, x_ptr, gout_ptr, y_ptr, gin_ptr, stream) -> None:
+        N.check(N.load().ppll_stage_block_backward(self.native(B), B, x_ptr, gout_ptr, y_ptr,
+                                                   gin_ptr, stream),
+                f"stage {self.stage_index} block backward")
+
     def error_word(self) -> int:
         """Sticky device error bits (synchronises this module's device)."""
         return int(self._flat["state"][2].item())

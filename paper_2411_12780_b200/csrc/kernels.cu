@@ -473,6 +473,27 @@ int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t
   return PPLL_OK;
 }
 
+// ReLU adjoint alone (tensor.py:156): out = g * [act > 0] (subgradient 0 at 0)
+template <typename T>
+__global__ void relu_mask_kernel(long n, const T* __restrict__ g, const T* __restrict__ act,
+                                 T* __restrict__ out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    DT<T>::st(out + i, to_f(act[i]) > 0.f ? to_f(g[i]) : 0.f);
+}
+
+int launch_relu_mask(long n, const void* g, const void* act, void* out, int dtype, cudaStream_t s) {
+  int blocks = (int)min((n + 255) / 256, (long)148 * 8);
+  if (blocks < 1) return PPLL_OK;
+  if (dtype == PPLL_F32)
+    relu_mask_kernel<<<blocks, 256, 0, s>>>(n, (const float*)g, (const float*)act, (float*)out);
+  else
+    relu_mask_kernel<<<blocks, 256, 0, s>>>(n, (const __nv_bfloat16*)g, (const __nv_bfloat16*)act,
+                                            (__nv_bfloat16*)out);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
 // ------------------------------------------------------------------------
 // ring flag words (runtime.py:88-115 push/pop/close semantics on device)
 // ------------------------------------------------------------------------

@@ -436,6 +436,7 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
                     float wd, int* err, cudaStream_t s);
 
 int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t s);
+int launch_relu_mask(long n, const void* g, const void* act, void* out, int dtype, cudaStream_t s);
 int launch_ring_publish(int* w, int seq, cudaStream_t s);
 int launch_ring_wait(const int* w, int seq, cudaStream_t s);
 int launch_ring_release(int* w, cudaStream_t s);

@@ -194,4 +194,75 @@ int ppll_stage_forward(ppll_stage* st, int B, const void* x_in, void* h_out, voi
   return PPLL_OK;
 }
 
+// ---- the paper's baselines: E2E / naive PP (runtime.py:248-284, 359-382) ----
+// Block forward only (aux heads unused), activations kept for the backward.
+int ppll_stage_block_forward(ppll_stage* st, int B, const void* x_in, void* h_out, void* stream) {
+  if (!st || B < 1 || B > st->max_batch || !x_in) {
+    set_error("ppll_stage_block_forward: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int i = 0; i < st->n_block; ++i) {
+    const void* in = i == 0 ? x_in : st->act_ptr(i - 1);
+    void* dual = (i == st->n_block - 1) ? h_out : nullptr;
+    int r = linear_fwd(B, st->in_w[i], st->out_w[i], in, st->in_w[i], st->w_ptr(i), st->b_ptr(i),
+                       st->act_ptr(i), st->out_w[i], dual, st->out_w[i], st->relu[i], st->dtype,
+                       st->ws, st->ws_elems, s);
+    if (r) return r;
+  }
+  return PPLL_OK;
+}
+
+// Backward through the block from dLoss/d(block output) `g_out` (after the
+// block's last ReLU), or — final stage, labels != NULL — from the task loss
+// on the block output; dLoss/d(block input) into `g_in` (NULL for stage 0,
+// whose input is the untracked data); then Nesterov over the BLOCK
+// parameters only (runtime.py:280-281, 378-380).  The step counter advances.
+int ppll_stage_block_backward(ppll_stage* st, int B, const void* x_in, const void* g_out,
+                              const int64_t* labels, void* g_in, void* stream) {
+  if (!st || B < 1 || B > st->max_batch || !x_in || (!g_out && !labels)) {
+    set_error("ppll_stage_block_backward: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int L = st->n_block - 1;
+  const int C = st->out_w[L];
+  int r;
+  char* G = st->g0;
+  char* Gn = st->g1;
+  if (labels) {
+    if (st->dtype == PPLL_F32)
+      r = launch_softmax_xent<float>(B, C, (const float*)st->act_ptr(L), C, labels, (float*)G, C,
+                                     st->loss_hist, st->step, st->err, s);
+    else
+      r = launch_softmax_xent<__nv_bfloat16>(B, C, (const __nv_bfloat16*)st->act_ptr(L), C, labels,
+                                             (__nv_bfloat16*)G, C, st->loss_hist, st->step,
+                                             st->err, s);
+  } else if (st->relu[L]) {
+    r = launch_relu_mask((long)B * C, g_out, st->act_ptr(L), G, st->dtype, s);
+  } else {
+    r = launch_cast((long)B * C, g_out, st->dtype, G, st->dtype, s);
+  }
+  if (r) return r;
+  for (int i = L; i >= 0; --i) {
+    const void* in = i == 0 ? x_in : st->act_ptr(i - 1);
+    r = linear_wgrad(B, st->in_w[i], st->out_w[i], in, st->in_w[i], G, st->out_w[i],
+                     st->grad + st->off[2 * i], st->grad + st->off[2 * i + 1], st->dtype, st->ws,
+                     st->ws_elems, s);
+    if (r) return r;
+    if (i > 0 || g_in) {
+      const void* mask = (i > 0 && st->relu[i - 1]) ? st->act_ptr(i - 1) : nullptr;
+      void* dst = i > 0 ? (void*)Gn : g_in;
+      r = linear_dgrad(B, st->in_w[i], st->out_w[i], G, st->out_w[i], st->w_ptr(i), mask,
+                       st->in_w[i], dst, st->in_w[i], st->dtype, st->ws, st->ws_elems, s);
+      if (r) return r;
+      char* t = G; G = Gn; Gn = t;
+    }
+  }
+  const int64_t nb = st->n_block < st->n_layers ? st->off[2 * st->n_block] : st->n_params;
+  return launch_nesterov(nb, st->theta, st->mom, st->grad,
+                         reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
+                         st->max_step, 0.f, st->mu, st->wd, st->err, s);
+}
+
 }  // extern "C"

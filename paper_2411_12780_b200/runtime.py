@@ -224,8 +224,8 @@ def run_epoch(mode: RunMode, modules: Sequence[LocalModule], dataset_iter: Itera
     if mode == RunMode.PPLL:
         return DevicePipeline(modules, config).run(dataset_iter)
     if mode in (RunMode.E2E, RunMode.NAIVE_PP):
-        raise InvalidMode(f"{mode.value} is a comparison baseline not built on the device yet "
-                          "(SURVEY §8f rank 1)")
+        return _run_backprop(modules, dataset_iter, config, pipelined=mode == RunMode.NAIVE_PP,
+                             virtual_time=False)
     raise ConfigMismatch(f"unknown mode {mode!r}")
 
 
@@ -238,8 +238,164 @@ def run_deterministic(mode: RunMode, modules: Sequence[LocalModule], dataset_ite
     if mode == RunMode.PPLL:
         return _run_ppll_roundrobin(modules, dataset_iter, config)
     if mode in (RunMode.E2E, RunMode.NAIVE_PP):
-        raise InvalidMode(f"{mode.value} is not built on the device yet (SURVEY §8f rank 1)")
+        # naive PP collapses to strict per-batch serialisation (runtime.py:423-426):
+        # both replay as the single-stream backprop chain with virtual time
+        return _run_backprop(modules, dataset_iter, config, pipelined=False, virtual_time=True)
     raise ConfigMismatch(f"unknown mode {mode!r}")
+
+
+# --------------------------------------------------------------------------
+# the paper's baselines: E2E and naive PP on the device
+# --------------------------------------------------------------------------
+
+def _run_backprop(modules, dataset_iter, config, pipelined: bool, virtual_time: bool):
+    """End-to-end backprop through all blocks (E2E, runtime.py:248-284) or the
+    same computation as a naive pipeline (NAIVE_PP, runtime.py:294-408 with
+    ppll=False): stage j forwards batch t, the final stage takes the task loss
+    on its block output, and dLoss/d(boundary) flows back stage to stage;
+    each stage then steps its BLOCK parameters (aux heads unused).  Both
+    modes compute identical numbers (test_runtime.py:154-179).
+
+    Device schedule: one stream per stage when ``pipelined`` (the boundary
+    activations and gradients are single buffers on the consumer's device,
+    ordered by CUDA events: forward j-1 -> forward j, backward j+1 ->
+    backward j), else a single stream.  Naive PP serialises every batch across
+    the whole pipeline, so stage j's forward of t+1 waits for its backward of t
+    by stream order — that bubble is the baseline's cost."""
+    mods = list(modules)
+    s = len(mods)
+    for m in mods:
+        if not getattr(m, "supports_e2e", False):
+            raise InvalidMode(f"E2E / NaivePP are built for the reference's MLP blocks; "
+                              f"{type(m).__name__} runs PPLL only")
+    metrics = EpochMetrics(n_stages=s)
+    step0 = [m.optimizer.step_count for m in mods]
+    dev0 = mods[0].device
+    streams = ([torch.cuda.Stream(device=m.device) for m in mods] if pipelined
+               else [torch.cuda.Stream(device=dev0)] * s)
+    src = torch.cuda.Stream(device=dev0)
+    _enable_peers(mods)
+    timing = config.timing and not virtual_time
+    bufs = None
+    maxb = 0
+    ev_fwd = [torch.cuda.Event() for _ in range(s)]
+    ev_bwd = [torch.cuda.Event() for _ in range(s)]
+    ev_in = torch.cuda.Event()
+    used = False
+    t_evs = [[] for _ in range(s)]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev0.record(src)
+    n = 0
+    images = 0
+    for x, y in dataset_iter:
+        xt = torch.as_tensor(np.asarray(x, dtype=np.float32) if not torch.is_tensor(x) else x)
+        B = int(xt.shape[0])
+        if B < 1:
+            raise WorkerPanic(-1, "empty batch")
+        if xt[0].numel() != mods[0].in_features:
+            raise WorkerPanic(0, f"DimensionMismatch: stage 0 expects width {mods[0].in_shape}, "
+                                 f"got {tuple(xt.shape)}")
+        yt = torch.as_tensor(np.asarray(y)) if not torch.is_tensor(y) else y
+        if yt.dtype.is_floating_point or tuple(yt.shape) != (B,):
+            raise WorkerPanic(0, "labels must be integers matching the batch")
+        for m in mods:
+            if m.optimizer.step_count + 1 > m.schedule.total_steps + 1:
+                raise WorkerPanic(m.stage_index, f"StepOutOfRange: step "
+                                  f"{m.optimizer.step_count} > {m.schedule.total_steps}")
+        if bufs is None or B > maxb:
+            for st in streams + [src]:
+                st.synchronize()
+            maxb = max(B, maxb)
+            for m in mods:
+                m.native(maxb)
+            bufs = {
+                "x": torch.empty((maxb, mods[0].in_features), dtype=mods[0].act_dtype, device=dev0),
+                "y": torch.empty((maxb,), dtype=torch.int64, device=mods[-1].device),
+                # h[j]: output of stage j on stage j+1's device; g[j]: its gradient on stage j's
+                "h": [torch.empty((maxb, mods[j].out_features), dtype=mods[j].act_dtype,
+                                  device=mods[j + 1].device) for j in range(s - 1)],
+                "g": [torch.empty((maxb, mods[j].out_features), dtype=mods[j].act_dtype,
+                                  device=mods[j].device) for j in range(s - 1)],
+            }
+        with torch.cuda.stream(src):
+            if used:
+                src.wait_event(ev_bwd[0])                  # stage 0 done with the input
+            xd = xt.reshape(B, -1).to(device=dev0, dtype=torch.float32, non_blocking=True)
+            if mods[0].act_dtype == torch.float32:
+                bufs["x"][:B].copy_(xd)
+            else:
+                N.check(N.load().ppll_cast(B * mods[0].in_features, xd.data_ptr(), N.F32,
+                                           bufs["x"].data_ptr(), N.BF16, src.cuda_stream), "cast")
+            if used:
+                src.wait_event(ev_bwd[s - 1])
+            bufs["y"][:B].copy_(yt.to(torch.int64), non_blocking=True)
+            ev_in.record(src)
+        used = True
+        xin = [bufs["x"]] + bufs["h"]
+        # forward, stage order (records precede the waits that name them)
+        for j, m in enumerate(mods):
+            st = streams[j]
+            st.wait_event(ev_in if j == 0 else ev_fwd[j - 1])
+            if timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                t_evs[j].append(e)
+            out = bufs["h"][j].data_ptr() if j < s - 1 else None
+            m.launch_block_forward(B, xin[j].data_ptr(), out, st.cuda_stream)
+            ev_fwd[j].record(st)
+            if timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                t_evs[j].append(e)
+        # backward, reverse stage order
+        for j in reversed(range(s)):
+            m, st = mods[j], streams[j]
+            if j == s - 1:
+                st.wait_event(ev_in)                       # labels
+                gout, yptr = None, bufs["y"].data_ptr()
+            else:
+                st.wait_event(ev_bwd[j + 1])
+                gout, yptr = bufs["g"][j].data_ptr(), None
+            gin = bufs["g"][j - 1].data_ptr() if j > 0 else None
+            if timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                t_evs[j].append(e)
+            m.launch_block_backward(B, xin[j].data_ptr(), gout, yptr, gin, st.cuda_stream)
+            ev_bwd[j].record(st)
+            if timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                t_evs[j].append(e)
+            m.optimizer.step_count += 1
+        n += 1
+        images += B
+    for st in set(streams) | {src}:
+        st.synchronize()
+    for j, m in enumerate(mods):
+        try:
+            m.raise_for_error(stage=j)
+        except WorkerPanic:
+            for k, mm in enumerate(mods):
+                mm.optimizer.step_count = step0[k] + max(0, mm.device_step() - step0[k])
+            raise
+    metrics.n_batches = n
+    metrics.images = images
+    metrics.batches_processed = [n] * s
+    metrics.loss_history = [[] for _ in range(s - 1)] + [mods[-1].loss_history(step0[-1], n)]
+    metrics.buffer_high_water = [min(1, n)] * s
+    if virtual_time:
+        metrics.wall_time = float(n)
+        metrics.busy_time = [float(n)] * s
+    elif timing and n:
+        ms = lambda e: ev0.elapsed_time(e) / 1e3  # noqa: E731
+        ts = [[ms(e) for e in t_evs[j]] for j in range(s)]
+        # per batch: fwd start/end, bwd start (after the gradient arrived) /
+        # end; busy excludes the wait for the returning gradient
+        # (runtime.py:369-372)
+        metrics.busy_time = [sum(b - a for a, b in zip(ts[j][0::2], ts[j][1::2])) for j in range(s)]
+        metrics.wall_time = max(t[-1] for t in ts)
+    return metrics
 
 
 # --------------------------------------------------------------------------

@@ -148,10 +148,52 @@ def gen_full_m():
     np.savez_compressed(os.path.join(HERE, "full_m.npz"), **out)
 
 
+def gen_e2e_naive():
+    """The paper's baselines on the reference: end-to-end backprop (E2E) and
+    naive pipeline parallelism (NAIVE_PP), threaded and deterministic.  All
+    four runs are bitwise identical on the reference (test_runtime.py:154-194);
+    the fixture keeps one copy plus the per-run agreement flags."""
+    out = {}
+    for tag, dims, s in [("s2", (48, 40, 32, 24, 10), 2), ("s4", (96, 64, 64, 48, 40, 10), 4),
+                         ("s3", (33, 17, 29, 13, 21, 7), 3)]:
+        rng = np.random.default_rng(77 + s)
+        B, n = 12, 5
+        data = [(rng.standard_normal((B, dims[0])), rng.integers(0, dims[-1], B))
+                for _ in range(n)]
+        runs = []
+        for mode in (lp.RunMode.E2E, lp.RunMode.NAIVE_PP):
+            for runner in (lp.run_deterministic, lp.run_epoch):
+                _, mods = make(dims, s, 2, 3, 42, 10, None)
+                m = runner(mode, mods, iter(data), lp.RunConfig(buffer_capacity=2))
+                runs.append((m, mods))
+        m0, mods0 = runs[0]
+        same = all(np.array_equal(flat(a), flat(b)) for _, ms in runs[1:]
+                   for a, b in zip(mods0, ms))
+        same_loss = all(m.loss_history == m0.loss_history for m, _ in runs[1:])
+        assert same and same_loss, tag
+        out[f"{tag}_dims"] = np.array(dims)
+        out[f"{tag}_s"] = s
+        out[f"{tag}_xs"] = np.stack([d[0] for d in data])
+        out[f"{tag}_ys"] = np.stack([d[1] for d in data])
+        out[f"{tag}_losses"] = np.array(m0.loss_history[s - 1])
+        out[f"{tag}_n_losses"] = np.array([len(h) for h in m0.loss_history])
+        for j, mod in enumerate(mods0):
+            out[f"{tag}_final_{j}"] = flat(mod)
+            out[f"{tag}_mom_{j}"] = flat_m(mod)
+            out[f"{tag}_step_{j}"] = mod.optimizer.step_count
+    np.savez_compressed(os.path.join(HERE, "e2e_naive.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        print("ok")
+        sys.exit(0)
     for case in CASES:
         print(case[0], gen_case(*case)[:, -1])
     gen_threaded_equivalence()
     gen_traces()
     gen_full_m()
+    gen_e2e_naive()
     print("ok")

@@ -457,3 +457,48 @@ def test_gelu_epilogues_match_torch(engine, M, K, Nn):
     base = dY.double() @ W.double().T
     assert rel(dX[2], base * dmk) < 1e-2
     assert rel(dX[3], base * mk) < 1e-2
+
+
+# --- the paper's baselines: E2E and naive PP (runtime.py:248-284, 359-382) -------
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("tag", ["s2", "s4", "s3"])
+def test_e2e_and_naive_pp_match_reference(tag, precision):
+    """run_epoch / run_deterministic in E2E and NAIVE_PP modes on the device
+    against the reference's (bitwise-identical) four runs; the four device
+    runs are bitwise identical to each other; aux heads are never touched."""
+    z = np.load(os.path.join(GOLDEN, "e2e_naive.npz"))
+    dims = tuple(int(d) for d in z[f"{tag}_dims"])
+    s = int(z[f"{tag}_s"])
+    data = list(zip(z[f"{tag}_xs"], z[f"{tag}_ys"]))
+    spec = lp.NetworkSpec(dims)
+    ltol, wtol = TOL[precision]
+    runs = []
+    for mode in (lp.RunMode.E2E, lp.RunMode.NAIVE_PP):
+        for runner in (lp.run_deterministic, lp.run_epoch):
+            hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=10, seed=42,
+                                   precision=precision)
+            mods = lp.build_modules(spec, lp.partition(spec, s), 2, 3, hyper)
+            init = [_flat(m) for m in mods]
+            met = runner(mode, mods, iter(data), lp.RunConfig(buffer_capacity=2))
+            runs.append((met, mods, init))
+    ref_l = z[f"{tag}_losses"]
+    for met, mods, init in runs:
+        assert met.n_batches == len(data) and met.batches_processed == [len(data)] * s
+        assert [len(h) for h in met.loss_history] == list(z[f"{tag}_n_losses"])
+        got = np.array(met.loss_history[-1])
+        if precision == "fp32":
+            assert np.abs(got - ref_l).max() <= ltol * max(1.0, np.abs(ref_l).max())
+        else:
+            assert (np.abs(got - ref_l) / np.abs(ref_l)).max() <= ltol
+        for j, m in enumerate(mods):
+            fin, want = _flat(m), z[f"{tag}_final_{j}"]
+            assert np.abs(fin - want).max() / np.abs(want).max() <= wtol
+            nb = sum(p.data.size for p in m.block_parameters())
+            assert np.array_equal(fin[nb:], init[j][nb:])          # aux untouched
+            assert m.optimizer.step_count == int(z[f"{tag}_step_{j}"]) == m.device_step()
+    base = runs[0]
+    for met, mods, _ in runs[1:]:
+        assert met.loss_history == base[0].loss_history
+        for a, b in zip(mods, base[1]):
+            assert np.array_equal(_flat(a), _flat(b))

@@ -148,3 +148,24 @@ def test_deterministic_trace_kat():
     assert dict(tr.staleness) == {0: 8}
     assert tr.high_water == [1, 1]
     assert tr.rounds == 5
+
+
+@pytest.mark.parametrize("tag", ["s2", "s4", "s3"])
+def test_e2e_naive_pp_match_reference(tag):
+    """E2E / naive-PP restatement vs the reference's four runs (threaded and
+    deterministic, both modes; bitwise identical there)."""
+    z = np.load(os.path.join(GOLDEN, "e2e_naive.npz"))
+    dims = tuple(int(d) for d in z[f"{tag}_dims"])
+    s = int(z[f"{tag}_s"])
+    plan = orc.partition(dims, s)
+    stages = orc.build_stages(dims, plan, 2, 3, 42)
+    losses = [orc.e2e_step(stages, x, y, 0.05, 0.001, 10, 0.9, 1e-4)
+              for x, y in zip(z[f"{tag}_xs"], z[f"{tag}_ys"])]
+    np.testing.assert_allclose(losses, z[f"{tag}_losses"], rtol=0, atol=1e-12)
+    assert list(z[f"{tag}_n_losses"]) == [0] * (s - 1) + [len(losses)]
+    for j, st in enumerate(stages):
+        f = np.concatenate([p.ravel() for p in st.params()])
+        mv = np.concatenate([v.ravel() for v in st.momenta])
+        np.testing.assert_allclose(f, z[f"{tag}_final_{j}"], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(mv, z[f"{tag}_mom_{j}"], rtol=0, atol=1e-12)
+        assert st.step_count == int(z[f"{tag}_step_{j}"])
