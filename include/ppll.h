@@ -119,6 +119,18 @@ int ppll_nesterov_step(int64_t n, float* theta, float* v, const float* g, void* 
 double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps);
 
 /* element conversion helpers (fp32 <-> bf16), n elements */
+/* ---- data path / evaluation -------------------------------------------- */
+/* dst[r,:] = cast(src[idx[r],:]) for r < n (fp32 rows of `width` features,
+ * dst fp32 or bf16), and labels_dst[r] = labels_src[idx[r]] when given: the
+ * batch assembly of BatchIterator.__next__ (data.py:169-173) from an
+ * HBM-resident dataset. */
+int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx, void* dst,
+                     int dst_dtype, const int64_t* labels_src, int64_t* labels_dst, void* stream);
+/* *count += #{r < B : argmax_c logits[r,c] == labels[r]} (first maximum, as
+ * numpy's argmax): the accuracy count of evaluate (harness.py:121-131). */
+int ppll_count_correct(int B, int C, const void* logits, int ldz, int dtype,
+                       const int64_t* labels, unsigned long long* count, void* stream);
+
 int ppll_cast(int64_t n, const void* src, int src_dtype, void* dst, int dst_dtype, void* stream);
 
 /* ---- one local step of a stage: blocks.py:266-289 ----------------------- */

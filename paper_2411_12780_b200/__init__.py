@@ -27,6 +27,9 @@ from .blocks import (
 from .errors import (
     ConfigMismatch,
     DimensionMismatch,
+    InvalidArg,
+    InvalidValue,
+    IoError,
     LabelOutOfRange,
     LocopipeError,
     MissingGradient,
@@ -51,6 +54,8 @@ from .runtime import (
     throughput,
 )
 from .tensor import Tensor, matmul, softmax_xent
+from .data import BatchIterator, Dataset, DeviceDataset, batches
+from .harness import CSV_HEADER, MetricsRecord, device_memory, evaluate, write_metrics_csv
 from .vit import VitLocalModule, VitSpec, balanced_depths, build_vit_modules
 from .resnet import ResLocalModule, ResNetSpec, build_resnet_modules, resnet_split
 

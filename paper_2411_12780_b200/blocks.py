@@ -214,6 +214,8 @@ class LocalModule:
         cap = max(batch, 1)
         lib = N.load()
         with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            free0 = torch.cuda.mem_get_info()[0]
             h = lib.ppll_stage_create(
                 L, len(self.layers), in_w, out_w, relu, offs, f["theta"].numel(), cap,
                 N.BF16 if self.precision == "bf16" else N.F32, f["theta"].data_ptr(),
@@ -224,6 +226,7 @@ class LocalModule:
         if not h:
             raise N.NativeError("ppll_stage_create failed: " +
                                 lib.ppll_last_error().decode(errors="replace"))
+        self._native_bytes = max(0, free0 - torch.cuda.mem_get_info(self.device)[0])
         self._native, self._native_batch = h, cap
         return h
 

@@ -207,6 +207,24 @@ double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps) {
   return lr_min + 0.5 * span * (1.0 + cos(M_PI * (double)step / (double)total_steps));
 }
 
+int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx, void* dst,
+                     int dst_dtype, const int64_t* labels_src, int64_t* labels_dst, void* stream) {
+  if (n < 0 || width < 1 || !src || !idx || !dst || (labels_src && !labels_dst)) {
+    set_error("gather_rows: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  return launch_gather_rows(n, width, src, idx, dst, dst_dtype, labels_src, labels_dst, S(stream));
+}
+
+int ppll_count_correct(int B, int C, const void* logits, int ldz, int dtype,
+                       const int64_t* labels, unsigned long long* count, void* stream) {
+  if (B < 0 || C < 1 || !logits || !labels || !count) {
+    set_error("count_correct: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  return launch_count_correct(B, C, logits, ldz, dtype, labels, count, S(stream));
+}
+
 int ppll_cast(int64_t n, const void* src, int src_dtype, void* dst, int dst_dtype, void* stream) {
   return launch_cast(n, src, src_dtype, dst, dst_dtype, S(stream));
 }

@@ -495,6 +495,91 @@ int launch_relu_mask(long n, const void* g, const void* act, void* out, int dtyp
 }
 
 // ------------------------------------------------------------------------
+// data path: HBM-resident dataset -> batch (data.py:107-179 order on device)
+// ------------------------------------------------------------------------
+// dst[r, :] = cast(src[idx[r], :]); one warp per row, 16-B vectors when the
+// row width allows (fp32 source, fp32 or bf16 destination).
+template <typename TD>
+__global__ void gather_rows_kernel(int n, long width, const float* __restrict__ src,
+                                   const int64_t* __restrict__ idx, TD* __restrict__ dst,
+                                   const int64_t* __restrict__ ysrc, int64_t* __restrict__ ydst,
+                                   int vec) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const long row = idx[r];
+  const float* s = src + row * width;
+  TD* d = dst + (long)r * width;
+  if (ysrc && lane == 0) ydst[r] = ysrc[row];
+  if (vec) {
+    for (long c = 4 * lane; c < width; c += 128) {
+      const float4 v = *reinterpret_cast<const float4*>(s + c);
+      if constexpr (sizeof(TD) == 4) {
+        *reinterpret_cast<float4*>(d + c) = v;
+      } else {
+        __nv_bfloat162 h[2] = {__floats2bfloat162_rn(v.x, v.y), __floats2bfloat162_rn(v.z, v.w)};
+        *reinterpret_cast<uint2*>(d + c) = *reinterpret_cast<uint2*>(h);
+      }
+    }
+  } else {
+    for (long c = lane; c < width; c += 32) DT<TD>::st(d + c, s[c]);
+  }
+}
+
+int launch_gather_rows(int n, long width, const float* src, const int64_t* idx, void* dst,
+                       int dst_dtype, const int64_t* ysrc, int64_t* ydst, cudaStream_t s) {
+  if (n <= 0) return PPLL_OK;
+  const int vec = (width % 4) == 0 && ((uintptr_t)src & 15) == 0 &&
+                  ((uintptr_t)dst & (dst_dtype == PPLL_F32 ? 15 : 7)) == 0;
+  const int blocks = (n + 7) / 8;
+  if (dst_dtype == PPLL_F32)
+    gather_rows_kernel<float><<<blocks, 256, 0, s>>>(n, width, src, idx, (float*)dst, ysrc, ydst,
+                                                     vec);
+  else
+    gather_rows_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(n, width, src, idx,
+                                                             (__nv_bfloat16*)dst, ysrc, ydst, vec);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+// evaluate (harness.py:121-131): count rows whose argmax (first maximum, like
+// numpy) equals the label; integer atomics, so the count is exact
+template <typename T>
+__global__ void count_correct_kernel(int B, int C, const T* __restrict__ z, long ldz,
+                                     const int64_t* __restrict__ y, unsigned long long* count) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= B) return;
+  float best = -INFINITY;
+  int arg = 0x7fffffff;
+  for (int c = lane; c < C; c += 32) {
+    const float v = to_f(z[(long)r * ldz + c]);
+    if (v > best || (v == best && c < arg) || (v != v && arg == 0x7fffffff)) { best = v; arg = c; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+  }
+  if (lane == 0 && (long long)arg == y[r]) atomicAdd(count, 1ull);
+}
+
+int launch_count_correct(int B, int C, const void* z, long ldz, int dtype, const int64_t* y,
+                         unsigned long long* count, cudaStream_t s) {
+  if (B <= 0) return PPLL_OK;
+  const int blocks = (B + 7) / 8;
+  if (dtype == PPLL_F32)
+    count_correct_kernel<<<blocks, 256, 0, s>>>(B, C, (const float*)z, ldz, y, count);
+  else
+    count_correct_kernel<<<blocks, 256, 0, s>>>(B, C, (const __nv_bfloat16*)z, ldz, y, count);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+// ------------------------------------------------------------------------
 // ring flag words (runtime.py:88-115 push/pop/close semantics on device)
 // ------------------------------------------------------------------------
 __device__ __forceinline__ int ld_acquire_sys(const int* p) {

@@ -148,6 +148,8 @@ class ResLocalModule(LocalModule):
         arr = (C.c_int64 * len(offs))(*offs)
         lib = N.load()
         with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            free0 = torch.cuda.mem_get_info()[0]
             h = lib.ppll_resnet_stage_create(
                 cfg, geo_a, og, arr, f["theta"].numel(), N.BF16 if self.precision == "bf16" else N.F32,
                 f["theta"].data_ptr(), f["grad"].data_ptr(), f["mom"].data_ptr(),
@@ -157,6 +159,7 @@ class ResLocalModule(LocalModule):
         if not h:
             raise N.NativeError("ppll_resnet_stage_create failed: " +
                                 lib.ppll_last_error().decode(errors="replace"))
+        self._native_bytes = max(0, free0 - torch.cuda.mem_get_info(self.device)[0])
         self._native, self._native_batch = h, batch
         return h
 

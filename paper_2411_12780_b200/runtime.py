@@ -561,6 +561,10 @@ class DevicePipeline:
             else:                                        # inputs already in HBM
                 ps = None
                 x_src, y_src = xt, yt
+                src.wait_stream(torch.cuda.current_stream(xt.device))   # producer of x
+                for t_ in (xt, yt):
+                    if torch.is_tensor(t_) and t_.is_cuda:
+                        t_.record_stream(src)            # no recycling while src reads
             with torch.cuda.stream(src):
                 if ps is not None:
                     src.wait_event(self.ev_h2d[ps])
@@ -570,7 +574,7 @@ class DevicePipeline:
                     e = torch.cuda.Event(enable_timing=True)
                     e.record(src)
                     t_src.append(e)
-                if not r.cast:
+                if not r.cast or x_src.dtype == r.x[0].dtype:
                     r.x[0][slot, :B].copy_(x_src, non_blocking=True)
                 else:
                     if x_src.dtype != torch.float32:

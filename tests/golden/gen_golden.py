@@ -184,6 +184,25 @@ def gen_e2e_naive():
     np.savez_compressed(os.path.join(HERE, "e2e_naive.npz"), **out)
 
 
+def gen_data_and_csv():
+    """BatchIterator orders (data.py:148-179) and the metrics CSV text
+    (harness.py:238-252) from the reference."""
+    orders = []
+    for n, bs, shuffle, seed in [(10, 3, True, 0), (10, 3, False, 0), (7, 7, True, 5),
+                                 (13, 4, True, 123), (1, 2, True, 9), (64, 16, True, 42)]:
+        ds = lp.Dataset(np.arange(n, dtype=np.float64)[:, None], np.zeros(n, dtype=np.int64), 1)
+        it = lp.batches(ds, bs, shuffle=shuffle, seed=seed)
+        orders.append({"n": n, "bs": bs, "shuffle": shuffle, "seed": seed, "len": len(it),
+                       "batches": [[int(v) for v in f[:, 0]] for f, _ in it]})
+    recs = [lp.MetricsRecord("PPLL", 1, 12.5, 0.25, 0.5, 0.375, 1000, 2000, 0.125),
+            lp.MetricsRecord("E2E", 0, 3.0, 2.302585093, 0.1, 0.09999999, 7, 8, 0.0),
+            lp.MetricsRecord("PPLL", 0, 1e-7, 1.0 / 3.0, 1.0, 0.0, 0, 0, 1.5)]
+    path = os.path.join(HERE, "metrics_ref.csv")
+    lp.write_metrics_csv(recs, path)
+    with open(os.path.join(HERE, "batch_orders.json"), "w") as f:
+        json.dump(orders, f, indent=0)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -196,4 +215,5 @@ if __name__ == "__main__":
     gen_traces()
     gen_full_m()
     gen_e2e_naive()
+    gen_data_and_csv()
     print("ok")

@@ -502,3 +502,68 @@ def test_e2e_and_naive_pp_match_reference(tag, precision):
         assert met.loss_history == base[0].loss_history
         for a, b in zip(mods, base[1]):
             assert np.array_equal(_flat(a), _flat(b))
+
+
+# --- data path and evaluation ---------------------------
+
+def _mlp_dataset(n=300, dims=(96, 64, 64, 48, 40, 10), seed=3):
+    rng = np.random.default_rng(seed)
+    return lp.Dataset(rng.standard_normal((n, dims[0])), rng.integers(0, dims[-1], n),
+                      dims[-1])
+
+
+def test_device_dataset_batches_equal_host_batches():
+    ds = _mlp_dataset()
+    dd = lp.DeviceDataset(ds)
+    for shuffle, seed in ((True, 4), (False, 0)):
+        host = list(lp.batches(ds, 64, shuffle=shuffle, seed=seed))
+        dev = list(dd.batches(64, shuffle=shuffle, seed=seed))
+        assert len(host) == len(dev) == 5
+        for (hx, hy), (dx, dy) in zip(host, dev):
+            assert np.array_equal(dx.cpu().numpy(), hx.astype(np.float32))
+            assert np.array_equal(dy.cpu().numpy(), hy)
+    bx, _ = next(dd.batches(64, True, 4, dtype=torch.bfloat16))
+    hx, _ = next(iter(lp.batches(ds, 64, True, 4)))
+    assert torch.equal(bx, torch.as_tensor(hx, dtype=torch.float32).bfloat16().cuda())
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_run_epoch_device_batches_equal_host_batches(precision):
+    ds = _mlp_dataset()
+    spec = lp.NetworkSpec((96, 64, 64, 48, 40, 10))
+    outs = []
+    for src in ("host", "device"):
+        hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=20, seed=42,
+                               precision=precision)
+        mods = lp.build_modules(spec, lp.partition(spec, 4), 2, 3, hyper)
+        it = (lp.batches(ds, 64, True, 7) if src == "host"
+              else lp.DeviceDataset(ds).batches(64, True, 7))
+        met = lp.run_epoch(lp.RunMode.PPLL, mods, it)
+        outs.append((met.loss_history, [_flat(m) for m in mods]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_evaluate_matches_oracle_forward(precision):
+    """evaluate (harness.py:121-131) on the device == argmax of an fp64
+    forward of the same (device) parameters, row for row up to ties."""
+    dims = (96, 64, 64, 48, 40, 10)
+    ds = _mlp_dataset(n=700, dims=dims)
+    spec = lp.NetworkSpec(dims)
+    hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=20, seed=42, precision=precision)
+    mods = lp.build_modules(spec, lp.partition(spec, 4), 2, 3, hyper)
+    lp.run_epoch(lp.RunMode.PPLL, mods, lp.batches(ds, 100, True, 1))
+    acc = lp.evaluate(mods, ds, chunk=256)
+    h = ds.features
+    for m in mods:
+        for layer in m.layers:
+            h = h @ layer.W.data.astype(np.float64) + layer.b.data.astype(np.float64)
+            if layer.relu_after:
+                h = np.maximum(h, 0.0)
+    ref = float((h.argmax(axis=1) == ds.labels).mean())
+    tol = 0.0 if precision == "fp32" else 0.03
+    assert abs(acc - ref) <= tol + 2.0 / ds.n, (acc, ref)
+    mem = lp.device_memory(mods[0])
+    assert mem["params_state_bytes"] > 0 and mem["workspace_bytes"] >= 0
