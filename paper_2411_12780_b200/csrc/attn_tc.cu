@@ -217,6 +217,8 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tm = *tslot;
+  // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
+  pdl_entry();
   const int row0 = b * Tn;
   if (tid == 0) {
     mbar_expect_tx(&bar[0], 16384 + 2 * NK * 128);
@@ -332,6 +334,8 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tm = *tslot;
+  // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
+  pdl_entry();
   const int row0 = b * Tn;
   // TMEM columns: S [0,128), dP [128,256); later dV [0,64), dK [64,128), dQ [128,192)
   if (tid == 0) {
@@ -501,7 +505,7 @@ int launch_attn_tc_fwd(int B, int Tn, int H, const __nv_bfloat16* qkv, __nv_bflo
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem));
     set = true;
   }
-  attn_tc_fwd_kernel<<<B * H, 128, fwd_smem(NK), s>>>(mq, mk, Tn, H, NK, o, lse,
+  launch_k(attn_tc_fwd_kernel, B * H, 128, fwd_smem(NK), s, mq, mk, Tn, H, NK, o, lse,
                                                   1.0f / sqrtf((float)kDh));
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -526,7 +530,7 @@ int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __n
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
     set = true;
   }
-  attn_tc_bwd_kernel<<<B * H, 128, bwd_smem(NK), s>>>(mq, mk, md, Tn, H, NK, o, dout, lse, dqkv,
+  launch_k(attn_tc_bwd_kernel, B * H, 128, bwd_smem(NK), s, mq, mk, md, Tn, H, NK, o, dout, lse, dqkv,
                                                   1.0f / sqrtf((float)kDh), bias_part);
   note_launch();
   PPLL_LAUNCH_CHECK();

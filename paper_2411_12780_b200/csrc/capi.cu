@@ -3,6 +3,7 @@
 #include <atomic>
 #include <math.h>
 #include <string.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -11,6 +12,7 @@ namespace ppll {
 static thread_local char t_err[512] = {0};
 static std::atomic<uint64_t> g_launches{0};
 int g_gemm_engine = PPLL_GEMM_AUTO;
+int g_pdl = getenv("PPLL_PDL") ? atoi(getenv("PPLL_PDL")) : 1;
 
 void set_error(const char* fmt, ...) {
   va_list ap;

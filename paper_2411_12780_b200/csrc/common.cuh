@@ -59,4 +59,40 @@ __device__ __forceinline__ float warp_max(float v) {
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every kernel of the library is
+// launched with programmatic stream serialisation and starts with
+// pdl_entry(): it waits (griddepcontrol.wait) until its stream predecessor
+// has completed and flushed, then immediately lets its own successor be
+// scheduled (griddepcontrol.launch_dependents).  A successor's CTAs therefore
+// launch and run their prologue (barrier init, TMEM allocation, tensor-map
+// prefetch — placed before pdl_wait in the tcgen05 kernels) while the
+// predecessor's last wave drains, instead of after it.  Inside CUDA graphs
+// the attribute becomes a programmatic edge.  PPLL_PDL=0 disables it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_entry() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+extern int g_pdl;
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace ppll

@@ -4,7 +4,7 @@
 //   C[M,N] = Σ_k A(m,k)·B(k,n)   bf16 operands, fp32 accumulation in TMEM.
 //
 // Persistent kernel: one CTA per SM walks a static schedule of work items
-// (128 x BN output tiles, optionally split along K).  Warp roles (320 thr):
+// (128 x BN output tiles, optionally split along K).  Warp roles (576 thr):
 //   warp 0      TMA producer (one elected lane): A/B k-blocks of 64 into a
 //               kStages-deep shared-memory ring (mbarrier full/empty);
 //   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x
@@ -12,12 +12,12 @@
 //               frees the smem slot; accumulators are DOUBLE-BUFFERED in
 //               TMEM (2 x BN columns) so tile i+1's MMAs overlap tile i's
 //               epilogue;
-//   warps 2..9  epilogue (two warps per TMEM lane quadrant, alternating
-//               32-column chunks): tcgen05.ld 32x32b.x32 (one accumulator row per
+//   warps 2..17 epilogue (four warps per TMEM lane quadrant, interleaved
+//               16-column chunks): tcgen05.ld 32x32b.x16 (one accumulator row per
 //               thread) → fused bias / residual / pre-activation store /
 //               ReLU|GELU / ReLU-mask|GELU-gradient / dual store (the ring
-//               push); each warp's 32x32 block is transposed through a 2-KB
-//               smem buffer so stores cover 8 rows x 64 B (full sectors); or fp32
+//               push); each warp's 32x16 block is transposed through a 1-KB
+//               smem buffer so stores cover 16 rows x 32 B (full sectors); or fp32
 //               split-K partials reduced afterwards in fixed split order
 //               (deterministic) by splitk_reduce_kernel with the same epilogue.
 // Operand layouts (128-byte swizzled, TMA box inner extent 64 elements):
@@ -35,7 +35,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kNumSMs = 148;
 
@@ -108,6 +108,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
@@ -115,7 +126,7 @@ struct Smem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
   static constexpr int EPI = 2 * BN * 4;          // bias slice per accumulator buffer
-  static constexpr int STG = kEpiWarps * 2048;    // per-warp store-transpose buffers
+  static constexpr int STG = kEpiWarps * 1024;    // per-warp store-transpose buffers
   static constexpr int TOTAL = STAGES * STAGE + EPI + STG + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
@@ -125,7 +136,7 @@ struct Sched {
   int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores
 };
 
-template <typename TO, bool A_K, bool B_K, int BN>
+template <typename TO, bool A_K, bool B_K, int BN, int F>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                int M, int N, int K, Sched sc, Epilogue<TO> ep, float* part) {
@@ -168,6 +179,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
+  pdl_entry();
 
   if (warp == 0) {
     // ------------------------- TMA producer -------------------------
@@ -238,11 +251,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     __syncwarp();
   } else {
     // ------------------------- epilogue -----------------------------
-    // thread = one accumulator row; 32-column segments move as 16-B vectors
-    // two warps per TMEM lane quadrant, alternating 32-column chunks
+    // thread = one accumulator row; kEpiWarps/4 warps per TMEM lane quadrant
+    // take interleaved 16-column chunks (more warps in flight per scheduler
+    // hide the TMEM-load / MUFU / store latencies of the fused epilogue)
+    constexpr int NG = kEpiWarps / 4;
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
-    const int half = (warp - 2) >> 2;
-    uint8_t* stg = stg_all + (warp - 2) * 2048;
+    const int grp = (warp - 2) >> 2;
+    uint8_t* stg = stg_all + (warp - 2) * 1024;
     int it = 0;
     for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
       const int tile = w % sc.tiles, z = w / sc.tiles;
@@ -261,19 +276,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const int row = m0 + q * 32 + lane;
       const bool live = row < M;
 #pragma unroll 1
-      for (int c = 32 * half; c < BN && n0 + c < N; c += 32 * (kEpiWarps / 4)) {
-        float ra[32], ka[32];
-        if (!split && live && !sc.probe) ep.load_aux32(row, n0 + c, ra, ka);   // overlaps the TMEM load
-        uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
-        float v[32];
+      for (int c = 16 * grp; c < BN && n0 + c < N; c += 16 * NG) {
+        float ra[16], ka[16];
+        uint4 qr[2], qk[2];
+        // residual / mask loads are issued before the TMEM load so they overlap it
+        if (!split && !sc.probe) {
+          ep.template aux_issue<F>(m0 + q * 32, M, n0 + c, qr, qk, lane);
+          if (live) ep.template load_aux16_t<F>(row, n0 + c, ra, ka);
+        }
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
+        if (!split && !sc.probe) ep.template aux_finish<F>(qr, qk, ra, ka, stg, lane);
+        float v[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
         if (split)
-          warp_store_block32<float>(part + (long)z * M * N, N, nullptr, 0, m0 + q * 32, M, n0 + c,
+          warp_store_block16<float>(part + (long)z * M * N, N, nullptr, 0, m0 + q * 32, M, n0 + c,
                                     N, (N % 4) == 0, v, stg, lane);
         else if (!sc.probe)
-          ep.finish_block32(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c, stg, lane);
+          ep.template finish_block16_t<F>(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c, stg, lane);
         else if (live && v[0] == 12345.f)   // keep the TMEM load live in probe mode
           ep.C[0] = v[1];
       }
@@ -360,7 +381,7 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  constexpr uint32_t kCols = BN < 32 ? 32 : BN;
+  constexpr uint32_t kCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)), "r"(kCols));
@@ -370,6 +391,8 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
+  pdl_entry();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -425,13 +448,13 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
   } else {
     // all MMAs retired => every operand slot has been consumed: the ring is
     // free and becomes this CTA's fp32 partial tile
-    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int q = warp & 3, grp = (warp - 2) >> 2;
     mbar_wait(&tfull[0], 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int r = q * 32 + lane;
     float* row = red + (long)r * BN;
 #pragma unroll 1
-    for (int c = 32 * half; c < BN; c += 64) {
+    for (int c = 32 * grp; c < BN; c += 32 * (kEpiWarps / 4)) {
       uint32_t v[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
 #pragma unroll
@@ -515,10 +538,10 @@ static bool make_map(CUtensorMap* map, const void* ptr, long inner, long outer, 
   return r == CUDA_SUCCESS;
 }
 
-template <typename TO, bool A_K, bool B_K, int BN>
+template <typename TO, bool A_K, bool B_K, int BN, int F>
 static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const Sched& sc,
                const Epilogue<TO>& ep, float* part, cudaStream_t s) {
-  auto kern = gemm_tc_kernel<TO, A_K, B_K, BN>;
+  auto kern = gemm_tc_kernel<TO, A_K, B_K, BN, F>;
   constexpr int smem = Smem<BN>::TOTAL;
   static bool attr_set = false;
   if (!attr_set) {
@@ -526,25 +549,58 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
     attr_set = true;
   }
   const int grid = sc.items < kNumSMs ? sc.items : kNumSMs;
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, M, N, K, sc, ep, part);
+  launch_k(kern, grid, kThreads, smem, s, ma, mb, M, N, K, sc, ep, part);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
 
-template <typename TO, bool A_K, bool B_K>
+template <typename TO, bool A_K, bool B_K, int F>
 static int dispatch_bn(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
                        const Sched& sc, const Epilogue<TO>& ep, float* part, cudaStream_t s) {
   switch (bn) {
-    case 256: return run<TO, A_K, B_K, 256>(ma, mb, M, N, K, sc, ep, part, s);
-    case 192: return run<TO, A_K, B_K, 192>(ma, mb, M, N, K, sc, ep, part, s);
-    case 128: return run<TO, A_K, B_K, 128>(ma, mb, M, N, K, sc, ep, part, s);
-    case 64: return run<TO, A_K, B_K, 64>(ma, mb, M, N, K, sc, ep, part, s);
-    case 32: return run<TO, A_K, B_K, 32>(ma, mb, M, N, K, sc, ep, part, s);
-    default: return run<TO, A_K, B_K, 16>(ma, mb, M, N, K, sc, ep, part, s);
+    case 256: return run<TO, A_K, B_K, 256, F>(ma, mb, M, N, K, sc, ep, part, s);
+    case 192: return run<TO, A_K, B_K, 192, F>(ma, mb, M, N, K, sc, ep, part, s);
+    case 128: return run<TO, A_K, B_K, 128, F>(ma, mb, M, N, K, sc, ep, part, s);
+    case 64: return run<TO, A_K, B_K, 64, F>(ma, mb, M, N, K, sc, ep, part, s);
+    case 32: return run<TO, A_K, B_K, 32, kEFGeneric>(ma, mb, M, N, K, sc, ep, part, s);
+    default: return run<TO, A_K, B_K, 16, kEFGeneric>(ma, mb, M, N, K, sc, ep, part, s);
   }
 }
 
+// epilogue specialisations instantiated per operand layout (bf16 outputs):
+//   forward (A K-major, W MN-major): bias | bias+res | bias+GELU' | plain | bias+ReLU
+//   dgrad   (both K-major)         : plain | ReLU mask | stored-derivative mask
+template <typename TO, bool A_K, bool B_K>
+static int dispatch_f(int f, int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
+                      int K, const Sched& sc, const Epilogue<TO>& ep, float* part,
+                      cudaStream_t s) {
+  if (sc.splits > 1 || sizeof(TO) == 4)   // fp32 partials / fp32 outputs: generic
+    return dispatch_bn<TO, A_K, B_K, kEFGeneric>(bn, ma, mb, M, N, K, sc, ep, part, s);
+  if constexpr (A_K && !B_K) {
+    switch (f) {
+      case 0: return dispatch_bn<TO, A_K, B_K, 0>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      case kEFBias: return dispatch_bn<TO, A_K, B_K, kEFBias>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      case kEFBias | kEFRes:
+        return dispatch_bn<TO, A_K, B_K, kEFBias | kEFRes>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      case kEFBias | kEFGeluD:
+        return dispatch_bn<TO, A_K, B_K, kEFBias | kEFGeluD>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      case kEFBias | kEFRelu:
+        return dispatch_bn<TO, A_K, B_K, kEFBias | kEFRelu>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      default: break;
+    }
+  } else if constexpr (A_K && B_K) {
+    switch (f) {
+      case 0: return dispatch_bn<TO, A_K, B_K, 0>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      case kEFMaskRelu:
+        return dispatch_bn<TO, A_K, B_K, kEFMaskRelu>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      case kEFMaskMul:
+        return dispatch_bn<TO, A_K, B_K, kEFMaskMul>(bn, ma, mb, M, N, K, sc, ep, part, s);
+      default: break;
+    }
+  }
+  return dispatch_bn<TO, A_K, B_K, kEFGeneric>(bn, ma, mb, M, N, K, sc, ep, part, s);
+}
 
 // ---- cluster split-K launcher ----------------------------------------------
 template <typename TO, bool A_K, bool B_K, int BN>
@@ -558,8 +614,10 @@ static cudaLaunchConfig_t cluster_cfg(int grid, int cs, cudaStream_t s, cudaLaun
   at[0].val.clusterDim.x = cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cfg;
 }
 template <typename TO, bool A_K, bool B_K, int BN>
@@ -581,7 +639,7 @@ static int cluster_capacity(int cs) {
   if (cap[cs] < 0) {
     cap[cs] = 0;
     if (cluster_attr_init<TO, A_K, B_K, BN>()) {
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       cudaLaunchConfig_t cfg = cluster_cfg<TO, A_K, B_K, BN>(cs * kNumSMs, cs, 0, at);
       int n = 0;
       if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_cluster_kernel<TO, A_K, B_K, BN>, &cfg) ==
@@ -600,7 +658,7 @@ static int run_cluster(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
     set_error("gemm_tc_cluster_kernel: smem attribute");
     return PPLL_ERR_CUDA;
   }
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = cluster_cfg<TO, A_K, B_K, BN>(tiles * cs, cs, s, at);
   PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_cluster_kernel<TO, A_K, B_K, BN>, ma, mb, M, N,
                                      K, mt, kps, C, ldc, vec));
@@ -611,6 +669,7 @@ template <typename TO, bool A_K, bool B_K>
 static int cluster_capacity_bn(int bn, int cs) {
   switch (bn) {
     case 256: return cluster_capacity<TO, A_K, B_K, 256>(cs);
+    case 192: return cluster_capacity<TO, A_K, B_K, 192>(cs);
     case 128: return cluster_capacity<TO, A_K, B_K, 128>(cs);
     default: return cluster_capacity<TO, A_K, B_K, 64>(cs);
   }
@@ -621,6 +680,7 @@ static int dispatch_cluster(int bn, const CUtensorMap& ma, const CUtensorMap& mb
                             cudaStream_t s) {
   switch (bn) {
     case 256: return run_cluster<TO, A_K, B_K, 256>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
+    case 192: return run_cluster<TO, A_K, B_K, 192>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
     case 128: return run_cluster<TO, A_K, B_K, 128>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
     default: return run_cluster<TO, A_K, B_K, 64>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
   }
@@ -692,8 +752,8 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   int cl_bn = 0, cl_cs = 0;
   if (plain && force_cl != 0 && K >= 8 * BK) {
     double cl_best = -1;
-    const int cb[3] = {256, 128, 64};
-    for (int i = 0; i < 3; ++i) {
+    const int cb[4] = {256, 192, 128, 64};
+    for (int i = 0; i < 4; ++i) {
       const int c = cb[i];
       if (c > 64 && N <= c / 2) continue;
       const long tiles = (long)mt * ceil_div(N, c);
@@ -727,6 +787,11 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   bool ok = a_kmajor ? make_map(&ma, A, K, M, lda, BM) : make_map(&ma, A, M, K, lda, 64);
   ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, bn) : make_map(&mb, B, N, K, ldb, 64));
   if (!ok) return PPLL_ERR_UNSUPPORTED;
+  static const int verbose = getenv("PPLL_GEMM_VERBOSE") ? atoi(getenv("PPLL_GEMM_VERBOSE")) : 0;
+  if (verbose)
+    fprintf(stderr, "[gemm_tc] M=%d N=%d K=%d %s%s bn=%d tiles=%d splits=%d cluster=%d flags=%d\n",
+            M, N, K, a_kmajor ? "A:K" : "A:MN", b_kmajor ? " B:K" : " B:MN", bn, sc.tiles,
+            sc.splits, cl_bn ? sc.splits : 0, epi_flags(ep));
   if (cl_bn) {
     const int cs = sc.splits;   // every CTA of the cluster owns >= 1 k-block
     Epilogue<TO> e = ep;
@@ -742,10 +807,11 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   e.partial = nullptr;
   float* part = sc.splits > 1 ? ws : nullptr;
   int r;
-  if (a_kmajor && !b_kmajor) r = dispatch_bn<TO, true, false>(bn, ma, mb, M, N, K, sc, e, part, s);
-  else if (a_kmajor && b_kmajor) r = dispatch_bn<TO, true, true>(bn, ma, mb, M, N, K, sc, e, part, s);
-  else if (!a_kmajor && !b_kmajor) r = dispatch_bn<TO, false, false>(bn, ma, mb, M, N, K, sc, e, part, s);
-  else r = dispatch_bn<TO, false, true>(bn, ma, mb, M, N, K, sc, e, part, s);
+  const int f = epi_flags(e);
+  if (a_kmajor && !b_kmajor) r = dispatch_f<TO, true, false>(f, bn, ma, mb, M, N, K, sc, e, part, s);
+  else if (a_kmajor && b_kmajor) r = dispatch_f<TO, true, true>(f, bn, ma, mb, M, N, K, sc, e, part, s);
+  else if (!a_kmajor && !b_kmajor) r = dispatch_f<TO, false, false>(f, bn, ma, mb, M, N, K, sc, e, part, s);
+  else r = dispatch_f<TO, false, true>(f, bn, ma, mb, M, N, K, sc, e, part, s);
   if (r || sc.splits == 1) return r;
   // deterministic split-K reduction (fixed split order) + the fused epilogue
   return launch_splitk_reduce<TO>(M, N, sc.splits, ws, ep, s);

@@ -25,6 +25,7 @@ template <typename TI, typename TO>
 __global__ void __launch_bounds__(256)
 gemm_simt_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs, long a_cs,
                  const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep, int k_per_split) {
+  pdl_entry();
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
   const int t = threadIdx.x;
@@ -90,6 +91,7 @@ gemm_simt_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs, long 
 template <typename TO>
 __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ part,
                                      Epilogue<TO> ep) {
+  pdl_entry();
   long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   long total = (long)M * N;
   for (; idx < total; idx += (long)gridDim.x * blockDim.x) {
@@ -109,6 +111,7 @@ template <typename TI, typename TO, int NP>
 __global__ void __launch_bounds__(256)
 gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
                     const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (m >= M) return;
@@ -134,6 +137,7 @@ template <typename TI, typename TO>
 __global__ void __launch_bounds__(256)
 gemm_dot_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs, long a_cs,
                 const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep, int m_fast) {
+  pdl_entry();
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long)M * N) return;
   const int m = m_fast ? (int)(idx % M) : (int)(idx / N);
@@ -160,9 +164,9 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
     Epilogue<TO> e = ep;
     e.partial = nullptr;
     if (N <= 16)
-      gemm_rowwarp_kernel<TI, TO, 16><<<ceil_div(M, 8), 256, 0, s>>>(M, N, K, A, a_rs, B, b_rs, b_cs, e);
+      launch_k(gemm_rowwarp_kernel<TI, TO, 16>, ceil_div(M, 8), 256, 0, s, M, N, K, A, a_rs, B, b_rs, b_cs, e);
     else
-      gemm_rowwarp_kernel<TI, TO, 32><<<ceil_div(M, 8), 256, 0, s>>>(M, N, K, A, a_rs, B, b_rs, b_cs, e);
+      launch_k(gemm_rowwarp_kernel<TI, TO, 32>, ceil_div(M, 8), 256, 0, s, M, N, K, A, a_rs, B, b_rs, b_cs, e);
     note_launch();
     PPLL_LAUNCH_CHECK();
     return PPLL_OK;
@@ -173,7 +177,7 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
     // fastest thread index along the dimension whose streamed operand is contiguous:
     // m when A is m-contiguous and N is small (its B element is then a warp broadcast)
     const int m_fast = (a_rs == 1 && (b_cs != 1 || N <= 32)) ? 1 : 0;
-    gemm_dot_kernel<TI, TO><<<ceil_div((long)M * N, 256), 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B,
+    launch_k(gemm_dot_kernel<TI, TO>, ceil_div((long)M * N, 256), 256, 0, s, M, N, K, A, a_rs, a_cs, B,
                                                                          b_rs, b_cs, e, m_fast);
     note_launch();
     PPLL_LAUNCH_CHECK();
@@ -195,17 +199,17 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
   if (splits == 1) {
     Epilogue<TO> e = ep;
     e.partial = nullptr;
-    gemm_simt_kernel<TI, TO><<<grid, 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, e, K);
+    launch_k(gemm_simt_kernel<TI, TO>, grid, 256, 0, s, M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, e, K);
     note_launch();
   } else {
     Epilogue<TO> e = ep;
     e.partial = ws;
-    gemm_simt_kernel<TI, TO><<<grid, 256, 0, s>>>(M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, e, kps);
+    launch_k(gemm_simt_kernel<TI, TO>, grid, 256, 0, s, M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, e, kps);
     note_launch();
     Epilogue<TO> r = ep;
     r.partial = nullptr;
     int blocks = min(ceil_div((long)M * N, 256), 148 * 8);
-    splitk_reduce_kernel<TO><<<blocks, 256, 0, s>>>(M, N, splits, ws, r);
+    launch_k(splitk_reduce_kernel<TO>, blocks, 256, 0, s, M, N, splits, ws, r);
     note_launch();
   }
   PPLL_LAUNCH_CHECK();
@@ -218,7 +222,7 @@ int launch_splitk_reduce(int M, int N, int splits, const float* ws, const Epilog
   Epilogue<TO> r = ep;
   r.partial = nullptr;
   int blocks = min(ceil_div((long)M * N, 256), 148 * 8);
-  splitk_reduce_kernel<TO><<<blocks, 256, 0, s>>>(M, N, splits, ws, r);
+  launch_k(splitk_reduce_kernel<TO>, blocks, 256, 0, s, M, N, splits, ws, r);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -239,6 +243,7 @@ template int launch_gemm_simt<__nv_bfloat16, float>(int, int, int, const __nv_bf
 template <typename T>
 __global__ void colsum_kernel(int M, int N, const T* __restrict__ G, long ld, int rpc,
                               float* __restrict__ out) {
+  pdl_entry();
   __shared__ float red[8][33];
   const int n = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * rpc, r1 = min(M, r0 + rpc);
@@ -268,12 +273,12 @@ int launch_colsum(int M, int N, const T* G, int ld, float* db, cudaStream_t s, f
   const int rpc = ceil_div(M, chunks);
   chunks = ceil_div(M, rpc);
   if (chunks <= 1) {
-    colsum_kernel<T><<<dim3(ceil_div(N, 32), 1), dim3(32, 8), 0, s>>>(M, N, G, ld, M, db);
+    launch_k(colsum_kernel<T>, dim3(ceil_div(N, 32), 1), dim3(32, 8), 0, s, M, N, G, ld, M, db);
     note_launch();
   } else {
-    colsum_kernel<T><<<dim3(ceil_div(N, 32), chunks), dim3(32, 8), 0, s>>>(M, N, G, ld, rpc, ws);
+    launch_k(colsum_kernel<T>, dim3(ceil_div(N, 32), chunks), dim3(32, 8), 0, s, M, N, G, ld, rpc, ws);
     note_launch();
-    colsum_kernel<float><<<dim3(ceil_div(N, 32), 1), dim3(32, 8), 0, s>>>(chunks, N, ws, N,
+    launch_k(colsum_kernel<float>, dim3(ceil_div(N, 32), 1), dim3(32, 8), 0, s, chunks, N, ws, N,
                                                                            chunks, db);
     note_launch();
   }
@@ -292,6 +297,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024)
 softmax_xent_kernel(int B, int C, const T* __restrict__ z, int ldz, const int64_t* __restrict__ y,
                     T* __restrict__ dz, int lddz, float* loss_hist, const int* step, int* err) {
+  pdl_entry();
   extern __shared__ float row_loss[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const float invB = 1.0f / (float)B;
@@ -344,7 +350,7 @@ int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* 
     set_error("softmax_xent: batch %d too large", B);
     return PPLL_ERR_ARG;
   }
-  softmax_xent_kernel<T><<<1, threads, smem, s>>>(B, C, z, ldz, y, dz, lddz, loss_hist, step, err);
+  launch_k(softmax_xent_kernel<T>, 1, threads, smem, s, B, C, z, ldz, y, dz, lddz, loss_hist, step, err);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(256)
 nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const float* __restrict__ g,
                 __nv_bfloat16* __restrict__ th_lp, const float* __restrict__ lr_table, int* step,
                 int max_step, float lr_host, float mu, float wd, int* err, unsigned int* done) {
+  pdl_entry();
   __shared__ int s_skip;
   __shared__ float s_lr;
   if (threadIdx.x == 0) {
@@ -441,7 +448,7 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
   }
   // step points to two int32 words: [step_count, block-completion scratch]
   unsigned int* done = step ? reinterpret_cast<unsigned int*>(step + 1) : nullptr;
-  nesterov_kernel<<<blocks, 256, 0, s>>>(n, th, v, g, th_lp, lr_table, step, max_step, lr_host,
+  launch_k(nesterov_kernel, blocks, 256, 0, s, n, th, v, g, th_lp, lr_table, step, max_step, lr_host,
                                          mu, wd, err, done);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -453,6 +460,7 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
 // ------------------------------------------------------------------------
 template <typename TS, typename TD>
 __global__ void cast_kernel(long n, const TS* __restrict__ s, TD* __restrict__ d) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     DT<TD>::st(d + i, to_f(s[i]));
 }
@@ -461,13 +469,13 @@ int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t
   int blocks = (int)min((n + 255) / 256, (long)148 * 8);
   if (blocks < 1) return PPLL_OK;
   if (sd == PPLL_F32 && dd == PPLL_BF16)
-    cast_kernel<<<blocks, 256, 0, s>>>(n, (const float*)src, (__nv_bfloat16*)dst);
+    launch_k(cast_kernel<float, __nv_bfloat16>, blocks, 256, 0, s, n, (const float*)src, (__nv_bfloat16*)dst);
   else if (sd == PPLL_BF16 && dd == PPLL_F32)
-    cast_kernel<<<blocks, 256, 0, s>>>(n, (const __nv_bfloat16*)src, (float*)dst);
+    launch_k(cast_kernel<__nv_bfloat16, float>, blocks, 256, 0, s, n, (const __nv_bfloat16*)src, (float*)dst);
   else if (sd == PPLL_F32 && dd == PPLL_F32)
-    cast_kernel<<<blocks, 256, 0, s>>>(n, (const float*)src, (float*)dst);
+    launch_k(cast_kernel<float, float>, blocks, 256, 0, s, n, (const float*)src, (float*)dst);
   else
-    cast_kernel<<<blocks, 256, 0, s>>>(n, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst);
+    launch_k(cast_kernel<__nv_bfloat16, __nv_bfloat16>, blocks, 256, 0, s, n, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -477,6 +485,7 @@ int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t
 template <typename T>
 __global__ void relu_mask_kernel(long n, const T* __restrict__ g, const T* __restrict__ act,
                                  T* __restrict__ out) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     DT<T>::st(out + i, to_f(act[i]) > 0.f ? to_f(g[i]) : 0.f);
 }
@@ -485,9 +494,9 @@ int launch_relu_mask(long n, const void* g, const void* act, void* out, int dtyp
   int blocks = (int)min((n + 255) / 256, (long)148 * 8);
   if (blocks < 1) return PPLL_OK;
   if (dtype == PPLL_F32)
-    relu_mask_kernel<<<blocks, 256, 0, s>>>(n, (const float*)g, (const float*)act, (float*)out);
+    launch_k(relu_mask_kernel<float>, blocks, 256, 0, s, n, (const float*)g, (const float*)act, (float*)out);
   else
-    relu_mask_kernel<<<blocks, 256, 0, s>>>(n, (const __nv_bfloat16*)g, (const __nv_bfloat16*)act,
+    launch_k(relu_mask_kernel<__nv_bfloat16>, blocks, 256, 0, s, n, (const __nv_bfloat16*)g, (const __nv_bfloat16*)act,
                                             (__nv_bfloat16*)out);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -504,6 +513,7 @@ __global__ void gather_rows_kernel(int n, long width, const float* __restrict__ 
                                    const int64_t* __restrict__ idx, TD* __restrict__ dst,
                                    const int64_t* __restrict__ ysrc, int64_t* __restrict__ ydst,
                                    int vec) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n) return;
@@ -533,10 +543,10 @@ int launch_gather_rows(int n, long width, const float* src, const int64_t* idx, 
                   ((uintptr_t)dst & (dst_dtype == PPLL_F32 ? 15 : 7)) == 0;
   const int blocks = (n + 7) / 8;
   if (dst_dtype == PPLL_F32)
-    gather_rows_kernel<float><<<blocks, 256, 0, s>>>(n, width, src, idx, (float*)dst, ysrc, ydst,
+    launch_k(gather_rows_kernel<float>, blocks, 256, 0, s, n, width, src, idx, (float*)dst, ysrc, ydst,
                                                      vec);
   else
-    gather_rows_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(n, width, src, idx,
+    launch_k(gather_rows_kernel<__nv_bfloat16>, blocks, 256, 0, s, n, width, src, idx,
                                                              (__nv_bfloat16*)dst, ysrc, ydst, vec);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -548,6 +558,7 @@ int launch_gather_rows(int n, long width, const float* src, const int64_t* idx, 
 template <typename T>
 __global__ void count_correct_kernel(int B, int C, const T* __restrict__ z, long ldz,
                                      const int64_t* __restrict__ y, unsigned long long* count) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= B) return;
@@ -571,9 +582,9 @@ int launch_count_correct(int B, int C, const void* z, long ldz, int dtype, const
   if (B <= 0) return PPLL_OK;
   const int blocks = (B + 7) / 8;
   if (dtype == PPLL_F32)
-    count_correct_kernel<<<blocks, 256, 0, s>>>(B, C, (const float*)z, ldz, y, count);
+    launch_k(count_correct_kernel<float>, blocks, 256, 0, s, B, C, (const float*)z, ldz, y, count);
   else
-    count_correct_kernel<<<blocks, 256, 0, s>>>(B, C, (const __nv_bfloat16*)z, ldz, y, count);
+    launch_k(count_correct_kernel<__nv_bfloat16>, blocks, 256, 0, s, B, C, (const __nv_bfloat16*)z, ldz, y, count);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -592,32 +603,35 @@ __device__ __forceinline__ void st_release_sys(int* p, int v) {
 }
 
 __global__ void ring_publish_kernel(int* w, int seq) {
+  pdl_entry();
   __threadfence_system();
   st_release_sys(w, seq);
 }
 __global__ void ring_wait_kernel(const int* w, int seq) {
+  pdl_entry();
   while (ld_acquire_sys(w) < seq) __nanosleep(64);
   __threadfence_system();
 }
 __global__ void ring_release_kernel(int* w) {
+  pdl_entry();
   __threadfence_system();
   atomicAdd_system(w, 1);
 }
 
 int launch_ring_publish(int* w, int seq, cudaStream_t s) {
-  ring_publish_kernel<<<1, 1, 0, s>>>(w, seq);
+  launch_k(ring_publish_kernel, 1, 1, 0, s, w, seq);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
 int launch_ring_wait(const int* w, int seq, cudaStream_t s) {
-  ring_wait_kernel<<<1, 1, 0, s>>>(w, seq);
+  launch_k(ring_wait_kernel, 1, 1, 0, s, w, seq);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
 int launch_ring_release(int* w, cudaStream_t s) {
-  ring_release_kernel<<<1, 1, 0, s>>>(w);
+  launch_k(ring_release_kernel, 1, 1, 0, s, w);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

@@ -136,6 +136,40 @@ __device__ __forceinline__ void ld_row32<__nv_bfloat16>(const __nv_bfloat16* p, 
     for (int i = 0; i < 32; ++i) o[i] = i < valid ? __bfloat162float(p[i]) : 0.f;
   }
 }
+// NV consecutive elements (NV % 8 == 0), 16-B vectors when `vec` and all valid
+template <int NV>
+__device__ __forceinline__ void ld_rowN(const float* p, bool vec, int valid, float (&o)[NV]) {
+  if (vec && valid == NV) {
+#pragma unroll
+    for (int i = 0; i < NV / 4; ++i) {
+      const float4 q = reinterpret_cast<const float4*>(p)[i];
+      o[4 * i] = q.x; o[4 * i + 1] = q.y; o[4 * i + 2] = q.z; o[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) o[i] = i < valid ? p[i] : 0.f;
+  }
+}
+template <int NV>
+__device__ __forceinline__ void ld_rowN(const __nv_bfloat16* p, bool vec, int valid, float (&o)[NV]) {
+  if (vec && valid == NV) {
+#pragma unroll
+    for (int i = 0; i < NV / 8; ++i) {
+      const uint4 q = reinterpret_cast<const uint4*>(p)[i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        o[8 * i + 2 * j] = f.x;
+        o[8 * i + 2 * j + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) o[i] = i < valid ? __bfloat162float(p[i]) : 0.f;
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void st_row32(T* p, bool vec, int valid, const float (&v)[32]);
 template <>
@@ -252,6 +286,159 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
   }
 }
 
+// Coalesced store of a warp's 32-row x 16-column block (thread = one row, 16
+// consecutive columns in registers, as tcgen05.ld 32x32b.x16 delivers them),
+// transposed through a 1-KB per-warp buffer: rows of 32 B (two 16-B chunks,
+// swapped on every other group of four rows so both the row-wise writes and
+// the column-wise reads are bank-conflict free); each store instruction then
+// covers 16 rows x 32 contiguous bytes (one full sector per row).  fp32 goes
+// in two 8-column passes.  `csum` as in warp_store_block32.
+template <typename TO>
+__device__ __forceinline__ void warp_store_block16(TO* out, long ld, TO* out2, long ld2, int row0,
+                                                   int M, int n0, int N, bool vec,
+                                                   const float (&v)[16], uint8_t* stg, int lane,
+                                                   float* csum = nullptr) {
+  constexpr int kEl = 16 / (int)sizeof(TO);          // elements per 16-B chunk
+  constexpr int kPasses = sizeof(TO) == 4 ? 2 : 1;   // 32-B row slices per 16 columns
+  constexpr int kCols = 16 / kPasses;                // columns per pass
+#pragma unroll
+  for (int p = 0; p < kPasses; ++p) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint4 q;
+      if constexpr (sizeof(TO) == 4) {
+        q = make_uint4(__float_as_uint(v[p * kCols + 4 * j]), __float_as_uint(v[p * kCols + 4 * j + 1]),
+                       __float_as_uint(v[p * kCols + 4 * j + 2]), __float_as_uint(v[p * kCols + 4 * j + 3]));
+      } else {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          h[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+      }
+      const int sj = j ^ ((lane >> 2) & 1);
+      *reinterpret_cast<uint4*>(stg + lane * 32 + sj * 16) = q;
+    }
+    __syncwarp();
+    float cs[kEl];
+#pragma unroll
+    for (int e = 0; e < kEl; ++e) cs[e] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = i * 16 + (lane >> 1), c = lane & 1;
+      const uint4 q = *reinterpret_cast<const uint4*>(stg + r * 32 + ((c ^ ((r >> 2) & 1)) * 16));
+      const int row = row0 + r;
+      const int col = n0 + p * kCols + c * kEl;
+      if (csum && row < M) {
+        const TO* e = reinterpret_cast<const TO*>(&q);
+#pragma unroll
+        for (int t = 0; t < kEl; ++t) cs[t] += to_f(e[t]);
+      }
+      if (row < M && col < N) {
+        if (vec && col + kEl <= N) {
+          *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
+          if (out2) *reinterpret_cast<uint4*>(out2 + (long)row * ld2 + col) = q;
+        } else {
+          const TO* e = reinterpret_cast<const TO*>(&q);
+          for (int t = 0; t < kEl && col + t < N; ++t) {
+            out[(long)row * ld + col + t] = e[t];
+            if (out2) out2[(long)row * ld2 + col + t] = e[t];
+          }
+        }
+      }
+    }
+    if (csum && row0 < M) {   // lanes with equal (lane & 1) hold the same columns
+#pragma unroll
+      for (int t = 0; t < kEl; ++t) {
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 2);
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 4);
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 8);
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 16);
+      }
+      const int col = n0 + p * kCols + (lane & 1) * kEl;
+      if (lane < 2) {
+        for (int t = 0; t < kEl; ++t)
+          if (col + t < N) csum[col + t] = cs[t];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Coalesced load of a warp's 32-row x 16-column bf16 block into thread-row
+// registers (the inverse of warp_store_block16): issue() puts 16 rows x 32 B
+// per instruction in flight (full sectors), finish() transposes them through
+// the same 1-KB swizzled buffer so lane r holds row r's 16 values.
+__device__ __forceinline__ void blk16_issue(const __nv_bfloat16* src, long ld, int row0, int M,
+                                            int n0, int N, bool vec, uint4 (&q)[2], int lane) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = i * 16 + (lane >> 1), c = lane & 1;
+    const int row = row0 + r, col = n0 + c * 8;
+    q[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (row < M && col < N) {
+      const __nv_bfloat16* p = src + (long)row * ld + col;
+      if (vec && col + 8 <= N) {
+        q[i] = *reinterpret_cast<const uint4*>(p);
+      } else {
+        __nv_bfloat16* e = reinterpret_cast<__nv_bfloat16*>(&q[i]);
+        for (int t = 0; t < 8 && col + t < N; ++t) e[t] = p[t];
+      }
+    }
+  }
+}
+__device__ __forceinline__ void blk16_finish(const uint4 (&q)[2], float (&k)[16], uint8_t* stg,
+                                             int lane) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = i * 16 + (lane >> 1), c = lane & 1;
+    *reinterpret_cast<uint4*>(stg + r * 32 + ((c ^ ((r >> 2) & 1)) * 16)) = q[i];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint4 t = *reinterpret_cast<const uint4*>(stg + lane * 32 + ((j ^ ((lane >> 2) & 1)) * 16));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      k[8 * j + 2 * e] = f.x;
+      k[8 * j + 2 * e + 1] = f.y;
+    }
+  }
+  __syncwarp();
+}
+
+// bf16-output GELU pair on the tanh form (one MUFU tanh per element, packed
+// FP32x2 arithmetic):  u = √(2/π)(x + 0.044715x³),  gelu = ½x(1 + tanh u),
+// gelu' = ½(1 + t) + ½x(1 − t²)·√(2/π)(1 + 0.134145x²).  Its distance to the
+// erf GELU (≤ 5e-4 absolute, tanh.approx included) is far below the bf16
+// resolution of the stored activations; fp32 outputs keep gelu_both2 (erf).
+__device__ __forceinline__ float tanh_approx(float x) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void gelu_tanh2(float& x0, float& x1, float& d0, float& d1) {
+  const f2 x{x0, x1};
+  const f2 x2 = fmul2(x, x);
+  const f2 p = ffma2(x2, splat2(0.0356774081363001f), splat2(0.7978845608028654f));
+  const f2 u = fmul2(x, p);
+  const f2 t{tanh_approx(u.x), tanh_approx(u.y)};
+  const f2 hx = fmul2(x, splat2(0.5f));
+  const f2 g = ffma2(hx, t, hx);
+  const f2 omt = ffma2(t, f2{-t.x, -t.y}, splat2(1.f));
+  const f2 q = ffma2(x2, splat2(0.1070322244089003f), splat2(0.7978845608028654f));
+  const f2 d = ffma2(fmul2(hx, omt), q, ffma2(t, splat2(0.5f), splat2(0.5f)));
+  x0 = g.x; x1 = g.y; d0 = d.x; d1 = d.y;
+}
+
+// Compile-time epilogue specialisations of the tcgen05 engine (the runtime
+// flag tests of the generic form cost ~40% of the epilogue's instructions).
+enum EpiF : int {
+  kEFBias = 1, kEFRes = 2, kEFRelu = 4, kEFGeluD = 8, kEFMaskRelu = 16, kEFMaskMul = 32,
+  kEFGeneric = 1 << 10
+};
+
 // GEMM epilogue:
 //   v -> (+bias[n]) -> (+R[m,n]) -> [store pre-activation P] -> act (ReLU|GELU)
 //     -> ReLU mask (v·[mask>0]) | GELU gradient (v·gelu'(mask)) | v·mask -> C (and C2)
@@ -306,15 +493,16 @@ struct Epilogue {
   // activation (with the GeluD derivative written into d) and mask, in place.
   // One GELU evaluation per element: on v (act GELU/GeluD) or on the mask
   // (GELU-gradient mask); the two are never combined (host-checked).
-  __device__ __forceinline__ void act_mask32(float (&v)[32], const float (&k)[32],
-                                             float (&d)[32]) const {
+  template <int NV>
+  __device__ __forceinline__ void act_mask(float (&v)[NV], const float (&k)[NV],
+                                           float (&d)[NV]) const {
     const bool ga = act == kActGelu || act == kActGeluD;
     if (ga) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) gelu_both2(v[i], v[i + 1], d[i], d[i + 1]);
+      for (int i = 0; i < NV; i += 2) gelu_both2(v[i], v[i + 1], d[i], d[i + 1]);
     } else if (mask_mode == kMaskGeluGrad) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < NV; i += 2) {
         float g0 = k[i], g1 = k[i + 1];
         gelu_both2(g0, g1, d[i], d[i + 1]);
         const f2 r = fmul2(f2{v[i], v[i + 1]}, f2{d[i], d[i + 1]});
@@ -322,14 +510,14 @@ struct Epilogue {
       }
     } else if (act == kActRelu) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      for (int i = 0; i < NV; ++i) v[i] = fmaxf(v[i], 0.f);
     }
     if (mask_mode == kMaskRelu) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
+      for (int i = 0; i < NV; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
     } else if (mask_mode == kMaskMul) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < NV; i += 2) {
         const f2 r = fmul2(f2{v[i], v[i + 1]}, f2{k[i], k[i + 1]});
         v[i] = r.x; v[i + 1] = r.y;
       }
@@ -361,11 +549,137 @@ struct Epilogue {
     }
     if (pre && act != kActGeluD)
       warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, v, stg, lane);
-    act_mask32(v, k, r);
+    act_mask<32>(v, k, r);
     if (pre && act == kActGeluD)
       warp_store_block32<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg, lane);
     warp_store_block32<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane,
                            cs_part ? cs_part + (long)(row0 >> 5) * ncols : nullptr);
+  }
+
+  // 16-column forms used by the tcgen05 engine (tcgen05.ld 32x32b.x16 chunks)
+  __device__ __forceinline__ void load_aux16(int m, int n0, float (&r)[16], float (&k)[16]) const {
+    const int valid = min(16, ncols - n0);
+    if (res) ld_rowN<16>(res + (long)m * ldres + n0, vec != 0, valid, r);
+    if (mask_mode != kMaskNone) ld_rowN<16>(mask + (long)m * ldmask + n0, vec != 0, valid, k);
+  }
+  __device__ __forceinline__ void finish_block16(int row0, int M, int n0, float (&v)[16],
+                                                 float (&r)[16], const float (&k)[16],
+                                                 const float* bias_s, uint8_t* stg,
+                                                 int lane) const {
+    const bool vv = vec != 0;
+    if (bias) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const float2 bb = *reinterpret_cast<const float2*>(bias_s + i);
+        const f2 t = fadd2(f2{v[i], v[i + 1]}, f2{bb.x, bb.y});
+        v[i] = t.x; v[i + 1] = t.y;
+      }
+    }
+    if (res) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const f2 t = fadd2(f2{v[i], v[i + 1]}, f2{r[i], r[i + 1]});
+        v[i] = t.x; v[i + 1] = t.y;
+      }
+    }
+    if (pre && act != kActGeluD)
+      warp_store_block16<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, v, stg, lane);
+    act_mask<16>(v, k, r);
+    if (pre && act == kActGeluD)
+      warp_store_block16<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg, lane);
+    warp_store_block16<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane,
+                           cs_part ? cs_part + (long)(row0 >> 5) * ncols : nullptr);
+  }
+
+  // specialised forms (F = EpiF bits, or kEFGeneric -> the runtime forms);
+  // C2 (ring push) and cs_part (fused column sums) stay runtime options
+  // bf16 specialisations: coalesced block loads issued before the TMEM load
+  // (aux_issue) and transposed into thread rows after it (aux_finish)
+  template <int F>
+  static constexpr bool kBlockAux = F != kEFGeneric && sizeof(TO) == 2 &&
+                                    (F & (kEFRes | kEFMaskRelu | kEFMaskMul)) != 0;
+  template <int F>
+  __device__ __forceinline__ void aux_issue(int row0, int M, int n0, uint4 (&qr)[2],
+                                            uint4 (&qk)[2], int lane) const {
+    if constexpr (kBlockAux<F>) {
+      if constexpr ((F & kEFRes) != 0)
+        blk16_issue(reinterpret_cast<const __nv_bfloat16*>(res), ldres, row0, M, n0, ncols,
+                    vec != 0, qr, lane);
+      if constexpr ((F & (kEFMaskRelu | kEFMaskMul)) != 0)
+        blk16_issue(reinterpret_cast<const __nv_bfloat16*>(mask), ldmask, row0, M, n0, ncols,
+                    vec != 0, qk, lane);
+    }
+  }
+  template <int F>
+  __device__ __forceinline__ void aux_finish(const uint4 (&qr)[2], const uint4 (&qk)[2],
+                                             float (&r)[16], float (&k)[16], uint8_t* stg,
+                                             int lane) const {
+    if constexpr (kBlockAux<F>) {
+      if constexpr ((F & kEFRes) != 0) blk16_finish(qr, r, stg, lane);
+      if constexpr ((F & (kEFMaskRelu | kEFMaskMul)) != 0) blk16_finish(qk, k, stg, lane);
+    }
+  }
+  template <int F>
+  __device__ __forceinline__ void load_aux16_t(int m, int n0, float (&r)[16], float (&k)[16]) const {
+    if constexpr (F == kEFGeneric) {
+      load_aux16(m, n0, r, k);
+    } else if constexpr (!kBlockAux<F>) {
+      const int valid = min(16, ncols - n0);
+      if constexpr ((F & kEFRes) != 0) ld_rowN<16>(res + (long)m * ldres + n0, vec != 0, valid, r);
+      if constexpr ((F & (kEFMaskRelu | kEFMaskMul)) != 0)
+        ld_rowN<16>(mask + (long)m * ldmask + n0, vec != 0, valid, k);
+    }
+  }
+  template <int F>
+  __device__ __forceinline__ void finish_block16_t(int row0, int M, int n0, float (&v)[16],
+                                                   float (&r)[16], const float (&k)[16],
+                                                   const float* bias_s, uint8_t* stg,
+                                                   int lane) const {
+    if constexpr (F == kEFGeneric) {
+      finish_block16(row0, M, n0, v, r, k, bias_s, stg, lane);
+    } else {
+      const bool vv = vec != 0;
+      if constexpr ((F & kEFBias) != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float2 bb = *reinterpret_cast<const float2*>(bias_s + i);
+          const f2 t = fadd2(f2{v[i], v[i + 1]}, f2{bb.x, bb.y});
+          v[i] = t.x; v[i + 1] = t.y;
+        }
+      }
+      if constexpr ((F & kEFRes) != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const f2 t = fadd2(f2{v[i], v[i + 1]}, f2{r[i], r[i + 1]});
+          v[i] = t.x; v[i + 1] = t.y;
+        }
+      }
+      if constexpr ((F & kEFGeluD) != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          if constexpr (sizeof(TO) == 2) gelu_tanh2(v[i], v[i + 1], r[i], r[i + 1]);
+          else gelu_both2(v[i], v[i + 1], r[i], r[i + 1]);
+        }
+        warp_store_block16<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg, lane);
+      }
+      if constexpr ((F & kEFRelu) != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      if constexpr ((F & kEFMaskRelu) != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = k[i] > 0.f ? v[i] : 0.f;
+      }
+      if constexpr ((F & kEFMaskMul) != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const f2 t = fmul2(f2{v[i], v[i + 1]}, f2{k[i], k[i + 1]});
+          v[i] = t.x; v[i + 1] = t.y;
+        }
+      }
+      warp_store_block16<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane,
+                             cs_part ? cs_part + (long)(row0 >> 5) * ncols : nullptr);
+    }
   }
 
   // 32 consecutive columns n0..n0+31 of row m (n0 % 32 == 0)
@@ -385,12 +699,28 @@ struct Epilogue {
     if (pre && act != kActGeluD) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, v);
     float k[32], d[32];
     if (mask_mode != kMaskNone) ld_row32<TO>(mask + (long)m * ldmask + n0, vv, valid, k);
-    act_mask32(v, k, d);
+    act_mask<32>(v, k, d);
     if (pre && act == kActGeluD) st_row32<TO>(pre + (long)m * ldpre + n0, vv, valid, d);
     st_row32<TO>(C + (long)m * ldc + n0, vv, valid, v);
     if (C2) st_row32<TO>(C2 + (long)m * ldc2 + n0, vv, valid, v);
   }
 };
+
+// host: the compile-time epilogue specialisation matching `e` (or kEFGeneric)
+template <typename TO>
+inline int epi_flags(const Epilogue<TO>& e) {
+  int f = 0;
+  if (e.bias) f |= kEFBias;
+  if (e.res) f |= kEFRes;
+  if (e.act == kActRelu) f |= kEFRelu;
+  else if (e.act == kActGeluD && e.pre) f |= kEFGeluD;
+  else if (e.act != kActNone) return kEFGeneric;
+  if (e.pre && e.act != kActGeluD) return kEFGeneric;
+  if (e.mask_mode == kMaskRelu) f |= kEFMaskRelu;
+  else if (e.mask_mode == kMaskMul) f |= kEFMaskMul;
+  else if (e.mask_mode != kMaskNone) return kEFGeneric;
+  return f;
+}
 
 // host: decide the vector flag from pointer alignment and leading dimensions
 template <typename TO>

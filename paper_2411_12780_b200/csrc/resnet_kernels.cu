@@ -20,6 +20,7 @@ static int grid_for(long n, int threads = 256) {
 template <typename T>
 __global__ void im2col_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo, int Kp,
                               const T* __restrict__ x, T* __restrict__ col) {
+  pdl_entry();
   const int p = (k - 1) / 2;
   const long total = (long)N * Ho * Wo * Kp;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -40,6 +41,7 @@ __global__ void im2col_kernel(int N, int H, int W, int C, int k, int stride, int
 template <typename T>
 __global__ void im2col_vec_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo,
                                   int Kp, const T* __restrict__ x, T* __restrict__ col) {
+  pdl_entry();
   // one thread per 8-channel vector (16 B for bf16)
   const int p = (k - 1) / 2;
   const int C8 = C / 8, K8 = Kp / 8;
@@ -68,10 +70,10 @@ int launch_im2col(int N, int H, int W, int C, int k, int stride, int Kp, const T
   const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
   if (sizeof(T) == 2 && C % 8 == 0 && Kp % 8 == 0) {
     const long n = (long)N * Ho * Wo * (Kp / 8);
-    im2col_vec_kernel<T><<<grid_for(n), 256, 0, s>>>(N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
+    launch_k(im2col_vec_kernel<T>, grid_for(n), 256, 0, s, N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
   } else {
     const long n = (long)N * Ho * Wo * Kp;
-    im2col_kernel<T><<<grid_for(n), 256, 0, s>>>(N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
+    launch_k(im2col_kernel<T>, grid_for(n), 256, 0, s, N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
   }
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -86,6 +88,7 @@ template <typename T>
 __global__ void col2im_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo, int Kp,
                               const T* __restrict__ dcol, const T* __restrict__ dres,
                               const T* __restrict__ mask, T* __restrict__ dx) {
+  pdl_entry();
   const int p = (k - 1) / 2;
   const long total = (long)N * H * W * C;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -128,6 +131,7 @@ __global__ void col2im_vec_kernel(int N, int H, int W, int C, int k, int stride,
                                   const __nv_bfloat16* __restrict__ dres,
                                   const __nv_bfloat16* __restrict__ mask,
                                   __nv_bfloat16* __restrict__ dx) {
+  pdl_entry();
   const int p = (k - 1) / 2, C8 = C / 8;
   const long total = (long)N * H * W * C8;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -177,7 +181,7 @@ int launch_col2im(int N, int H, int W, int C, int k, int stride, int Kp, const T
   const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
   if constexpr (sizeof(T) == 2) {
     if (C % 8 == 0 && Kp % 8 == 0) {
-      col2im_vec_kernel<<<grid_for((long)N * H * W * C / 8), 256, 0, s>>>(
+      launch_k(col2im_vec_kernel, grid_for((long)N * H * W * C / 8), 256, 0, s, 
           N, H, W, C, k, stride, Ho, Wo, Kp, (const __nv_bfloat16*)dcol,
           (const __nv_bfloat16*)dres, (const __nv_bfloat16*)mask, (__nv_bfloat16*)dx);
       note_launch();
@@ -185,7 +189,7 @@ int launch_col2im(int N, int H, int W, int C, int k, int stride, int Kp, const T
       return PPLL_OK;
     }
   }
-  col2im_kernel<T><<<grid_for((long)N * H * W * C), 256, 0, s>>>(N, H, W, C, k, stride, Ho, Wo,
+  launch_k(col2im_kernel<T>, grid_for((long)N * H * W * C), 256, 0, s, N, H, W, C, k, stride, Ho, Wo,
                                                                   Kp, dcol, dres, mask, dx);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -210,6 +214,7 @@ __device__ __forceinline__ Welford wf_merge(Welford a, Welford b) {
 template <typename T>
 __global__ void bn_stats_part_kernel(int P, int C, const T* __restrict__ z, int rpc,
                                      float* __restrict__ part) {
+  pdl_entry();
   __shared__ Welford red[8][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * rpc, r1 = min(P, r0 + rpc);
@@ -237,6 +242,7 @@ __global__ void bn_stats_part_kernel(int P, int C, const T* __restrict__ z, int 
 // deterministic
 __global__ void bn_stats_final_kernel(int chunks, int C, const float* __restrict__ part,
                                       float* __restrict__ mean, float* __restrict__ rstd) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= C) return;
@@ -266,9 +272,9 @@ int launch_bn_stats(int P, int C, const T* z, float* part, float* mean, float* r
                     cudaStream_t s) {
   const int chunks = bn_chunks(P);
   const int rpc = ceil_div(P, chunks);
-  bn_stats_part_kernel<T><<<dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s>>>(P, C, z, rpc, part);
+  launch_k(bn_stats_part_kernel<T>, dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s, P, C, z, rpc, part);
   note_launch();
-  bn_stats_final_kernel<<<ceil_div(C, 8), 256, 0, s>>>(chunks, C, part, mean, rstd);
+  launch_k(bn_stats_final_kernel, ceil_div(C, 8), 256, 0, s, chunks, C, part, mean, rstd);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -282,6 +288,7 @@ __global__ void bn_apply_kernel(long total, int C, const T* __restrict__ z, cons
                                 const float* __restrict__ mean2, const float* __restrict__ rstd2,
                                 const float* __restrict__ g2, const float* __restrict__ b2,
                                 const T* __restrict__ res, int relu, T* __restrict__ y) {
+  pdl_entry();
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
     const int c = (int)(idx % C);
@@ -298,7 +305,7 @@ int launch_bn_apply(long P, int C, const T* z, const float* mean, const float* r
                     const float* b, const T* z2, const float* mean2, const float* rstd2,
                     const float* g2, const float* b2, const T* res, int relu, T* y, cudaStream_t s) {
   const long total = P * C;
-  bn_apply_kernel<T><<<grid_for(total), 256, 0, s>>>(total, C, z, mean, rstd, g, b, z2, mean2,
+  launch_k(bn_apply_kernel<T>, grid_for(total), 256, 0, s, total, C, z, mean, rstd, g, b, z2, mean2,
                                                      rstd2, g2, b2, res, relu, y);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -309,6 +316,7 @@ int launch_bn_apply(long P, int C, const T* z, const float* mean, const float* r
 template <typename T>
 __global__ void relu_mask_kernel(long total, const T* __restrict__ dout, const T* __restrict__ out,
                                  T* __restrict__ dy) {
+  pdl_entry();
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x)
     DT<T>::st(dy + idx, to_f(out[idx]) > 0.f ? to_f(dout[idx]) : 0.f);
@@ -316,7 +324,7 @@ __global__ void relu_mask_kernel(long total, const T* __restrict__ dout, const T
 
 template <typename T>
 int launch_relu_mask(long n, const T* dout, const T* out, T* dy, cudaStream_t s) {
-  relu_mask_kernel<T><<<grid_for(n), 256, 0, s>>>(n, dout, out, dy);
+  launch_k(relu_mask_kernel<T>, grid_for(n), 256, 0, s, n, dout, out, dy);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -327,6 +335,7 @@ template <typename T>
 __global__ void bn_bwd_part_kernel(int P, int C, const T* __restrict__ dy, const T* __restrict__ z,
                                    const float* __restrict__ mean, const float* __restrict__ rstd,
                                    int rpc, float* __restrict__ part) {
+  pdl_entry();
   __shared__ float red[2][8][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * rpc, r1 = min(P, r0 + rpc);
@@ -356,6 +365,7 @@ __global__ void bn_bwd_part_kernel(int P, int C, const T* __restrict__ dy, const
 // one warp per channel: lane-strided partial sums, fixed butterfly
 __global__ void bn_bwd_final_kernel(int chunks, int C, const float* __restrict__ part,
                                     float* __restrict__ dg, float* __restrict__ db) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= C) return;
@@ -379,6 +389,7 @@ __global__ void bn_bwd_dx_kernel(long total, int C, float invP, const T* __restr
                                  const float* __restrict__ rstd, const float* __restrict__ g,
                                  const float* __restrict__ dg, const float* __restrict__ db,
                                  T* __restrict__ dz) {
+  pdl_entry();
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
     const int c = (int)(idx % C);
@@ -393,13 +404,13 @@ int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, cons
                   const float* g, float* part, float* dg, float* db, T* dz, cudaStream_t s) {
   const int chunks = bn_chunks(P);
   const int rpc = ceil_div(P, chunks);
-  bn_bwd_part_kernel<T><<<dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s>>>(P, C, dy, z, mean,
+  launch_k(bn_bwd_part_kernel<T>, dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s, P, C, dy, z, mean,
                                                                               rstd, rpc, part);
   note_launch();
-  bn_bwd_final_kernel<<<ceil_div(C, 8), 256, 0, s>>>(chunks, C, part, dg, db);
+  launch_k(bn_bwd_final_kernel, ceil_div(C, 8), 256, 0, s, chunks, C, part, dg, db);
   note_launch();
   const long total = (long)P * C;
-  bn_bwd_dx_kernel<T><<<grid_for(total), 256, 0, s>>>(total, C, 1.f / (float)P, dy, z, mean, rstd,
+  launch_k(bn_bwd_dx_kernel<T>, grid_for(total), 256, 0, s, total, C, 1.f / (float)P, dy, z, mean, rstd,
                                                       g, dg, db, dz);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -411,6 +422,7 @@ int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, cons
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void gap_kernel(int N, int HW, int C, const T* __restrict__ x, T* __restrict__ out) {
+  pdl_entry();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= N * C) return;
   const int n = idx / C, c = idx % C;
@@ -421,6 +433,7 @@ __global__ void gap_kernel(int N, int HW, int C, const T* __restrict__ x, T* __r
 
 template <typename T>
 __global__ void gap_bwd_kernel(int N, int HW, int C, const T* __restrict__ dp, T* __restrict__ dx) {
+  pdl_entry();
   const long total = (long)N * HW * C;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
@@ -432,14 +445,14 @@ __global__ void gap_bwd_kernel(int N, int HW, int C, const T* __restrict__ dp, T
 
 template <typename T>
 int launch_gap(int N, int HW, int C, const T* x, T* out, cudaStream_t s) {
-  gap_kernel<T><<<ceil_div(N * C, 256), 256, 0, s>>>(N, HW, C, x, out);
+  launch_k(gap_kernel<T>, ceil_div(N * C, 256), 256, 0, s, N, HW, C, x, out);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
 template <typename T>
 int launch_gap_bwd(int N, int HW, int C, const T* dp, T* dx, cudaStream_t s) {
-  gap_bwd_kernel<T><<<grid_for((long)N * HW * C), 256, 0, s>>>(N, HW, C, dp, dx);
+  launch_k(gap_bwd_kernel<T>, grid_for((long)N * HW * C), 256, 0, s, N, HW, C, dp, dx);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(256)
 ln_fwd_vkernel(int M, const T* __restrict__ x, long ldx, const float* __restrict__ g,
                const float* __restrict__ b, T* __restrict__ y, long ldy, float* __restrict__ mean,
                float* __restrict__ rstd) {
+  pdl_entry();
   constexpr int D = 16 * EPL;
   const int lane = threadIdx.x & 31, hl = lane & 15;
   const int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + (lane >> 4);
@@ -134,6 +135,7 @@ ln_bwd_vkernel(int M, const __nv_bfloat16* __restrict__ dy, long lddy,
                const float* __restrict__ rstd, const float* __restrict__ g,
                const __nv_bfloat16* __restrict__ dres, long ldres, __nv_bfloat16* __restrict__ dx,
                long lddx, float* __restrict__ part) {
+  pdl_entry();
   // LPR lanes per row (16: two rows per warp; 32: one row per warp)
   constexpr int D = LPR * EPL, NQ = EPL / 8, RPW = 32 / LPR, RPB = 8 * RPW;
   __shared__ float red[NS][D];
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(256)
 ln_fwd_kernel(int M, int D, const T* __restrict__ x, long ldx, const float* __restrict__ g,
               const float* __restrict__ b, T* __restrict__ y, long ldy, float* __restrict__ mean,
               float* __restrict__ rstd) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= M) return;
@@ -281,6 +284,7 @@ ln_bwd_kernel(int M, int D, const T* __restrict__ dy, long lddy, const T* __rest
               const float* __restrict__ mean, const float* __restrict__ rstd,
               const float* __restrict__ g, const T* __restrict__ dres, long ldres,
               T* __restrict__ dx, long lddx, float* __restrict__ part, int rows_per_block) {
+  pdl_entry();
   __shared__ float red[2][32 * VPL];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float pg[VPL], pb[VPL];
@@ -350,6 +354,7 @@ ln_bwd_kernel(int M, int D, const T* __restrict__ dy, long lddy, const T* __rest
 __global__ void __launch_bounds__(1024)
 ln_param_reduce_kernel(int nblk, int D, int NS, const float* __restrict__ part,
                        float* __restrict__ o0, float* __restrict__ o1, float* __restrict__ o2) {
+  pdl_entry();
   __shared__ float red[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x;   // column of the [nblk, NS·D] matrix
   float s = 0.f;
@@ -381,18 +386,18 @@ int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const floa
       aligned16(b)) {
     const int blocks = ceil_div(M, 16);     // 8 warps x 2 rows
     switch (D / 16) {
-#define LNF(E) case E: ln_fwd_vkernel<T, E><<<blocks, 256, 0, s>>>(M, x, ldx, g, b, y, ldy, mean, rstd); break;
+#define LNF(E) case E: launch_k(ln_fwd_vkernel<T, E>, blocks, 256, 0, s, M, x, ldx, g, b, y, ldy, mean, rstd); break;
       LNF(8) LNF(16) LNF(24) LNF(32) LNF(40) LNF(48) LNF(56) LNF(64)
 #undef LNF
     }
   } else {
     const int blocks = ceil_div(M, 8);
     if (D <= 384)
-      ln_fwd_kernel<T, 12><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+      launch_k(ln_fwd_kernel<T, 12>, blocks, 256, 0, s, M, D, x, ldx, g, b, y, ldy, mean, rstd);
     else if (D <= 768)
-      ln_fwd_kernel<T, 24><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+      launch_k(ln_fwd_kernel<T, 24>, blocks, 256, 0, s, M, D, x, ldx, g, b, y, ldy, mean, rstd);
     else
-      ln_fwd_kernel<T, 32><<<blocks, 256, 0, s>>>(M, D, x, ldx, g, b, y, ldy, mean, rstd);
+      launch_k(ln_fwd_kernel<T, 32>, blocks, 256, 0, s, M, D, x, ldx, g, b, y, ldy, mean, rstd);
   }
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -423,7 +428,7 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
     using B16 = __nv_bfloat16;
     const B16 *dyb = (const B16*)dy, *xb = (const B16*)x, *rb = (const B16*)dres;
     B16* dxb = (B16*)dx;
-#define LNB(E, NSV, L) ln_bwd_vkernel<E, NSV, L><<<nblk, 256, 0, s>>>(M, dyb, lddy, xb, ldx, mean, rstd, g, rb, ldres, dxb, lddx, part)
+#define LNB(E, NSV, L) launch_k(ln_bwd_vkernel<E, NSV, L>, nblk, 256, 0, s, M, dyb, lddy, xb, ldx, mean, rstd, g, rb, ldres, dxb, lddx, part)
 #define LNB_ALL(NSV)                          \
     switch (D) {                              \
       case 128: LNB(8, NSV, 16); break;       \
@@ -442,16 +447,16 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
   } else {
     if (dxsum && !dx) { set_error("layernorm: bias sum needs the dx output"); return PPLL_ERR_ARG; }
     if (D <= 384)
-      ln_bwd_kernel<T, 12><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+      launch_k(ln_bwd_kernel<T, 12>, nblk, 256, 0, s, M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
     else if (D <= 768)
-      ln_bwd_kernel<T, 24><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+      launch_k(ln_bwd_kernel<T, 24>, nblk, 256, 0, s, M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
     else
-      ln_bwd_kernel<T, 32><<<nblk, 256, 0, s>>>(M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
+      launch_k(ln_bwd_kernel<T, 32>, nblk, 256, 0, s, M, D, dy, lddy, x, ldx, mean, rstd, g, dres, ldres, dx, lddx, part, rpb);
   }
   note_launch();
   PPLL_LAUNCH_CHECK();
   if (part && (dg || (vec && dxsum))) {
-    ln_param_reduce_kernel<<<ceil_div(NS * D, 32), dim3(32, 32), 0, s>>>(nblk, D, NS, part, dg, db,
+    launch_k(ln_param_reduce_kernel, ceil_div(NS * D, 32), dim3(32, 32), 0, s, nblk, D, NS, part, dg, db,
                                                                         vec ? dxsum : nullptr);
     note_launch();
     PPLL_LAUNCH_CHECK();
@@ -488,6 +493,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 attn_fwd_kernel(int Tn, int H, const T* __restrict__ qkv, T* __restrict__ o, float* __restrict__ lse,
                 float scale) {
+  pdl_entry();
   extern __shared__ float sm[];
   float* Q = sm;
   float* Kk = Q + Tn * kLd;
@@ -545,6 +551,7 @@ __global__ void __launch_bounds__(256)
 attn_bwd_kernel(int Tn, int H, const T* __restrict__ qkv, const T* __restrict__ o,
                 const T* __restrict__ dout, const float* __restrict__ lse, T* __restrict__ dqkv,
                 float scale) {
+  pdl_entry();
   extern __shared__ float sm[];
   float* Q = sm;
   float* Kk = Q + Tn * kLd;
@@ -629,7 +636,7 @@ int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     set = true;
   }
-  attn_fwd_kernel<T><<<B * H, 256, smem, s>>>(Tn, H, qkv, o, lse, 1.0f / sqrtf((float)dh));
+  launch_k(attn_fwd_kernel<T>, B * H, 256, smem, s, Tn, H, qkv, o, lse, 1.0f / sqrtf((float)dh));
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -647,7 +654,7 @@ int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, cons
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     set = true;
   }
-  attn_bwd_kernel<T><<<B * H, 256, smem, s>>>(Tn, H, qkv, o, dout, lse, dqkv,
+  launch_k(attn_bwd_kernel<T>, B * H, 256, smem, s, Tn, H, qkv, o, dout, lse, dqkv,
                                               1.0f / sqrtf((float)dh));
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -661,6 +668,7 @@ int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, cons
 template <typename T>
 __global__ void patchify_kernel(int B, int C, int HW, int p, const T* __restrict__ img,
                                 T* __restrict__ out) {
+  pdl_entry();
   const int np = HW / p, P = np * np, pd = C * p * p;
   const long total = (long)B * P * pd;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -679,6 +687,7 @@ template <typename T>
 __global__ void embed_kernel(int B, int P, int D, const T* __restrict__ tok,
                              const float* __restrict__ cls, const float* __restrict__ pos,
                              T* __restrict__ x) {
+  pdl_entry();
   const int Tn = P + 1;
   const long total = (long)B * Tn * D;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -695,6 +704,7 @@ __global__ void embed_kernel(int B, int P, int D, const T* __restrict__ tok,
 template <typename T>
 __global__ void embed_bwd_kernel(int B, int P, int D, const T* __restrict__ dx, T* __restrict__ dtok,
                                  float* __restrict__ dcls, float* __restrict__ dpos) {
+  pdl_entry();
   const int Tn = P + 1;
   const long nt = (long)Tn * D;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < nt;
@@ -715,6 +725,7 @@ __global__ void embed_bwd_kernel(int B, int P, int D, const T* __restrict__ dx, 
 template <typename T>
 __global__ void scatter_cls_kernel(int B, int Tn, int D, const T* __restrict__ dz,
                                    T* __restrict__ dx) {
+  pdl_entry();
   const long total = (long)B * Tn * D;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
@@ -730,7 +741,7 @@ static int grid_for(long n) { return (int)min((n + 255) / 256, (long)148 * 16); 
 template <typename T>
 int launch_patchify(int B, int C, int HW, int p, const T* img, T* out, cudaStream_t s) {
   const long n = (long)B * (HW / p) * (HW / p) * C * p * p;
-  patchify_kernel<T><<<grid_for(n), 256, 0, s>>>(B, C, HW, p, img, out);
+  launch_k(patchify_kernel<T>, grid_for(n), 256, 0, s, B, C, HW, p, img, out);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -738,7 +749,7 @@ int launch_patchify(int B, int C, int HW, int p, const T* img, T* out, cudaStrea
 template <typename T>
 int launch_embed(int B, int P, int D, const T* tok, const float* cls, const float* pos, T* x,
                  cudaStream_t s) {
-  embed_kernel<T><<<grid_for((long)B * (P + 1) * D), 256, 0, s>>>(B, P, D, tok, cls, pos, x);
+  launch_k(embed_kernel<T>, grid_for((long)B * (P + 1) * D), 256, 0, s, B, P, D, tok, cls, pos, x);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -746,14 +757,14 @@ int launch_embed(int B, int P, int D, const T* tok, const float* cls, const floa
 template <typename T>
 int launch_embed_bwd(int B, int P, int D, const T* dx, T* dtok, float* dcls, float* dpos,
                      cudaStream_t s) {
-  embed_bwd_kernel<T><<<grid_for((long)(P + 1) * D), 256, 0, s>>>(B, P, D, dx, dtok, dcls, dpos);
+  launch_k(embed_bwd_kernel<T>, grid_for((long)(P + 1) * D), 256, 0, s, B, P, D, dx, dtok, dcls, dpos);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
 template <typename T>
 int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s) {
-  scatter_cls_kernel<T><<<grid_for((long)B * Tn * D), 256, 0, s>>>(B, Tn, D, dz, dx);
+  launch_k(scatter_cls_kernel<T>, grid_for((long)B * Tn * D), 256, 0, s, B, Tn, D, dz, dx);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
