@@ -364,13 +364,13 @@ def _time_kernel(fn, dev, reps=20):
     timed kernel does not pay for write-backs of a dirty flush)."""
     import torch
     flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)
-    sink = torch.empty(1, dtype=torch.float32, device=dev)
+    sink = torch.empty(1, dtype=torch.float32, device=dev)  # noqa: F841 (reduction target)
     st = torch.cuda.current_stream(dev)
     for _ in range(3):
         fn(st.cuda_stream)
     times = []
     for _ in range(reps):
-        torch.sum(flush, out=sink)
+        torch.sum(flush, dim=(0,), out=sink[0])
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         fn(st.cuda_stream)
@@ -546,6 +546,35 @@ def roofline_gemm(wl, tf_burst, hbm, dev):
             "per_gemm": table, "engine_calibration": engine_calibration(tf_burst, dev)}
 
 
+def cost_model(wl, args, dev, measured_seq_ips, measured_ips):
+    """calibrate the reference's batch-time model with
+    stage profiles measured on this GPU (lp.calibrate on scratch modules of
+    the same workload), then simulate the PPLL schedule with one stage per
+    GPU.  The single-GPU sequential schedule it implies (Σ cycles) is checked
+    against the measured one; the one-stage-per-GPU prediction is what the
+    N = s scaling run should approach."""
+    import paper_2411_12780_b200 as lp
+    mods = build(wl, args.precision, dev, 10 ** 6)
+    B = wl["batch"]
+    prof = lp.calibrate(mods, B)
+    s = len(prof)
+    r = lp.simulate_schedule(prof, lp.CommModel(0.0), "ppll", 8 * s, args.capacity)
+    seq = sum(p.cycle for p in prof)
+    for m in mods:
+        m.close()
+    return {"stage_cycle_ms": [round(p.cycle * 1e3, 4) for p in prof],
+            "stage_push_ms": [round(p.f * 1e3, 4) for p in prof],
+            "comm": "0 (the producer's last GEMM epilogue stores the boundary activation "
+                    "into the consumer's ring slot; no separate transfer)",
+            "predicted_sequential_images_per_s": B / seq,
+            "measured_sequential_images_per_s": measured_seq_ips,
+            "predicted_one_stage_per_gpu": {
+                "n_gpus": s, "steady_batch_ms": r.steady_batch_time * 1e3,
+                "images_per_s": B / r.steady_batch_time,
+                "idle_fraction": [round(x, 4) for x in r.idle_fraction(s)]},
+            "measured_single_gpu_pipeline_images_per_s": measured_ips}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -667,6 +696,8 @@ def main():
         roof_extra = None
     roof["peak_kind"] = peak_kind
 
+    cmodel = cost_model(wl, args, dev, seq_ips, value) if world == 1 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ips, done, dt, Bc = cpu_reference(wl, 10 ** 6, warmup=1, time_budget=15.0,
@@ -694,6 +725,7 @@ def main():
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),
             "staleness": {str(k): v for k, v in sorted(met.staleness.items())},
+            "cost_model": cmodel,
             "final_losses": [h[-1] for h in met.loss_history],
         }
         print(json.dumps(line), flush=True)

@@ -27,7 +27,10 @@ from .blocks import (
 from .errors import (
     ConfigMismatch,
     DimensionMismatch,
+    EmptyEvents,
+    EmptyProfiles,
     InvalidArg,
+    InvalidMode,
     InvalidValue,
     IoError,
     LabelOutOfRange,
@@ -55,6 +58,22 @@ from .runtime import (
 )
 from .tensor import Tensor, matmul, softmax_xent
 from .data import BatchIterator, Dataset, DeviceDataset, batches
+from .costs import (
+    CommModel,
+    CostEstimate,
+    ScheduleEvent,
+    ScheduleResult,
+    StageProfile,
+    calibrate,
+    ppll_beats_pp,
+    ratio_ideal,
+    render_gantt_csv,
+    simulate_schedule,
+    steady_throughput,
+    t_e2e,
+    t_pp,
+    t_ppll,
+)
 from .harness import CSV_HEADER, MetricsRecord, device_memory, evaluate, write_metrics_csv
 from .vit import VitLocalModule, VitSpec, balanced_depths, build_vit_modules
 from .resnet import ResLocalModule, ResNetSpec, build_resnet_modules, resnet_split

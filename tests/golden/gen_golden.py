@@ -203,6 +203,41 @@ def gen_data_and_csv():
         json.dump(orders, f, indent=0)
 
 
+def gen_costs():
+    """costs.py analytic forms, simulator timelines and Gantt CSV (reference)."""
+    cases = []
+    profs = [
+        [(1.0, 2.0, 0.5, 0.5, 1.0, 0.25), (1.0, 2.0, 0.5, 0.25, 0.5, 0.125),
+         (1.0, 2.0, 0.5, 0.0, 0.0, 0.0)],
+        [(0.3, 0.7, 0.1, 0.9, 1.1, 0.2), (0.5, 0.2, 0.05, 0.0, 0.0, 0.0)],
+        [(2.0, 4.0, 1.0, 0.0, 0.0, 0.0)],
+        [(0.1 * (j + 1), 0.3, 0.05, 0.2 / (j + 1), 0.1, 0.01) for j in range(5)],
+    ]
+    for pi, pr in enumerate(profs):
+        sp = [lp.StageProfile(*p) for p in pr]
+        for q in (0.0, 0.35):
+            cm = lp.CommModel(q)
+            case = {"profiles": pr, "q": q,
+                    "t_e2e": [lp.t_e2e(sp).batch_time, lp.t_e2e(sp).components],
+                    "t_pp": [lp.t_pp(sp, cm).batch_time, lp.t_pp(sp, cm).components],
+                    "t_ppll": [lp.t_ppll(sp, cm).batch_time, lp.t_ppll(sp, cm).components],
+                    "beats": list(lp.ppll_beats_pp(sp, cm)), "sims": {}}
+            for mode in ("e2e", "naive_pp", "ppll"):
+                for n, cap in ((7, 2), (3, 1), (12, 3)):
+                    r = lp.simulate_schedule(sp, cm, mode, n, cap)
+                    case["sims"][f"{mode}/{n}/{cap}"] = {
+                        "makespan": r.makespan, "steady": r.steady_batch_time,
+                        "finish": list(r.batch_finish),
+                        "events": [[e.stage, e.kind, e.batch_id, e.start, e.end]
+                                   for e in r.events]}
+            case["gantt"] = lp.render_gantt_csv(
+                lp.simulate_schedule(sp, cm, "ppll", 4, 2).events)
+            cases.append(case)
+    ratios = [[k, s, lp.ratio_ideal(k, s)] for k in (0.0, 0.5, 2.0) for s in (1, 2, 4, 8)]
+    with open(os.path.join(HERE, "costs.json"), "w") as f:
+        json.dump({"cases": cases, "ratios": ratios}, f)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -216,4 +251,5 @@ if __name__ == "__main__":
     gen_full_m()
     gen_e2e_naive()
     gen_data_and_csv()
+    gen_costs()
     print("ok")

@@ -567,3 +567,16 @@ def test_evaluate_matches_oracle_forward(precision):
     assert abs(acc - ref) <= tol + 2.0 / ds.n, (acc, ref)
     mem = lp.device_memory(mods[0])
     assert mem["params_state_bytes"] > 0 and mem["workspace_bytes"] >= 0
+
+
+def test_calibrate_feeds_the_schedule_simulator():
+    """costs.calibrate measures every stage on the device; the simulated
+    one-stage-per-GPU PPLL schedule is governed by the slowest stage."""
+    spec = lp.NetworkSpec((96, 64, 64, 48, 40, 10))
+    hyper = lp.Hyperparams(total_steps=10 ** 6, seed=1)
+    mods = lp.build_modules(spec, lp.partition(spec, 4), 2, 3, hyper)
+    prof = lp.calibrate(mods, 32, reps=5)
+    assert len(prof) == 4 and all(p.cycle > 0 and p.f > 0 for p in prof)
+    r = lp.simulate_schedule(prof, lp.CommModel(), "ppll", 32, 2)
+    assert r.steady_batch_time == pytest.approx(max(p.cycle for p in prof), rel=1e-6)
+    assert min(r.idle_fraction(4)) < 1e-6
