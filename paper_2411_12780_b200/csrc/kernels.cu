@@ -105,32 +105,100 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __re
 // would idle most of its lanes, so use
 //  * row-warp: one warp per output row, lanes split K, NP accumulators,
 //    butterfly reduction (A k-contiguous, N <= 32);
+//  * col-warp: lanes own 32 consecutive output rows (A m-contiguous), the 8
+//    warps split K, fixed-order reduction across warps (N <= 32);
 //  * dot: one thread per output element, the coalesced operand dimension
 //    mapped to the fastest thread index.
+// Both warp forms stage B (the K x N classifier weights / upstream gradient)
+// in shared memory in chunks of 4096 / NP rows (16 KB), so the inner loop
+// streams only A.
+
 template <typename TI, typename TO, int NP>
 __global__ void __launch_bounds__(256)
 gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
                     const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep) {
   pdl_entry();
+  constexpr int kSkK = 4096 / NP;
+  __shared__ float bs[kSkK * NP];
   const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (m >= M) return;
+  const bool live = m < M;
   float acc[NP];
 #pragma unroll
   for (int n = 0; n < NP; ++n) acc[n] = 0.f;
-  const TI* ar = A + (long)m * a_rs;
-  for (int k = lane; k < K; k += 32) {
-    const float a = to_f(ar[k]);
-    const TI* br = Bm + (long)k * b_rs;
+  const TI* ar = A + (long)(live ? m : 0) * a_rs;
+  for (int k0 = 0; k0 < K; k0 += kSkK) {
+    const int kc = min(kSkK, K - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kc * NP; i += blockDim.x) {
+      const int kk = i / NP, n = i % NP;
+      bs[i] = n < N ? to_f(Bm[(long)(k0 + kk) * b_rs + (long)n * b_cs]) : 0.f;
+    }
+    __syncthreads();
+    if (live) {
+      for (int kk = lane; kk < kc; kk += 32) {
+        const float a = to_f(ar[k0 + kk]);
+        const float* br = bs + kk * NP;
 #pragma unroll
-    for (int n = 0; n < NP; ++n)
-      if (n < N) acc[n] = fmaf(a, to_f(br[(long)n * b_cs]), acc[n]);
+        for (int n = 0; n < NP; ++n) acc[n] = fmaf(a, br[n], acc[n]);
+      }
+    }
   }
+  if (!live) return;
 #pragma unroll
   for (int n = 0; n < NP; ++n) acc[n] = warp_sum(acc[n]);
 #pragma unroll
   for (int n = 0; n < NP; ++n)
     if (n < N && lane == n) ep.apply(m, n, acc[n]);
+}
+
+template <typename TI, typename TO, int NP>
+__global__ void __launch_bounds__(256)
+gemm_colwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_cs,
+                    const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep) {
+  pdl_entry();
+  constexpr int kSkK = 4096 / NP;
+  __shared__ float bs[kSkK * NP];
+  __shared__ float red[8][8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int m = blockIdx.x * 32 + lane;
+  const bool live = m < M;
+  float acc[NP];
+#pragma unroll
+  for (int n = 0; n < NP; ++n) acc[n] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += kSkK) {
+    const int kc = min(kSkK, K - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kc * NP; i += blockDim.x) {
+      const int kk = i / NP, n = i % NP;
+      bs[i] = n < N ? to_f(Bm[(long)(k0 + kk) * b_rs + (long)n * b_cs]) : 0.f;
+    }
+    __syncthreads();
+    if (live) {
+      for (int kk = w; kk < kc; kk += 8) {
+        const float a = to_f(A[(long)(k0 + kk) * a_cs + m]);
+        const float* br = bs + kk * NP;
+#pragma unroll
+        for (int n = 0; n < NP; ++n) acc[n] = fmaf(a, br[n], acc[n]);
+      }
+    }
+  }
+  // fixed-order reduction over the 8 K-slices, eight output columns at a time
+#pragma unroll
+  for (int n0 = 0; n0 < NP; n0 += 8) {
+    __syncthreads();
+#pragma unroll
+    for (int n = 0; n < 8; ++n) red[w][n][lane] = acc[n0 + n];
+    __syncthreads();
+    if (w == 0 && live) {
+      for (int n = 0; n < 8 && n0 + n < N; ++n) {
+        float t = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += red[q][n][lane];
+        ep.apply(m, n0 + n, t);
+      }
+    }
+  }
 }
 
 template <typename TI, typename TO>
@@ -167,6 +235,17 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
       launch_k(gemm_rowwarp_kernel<TI, TO, 16>, ceil_div(M, 8), 256, 0, s, M, N, K, A, a_rs, B, b_rs, b_cs, e);
     else
       launch_k(gemm_rowwarp_kernel<TI, TO, 32>, ceil_div(M, 8), 256, 0, s, M, N, K, A, a_rs, B, b_rs, b_cs, e);
+    note_launch();
+    PPLL_LAUNCH_CHECK();
+    return PPLL_OK;
+  }
+  if (N <= 32 && a_rs == 1 && K >= 64) {
+    Epilogue<TO> e = ep;
+    e.partial = nullptr;
+    if (N <= 16)
+      launch_k(gemm_colwarp_kernel<TI, TO, 16>, ceil_div(M, 32), 256, 0, s, M, N, K, A, a_cs, B, b_rs, b_cs, e);
+    else
+      launch_k(gemm_colwarp_kernel<TI, TO, 32>, ceil_div(M, 32), 256, 0, s, M, N, K, A, a_cs, B, b_rs, b_cs, e);
     note_launch();
     PPLL_LAUNCH_CHECK();
     return PPLL_OK;

@@ -683,56 +683,92 @@ __global__ void patchify_kernel(int B, int C, int HW, int p, const T* __restrict
 }
 
 // x[b,0,:] = cls + pos[0]; x[b,1+i,:] = tok[b,i,:] + pos[1+i]
-template <typename T>
+// (VEC: 8 consecutive features per thread as 16-B bf16 vectors, D % 8 == 0)
+template <typename T, int VEC>
 __global__ void embed_kernel(int B, int P, int D, const T* __restrict__ tok,
                              const float* __restrict__ cls, const float* __restrict__ pos,
                              T* __restrict__ x) {
   pdl_entry();
   const int Tn = P + 1;
-  const long total = (long)B * Tn * D;
+  const long total = (long)B * Tn * D / VEC;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
-    const int d = (int)(idx % D);
-    const long bt = idx / D;
+    const long e0 = idx * VEC;
+    const int d = (int)(e0 % D);
+    const long bt = e0 / D;
     const int t = (int)(bt % Tn), b = (int)(bt / Tn);
-    const float v = t == 0 ? cls[d] : to_f(tok[((long)b * P + t - 1) * D + d]);
-    DT<T>::st(x + idx, v + pos[(long)t * D + d]);
+    float v[VEC];
+    if (t == 0) {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = cls[d + i];
+    } else if constexpr (VEC == 8) {
+      ldv<8>(tok + ((long)b * P + t - 1) * D + d, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = to_f(tok[((long)b * P + t - 1) * D + d + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] += pos[(long)t * D + d + i];
+    if constexpr (VEC == 8) {
+      stv<8>(x + e0, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) DT<T>::st(x + e0 + i, v[i]);
+    }
   }
 }
 
 // dtok[b,i,:] = dx[b,1+i,:]; dcls = Σ_b dx[b,0,:]; dpos[t,:] = Σ_b dx[b,t,:]
+// block (32 features x 8 batch groups) per token position, fixed-order
+// combination of the 8 partial sums (deterministic)
 template <typename T>
-__global__ void embed_bwd_kernel(int B, int P, int D, const T* __restrict__ dx, T* __restrict__ dtok,
-                                 float* __restrict__ dcls, float* __restrict__ dpos) {
+__global__ void __launch_bounds__(256)
+embed_bwd_kernel(int B, int P, int D, const T* __restrict__ dx, T* __restrict__ dtok,
+                 float* __restrict__ dcls, float* __restrict__ dpos) {
   pdl_entry();
+  __shared__ float red[8][33];
   const int Tn = P + 1;
-  const long nt = (long)Tn * D;
-  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < nt;
-       idx += (long)gridDim.x * blockDim.x) {
-    const int t = (int)(idx / D), d = (int)(idx % D);
-    float s = 0.f;
-    for (int b = 0; b < B; ++b) {
+  const int d = blockIdx.x * 32 + threadIdx.x, t = blockIdx.y, g = threadIdx.y;
+  float s = 0.f;
+  if (d < D) {
+    for (int b = g; b < B; b += 8) {
       const float v = to_f(dx[((long)b * Tn + t) * D + d]);
       s += v;
       if (t > 0) DT<T>::st(dtok + ((long)b * P + t - 1) * D + d, v);
     }
-    dpos[idx] = s;
-    if (t == 0) dcls[d] = s;
+  }
+  red[g][threadIdx.x] = s;
+  __syncthreads();
+  if (g == 0 && d < D) {
+    float tot = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += red[q][threadIdx.x];
+    dpos[(long)t * D + d] = tot;
+    if (t == 0) dcls[d] = tot;
   }
 }
 
 // dx = 0 except the cls rows: dx[b,0,:] = dcls_rows[b,:] (head backward)
-template <typename T>
+template <typename T, int VEC>
 __global__ void scatter_cls_kernel(int B, int Tn, int D, const T* __restrict__ dz,
                                    T* __restrict__ dx) {
   pdl_entry();
-  const long total = (long)B * Tn * D;
+  const long total = (long)B * Tn * D / VEC;
   for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long)gridDim.x * blockDim.x) {
-    const int d = (int)(idx % D);
-    const long bt = idx / D;
+    const long e0 = idx * VEC;
+    const int d = (int)(e0 % D);
+    const long bt = e0 / D;
     const int t = (int)(bt % Tn), b = (int)(bt / Tn);
-    DT<T>::st(dx + idx, t == 0 ? to_f(dz[(long)b * D + d]) : 0.f);
+    if constexpr (VEC == 8) {
+      uint4 q = make_uint4(0u, 0u, 0u, 0u);
+      if (t == 0) q = *reinterpret_cast<const uint4*>(dz + (long)b * D + d);
+      *reinterpret_cast<uint4*>(dx + e0) = q;
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+        DT<T>::st(dx + e0 + i, t == 0 ? to_f(dz[(long)b * D + d + i]) : 0.f);
+    }
   }
 }
 
@@ -749,7 +785,11 @@ int launch_patchify(int B, int C, int HW, int p, const T* img, T* out, cudaStrea
 template <typename T>
 int launch_embed(int B, int P, int D, const T* tok, const float* cls, const float* pos, T* x,
                  cudaStream_t s) {
-  launch_k(embed_kernel<T>, grid_for((long)B * (P + 1) * D), 256, 0, s, B, P, D, tok, cls, pos, x);
+  const bool v8 = sizeof(T) == 2 && D % 8 == 0 && ((uintptr_t)tok & 15) == 0 && ((uintptr_t)x & 15) == 0;
+  if (v8)
+    launch_k(embed_kernel<T, 8>, grid_for((long)B * (P + 1) * D / 8), 256, 0, s, B, P, D, tok, cls, pos, x);
+  else
+    launch_k(embed_kernel<T, 1>, grid_for((long)B * (P + 1) * D), 256, 0, s, B, P, D, tok, cls, pos, x);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -757,14 +797,18 @@ int launch_embed(int B, int P, int D, const T* tok, const float* cls, const floa
 template <typename T>
 int launch_embed_bwd(int B, int P, int D, const T* dx, T* dtok, float* dcls, float* dpos,
                      cudaStream_t s) {
-  launch_k(embed_bwd_kernel<T>, grid_for((long)(P + 1) * D), 256, 0, s, B, P, D, dx, dtok, dcls, dpos);
+  launch_k(embed_bwd_kernel<T>, dim3(ceil_div(D, 32), P + 1), dim3(32, 8), 0, s, B, P, D, dx, dtok, dcls, dpos);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
 template <typename T>
 int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s) {
-  launch_k(scatter_cls_kernel<T>, grid_for((long)B * Tn * D), 256, 0, s, B, Tn, D, dz, dx);
+  const bool v8 = sizeof(T) == 2 && D % 8 == 0 && ((uintptr_t)dz & 15) == 0 && ((uintptr_t)dx & 15) == 0;
+  if (v8)
+    launch_k(scatter_cls_kernel<T, 8>, grid_for((long)B * Tn * D / 8), 256, 0, s, B, Tn, D, dz, dx);
+  else
+    launch_k(scatter_cls_kernel<T, 1>, grid_for((long)B * Tn * D), 256, 0, s, B, Tn, D, dz, dx);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
