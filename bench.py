@@ -48,11 +48,13 @@ WORKLOADS = {
     # configs[0]: ResNet-32 / 4 blocks, CIFAR-shaped, batch 128
     "resnet32": dict(kind="resnet", spec=dict(n=5, image=32, channels=3, widths=(16, 32, 64),
                                               classes=10),
-                     s=4, d_prime=1, interval=3, batch=128, ref_batch=8, data_shape="CIFAR-10"),
+                     s=4, d_prime=1, interval=3, batch=128, ref_batch=8, data_shape="CIFAR-10",
+                     split="cost"),
     # configs[2]: ResNet-110 / 8 blocks, SVHN-shaped, batch 256
     "resnet110": dict(kind="resnet", spec=dict(n=18, image=32, channels=3, widths=(16, 32, 64),
                                                classes=10),
-                      s=8, d_prime=1, interval=3, batch=256, ref_batch=4, data_shape="SVHN"),
+                      s=8, d_prime=1, interval=3, batch=256, ref_batch=4, data_shape="SVHN",
+                      split="cost"),
     "mlp_m": dict(kind="mlp", dims=(3072, 1024, 1024, 1024, 1024, 10), s=4, d_prime=2,
                   interval=3, batch=128, ref_batch=128),
 }
@@ -132,7 +134,13 @@ def describe(wl, name):
 
 
 def cfg_dict(wl, args):
-    return {"workload": describe(wl, args.workload),
+    extra = {}
+    if wl["kind"] == "resnet" and wl.get("split") == "cost":
+        from paper_2411_12780_b200.resnet import ResNetSpec, balanced_resnet_split
+        sp = balanced_resnet_split(ResNetSpec(**wl["spec"]), wl["s"], wl["d_prime"], wl["interval"])
+        extra["stage_split"] = ("cost-balanced (stem on stage 0) blocks per stage "
+                                f"{[len(b) for b in sp]}")
+    return extra | {"workload": describe(wl, args.workload),
             "global_batch": wl["batch"] * max(1, args.gpus), "stages": wl["s"],
             "buffer_capacity": args.capacity, "precision": args.precision,
             "placement": "all stages on each GPU (replicas)" if args.gpus > 1 else
@@ -234,7 +242,8 @@ def build(wl, precision, device, total_steps):
                                 wl["interval"], hyper, devices=[device] * wl["s"])
     if wl["kind"] == "resnet":
         return lp.build_resnet_modules(lp.ResNetSpec(**wl["spec"]), wl["s"], wl["d_prime"],
-                                       wl["interval"], hyper, devices=[device] * wl["s"])
+                                       wl["interval"], hyper, devices=[device] * wl["s"],
+                                       split=wl.get("split", "even"))
     spec = lp.VitSpec(**wl["spec"])
     return lp.build_vit_modules(spec, lp.balanced_depths(spec.depth, wl["s"]), wl["d_prime"],
                                 wl["interval"], hyper, devices=[device] * wl["s"])
@@ -273,6 +282,7 @@ def run_sharded(args, wl, rank, world, local, dev):
     elif wl["kind"] == "resnet":
         spec = lp.ResNetSpec(**wl["spec"])
         mods = lp.build_resnet_modules(spec, s, wl["d_prime"], wl["interval"], hyper,
+                                       split=wl.get("split", "even"),
                                        devices=[dev] * s, only=mine)
     else:
         spec = lp.VitSpec(**wl["spec"])

@@ -70,6 +70,59 @@ def resnet_split(spec: ResNetSpec, s: int) -> list:
     return out
 
 
+def _unit_cost(hwc: float) -> float:
+    """Relative cost of a basic block whose output map has ``hwc`` elements
+    per image: a fixed per-layer launch/latency part plus a part proportional
+    to the activation bytes its memory-bound kernels (im2col, BN, col2im)
+    move; constants fit to the measured stage cycles of the even ResNet-32
+    split on B200 (0.15 ms per 8x8x64 block, 0.32 ms per 32x32x16 block)."""
+    return 0.093 + 1.38e-5 * hwc
+
+
+def balanced_resnet_split(spec: ResNetSpec, s: int, d_prime: int, n: int) -> list:
+    """Contiguous split of the units [stem, blocks...] minimising the most
+    expensive stage (minimax DP), each stage charged for its blocks, its aux
+    head (aux_depth(j, d', n) convs at its output map, none on the final
+    stage) and the stem on stage 0.  The even split gives the early,
+    high-resolution stages 2.5x the cycle of the last one; this balances the
+    one-stage-per-GPU pipeline (the cost model's idle prediction)."""
+    units = spec.n_blocks + 1
+    if s < 1 or s > units:
+        raise ConfigMismatch(f"cannot split {units} units into {s} stages")
+    ucost = [0.5 * _unit_cost(spec.image * spec.image * spec.widths[0])]
+    geo = []
+    for b in range(spec.n_blocks):
+        cin, cout, stride, h_in = block_geometry(spec, b)
+        h = h_in // stride
+        ucost.append(_unit_cost(h * h * cout) + (0.03 if stride != 1 or cin != cout else 0.0))
+        geo.append(h * h * cout)
+    out_hwc = [spec.image * spec.image * spec.widths[0]] + geo
+
+    def stage_cost(j, a, b_):          # units a..b_-1 on stage j
+        c = sum(ucost[a:b_])
+        if j < s - 1:
+            c += aux_depth(j, d_prime, n) * 0.5 * _unit_cost(out_hwc[b_ - 1])
+        return c
+
+    INF = float("inf")
+    best = [[INF] * (units + 1) for _ in range(s + 1)]
+    cut = [[0] * (units + 1) for _ in range(s + 1)]
+    best[0][0] = 0.0
+    for j in range(1, s + 1):
+        for i in range(j, units - (s - j) + 1):
+            for k in range(j - 1, i):
+                v = max(best[j - 1][k], stage_cost(j - 1, k, i))
+                if v < best[j][i] - 1e-12:
+                    best[j][i], cut[j][i] = v, k
+    bounds, i = [], units
+    for j in range(s, 0, -1):
+        k = cut[j][i]
+        bounds.append((k, i))
+        i = k
+    bounds.reverse()
+    return [[x - 1 for x in range(a, b_) if x >= 1] for a, b_ in bounds]
+
+
 def stage_out_geometry(spec: ResNetSpec, blocks):
     if not blocks:
         return spec.widths[0], spec.image
@@ -184,12 +237,18 @@ class ResLocalModule(LocalModule):
 
 def build_resnet_modules(spec: ResNetSpec, s: int, d_prime: int, n: int, hyper: Hyperparams,
                          devices: Sequence | None = None,
-                         only: Sequence[int] | None = None) -> list:
+                         only: Sequence[int] | None = None, split: str | list = "even") -> list:
     """One ResLocalModule per stage.  Init (blocks.py:198-237 style):
     ``default_rng(seed + j)``; conv W ~ U(±1/√fan_in) drawn in layer order
     (stem, per block w1, w2[, ws], aux convs), then the head W and b; BN gamma=1,
-    beta=0 (no draws)."""
-    split = resnet_split(spec, s)
+    beta=0 (no draws).  ``split``: "even" (resnet_split), "cost"
+    (balanced_resnet_split) or an explicit list of block-index lists."""
+    if split == "even":
+        split = resnet_split(spec, s)
+    elif split == "cost":
+        split = balanced_resnet_split(spec, s, d_prime, n)
+    elif len(split) != s:
+        raise ConfigMismatch(f"split has {len(split)} stages, expected {s}")
     mods = []
     for j, blocks in enumerate(split):
         if only is not None and j not in only:

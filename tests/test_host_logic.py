@@ -177,3 +177,14 @@ def test_compute_refuses_cpu_tensors():
     b = lp.Tensor(torch.zeros(3, 4), device="cpu")
     with pytest.raises(RuntimeError, match="CUDA"):
         lp.matmul(a, b)
+
+
+def test_balanced_resnet_split_is_contiguous_and_minimax():
+    from paper_2411_12780_b200.resnet import ResNetSpec, balanced_resnet_split, resnet_split
+    for spec, s in ((ResNetSpec(), 4), (ResNetSpec(n=18), 8), (ResNetSpec(n=2), 3)):
+        b = balanced_resnet_split(spec, s, 1, 3)
+        flat = [x for blk in b for x in blk]
+        assert flat == list(range(spec.n_blocks)) and len(b) == s
+        assert all(len(blk) >= 1 for blk in b[1:])
+    # the high-resolution early blocks are spread thinner than the even split
+    assert len(balanced_resnet_split(ResNetSpec(), 4, 1, 3)[0]) < len(resnet_split(ResNetSpec(), 4)[0])
