@@ -124,8 +124,11 @@ int linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY, in
   }
   r = PPLL_ERR_UNSUPPORTED;
   if (g_gemm_engine != PPLL_GEMM_SIMT) {
+    ep.colsum_b = db;   // the cluster split-K kernel can produce db alongside dW
     r = launch_gemm_tc<float>(K, N, M, (const bf16*)X, ldx, false, (const bf16*)dY, lddy, false, ep,
                               ws, ws_elems, s);
+    ep.colsum_b = nullptr;
+    if (r == kGemmColsumFused) return PPLL_OK;
     if (r != PPLL_OK && (r != PPLL_ERR_UNSUPPORTED || g_gemm_engine == PPLL_GEMM_TCGEN05)) return r;
   }
   if (r == PPLL_ERR_UNSUPPORTED)

@@ -71,6 +71,33 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// multicast forms (thread-block cluster of 2 along M): the box lands at the
+// same smem offset in every CTA of ctaMask and completes bytes on each CTA's
+// barrier at the same offset; the commit arrives on every CTA's barrier
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                               int x, int y, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
@@ -136,7 +163,12 @@ struct Sched {
   int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores
 };
 
-template <typename TO, bool A_K, bool B_K, int BN, int F>
+// MC: the CTA pair of a 2-CTA cluster computes vertically adjacent tiles
+// (m-tiles 2p, 2p+1, same n-tile) and shares the B operand — each CTA fetches
+// half of every B k-block and multicasts it to both, halving B's L2->SM
+// traffic; a slot is refilled only when both CTAs' MMAs have consumed it
+// (empty barriers count the two CTAs' multicast commits).
+template <typename TO, bool A_K, bool B_K, int BN, int F, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                int M, int N, int K, Sched sc, Epilogue<TO> ep, float* part) {
@@ -160,7 +192,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], MC ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -169,6 +201,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  // work decomposition: MC clusters walk pair-tiles, the CTA rank picks the row
+  const int rank = MC ? (int)cta_rank_in_cluster() : 0;
+  const int wid0 = MC ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+  const int wstride = MC ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int mtw = MC ? (sc.mt + 1) / 2 : sc.mt;          // m-tiles (pairs) per n column
+  const int tiles_w = mtw * sc.nt;
+  const int items_w = MC ? tiles_w : sc.items;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -179,6 +218,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if constexpr (MC) cluster_sync();   // peers' barriers initialised before any multicast
   // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
   pdl_entry();
 
@@ -186,9 +226,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
       int kb_total = 0;
-      for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
-        const int tile = w % sc.tiles, z = w / sc.tiles;
-        const int m0 = (tile % sc.mt) * BM, n0 = (tile / sc.mt) * BN;
+      for (int w = wid0; w < items_w; w += wstride) {
+        const int tile = w % tiles_w, z = MC ? 0 : w / sc.tiles;
+        const int m0 = ((tile % mtw) * (MC ? 2 : 1) + rank) * BM, n0 = (tile / mtw) * BN;
         const int kbeg = z * sc.kps, kend = min(K, kbeg + sc.kps);
         for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb_total) {
           const int st = kb_total % S;
@@ -203,7 +243,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             for (int i = 0; i < BM / 64; ++i)
               tma_load_2d(&map_a, &full[st], sa + i * 8192, m0 + 64 * i, k0);
           }
-          if (B_K) {
+          if constexpr (MC) {
+            // this CTA fetches its half of B and multicasts it to the pair
+            if (B_K) {
+              tma_load_2d_mc(&map_b, &full[st], sb + rank * (BN / 2) * 128, k0,
+                             n0 + rank * (BN / 2), (uint16_t)3);
+            } else {
+#pragma unroll
+              for (int i = 0; i < (BN + 63) / 64; ++i)
+                if ((i & 1) == rank)
+                  tma_load_2d_mc(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0,
+                                 (uint16_t)3);
+            }
+          } else if (B_K) {
             tma_load_2d(&map_b, &full[st], sb, k0, n0);
           } else {
 #pragma unroll
@@ -220,8 +272,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                            ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
       int kb_total = 0, it = 0;
-      for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
-        const int z = w / sc.tiles;
+      for (int w = wid0; w < items_w; w += wstride, ++it) {
+        const int z = MC ? 0 : w / sc.tiles;
         const int kbeg = z * sc.kps, kend = min(K, kbeg + sc.kps);
         const int acc = it & 1;
         const uint32_t dtm = tmem + (uint32_t)(acc * BN);
@@ -243,7 +295,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             mma_bf16(dtm, ad, bd, idesc, first ? 0u : 1u);
             first = 0;
           }
-          mma_commit(&empty[st]);
+          if constexpr (MC) mma_commit_mc(&empty[st], (uint16_t)3);   // both CTAs' slot
+          else mma_commit(&empty[st]);
         }
         mma_commit(&tfull[acc]);
       }
@@ -259,9 +312,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int grp = (warp - 2) >> 2;
     uint8_t* stg = stg_all + (warp - 2) * 1024;
     int it = 0;
-    for (int w = blockIdx.x; w < sc.items; w += gridDim.x, ++it) {
-      const int tile = w % sc.tiles, z = w / sc.tiles;
-      const int m0 = (tile % sc.mt) * BM, n0 = (tile / sc.mt) * BN;
+    for (int w = wid0; w < items_w; w += wstride, ++it) {
+      const int tile = w % tiles_w, z = MC ? 0 : w / sc.tiles;
+      const int m0 = ((tile % mtw) * (MC ? 2 : 1) + rank) * BM, n0 = (tile / mtw) * BN;
       const int acc = it & 1;
       const bool split = sc.splits > 1;
       float* bs = bias_s + acc * BN;
@@ -306,6 +359,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  // the peer's last multicast commits land on this CTA's barriers: stay alive
+  if constexpr (MC) cluster_sync();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -351,7 +406,7 @@ template <typename TO, bool A_K, bool B_K, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ CUtensorMap map_b, int M, int N, int K, int mt,
-                       int kps, TO* __restrict__ C, long ldc, int vec) {
+                       int kps, TO* __restrict__ C, long ldc, int vec, float* __restrict__ db) {
   using L = Smem<BN>;
   constexpr int S = L::STAGES;
   static_assert(S * L::STAGE >= BM * BN * 4, "reduction buffer must fit in the operand ring");
@@ -369,13 +424,19 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
   const int tile = blockIdx.x / CS;
   const int m0 = (tile % mt) * BM, n0 = (tile / mt) * BN;
   const int kbeg = rank * kps, kend = min(K, kbeg + kps);
+  // fused bias gradient db[n] = Σ_k B(k, n) (the Σ rows of dY of a weight
+  // gradient): the idle epilogue warps of the m-tile-0 clusters sum each B
+  // k-block from shared memory while the MMAs run (MN-major B only)
+  const bool do_cs = !B_K && db != nullptr && (tile % mt) == 0;
+  float* cs_red = reinterpret_cast<float*>(smem + S * L::STAGE + L::EPI);   // STG area
+  float* cs_part = reinterpret_cast<float*>(smem + S * L::STAGE);           // EPI area
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], do_cs ? 1 + kEpiWarps : 1);
     }
     mbar_init(&tfull[0], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -446,6 +507,45 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     __syncwarp();
   } else {
+    if (do_cs) {
+      // thread t: 8-column chunk ch = t % NCH of the B tile, rows rg, rg + RG, ...
+      constexpr int NCH = BN / 8, RG = (32 * kEpiWarps) / NCH;
+      const int t = threadIdx.x - 64, ch = t % NCH, rg = t / NCH;
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      int kb = 0;
+      for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb) {
+        const int st = kb % S;
+        mbar_wait(&full[st], (kb / S) & 1);
+        if (rg < RG) {
+          const uint8_t* sb = smem + st * L::STAGE + L::A_BYTES + (ch >> 3) * 8192;
+          const int c16 = ch & 7;
+          for (int r = rg; r < BK; r += RG) {
+            const uint4 q = *reinterpret_cast<const uint4*>(sb + r * 128 + ((c16 ^ (r & 7)) * 16));
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              acc[2 * e] += f.x;
+              acc[2 * e + 1] += f.y;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done with the slot
+      }
+      if (rg < RG) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cs_red[rg * BN + ch * 8 + e] = acc[e];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      for (int c = t; c < BN; c += 32 * kEpiWarps) {
+        float v = 0.f;
+        for (int g = 0; g < RG; ++g) v += cs_red[g * BN + c];      // fixed order
+        cs_part[c] = v;
+      }
+    }
     // all MMAs retired => every operand slot has been consumed: the ring is
     // free and becomes this CTA's fp32 partial tile
     const int q = warp & 3, grp = (warp - 2) >> 2;
@@ -497,6 +597,19 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int t = 0; t < 4 && gcol + t < N; ++t) DT<TO>::st(dst + t, e[t]);
         }
       }
+    }
+  }
+  if (do_cs && rank == 0) {   // Σ of the K-slice column sums in fixed rank order
+    const uint32_t cs_addr = smem_u32(cs_part);
+    for (int c = threadIdx.x; c < BN / 4; c += kThreads) {
+      float4 acc = ld_dsmem_f4(cs_addr + 16 * c, 0);
+      for (int src = 1; src < CS; ++src) {
+        const float4 t = ld_dsmem_f4(cs_addr + 16 * c, (uint32_t)src);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      const float e[4] = {acc.x, acc.y, acc.z, acc.w};
+      for (int j = 0; j < 4; ++j)
+        if (n0 + 4 * c + j < N) db[n0 + 4 * c + j] = e[j];
     }
   }
   cluster_sync_all();   // peers may still be reading this CTA's partial until here
@@ -553,6 +666,74 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
+}
+
+// 2-CTA clusters sharing B by multicast (see gemm_tc_kernel MC)
+template <typename TO, bool A_K, bool B_K, int BN, int F>
+static int run_mc(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
+                  const Sched& sc, const Epilogue<TO>& ep, cudaStream_t s) {
+  auto kern = gemm_tc_kernel<TO, A_K, B_K, BN, F, true>;
+  constexpr int smem = Smem<BN>::TOTAL;
+  static bool attr_set = false;
+  if (!attr_set) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  const int pairs = ((sc.mt + 1) / 2) * sc.nt;
+  const int grid = 2 * (pairs < kNumSMs / 2 ? pairs : kNumSMs / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  float* part = nullptr;
+  PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, sc, ep, part));
+  note_launch();
+  return PPLL_OK;
+}
+template <typename TO, bool A_K, bool B_K, int F>
+static int dispatch_mc(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
+                       const Sched& sc, const Epilogue<TO>& ep, cudaStream_t s) {
+  switch (bn) {
+    case 256: return run_mc<TO, A_K, B_K, 256, F>(ma, mb, M, N, K, sc, ep, s);
+    case 192: return run_mc<TO, A_K, B_K, 192, F>(ma, mb, M, N, K, sc, ep, s);
+    default: return run_mc<TO, A_K, B_K, 128, F>(ma, mb, M, N, K, sc, ep, s);
+  }
+}
+// specialised epilogues with multicast (bf16 outputs, no split-K, BN >= 128)
+template <typename TO, bool A_K, bool B_K>
+static int dispatch_f_mc(int f, int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M,
+                         int N, int K, const Sched& sc, const Epilogue<TO>& ep, cudaStream_t s) {
+  if constexpr (A_K && !B_K && sizeof(TO) == 2) {
+    switch (f) {
+      case 0: return dispatch_mc<TO, A_K, B_K, 0>(bn, ma, mb, M, N, K, sc, ep, s);
+      case kEFBias: return dispatch_mc<TO, A_K, B_K, kEFBias>(bn, ma, mb, M, N, K, sc, ep, s);
+      case kEFBias | kEFRes:
+        return dispatch_mc<TO, A_K, B_K, kEFBias | kEFRes>(bn, ma, mb, M, N, K, sc, ep, s);
+      case kEFBias | kEFGeluD:
+        return dispatch_mc<TO, A_K, B_K, kEFBias | kEFGeluD>(bn, ma, mb, M, N, K, sc, ep, s);
+      case kEFBias | kEFRelu:
+        return dispatch_mc<TO, A_K, B_K, kEFBias | kEFRelu>(bn, ma, mb, M, N, K, sc, ep, s);
+      default: break;
+    }
+  } else if constexpr (A_K && B_K && sizeof(TO) == 2) {
+    switch (f) {
+      case 0: return dispatch_mc<TO, A_K, B_K, 0>(bn, ma, mb, M, N, K, sc, ep, s);
+      case kEFMaskRelu: return dispatch_mc<TO, A_K, B_K, kEFMaskRelu>(bn, ma, mb, M, N, K, sc, ep, s);
+      case kEFMaskMul: return dispatch_mc<TO, A_K, B_K, kEFMaskMul>(bn, ma, mb, M, N, K, sc, ep, s);
+      default: break;
+    }
+  }
+  return PPLL_ERR_UNSUPPORTED;
 }
 
 template <typename TO, bool A_K, bool B_K, int F>
@@ -653,7 +834,8 @@ static int cluster_capacity(int cs) {
 }
 template <typename TO, bool A_K, bool B_K, int BN>
 static int run_cluster(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int mt,
-                       int tiles, int cs, int kps, TO* C, long ldc, int vec, cudaStream_t s) {
+                       int tiles, int cs, int kps, TO* C, long ldc, int vec, float* db,
+                       cudaStream_t s) {
   if (!cluster_attr_init<TO, A_K, B_K, BN>()) {
     set_error("gemm_tc_cluster_kernel: smem attribute");
     return PPLL_ERR_CUDA;
@@ -661,7 +843,7 @@ static int run_cluster(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = cluster_cfg<TO, A_K, B_K, BN>(tiles * cs, cs, s, at);
   PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_cluster_kernel<TO, A_K, B_K, BN>, ma, mb, M, N,
-                                     K, mt, kps, C, ldc, vec));
+                                     K, mt, kps, C, ldc, vec, db));
   note_launch();
   return PPLL_OK;
 }
@@ -677,12 +859,12 @@ static int cluster_capacity_bn(int bn, int cs) {
 template <typename TO, bool A_K, bool B_K>
 static int dispatch_cluster(int bn, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
                             int K, int mt, int tiles, int cs, int kps, TO* C, long ldc, int vec,
-                            cudaStream_t s) {
+                            float* db, cudaStream_t s) {
   switch (bn) {
-    case 256: return run_cluster<TO, A_K, B_K, 256>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
-    case 192: return run_cluster<TO, A_K, B_K, 192>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
-    case 128: return run_cluster<TO, A_K, B_K, 128>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
-    default: return run_cluster<TO, A_K, B_K, 64>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, s);
+    case 256: return run_cluster<TO, A_K, B_K, 256>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, db, s);
+    case 192: return run_cluster<TO, A_K, B_K, 192>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, db, s);
+    case 128: return run_cluster<TO, A_K, B_K, 128>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, db, s);
+    default: return run_cluster<TO, A_K, B_K, 64>(ma, mb, M, N, K, mt, tiles, cs, kps, C, ldc, vec, db, s);
   }
 }
 template <typename TO>
@@ -783,25 +965,51 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   sc.items = sc.tiles * sc.splits;
   static const int probe = getenv("PPLL_GEMM_PROBE") ? atoi(getenv("PPLL_GEMM_PROBE")) : 0;
   sc.probe = probe;
-  CUtensorMap ma, mb;
-  bool ok = a_kmajor ? make_map(&ma, A, K, M, lda, BM) : make_map(&ma, A, M, K, lda, 64);
-  ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, bn) : make_map(&mb, B, N, K, ldb, 64));
-  if (!ok) return PPLL_ERR_UNSUPPORTED;
+  // 2-CTA multicast of B: specialised bf16 epilogues, no split, >= 2 m-tiles
+  // opt-in (PPLL_GEMM_MC=1): measured 0-5 % slower than the unpaired kernel on the ViT
+  // shapes, whose mainloop is bound by per-SM smem fill (bytes in flight / latency), which
+  // multicast does not change (each SM still receives the whole B tile)
+  static const int force_mc = getenv("PPLL_GEMM_MC") ? atoi(getenv("PPLL_GEMM_MC")) : 0;
+  const int fl = epi_flags(ep);
+  const bool mc = force_mc != 0 && !cl_bn && sc.splits == 1 && sizeof(TO) == 2 && a_kmajor &&
+                  bn >= 128 && mt >= 2 && fl != kEFGeneric &&
+                  (b_kmajor ? (fl == 0 || fl == kEFMaskRelu || fl == kEFMaskMul)
+                            : (fl == 0 || fl == kEFBias || fl == (kEFBias | kEFRes) ||
+                               fl == (kEFBias | kEFGeluD) || fl == (kEFBias | kEFRelu)));
   static const int verbose = getenv("PPLL_GEMM_VERBOSE") ? atoi(getenv("PPLL_GEMM_VERBOSE")) : 0;
   if (verbose)
-    fprintf(stderr, "[gemm_tc] M=%d N=%d K=%d %s%s bn=%d tiles=%d splits=%d cluster=%d flags=%d\n",
-            M, N, K, a_kmajor ? "A:K" : "A:MN", b_kmajor ? " B:K" : " B:MN", bn, sc.tiles,
-            sc.splits, cl_bn ? sc.splits : 0, epi_flags(ep));
+    fprintf(stderr, "[gemm_tc] M=%d N=%d K=%d %s%s bn=%d tiles=%d splits=%d cluster=%d mc=%d "
+            "flags=%d\n", M, N, K, a_kmajor ? "A:K" : "A:MN", b_kmajor ? " B:K" : " B:MN", bn,
+            sc.tiles, sc.splits, cl_bn ? sc.splits : 0, (int)mc, fl);
+  CUtensorMap ma, mb;
+  bool ok = a_kmajor ? make_map(&ma, A, K, M, lda, BM) : make_map(&ma, A, M, K, lda, 64);
+  ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, mc ? bn / 2 : bn)
+                       : make_map(&mb, B, N, K, ldb, 64));
+  if (!ok) return PPLL_ERR_UNSUPPORTED;
+  if (mc) {
+    Epilogue<TO> e = ep;
+    e.partial = nullptr;
+    const int r = b_kmajor ? dispatch_f_mc<TO, true, true>(fl, bn, ma, mb, M, N, K, sc, e, s)
+                           : dispatch_f_mc<TO, true, false>(fl, bn, ma, mb, M, N, K, sc, e, s);
+    if (r != PPLL_ERR_UNSUPPORTED) return r;
+    // (unsupported combination: rebuild the B map for the plain path)
+    if (b_kmajor && !make_map(&mb, B, K, N, ldb, bn)) return PPLL_ERR_UNSUPPORTED;
+  }
   if (cl_bn) {
     const int cs = sc.splits;   // every CTA of the cluster owns >= 1 k-block
     Epilogue<TO> e = ep;
+    // fused bias column sums of the MN-major B operand (weight gradients)
+    float* db = (!b_kmajor && ep.colsum_b) ? ep.colsum_b : nullptr;
+    int r;
     if (a_kmajor && !b_kmajor)
-      return dispatch_cluster<TO, true, false>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
-    if (a_kmajor && b_kmajor)
-      return dispatch_cluster<TO, true, true>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
-    if (!a_kmajor && !b_kmajor)
-      return dispatch_cluster<TO, false, false>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
-    return dispatch_cluster<TO, false, true>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, s);
+      r = dispatch_cluster<TO, true, false>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, db, s);
+    else if (a_kmajor && b_kmajor)
+      r = dispatch_cluster<TO, true, true>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, nullptr, s);
+    else if (!a_kmajor && !b_kmajor)
+      r = dispatch_cluster<TO, false, false>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, db, s);
+    else
+      r = dispatch_cluster<TO, false, true>(bn, ma, mb, M, N, K, mt, sc.tiles, cs, sc.kps, e.C, e.ldc, e.vec, nullptr, s);
+    return (r == PPLL_OK && db) ? kGemmColsumFused : r;
   }
   Epilogue<TO> e = ep;
   e.partial = nullptr;

@@ -464,6 +464,7 @@ struct Epilogue {
   int vec = 0;
   float* partial = nullptr;  // split-K workspace (internal)
   float* cs_part = nullptr;  // fused column sums: [ceil(M/32)][ncols] partial rows (or null)
+  float* colsum_b = nullptr; // weight-gradient GEMMs: Σ_k B(k, n) (bias gradient), if fused
 
   __device__ __forceinline__ float act_f(float v) const {
     if (act == kActRelu) return fmaxf(v, 0.f);
@@ -740,6 +741,9 @@ template <typename TI, typename TO>
 int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, const TI* B,
                      long b_rs, long b_cs, const Epilogue<TO>& ep, float* ws, size_t ws_elems,
                      cudaStream_t s);
+
+// launch_gemm_tc return value when Epilogue::colsum_b was produced in-kernel
+constexpr int kGemmColsumFused = 1000;
 
 // tcgen05 GEMM (gemm_tc.cu).  a_kmajor: A(m,k)=A[m*lda+k] else A[k*lda+m];
 // b_kmajor: B(k,n)=B[n*ldb+k] else B[k*ldb+n].  Returns PPLL_ERR_UNSUPPORTED

@@ -230,13 +230,11 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     og.mask = b.u;
     og.ldmask = F;
     og.mask_mode = kMaskMul;
-    og.db = st->G(st->po(l, kB1));      // db1 = Σ rows dU, fused into this epilogue
-    og.cs_ws = st->cs_part;
-    og.cs_ws_elems = st->cs_part_elems;
     r = gemm_dgrad(M, F, D, dx2, D, st->W(st->po(l, kW2)), og, st->dbig, F, st->dtype, st->ws,
                    st->ws_elems, s);
     if (r) return r;
-    r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), nullptr,
+    // db1 = Σ rows dU: summed from the dU tiles in smem by the cluster wgrad
+    r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
                      st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
     r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,

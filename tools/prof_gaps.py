@@ -2,7 +2,7 @@
 graph on a single stream: per-kernel durations, the idle gaps between
 consecutive kernels, and the step's wall time (torch.profiler / CUPTI).
 
-usage: python tools/prof_gaps.py [vit|resnet] [stage]
+usage: python tools/prof_gaps.py [vit|resnet] [stage] [batch]
 """
 import os
 import sys
@@ -24,7 +24,7 @@ if fam == "vit":
 else:
     mods = lp.build_resnet_modules(lp.ResNetSpec(), 4, 1, 3, hyper)
 m = mods[j]
-B = 128
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 128
 x = torch.randn((B,) + tuple(m.in_shape), device="cuda").to(m.act_dtype)
 y = torch.as_tensor(np.random.default_rng(0).integers(0, 10, B), device="cuda")
 out = torch.empty((B,) + tuple(m.out_shape), device="cuda", dtype=m.act_dtype)
