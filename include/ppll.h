@@ -54,6 +54,9 @@ uint64_t ppll_launch_count(void);
 void ppll_set_gemm_engine(int engine);
 /* ViT attention engine: 0 = tcgen05 when supported (bf16, T <= 128), 1 = SIMT */
 void ppll_set_attn_engine(int engine);
+/* profiling hook: device buffer of the GEMM timeline probe (PPLL_GEMM_TIMELINE
+ * set): 148 CTAs x 4 tiles x {MMA start, MMA done, epilogue done, -} u64 ns */
+void* ppll_gemm_timeline(void);
 
 /* ---- primitive ops: tensor.py ------------------------------------------ */
 

@@ -27,6 +27,7 @@ SIGNATURES = {
     "ppll_launch_count": (_u64, []),
     "ppll_set_gemm_engine": (None, [_i]),
     "ppll_set_attn_engine": (None, [_i]),
+    "ppll_gemm_timeline": (_vp, []),
     "ppll_linear_fwd": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _vp]),
     "ppll_linear_fwd_ex": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _i, _vp, _i,
                                 _vp, _i, _i, _vp]),

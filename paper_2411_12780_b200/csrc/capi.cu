@@ -147,6 +147,8 @@ extern "C" {
 int ppll_abi_version(void) { return PPLL_ABI_VERSION; }
 const char* ppll_last_error(void) { return ppll::last_error(); }
 uint64_t ppll_launch_count(void) { return g_launches.load(); }
+// (profiling hook) the GEMM timeline buffer of PPLL_GEMM_TIMELINE, 148 x 4 x 4 u64
+void* ppll_gemm_timeline(void) { return ppll::tc::timeline_buffer(); }
 void ppll_set_gemm_engine(int engine) { g_gemm_engine = engine; }
 
 int ppll_linear_fwd(int M, int K, int N, const void* X, int ldx, const void* W, const float* b,

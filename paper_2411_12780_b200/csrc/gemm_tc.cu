@@ -146,6 +146,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;     // 16 KB
@@ -161,7 +174,15 @@ struct Smem {
 struct Sched {
   int mt, nt, tiles, splits, kps, items;
   int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores
+  // timeline probe (PPLL_GEMM_TIMELINE): per CTA and tile, %globaltimer at
+  // MMA start / MMA done (tfull observed) / epilogue done, 4 tiles max
+  unsigned long long* tl;
 };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // MC: the CTA pair of a 2-CTA cluster computes vertically adjacent tiles
 // (m-tiles 2p, 2p+1, same n-tile) and shares the B operand — each CTA fetches
@@ -279,6 +300,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const uint32_t dtm = tmem + (uint32_t)(acc * BN);
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (sc.tl && it < 4) sc.tl[(blockIdx.x * 4 + it) * 4 + 0] = gtimer();
         int first = 1;
         for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb_total) {
           const int st = kb_total % S;
@@ -326,6 +348,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (sc.tl && it < 4 && warp == 2 && lane == 0) sc.tl[(blockIdx.x * 4 + it) * 4 + 1] = gtimer();
       const int row = m0 + q * 32 + lane;
       const bool live = row < M;
 #pragma unroll 1
@@ -355,6 +378,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (sc.tl && it < 4 && lane == 0) atomicMax(&sc.tl[(blockIdx.x * 4 + it) * 4 + 2], gtimer());
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -875,6 +899,12 @@ static int capacity_any(bool ak, bool bk, int bn, int cs) {
   return cluster_capacity_bn<TO, false, true>(bn, cs);
 }
 
+unsigned long long* timeline_buffer() {
+  static unsigned long long* buf = nullptr;
+  if (!buf && cudaMalloc(&buf, kNumSMs * 4 * 4 * 8) != cudaSuccess) buf = nullptr;
+  return buf;
+}
+
 // per-k-block (BK=64) mainloop cycles of a 128 x c tile: max(tensor floor,
 // operand bytes (A 4 KB + B c·32 B per K=16) streamed L2 -> smem at ~80 B/cycle/SM)
 static inline double kblock_cycles(int c) { return 4.0 * fmax(c / 2.0, (4096.0 + 32.0 * c) / 80.0); }
@@ -965,6 +995,8 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   sc.items = sc.tiles * sc.splits;
   static const int probe = getenv("PPLL_GEMM_PROBE") ? atoi(getenv("PPLL_GEMM_PROBE")) : 0;
   sc.probe = probe;
+  static const int tl_on = getenv("PPLL_GEMM_TIMELINE") ? 1 : 0;
+  sc.tl = tl_on ? timeline_buffer() : nullptr;
   // 2-CTA multicast of B: specialised bf16 epilogues, no split, >= 2 m-tiles
   // opt-in (PPLL_GEMM_MC=1): measured 0-5 % slower than the unpaired kernel on the ViT
   // shapes, whose mainloop is bound by per-SM smem fill (bytes in flight / latency), which

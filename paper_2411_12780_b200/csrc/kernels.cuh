@@ -742,6 +742,10 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
                      long b_rs, long b_cs, const Epilogue<TO>& ep, float* ws, size_t ws_elems,
                      cudaStream_t s);
 
+namespace tc {
+unsigned long long* timeline_buffer();   // PPLL_GEMM_TIMELINE probe (gemm_tc.cu)
+}
+
 // launch_gemm_tc return value when Epilogue::colsum_b was produced in-kernel
 constexpr int kGemmColsumFused = 1000;
 
