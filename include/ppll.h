@@ -122,6 +122,16 @@ int ppll_nesterov_step(int64_t n, float* theta, float* v, const float* g, void* 
 double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps);
 
 /* element conversion helpers (fp32 <-> bf16), n elements */
+/* Implicit-GEMM 3x3 convolution, stride 1, pad 1, NHWC bf16 (tcgen05, TMA
+ * gathers the shifted windows — no im2col matrix).  w is the GEMM weight
+ * [9·Cin, Cout] (row tap·Cin + ci, tap = 3r + s).  dgrad = 0: y[N,H,W,Cout] =
+ * conv(x[N,H,W,Cin]); dgrad = 1: y[N,H,W,Cin] = the input gradient for
+ * x = dZ[N,H,W,Cout] (transposed convolution).  Cin, Cout ∈ {16, 32, 64},
+ * N·H·W % 128 == 0; PPLL_ERR_UNSUPPORTED otherwise.  The ResNet stages'
+ * stride-1 convolutions (the extension family; no reference counterpart). */
+int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x, const void* w,
+                      void* y, int dgrad, void* stream);
+
 /* ---- data path / evaluation -------------------------------------------- */
 /* dst[r,:] = cast(src[idx[r],:]) for r < n (fp32 rows of `width` features,
  * dst fp32 or bf16), and labels_dst[r] = labels_src[idx[r]] when given: the

@@ -1,0 +1,346 @@
+// Implicit-GEMM 3x3 convolution (stride 1, pad 1, NHWC bf16) on tcgen05
+// tensor cores for the ResNet stages — no im2col matrix.
+//
+//   out[p, co] = Σ_tap Σ_ci  x[p + off(tap), ci] · Wtap[co, ci]
+//
+// Output tile = 128 consecutive pixels (whole image rows: 128 / W rows, or
+// 128 / (H·W) images for 8x8 maps).  For every tap the TMA engine fetches the
+// shifted input window as ONE 4-D box {CI, W, rows, images} of the NHWC
+// tensor: out-of-range rows / columns (the zero padding) come back as zeros,
+// and the box lands in shared memory as a K-major [128 pixels x CI] tile in
+// the swizzle mode matching its 32/64/128-B rows.  The nine tap tiles of a
+// pixel tile are nine k-blocks of K = CI; the 3x3 weights (≤ 73 KB) are
+// staged once per CTA as nine K-major [CO x CI] tiles in the same swizzle.
+// Persistent CTAs, warp roles as in gemm_tc.cu (TMA producer, MMA issuer,
+// 16 epilogue warps over double-buffered TMEM accumulators, the GEMM
+// engine's generic fused epilogue).
+//
+// The input gradient of the same convolution is this kernel applied to dZ
+// with the taps mirrored and the weights transposed (transposed convolution,
+// stride 1): `dgrad` selects that weight view, so the dZ·Wᵀ GEMM and the
+// col2im gather of the explicit path disappear (its residual-add and ReLU
+// mask ride in the epilogue).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "common.cuh"
+#include "kernels.cuh"
+#include "resnet.cuh"
+
+namespace ppll {
+namespace cv {
+
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kNumSMs = 148;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// K-major operand descriptor for rows of RB = 32/64/128 bytes (SW32/64/128):
+// 8-row swizzle atoms of 8·RB bytes (SBO), K advanced by +32 B per K=16 step
+template <int RB>
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
+  constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(((8 * RB) >> 4) & 0x3FFF) << 32;   // SBO
+  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
+  d |= layout << 61;
+  return d;
+}
+// the byte offset of 16-B chunk j of row r in a K-major swizzled tile (the
+// pattern TMA writes and UMMA reads for SW32 / SW64 / SW128)
+template <int RB>
+__device__ __forceinline__ int swz(int r, int j) {
+  const int f = RB == 128 ? (r & 7) : (RB == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+  return r * RB + ((j ^ f) * 16);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int CI, int CO>
+struct ConvSmem {
+  static constexpr int RB = CI * 2;                  // A / B row bytes (K = CI)
+  static constexpr int A_BYTES = 128 * RB;           // one tap of a pixel tile
+  static constexpr int W_BYTES = 9 * CO * RB;        // nine [CO x CI] weight tiles
+  static constexpr int STAGES = CI == 64 ? 6 : 9;    // tap slots (smem-limited at CI = 64)
+  static constexpr int STG = kEpiWarps * 1024;
+  static constexpr int TOTAL = STAGES * A_BYTES + W_BYTES + STG + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = 2 * CO <= 32 ? 32 : (2 * CO <= 64 ? 64 : 128);
+};
+
+// W (global, bf16) is the GEMM weight [k·k·Cin (padded), Cout], row (tap·Cin + ci).
+// fwd:   Wtap[co][ci] = W[(tap·CI + ci)·CO + co]             (CI = Cin, CO = Cout)
+// dgrad: Wtap[co][ci] = W[((8 − tap)·CO + co)·CI + ci]       (CI = Cout, CO = Cin)
+template <int CI, int CO>
+__global__ void __launch_bounds__(kThreads, 1)
+conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ wg,
+                  int dgrad, int P, int H, int Wd, int rows, int imgs, Epilogue<__nv_bfloat16> ep) {
+  using L = ConvSmem<CI, CO>;
+  constexpr int S = L::STAGES, RB = L::RB;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
+  uint8_t* sw = smem + S * L::A_BYTES;               // weight tiles
+  uint8_t* stg_all = sw + L::W_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + L::STG);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles = P / 128;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  pdl_entry();   // the weights below are written by the predecessor (optimizer step)
+  // stage the nine weight tiles, K-major and swizzled like the TMA'd A tiles
+  for (int i = threadIdx.x; i < 9 * CO * (CI / 8); i += kThreads) {
+    const int j = i % (CI / 8), co = (i / (CI / 8)) % CO, tap = i / (CI / 8) / CO;
+    __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ci = 8 * j + e;
+      v[e] = dgrad ? wg[((long)(8 - tap) * CO + co) * CI + ci] : wg[((long)tap * CI + ci) * CO + co];
+    }
+    *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = *reinterpret_cast<uint4*>(v);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int HWp = H * Wd;
+
+  if (warp == 0) {
+    // ------------------------- TMA producer -------------------------
+    if (lane == 0) {
+      int kb = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int p0 = t * 128, n0 = p0 / HWp, h0 = (p0 % HWp) / Wd;
+        for (int tap = 0; tap < 9; ++tap, ++kb) {
+          const int st = kb % S;
+          mbar_wait(&empty[st], ((kb / S) & 1) ^ 1);
+          mbar_expect_tx(&full[st], L::A_BYTES);
+          tma_load_4d(&xmap, &full[st], smem + st * L::A_BYTES, 0, tap % 3 - 1, h0 + tap / 3 - 1,
+                      n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------- MMA issuer ---------------------------
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CO >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);
+    if (lane == 0) {
+      int kb = 0, it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int tap = 0; tap < 9; ++tap, ++kb) {
+          const int st = kb % S;
+          mbar_wait(&full[st], (kb / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + st * L::A_BYTES);
+          const uint32_t sb = smem_u32(sw + tap * CO * RB);
+#pragma unroll
+          for (int k = 0; k < CI / 16; ++k)
+            mma_bf16(tmem + (uint32_t)(acc * CO), kdesc<RB>(sa + 32 * k), kdesc<RB>(sb + 32 * k),
+                     idesc, (tap | k) ? 1u : 0u);
+          mma_commit(&empty[st]);
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------- epilogue -----------------------------
+    const int q = warp & 3, grp = (warp - 2) >> 2;
+    uint8_t* stg = stg_all + (warp - 2) * 1024;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1, m0 = t * 128;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 16 * grp; c < CO; c += 64) {
+        float ra[16], ka[16];
+        if (row < P) ep.load_aux16(row, c, ra, ka);
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CO + c), r);
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        ep.finish_block16(m0 + q * 32, P, c, v, ra, ka, nullptr, stg, lane);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int CI, int CO>
+static int run(const CUtensorMap& xm, const __nv_bfloat16* w, int dgrad, int P, int H, int Wd,
+               int rows, int imgs, const Epilogue<__nv_bfloat16>& ep, cudaStream_t s) {
+  auto kern = conv3x3_tc_kernel<CI, CO>;
+  constexpr int smem = ConvSmem<CI, CO>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int tiles = P / 128;
+  launch_k(kern, tiles < kNumSMs ? tiles : kNumSMs, kThreads, smem, s, xm, w, dgrad, P, H, Wd,
+           rows, imgs, ep);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
+}  // namespace cv
+
+// out = conv3x3(x) (stride 1, pad 1) with CI input / CO output channels, NHWC
+// bf16; `dgrad` = the transposed convolution of the forward weights (input
+// gradient).  Returns PPLL_ERR_UNSUPPORTED for shapes the kernel does not
+// cover (the caller keeps the explicit im2col path).
+int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* x,
+                      const __nv_bfloat16* w, bool dgrad, const Epilogue<__nv_bfloat16>& ep,
+                      cudaStream_t s) {
+  using namespace cv;
+  const long P = (long)N * H * W;
+  if (CI % 16 || CO % 16 || CI > 64 || CO > 64 || P % 128) return PPLL_ERR_UNSUPPORTED;
+  int rows, imgs;
+  if (W > 128 || 128 % W) return PPLL_ERR_UNSUPPORTED;
+  if (128 / W <= H) {
+    rows = 128 / W;
+    imgs = 1;
+    if (H % rows) return PPLL_ERR_UNSUPPORTED;
+  } else {
+    if (128 % (H * W)) return PPLL_ERR_UNSUPPORTED;
+    rows = H;
+    imgs = 128 / (H * W);
+  }
+  if (((uintptr_t)x & 15) || ((uintptr_t)w & 15)) return PPLL_ERR_UNSUPPORTED;
+  auto enc = encoder();
+  if (!enc) return PPLL_ERR_UNSUPPORTED;
+  CUtensorMap xm;
+  cuuint64_t dims[4] = {(cuuint64_t)CI, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)CI * 2, (cuuint64_t)W * CI * 2, (cuuint64_t)H * W * CI * 2};
+  cuuint32_t box[4] = {(cuuint32_t)CI, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle sz = CI == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : (CI == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  if (enc(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<__nv_bfloat16*>(x), dims, strides,
+          box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return PPLL_ERR_UNSUPPORTED;
+  Epilogue<__nv_bfloat16> e = ep;
+  const int d = dgrad ? 1 : 0, Pi = (int)P;
+#define CONV_CASE(A, B) \
+  if (CI == A && CO == B) return run<A, B>(xm, w, d, Pi, H, W, rows, imgs, e, s);
+  CONV_CASE(16, 16) CONV_CASE(32, 32) CONV_CASE(64, 64)
+  CONV_CASE(16, 32) CONV_CASE(32, 16) CONV_CASE(32, 64) CONV_CASE(64, 32)
+#undef CONV_CASE
+  return PPLL_ERR_UNSUPPORTED;
+}
+
+}  // namespace ppll
+
+extern "C" int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x,
+                                 const void* w, void* y, int dgrad, void* stream) {
+  using namespace ppll;
+  Epilogue<__nv_bfloat16> e;
+  const int co = dgrad ? Cin : Cout, ci = dgrad ? Cout : Cin;
+  e.C = (__nv_bfloat16*)y;
+  e.ldc = co;
+  epilogue_finalize(e, co);
+  return launch_conv3x3_tc(N, H, W, ci, co, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
+                           dgrad != 0, e, reinterpret_cast<cudaStream_t>(stream));
+}

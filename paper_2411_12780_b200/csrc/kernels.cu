@@ -295,13 +295,42 @@ int launch_gemm_simt(int M, int N, int K, const TI* A, long a_rs, long a_cs, con
   return PPLL_OK;
 }
 
+// split-K reduction with the splits spread over 8 thread rows: block (32
+// outputs x 8 split groups); each thread sums splits g, g+8, ... in order,
+// then a fixed-order combination of the 8 partials (deterministic)
+template <typename TO>
+__global__ void __launch_bounds__(256)
+splitk_reduce2_kernel(int M, int N, int splits, const float* __restrict__ part, Epilogue<TO> ep) {
+  pdl_entry();
+  __shared__ float red[8][33];
+  const long total = (long)M * N;
+  const long idx = (long)blockIdx.x * 32 + threadIdx.x;
+  float s = 0.f;
+  if (idx < total)
+    for (int z = threadIdx.y; z < splits; z += 8) s += part[(long)z * total + idx];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && idx < total) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+    ep.apply((int)(idx / N), (int)(idx % N), t);
+  }
+}
+
 template <typename TO>
 int launch_splitk_reduce(int M, int N, int splits, const float* ws, const Epilogue<TO>& ep,
                          cudaStream_t s) {
   Epilogue<TO> r = ep;
   r.partial = nullptr;
-  int blocks = min(ceil_div((long)M * N, 256), 148 * 8);
-  launch_k(splitk_reduce_kernel<TO>, blocks, 256, 0, s, M, N, splits, ws, r);
+  const long total = (long)M * N;
+  if (splits >= 16 && total <= 148L * 8 * 256) {
+    // few outputs, many splits (conv weight gradients): parallel over the splits
+    launch_k(splitk_reduce2_kernel<TO>, ceil_div(total, 32), dim3(32, 8), 0, s, M, N, splits, ws, r);
+  } else {
+    int blocks = min(ceil_div(total, 256), 148 * 8);
+    launch_k(splitk_reduce_kernel<TO>, blocks, 256, 0, s, M, N, splits, ws, r);
+  }
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

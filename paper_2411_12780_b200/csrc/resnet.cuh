@@ -27,6 +27,14 @@ int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, cons
                   const float* g, float* part, float* dg, float* db, T* dz, cudaStream_t s);
 template <typename T>
 int launch_gap(int N, int HW, int C, const T* x, T* out, cudaStream_t s);
+
+template <typename TO> struct Epilogue;
+// implicit-GEMM 3x3 / stride-1 convolution on tcgen05 (conv_tc.cu); dgrad =
+// transposed convolution with the forward weights.  PPLL_ERR_UNSUPPORTED for
+// shapes it does not cover.
+int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* x,
+                      const __nv_bfloat16* w, bool dgrad, const Epilogue<__nv_bfloat16>& ep,
+                      cudaStream_t s);
 template <typename T>
 int launch_gap_bwd(int N, int HW, int C, const T* dp, T* dx, cudaStream_t s);
 

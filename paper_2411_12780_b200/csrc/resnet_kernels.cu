@@ -13,6 +13,19 @@ static int grid_for(long n, int threads = 256) {
   return (int)min((n + threads - 1) / threads, (long)148 * 16);
 }
 
+// unsigned 32-bit division by a runtime constant: q = (umulhi(n, m) + n) >> s
+// (valid for n < 2^31); replaces the 64-bit divisions of the index math
+struct FastDiv {
+  unsigned d, m, s;
+  FastDiv() = default;
+  explicit FastDiv(unsigned dv) : d(dv) {
+    s = 0;
+    while ((1u << s) < dv) ++s;
+    m = (unsigned)((((unsigned long long)1 << 32) * ((1ull << s) - dv)) / dv + 1);
+  }
+  __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
 // ---------------------------------------------------------------------------
 // im2col: x [N,H,W,C] -> col [N·Ho·Wo, Kp], column (r·k + s)·C + c, zero pad
 // (spatial padding (k-1)/2 and columns >= k·k·C).  8-channel vectors when C%8==0.
@@ -38,28 +51,27 @@ __global__ void im2col_kernel(int N, int H, int W, int C, int k, int stride, int
   }
 }
 
-template <typename T>
-__global__ void im2col_vec_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo,
-                                  int Kp, const T* __restrict__ x, T* __restrict__ col) {
+__global__ void im2col_vec_kernel(int total, int H, int W, int C, int k, int stride, int Kp,
+                                  FastDiv fK8, FastDiv fC8, FastDiv fk, FastDiv fWo, FastDiv fHo,
+                                  const __nv_bfloat16* __restrict__ x,
+                                  __nv_bfloat16* __restrict__ col) {
   pdl_entry();
-  // one thread per 8-channel vector (16 B for bf16)
+  // one thread per 8-channel vector (16 B); 32-bit fast-division index math
   const int p = (k - 1) / 2;
-  const int C8 = C / 8, K8 = Kp / 8;
-  const long total = (long)N * Ho * Wo * K8;
-  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long)gridDim.x * blockDim.x) {
-    const int k8 = (int)(idx % K8);
-    const long pix = idx / K8;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += gridDim.x * blockDim.x) {
+    const unsigned pix = fK8.div(idx), k8 = idx - pix * fK8.d;
+    const unsigned tap = fC8.div(k8), c8 = k8 - tap * fC8.d;
     uint4 v = make_uint4(0, 0, 0, 0);
-    const int tap = k8 / C8, c8 = k8 % C8;
-    if (tap < k * k) {
-      const int r = tap / k, s = tap % k;
-      const int wo = (int)(pix % Wo), ho = (int)((pix / Wo) % Ho), n = (int)(pix / ((long)Wo * Ho));
-      const int h = ho * stride - p + r, w = wo * stride - p + s;
+    if (tap < (unsigned)(k * k)) {
+      const unsigned r = fk.div(tap), sx = tap - r * fk.d;
+      const unsigned q = fWo.div(pix), wo = pix - q * fWo.d;
+      const unsigned n = fHo.div(q), ho = q - n * fHo.d;
+      const int h = (int)ho * stride - p + (int)r, w = (int)wo * stride - p + (int)sx;
       if (h >= 0 && h < H && w >= 0 && w < W)
         v = *reinterpret_cast<const uint4*>(x + (((long)n * H + h) * W + w) * C + c8 * 8);
     }
-    *reinterpret_cast<uint4*>(col + pix * Kp + (long)k8 * 8) = v;
+    *reinterpret_cast<uint4*>(col + (long)pix * Kp + (long)k8 * 8) = v;
   }
 }
 
@@ -68,9 +80,11 @@ int launch_im2col(int N, int H, int W, int C, int k, int stride, int Kp, const T
                   cudaStream_t s) {
   const int p = (k - 1) / 2;
   const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
-  if (sizeof(T) == 2 && C % 8 == 0 && Kp % 8 == 0) {
-    const long n = (long)N * Ho * Wo * (Kp / 8);
-    launch_k(im2col_vec_kernel<T>, grid_for(n), 256, 0, s, N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
+  const long nv = (long)N * Ho * Wo * (Kp / 8);
+  if (sizeof(T) == 2 && C % 8 == 0 && Kp % 8 == 0 && nv < (1L << 31)) {
+    launch_k(im2col_vec_kernel, grid_for(nv), 256, 0, s, (int)nv, H, W, C, k, stride, Kp,
+             FastDiv(Kp / 8), FastDiv(C / 8), FastDiv(k), FastDiv(Wo), FastDiv(Ho),
+             (const __nv_bfloat16*)x, (__nv_bfloat16*)col);
   } else {
     const long n = (long)N * Ho * Wo * Kp;
     launch_k(im2col_kernel<T>, grid_for(n), 256, 0, s, N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
@@ -126,19 +140,21 @@ __device__ __forceinline__ void acc8(float* a, uint4 q) {
     a[2 * j + 1] += f.y;
   }
 }
-__global__ void col2im_vec_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo,
-                                  int Kp, const __nv_bfloat16* __restrict__ dcol,
+__global__ void col2im_vec_kernel(int total, int H, int W, int C, int k, int stride, int Ho, int Wo,
+                                  int Kp, FastDiv fC8, FastDiv fW, FastDiv fH,
+                                  const __nv_bfloat16* __restrict__ dcol,
                                   const __nv_bfloat16* __restrict__ dres,
                                   const __nv_bfloat16* __restrict__ mask,
                                   __nv_bfloat16* __restrict__ dx) {
   pdl_entry();
-  const int p = (k - 1) / 2, C8 = C / 8;
-  const long total = (long)N * H * W * C8;
-  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(idx % C8);
-    const long q = idx / C8;
-    const int w = (int)(q % W), h = (int)((q / W) % H), n = (int)(q / ((long)W * H));
+  const int p = (k - 1) / 2;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += gridDim.x * blockDim.x) {
+    const unsigned q = fC8.div(idx), c8 = idx - q * fC8.d;
+    const unsigned q2 = fW.div(q), wq = q - q2 * fW.d;
+    const unsigned n = fH.div(q2);
+    const int h = (int)(q2 - n * fH.d);
+    const int w = (int)wq;
     float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int r = 0; r < k; ++r) {
       const int hh = h + p - r;
@@ -154,7 +170,7 @@ __global__ void col2im_vec_kernel(int N, int H, int W, int C, int k, int stride,
                     dcol + (((long)n * Ho + ho) * Wo + wo) * Kp + (r * k + s2) * C + c8 * 8));
       }
     }
-    const long o = q * C + c8 * 8;
+    const long o = (long)q * C + c8 * 8;
     if (dres) acc8(a, *reinterpret_cast<const uint4*>(dres + o));
     if (mask) {
       const uint4 mq = *reinterpret_cast<const uint4*>(mask + o);
@@ -180,10 +196,11 @@ int launch_col2im(int N, int H, int W, int C, int k, int stride, int Kp, const T
   const int p = (k - 1) / 2;
   const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
   if constexpr (sizeof(T) == 2) {
-    if (C % 8 == 0 && Kp % 8 == 0) {
-      launch_k(col2im_vec_kernel, grid_for((long)N * H * W * C / 8), 256, 0, s, 
-          N, H, W, C, k, stride, Ho, Wo, Kp, (const __nv_bfloat16*)dcol,
-          (const __nv_bfloat16*)dres, (const __nv_bfloat16*)mask, (__nv_bfloat16*)dx);
+    const long nv = (long)N * H * W * C / 8;
+    if (C % 8 == 0 && Kp % 8 == 0 && nv < (1L << 31)) {
+      launch_k(col2im_vec_kernel, grid_for(nv), 256, 0, s, (int)nv, H, W, C, k, stride, Ho, Wo, Kp,
+               FastDiv(C / 8), FastDiv(W), FastDiv(H), (const __nv_bfloat16*)dcol,
+               (const __nv_bfloat16*)dres, (const __nv_bfloat16*)mask, (__nv_bfloat16*)dx);
       note_launch();
       PPLL_LAUNCH_CHECK();
       return PPLL_OK;
@@ -267,12 +284,224 @@ __global__ void bn_stats_final_kernel(int chunks, int C, const float* __restrict
 
 int bn_chunks(int P) { return max(1, min(ceil_div(P, 256), 256)); }
 
+// ---------------------------------------------------------------------------
+// Vectorised NHWC forms (bf16, C % 8 == 0, 256 % (C/8) == 0): a thread owns
+// one 16-B vector of 8 channels of a row; a 256-thread block covers
+// RB = 256·8/C rows per pass, fully coalesced.  Statistics accumulate per
+// thread as shifted sums (shift = the thread's first value, so the variance
+// does not cancel), become Welford triples, and merge in a fixed smem tree
+// (deterministic).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __bfloat1622float2(h[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 q;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+  return q;
+}
+static bool bn_vec_ok(int C, const void* a, const void* b = nullptr, const void* c = nullptr) {
+  auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return C % 8 == 0 && C <= 256 && 256 % (C / 8) == 0 && al(a) && al(b) && al(c);
+}
+static int bn_vec_rpc(int P, int C) {
+  const int RB = 256 / (C / 8);
+  int rpc = max(RB * 8, ceil_div(P, bn_chunks(P)));
+  return ceil_div(rpc, RB) * RB;
+}
+
+__global__ void __launch_bounds__(256)
+bn_stats_part_vkernel(int P, int C, const __nv_bfloat16* __restrict__ z, int rpc,
+                      float* __restrict__ part) {
+  pdl_entry();
+  __shared__ float red[256 * 8 * 3];          // [RB][C][3] Welford triples
+  const int V = C / 8, RB = 256 / V, t = threadIdx.x, vc = t % V, ro = t / V;
+  const int r0 = blockIdx.x * rpc, r1 = min(P, r0 + rpc);
+  float K[8], sm[8], sq[8];
+  int n = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) K[e] = sm[e] = sq[e] = 0.f;
+  for (int r = r0 + ro; r < r1; r += RB) {
+    float v[8];
+    unpack8(*reinterpret_cast<const uint4*>(z + (long)r * C + vc * 8), v);
+    if (n == 0) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) K[e] = v[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = v[e] - K[e];
+      sm[e] += d;
+      sq[e] = fmaf(d, d, sq[e]);
+    }
+    ++n;
+  }
+  const float fn = (float)n;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float* w = red + ((long)ro * C + vc * 8 + e) * 3;
+    w[0] = fn;
+    w[1] = n ? K[e] + sm[e] / fn : 0.f;
+    w[2] = n ? fmaxf(sq[e] - sm[e] * sm[e] / fn, 0.f) : 0.f;
+  }
+  __syncthreads();
+  for (int stride = RB / 2; stride >= 1; stride >>= 1) {
+    for (int i = t; i < stride * C; i += 256) {
+      float* a = red + (long)i * 3;
+      const float* b = red + ((long)i + (long)stride * C) * 3;
+      const Welford m = wf_merge(Welford{a[0], a[1], a[2]}, Welford{b[0], b[1], b[2]});
+      a[0] = m.n; a[1] = m.mean; a[2] = m.m2;
+    }
+    __syncthreads();
+  }
+  for (int c = t; c < C; c += 256) {
+    float* o = part + ((long)blockIdx.x * C + c) * 3;
+    o[0] = red[c * 3]; o[1] = red[c * 3 + 1]; o[2] = red[c * 3 + 2];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+bn_bwd_part_vkernel(int P, int C, const __nv_bfloat16* __restrict__ dy,
+                    const __nv_bfloat16* __restrict__ z, const float* __restrict__ mean,
+                    const float* __restrict__ rstd, int rpc, float* __restrict__ part) {
+  pdl_entry();
+  __shared__ float red[256 * 8 * 2];          // [RB][C][2]
+  const int V = C / 8, RB = 256 / V, t = threadIdx.x, vc = t % V, ro = t / V;
+  const int r0 = blockIdx.x * rpc, r1 = min(P, r0 + rpc);
+  float mu[8], rs[8], sg[8], sb[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    mu[e] = mean[vc * 8 + e];
+    rs[e] = rstd[vc * 8 + e];
+    sg[e] = sb[e] = 0.f;
+  }
+  for (int r = r0 + ro; r < r1; r += RB) {
+    float d[8], x[8];
+    unpack8(*reinterpret_cast<const uint4*>(dy + (long)r * C + vc * 8), d);
+    unpack8(*reinterpret_cast<const uint4*>(z + (long)r * C + vc * 8), x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      sg[e] = fmaf(d[e], (x[e] - mu[e]) * rs[e], sg[e]);
+      sb[e] += d[e];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[((long)ro * C + vc * 8 + e) * 2] = sg[e];
+    red[((long)ro * C + vc * 8 + e) * 2 + 1] = sb[e];
+  }
+  __syncthreads();
+  for (int stride = RB / 2; stride >= 1; stride >>= 1) {
+    for (int i = t; i < stride * C; i += 256) {
+      red[(long)i * 2] += red[((long)i + (long)stride * C) * 2];
+      red[(long)i * 2 + 1] += red[((long)i + (long)stride * C) * 2 + 1];
+    }
+    __syncthreads();
+  }
+  for (int c = t; c < C; c += 256) {
+    part[((long)blockIdx.x * 2 + 0) * C + c] = red[c * 2];
+    part[((long)blockIdx.x * 2 + 1) * C + c] = red[c * 2 + 1];
+  }
+}
+
+// y = act(BN(z) [+ BN2(z2) | + res]), 8 channels per thread
+__global__ void bn_apply_vkernel(long nvec, int C, const __nv_bfloat16* __restrict__ z,
+                                 const float* __restrict__ mean, const float* __restrict__ rstd,
+                                 const float* __restrict__ g, const float* __restrict__ b,
+                                 const __nv_bfloat16* __restrict__ z2,
+                                 const float* __restrict__ mean2, const float* __restrict__ rstd2,
+                                 const float* __restrict__ g2, const float* __restrict__ b2,
+                                 const __nv_bfloat16* __restrict__ res, int relu,
+                                 __nv_bfloat16* __restrict__ y) {
+  pdl_entry();
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (long)gridDim.x * blockDim.x) {
+    const int c0 = (int)((i * 8) % C);
+    float v[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(z)[i], v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      o[e] = (v[e] - mean[c0 + e]) * rstd[c0 + e] * g[c0 + e] + b[c0 + e];
+    if (z2) {
+      unpack8(reinterpret_cast<const uint4*>(z2)[i], v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        o[e] += (v[e] - mean2[c0 + e]) * rstd2[c0 + e] * g2[c0 + e] + b2[c0 + e];
+    }
+    if (res) {
+      unpack8(reinterpret_cast<const uint4*>(res)[i], v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] += v[e];
+    }
+    if (relu) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = fmaxf(o[e], 0.f);
+    }
+    reinterpret_cast<uint4*>(y)[i] = pack8(o);
+  }
+}
+
+// dz = g·rstd/P · (P·dy − db − xhat·dg), 8 channels per thread
+__global__ void bn_bwd_dx_vkernel(long nvec, int C, float invP, const __nv_bfloat16* __restrict__ dy,
+                                  const __nv_bfloat16* __restrict__ z,
+                                  const float* __restrict__ mean, const float* __restrict__ rstd,
+                                  const float* __restrict__ g, const float* __restrict__ dg,
+                                  const float* __restrict__ db, __nv_bfloat16* __restrict__ dz) {
+  pdl_entry();
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (long)gridDim.x * blockDim.x) {
+    const int c0 = (int)((i * 8) % C);
+    float d[8], x[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(dy)[i], d);
+    unpack8(reinterpret_cast<const uint4*>(z)[i], x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = c0 + e;
+      const float rs = rstd[c];
+      const float xh = (x[e] - mean[c]) * rs;
+      o[e] = g[c] * rs * (d[e] - (db[c] + xh * dg[c]) * invP);
+    }
+    reinterpret_cast<uint4*>(dz)[i] = pack8(o);
+  }
+}
+
+__global__ void relu_mask_vkernel(long nvec, const __nv_bfloat16* __restrict__ dout,
+                                  const __nv_bfloat16* __restrict__ out,
+                                  __nv_bfloat16* __restrict__ dy) {
+  pdl_entry();
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (long)gridDim.x * blockDim.x) {
+    float d[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(dout)[i], d);
+    unpack8(reinterpret_cast<const uint4*>(out)[i], o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) d[e] = o[e] > 0.f ? d[e] : 0.f;
+    reinterpret_cast<uint4*>(dy)[i] = pack8(d);
+  }
+}
+
+
+
 template <typename T>
 int launch_bn_stats(int P, int C, const T* z, float* part, float* mean, float* rstd,
                     cudaStream_t s) {
-  const int chunks = bn_chunks(P);
-  const int rpc = ceil_div(P, chunks);
-  launch_k(bn_stats_part_kernel<T>, dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s, P, C, z, rpc, part);
+  int chunks = bn_chunks(P);
+  int rpc = ceil_div(P, chunks);
+  if (sizeof(T) == 2 && bn_vec_ok(C, z)) {
+    rpc = bn_vec_rpc(P, C);
+    chunks = ceil_div(P, rpc);
+    launch_k(bn_stats_part_vkernel, chunks, 256, 0, s, P, C, (const __nv_bfloat16*)z, rpc, part);
+  } else {
+    launch_k(bn_stats_part_kernel<T>, dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s, P, C, z, rpc, part);
+  }
   note_launch();
   launch_k(bn_stats_final_kernel, ceil_div(C, 8), 256, 0, s, chunks, C, part, mean, rstd);
   note_launch();
@@ -305,8 +534,13 @@ int launch_bn_apply(long P, int C, const T* z, const float* mean, const float* r
                     const float* b, const T* z2, const float* mean2, const float* rstd2,
                     const float* g2, const float* b2, const T* res, int relu, T* y, cudaStream_t s) {
   const long total = P * C;
-  launch_k(bn_apply_kernel<T>, grid_for(total), 256, 0, s, total, C, z, mean, rstd, g, b, z2, mean2,
-                                                     rstd2, g2, b2, res, relu, y);
+  if (sizeof(T) == 2 && bn_vec_ok(C, z, z2, res) && bn_vec_ok(C, y))
+    launch_k(bn_apply_vkernel, grid_for(total / 8), 256, 0, s, total / 8, C,
+             (const __nv_bfloat16*)z, mean, rstd, g, b, (const __nv_bfloat16*)z2, mean2, rstd2, g2,
+             b2, (const __nv_bfloat16*)res, relu, (__nv_bfloat16*)y);
+  else
+    launch_k(bn_apply_kernel<T>, grid_for(total), 256, 0, s, total, C, z, mean, rstd, g, b, z2, mean2,
+                                                       rstd2, g2, b2, res, relu, y);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -324,7 +558,12 @@ __global__ void relu_mask_kernel(long total, const T* __restrict__ dout, const T
 
 template <typename T>
 int launch_relu_mask(long n, const T* dout, const T* out, T* dy, cudaStream_t s) {
-  launch_k(relu_mask_kernel<T>, grid_for(n), 256, 0, s, n, dout, out, dy);
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (sizeof(T) == 2 && n % 8 == 0 && al(dout) && al(out) && al(dy))
+    launch_k(relu_mask_vkernel, grid_for(n / 8), 256, 0, s, n / 8, (const __nv_bfloat16*)dout,
+             (const __nv_bfloat16*)out, (__nv_bfloat16*)dy);
+  else
+    launch_k(relu_mask_kernel<T>, grid_for(n), 256, 0, s, n, dout, out, dy);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -402,16 +641,29 @@ __global__ void bn_bwd_dx_kernel(long total, int C, float invP, const T* __restr
 template <typename T>
 int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, const float* rstd,
                   const float* g, float* part, float* dg, float* db, T* dz, cudaStream_t s) {
-  const int chunks = bn_chunks(P);
-  const int rpc = ceil_div(P, chunks);
-  launch_k(bn_bwd_part_kernel<T>, dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s, P, C, dy, z, mean,
-                                                                              rstd, rpc, part);
+  int chunks = bn_chunks(P);
+  int rpc = ceil_div(P, chunks);
+  const bool vec = sizeof(T) == 2 && bn_vec_ok(C, dy, z, dz);
+  if (vec) {
+    rpc = bn_vec_rpc(P, C);
+    chunks = ceil_div(P, rpc);
+    launch_k(bn_bwd_part_vkernel, chunks, 256, 0, s, P, C, (const __nv_bfloat16*)dy,
+             (const __nv_bfloat16*)z, mean, rstd, rpc, part);
+  } else {
+    launch_k(bn_bwd_part_kernel<T>, dim3(ceil_div(C, 32), chunks), dim3(32, 8), 0, s, P, C, dy, z,
+             mean, rstd, rpc, part);
+  }
   note_launch();
   launch_k(bn_bwd_final_kernel, ceil_div(C, 8), 256, 0, s, chunks, C, part, dg, db);
   note_launch();
   const long total = (long)P * C;
-  launch_k(bn_bwd_dx_kernel<T>, grid_for(total), 256, 0, s, total, C, 1.f / (float)P, dy, z, mean, rstd,
-                                                      g, dg, db, dz);
+  if (vec)
+    launch_k(bn_bwd_dx_vkernel, grid_for(total / 8), 256, 0, s, total / 8, C, 1.f / (float)P,
+             (const __nv_bfloat16*)dy, (const __nv_bfloat16*)z, mean, rstd, g, dg, db,
+             (__nv_bfloat16*)dz);
+  else
+    launch_k(bn_bwd_dx_kernel<T>, grid_for(total), 256, 0, s, total, C, 1.f / (float)P, dy, z, mean,
+             rstd, g, dg, db, dz);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -443,9 +695,37 @@ __global__ void gap_bwd_kernel(int N, int HW, int C, const T* __restrict__ dp, T
   }
 }
 
+// one block per image: 8-channel vectors x RB rows per pass, fixed smem tree
+__global__ void __launch_bounds__(256)
+gap_vkernel(int HW, int C, const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ out) {
+  pdl_entry();
+  __shared__ float red[256 * 8];
+  const int V = C / 8, RB = 256 / V, t = threadIdx.x, vc = t % V, ro = t / V, n = blockIdx.x;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = ro; r < HW; r += RB) {
+    float v[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + ((long)n * HW + r) * C + vc * 8), v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += v[e];
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[ro * C + vc * 8 + e] = acc[e];
+  __syncthreads();
+  for (int stride = RB / 2; stride >= 1; stride >>= 1) {
+    for (int i = t; i < stride * C; i += 256) red[i] += red[i + stride * C];
+    __syncthreads();
+  }
+  for (int c = t; c < C; c += 256) out[(long)n * C + c] = __float2bfloat16_rn(red[c] / (float)HW);
+}
+
 template <typename T>
 int launch_gap(int N, int HW, int C, const T* x, T* out, cudaStream_t s) {
-  launch_k(gap_kernel<T>, ceil_div(N * C, 256), 256, 0, s, N, HW, C, x, out);
+  if (sizeof(T) == 2 && bn_vec_ok(C, x))
+    launch_k(gap_vkernel, N, 256, 0, s, HW, C, (const __nv_bfloat16*)x, (__nv_bfloat16*)out);
+  else
+    launch_k(gap_kernel<T>, ceil_div(N * C, 256), 256, 0, s, N, HW, C, x, out);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

@@ -15,6 +15,7 @@
 // W[k·k·Cin(padded to Kp), Cout] on the tcgen05 GEMM engine; its input
 // gradient is (dZ · Wᵀ) → col2im.  BatchNorm uses batch statistics (training
 // mode) with deterministic Welford / fixed-order reductions.
+#include <stdlib.h>
 #include <algorithm>
 #include <vector>
 #include "common.cuh"
@@ -26,6 +27,8 @@ struct ConvBN {            // conv (+ its BN) activations kept for the backward
   int cin, cout, k, stride, h_in, h_out, kp;
   char *col, *z;
   float *mean, *rstd;
+  const void* x_in = nullptr;   // conv input (implicit path: im2col deferred to the wgrad)
+  bool implicit = false;        // forward ran as the implicit-GEMM kernel
 };
 struct Block {
   ConvBN c1, c2;
@@ -99,23 +102,46 @@ static bool make_conv(ppll_resnet_stage* st, ConvBN& c, int cin, int cout, int k
   return c.col && c.z && c.mean && c.rstd;
 }
 
-// conv (im2col · W) → BN statistics; returns z in c.z
+static bool use_implicit(const ppll_resnet_stage* st, const ConvBN& c) {
+  static const int off = getenv("PPLL_CONV_IMPLICIT") ? !atoi(getenv("PPLL_CONV_IMPLICIT")) : 0;
+  return !off && st->dtype == PPLL_BF16 && c.k == 3 && c.stride == 1;
+}
+
+// conv → BN statistics; returns z in c.z.  3x3 stride-1 convolutions run as
+// the implicit-GEMM kernel (conv_tc.cu, TMA gathers the shifted windows);
+// the rest as im2col · W on the GEMM engine
 template <typename TT>
 static int conv_bn_fwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* x, int64_t w_off,
                        cudaStream_t s) {
   const int P = B * c.h_out * c.h_out;
-  int r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)x,
-                            (TT*)c.col, s);
-  if (r) return r;
-  LinOpts o;
-  r = gemm_fwd(P, c.kp, c.cout, c.col, c.kp, st->W(w_off), o, c.z, c.cout, st->dtype, st->ws,
-               st->ws_elems, s);
-  if (r) return r;
+  int r = PPLL_ERR_UNSUPPORTED;
+  c.implicit = false;
+  c.x_in = x;
+  if (use_implicit(st, c)) {
+    Epilogue<__nv_bfloat16> e;
+    e.C = (__nv_bfloat16*)c.z;
+    e.ldc = c.cout;
+    epilogue_finalize(e, c.cout);
+    r = launch_conv3x3_tc(B, c.h_in, c.h_in, c.cin, c.cout, (const __nv_bfloat16*)x,
+                          (const __nv_bfloat16*)st->W(w_off), false, e, s);
+    if (r != PPLL_OK && r != PPLL_ERR_UNSUPPORTED) return r;
+    c.implicit = r == PPLL_OK;
+  }
+  if (!c.implicit) {
+    r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)x,
+                          (TT*)c.col, s);
+    if (r) return r;
+    LinOpts o;
+    r = gemm_fwd(P, c.kp, c.cout, c.col, c.kp, st->W(w_off), o, c.z, c.cout, st->dtype, st->ws,
+                 st->ws_elems, s);
+    if (r) return r;
+  }
   return launch_bn_stats<TT>(P, c.cout, (const TT*)c.z, st->bn_part, c.mean, c.rstd, s);
 }
 
 // given dy (gradient w.r.t. the BN output, ReLU already applied): BN backward,
-// weight gradient, and (if dx) the input gradient col2im(dZ·Wᵀ) (+dres, ⊙mask)
+// weight gradient, and (if dx) the input gradient (+dres, ⊙mask): the
+// transposed implicit convolution, or col2im(dZ·Wᵀ)
 template <typename TT>
 static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, int64_t w_off,
                        int64_t g_off, int64_t b_off, void* dx, const void* dres,
@@ -124,9 +150,28 @@ static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, 
   int r = launch_bn_bwd<TT>(P, c.cout, (const TT*)dy, (const TT*)c.z, c.mean, c.rstd,
                             st->P(g_off), st->bn_part, st->G(g_off), st->G(b_off), (TT*)st->dz, s);
   if (r) return r;
+  if (c.implicit) {   // the weight gradient still contracts over the im2col'd input
+    r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)c.x_in,
+                          (TT*)c.col, s);
+    if (r) return r;
+  }
   r = linear_wgrad(P, c.kp, c.cout, c.col, c.kp, st->dz, c.cout, st->G(w_off), nullptr,
                    st->dtype, st->ws, st->ws_elems, s);
   if (r || !dx) return r;
+  if (c.implicit) {
+    Epilogue<__nv_bfloat16> e;
+    e.C = (__nv_bfloat16*)dx;
+    e.ldc = c.cin;
+    e.res = (const __nv_bfloat16*)dres;
+    e.ldres = c.cin;
+    e.mask = (const __nv_bfloat16*)mask;
+    e.ldmask = c.cin;
+    e.mask_mode = mask ? kMaskRelu : kMaskNone;
+    epilogue_finalize(e, c.cin);
+    r = launch_conv3x3_tc(B, c.h_out, c.h_out, c.cout, c.cin, (const __nv_bfloat16*)st->dz,
+                          (const __nv_bfloat16*)st->W(w_off), true, e, s);
+    if (r != PPLL_ERR_UNSUPPORTED) return r;
+  }
   LinOpts none;
   r = gemm_dgrad(P, c.kp, c.cout, st->dz, c.cout, st->W(w_off), none, st->dcol, c.kp, st->dtype,
                  st->ws, st->ws_elems, s);

@@ -101,3 +101,34 @@ def test_resnet_pipeline_bitwise_equals_roundrobin(precision):
     assert ma.loss_history == mb.loss_history
     for x, z in zip(a, b):
         assert np.array_equal(_flat(x), _flat(z))
+
+
+@pytest.mark.parametrize("N,H,Cin,Cout", [(4, 32, 16, 16), (2, 16, 32, 32), (4, 8, 64, 64),
+                                          (2, 16, 16, 32), (6, 8, 64, 32)])
+def test_implicit_conv3x3_matches_torch(N, H, Cin, Cout):
+    """The implicit-GEMM conv (TMA 4-D window gathers, SW32/64/128 K-major
+    tiles) against torch conv2d on the same bf16 values: forward and the
+    transposed-convolution input gradient."""
+    import torch.nn.functional as Fn
+    from paper_2411_12780_b200 import _native as N_
+    g = torch.Generator(device="cuda").manual_seed(N * H + Cin)
+    x = torch.randn(N, H, H, Cin, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(9 * Cin, Cout, device="cuda", generator=g) / (9 * Cin) ** 0.5).bfloat16()
+    dz = torch.randn(N, H, H, Cout, device="cuda", generator=g).bfloat16()
+    lib = N_.load()
+    s = torch.cuda.current_stream().cuda_stream
+    y = torch.empty(N, H, H, Cout, device="cuda", dtype=torch.bfloat16)
+    dx = torch.empty(N, H, H, Cin, device="cuda", dtype=torch.bfloat16)
+    N_.check(lib.ppll_conv3x3_bf16(N, H, H, Cin, Cout, x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                   0, s), "conv fwd")
+    N_.check(lib.ppll_conv3x3_bf16(N, H, H, Cin, Cout, dz.data_ptr(), w.data_ptr(),
+                                   dx.data_ptr(), 1, s), "conv dgrad")
+    torch.cuda.synchronize()
+    # torch weight [Cout, Cin, 3, 3] from the GEMM layout [(3r+s)·Cin + ci, co]
+    wt = w.float().reshape(3, 3, Cin, Cout).permute(3, 2, 0, 1).contiguous()
+    xr = x.float().permute(0, 3, 1, 2)
+    ref = Fn.conv2d(xr, wt, padding=1).permute(0, 2, 3, 1)
+    ref_dx = Fn.conv_transpose2d(dz.float().permute(0, 3, 1, 2), wt, padding=1).permute(0, 2, 3, 1)
+    for got, want in ((y, ref), (dx, ref_dx)):
+        err = (got.float() - want).abs().max().item() / (want.abs().max().item() + 1e-9)
+        assert err < 1e-2, err
