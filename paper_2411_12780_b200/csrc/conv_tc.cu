@@ -29,9 +29,11 @@
 namespace ppll {
 namespace cv {
 
-constexpr int kEpiWarps = 16;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kNumSMs = 148;
+// epilogue warps: 4 per 16 output channels (one 16-column chunk per TMEM lane
+// quadrant and warp), so small-CO convolutions fit several CTAs per SM
+template <int CO> constexpr int epi_warps() { return 4 * (CO / 16); }
+template <int CO> constexpr int conv_threads() { return 64 + 32 * epi_warps<CO>(); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -114,8 +116,8 @@ struct ConvSmem {
   static constexpr int RB = CI * 2;                  // A / B row bytes (K = CI)
   static constexpr int A_BYTES = 128 * RB;           // one tap of a pixel tile
   static constexpr int W_BYTES = 9 * CO * RB;        // nine [CO x CI] weight tiles
-  static constexpr int STAGES = CI == 64 ? 6 : 9;    // tap slots (smem-limited at CI = 64)
-  static constexpr int STG = kEpiWarps * 1024;
+  static constexpr int STAGES = CI == 64 ? 6 : 18;   // tap slots (two pixel tiles below CI = 64)
+  static constexpr int STG = epi_warps<CO>() * 1024;
   static constexpr int TOTAL = STAGES * A_BYTES + W_BYTES + STG + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = 2 * CO <= 32 ? 32 : (2 * CO <= 64 ? 64 : 128);
 };
@@ -124,11 +126,12 @@ struct ConvSmem {
 // fwd:   Wtap[co][ci] = W[(tap·CI + ci)·CO + co]             (CI = Cin, CO = Cout)
 // dgrad: Wtap[co][ci] = W[((8 − tap)·CO + co)·CI + ci]       (CI = Cout, CO = Cin)
 template <int CI, int CO>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(conv_threads<CO>(), 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ wg,
                   int dgrad, int P, int H, int Wd, int rows, int imgs, Epilogue<__nv_bfloat16> ep) {
   using L = ConvSmem<CI, CO>;
   constexpr int S = L::STAGES, RB = L::RB;
+  constexpr int kEpiWarps = epi_warps<CO>(), kThreads = conv_threads<CO>();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
@@ -160,16 +163,24 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   pdl_entry();   // the weights below are written by the predecessor (optimizer step)
-  // stage the nine weight tiles, K-major and swizzled like the TMA'd A tiles
-  for (int i = threadIdx.x; i < 9 * CO * (CI / 8); i += kThreads) {
-    const int j = i % (CI / 8), co = (i / (CI / 8)) % CO, tap = i / (CI / 8) / CO;
-    __nv_bfloat16 v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ci = 8 * j + e;
-      v[e] = dgrad ? wg[((long)(8 - tap) * CO + co) * CI + ci] : wg[((long)tap * CI + ci) * CO + co];
+  // stage the nine weight tiles, K-major and swizzled like the TMA'd A tiles,
+  // reading the global weight rows as 16-B vectors
+  if (dgrad) {   // Wtap[co][ci..ci+7] is contiguous in W
+    for (int i = threadIdx.x; i < 9 * CO * (CI / 8); i += kThreads) {
+      const int j = i % (CI / 8), co = (i / (CI / 8)) % CO, tap = i / (CI / 8) / CO;
+      const uint4 q = *reinterpret_cast<const uint4*>(wg + ((long)(8 - tap) * CO + co) * CI + 8 * j);
+      *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = q;
     }
-    *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = *reinterpret_cast<uint4*>(v);
+  } else {       // W row (tap, ci) holds co contiguous: scatter into [co][ci]
+    for (int i = threadIdx.x; i < 9 * CI * (CO / 8); i += kThreads) {
+      const int j = i % (CO / 8), ci = (i / (CO / 8)) % CI, tap = i / (CO / 8) / CI;
+      const uint4 q = *reinterpret_cast<const uint4*>(wg + ((long)tap * CI + ci) * CO + 8 * j);
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        *reinterpret_cast<__nv_bfloat16*>(sw + tap * CO * RB + swz<RB>(8 * j + t, ci >> 3) +
+                                          (ci & 7) * 2) = e[t];
+    }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -277,8 +288,11 @@ static int run(const CUtensorMap& xm, const __nv_bfloat16* w, int dgrad, int P, 
     attr = true;
   }
   const int tiles = P / 128;
-  launch_k(kern, tiles < kNumSMs ? tiles : kNumSMs, kThreads, smem, s, xm, w, dgrad, P, H, Wd,
-           rows, imgs, ep);
+  int per_sm = 1;
+  PPLL_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, conv_threads<CO>(),
+                                                                smem));
+  const int grid = tiles < kNumSMs * per_sm ? tiles : kNumSMs * (per_sm > 0 ? per_sm : 1);
+  launch_k(kern, grid, conv_threads<CO>(), smem, s, xm, w, dgrad, P, H, Wd, rows, imgs, ep);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

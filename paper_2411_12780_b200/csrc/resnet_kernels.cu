@@ -30,21 +30,24 @@ struct FastDiv {
 // im2col: x [N,H,W,C] -> col [N·Ho·Wo, Kp], column (r·k + s)·C + c, zero pad
 // (spatial padding (k-1)/2 and columns >= k·k·C).  8-channel vectors when C%8==0.
 // ---------------------------------------------------------------------------
+// scalar form (C % 8 != 0, e.g. the 3-channel stem): one thread per 2-element
+// pair of a column row, 32-bit fast-division index math
 template <typename T>
-__global__ void im2col_kernel(int N, int H, int W, int C, int k, int stride, int Ho, int Wo, int Kp,
+__global__ void im2col_kernel(int total, int H, int W, int C, int k, int stride, int Kp,
+                              FastDiv fKp, FastDiv fC, FastDiv fk, FastDiv fWo, FastDiv fHo,
                               const T* __restrict__ x, T* __restrict__ col) {
   pdl_entry();
   const int p = (k - 1) / 2;
-  const long total = (long)N * Ho * Wo * Kp;
-  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long)gridDim.x * blockDim.x) {
-    const int kk = (int)(idx % Kp);
-    const long pix = idx / Kp;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += gridDim.x * blockDim.x) {
+    const unsigned pix = fKp.div(idx), kk = idx - pix * fKp.d;
     float v = 0.f;
-    if (kk < k * k * C) {
-      const int tap = kk / C, c = kk % C, r = tap / k, s = tap % k;
-      const int wo = (int)(pix % Wo), ho = (int)((pix / Wo) % Ho), n = (int)(pix / ((long)Wo * Ho));
-      const int h = ho * stride - p + r, w = wo * stride - p + s;
+    if (kk < (unsigned)(k * k * C)) {
+      const unsigned tap = fC.div(kk), c = kk - tap * fC.d;
+      const unsigned r = fk.div(tap), sx = tap - r * fk.d;
+      const unsigned q = fWo.div(pix), wo = pix - q * fWo.d;
+      const unsigned n = fHo.div(q), ho = q - n * fHo.d;
+      const int h = (int)ho * stride - p + (int)r, w = (int)wo * stride - p + (int)sx;
       if (h >= 0 && h < H && w >= 0 && w < W) v = to_f(x[(((long)n * H + h) * W + w) * C + c]);
     }
     DT<T>::st(col + idx, v);
@@ -87,7 +90,12 @@ int launch_im2col(int N, int H, int W, int C, int k, int stride, int Kp, const T
              (const __nv_bfloat16*)x, (__nv_bfloat16*)col);
   } else {
     const long n = (long)N * Ho * Wo * Kp;
-    launch_k(im2col_kernel<T>, grid_for(n), 256, 0, s, N, H, W, C, k, stride, Ho, Wo, Kp, x, col);
+    if (n >= (1L << 31)) {
+      set_error("im2col: %ld elements exceed the 32-bit index path", n);
+      return PPLL_ERR_UNSUPPORTED;
+    }
+    launch_k(im2col_kernel<T>, grid_for(n), 256, 0, s, (int)n, H, W, C, k, stride, Kp,
+             FastDiv(Kp), FastDiv(C), FastDiv(k), FastDiv(Wo), FastDiv(Ho), x, col);
   }
   note_launch();
   PPLL_LAUNCH_CHECK();
