@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .runtime import EpochMetrics
+from .runtime import EpochMetrics, _capture
 
 _HANDLE = 64
 
@@ -250,8 +250,7 @@ class DistributedPipeline:
             cap = torch.cuda.Stream(device=self.device)
             cap.wait_stream(stream)
             n0 = N.launch_count()
-            with torch.cuda.graph(g, stream=cap):
-                self._launch(p, slot, B, cap)
+            _capture(g, cap, lambda: self._launch(p, slot, B, cap))
             self.graph_kernels[key] = N.launch_count() - n0
             stream.wait_stream(cap)
             self.graphs[key] = g

@@ -222,7 +222,7 @@ def run_epoch(mode: RunMode, modules: Sequence[LocalModule], dataset_iter: Itera
     config = config or RunConfig()
     _validate_modules(modules)
     if mode == RunMode.PPLL:
-        return DevicePipeline(modules, config).run(dataset_iter)
+        return _pipeline_for(modules, config).run(dataset_iter)
     if mode in (RunMode.E2E, RunMode.NAIVE_PP):
         return _run_backprop(modules, dataset_iter, config, pipelined=mode == RunMode.NAIVE_PP,
                              virtual_time=False)
@@ -398,6 +398,31 @@ def _run_backprop(modules, dataset_iter, config, pipelined: bool, virtual_time: 
     return metrics
 
 
+def _pipeline_for(modules, config):
+    """The DevicePipeline of this module list and ring configuration, reused
+    across epochs (its rings, staging buffers and per-(stage, slot) CUDA graphs
+    are built once; a training loop calls run_epoch once per epoch)."""
+    key = (tuple(id(m) for m in modules), config.buffer_capacity, config.use_graphs,
+           config.timing)
+    cache = modules[0].__dict__.setdefault("_pipelines", {})
+    pipe = cache.get(key)
+    if pipe is None:
+        pipe = cache[key] = DevicePipeline(modules, config)
+    return pipe
+
+
+def _capture(graph, stream, fn):
+    """Capture fn() into graph on stream.  The graphs hold only library kernel
+    launches and copies into preallocated buffers, so the allocator pool
+    bookkeeping (and the cache flush) of torch.cuda.graph is skipped."""
+    with torch.cuda.stream(stream):
+        graph.capture_begin(capture_error_mode="thread_local")
+        try:
+            fn()
+        finally:
+            graph.capture_end()
+
+
 # --------------------------------------------------------------------------
 # device rings
 # --------------------------------------------------------------------------
@@ -500,8 +525,7 @@ class DevicePipeline:
             cap = torch.cuda.Stream(device=self.modules[j].device)
             cap.wait_stream(stream)
             with torch.cuda.device(self.modules[j].device):
-                with torch.cuda.graph(g, stream=cap):
-                    self._launch(j, slot, B, cap)
+                _capture(g, cap, lambda: self._launch(j, slot, B, cap))
             stream.wait_stream(cap)
             self.graphs[key] = g
         with torch.cuda.stream(stream):
