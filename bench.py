@@ -55,6 +55,10 @@ WORKLOADS = {
                                                classes=10),
                       s=8, d_prime=1, interval=3, batch=256, ref_batch=4, data_shape="SVHN",
                       split="cost"),
+    # configs[3]: ViT-base / 8 blocks, STL-10-shaped 96x96, patch 16 (T = 37), batch 128
+    "vit_b": dict(kind="vit", spec=dict(image=96, channels=3, patch=16, dim=768, heads=12,
+                                        mlp=3072, depth=12, classes=10),
+                  s=8, d_prime=1, interval=3, batch=128, ref_batch=1, data_shape="STL-10"),
     "mlp_m": dict(kind="mlp", dims=(3072, 1024, 1024, 1024, 1024, 10), s=4, d_prime=2,
                   interval=3, batch=128, ref_batch=128),
 }
@@ -115,6 +119,11 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def balanced_depths_list(depth, s):
+    q, r = divmod(depth, s)
+    return [q + (1 if j < r else 0) for j in range(s)]
+
+
 def describe(wl, name):
     if wl["kind"] == "resnet":
         sp = wl["spec"]
@@ -124,11 +133,13 @@ def describe(wl, name):
                 f"{wl['data_shape']}-shaped {sp['image']}x{sp['image']}x3 NHWC, batch {wl['batch']}")
     if wl["kind"] == "vit":
         sp = wl["spec"]
-        return (f"{name}: PPLL ViT-small/{sp['patch']} depth {sp['depth']} D={sp['dim']} "
-                f"heads={sp['heads']} MLP={sp['mlp']}, {wl['s']} gradient-isolated blocks of "
-                f"{sp['depth'] // wl['s']} layers, aux = aux_depth(l,{wl['d_prime']},"
-                f"{wl['interval']}) transformer layers + LN + classifier, CIFAR-shaped "
-                f"{sp['channels']}x{sp['image']}x{sp['image']}, {sp['classes']} classes")
+        size = "base" if sp["dim"] >= 768 else "small"
+        return (f"{name}: PPLL ViT-{size}/{sp['patch']} depth {sp['depth']} D={sp['dim']} "
+                f"heads={sp['heads']} MLP={sp['mlp']}, {wl['s']} gradient-isolated blocks "
+                f"(layers {balanced_depths_list(sp['depth'], wl['s'])}), aux = aux_depth(l,"
+                f"{wl['d_prime']},{wl['interval']}) transformer layers + LN + classifier, "
+                f"{wl.get('data_shape', 'CIFAR-10')}-shaped {sp['channels']}x{sp['image']}x"
+                f"{sp['image']}, {sp['classes']} classes, batch {wl['batch']}")
     return (f"{name}: PPLL MLP {'-'.join(map(str, wl['dims']))}, {wl['s']} gradient-isolated "
             f"stages, d'={wl['d_prime']}, n={wl['interval']}, CIFAR-shaped 3x32x32 inputs")
 
@@ -183,7 +194,7 @@ def cpu_reference(wl, n_batches, warmup=1, time_budget=None, batch=None):
     else:
         import vit_oracle as vo
         spec = vo.VitSpec(**wl["spec"])
-        depths = [spec.depth // wl["s"]] * wl["s"]
+        depths = balanced_depths_list(spec.depth, wl["s"])
         stages = vo.build_vit_stages(spec, depths, wl["d_prime"], wl["interval"], 42)
         data = [(rng.standard_normal((B, spec.channels, spec.image, spec.image)),
                  rng.integers(0, spec.classes, B)) for _ in range(4)]

@@ -159,3 +159,25 @@ def test_vit_s_geometry_bf16_vs_oracle():
     for m, st in zip(mods, stages):
         a, b = _flat(m), _flat_o(st)
         assert np.abs(a - b).max() / np.abs(b).max() <= 5e-2
+
+
+VIT_B = dict(image=96, channels=3, patch=16, dim=768, heads=12, mlp=3072, depth=2, classes=10)
+
+
+def test_vit_b_stl_geometry_bf16_vs_oracle():
+    """configs[3] geometry: ViT-B (D 768, 12 heads, MLP 3072) at 96x96 patch 16
+    (T = 37) — the wide-row LayerNorm, D=768 GEMMs and T=37 attention."""
+    spec, mods, stages = _pair(VIT_B, [1, 1], 1, 3, "bf16", 2)
+    rng = np.random.default_rng(3)
+    img = rng.standard_normal((2, 3, 96, 96))
+    y = rng.integers(0, 10, 2)
+    h, hr = lp.Tensor(img), img
+    for m, st in zip(mods, stages):
+        loss, h = lp.local_loss_and_update(m, h, y)
+        ref, hr, _ = vo.local_step(st, hr, y, 0.05, 0.001, 2, 0.9, 1e-4)
+        assert abs(loss - ref) <= 3e-2 * abs(ref)
+        assert np.abs(h.data - hr).max() / np.abs(hr).max() <= 5e-2
+        hr = h.data
+    for m, st in zip(mods, stages):
+        a, b = _flat(m), _flat_o(st)
+        assert np.abs(a - b).max() / np.abs(b).max() <= 5e-2
