@@ -139,6 +139,13 @@ int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x, con
  * HBM-resident dataset. */
 int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx, void* dst,
                      int dst_dtype, const int64_t* labels_src, int64_t* labels_dst, void* stream);
+/* Same gather from a dataset held as the IDX file's pixel bytes (uint8):
+ * dst[r,c] = src[idx[r],c] / 255 (IEEE division, then the dst cast) — the
+ * [0,1] scaling of load_idx (data.py:137-139) applied per batch on the
+ * device, so the resident dataset costs 1 B per feature. */
+int ppll_gather_rows_u8(int n, int64_t width, const uint8_t* src, const int64_t* idx, void* dst,
+                        int dst_dtype, const int64_t* labels_src, int64_t* labels_dst,
+                        void* stream);
 /* *count += #{r < B : argmax_c logits[r,c] == labels[r]} (first maximum, as
  * numpy's argmax): the accuracy count of evaluate (harness.py:121-131). */
 int ppll_count_correct(int B, int C, const void* logits, int ldz, int dtype,

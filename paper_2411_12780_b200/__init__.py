@@ -25,7 +25,9 @@ from .blocks import (
     partition,
 )
 from .errors import (
+    BadMagic,
     ConfigMismatch,
+    CountMismatch,
     DimensionMismatch,
     EmptyEvents,
     EmptyProfiles,
@@ -40,6 +42,7 @@ from .errors import (
     PushAfterClose,
     StepOutOfRange,
     TooManyStages,
+    TruncatedFile,
     WorkerPanic,
     ZeroDuration,
 )
@@ -57,7 +60,8 @@ from .runtime import (
     throughput,
 )
 from .tensor import Tensor, matmul, softmax_xent
-from .data import BatchIterator, Dataset, DeviceDataset, batches
+from .data import (BatchIterator, Dataset, DeviceDataset, IdxDataset, batches, gen_blobs,
+                   gen_spirals, load_idx, spiral_reference)
 from .costs import (
     CommModel,
     CostEstimate,
@@ -74,7 +78,9 @@ from .costs import (
     t_pp,
     t_ppll,
 )
-from .harness import CSV_HEADER, MetricsRecord, device_memory, evaluate, write_metrics_csv
+from .harness import (CSV_HEADER, ComparisonReport, ExperimentConfig, MetricsRecord, ModeSummary,
+                      build_pipeline, device_memory, estimate_k, evaluate, make_datasets,
+                      report_table, run_experiment, validate_config, write_metrics_csv)
 from .vit import VitLocalModule, VitSpec, balanced_depths, build_vit_modules
 from .resnet import ResLocalModule, ResNetSpec, build_resnet_modules, resnet_split
 

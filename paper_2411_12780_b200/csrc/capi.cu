@@ -223,6 +223,18 @@ int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx,
   return launch_gather_rows(n, width, src, idx, dst, dst_dtype, labels_src, labels_dst, S(stream));
 }
 
+int ppll_gather_rows_u8(int n, int64_t width, const uint8_t* src, const int64_t* idx, void* dst,
+                        int dst_dtype, const int64_t* labels_src, int64_t* labels_dst,
+                        void* stream) {
+  if (n < 0 || width < 1 || !src || !idx || !dst || (labels_src && !labels_dst) ||
+      (dst_dtype != PPLL_F32 && dst_dtype != PPLL_BF16)) {
+    set_error("gather_rows_u8: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  return launch_gather_rows_u8(n, width, src, idx, dst, dst_dtype, labels_src, labels_dst,
+                               S(stream));
+}
+
 int ppll_count_correct(int B, int C, const void* logits, int ldz, int dtype,
                        const int64_t* labels, unsigned long long* count, void* stream) {
   if (B < 0 || C < 1 || !logits || !labels || !count) {

@@ -661,6 +661,61 @@ int launch_gather_rows(int n, long width, const float* src, const int64_t* idx, 
   return PPLL_OK;
 }
 
+// IDX pixels kept in HBM as the file's bytes (1 B/feature, a quarter of fp32):
+// one warp per row, 16 pixels per lane-load, value = byte / 255 with IEEE
+// division (load_idx scales to [0,1], data.py:137-139), fused bf16 cast
+template <typename TD>
+__global__ void gather_rows_u8_kernel(int n, long width, const uint8_t* __restrict__ src,
+                                      const int64_t* __restrict__ idx, TD* __restrict__ dst,
+                                      const int64_t* __restrict__ ysrc, int64_t* __restrict__ ydst,
+                                      int vec) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const long row = idx[r];
+  const uint8_t* s = src + row * width;
+  TD* d = dst + (long)r * width;
+  if (ysrc && lane == 0) ydst[r] = ysrc[row];
+  if (vec) {
+    for (long c = 16 * lane; c < width; c += 512) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(s + c));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float f[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) f[b] = __fdiv_rn((float)((w[q] >> (8 * b)) & 0xffu), 255.f);
+        if constexpr (sizeof(TD) == 4) {
+          *reinterpret_cast<float4*>(d + c + 4 * q) = make_float4(f[0], f[1], f[2], f[3]);
+        } else {
+          __nv_bfloat162 h[2] = {__floats2bfloat162_rn(f[0], f[1]), __floats2bfloat162_rn(f[2], f[3])};
+          *reinterpret_cast<uint2*>(d + c + 4 * q) = *reinterpret_cast<uint2*>(h);
+        }
+      }
+    }
+  } else {
+    for (long c = lane; c < width; c += 32) DT<TD>::st(d + c, __fdiv_rn((float)s[c], 255.f));
+  }
+}
+
+int launch_gather_rows_u8(int n, long width, const uint8_t* src, const int64_t* idx, void* dst,
+                          int dst_dtype, const int64_t* ysrc, int64_t* ydst, cudaStream_t s) {
+  if (n <= 0) return PPLL_OK;
+  const int vec = (width % 16) == 0 && ((uintptr_t)src & 15) == 0 &&
+                  ((uintptr_t)dst & (dst_dtype == PPLL_F32 ? 15 : 7)) == 0;
+  const int blocks = (n + 7) / 8;
+  if (dst_dtype == PPLL_F32)
+    launch_k(gather_rows_u8_kernel<float>, blocks, 256, 0, s, n, width, src, idx, (float*)dst,
+             ysrc, ydst, vec);
+  else
+    launch_k(gather_rows_u8_kernel<__nv_bfloat16>, blocks, 256, 0, s, n, width, src, idx,
+             (__nv_bfloat16*)dst, ysrc, ydst, vec);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
 // evaluate (harness.py:121-131): count rows whose argmax (first maximum, like
 // numpy) equals the label; integer atomics, so the count is exact
 template <typename T>

@@ -776,6 +776,8 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
 int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t s);
 int launch_gather_rows(int n, long width, const float* src, const int64_t* idx, void* dst,
                        int dst_dtype, const int64_t* ysrc, int64_t* ydst, cudaStream_t s);
+int launch_gather_rows_u8(int n, long width, const uint8_t* src, const int64_t* idx, void* dst,
+                          int dst_dtype, const int64_t* ysrc, int64_t* ydst, cudaStream_t s);
 int launch_count_correct(int B, int C, const void* z, long ldz, int dtype, const int64_t* y,
                          unsigned long long* count, cudaStream_t s);
 int launch_relu_mask(long n, const void* g, const void* act, void* out, int dtype, cudaStream_t s);

@@ -12,18 +12,24 @@ row, 16-B vectors, optional fused bf16 cast), so an epoch moves no host data
 per batch.  ``run_epoch`` consumes either form (host arrays are staged
 through pinned memory; device tensors go straight to the first ring).
 
-The synthetic generators and the IDX reader of the reference are data
-tooling outside the hot path and are not rebuilt here.
+The reference's dataset sources are here too: the
+seeded synthetic generators ``gen_blobs`` / ``gen_spirals`` (same PCG64 draw
+order, so the same seed gives the same rows) and the big-endian IDX reader
+``load_idx``.  An IDX dataset keeps the file's pixel bytes next to the
+float view; ``DeviceDataset`` then holds those bytes in HBM (1 B/feature)
+and ``ppll_gather_rows_u8`` applies the /255 scaling per batch on the device.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+import struct
+from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import torch
 
 from . import _native as N
-from .errors import InvalidArg
+from .errors import BadMagic, CountMismatch, InvalidArg, TruncatedFile
 
 
 @dataclass(frozen=True)
@@ -52,6 +58,120 @@ class Dataset:
     @property
     def dim(self) -> int:
         return self.features.shape[1]
+
+
+@dataclass(frozen=True)
+class IdxDataset(Dataset):
+    """A ``Dataset`` read from IDX files that also keeps the raw pixel bytes
+    ``[N x D]`` uint8 (``features == pixels / 255``)."""
+
+    pixels: np.ndarray = field(default=None, repr=False, compare=False)
+
+
+# blob class means: the class index unravelled on a side^dim integer lattice,
+# scaled by 4 (data.py:14-16, 64-75)
+BLOB_LATTICE_SPACING = 4.0
+# spiral arm: theta in [0.5, 0.5 + 1.5 * 2pi), radius = theta / theta_end
+# (data.py:18-21, 78-87)
+SPIRAL_BASE_ANGLE = 0.5
+SPIRAL_TURNS = 1.5
+
+
+def gen_blobs(n_per_class: int, classes: int, dim: int, spread: float,
+              seed: int) -> Dataset:
+    """One isotropic Gaussian cluster per class (data.py:52-75).
+
+    Rows are grouped by class; class ``c`` is centred at the lattice point
+    ``unravel_index(c, (side,)*dim) * 4`` with the smallest ``side`` such that
+    ``side**dim >= classes``.  One ``default_rng(seed)``, drawn class by class
+    ``normal(0, spread, (n_per_class, dim))``, so equal seeds give bit-equal
+    data.  ``spread == 0`` puts every row on its mean.
+    """
+    if min(n_per_class, classes, dim) < 1:
+        raise InvalidArg("n_per_class, classes, and dim must all be >= 1")
+    if spread < 0:
+        raise InvalidArg(f"spread must be >= 0, got {spread}")
+    side = 1
+    while side ** dim < classes:
+        side += 1
+    rng = np.random.default_rng(seed)
+    n = classes * n_per_class
+    features = np.empty((n, dim), dtype=np.float64)
+    for c in range(classes):
+        centre = np.asarray(np.unravel_index(c, (side,) * dim), dtype=np.float64)
+        rows = slice(c * n_per_class, (c + 1) * n_per_class)
+        features[rows] = centre * BLOB_LATTICE_SPACING + \
+            rng.normal(0.0, spread, size=(n_per_class, dim))
+    labels = np.repeat(np.arange(classes, dtype=np.int64), n_per_class)
+    return Dataset(features, labels, classes)
+
+
+def spiral_reference(n_per_class: int) -> tuple[np.ndarray, np.ndarray]:
+    """The two noise-free spiral arms, ``[n x 2]`` each (data.py:78-87); the
+    second arm is the first rotated by pi."""
+    t = np.arange(n_per_class, dtype=np.float64) / n_per_class
+    end = SPIRAL_BASE_ANGLE + 2.0 * np.pi * SPIRAL_TURNS
+    theta = SPIRAL_BASE_ANGLE + 2.0 * np.pi * SPIRAL_TURNS * t
+    r = theta / end
+    arm = np.stack([r * np.cos(theta), r * np.sin(theta)], axis=1)
+    return arm, -arm
+
+
+def gen_spirals(n_per_class: int, noise: float, seed: int) -> Dataset:
+    """Two interleaved spiral arms, class 0 then class 1, plus isotropic
+    Gaussian noise ``normal(0, noise, (2n, 2))`` from ``default_rng(seed)``
+    (data.py:90-104)."""
+    if n_per_class < 1:
+        raise InvalidArg("n_per_class must be >= 1")
+    if noise < 0:
+        raise InvalidArg(f"noise must be >= 0, got {noise}")
+    arm0, arm1 = spiral_reference(n_per_class)
+    clean = np.concatenate([arm0, arm1], axis=0)
+    labels = np.repeat(np.array([0, 1], dtype=np.int64), n_per_class)
+    noisy = clean + np.random.default_rng(seed).normal(0.0, noise, size=clean.shape)
+    return Dataset(noisy, labels, 2)
+
+
+_IDX_IMAGES = 0x00000803     # unsigned-byte data, 3 dimensions
+_IDX_LABELS = 0x00000801     # unsigned-byte data, 1 dimension
+
+
+def _idx_dims(raw: bytes, n_dims: int, magic: int, path) -> tuple[int, ...]:
+    """Big-endian magic + ``n_dims`` uint32 sizes (data.py:107-115)."""
+    need = 4 * (n_dims + 1)
+    if len(raw) < need:
+        raise TruncatedFile(f"{path}: header needs {need} bytes, file has {len(raw)}")
+    head = struct.unpack(">" + "I" * (n_dims + 1), raw[:need])
+    if head[0] != magic:
+        raise BadMagic(f"{path}: magic {head[0]:#010x}, expected {magic:#010x}")
+    return head[1:]
+
+
+def load_idx(images_path, labels_path) -> IdxDataset:
+    """An IDX image/label pair as a flat dataset (data.py:118-144).
+
+    Images ``[count, rows, cols]`` bytes become feature rows scaled by 1/255;
+    labels are bytes; ``num_classes = max label + 1``.  Bytes after the
+    declared payload are ignored; a short payload raises ``TruncatedFile``, a
+    wrong magic ``BadMagic``, differing counts ``CountMismatch``.
+    """
+    img = Path(images_path).read_bytes()
+    count, rows, cols = _idx_dims(img, 3, _IDX_IMAGES, images_path)
+    n_pix = count * rows * cols
+    if len(img) - 16 < n_pix:
+        raise TruncatedFile(f"{images_path}: payload has {len(img) - 16} bytes, "
+                            f"header declares {n_pix}")
+    lbl = Path(labels_path).read_bytes()
+    (n_lbl,) = _idx_dims(lbl, 1, _IDX_LABELS, labels_path)
+    if len(lbl) - 8 < n_lbl:
+        raise TruncatedFile(f"{labels_path}: payload has {len(lbl) - 8} bytes, "
+                            f"header declares {n_lbl}")
+    if n_lbl != count:
+        raise CountMismatch(f"{count} images but {n_lbl} labels")
+    pixels = np.frombuffer(img, dtype=np.uint8, count=n_pix, offset=16).reshape(count, rows * cols).copy()
+    labels = np.frombuffer(lbl, dtype=np.uint8, count=n_lbl, offset=8).astype(np.int64)
+    features = pixels.astype(np.float64) / 255.0
+    return IdxDataset(features, labels, int(labels.max()) + 1 if n_lbl else 0, pixels=pixels)
 
 
 def _order(n: int, shuffle: bool, seed: int) -> np.ndarray:
@@ -92,7 +212,8 @@ def batches(dataset: Dataset, batch_size: int, shuffle: bool = False,
 
 
 class DeviceDataset:
-    """A ``Dataset`` resident in HBM (fp32 features, int64 labels).
+    """A ``Dataset`` resident in HBM (fp32 features, int64 labels; an
+    ``IdxDataset`` is held as its uint8 pixels and scaled per batch).
 
     ``batches(batch_size, shuffle, seed, dtype)`` yields ``(x, y)`` device
     tensors in exactly ``BatchIterator``'s order; ``x`` is fp32 or, with
@@ -105,8 +226,10 @@ class DeviceDataset:
         self.dataset = dataset
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
-        self.features = torch.as_tensor(np.ascontiguousarray(dataset.features, dtype=np.float32),
-                                        device=self.device)
+        pixels = getattr(dataset, "pixels", None)
+        src = pixels if pixels is not None else np.ascontiguousarray(dataset.features,
+                                                                     dtype=np.float32)
+        self.features = torch.as_tensor(np.ascontiguousarray(src), device=self.device)
         self.labels = torch.as_tensor(np.asarray(dataset.labels, dtype=np.int64),
                                       device=self.device)
 
@@ -123,9 +246,10 @@ class DeviceDataset:
         """out_x[r] = features[idx[r]], out_y[r] = labels[idx[r]] (device)."""
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         code = N.BF16 if out_x.dtype == torch.bfloat16 else N.F32
-        N.check(N.load().ppll_gather_rows(int(idx.numel()), self.dim, self.features.data_ptr(),
-                                          idx.data_ptr(), out_x.data_ptr(), code,
-                                          self.labels.data_ptr(), out_y.data_ptr(), s), "gather")
+        fn = N.load().ppll_gather_rows_u8 if self.features.dtype == torch.uint8 \
+            else N.load().ppll_gather_rows
+        N.check(fn(int(idx.numel()), self.dim, self.features.data_ptr(), idx.data_ptr(),
+                   out_x.data_ptr(), code, self.labels.data_ptr(), out_y.data_ptr(), s), "gather")
 
     def batches(self, batch_size: int, shuffle: bool = False, seed: int = 0,
                 dtype=torch.float32):

@@ -724,7 +724,8 @@ def _run_ppll_roundrobin(modules, dataset_iter, config) -> EpochMetrics:
                     N.check(lib.ppll_cast(B * modules[0].in_features, xd.data_ptr(), N.F32,
                                           r.x[0][slot].data_ptr(), N.BF16, stream.cuda_stream),
                             "cast")
-                r.y[0][slot, :B].copy_(torch.as_tensor(np.asarray(y)).to(torch.int64))
+                yt = y if torch.is_tensor(y) else torch.as_tensor(np.asarray(y))
+                r.y[0][slot, :B].copy_(yt.to(torch.int64))
             progress[0] = next_id
             bufs[0].append(next_id)
             high_water[0] = max(high_water[0], len(bufs[0]))

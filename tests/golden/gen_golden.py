@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import json
 import os
+import struct
 import sys
 
 import numpy as np
@@ -203,6 +204,61 @@ def gen_data_and_csv():
         json.dump(orders, f, indent=0)
 
 
+def gen_datasets():
+    """Synthetic generators (data.py:52-104) and the IDX reader (data.py:107-144)
+    of the reference on fixed seeds / hand-packed bytes."""
+    import tempfile
+    out = {}
+    for i, (npc, c, d, spread, seed) in enumerate([(30, 3, 5, 0.4, 1), (2, 4, 2, 0.0, 0),
+                                                    (10, 2, 3, 0.5, 7), (7, 9, 2, 0.25, 11),
+                                                    (4, 5, 1, 1.5, 3)]):
+        ds = lp.gen_blobs(npc, c, d, spread, seed)
+        out[f"blobs{i}_args"] = np.array([npc, c, d, spread, seed], dtype=np.float64)
+        out[f"blobs{i}_x"], out[f"blobs{i}_y"] = ds.features, ds.labels
+    for i, (npc, noise, seed) in enumerate([(150, 0.0, 4), (150, 0.05, 4), (33, 0.2, 9)]):
+        ds = lp.gen_spirals(npc, noise, seed)
+        out[f"spiral{i}_args"] = np.array([npc, noise, seed], dtype=np.float64)
+        out[f"spiral{i}_x"], out[f"spiral{i}_y"] = ds.features, ds.labels
+    a0, a1 = lp.spiral_reference(200)
+    out["spiral_ref0"], out["spiral_ref1"] = a0, a1
+    rng = np.random.default_rng(77)
+    count, rows, cols = 37, 5, 7
+    img = struct.pack(">IIII", 0x803, count, rows, cols) + \
+        rng.integers(0, 256, count * rows * cols, dtype=np.uint8).tobytes() + b"tail"
+    lbl = struct.pack(">II", 0x801, count) + rng.integers(0, 6, count, dtype=np.uint8).tobytes()
+    with tempfile.TemporaryDirectory() as td:
+        ip, lp_ = os.path.join(td, "i.idx"), os.path.join(td, "l.idx")
+        open(ip, "wb").write(img)
+        open(lp_, "wb").write(lbl)
+        ds = lp.load_idx(ip, lp_)
+    out["idx_images"] = np.frombuffer(img, dtype=np.uint8)
+    out["idx_labels"] = np.frombuffer(lbl, dtype=np.uint8)
+    out["idx_x"], out["idx_y"] = ds.features, ds.labels
+    out["idx_classes"] = np.array(ds.num_classes)
+    np.savez_compressed(os.path.join(HERE, "datasets.npz"), **out)
+
+
+def gen_experiment():
+    """harness.run_experiment (deterministic) on blobs and spirals configs:
+    every metrics column except batches/s, plus the report's shape."""
+    from locopipe.config import ExperimentConfig
+    out = []
+    for kw in [dict(dataset="blobs", n_per_class=40, classes=4, dim=6, spread=0.6, seed=3,
+                    layer_dims=(6, 24, 20, 16, 4), stages=3, batch_size=16, epochs=2,
+                    lr0=0.05, lr_min=0.001, aux_depth_max=1, aux_depth_interval=2),
+               dict(dataset="spirals", n_per_class=50, noise=0.05, seed=9,
+                    layer_dims=(2, 32, 32, 2), stages=2, batch_size=20, epochs=2, lr0=0.1)]:
+        cfg = ExperimentConfig(**kw)
+        recs, rep = lp.run_experiment(cfg, deterministic=True)
+        out.append({"config": {k: list(v) if isinstance(v, tuple) else v for k, v in kw.items()},
+                    "records": [[r.mode, r.epoch, r.mean_loss, r.train_acc, r.test_acc,
+                                 r.params_max_stage, r.activations_max_stage, r.mean_staleness]
+                                for r in recs],
+                    "modes": [sm.mode for sm in rep.summaries], "stages": rep.stages})
+    with open(os.path.join(HERE, "experiment.json"), "w") as f:
+        json.dump(out, f, indent=0)
+
+
 def gen_costs():
     """costs.py analytic forms, simulator timelines and Gantt CSV (reference)."""
     cases = []
@@ -252,4 +308,6 @@ if __name__ == "__main__":
     gen_e2e_naive()
     gen_data_and_csv()
     gen_costs()
+    gen_datasets()
+    gen_experiment()
     print("ok")

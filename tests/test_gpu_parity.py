@@ -527,6 +527,31 @@ def test_device_dataset_batches_equal_host_batches():
     assert torch.equal(bx, torch.as_tensor(hx, dtype=torch.float32).bfloat16().cuda())
 
 
+def test_device_idx_dataset_u8_gather(tmp_path):
+    """An IDX dataset lives in HBM as its pixel bytes; the per-batch /255
+    (ppll_gather_rows_u8) reproduces load_idx's features exactly in fp32
+    and as their bf16 rounding."""
+    import struct
+    rng = np.random.default_rng(3)
+    count, rows, cols = 203, 32, 48          # 1536 features: the 16-B vector path
+    for c in (cols, 7):                       # and a ragged width (scalar path)
+        pix = rng.integers(0, 256, (count, rows * c), dtype=np.uint8)
+        lab = rng.integers(0, 10, count, dtype=np.uint8)
+        (tmp_path / "i").write_bytes(struct.pack(">IIII", 0x803, count, rows, c) + pix.tobytes())
+        (tmp_path / "l").write_bytes(struct.pack(">II", 0x801, count) + lab.tobytes())
+        ds = lp.load_idx(tmp_path / "i", tmp_path / "l")
+        dd = lp.DeviceDataset(ds)
+        assert dd.features.dtype == torch.uint8
+        host = list(lp.batches(ds, 64, shuffle=True, seed=5))
+        dev = list(dd.batches(64, shuffle=True, seed=5))
+        dev16 = list(dd.batches(64, shuffle=True, seed=5, dtype=torch.bfloat16))
+        assert len(host) == len(dev) == 4
+        for (hx, hy), (dx, dy), (bx, _) in zip(host, dev, dev16):
+            assert np.array_equal(dx.cpu().numpy(), hx.astype(np.float32))
+            assert np.array_equal(dy.cpu().numpy(), hy)
+            assert torch.equal(bx, dx.bfloat16())
+
+
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_run_epoch_device_batches_equal_host_batches(precision):
     ds = _mlp_dataset()
@@ -580,3 +605,35 @@ def test_calibrate_feeds_the_schedule_simulator():
     r = lp.simulate_schedule(prof, lp.CommModel(), "ppll", 32, 2)
     assert r.steady_batch_time == pytest.approx(max(p.cycle for p in prof), rel=1e-6)
     assert min(r.idle_fraction(4)) < 1e-6
+
+
+def test_run_experiment_matches_reference(tmp_path):
+    """harness.run_experiment on the device (all three modes, 2 epochs, blobs
+    and spirals) against the reference's own run (tests/golden/experiment.json):
+    losses within the fp32 tolerance, accuracies within 2 rows, the float-count
+    memory proxy and the deterministic staleness exact."""
+    import json
+    cases = json.load(open(os.path.join(GOLDEN, "experiment.json")))
+    for case in cases:
+        kw = {k: tuple(v) if isinstance(v, list) else v for k, v in case["config"].items()}
+        cfg = lp.ExperimentConfig(**kw)
+        recs, rep = lp.run_experiment(cfg, deterministic=True)
+        n = cfg.n_per_class * (cfg.classes if cfg.dataset == "blobs" else 2)
+        assert len(recs) == len(case["records"])
+        for r, g in zip(recs, case["records"]):
+            assert (r.mode, r.epoch) == (g[0], g[1])
+            assert abs(r.mean_loss - g[2]) <= 5e-5, (r, g)
+            assert abs(r.train_acc - g[3]) <= 2.0 / n and abs(r.test_acc - g[4]) <= 2.0 / n, (r, g)
+            assert (r.params_max_stage, r.activations_max_stage) == (g[5], g[6])
+            assert abs(r.mean_staleness - g[7]) < 1e-12
+        assert [s.mode for s in rep.summaries] == case["modes"] and rep.stages == case["stages"]
+        assert rep.measured_k > 0 and rep.ppll_over_pp_throughput > 0
+        lp.write_metrics_csv(recs, tmp_path / "metrics.csv")
+        assert lp.report_table(rep).count("\n") == len(cfg.modes) + 2
+    # the threaded device pipeline trains bit-identically to the deterministic replay
+    cfg = lp.ExperimentConfig(**{k: tuple(v) if isinstance(v, list) else v
+                                 for k, v in cases[0]["config"].items()})
+    thr, _ = lp.run_experiment(cfg)
+    det, _ = lp.run_experiment(cfg, deterministic=True)
+    for a, b in zip(thr, det):
+        assert (a.mean_loss, a.train_acc, a.test_acc) == (b.mean_loss, b.train_acc, b.test_acc)
