@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libppll_b200.so")
+LIB_PATH = os.environ.get("PPLL_LIB") or os.path.join(_HERE, "lib", "libppll_b200.so")
 
 PPLL_OK, PPLL_ERR_ARG, PPLL_ERR_CUDA, PPLL_ERR_UNSUPPORTED, PPLL_ERR_CLOSED = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1

@@ -172,8 +172,13 @@ struct Smem {
 };
 
 struct Sched {
+  // TMA store maps of the outputs C and pre (valid when tma_st): the kernel
+  // takes Sched as a __grid_constant__ parameter so the maps live in param space
+  CUtensorMap st_c, st_p;
+  int tma_st;
   int mt, nt, tiles, splits, kps, items;
-  int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores
+  int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores,
+              // 2 = bias+GELU math only, 3 = stores only (interior tiles)
   // timeline probe (PPLL_GEMM_TIMELINE): per CTA and tile, %globaltimer at
   // MMA start / MMA done (tfull observed) / epilogue done, 4 tiles max
   unsigned long long* tl;
@@ -192,7 +197,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <typename TO, bool A_K, bool B_K, int BN, int F, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               int M, int N, int K, Sched sc, Epilogue<TO> ep, float* part) {
+               int M, int N, int K, const __grid_constant__ Sched sc, Epilogue<TO> ep,
+               float* part) {
   using L = Smem<BN>;
   constexpr int S = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -351,6 +357,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       if (sc.tl && it < 4 && warp == 2 && lane == 0) sc.tl[(blockIdx.x * 4 + it) * 4 + 1] = gtimer();
       const int row = m0 + q * 32 + lane;
       const bool live = row < M;
+      // interior tiles store without bounds tests (uniform per tile)
+      const bool full = F != kEFGeneric && ep.vec && m0 + BM <= M && n0 + BN <= N;
+      const bool tst = F != kEFGeneric && !MC && sc.tma_st;
 #pragma unroll 1
       for (int c = 16 * grp; c < BN && n0 + c < N; c += 16 * NG) {
         float ra[16], ka[16];
@@ -362,16 +371,46 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         uint32_t r[16];
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), r);
-        if (!split && !sc.probe) ep.template aux_finish<F>(qr, qk, ra, ka, stg, lane);
+        if (!split && !sc.probe) {
+          // aux_finish transposes through stg: the last bulk store must have read it
+          if (tst && (F & (kEFRes | kEFMaskRelu | kEFMaskMul)) != 0) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+          }
+          ep.template aux_finish<F>(qr, qk, ra, ka, stg, lane);
+        }
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
         if (split)
           warp_store_block16<float>(part + (long)z * M * N, N, nullptr, 0, m0 + q * 32, M, n0 + c,
                                     N, (N % 4) == 0, v, stg, lane);
-        else if (!sc.probe)
-          ep.template finish_block16_t<F>(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c, stg, lane);
-        else if (live && v[0] == 12345.f)   // keep the TMEM load live in probe mode
+        else if (!sc.probe) {
+          if (tst)
+            ep.template finish_block16_t<F, true, true>(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c,
+                                                        stg, lane, &sc.st_c, &sc.st_p);
+          else if (full)
+            ep.template finish_block16_t<F, true>(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c, stg,
+                                                  lane);
+          else
+            ep.template finish_block16_t<F>(m0 + q * 32, M, n0 + c, v, ra, ka, bs + c, stg, lane);
+        }
+        else if (sc.probe == 2) {           // math only (bias + GELU pair), no stores
+          float d[16], acc_s = 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            v[i] += bs[c + i]; v[i + 1] += bs[c + i + 1];
+            gelu_tanh2(v[i], v[i + 1], d[i], d[i + 1]);
+            acc_s += v[i] + v[i + 1] + d[i] + d[i + 1];
+          }
+          if (live && acc_s == 12345.f) ep.C[0] = (TO)acc_s;
+        } else if (sc.probe == 3) {         // stores only (both outputs, no math)
+          warp_store_block16<TO, true>(ep.C, ep.ldc, nullptr, 0, m0 + q * 32, M, n0 + c, N, true,
+                                       v, stg, lane);
+          if (ep.pre)
+            warp_store_block16<TO, true>(ep.pre, ep.ldpre, nullptr, 0, m0 + q * 32, M, n0 + c, N,
+                                         true, v, stg, lane);
+        } else if (live && v[0] == 12345.f)   // keep the TMEM load live in probe mode
           ep.C[0] = v[1];
       }
       // accumulator buffer drained: hand it back to the MMA warp
@@ -380,6 +419,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (sc.tl && it < 4 && lane == 0) atomicMax(&sc.tl[(blockIdx.x * 4 + it) * 4 + 2], gtimer());
     }
+    if (F != kEFGeneric && !MC && sc.tma_st) tma_store_drain(lane);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -672,6 +712,25 @@ static bool make_map(CUtensorMap* map, const void* ptr, long inner, long outer, 
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 2-D output map for the epilogue's TMA stores: box {32 B, 32 rows} (one
+// warp's 32-row x 16-column block, or 8 fp32 columns), 32-B swizzle (the
+// layout warp_store_tma16 writes), dims {N, M} so ragged edges are clipped.
+template <typename TO>
+static bool make_store_map(CUtensorMap* map, const void* ptr, long n, long m, long ld) {
+  auto enc = get_encode();
+  if (!enc || !ptr) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(TO))};
+  cuuint32_t box[2] = {(cuuint32_t)(32 / sizeof(TO)), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, sizeof(TO) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                        : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -987,6 +1046,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
     }
   }
   Sched sc;
+  sc.tma_st = 0;
   sc.mt = mt;
   sc.nt = ceil_div(N, bn);
   sc.tiles = sc.mt * sc.nt;
@@ -1048,6 +1108,11 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   float* part = sc.splits > 1 ? ws : nullptr;
   int r;
   const int f = epi_flags(e);
+  // epilogue stores through the TMA engine (PPLL_GEMM_TMA_STORE=0: st.global)
+  static const int tma_env = getenv("PPLL_GEMM_TMA_STORE") ? atoi(getenv("PPLL_GEMM_TMA_STORE")) : 1;
+  if (tma_env && sc.splits == 1 && f != kEFGeneric && !e.C2 && !e.cs_part && e.vec && !sc.probe)
+    sc.tma_st = make_store_map<TO>(&sc.st_c, e.C, N, M, e.ldc) &&
+                (!(f & kEFGeluD) || make_store_map<TO>(&sc.st_p, e.pre, N, M, e.ldpre));
   if (a_kmajor && !b_kmajor) r = dispatch_f<TO, true, false>(f, bn, ma, mb, M, N, K, sc, e, part, s);
   else if (a_kmajor && b_kmajor) r = dispatch_f<TO, true, true>(f, bn, ma, mb, M, N, K, sc, e, part, s);
   else if (!a_kmajor && !b_kmajor) r = dispatch_f<TO, false, false>(f, bn, ma, mb, M, N, K, sc, e, part, s);

@@ -214,7 +214,7 @@ __device__ __forceinline__ void st_row32<__nv_bfloat16>(__nv_bfloat16* p, bool v
 // `csum` (optional): this 32-row block's column sums of the stored (rounded)
 // values, rows >= M excluded, written as one partial row csum[n0 .. n0+31]
 // (a fused bias-gradient Σ_rows; reduced over the row blocks afterwards).
-template <typename TO>
+template <typename TO, bool kFull = false>
 __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, long ld2, int row0,
                                                    int M, int n0, int N, bool vec,
                                                    const float (&v)[32], uint8_t* stg, int lane,
@@ -251,12 +251,15 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
       const uint4 q = *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
       const int row = row0 + r;
       const int col = n0 + p * kCols + c * kEl;
-      if (csum && row < M) {
+      if (csum && (kFull || row < M)) {
         const TO* e = reinterpret_cast<const TO*>(&q);
 #pragma unroll
         for (int t = 0; t < kEl; ++t) cs[t] += to_f(e[t]);
       }
-      if (row < M && col < N) {
+      if constexpr (kFull) {
+        *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
+        if (out2) *reinterpret_cast<uint4*>(out2 + (long)row * ld2 + col) = q;
+      } else if (row < M && col < N) {
         if (vec && col + kEl <= N) {
           *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
           if (out2) *reinterpret_cast<uint4*>(out2 + (long)row * ld2 + col) = q;
@@ -286,6 +289,56 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
   }
 }
 
+// The same 32-row x 16-column block written by the TMA engine: the lanes put
+// it into the warp's 1-KB buffer in the 32-B-swizzled layout of a
+// {32 B, 32 rows} box (rows of 32 B, 16-B halves swapped on every other group
+// of four rows: conflict-free STS.128), then one lane issues a bulk tensor
+// store.  Rows >= M / columns >= N are clipped by the tensor map, so ragged
+// tiles need no tests.  Before the buffer is rewritten the previous bulk store
+// must have finished READING it (wait_group.read); global completion is
+// awaited once at kernel exit (tma_store_drain).
+template <typename TO>
+__device__ __forceinline__ void warp_store_tma16(const void* map, int row0, int n0,
+                                                 const float (&v)[16], uint8_t* stg, int lane) {
+  constexpr int kPasses = sizeof(TO) == 4 ? 2 : 1;
+  constexpr int kCols = 16 / kPasses;
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stg));
+#pragma unroll
+  for (int p = 0; p < kPasses; ++p) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint4 q;
+      if constexpr (sizeof(TO) == 4) {
+        q = make_uint4(__float_as_uint(v[p * kCols + 4 * j]), __float_as_uint(v[p * kCols + 4 * j + 1]),
+                       __float_as_uint(v[p * kCols + 4 * j + 2]), __float_as_uint(v[p * kCols + 4 * j + 3]));
+      } else {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          h[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+      }
+      const int sj = j ^ ((lane >> 2) & 1);
+      *reinterpret_cast<uint4*>(stg + lane * 32 + sj * 16) = q;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+              reinterpret_cast<uint64_t>(map)),
+          "r"(n0 + p * kCols), "r"(row0), "r"(sa)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+}
+__device__ __forceinline__ void tma_store_drain(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
 // Coalesced store of a warp's 32-row x 16-column block (thread = one row, 16
 // consecutive columns in registers, as tcgen05.ld 32x32b.x16 delivers them),
 // transposed through a 1-KB per-warp buffer: rows of 32 B (two 16-B chunks,
@@ -293,7 +346,8 @@ __device__ __forceinline__ void warp_store_block32(TO* out, long ld, TO* out2, l
 // the column-wise reads are bank-conflict free); each store instruction then
 // covers 16 rows x 32 contiguous bytes (one full sector per row).  fp32 goes
 // in two 8-column passes.  `csum` as in warp_store_block32.
-template <typename TO>
+// kFull: the block lies inside [M, N] and `vec` holds — no bounds tests.
+template <typename TO, bool kFull = false>
 __device__ __forceinline__ void warp_store_block16(TO* out, long ld, TO* out2, long ld2, int row0,
                                                    int M, int n0, int N, bool vec,
                                                    const float (&v)[16], uint8_t* stg, int lane,
@@ -322,18 +376,29 @@ __device__ __forceinline__ void warp_store_block16(TO* out, long ld, TO* out2, l
     float cs[kEl];
 #pragma unroll
     for (int e = 0; e < kEl; ++e) cs[e] = 0.f;
+    // both shared-memory reads before any global store: the stores then do
+    // not serialise on the reused source registers
+    uint4 qs[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int r = i * 16 + (lane >> 1), c = lane & 1;
-      const uint4 q = *reinterpret_cast<const uint4*>(stg + r * 32 + ((c ^ ((r >> 2) & 1)) * 16));
+      qs[i] = *reinterpret_cast<const uint4*>(stg + r * 32 + ((c ^ ((r >> 2) & 1)) * 16));
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = i * 16 + (lane >> 1), c = lane & 1;
+      const uint4 q = qs[i];
       const int row = row0 + r;
       const int col = n0 + p * kCols + c * kEl;
-      if (csum && row < M) {
+      if (csum && (kFull || row < M)) {
         const TO* e = reinterpret_cast<const TO*>(&q);
 #pragma unroll
         for (int t = 0; t < kEl; ++t) cs[t] += to_f(e[t]);
       }
-      if (row < M && col < N) {
+      if constexpr (kFull) {
+        *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
+        if (out2) *reinterpret_cast<uint4*>(out2 + (long)row * ld2 + col) = q;
+      } else if (row < M && col < N) {
         if (vec && col + kEl <= N) {
           *reinterpret_cast<uint4*>(out + (long)row * ld + col) = q;
           if (out2) *reinterpret_cast<uint4*>(out2 + (long)row * ld2 + col) = q;
@@ -631,11 +696,14 @@ struct Epilogue {
         ld_rowN<16>(mask + (long)m * ldmask + n0, vec != 0, valid, k);
     }
   }
-  template <int F>
+  // kFull: interior tile, unchecked stores; kTma: TMA bulk stores through the
+  // maps tm_c (C) and tm_p (pre)
+  template <int F, bool kFull = false, bool kTma = false>
   __device__ __forceinline__ void finish_block16_t(int row0, int M, int n0, float (&v)[16],
                                                    float (&r)[16], const float (&k)[16],
                                                    const float* bias_s, uint8_t* stg,
-                                                   int lane) const {
+                                                   int lane, const void* tm_c = nullptr,
+                                                   const void* tm_p = nullptr) const {
     if constexpr (F == kEFGeneric) {
       finish_block16(row0, M, n0, v, r, k, bias_s, stg, lane);
     } else {
@@ -661,7 +729,9 @@ struct Epilogue {
           if constexpr (sizeof(TO) == 2) gelu_tanh2(v[i], v[i + 1], r[i], r[i + 1]);
           else gelu_both2(v[i], v[i + 1], r[i], r[i + 1]);
         }
-        warp_store_block16<TO>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg, lane);
+        if constexpr (kTma) warp_store_tma16<TO>(tm_p, row0, n0, r, stg, lane);
+        else warp_store_block16<TO, kFull>(pre, ldpre, nullptr, 0, row0, M, n0, ncols, vv, r, stg,
+                                           lane);
       }
       if constexpr ((F & kEFRelu) != 0) {
 #pragma unroll
@@ -678,8 +748,9 @@ struct Epilogue {
           v[i] = t.x; v[i + 1] = t.y;
         }
       }
-      warp_store_block16<TO>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane,
-                             cs_part ? cs_part + (long)(row0 >> 5) * ncols : nullptr);
+      if constexpr (kTma) warp_store_tma16<TO>(tm_c, row0, n0, v, stg, lane);
+      else warp_store_block16<TO, kFull>(C, ldc, C2, ldc2, row0, M, n0, ncols, vv, v, stg, lane,
+                                         cs_part ? cs_part + (long)(row0 >> 5) * ncols : nullptr);
     }
   }
 
