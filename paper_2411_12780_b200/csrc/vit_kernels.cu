@@ -138,96 +138,134 @@ ln_bwd_vkernel(int M, const __nv_bfloat16* __restrict__ dy, long lddy,
   pdl_entry();
   // LPR lanes per row (16: two rows per warp; 32: one row per warp)
   constexpr int D = LPR * EPL, NQ = EPL / 8, RPW = 32 / LPR, RPB = 8 * RPW;
-  __shared__ float red[NS][D];
+  // parameter-gradient accumulators live in shared memory, one [NS][D] slab
+  // per row slot (registers go to the prefetch ring): [RPB][NS][D]
+  extern __shared__ float accS[];
   const int lane = threadIdx.x & 31, hl = lane & (LPR - 1), w = threadIdx.x >> 5;
   const int c0 = hl * EPL;
-  float gg[EPL];
-  ldv<EPL>(g + c0, gg);
-  float acc[NS][EPL];
+  float* my = accS + (size_t)(RPW * w + (LPR == 16 ? (lane >> 4) : 0)) * NS * D + c0;
 #pragma unroll
   for (int k = 0; k < NS; ++k)
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) acc[k][i] = 0.f;
+    for (int i = 0; i < EPL; i += 4) *reinterpret_cast<float4*>(my + k * D + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  // gamma staged in shared memory after the accumulator slabs
+  float* gS = accS + (size_t)RPB * NS * D;
+  for (int c = threadIdx.x; c < D; c += blockDim.x) gS[c] = g[c];
+  __syncthreads();
+  const float* gg = gS + c0;
   const int stride = gridDim.x * RPB;
-  int row = blockIdx.x * RPB + RPW * w + (LPR == 16 ? (lane >> 4) : 0);
-  uint4 qd[NQ], qx[NQ], qr[NQ];
-  float mu = 0.f, rs = 0.f;
-  if (row < M) {
-    ldq<EPL>(dy + (long)row * lddy + c0, qd);
-    ldq<EPL>(x + (long)row * ldx + c0, qx);
-    if (dres) ldq<EPL>(dres + (long)row * ldres + c0, qr);
-    mu = mean[row];
-    rs = rstd[row];
+  const int row0 = blockIdx.x * RPB + RPW * w + (LPR == 16 ? (lane >> 4) : 0);
+  // PF-deep prefetch ring: rows row0 + (it + k)·stride for the next PF trips
+  // are in flight while the current one is reduced (HBM latency hiding: one
+  // block of 8 warps per SM, so bytes in flight come from depth, not warps)
+  constexpr int PF = 2;
+  uint4 qd[PF][NQ], qx[PF][NQ], qr[PF][NQ];
+  float mu[PF], rs[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    const int r = row0 + k * stride;
+    mu[k] = rs[k] = 0.f;
+    if (r < M) {
+      ldq<EPL>(dy + (long)r * lddy + c0, qd[k]);
+      ldq<EPL>(x + (long)r * ldx + c0, qx[k]);
+      if (dres) ldq<EPL>(dres + (long)r * ldres + c0, qr[k]);
+      mu[k] = mean[r];
+      rs[k] = rstd[r];
+    }
   }
   // every half-warp runs the same trip count (shuffles stay converged)
   const int trips = (M + stride - 1) / stride;
-  for (int it = 0; it < trips; ++it) {
-    const bool live = row < M;
-    float d[EPL], xh[EPL], o[EPL];
-    if (live) {
-      unq<EPL>(qd, d);
-      unq<EPL>(qx, xh);
-      if (dres) unq<EPL>(qr, o);
-    } else {
+  for (int it0 = 0; it0 < trips; it0 += PF) {
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) d[i] = xh[i] = o[i] = 0.f;
-    }
-    const float cmu = mu, crs = rs;
-    const int crow = row;
-    row += stride;
-    if (row < M) {   // prefetch the next row
-      ldq<EPL>(dy + (long)row * lddy + c0, qd);
-      ldq<EPL>(x + (long)row * ldx + c0, qx);
-      if (dres) ldq<EPL>(dres + (long)row * ldres + c0, qr);
-      mu = mean[row];
-      rs = rstd[row];
-    }
-    float s1 = 0.f, s2 = 0.f;
+    for (int k = 0; k < PF; ++k) {
+      if (it0 + k >= trips) break;
+      const int crow = row0 + (it0 + k) * stride;
+      const bool live = crow < M;
+      float d[EPL], xh[EPL], o[EPL];
+      if (live) {
+        unq<EPL>(qd[k], d);
+        unq<EPL>(qx[k], xh);
+        if (dres) unq<EPL>(qr[k], o);
+      } else {
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) {
-      xh[i] = (xh[i] - cmu) * crs;
-      acc[0][i] += d[i] * xh[i];
-      acc[1][i] += d[i];
-      const float dxh = d[i] * gg[i];
-      s1 += dxh;
-      s2 += dxh * xh[i];
-    }
-    if (LPR == 16) {
-      s1 = half_sum(s1) * (1.f / D);
-      s2 = half_sum(s2) * (1.f / D);
-    } else {
-      s1 = warp_sum(s1) * (1.f / D);
-      s2 = warp_sum(s2) * (1.f / D);
-    }
-    if (live) {
+        for (int i = 0; i < EPL; ++i) d[i] = xh[i] = o[i] = 0.f;
+      }
+      const float cmu = mu[k], crs = rs[k];
+      const int nrow = crow + PF * stride;
+      if (nrow < M) {   // refill this slot PF trips ahead
+        ldq<EPL>(dy + (long)nrow * lddy + c0, qd[k]);
+        ldq<EPL>(x + (long)nrow * ldx + c0, qx[k]);
+        if (dres) ldq<EPL>(dres + (long)nrow * ldres + c0, qr[k]);
+        mu[k] = mean[nrow];
+        rs[k] = rstd[nrow];
+      }
+      float s1 = 0.f, s2 = 0.f;
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
-        const float t = crs * (d[i] * gg[i] - s1 - xh[i] * s2);
-        o[i] = dres ? o[i] + t : t;
-        if (NS == 3) acc[2][i] += o[i];
+        xh[i] = (xh[i] - cmu) * crs;
+        const float dxh = d[i] * gg[i];
+        s1 += dxh;
+        s2 += dxh * xh[i];
       }
-      if (dx) stv<EPL>(dx + (long)crow * lddx + c0, o);
+#pragma unroll
+      for (int i = 0; i < EPL; i += 4) {
+        float4 a = *reinterpret_cast<float4*>(my + i);
+        float4 b = *reinterpret_cast<float4*>(my + D + i);
+        a.x += d[i] * xh[i]; a.y += d[i + 1] * xh[i + 1];
+        a.z += d[i + 2] * xh[i + 2]; a.w += d[i + 3] * xh[i + 3];
+        b.x += d[i]; b.y += d[i + 1]; b.z += d[i + 2]; b.w += d[i + 3];
+        *reinterpret_cast<float4*>(my + i) = a;
+        *reinterpret_cast<float4*>(my + D + i) = b;
+      }
+      if (LPR == 16) {
+        s1 = half_sum(s1) * (1.f / D);
+        s2 = half_sum(s2) * (1.f / D);
+      } else {
+        s1 = warp_sum(s1) * (1.f / D);
+        s2 = warp_sum(s2) * (1.f / D);
+      }
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const float t = crs * (d[i] * gg[i] - s1 - xh[i] * s2);
+          o[i] = dres ? o[i] + t : t;
+        }
+        if (NS == 3) {
+#pragma unroll
+          for (int i = 0; i < EPL; i += 4) {
+            float4 c = *reinterpret_cast<float4*>(my + 2 * D + i);
+            c.x += o[i]; c.y += o[i + 1]; c.z += o[i + 2]; c.w += o[i + 3];
+            *reinterpret_cast<float4*>(my + 2 * D + i) = c;
+          }
+        }
+        if (dx) stv<EPL>(dx + (long)crow * lddx + c0, o);
+      }
     }
   }
   if (!part) return;
-  // the two half-warps own the same columns; then warps combine in fixed order
-  if (LPR == 16) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k)
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[k][i] += __shfl_xor_sync(0xffffffffu, acc[k][i], 16);
+  __syncthreads();
+  // slots summed in a fixed order (deterministic)
+  for (int c = threadIdx.x; c < NS * D; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < RPB; ++k) t += accS[(size_t)k * NS * D + c];
+    part[(long)blockIdx.x * NS * D + c] = t;
   }
-  for (int k8 = 0; k8 < 8; ++k8) {
-    if (w == k8 && lane < LPR) {
-#pragma unroll
-      for (int k = 0; k < NS; ++k)
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) red[k][c0 + i] = (k8 == 0 ? 0.f : red[k][c0 + i]) + acc[k][i];
-    }
-    __syncthreads();
+}
+template <int EPL, int NS, int LPR>
+static void launch_ln_bwd_v(int nblk, cudaStream_t s, int M, const __nv_bfloat16* dy, long lddy,
+                            const __nv_bfloat16* x, long ldx, const float* mean,
+                            const float* rstd, const float* g, const __nv_bfloat16* dres,
+                            long ldres, __nv_bfloat16* dx, long lddx, float* part) {
+  constexpr int smem = (8 * (32 / LPR) * NS + 1) * LPR * EPL * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ln_bwd_vkernel<EPL, NS, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    attr = true;
   }
-  for (int c = threadIdx.x; c < NS * D; c += blockDim.x)
-    part[(long)blockIdx.x * NS * D + c] = (&red[0][0])[c];
+  launch_k(ln_bwd_vkernel<EPL, NS, LPR>, nblk, 256, smem, s, M, dy, lddy, x, ldx, mean, rstd, g,
+           dres, ldres, dx, lddx, part);
 }
 
 // ---------------------------------------------------------------------------
@@ -428,7 +466,7 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
     using B16 = __nv_bfloat16;
     const B16 *dyb = (const B16*)dy, *xb = (const B16*)x, *rb = (const B16*)dres;
     B16* dxb = (B16*)dx;
-#define LNB(E, NSV, L) launch_k(ln_bwd_vkernel<E, NSV, L>, nblk, 256, 0, s, M, dyb, lddy, xb, ldx, mean, rstd, g, rb, ldres, dxb, lddx, part)
+#define LNB(E, NSV, L) launch_ln_bwd_v<E, NSV, L>(nblk, s, M, dyb, lddy, xb, ldx, mean, rstd, g, rb, ldres, dxb, lddx, part)
 #define LNB_ALL(NSV)                          \
     switch (D) {                              \
       case 128: LNB(8, NSV, 16); break;       \
