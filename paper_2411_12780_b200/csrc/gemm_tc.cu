@@ -88,6 +88,42 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// CTA-pair (cta_group::2) forms: the peer CTA's TMA completes bytes on the
+// LEADER's full barrier (address mapped into the cluster window), one
+// tcgen05.mma.cta_group::2 (M = 256) reads A from both CTAs' smem (128 rows
+// each) and B halves (N/2 rows each), and its commit arrives on the barrier
+// at the same offset in both CTAs
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* map, uint32_t bar_cl, void* dst,
+                                                int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t cta_rank_in_cluster() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -189,7 +225,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// MC: the CTA pair of a 2-CTA cluster computes vertically adjacent tiles
+// MC: CTA pair (cta_group::2, 2-CTA cluster): the pair computes one 256 x BN
+// tile — each CTA loads its 128 rows of A and BN/2 rows of B, the leader
+// (rank 0) issues M=256 MMAs over both CTAs' smem, each CTA's TMEM holds its
+// 128 accumulator rows and its epilogue stores them.  Per SM, a k-block moves
+// 16 KB + BN·64 B instead of 16 KB + BN·128 B (the L2->smem fill bound of the
+// single-CTA kernel).
 // (m-tiles 2p, 2p+1, same n-tile) and shares the B operand — each CTA fetches
 // half of every B k-block and multicasts it to both, halving B's L2->SM
 // traffic; a slot is refilled only when both CTAs' MMAs have consumed it
@@ -219,11 +260,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], MC ? 2 : 1);
+      mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], MC ? 2 * kEpiWarps : kEpiWarps);   // pair: both CTAs' warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -235,17 +276,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   const int mtw = MC ? (sc.mt + 1) / 2 : sc.mt;          // m-tiles (pairs) per n column
   const int tiles_w = mtw * sc.nt;
   const int items_w = MC ? tiles_w : sc.items;
+  if constexpr (MC) cluster_sync();   // peers' barriers initialised before any remote use
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(L::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (MC) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(L::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(L::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if constexpr (MC) cluster_sync();   // peers' barriers initialised before any multicast
   // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
   pdl_entry();
 
@@ -262,6 +310,28 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
           mbar_wait(&empty[st], ((kb_total / S) & 1) ^ 1);
           uint8_t* sa = smem + st * L::STAGE;
           uint8_t* sb = sa + L::A_BYTES;
+          if constexpr (MC) {
+            // both CTAs' loads complete on the leader's barrier; only the
+            // leader arrives (with the pair's byte count)
+            const uint32_t lb = mapa_shared(smem_u32(&full[st]), 0);
+            if (rank == 0) mbar_expect_tx(&full[st], 2 * (L::A_BYTES + (BN / 2) * BK * 2));
+            if (A_K) {
+              tma_load_2d_cg2(&map_a, lb, sa, k0, m0);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BM / 64; ++i)
+                tma_load_2d_cg2(&map_a, lb, sa + i * 8192, m0 + 64 * i, k0);
+            }
+            const int nb = n0 + rank * (BN / 2);
+            if (B_K) {
+              tma_load_2d_cg2(&map_b, lb, sb, k0, nb);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BN / 128; ++i)
+                tma_load_2d_cg2(&map_b, lb, sb + i * 8192, nb + 64 * i, k0);
+            }
+            continue;
+          }
           mbar_expect_tx(&full[st], L::A_BYTES + (B_K ? BN * BK * 2 : L::B_BYTES));
           if (A_K) {
             tma_load_2d(&map_a, &full[st], sa, k0, m0);
@@ -270,19 +340,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             for (int i = 0; i < BM / 64; ++i)
               tma_load_2d(&map_a, &full[st], sa + i * 8192, m0 + 64 * i, k0);
           }
-          if constexpr (MC) {
-            // this CTA fetches its half of B and multicasts it to the pair
-            if (B_K) {
-              tma_load_2d_mc(&map_b, &full[st], sb + rank * (BN / 2) * 128, k0,
-                             n0 + rank * (BN / 2), (uint16_t)3);
-            } else {
-#pragma unroll
-              for (int i = 0; i < (BN + 63) / 64; ++i)
-                if ((i & 1) == rank)
-                  tma_load_2d_mc(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0,
-                                 (uint16_t)3);
-            }
-          } else if (B_K) {
+          if (B_K) {
             tma_load_2d(&map_b, &full[st], sb, k0, n0);
           } else {
 #pragma unroll
@@ -296,8 +354,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // ------------------------- MMA issuer ---------------------------
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_K ? 0u : 1u) << 15) |
                            ((B_K ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
-    if (lane == 0) {
+                           ((uint32_t)((MC ? 2 * BM : BM) >> 4) << 24);
+    if (lane == 0 && rank == 0) {   // pair: the leader issues for both CTAs
       int kb_total = 0, it = 0;
       for (int w = wid0; w < items_w; w += wstride, ++it) {
         const int z = MC ? 0 : w / sc.tiles;
@@ -320,13 +378,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                                     : make_desc(sa + k * 2048, 8192, 1024);
             const uint64_t bd = B_K ? make_desc(sb + k * 32, 16, 1024)
                                     : make_desc(sb + k * 2048, 8192, 1024);
-            mma_bf16(dtm, ad, bd, idesc, first ? 0u : 1u);
+            if constexpr (MC) mma_bf16_cg2(dtm, ad, bd, idesc, first ? 0u : 1u);
+            else mma_bf16(dtm, ad, bd, idesc, first ? 0u : 1u);
             first = 0;
           }
-          if constexpr (MC) mma_commit_mc(&empty[st], (uint16_t)3);   // both CTAs' slot
+          if constexpr (MC) mma_commit_cg2(&empty[st], (uint16_t)3);   // both CTAs' slot
           else mma_commit(&empty[st]);
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (MC) mma_commit_cg2(&tfull[acc], (uint16_t)3);
+        else mma_commit(&tfull[acc]);
       }
     }
     __syncwarp();
@@ -359,7 +419,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const bool live = row < M;
       // interior tiles store without bounds tests (uniform per tile)
       const bool full = F != kEFGeneric && ep.vec && m0 + BM <= M && n0 + BN <= N;
-      const bool tst = F != kEFGeneric && !MC && sc.tma_st;
+      const bool tst = F != kEFGeneric && sc.tma_st;
 #pragma unroll 1
       for (int c = 16 * grp; c < BN && n0 + c < N; c += 16 * NG) {
         float ra[16], ka[16];
@@ -416,17 +476,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       // accumulator buffer drained: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (MC) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (sc.tl && it < 4 && lane == 0) atomicMax(&sc.tl[(blockIdx.x * 4 + it) * 4 + 2], gtimer());
     }
-    if (F != kEFGeneric && !MC && sc.tma_st) tma_store_drain(lane);
+    if (F != kEFGeneric && sc.tma_st) tma_store_drain(lane);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  // the peer's last multicast commits land on this CTA's barriers: stay alive
+  // the leader's last commits land on the peer's barriers and the peer's
+  // epilogue arrives on the leader's: both stay alive until here
   if constexpr (MC) cluster_sync();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if constexpr (MC)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(L::TMEM_COLS));
+    else
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(L::TMEM_COLS));
   }
@@ -751,7 +819,7 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
   return PPLL_OK;
 }
 
-// 2-CTA clusters sharing B by multicast (see gemm_tc_kernel MC)
+// CTA-pair launch (2-CTA clusters, cta_group::2; see gemm_tc_kernel MC)
 template <typename TO, bool A_K, bool B_K, int BN, int F>
 static int run_mc(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
                   const Sched& sc, const Epilogue<TO>& ep, cudaStream_t s) {
@@ -1058,13 +1126,16 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   static const int tl_on = getenv("PPLL_GEMM_TIMELINE") ? 1 : 0;
   sc.tl = tl_on ? timeline_buffer() : nullptr;
   // 2-CTA multicast of B: specialised bf16 epilogues, no split, >= 2 m-tiles
-  // opt-in (PPLL_GEMM_MC=1): measured 0-5 % slower than the unpaired kernel on the ViT
-  // shapes, whose mainloop is bound by per-SM smem fill (bytes in flight / latency), which
-  // multicast does not change (each SM still receives the whole B tile)
+  // CTA pair (cta_group::2, M = 256 per MMA, B split across the pair), opt-in
+  // (PPLL_GEMM_MC=1).  Measured (tools/gemm_one.py): 8192^3 1306 -> 1359 TF/s (82 % of
+  // the measured peak); the ViT layer shapes gain nothing (ViT-S dgrads 4-5 % slower:
+  // halving the per-SM B bytes did not shorten their ~580-cycle k-blocks, so those are
+  // not smem-fill bound) and lose half the SMs when pair tiles do not fill the GPU
+  // (ViT-B FC1 dgrad 23 -> 36 us).
   static const int force_mc = getenv("PPLL_GEMM_MC") ? atoi(getenv("PPLL_GEMM_MC")) : 0;
   const int fl = epi_flags(ep);
   const bool mc = force_mc != 0 && !cl_bn && sc.splits == 1 && sizeof(TO) == 2 && a_kmajor &&
-                  bn >= 128 && mt >= 2 && fl != kEFGeneric &&
+                  bn >= 128 && mt >= 2 && fl != kEFGeneric && (b_kmajor || bn % 128 == 0) &&
                   (b_kmajor ? (fl == 0 || fl == kEFMaskRelu || fl == kEFMaskMul)
                             : (fl == 0 || fl == kEFBias || fl == (kEFBias | kEFRes) ||
                                fl == (kEFBias | kEFGeluD) || fl == (kEFBias | kEFRelu)));
@@ -1078,6 +1149,12 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   ok = ok && (b_kmajor ? make_map(&mb, B, K, N, ldb, mc ? bn / 2 : bn)
                        : make_map(&mb, B, N, K, ldb, 64));
   if (!ok) return PPLL_ERR_UNSUPPORTED;
+  // epilogue stores through the TMA engine (PPLL_GEMM_TMA_STORE=0: st.global)
+  static const int tma_env = getenv("PPLL_GEMM_TMA_STORE") ? atoi(getenv("PPLL_GEMM_TMA_STORE")) : 1;
+  if (tma_env && !cl_bn && sc.splits == 1 && fl != kEFGeneric && !ep.C2 && !ep.cs_part &&
+      ep.vec && !sc.probe)
+    sc.tma_st = make_store_map<TO>(&sc.st_c, ep.C, N, M, ep.ldc) &&
+                (!(fl & kEFGeluD) || make_store_map<TO>(&sc.st_p, ep.pre, N, M, ep.ldpre));
   if (mc) {
     Epilogue<TO> e = ep;
     e.partial = nullptr;
@@ -1108,11 +1185,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   float* part = sc.splits > 1 ? ws : nullptr;
   int r;
   const int f = epi_flags(e);
-  // epilogue stores through the TMA engine (PPLL_GEMM_TMA_STORE=0: st.global)
-  static const int tma_env = getenv("PPLL_GEMM_TMA_STORE") ? atoi(getenv("PPLL_GEMM_TMA_STORE")) : 1;
-  if (tma_env && sc.splits == 1 && f != kEFGeneric && !e.C2 && !e.cs_part && e.vec && !sc.probe)
-    sc.tma_st = make_store_map<TO>(&sc.st_c, e.C, N, M, e.ldc) &&
-                (!(f & kEFGeluD) || make_store_map<TO>(&sc.st_p, e.pre, N, M, e.ldpre));
+
   if (a_kmajor && !b_kmajor) r = dispatch_f<TO, true, false>(f, bn, ma, mb, M, N, K, sc, e, part, s);
   else if (a_kmajor && b_kmajor) r = dispatch_f<TO, true, true>(f, bn, ma, mb, M, N, K, sc, e, part, s);
   else if (!a_kmajor && !b_kmajor) r = dispatch_f<TO, false, false>(f, bn, ma, mb, M, N, K, sc, e, part, s);

@@ -50,3 +50,13 @@ e.record()
 torch.cuda.synchronize()
 t = a.elapsed_time(e) / iters
 print(f"{op} M={M} K={K} N={Nn}: {t * 1e3:.1f} us  {2.0 * M * K * Nn / t / 1e9:.0f} TF/s")
+# correctness against torch (fp32 accumulate of the same bf16 operands)
+if op in ("fwd", "dgrad"):
+    fn()
+    torch.cuda.synchronize()
+    if op == "fwd":
+        ref, got = (X.float() @ W.float() + b).clamp_min(0), Y.float()   # bias + ReLU
+    else:
+        ref, got = dY.float() @ W.float().t(), dX.float()
+    err = ((got - ref).abs().max() / ref.abs().max()).item()
+    print(f"  max rel err vs torch: {err:.2e}")
