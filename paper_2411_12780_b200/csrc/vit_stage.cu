@@ -56,6 +56,11 @@ struct ppll_vit_stage {
   float* attn_bpart = nullptr;
   float* ws = nullptr;
   size_t ws_elems = 0;
+  // weight gradients run on a side stream (off the dgrad critical path), with
+  // their own split-K workspace; events fork/join it to the step's stream
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  float* ws2 = nullptr;
   std::vector<void*> allocs;
 
   int layers() const { return n_block + n_aux; }
@@ -181,11 +186,38 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
                   st->ws, st->ws_elems, s);
 }
 
+// Fork/join of the side stream inside one stage step (capturable: a CUDA
+// graph records the event edges).  Without a side stream everything stays on
+// the step's stream and the calls are no-ops.
+struct SideFlow {
+  cudaStream_t s, ss;
+  cudaEvent_t* ev;
+  int n = 0, cap;
+  bool on() const { return ss != s; }
+  void fork() {            // side work after everything enqueued on s so far
+    if (!on() || n >= cap) return;
+    cudaEventRecord(ev[n], s);
+    cudaStreamWaitEvent(ss, ev[n++], 0);
+  }
+  cudaEvent_t mark() {     // completion of the side work enqueued so far
+    if (!on() || n >= cap) return nullptr;
+    cudaEventRecord(ev[n], ss);
+    return ev[n++];
+  }
+  void join(cudaEvent_t e) {
+    if (e) cudaStreamWaitEvent(s, e, 0);
+  }
+};
+
 template <typename TT>
 static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
                     void* x_out, cudaStream_t s) {
   const int T = st->T, D = st->D, F = st->F, H = st->H, C = st->C;
   const int M = B * T;
+  static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
+  SideFlow sf{s, (side_on && st->side) ? st->side : s, st->ev.data(), 0, (int)st->ev.size()};
+  const cudaStream_t ss = sf.ss;
+  float* wsw = sf.on() ? st->ws2 : st->ws;   // the weight gradients' workspace
   int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
   if (r) return r;
   r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
@@ -193,8 +225,9 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   if (r) return r;
   const TT* xlast = (const TT*)st->L[st->layers() - 1].x2;
   // ---- head backward ----
+  sf.fork();
   r = linear_wgrad(B, D, C, st->zc, D, st->dlog, C, st->G(st->ho(2)), st->G(st->ho(3)), st->dtype,
-                   st->ws, st->ws_elems, s);
+                   wsw, st->ws_elems, ss);
   if (r) return r;
   LinOpts none;
   r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
@@ -210,6 +243,9 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   char* dx2 = st->dxa;   // gradient w.r.t. the current layer's output
   char* dx1 = st->dxb;
   char* dxn_out = st->dxc;
+  // side-stream completion of the previous (higher) layer's weight gradients:
+  // the main stream waits on them before overwriting the buffers they read
+  cudaEvent_t e_w2 = nullptr, e_w1 = nullptr, e_wo = nullptr, e_wqkv = nullptr;
   for (int l = st->layers() - 1; l >= 0; --l) {
     LayerBufs& b = st->L[l];
     const void* xin_l = l > 0 ? (const void*)st->L[l - 1].x2
@@ -223,9 +259,12 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
                             st->ws_elems);
       if (r) return r;
     }
-    r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, st->ws,
-                     st->ws_elems, s);
+    sf.fork();
+    r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, wsw,
+                     st->ws_elems, ss);
     if (r) return r;
+    const cudaEvent_t n_w2 = sf.mark();
+    sf.join(e_w1);   // dbig is still read by the layer above's W1 gradient
     LinOpts og;
     og.mask = b.u;
     og.ldmask = F;
@@ -234,31 +273,39 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
                    st->ws_elems, s);
     if (r) return r;
     // db1 = Σ rows dU: summed from the dU tiles in smem by the cluster wgrad
+    sf.fork();
     r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
-                     st->dtype, st->ws, st->ws_elems, s);
+                     st->dtype, wsw, st->ws_elems, ss);
     if (r) return r;
+    e_w1 = sf.mark();
     r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
                    st->ws, st->ws_elems, s);
     if (r) return r;
     // LN2 backward (+ residual) -> dx1, with dbo = Σ rows dx1 fused
+    sf.join(e_wo);   // dx1 is still read by the layer above's Wo gradient
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
                           st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, st->ln_part,
                           st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s,
                           st->G(st->po(l, kBo)));
     if (r) return r;
-    r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, st->ws,
-                     st->ws_elems, s);
+    sf.fork();
+    r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, wsw,
+                     st->ws_elems, ss);
     if (r) return r;
+    e_wo = sf.mark();
     r = gemm_dgrad(M, D, D, dx1, D, st->W(st->po(l, kWo)), none, st->dO, D, st->dtype, st->ws,
                    st->ws_elems, s);
     if (r) return r;
+    sf.join(e_wqkv);   // dqkv is still read by the layer above's Wqkv gradient
     r = attn_bwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
                          b.lse, (TT*)st->dqkv, st->G(st->po(l, kBqkv)), st->attn_bpart, st->ws,
                          st->ws_elems, s);
     if (r) return r;
+    sf.fork();
     r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)), nullptr,
-                     st->dtype, st->ws, st->ws_elems, s);
+                     st->dtype, wsw, st->ws_elems, ss);
     if (r) return r;
+    e_wqkv = sf.mark();
     r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
                    st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
@@ -266,6 +313,8 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     // into the detached stage input (blocks.py:277-278).  Its row sum is the
     // bias gradient db2 of the layer below (fused).
     const bool need_dx = l > 0 || st->has_patch;
+    sf.join(e_w2);   // dxn_out was the layer above's dx2, read by its W2 gradient
+    e_w2 = n_w2;
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
                           st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
                           need_dx ? (TT*)dxn_out : nullptr, D, st->ln_part,
@@ -285,6 +334,8 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
                      st->G(st->off[1]), st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
   }
+  // every weight gradient has landed before the optimizer reads them
+  sf.join(sf.mark());
   return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
                          st->max_step, 0.f, st->mu, st->wd, st->err, s);
@@ -350,6 +401,15 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
   // split-K workspace: 16 partial copies of the largest weight gradient
   st->ws_elems = 16 * (size_t)D * (F > 3 * D ? F : 3 * D);
   st->ws = (float*)A(st->ws_elems * 4);
+  st->ws2 = (float*)A(st->ws_elems * 4);
+  if (cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) != cudaSuccess) {
+    st->side = nullptr;
+    cudaGetLastError();
+  } else {
+    st->ev.resize(8 * (size_t)st->layers() + 8);
+    for (auto& e : st->ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  }
   if (!ok) {
     set_error("ppll_vit_stage_create: out of device memory");
     ppll_vit_stage_destroy(st);
@@ -360,6 +420,9 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
 
 void ppll_vit_stage_destroy(ppll_vit_stage* st) {
   if (!st) return;
+  for (cudaEvent_t e : st->ev)
+    if (e) cudaEventDestroy(e);
+  if (st->side) cudaStreamDestroy(st->side);
   for (void* p : st->allocs) cudaFree(p);
   delete st;
 }
