@@ -96,3 +96,39 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 }
 
 }  // namespace ppll
+
+namespace ppll {
+// Fork/join of a stage step's side stream (capturable: a CUDA graph records
+// the event edges).  Without a side stream everything stays on the step's
+// stream and the calls are no-ops.  The last event is reserved: if a step
+// ever needs more events than the pool holds, the side work is joined and the
+// rest of the step runs on the main stream (always correct, just serial).
+struct SideFlow {
+  cudaStream_t s, ss;
+  cudaEvent_t* ev;
+  int n = 0, cap;
+  bool on() const { return ss != s; }
+  bool reserve() {
+    if (n < cap - 1) return true;
+    if (on()) {
+      cudaEventRecord(ev[cap - 1], ss);
+      cudaStreamWaitEvent(s, ev[cap - 1], 0);
+      ss = s;
+    }
+    return false;
+  }
+  void fork() {            // side work after everything enqueued on s so far
+    if (!on() || !reserve()) return;
+    cudaEventRecord(ev[n], s);
+    cudaStreamWaitEvent(ss, ev[n++], 0);
+  }
+  cudaEvent_t mark() {     // completion of the side work enqueued so far
+    if (!on() || !reserve()) return nullptr;
+    cudaEventRecord(ev[n], ss);
+    return ev[n++];
+  }
+  void join(cudaEvent_t e) {
+    if (e) cudaStreamWaitEvent(s, e, 0);
+  }
+};
+}  // namespace ppll

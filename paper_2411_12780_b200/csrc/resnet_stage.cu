@@ -69,6 +69,13 @@ struct ppll_resnet_stage {
   float* bn_part = nullptr;
   float* ws = nullptr;
   size_t ws_elems = 0;
+  // weight gradients (im2col + GEMM) on a side stream; the BN-backward output
+  // dz is double-buffered so the next conv's BN backward need not wait for
+  // the previous conv's weight gradient
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  float* ws2 = nullptr;
+  char* dz2 = nullptr;
   std::vector<void*> allocs;
 
   char* alloc(size_t bytes) {
@@ -142,22 +149,38 @@ static int conv_bn_fwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* x, i
 // given dy (gradient w.r.t. the BN output, ReLU already applied): BN backward,
 // weight gradient, and (if dx) the input gradient (+dres, ⊙mask): the
 // transposed implicit convolution, or col2im(dZ·Wᵀ)
+// side-stream state of one backward pass: convs alternate between the two dz
+// buffers; dz_done[i] = completion of the weight gradient that last read dz[i]
+struct BwdSide {
+  SideFlow sf;
+  char* dz[2];
+  cudaEvent_t dz_done[2] = {nullptr, nullptr};
+  int k = 0;
+  float* wsw;
+};
+
 template <typename TT>
 static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, int64_t w_off,
                        int64_t g_off, int64_t b_off, void* dx, const void* dres,
-                       const void* mask, cudaStream_t s) {
+                       const void* mask, cudaStream_t s, BwdSide& bs) {
   const int P = B * c.h_out * c.h_out;
+  const int slot = bs.k++ & 1;
+  char* dz = bs.dz[slot];
+  bs.sf.join(bs.dz_done[slot]);   // the weight gradient two convs back read this buffer
   int r = launch_bn_bwd<TT>(P, c.cout, (const TT*)dy, (const TT*)c.z, c.mean, c.rstd,
-                            st->P(g_off), st->bn_part, st->G(g_off), st->G(b_off), (TT*)st->dz, s);
+                            st->P(g_off), st->bn_part, st->G(g_off), st->G(b_off), (TT*)dz, s);
   if (r) return r;
+  bs.sf.fork();
   if (c.implicit) {   // the weight gradient still contracts over the im2col'd input
     r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)c.x_in,
-                          (TT*)c.col, s);
+                          (TT*)c.col, bs.sf.ss);
     if (r) return r;
   }
-  r = linear_wgrad(P, c.kp, c.cout, c.col, c.kp, st->dz, c.cout, st->G(w_off), nullptr,
-                   st->dtype, st->ws, st->ws_elems, s);
-  if (r || !dx) return r;
+  r = linear_wgrad(P, c.kp, c.cout, c.col, c.kp, dz, c.cout, st->G(w_off), nullptr,
+                   st->dtype, bs.wsw, st->ws_elems, bs.sf.ss);
+  if (r) return r;
+  bs.dz_done[slot] = bs.sf.mark();
+  if (!dx) return r;
   if (c.implicit) {
     Epilogue<__nv_bfloat16> e;
     e.C = (__nv_bfloat16*)dx;
@@ -168,12 +191,12 @@ static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, 
     e.ldmask = c.cin;
     e.mask_mode = mask ? kMaskRelu : kMaskNone;
     epilogue_finalize(e, c.cin);
-    r = launch_conv3x3_tc(B, c.h_out, c.h_out, c.cout, c.cin, (const __nv_bfloat16*)st->dz,
+    r = launch_conv3x3_tc(B, c.h_out, c.h_out, c.cout, c.cin, (const __nv_bfloat16*)dz,
                           (const __nv_bfloat16*)st->W(w_off), true, e, s);
     if (r != PPLL_ERR_UNSUPPORTED) return r;
   }
   LinOpts none;
-  r = gemm_dgrad(P, c.kp, c.cout, st->dz, c.cout, st->W(w_off), none, st->dcol, c.kp, st->dtype,
+  r = gemm_dgrad(P, c.kp, c.cout, dz, c.cout, st->W(w_off), none, st->dcol, c.kp, st->dtype,
                  st->ws, st->ws_elems, s);
   if (r) return r;
   return launch_col2im<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)st->dcol,
@@ -251,9 +274,15 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
   r = launch_softmax_xent<TT>(B, st->classes, (const TT*)st->logits, st->classes, labels,
                               (TT*)st->dlog, st->classes, st->loss_hist, st->step, st->err, s);
   if (r) return r;
+  static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
+  const bool side = side_on && st->side && st->dz2;
+  BwdSide bs{SideFlow{s, side ? st->side : s, st->ev.data(), 0, (int)st->ev.size()},
+             {st->dz, side ? st->dz2 : st->dz}};
+  bs.wsw = side ? st->ws2 : st->ws;
   // head
+  bs.sf.fork();
   r = linear_wgrad(B, C, st->classes, st->pooled, C, st->dlog, st->classes, st->G(st->head_off[0]),
-                   st->G(st->head_off[1]), st->dtype, st->ws, st->ws_elems, s);
+                   st->G(st->head_off[1]), st->dtype, bs.wsw, st->ws_elems, bs.sf.ss);
   if (r) return r;
   LinOpts none;
   r = gemm_dgrad(B, C, st->classes, st->dlog, st->classes, st->W(st->head_off[0]), none, st->dp,
@@ -269,7 +298,7 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
     r = launch_relu_mask<TT>((long)B * HW * C, (const TT*)dx, (const TT*)a.out, (TT*)st->dy, s);
     if (r) return r;
     r = conv_bn_bwd<TT>(st, a.c, B, st->dy, a.off[0], a.off[1], a.off[2], dx_next, nullptr, nullptr,
-                        s);
+                        s, bs);
     if (r) return r;
     char* t = dx; dx = dx_next; dx_next = t;
   }
@@ -282,12 +311,12 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
     if (r) return r;
     // conv2: input gradient masked by the ReLU that produced a1 -> dy
     r = conv_bn_bwd<TT>(st, b.c2, B, st->dsum, b.off[3], b.off[4], b.off[5], st->dy, nullptr, b.a1,
-                        s);
+                        s, bs);
     if (r) return r;
     const void* dres = nullptr;
     if (b.has_sc) {
       r = conv_bn_bwd<TT>(st, b.sc, B, st->dsum, b.off[6], b.off[7], b.off[8],
-                          need_dx ? st->dtmp : nullptr, nullptr, nullptr, s);
+                          need_dx ? st->dtmp : nullptr, nullptr, nullptr, s, bs);
       if (r) return r;
       dres = st->dtmp;
     } else {
@@ -295,7 +324,7 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
     }
     // conv1 (+ shortcut / identity gradient) -> gradient of the block input
     r = conv_bn_bwd<TT>(st, b.c1, B, st->dy, b.off[0], b.off[1], b.off[2],
-                        need_dx ? dx_next : nullptr, dres, nullptr, s);
+                        need_dx ? dx_next : nullptr, dres, nullptr, s, bs);
     if (r) return r;
     char* t = dx; dx = dx_next; dx_next = t;
   }
@@ -305,9 +334,10 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
     r = launch_relu_mask<TT>(P * c.cout, (const TT*)dx, (const TT*)st->stem_out, (TT*)st->dy, s);
     if (r) return r;
     r = conv_bn_bwd<TT>(st, c, B, st->dy, st->stem_off[0], st->stem_off[1], st->stem_off[2],
-                        nullptr, nullptr, nullptr, s);
+                        nullptr, nullptr, nullptr, s, bs);
     if (r) return r;
   }
+  bs.sf.join(bs.sf.mark());   // every weight gradient has landed
   return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
                          st->max_step, 0.f, st->mu, st->wd, st->err, s);
@@ -398,6 +428,19 @@ ppll_resnet_stage* ppll_resnet_stage_create(const int* cfg, const int* geo, cons
   st->ws = (float*)st->alloc(st->ws_elems * 4);
   ok = ok && st->pooled && st->logits && st->dlog && st->dp && st->dsum && st->dz && st->dy &&
        st->dxa && st->dxb && st->dtmp && st->dcol && st->bn_part && st->ws;
+  st->ws2 = (float*)st->alloc(st->ws_elems * 4);
+  st->dz2 = st->alloc(maxPC * e);
+  ok = ok && st->ws2 && st->dz2;
+  if (ok && cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) == cudaSuccess) {
+    int convs = 2 + (st->has_stem ? 1 : 0) + (int)st->aux.size();
+    for (const Block& b : st->blocks) convs += b.has_sc ? 3 : 2;
+    st->ev.resize(2 * (size_t)convs + 8);
+    for (auto& ev : st->ev)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  } else {
+    st->side = nullptr;
+    cudaGetLastError();
+  }
   if (!ok) {
     set_error("ppll_resnet_stage_create: out of device memory");
     ppll_resnet_stage_destroy(st);
@@ -408,6 +451,9 @@ ppll_resnet_stage* ppll_resnet_stage_create(const int* cfg, const int* geo, cons
 
 void ppll_resnet_stage_destroy(ppll_resnet_stage* st) {
   if (!st) return;
+  for (cudaEvent_t ev : st->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (st->side) cudaStreamDestroy(st->side);
   for (void* p : st->allocs) cudaFree(p);
   delete st;
 }

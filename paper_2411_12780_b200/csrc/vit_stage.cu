@@ -186,29 +186,6 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
                   st->ws, st->ws_elems, s);
 }
 
-// Fork/join of the side stream inside one stage step (capturable: a CUDA
-// graph records the event edges).  Without a side stream everything stays on
-// the step's stream and the calls are no-ops.
-struct SideFlow {
-  cudaStream_t s, ss;
-  cudaEvent_t* ev;
-  int n = 0, cap;
-  bool on() const { return ss != s; }
-  void fork() {            // side work after everything enqueued on s so far
-    if (!on() || n >= cap) return;
-    cudaEventRecord(ev[n], s);
-    cudaStreamWaitEvent(ss, ev[n++], 0);
-  }
-  cudaEvent_t mark() {     // completion of the side work enqueued so far
-    if (!on() || n >= cap) return nullptr;
-    cudaEventRecord(ev[n], ss);
-    return ev[n++];
-  }
-  void join(cudaEvent_t e) {
-    if (e) cudaStreamWaitEvent(s, e, 0);
-  }
-};
-
 template <typename TT>
 static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
                     void* x_out, cudaStream_t s) {
@@ -216,7 +193,6 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   const int M = B * T;
   static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
   SideFlow sf{s, (side_on && st->side) ? st->side : s, st->ev.data(), 0, (int)st->ev.size()};
-  const cudaStream_t ss = sf.ss;
   float* wsw = sf.on() ? st->ws2 : st->ws;   // the weight gradients' workspace
   int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
   if (r) return r;
@@ -227,7 +203,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   // ---- head backward ----
   sf.fork();
   r = linear_wgrad(B, D, C, st->zc, D, st->dlog, C, st->G(st->ho(2)), st->G(st->ho(3)), st->dtype,
-                   wsw, st->ws_elems, ss);
+                   wsw, st->ws_elems, sf.ss);
   if (r) return r;
   LinOpts none;
   r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
@@ -261,7 +237,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     }
     sf.fork();
     r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, wsw,
-                     st->ws_elems, ss);
+                     st->ws_elems, sf.ss);
     if (r) return r;
     const cudaEvent_t n_w2 = sf.mark();
     sf.join(e_w1);   // dbig is still read by the layer above's W1 gradient
@@ -275,7 +251,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     // db1 = Σ rows dU: summed from the dU tiles in smem by the cluster wgrad
     sf.fork();
     r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
-                     st->dtype, wsw, st->ws_elems, ss);
+                     st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_w1 = sf.mark();
     r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
@@ -290,7 +266,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     if (r) return r;
     sf.fork();
     r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, wsw,
-                     st->ws_elems, ss);
+                     st->ws_elems, sf.ss);
     if (r) return r;
     e_wo = sf.mark();
     r = gemm_dgrad(M, D, D, dx1, D, st->W(st->po(l, kWo)), none, st->dO, D, st->dtype, st->ws,
@@ -303,7 +279,7 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     if (r) return r;
     sf.fork();
     r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)), nullptr,
-                     st->dtype, wsw, st->ws_elems, ss);
+                     st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_wqkv = sf.mark();
     r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
