@@ -33,8 +33,13 @@ struct ppll_stage {
   std::vector<size_t> act_off;   // bytes
   char* g0 = nullptr;
   char* g1 = nullptr;
+  char* g2 = nullptr;             // third gradient buffer (side-stream weight gradients)
   float* ws = nullptr;
   size_t ws_elems = 0;
+  // weight gradients on a side stream, each layer's concurrent with its dgrad
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  float* ws2 = nullptr;
   size_t esz = 4;
 
   void* act_ptr(int i) const { return act + act_off[i]; }
@@ -109,6 +114,18 @@ ppll_stage* ppll_stage_create(int n_layers, int n_block, const int* in_w, const 
   }
   // split-K tickets live at the end of the workspace and must start at zero
   cudaMemset(st->ws, 0, st->ws_elems * sizeof(float));
+  if (cudaMalloc(&st->g2, gbytes) == cudaSuccess &&
+      cudaMalloc(&st->ws2, st->ws_elems * sizeof(float)) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) == cudaSuccess) {
+    cudaMemset(st->ws2, 0, st->ws_elems * sizeof(float));
+    st->ev.resize(2 * (size_t)n_layers + 4);
+    for (auto& e : st->ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr;
+    for (auto e : st->ev)
+      if (!e) { st->ev.clear(); break; }
+  }
+  cudaGetLastError();
+  if (st->ev.empty() && st->side) { cudaStreamDestroy(st->side); st->side = nullptr; }
   return st;
 }
 
@@ -117,7 +134,12 @@ void ppll_stage_destroy(ppll_stage* st) {
   if (st->act) cudaFree(st->act);
   if (st->g0) cudaFree(st->g0);
   if (st->g1) cudaFree(st->g1);
+  if (st->g2) cudaFree(st->g2);
   if (st->ws) cudaFree(st->ws);
+  if (st->ws2) cudaFree(st->ws2);
+  for (cudaEvent_t e : st->ev)
+    if (e) cudaEventDestroy(e);
+  if (st->side) cudaStreamDestroy(st->side);
   delete st;
 }
 
@@ -154,23 +176,35 @@ int ppll_stage_step(ppll_stage* st, int B, const void* x_in, const int64_t* labe
                                            (__nv_bfloat16*)st->g0, C, st->loss_hist, st->step,
                                            st->err, s);
   if (r) return r;
-  // 3. backward, last layer first; no dX for the detached block input
-  char* G = st->g0;
-  char* Gn = st->g1;
+  // 3. backward, last layer first; no dX for the detached block input.  The
+  // weight gradient of layer i runs on the side stream beside its dgrad; the
+  // layer gradients rotate over three buffers, and a dgrad waits for the
+  // weight gradient that last read the buffer it overwrites.
+  static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
+  const bool side = side_on && st->side && st->g2;
+  SideFlow sf{s, side ? st->side : s, st->ev.data(), 0, (int)st->ev.size()};
+  char* buf[3] = {st->g0, st->g1, side ? st->g2 : st->g0};
+  cudaEvent_t read_done[3] = {nullptr, nullptr, nullptr};
+  int cur = 0;
   for (int i = L; i >= 0; --i) {
     const void* in = i == 0 ? x_in : st->act_ptr(i - 1);
-    r = linear_wgrad(B, st->in_w[i], st->out_w[i], in, st->in_w[i], G, st->out_w[i],
-                     st->grad + st->off[2 * i], st->grad + st->off[2 * i + 1], st->dtype, st->ws,
-                     st->ws_elems, s);
+    sf.fork();
+    r = linear_wgrad(B, st->in_w[i], st->out_w[i], in, st->in_w[i], buf[cur], st->out_w[i],
+                     st->grad + st->off[2 * i], st->grad + st->off[2 * i + 1], st->dtype,
+                     sf.on() ? st->ws2 : st->ws, st->ws_elems, sf.ss);
     if (r) return r;
+    read_done[cur] = sf.mark();
     if (i > 0) {
+      const int nxt = side ? (cur + 1) % 3 : 1 - cur;
+      sf.join(read_done[nxt]);
       const void* mask = st->relu[i - 1] ? st->act_ptr(i - 1) : nullptr;
-      r = linear_dgrad(B, st->in_w[i], st->out_w[i], G, st->out_w[i], st->w_ptr(i), mask,
-                       st->in_w[i], Gn, st->in_w[i], st->dtype, st->ws, st->ws_elems, s);
+      r = linear_dgrad(B, st->in_w[i], st->out_w[i], buf[cur], st->out_w[i], st->w_ptr(i), mask,
+                       st->in_w[i], buf[nxt], st->in_w[i], st->dtype, st->ws, st->ws_elems, s);
       if (r) return r;
-      char* t = G; G = Gn; Gn = t;
+      cur = nxt;
     }
   }
+  sf.join(sf.mark());   // every weight gradient has landed
   // 4. cosine-LR Nesterov over all stage params (block + aux), one launch
   return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
