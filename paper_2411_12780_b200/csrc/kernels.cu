@@ -127,8 +127,16 @@ gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
 #pragma unroll
   for (int n = 0; n < NP; ++n) acc[n] = 0.f;
   const TI* ar = A + (long)(live ? m : 0) * a_rs;
+  constexpr int kJ = kSkK / 32;
   for (int k0 = 0; k0 < K; k0 += kSkK) {
     const int kc = min(kSkK, K - k0);
+    // the row's A chunk is loaded before the B staging so both latencies overlap
+    float av[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int kk = lane + 32 * j;
+      av[j] = (live && kk < kc) ? to_f(ar[k0 + kk]) : 0.f;
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < kc * NP; i += blockDim.x) {
       const int kk = i / NP, n = i % NP;
@@ -136,11 +144,14 @@ gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
     }
     __syncthreads();
     if (live) {
-      for (int kk = lane; kk < kc; kk += 32) {
-        const float a = to_f(ar[k0 + kk]);
-        const float* br = bs + kk * NP;
 #pragma unroll
-        for (int n = 0; n < NP; ++n) acc[n] = fmaf(a, br[n], acc[n]);
+      for (int j = 0; j < kJ; ++j) {
+        const int kk = lane + 32 * j;
+        if (kk < kc) {
+          const float* br = bs + kk * NP;
+#pragma unroll
+          for (int n = 0; n < NP; ++n) acc[n] = fmaf(av[j], br[n], acc[n]);
+        }
       }
     }
   }
@@ -407,30 +418,41 @@ softmax_xent_kernel(int B, int C, const T* __restrict__ z, int ldz, const int64_
                     T* __restrict__ dz, int lddz, float* loss_hist, const int* step, int* err) {
   pdl_entry();
   extern __shared__ float row_loss[];
+  // a half-warp per row (16 lanes stride the classes): two rows per warp in
+  // flight; every half-warp runs the same trip count so shuffles stay converged
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int sl = lane & 15, seg = lane >> 4;
   const float invB = 1.0f / (float)B;
-  for (int r = w; r < B; r += nw) {
-    const T* zr = z + (long)r * ldz;
-    const long lab = y[r];
+  const int trips = (B + 2 * nw - 1) / (2 * nw);
+  for (int it = 0; it < trips; ++it) {
+    const int r = (it * nw + w) * 2 + seg;
+    const bool live = r < B;
+    const T* zr = z + (long)(live ? r : 0) * ldz;
+    const long lab = live ? y[r] : 0;
     const bool bad = (lab < 0 || lab >= C);
     float mx = -INFINITY;
-    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, to_f(zr[c]));
-    mx = warp_max(mx);
+    for (int c = sl; c < C; c += 16) mx = fmaxf(mx, to_f(zr[c]));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float se = 0.f, zl = 0.f;
-    for (int c = lane; c < C; c += 32) {
+    for (int c = sl; c < C; c += 16) {
       const float v = to_f(zr[c]);
       se += __expf(v - mx);
       if (c == lab) zl = v;
     }
-    se = warp_sum(se);
-    zl = warp_sum(zl);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      se += __shfl_xor_sync(0xffffffffu, se, o);
+      zl += __shfl_xor_sync(0xffffffffu, zl, o);
+    }
+    if (!live) continue;
     const float inv = 1.0f / se;
     T* dr = dz + (long)r * lddz;
-    for (int c = lane; c < C; c += 32) {
+    for (int c = sl; c < C; c += 16) {
       const float p = __expf(to_f(zr[c]) - mx) * inv;
       DT<T>::st(dr + c, bad ? 0.f : (p - (c == lab ? 1.f : 0.f)) * invB);
     }
-    if (lane == 0) {
+    if (sl == 0) {
       row_loss[r] = bad ? 0.f : -((zl - mx) - logf(se));
       if (bad && err) atomicOr(err, kErrLabel);
     }
