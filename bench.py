@@ -333,8 +333,9 @@ def run_sharded(args, wl, rank, world, local, dev):
     idle = met.idle_fraction
     # e2e: host numpy batches through the same sharded pipeline (rank 0 H2D)
     rng = np.random.default_rng(7)
-    host = [(rng.standard_normal((B,) + in_shape).astype(np.float32),
-             rng.integers(0, n_cls, B)) for _ in range(8)]
+    # inputs in pinned host memory (the contract's e2e: H2D from pinned buffers)
+    host = [(torch.from_numpy(rng.standard_normal((B,) + in_shape).astype(np.float32)).pin_memory(),
+             torch.from_numpy(rng.integers(0, n_cls, B)).pin_memory()) for _ in range(8)]
     e2e_steps = max(60, args.steps)
     dist.barrier()
     torch.cuda.synchronize(dev)
@@ -375,7 +376,7 @@ def run_sharded(args, wl, rank, world, local, dev):
             "e2e": {"value": e2e_steps * B / e2e_dt, "unit": "images/s",
                     "h2d_bytes_per_step": B * int(np.prod(in_shape)) * 4 + B * 8,
                     "d2h_bytes_per_step": 4 * s,
-                    "api": "DistributedPipeline.run on host numpy batches (rank 0 H2D)"},
+                    "api": "DistributedPipeline.run on pinned host batches (rank 0 H2D)"},
             "roofline": roof, "cpu_baseline": None,
             "gpu_launches": int(sum(launch_counts)),
             "clocks": clk.summary(),
@@ -744,8 +745,9 @@ def main():
 
     # ---- e2e through the public API: host numpy batches ----
     rng = np.random.default_rng(7 + rank)
-    host = [(rng.standard_normal((B,) + in_shape).astype(np.float32),
-             rng.integers(0, n_cls, B)) for _ in range(8)]
+    # inputs in pinned host memory (the contract's e2e: H2D from pinned buffers)
+    host = [(torch.from_numpy(rng.standard_normal((B,) + in_shape).astype(np.float32)).pin_memory(),
+             torch.from_numpy(rng.integers(0, n_cls, B)).pin_memory()) for _ in range(8)]
     # one untimed epoch first (pipeline staging / graphs are cached per module
     # set), then enough batches that the epoch's fill and drain amortise
     lp.run_epoch(lp.RunMode.PPLL, mods, (host[i % 8] for i in range(2 * wl["s"] + 2)), cfg)
@@ -764,7 +766,7 @@ def main():
     e2e = {"value": e2e_steps * B * world / e2e_dt, "unit": "images/s",
            "h2d_bytes_per_step": B * int(np.prod(in_shape)) * 4 + B * 8,
            "d2h_bytes_per_step": 4 * wl["s"],
-           "api": "paper_2411_12780_b200.run_epoch(RunMode.PPLL, modules, host numpy batches)"}
+           "api": "paper_2411_12780_b200.run_epoch(RunMode.PPLL, modules, pinned host batches)"}
 
     if wl["kind"] == "vit":
         roof = roofline_gemm(wl, tf_burst, hbm, dev)

@@ -498,6 +498,7 @@ class DevicePipeline:
         self.rings = _Rings(self.modules, self.M, self.max_batch)
         self.graphs = {}
         self.ev_h2d = [torch.cuda.Event() for _ in range(self.rings.P)]
+        self.held = [None] * self.rings.P
         self.ev_cast = [torch.cuda.Event() for _ in range(self.rings.P)]
         self.used_stage = [False] * self.rings.P
 
@@ -571,15 +572,28 @@ class DevicePipeline:
                 ps = batch_id % r.P
                 if self.used_stage[ps]:
                     self.ev_h2d[ps].synchronize()        # recycle pinned staging
-                r.x_pin[ps, :B].copy_(xt)
-                r.y_pin[ps, :B].copy_(yt)
+                    self.held[ps] = None
+                # caller-pinned fp32 / int64 tensors are copied straight to the
+                # device (held until the copy completes); anything else goes
+                # through this pipeline's pinned staging slot first
+                x_pinned = (xt.is_pinned() and xt.dtype == torch.float32 and
+                            xt.is_contiguous())
+                y_pinned = (torch.is_tensor(yt) and yt.is_pinned() and
+                            yt.dtype == torch.int64)
+                if not x_pinned:
+                    r.x_pin[ps, :B].copy_(xt)
+                if not y_pinned:
+                    r.y_pin[ps, :B].copy_(yt)
                 h2d = self.h2d_stream
                 with torch.cuda.stream(h2d):
                     if self.used_stage[ps]:
                         h2d.wait_event(self.ev_cast[ps])  # device staging slot consumed
-                    r.x_stage[ps, :B].copy_(r.x_pin[ps, :B], non_blocking=True)
-                    r.y_stage[ps, :B].copy_(r.y_pin[ps, :B], non_blocking=True)
+                    r.x_stage[ps, :B].copy_(xt if x_pinned else r.x_pin[ps, :B],
+                                            non_blocking=True)
+                    r.y_stage[ps, :B].copy_(yt if y_pinned else r.y_pin[ps, :B],
+                                            non_blocking=True)
                     self.ev_h2d[ps].record(h2d)
+                self.held[ps] = (xt, yt) if (x_pinned or y_pinned) else None
                 self.used_stage[ps] = True
                 x_src, y_src = r.x_stage[ps, :B], r.y_stage[ps, :B]
             else:                                        # inputs already in HBM

@@ -557,17 +557,24 @@ def test_run_epoch_device_batches_equal_host_batches(precision):
     ds = _mlp_dataset()
     spec = lp.NetworkSpec((96, 64, 64, 48, 40, 10))
     outs = []
-    for src in ("host", "device"):
+    for src in ("host", "device", "pinned"):
         hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=20, seed=42,
                                precision=precision)
         mods = lp.build_modules(spec, lp.partition(spec, 4), 2, 3, hyper)
-        it = (lp.batches(ds, 64, True, 7) if src == "host"
-              else lp.DeviceDataset(ds).batches(64, True, 7))
+        if src == "host":
+            it = lp.batches(ds, 64, True, 7)
+        elif src == "device":
+            it = lp.DeviceDataset(ds).batches(64, True, 7)
+        else:   # caller-pinned host tensors: copied straight to the device
+            it = [(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).pin_memory(),
+                   torch.from_numpy(np.asarray(y, dtype=np.int64)).pin_memory())
+                  for x, y in lp.batches(ds, 64, True, 7)]
         met = lp.run_epoch(lp.RunMode.PPLL, mods, it)
         outs.append((met.loss_history, [_flat(m) for m in mods]))
-    assert outs[0][0] == outs[1][0]
-    for a, b in zip(outs[0][1], outs[1][1]):
-        assert np.array_equal(a, b)
+    for o in outs[1:]:
+        assert outs[0][0] == o[0]
+        for a, b in zip(outs[0][1], o[1]):
+            assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
