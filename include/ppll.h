@@ -139,6 +139,11 @@ int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x, con
  * HBM-resident dataset. */
 int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx, void* dst,
                      int dst_dtype, const int64_t* labels_src, int64_t* labels_dst, void* stream);
+/* out_ms[i] = milliseconds from event `ref` to events[i] (cudaEvent_t
+ * handles, all recorded and complete): the per-step timestamps behind
+ * EpochMetrics busy / wall time (runtime.py:340-354, 383-406), read in one
+ * call instead of one driver round trip per event. */
+int ppll_events_elapsed(int n, const uint64_t* events, uint64_t ref, float* out_ms);
 /* Same gather from a dataset held as the IDX file's pixel bytes (uint8):
  * dst[r,c] = src[idx[r],c] / 255 (IEEE division, then the dst cast) — the
  * [0,1] scaling of load_idx (data.py:137-139) applied per batch on the

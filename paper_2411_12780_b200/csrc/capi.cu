@@ -223,6 +223,22 @@ int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx,
   return launch_gather_rows(n, width, src, idx, dst, dst_dtype, labels_src, labels_dst, S(stream));
 }
 
+int ppll_events_elapsed(int n, const uint64_t* events, uint64_t ref, float* out_ms) {
+  if (n < 0 || (n && (!events || !out_ms)) || !ref) {
+    set_error("events_elapsed: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  for (int i = 0; i < n; ++i) {
+    const cudaError_t e = cudaEventElapsedTime(
+        &out_ms[i], reinterpret_cast<cudaEvent_t>(ref), reinterpret_cast<cudaEvent_t>(events[i]));
+    if (e != cudaSuccess) {
+      set_error("events_elapsed: %s", cudaGetErrorString(e));
+      return PPLL_ERR_CUDA;
+    }
+  }
+  return PPLL_OK;
+}
+
 int ppll_gather_rows_u8(int n, int64_t width, const uint8_t* src, const int64_t* idx, void* dst,
                         int dst_dtype, const int64_t* labels_src, int64_t* labels_dst,
                         void* stream) {

@@ -538,6 +538,16 @@ class DevicePipeline:
         metrics = EpochMetrics(n_stages=s)
         step0 = [m.optimizer.step_count for m in mods]
         timing = self.config.timing
+        # timing events come from a pool reused across epochs (an event is
+        # only re-recorded after the previous epoch read its elapsed time)
+        pool = self.__dict__.setdefault("_tev_pool", [])
+        tev_i = [0]
+
+        def tev():
+            if tev_i[0] == len(pool):
+                pool.append(torch.cuda.Event(enable_timing=True))
+            tev_i[0] += 1
+            return pool[tev_i[0] - 1]
         t_start, t_end, t_src = [[] for _ in range(s)], [[] for _ in range(s)], []
         ev0 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(self.src_stream):
@@ -609,7 +619,7 @@ class DevicePipeline:
                 if self.used_free[0][slot]:
                     src.wait_event(self.ev_free[0][slot])
                 if timing:
-                    e = torch.cuda.Event(enable_timing=True)
+                    e = tev()
                     e.record(src)
                     t_src.append(e)
                 if not r.cast or x_src.dtype == r.x[0].dtype:
@@ -631,7 +641,7 @@ class DevicePipeline:
                 if j < s - 1 and self.used_free[j + 1][slot]:
                     st.wait_event(self.ev_free[j + 1][slot])           # credit (backpressure)
                 if timing:
-                    e = torch.cuda.Event(enable_timing=True)
+                    e = tev()
                     e.record(st)
                     t_start[j].append(e)
                 self._step(j, slot, B)
@@ -640,7 +650,7 @@ class DevicePipeline:
                 if j < s - 1:
                     self.ev_ready[j + 1][slot].record(st)              # push
                 if timing:
-                    e = torch.cuda.Event(enable_timing=True)
+                    e = tev()
                     e.record(st)
                     t_end[j].append(e)
                 mods[j].optimizer.step_count += 1
@@ -665,10 +675,17 @@ class DevicePipeline:
         metrics.loss_history = [m.loss_history(step0[j], n) for j, m in enumerate(mods)]
         metrics.buffer_high_water = [0] * s
         if timing and n:
-            ms = lambda e: ev0.elapsed_time(e)  # noqa: E731
-            src_t = [ms(e) for e in t_src]
-            st_t = [[ms(e) for e in t_start[j]] for j in range(s)]
-            en_t = [[ms(e) for e in t_end[j]] for j in range(s)]
+            # every timestamp in one native call (cudaEventElapsedTime loop)
+            evs = t_src + [e for j in range(s) for e in t_start[j]] + \
+                [e for j in range(s) for e in t_end[j]]
+            handles = np.array([e.cuda_event for e in evs], dtype=np.uint64)
+            out = np.empty(len(evs), dtype=np.float32)
+            N.check(N.load().ppll_events_elapsed(len(evs), handles.ctypes.data, ev0.cuda_event,
+                                                 out.ctypes.data), "events_elapsed")
+            flat = out.astype(np.float64).tolist()
+            src_t = flat[:n]
+            st_t = [flat[n + j * n:n + (j + 1) * n] for j in range(s)]
+            en_t = [flat[n + s * n + j * n:n + s * n + (j + 1) * n] for j in range(s)]
             metrics.wall_time = max(en_t[-1][-1], max(v[-1] for v in en_t)) / 1e3
             metrics.busy_time = [sum(b - a for a, b in zip(st_t[j], en_t[j])) / 1e3
                                  for j in range(s)]
