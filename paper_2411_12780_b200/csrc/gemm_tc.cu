@@ -420,13 +420,27 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       // interior tiles store without bounds tests (uniform per tile)
       const bool full = F != kEFGeneric && ep.vec && m0 + BM <= M && n0 + BN <= N;
       const bool tst = F != kEFGeneric && sc.tma_st;
+      // residual / mask blocks (bf16 specialised forms) are fetched one chunk
+      // ahead: chunk c+1's global loads are in flight while chunk c computes
+      constexpr bool kAhead = Epilogue<TO>::template kBlockAux<F>;
+      uint4 nqr[2], nqk[2];
+      if (kAhead && !split && !sc.probe && 16 * grp < BN && n0 + 16 * grp < N)
+        ep.template aux_issue<F>(m0 + q * 32, M, n0 + 16 * grp, nqr, nqk, lane);
 #pragma unroll 1
       for (int c = 16 * grp; c < BN && n0 + c < N; c += 16 * NG) {
         float ra[16], ka[16];
         uint4 qr[2], qk[2];
         // residual / mask loads are issued before the TMEM load so they overlap it
         if (!split && !sc.probe) {
-          ep.template aux_issue<F>(m0 + q * 32, M, n0 + c, qr, qk, lane);
+          if constexpr (kAhead) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) { qr[j] = nqr[j]; qk[j] = nqk[j]; }
+            const int cn = c + 16 * NG;
+            if (cn < BN && n0 + cn < N)
+              ep.template aux_issue<F>(m0 + q * 32, M, n0 + cn, nqr, nqk, lane);
+          } else {
+            ep.template aux_issue<F>(m0 + q * 32, M, n0 + c, qr, qk, lane);
+          }
           if (live) ep.template load_aux16_t<F>(row, n0 + c, ra, ka);
         }
         uint32_t r[16];
