@@ -235,34 +235,25 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
     const int q = warp & 3, grp = (warp - 2) >> 2;
     uint8_t* stg = stg_all + (warp - 2) * 1024;
     int it = 0;
-    // CO <= 64: exactly one 16-channel chunk per warp and tile.  The residual
-    // / mask rows of the NEXT tile are loaded while this tile is finished, and
-    // the accumulator is handed back as soon as it is in registers.
-    static_assert(epi_warps<CO>() * 4 == CO, "one chunk per epilogue warp");
-    const int c = 16 * grp;
-    float ra[16], ka[16];
-    {
-      const int row = blockIdx.x * 128 + q * 32 + lane;
-      if ((int)blockIdx.x < tiles && row < P) ep.load_aux16(row, c, ra, ka);
-    }
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int acc = it & 1, m0 = t * 128;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t r[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CO + c), r);
+      const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 16 * grp; c < CO; c += 64) {
+        float ra[16], ka[16];
+        if (row < P) ep.load_aux16(row, c, ra, ka);
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CO + c), r);
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        ep.finish_block16(m0 + q * 32, P, c, v, ra, ka, nullptr, stg, lane);
+      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      float v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-      float na[16], nk[16];
-      const int tn = t + (int)gridDim.x, rown = tn * 128 + q * 32 + lane;
-      if (tn < tiles && rown < P) ep.load_aux16(rown, c, na, nk);
-      ep.finish_block16(m0 + q * 32, P, c, v, ra, ka, nullptr, stg, lane);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) { ra[i] = na[i]; ka[i] = nk[i]; }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
