@@ -497,7 +497,8 @@ template int launch_softmax_xent<__nv_bfloat16>(int, int, const __nv_bfloat16*, 
 __global__ void __launch_bounds__(256)
 nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const float* __restrict__ g,
                 __nv_bfloat16* __restrict__ th_lp, const float* __restrict__ lr_table, int* step,
-                int max_step, float lr_host, float mu, float wd, int* err, unsigned int* done) {
+                int max_step, float lr_host, float mu, float wd, int* err, unsigned int* done,
+                int advance) {
   pdl_entry();
   __shared__ int s_skip;
   __shared__ float s_lr;
@@ -550,7 +551,7 @@ nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const flo
     }
   }
   if (bad && err) atomicOr(err, kErrParamNonFinite);
-  if (step) {
+  if (step && advance) {
     // last block advances the step counter after every block has read it
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -567,7 +568,8 @@ nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const flo
 
 int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* th_lp,
                     const float* lr_table, int* step, int max_step, float lr_host, float mu,
-                    float wd, int* err, cudaStream_t s) {
+                    float wd, int* err, cudaStream_t s, bool advance) {
+  if (n <= 0 && !advance) return PPLL_OK;
   long n4 = (n + 3) / 4;
   int blocks = (int)min((n4 + 255) / 256, (long)148 * 4);
   if (blocks < 1) blocks = 1;
@@ -579,7 +581,7 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
   // step points to two int32 words: [step_count, block-completion scratch]
   unsigned int* done = step ? reinterpret_cast<unsigned int*>(step + 1) : nullptr;
   launch_k(nesterov_kernel, blocks, 256, 0, s, n, th, v, g, th_lp, lr_table, step, max_step, lr_host,
-                                         mu, wd, err, done);
+                                         mu, wd, err, done, advance ? 1 : 0);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

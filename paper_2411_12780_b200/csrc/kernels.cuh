@@ -840,9 +840,11 @@ template <typename T>
 int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* dz, int lddz,
                         float* loss_hist, const int* step, int* err, cudaStream_t s);
 
+// advance = false: update only (the step counter is advanced by the step's
+// last launch, after every range has read it)
 int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* th_lp,
                     const float* lr_table, int* step, int max_step, float lr_host, float mu,
-                    float wd, int* err, cudaStream_t s);
+                    float wd, int* err, cudaStream_t s, bool advance = true);
 
 int launch_cast(long n, const void* src, int sd, void* dst, int dd, cudaStream_t s);
 int launch_gather_rows(int n, long width, const float* src, const int64_t* idx, void* dst,
