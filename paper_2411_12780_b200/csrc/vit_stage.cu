@@ -194,12 +194,6 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
   SideFlow sf{s, (side_on && st->side) ? st->side : s, st->ev.data(), 0, (int)st->ev.size()};
   float* wsw = sf.on() ? st->ws2 : st->ws;   // the weight gradients' workspace
-  // Nesterov over the flat-parameter range [b0, b1) (optim.py:71-89)
-  auto update = [&](int64_t b0, int64_t b1, cudaStream_t us, bool advance) {
-    __nv_bfloat16* lp = st->theta_lp ? reinterpret_cast<__nv_bfloat16*>(st->theta_lp) + b0 : nullptr;
-    return launch_nesterov(b1 - b0, st->theta + b0, st->mom + b0, st->grad + b0, lp, st->lr_table,
-                           st->step, st->max_step, 0.f, st->mu, st->wd, st->err, us, advance);
-  };
   int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
   if (r) return r;
   r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
@@ -306,16 +300,6 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     char* t = dx2;
     dx2 = dxn_out;
     dxn_out = t;
-    // every gradient of layer l is final here (its Wqkv gradient is the last
-    // side-stream item; b2 of layer l came from the LN1 backward above it):
-    // its Nesterov update runs on the side stream while the main stream
-    // continues with the layers below
-    if (sf.on()) {
-      sf.fork();
-      const int64_t b0 = st->po(l, 0), b1 = l + 1 < st->layers() ? st->po(l + 1, 0) : st->ho(0);
-      r = update(b0, b1, sf.ss, false);
-      if (r) return r;
-    }
   }
   if (st->has_patch) {
     const int P = T - 1, pd = st->img_c * st->patch * st->patch;
@@ -326,16 +310,11 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
                      st->G(st->off[1]), st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
   }
-  // every weight gradient (and layer update) has landed
+  // every weight gradient has landed before the optimizer reads them
   sf.join(sf.mark());
-  if (!sf.on()) return update(0, st->n_params, s, true);
-  // the rest (patch embedding, head) on the main stream; this last launch
-  // advances the step counter after every range has read it
-  if (st->po(0, 0) > 0) {
-    r = update(0, st->po(0, 0), s, false);
-    if (r) return r;
-  }
-  return update(st->ho(0), st->n_params, s, true);
+  return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
+                         reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
+                         st->max_step, 0.f, st->mu, st->wd, st->err, s);
 }
 
 extern "C" {
@@ -403,7 +382,7 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
     st->side = nullptr;
     cudaGetLastError();
   } else {
-    st->ev.resize(10 * (size_t)st->layers() + 8);
+    st->ev.resize(8 * (size_t)st->layers() + 8);
     for (auto& e : st->ev)
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) ok = false;
   }
