@@ -193,9 +193,14 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   // atom overwrites Q (dead once S = Q·Kᵀ has retired), K and V hold only
   // their NK rows, and O = P·V reuses the S columns after they are read.
   const int kbytes = (NK * 128 + 1023) & ~1023;
+  // NK <= 64 (e.g. ViT-B/16 at 96x96, T = 37): P is one 64-key atom (it
+  // overwrites Q exactly) and S / O fit 64 TMEM columns, so ~30 KB of smem
+  // and 64 columns per CTA: more CTAs per SM than the 128-key layout
+  const bool small = NK <= 64;
+  const uint32_t tcols = small ? 64u : 128u;
   uint8_t* sQ = sm;                 // 16 KB
-  uint8_t* sP = sm;                 // 32 KB: [Q | keys 64..127 atom]
-  uint8_t* sK = sm + 32768;         // NK*128 B (<= 16 KB)
+  uint8_t* sP = sm;                 // [Q | keys 64..127 atom]: 16 KB or 32 KB
+  uint8_t* sK = sm + (small ? 16384 : 32768);   // NK*128 B (<= 16 KB)
   uint8_t* sV = sK + kbytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + kbytes);   // [0]=tma [1]=mma
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
@@ -209,8 +214,8 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
-        smem_u32(tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tslot)), "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -248,7 +253,8 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   }
   float sum = 0.f;
   const bool live = r < Tn;
-  for (int c = 0; c < 128; c += 16) {
+  const int pkeys = small ? 64 : 128;   // P columns written (zeros past NK)
+  for (int c = 0; c < pkeys; c += 16) {
     float v[16];
     if (c < NK) ld16(lane_base + c, v);
 #pragma unroll
@@ -290,7 +296,7 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(tcols));
   }
 }
 
@@ -479,7 +485,9 @@ static bool map2d(CUtensorMap* m, const void* ptr, long inner, long outer, long 
 }
 
 constexpr int kFwdSmem = 16384 * 2 + 32768 + 1024 + 64;   // upper bound (NK = 128)
-inline int fwd_smem(int NK) { return 32768 + 2 * ((NK * 128 + 1023) & ~1023) + 1024 + 64; }
+inline int fwd_smem(int NK) {
+  return (NK <= 64 ? 16384 : 32768) + 2 * ((NK * 128 + 1023) & ~1023) + 1024 + 64;
+}
 constexpr int kBwdSmem = 16384 * 3 + 32768 * 2 + 1024 + 64;   // upper bound (NK = 128)
 inline int bwd_smem(int NK) { return 16384 * 2 + ((NK * 128 + 1023) & ~1023) + 32768 * 2 + 1024 + 64; }
 
