@@ -1127,6 +1127,13 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
       cl_bn = 0;
     }
   }
+  // (profiling) force the tile width: PPLL_GEMM_BN=64|128|192|256
+  static const int force_bn = getenv("PPLL_GEMM_BN") ? atoi(getenv("PPLL_GEMM_BN")) : 0;
+  if (force_bn && !cl_bn && (force_bn == 64 || force_bn == 128 || force_bn == 192 ||
+                             force_bn == 256)) {
+    bn = force_bn;
+    splits = 1;
+  }
   Sched sc;
   sc.tma_st = 0;
   sc.mt = mt;
