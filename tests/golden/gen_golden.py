@@ -259,6 +259,36 @@ def gen_experiment():
         json.dump(out, f, indent=0)
 
 
+def gen_experiment_idx():
+    """run_experiment on an IDX image/label pair (data.py:118-144 through
+    harness.py:78-206), deterministic schedule, all three modes."""
+    import tempfile
+    from locopipe.config import ExperimentConfig
+    rng = np.random.default_rng(21)
+    count, rows, cols = 90, 4, 5
+    lab = rng.integers(0, 3, count).astype(np.uint8)
+    # class-dependent pixel means so the run learns something
+    pix = np.clip(rng.normal(60 + 60 * lab[:, None], 40, (count, rows * cols)), 0, 255).astype(np.uint8)
+    img = struct.pack(">IIII", 0x803, count, rows, cols) + pix.tobytes()
+    lbl = struct.pack(">II", 0x801, count) + lab.tobytes()
+    with tempfile.TemporaryDirectory() as td:
+        ip, lp_ = os.path.join(td, "i.idx"), os.path.join(td, "l.idx")
+        open(ip, "wb").write(img)
+        open(lp_, "wb").write(lbl)
+        kw = dict(dataset="idx", idx_train_images=ip, idx_train_labels=lp_,
+                  layer_dims=(rows * cols, 16, 12, 3), stages=2, batch_size=16, epochs=2,
+                  lr0=0.05, lr_min=0.001, seed=5)
+        recs, rep = lp.run_experiment(ExperimentConfig(**kw), deterministic=True)
+    out = {"images": list(img), "labels": list(lbl),
+           "config": {k: list(v) if isinstance(v, tuple) else v for k, v in kw.items()
+                      if not k.startswith("idx_")},
+           "records": [[r.mode, r.epoch, r.mean_loss, r.train_acc, r.test_acc,
+                        r.params_max_stage, r.activations_max_stage, r.mean_staleness]
+                       for r in recs]}
+    with open(os.path.join(HERE, "experiment_idx.json"), "w") as f:
+        json.dump(out, f)
+
+
 def gen_costs():
     """costs.py analytic forms, simulator timelines and Gantt CSV (reference)."""
     cases = []
@@ -310,4 +340,5 @@ if __name__ == "__main__":
     gen_costs()
     gen_datasets()
     gen_experiment()
+    gen_experiment_idx()
     print("ok")

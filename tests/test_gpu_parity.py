@@ -644,3 +644,25 @@ def test_run_experiment_matches_reference(tmp_path):
     det, _ = lp.run_experiment(cfg, deterministic=True)
     for a, b in zip(thr, det):
         assert (a.mean_loss, a.train_acc, a.test_acc) == (b.mean_loss, b.train_acc, b.test_acc)
+
+
+def test_run_experiment_on_idx_matches_reference(tmp_path):
+    """The IDX path end to end: load_idx -> HBM-resident pixel bytes -> the
+    device u8 gather -> run_experiment (all modes), against the reference's
+    own run on the same files (tests/golden/experiment_idx.json)."""
+    import json
+    g = json.load(open(os.path.join(GOLDEN, "experiment_idx.json")))
+    (tmp_path / "i.idx").write_bytes(bytes(g["images"]))
+    (tmp_path / "l.idx").write_bytes(bytes(g["labels"]))
+    kw = {k: tuple(v) if isinstance(v, list) else v for k, v in g["config"].items()}
+    cfg = lp.ExperimentConfig(idx_train_images=str(tmp_path / "i.idx"),
+                              idx_train_labels=str(tmp_path / "l.idx"), **kw)
+    recs, rep = lp.run_experiment(cfg, deterministic=True)
+    n = len(g["labels"]) - 8
+    assert len(recs) == len(g["records"])
+    for r, ref in zip(recs, g["records"]):
+        assert (r.mode, r.epoch) == (ref[0], ref[1])
+        assert abs(r.mean_loss - ref[2]) <= 5e-5, (r, ref)
+        assert abs(r.train_acc - ref[3]) <= 2.0 / n and abs(r.test_acc - ref[4]) <= 2.0 / n
+        assert (r.params_max_stage, r.activations_max_stage) == (ref[5], ref[6])
+        assert abs(r.mean_staleness - ref[7]) < 1e-12
