@@ -42,6 +42,7 @@ SIGNATURES = {
     "ppll_gather_rows": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_gather_rows_u8": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_events_elapsed": (_i, [_i, _vp, C.c_uint64, _vp]),
+    "ppll_set_pdl": (_i, [_i]),
     "ppll_count_correct": (_i, [_i, _i, _vp, _i, _i, _vp, _vp, _vp]),
     "ppll_stage_create": (_vp, [_i, _i, _vp, _vp, _vp, _vp, _i64, _i, _i, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _i, _vp, _vp, _f, _f]),

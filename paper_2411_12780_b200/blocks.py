@@ -150,6 +150,11 @@ class LocalModule:
     """One gradient-isolated pipeline stage: block layers + optional aux head
     (blocks.py:147-187), resident on one CUDA device."""
 
+    # keep programmatic dependent launch when several stage streams share a
+    # GPU (measured: the many short MLP / ResNet kernels gain from it; the
+    # ViT step's long GEMMs lose 1.4 % — VitLocalModule turns it off)
+    shared_gpu_pdl = True
+
     def __init__(self, stage_index, layers, aux, optimizer, schedule, assigned_aux_depth,
                  *, flat=None, device=None, precision="fp32"):
         if not layers:

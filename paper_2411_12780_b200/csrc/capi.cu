@@ -223,6 +223,12 @@ int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx,
   return launch_gather_rows(n, width, src, idx, dst, dst_dtype, labels_src, labels_dst, S(stream));
 }
 
+int ppll_set_pdl(int on) {
+  const int prev = g_pdl;
+  g_pdl = on ? 1 : 0;
+  return prev;
+}
+
 int ppll_events_elapsed(int n, const uint64_t* events, uint64_t ref, float* out_ms) {
   if (n < 0 || (n && (!events || !out_ms)) || !ref) {
     set_error("events_elapsed: invalid arguments");

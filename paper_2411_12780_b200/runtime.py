@@ -24,6 +24,8 @@ event timestamps recorded around every stage step.
 """
 from __future__ import annotations
 
+import os
+
 import threading
 import time
 from collections import Counter, deque
@@ -534,6 +536,27 @@ class DevicePipeline:
 
     # -- the epoch -------------------------------------------------------
     def run(self, dataset_iter: Iterable) -> EpochMetrics:
+        """One epoch.  Programmatic dependent launch (PDL) pays when a GPU runs
+        one stage stream (the next kernel's prologue overlaps the current
+        tail).  With several stage streams on a GPU it depends on the family
+        (``shared_gpu_pdl``): early-launched kernels hold SM slots while they
+        wait, which costs the ViT step (4 streams on one B200: PDL off
+        +1.4 %) but not the short-kernel ResNet / MLP steps (PDL off -11 %
+        for ResNet-32).  PPLL_PDL in the environment overrides."""
+        per_dev = {}
+        for st, m in zip(self.streams, self.modules):
+            per_dev.setdefault(str(m.device), set()).add(st.cuda_stream)
+        shared = (max(len(v) for v in per_dev.values()) > 1 and
+                  not all(getattr(m, "shared_gpu_pdl", True) for m in self.modules))
+        lib = N.load()
+        prev = None if "PPLL_PDL" in os.environ else lib.ppll_set_pdl(0 if shared else 1)
+        try:
+            return self._run(dataset_iter)
+        finally:
+            if prev is not None:
+                lib.ppll_set_pdl(prev)
+
+    def _run(self, dataset_iter: Iterable) -> EpochMetrics:
         mods, M, s = self.modules, self.M, len(self.modules)
         metrics = EpochMetrics(n_stages=s)
         step0 = [m.optimizer.step_count for m in mods]

@@ -100,6 +100,8 @@ def balanced_depths(depth: int, s: int) -> list:
 class VitLocalModule(LocalModule):
     """One ViT stage: [patch embed] + block layers + aux layers + head."""
 
+    shared_gpu_pdl = False   # see LocalModule.shared_gpu_pdl
+
     def __init__(self, stage_index, spec, groups, n_block, n_aux, optimizer, schedule,
                  assigned_aux_depth, *, flat, device, precision, final):
         self.spec = spec
