@@ -26,6 +26,7 @@ process group (gloo is enough); nothing on the data path uses a collective.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -262,7 +263,19 @@ class DistributedPipeline:
     def run(self, batches: Iterable | None, n_batches: int, batch_size: int) -> dict:
         """Enqueue ``n_batches`` batches through this rank's stages.  The rank
         owning stage 0 consumes ``batches`` (device or host (x, y) pairs).
-        Returns this rank's timings and loss histories (after a sync)."""
+        Returns this rank's timings and loss histories (after a sync).  PDL
+        policy as in ``DevicePipeline.run`` (off for several ViT stage
+        streams on this GPU unless PPLL_PDL is set)."""
+        off = (len(self.mods) > 1 and
+               not all(getattr(m, "shared_gpu_pdl", True) for m in self.mods.values()))
+        prev = None if "PPLL_PDL" in os.environ else self.lib.ppll_set_pdl(0 if off else 1)
+        try:
+            return self._run(batches, n_batches, batch_size)
+        finally:
+            if prev is not None:
+                self.lib.ppll_set_pdl(prev)
+
+    def _run(self, batches: Iterable | None, n_batches: int, batch_size: int) -> dict:
         M, B = self.M, batch_size
         lib = self.lib
         step0 = {j: m.optimizer.step_count for j, m in self.mods.items()}
