@@ -44,23 +44,23 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     "vit_s": dict(kind="vit", spec=dict(image=32, channels=3, patch=4, dim=384, heads=6,
                                         mlp=1536, depth=8, classes=10),
-                  s=4, d_prime=1, interval=3, batch=128, ref_batch=4),
+                  s=4, d_prime=1, interval=3, batch=128),
     # configs[0]: ResNet-32 / 4 blocks, CIFAR-shaped, batch 128
     "resnet32": dict(kind="resnet", spec=dict(n=5, image=32, channels=3, widths=(16, 32, 64),
                                               classes=10),
-                     s=4, d_prime=1, interval=3, batch=128, ref_batch=8, data_shape="CIFAR-10",
+                     s=4, d_prime=1, interval=3, batch=128, data_shape="CIFAR-10",
                      split="cost"),
     # configs[2]: ResNet-110 / 8 blocks, SVHN-shaped, batch 256
     "resnet110": dict(kind="resnet", spec=dict(n=18, image=32, channels=3, widths=(16, 32, 64),
                                                classes=10),
-                      s=8, d_prime=1, interval=3, batch=256, ref_batch=4, data_shape="SVHN",
+                      s=8, d_prime=1, interval=3, batch=256, data_shape="SVHN",
                       split="cost"),
     # configs[3]: ViT-base / 8 blocks, STL-10-shaped 96x96, patch 16 (T = 37), batch 128
     "vit_b": dict(kind="vit", spec=dict(image=96, channels=3, patch=16, dim=768, heads=12,
                                         mlp=3072, depth=12, classes=10),
-                  s=8, d_prime=1, interval=3, batch=128, ref_batch=1, data_shape="STL-10"),
+                  s=8, d_prime=1, interval=3, batch=128, data_shape="STL-10"),
     "mlp_m": dict(kind="mlp", dims=(3072, 1024, 1024, 1024, 1024, 10), s=4, d_prime=2,
-                  interval=3, batch=128, ref_batch=128),
+                  interval=3, batch=128),
 }
 
 
@@ -143,9 +143,23 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def balanced_depths_list(depth, s):
-    q, r = divmod(depth, s)
-    return [q + (1 if j < r else 0) for j in range(s)]
+def vit_depths(wl):
+    """Layers per ViT block: cost-balanced (``balanced_vit_depths``: block
+    layers + aux head + patch embedding per stage) unless the workload says
+    ``split="even"``."""
+    from paper_2411_12780_b200.vit import VitSpec, balanced_depths, balanced_vit_depths
+    spec = VitSpec(**wl["spec"])
+    if wl.get("split", "cost") == "even":
+        return balanced_depths(spec.depth, wl["s"])
+    return balanced_vit_depths(spec, wl["s"], wl["d_prime"], wl["interval"])
+
+
+def resnet_blocks(wl):
+    from paper_2411_12780_b200.resnet import ResNetSpec, balanced_resnet_split, resnet_split
+    spec = ResNetSpec(**wl["spec"])
+    if wl.get("split", "even") == "cost":
+        return balanced_resnet_split(spec, wl["s"], wl["d_prime"], wl["interval"])
+    return resnet_split(spec, wl["s"])
 
 
 def describe(wl, name):
@@ -160,39 +174,65 @@ def describe(wl, name):
         size = "base" if sp["dim"] >= 768 else "small"
         return (f"{name}: PPLL ViT-{size}/{sp['patch']} depth {sp['depth']} D={sp['dim']} "
                 f"heads={sp['heads']} MLP={sp['mlp']}, {wl['s']} gradient-isolated blocks "
-                f"(layers {balanced_depths_list(sp['depth'], wl['s'])}), aux = aux_depth(l,"
+                f"(layers {vit_depths(wl)}), aux = aux_depth(l,"
                 f"{wl['d_prime']},{wl['interval']}) transformer layers + LN + classifier, "
                 f"{wl.get('data_shape', 'CIFAR-10')}-shaped {sp['channels']}x{sp['image']}x"
                 f"{sp['image']}, {sp['classes']} classes, batch {wl['batch']}")
     return (f"{name}: PPLL MLP {'-'.join(map(str, wl['dims']))}, {wl['s']} gradient-isolated "
-            f"stages, d'={wl['d_prime']}, n={wl['interval']}, CIFAR-shaped 3x32x32 inputs")
+            f"stages, d'={wl['d_prime']}, n={wl['interval']}, CIFAR-shaped 3x32x32 inputs, "
+            f"batch {wl['batch']}")
 
 
 def cfg_dict(wl, args):
     extra = {}
-    if wl["kind"] == "resnet" and wl.get("split") == "cost":
-        from paper_2411_12780_b200.resnet import ResNetSpec, balanced_resnet_split
-        sp = balanced_resnet_split(ResNetSpec(**wl["spec"]), wl["s"], wl["d_prime"], wl["interval"])
-        extra["stage_split"] = ("cost-balanced (stem on stage 0) blocks per stage "
-                                f"{[len(b) for b in sp]}")
+    if wl["kind"] == "resnet":
+        extra["stage_split"] = (f"{wl.get('split', 'even')} split, blocks per stage "
+                                f"{[len(b) for b in resnet_blocks(wl)]} (stem on stage 0)")
+    elif wl["kind"] == "vit":
+        extra["stage_split"] = f"{wl.get('split', 'cost')} split, layers per stage {vit_depths(wl)}"
     return extra | {"workload": describe(wl, args.workload),
-            "global_batch": wl["batch"] * max(1, args.gpus), "stages": wl["s"],
+            "global_batch": wl["batch"], "stages": wl["s"], "d_prime": wl["d_prime"],
             "buffer_capacity": args.capacity, "precision": args.precision,
-            "placement": "all stages on each GPU (replicas)" if args.gpus > 1 else
-                         "all stages on one GPU, one CUDA stream per stage",
+            "placement": "all stages on one GPU, one CUDA stream per stage",
             "l2": "no flush between steps; per-step working set (64-batch resident input "
                   "pool + per-stage params/momenta/grads/activations) exceeds the 126 MB L2"}
 
 
+def bench_phases(steps: int, warmup: int, s: int) -> dict:
+    """Local steps every module takes in one N=1 bench run, phase by phase
+    (main() consumes exactly these; the cosine-LR horizon ``total_steps`` is
+    sized from them — cosine_lr raises StepOutOfRange past it, optim.py:39-44)."""
+    return {"warmup": warmup, "launch_probe": 1, "timed": steps, "sequential_warmup": 3,
+            "sequential": max(10, steps // 3), "e2e_warmup": 2 * s + 2,
+            "e2e": max(100, steps)}
+
+
+def sharded_phases(steps: int, warmup: int) -> dict:
+    """The same for the N>1 (one process per GPU) path."""
+    return {"warmup": warmup, "timed": steps, "e2e": max(60, steps)}
+
+
+def step_budget(phases: dict) -> int:
+    return sum(phases.values()) + 16
+
+
 # ---------------------------------------------------------------------------
-# the reference arm / CPU baseline: the oracle port on host cores
+# the reference arm / CPU baseline: the reference algorithm on host cores
 # ---------------------------------------------------------------------------
 
-def cpu_reference(wl, n_batches, warmup=1, time_budget=None, batch=None):
-    """Images/s of the oracle port running the sequential local-learning
-    schedule (bitwise the PPLL result) on host cores."""
+def cpu_reference(wl, n_batches, warmup=1, time_budget=None):
+    """Images/s of the reference algorithm on the host cores, sequential
+    local-learning schedule (bitwise the PPLL result), at the
+    workload's full batch and stage split; the number of steps (not the
+    batch) is time-bounded.  MLP: the numpy float64 oracle port of the
+    reference (pinned to its golden vectors).  ViT / ResNet (no reference
+    implementation exists): the torch-CPU fp32 restatement (oracle/torch_cpu.py,
+    BASELINE.md §3), every host thread to torch's intra-op pool."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    B = batch or wl["batch"]
+    import torch
+    cores = len(os.sched_getaffinity(0))
+    torch.set_num_threads(cores)
+    B = wl["batch"]
     rng = np.random.default_rng(0)
     if wl["kind"] == "mlp":
         import ppll_oracle as orc
@@ -200,63 +240,63 @@ def cpu_reference(wl, n_batches, warmup=1, time_budget=None, batch=None):
         stages = orc.build_stages(dims, orc.partition(dims, wl["s"]), wl["d_prime"],
                                   wl["interval"], 42)
         data = [(rng.standard_normal((B, dims[0])), rng.integers(0, dims[-1], B))
-                for _ in range(4)]
+                for _ in range(2)]
+        kind = "numpy float64 oracle port of the reference (sequential schedule)"
 
         def step(x, y):
             orc.sequential_ppll(stages, [(x, y)], 0.05, 0.001, 10 ** 6, 0.9, 1e-4)
-    elif wl["kind"] == "resnet":
-        import resnet_oracle as ro
-        spec = ro.ResNetSpec(**wl["spec"])
-        stages = ro.build_resnet_stages(spec, wl["s"], wl["d_prime"], wl["interval"], 42)
-        data = [(rng.standard_normal((B, spec.image, spec.image, spec.channels)),
-                 rng.integers(0, spec.classes, B)) for _ in range(4)]
-
-        def step(x, y):
-            h = x
-            for st in stages:
-                _, h, _ = ro.local_step(st, h, y, 0.05, 0.001, 10 ** 6, 0.9, 1e-4)
     else:
-        import vit_oracle as vo
-        spec = vo.VitSpec(**wl["spec"])
-        depths = balanced_depths_list(spec.depth, wl["s"])
-        stages = vo.build_vit_stages(spec, depths, wl["d_prime"], wl["interval"], 42)
-        data = [(rng.standard_normal((B, spec.channels, spec.image, spec.image)),
-                 rng.integers(0, spec.classes, B)) for _ in range(4)]
+        import torch_cpu as tc
+        if wl["kind"] == "resnet":
+            import resnet_oracle as ro
+            spec = ro.ResNetSpec(**wl["spec"])
+            stages = [tc.from_resnet(st) for st in ro.build_resnet_stages(
+                spec, wl["s"], wl["d_prime"], wl["interval"], 42, split=resnet_blocks(wl))]
+            shape = (B, spec.image, spec.image, spec.channels)
+        else:
+            import vit_oracle as vo
+            spec = vo.VitSpec(**wl["spec"])
+            stages = [tc.from_vit(st) for st in vo.build_vit_stages(
+                spec, vit_depths(wl), wl["d_prime"], wl["interval"], 42)]
+            shape = (B, spec.channels, spec.image, spec.image)
+        data = [(torch.tensor(rng.standard_normal(shape), dtype=torch.float32),
+                 rng.integers(0, spec.classes, B)) for _ in range(2)]
+        kind = "torch-CPU fp32 restatement (oracle/torch_cpu.py, sequential schedule)"
 
         def step(x, y):
             h = x
             for st in stages:
-                _, h, _ = vo.local_step(st, h, y, 0.05, 0.001, 10 ** 6, 0.9, 1e-4)
+                _, h, _ = tc.local_step(st, h, y, 0.05, 0.001, 10 ** 6, 0.9, 1e-4)
     for i in range(warmup):
-        step(*data[i % 4])
+        step(*data[i % 2])
     t0 = time.perf_counter()
     done = 0
     for i in range(n_batches):
-        step(*data[i % 4])
+        step(*data[i % 2])
         done += 1
         if time_budget and time.perf_counter() - t0 > time_budget:
             break
     dt = time.perf_counter() - t0
-    return done * B / dt, done, dt, B
+    return {"value": done * B / dt, "unit": "images/s", "cores": cores, "kind": "port",
+            "sample": f"{done} steps x batch {B} through all {wl['s']} stages, {kind}, "
+                      f"{cores} threads, {dt:.1f} s",
+            "steps": done, "seconds": dt, "dtype": "f64" if wl["kind"] == "mlp" else "fp32"}
 
 
 def run_reference_arm(args, wl, rank):
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0))
-    ips, done, dt, B = cpu_reference(wl, args.steps, warmup=min(args.warmup, 1),
-                                     time_budget=150.0, batch=wl["ref_batch"])
+    warm = min(args.warmup, 1)
+    cpu = cpu_reference(wl, args.steps, warmup=warm, time_budget=120.0)
+    ips = cpu["value"]
     line = {
         "impl": "reference", "metric": "images/sec training (device-timed) at 1/2/4/8 B200; "
         "pipeline idle fraction", "value": ips, "unit": "images/s",
-        "n_gpus": args.gpus, "steps": done, "warmup": min(args.warmup, 1),
-        "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "n_gpus": args.gpus, "steps": cpu["steps"], "warmup": warm,
+        "ms_per_step": 1e3 * cpu["seconds"] / max(cpu["steps"], 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cpu["dtype"], "data": "synthetic",
         "config": cfg_dict(wl, args),
-        "cpu_baseline": {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"{done} steps x {B} images through all {wl['s']} stages "
-                                   f"(numpy fp64 oracle port, sequential schedule, all "
-                                   f"{cores} cores to BLAS; time-bounded at 150 s)"},
+        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": ips, "unit": "images/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -278,9 +318,9 @@ def build(wl, precision, device, total_steps):
     if wl["kind"] == "resnet":
         return lp.build_resnet_modules(lp.ResNetSpec(**wl["spec"]), wl["s"], wl["d_prime"],
                                        wl["interval"], hyper, devices=[device] * wl["s"],
-                                       split=wl.get("split", "even"))
+                                       split=resnet_blocks(wl))
     spec = lp.VitSpec(**wl["spec"])
-    return lp.build_vit_modules(spec, lp.balanced_depths(spec.depth, wl["s"]), wl["d_prime"],
+    return lp.build_vit_modules(spec, vit_depths(wl), wl["d_prime"],
                                 wl["interval"], hyper, devices=[device] * wl["s"])
 
 
@@ -304,7 +344,7 @@ def run_sharded(args, wl, rank, world, local, dev):
     placement = stage_placement(s, world)
     mine = [j for j in range(s) if placement[j] == rank]
     B = wl["batch"]
-    total = args.warmup + 2 * args.steps + 16
+    total = step_budget(sharded_phases(args.steps, args.warmup))
     hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=total, seed=42,
                            precision=args.precision)
     if wl["kind"] == "mlp":
@@ -317,11 +357,11 @@ def run_sharded(args, wl, rank, world, local, dev):
     elif wl["kind"] == "resnet":
         spec = lp.ResNetSpec(**wl["spec"])
         mods = lp.build_resnet_modules(spec, s, wl["d_prime"], wl["interval"], hyper,
-                                       split=wl.get("split", "even"),
+                                       split=resnet_blocks(dict(wl, s=s)),
                                        devices=[dev] * s, only=mine)
     else:
         spec = lp.VitSpec(**wl["spec"])
-        mods = lp.build_vit_modules(spec, lp.balanced_depths(spec.depth, s), wl["d_prime"],
+        mods = lp.build_vit_modules(spec, vit_depths(dict(wl, s=s)), wl["d_prime"],
                                     wl["interval"], hyper, devices=[dev] * s, only=mine)
     pipe = DistributedPipeline(mods, placement, rank, None, capacity=args.capacity, max_batch=B,
                                use_graphs=not args.no_graphs)
@@ -360,7 +400,7 @@ def run_sharded(args, wl, rank, world, local, dev):
     # inputs in pinned host memory (the contract's e2e: H2D from pinned buffers)
     host = [(torch.from_numpy(rng.standard_normal((B,) + in_shape).astype(np.float32)).pin_memory(),
              torch.from_numpy(rng.integers(0, n_cls, B)).pin_memory()) for _ in range(8)]
-    e2e_steps = max(60, args.steps)
+    e2e_steps = sharded_phases(args.steps, args.warmup)["e2e"]
     dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
@@ -675,7 +715,30 @@ def cost_model(wl, args, dev, measured_seq_ips, measured_ips):
             "measured_single_gpu_pipeline_images_per_s": measured_ips}
 
 
-def main():
+def _guard(name, fn, *a, **k):
+    """Auxiliary legs (rooflines, cost model, CPU baseline) must not take the
+    bench line down with them: a failure is reported in the line instead."""
+    try:
+        return fn(*a, **k)
+    except Exception as e:          # noqa: BLE001
+        print(f"[bench] {name} failed: {type(e).__name__}: {e}", file=sys.stderr, flush=True)
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
+def workload_from_args(args) -> dict:
+    wl = dict(WORKLOADS[args.workload])
+    if args.batch:
+        wl["batch"] = args.batch
+    if args.d_prime is not None:
+        wl["d_prime"] = args.d_prime
+    if args.stages:
+        wl["s"] = args.stages
+    if args.split:
+        wl["split"] = args.split
+    return wl
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
@@ -684,11 +747,20 @@ def main():
     ap.add_argument("--workload", default="vit_s", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--capacity", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=0, help="override the workload batch (C5 sweep)")
+    ap.add_argument("--d-prime", type=int, default=None, help="max aux depth d' (PAPER.md:271)")
+    ap.add_argument("--stages", type=int, default=0, help="override the stage count (C5 sweep)")
+    ap.add_argument("--split", default=None, choices=["even", "cost"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
-    wl = WORKLOADS[args.workload]
+    return args
+
+
+def main():
+    args = parse_args()
+    wl = workload_from_args(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -712,14 +784,14 @@ def main():
         return run_sharded(args, wl, rank, world, local, dev)
     hbm, tf_burst, tf_sus, peak_kind = peaks()
     B = wl["batch"]
-    total = args.warmup + 3 * args.steps + 64
-    mods = build(wl, args.precision, dev, total)
+    ph = bench_phases(args.steps, args.warmup, wl["s"])
+    mods = build(wl, args.precision, dev, step_budget(ph))
     in_shape = tuple(mods[0].in_shape)
     n_cls = mods[-1].num_classes
     cfg = lp.RunConfig(buffer_capacity=args.capacity, use_graphs=not args.no_graphs,
                        timing=True)
     pipe = lp.DevicePipeline(mods, cfg)
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    gen = torch.Generator(device=dev).manual_seed(1234)
     pool_x = torch.randn((64, B) + in_shape, device=dev, generator=gen)
     pool_y = torch.randint(0, n_cls, (64, B), device=dev, generator=gen)
 
@@ -727,28 +799,21 @@ def main():
         for i in range(k):
             yield pool_x[(off + i) % 64], pool_y[(off + i) % 64]
 
-    pipe.run(batches(args.warmup))                    # warm-up (+ graph capture)
+    pipe.run(batches(ph["warmup"]))                   # warm-up (+ graph capture)
     before = N.launch_count()
     probe = lp.DevicePipeline(mods, lp.RunConfig(buffer_capacity=args.capacity,
                                                  use_graphs=False, timing=False))
-    probe.run(batches(1, 7))
+    probe.run(batches(ph["launch_probe"], 7))
     launches_per_step = N.launch_count() - before
     torch.cuda.synchronize(dev)
 
     # ---- the timed region: PPLL pipeline, inputs resident in HBM ----
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
-        met = pipe.run(batches(args.steps, 11))
+        met = pipe.run(batches(ph["timed"], 11))
     torch.cuda.synchronize(dev)
     wall = met.wall_time
-    if world > 1:
-        t = torch.tensor([wall], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        wall = float(t.item())
-        dist.barrier()
-    value = met.images * world / wall
+    value = met.images / wall
     idle = met.idle_fraction
 
     # ---- the sequential local-learning schedule on one stream (paper's S=1) ----
@@ -757,88 +822,77 @@ def main():
     cur = torch.cuda.current_stream(dev)
     seq.streams = [cur] * len(mods)
     seq.src_stream = cur
-    seq.run(batches(3))
+    seq.run(batches(ph["sequential_warmup"]))
     torch.cuda.synchronize(dev)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nseq = max(10, args.steps // 3)
+    nseq = ph["sequential"]
     a.record()
     seq.run(batches(nseq, 5))
     b.record()
     b.synchronize()
     seq_ips = nseq * B / (a.elapsed_time(b) * 1e-3)
 
-    # ---- e2e through the public API: host numpy batches ----
-    rng = np.random.default_rng(7 + rank)
-    # inputs in pinned host memory (the contract's e2e: H2D from pinned buffers)
+    # ---- e2e through the public API: pinned host batches ----
+    rng = np.random.default_rng(7)
     host = [(torch.from_numpy(rng.standard_normal((B,) + in_shape).astype(np.float32)).pin_memory(),
              torch.from_numpy(rng.integers(0, n_cls, B)).pin_memory()) for _ in range(8)]
     # one untimed epoch first (pipeline staging / graphs are cached per module
     # set), then enough batches that the epoch's fill and drain amortise
-    lp.run_epoch(lp.RunMode.PPLL, mods, (host[i % 8] for i in range(2 * wl["s"] + 2)), cfg)
-    e2e_steps = max(100, args.steps)
-    if world > 1:
-        dist.barrier()
+    lp.run_epoch(lp.RunMode.PPLL, mods, (host[i % 8] for i in range(ph["e2e_warmup"])), cfg)
+    e2e_steps = ph["e2e"]
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     m2 = lp.run_epoch(lp.RunMode.PPLL, mods, (host[i % 8] for i in range(e2e_steps)), cfg)
     _ = [sum(h) for h in m2.loss_history]           # losses read back (D2H)
     e2e_dt = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_dt = float(t.item())
-    e2e = {"value": e2e_steps * B * world / e2e_dt, "unit": "images/s",
+    e2e = {"value": e2e_steps * B / e2e_dt, "unit": "images/s",
            "h2d_bytes_per_step": B * int(np.prod(in_shape)) * 4 + B * 8,
            "d2h_bytes_per_step": 4 * wl["s"],
            "api": "paper_2411_12780_b200.run_epoch(RunMode.PPLL, modules, pinned host batches)"}
+    used = [m.optimizer.step_count for m in mods]
+    assert max(used) <= step_budget(ph), (used, ph)
 
     if wl["kind"] == "vit":
-        roof = roofline_gemm(wl, tf_burst, hbm, dev)
-        roof_extra = roofline_nesterov(mods, hbm, dev)
+        roof = _guard("roofline_gemm", roofline_gemm, wl, tf_burst, hbm, dev)
+        roof_extra = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
     elif wl["kind"] == "resnet" and args.precision == "bf16":
-        roof = roofline_conv(wl, tf_burst, hbm, dev)
-        roof_extra = roofline_nesterov(mods, hbm, dev)
+        roof = _guard("roofline_conv", roofline_conv, wl, tf_burst, hbm, dev)
+        roof_extra = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
     else:
-        roof = roofline_nesterov(mods, hbm, dev)
+        roof = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
         roof_extra = None
-    roof["peak_kind"] = peak_kind
+    if isinstance(roof, dict):
+        roof["peak_kind"] = peak_kind
 
-    cmodel = cost_model(wl, args, dev, seq_ips, value) if world == 1 else None
+    cmodel = _guard("cost_model", cost_model, wl, args, dev, seq_ips, value)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ips, done, dt, Bc = cpu_reference(wl, 10 ** 6, warmup=1, time_budget=15.0,
-                                          batch=wl["ref_batch"])
-        cpu = {"value": ips, "unit": "images/s", "cores": len(os.sched_getaffinity(0)),
-               "kind": "port",
-               "sample": f"{done} steps x {Bc} images through all {wl['s']} stages, "
-                         f"sequential schedule, numpy fp64 oracle port ({dt:.1f} s)"}
+    if not args.no_cpu_baseline:
+        cpu = _guard("cpu_baseline", cpu_reference, wl, 10 ** 6, warmup=1, time_budget=20.0)
+        if isinstance(cpu, dict) and "value" in cpu:
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
-    if rank == 0:
-        line = {
-            "metric": "images/sec training (device-timed) at 1/2/4/8 B200; pipeline idle fraction",
-            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": args.precision, "data": "synthetic (seeded N(0,1) CIFAR-shaped inputs, "
-            "uniform labels; random-init weights drawn like the reference)",
-            "config": cfg_dict(wl, args) | {"parallelism": f"replicas{world}" if world > 1
-                                            else "pp-streams"},
-            "idle_fraction": {"per_stage": [round(x, 4) for x in idle],
-                              "mean": round(sum(idle) / len(idle), 4)},
-            "sequential_schedule_images_per_s": seq_ips,
-            "e2e": e2e, "roofline": roof, "roofline_optimizer": roof_extra,
-            "cpu_baseline": cpu,
-            "gpu_launches": int(launches_per_step * args.steps),
-            "clocks": clk.summary(),
-            "staleness": {str(k): v for k, v in sorted(met.staleness.items())},
-            "cost_model": cmodel,
-            "final_losses": [h[-1] for h in met.loss_history],
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    line = {
+        "metric": "images/sec training (device-timed) at 1/2/4/8 B200; pipeline idle fraction",
+        "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic (seeded N(0,1) CIFAR-shaped inputs, "
+        "uniform labels; random-init weights drawn like the reference)",
+        "config": cfg_dict(wl, args) | {"parallelism": "pp-streams"},
+        "idle_fraction": {"per_stage": [round(x, 4) for x in idle],
+                          "mean": round(sum(idle) / len(idle), 4)},
+        "sequential_schedule_images_per_s": seq_ips,
+        "e2e": e2e, "roofline": roof, "roofline_optimizer": roof_extra,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clk.summary(),
+        "staleness": {str(k): v for k, v in sorted(met.staleness.items())},
+        "cost_model": cmodel,
+        "step_budget": {"phases": ph, "total_steps": step_budget(ph), "used": used},
+        "final_losses": [h[-1] for h in met.loss_history],
+    }
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -134,8 +134,14 @@ class ResStage:
         return [a for _, _, a in self.param_list()]
 
 
-def build_resnet_stages(spec: ResNetSpec, s: int, d_prime: int, n_int: int, seed: int):
-    split = resnet_split(spec, s)
+def build_resnet_stages(spec: ResNetSpec, s: int, d_prime: int, n_int: int, seed: int,
+                        split=None):
+    """``split``: per stage the list of block indices (default: the even
+    ``resnet_split``; the product's cost-balanced split is passed in
+    explicitly by the tests that use it)."""
+    split = resnet_split(spec, s) if split is None else [list(b) for b in split]
+    if len(split) != s:
+        raise ValueError(f"split has {len(split)} stages, expected {s}")
     stages = []
     for j, blocks in enumerate(split):
         rng = np.random.default_rng(seed + j)

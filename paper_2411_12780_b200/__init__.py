@@ -81,7 +81,8 @@ from .costs import (
 from .harness import (CSV_HEADER, ComparisonReport, ExperimentConfig, MetricsRecord, ModeSummary,
                       build_pipeline, device_memory, estimate_k, evaluate, make_datasets,
                       report_table, run_experiment, validate_config, write_metrics_csv)
-from .vit import VitLocalModule, VitSpec, balanced_depths, build_vit_modules
+from .vit import (VitLocalModule, VitSpec, balanced_depths, balanced_vit_depths,
+                  build_vit_modules, vit_stage_costs)
 from .resnet import ResLocalModule, ResNetSpec, build_resnet_modules, resnet_split
 
 __version__ = "0.1.0"

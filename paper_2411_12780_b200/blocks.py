@@ -395,7 +395,7 @@ def _materialise(j, host, n_block, assigned, hidden, hyper, device):
         "lr": lr_table(sched, device),
         # [step_count, nesterov block-completion scratch, error word, pad]
         "state": torch.zeros(4, dtype=torch.int32, device=device),
-        "loss": torch.zeros(hyper.total_steps + 1, dtype=torch.float32, device=device),
+        "loss": torch.zeros(hyper.total_steps + 2, dtype=torch.float32, device=device),
     }
     layers, params, moms = [], [], []
     k = 0

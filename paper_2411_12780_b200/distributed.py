@@ -34,6 +34,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from .errors import WorkerPanic
 from .runtime import EpochMetrics, _capture
 
 _HANDLE = 64
@@ -164,6 +165,11 @@ class DistributedPipeline:
         self.graphs = {}
         self.graph_kernels = {}
         self.replayed_kernels = 0      # kernels launched through graph replays
+        # batches this pipeline has already moved: the ready flags and credit
+        # counters are never reset, so every run() continues the global batch
+        # sequence (seq = t + 1, credit >= t - M + 1 for the GLOBAL index t);
+        # restarting at 0 would let a consumer pass on the previous run's flags
+        self.batches_done = 0
         self._setup()
 
     # -- setup ---------------------------------------------------------------
@@ -259,6 +265,11 @@ class DistributedPipeline:
             g.replay()
         self.replayed_kernels += self.graph_kernels[key]
 
+    def _drain(self):
+        for st in self.streams.values():
+            st.synchronize()
+        self.src_stream.synchronize()
+
     # -- the epoch -------------------------------------------------------------
     def run(self, batches: Iterable | None, n_batches: int, batch_size: int) -> dict:
         """Enqueue ``n_batches`` batches through this rank's stages.  The rank
@@ -287,8 +298,15 @@ class DistributedPipeline:
         for st in self.streams.values():
             st.wait_stream(self.src_stream)
         m0 = self.mods.get(0)
-        for t in range(n_batches):
+        base = self.batches_done
+        for t_local in range(n_batches):
+            t = base + t_local                 # global batch index (flags / credits)
             slot = t % M
+            for j, m in self.mods.items():     # host-side twin of the device step guard
+                if m.optimizer.step_count + 1 > m.schedule.total_steps + 1:
+                    self._drain()
+                    raise WorkerPanic(j, f"StepOutOfRange: step {m.optimizer.step_count} > "
+                                         f"{m.schedule.total_steps}")
             if m0 is not None:
                 x, y = next(it)
                 xt = torch.as_tensor(x).reshape(B, -1)
@@ -342,12 +360,19 @@ class DistributedPipeline:
                 e.record(st)
                 t_end[j].append(e)
                 self.mods[j].optimizer.step_count += 1
-        for st in self.streams.values():
-            st.synchronize()
-        self.src_stream.synchronize()
+            self.batches_done = t + 1
+        self._drain()
         out = {"wall": 0.0, "busy": {}, "loss": {}, "errors": {}}
         for j, m in self.mods.items():
             out["errors"][j] = m.error_word()
+        if any(out["errors"].values()):
+            # resync the host step counters with the device ones, then surface
+            # the first failing local stage (runtime.py:400-402)
+            for j, m in self.mods.items():
+                m.optimizer.step_count = step0[j] + max(0, m.device_step() - step0[j])
+            for j, m in sorted(self.mods.items()):
+                m.raise_for_error(stage=j)
+        for j, m in self.mods.items():
             out["loss"][j] = m.loss_history(step0[j], n_batches)
             if n_batches:
                 out["busy"][j] = sum(a.elapsed_time(b) for a, b in zip(t_start[j], t_end[j])) / 1e3

@@ -307,7 +307,7 @@ def build_resnet_modules(spec: ResNetSpec, s: int, d_prime: int, n: int, hyper: 
         flat = {"theta": theta, "mom": mom, "grad": grad, "theta_lp": theta_lp, "offsets": nat,
                 "lr": lr_table(sched, device),
                 "state": torch.zeros(4, dtype=torch.int32, device=device),
-                "loss": torch.zeros(hyper.total_steps + 1, dtype=torch.float32, device=device)}
+                "loss": torch.zeros(hyper.total_steps + 2, dtype=torch.float32, device=device)}
         groups, moms = [], []
         for (g, k, a, _), o in zip(host, offsets):
             view = theta[o:o + a.size].view(a.shape)

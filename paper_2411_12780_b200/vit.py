@@ -97,6 +97,71 @@ def balanced_depths(depth: int, s: int) -> list:
     return [q + (1 if j < r else 0) for j in range(s)]
 
 
+def vit_layer_cost(spec: "VitSpec", first: bool = False) -> float:
+    """Training FLOPs of one transformer layer per image (forward, input
+    gradient, weight gradient).  ``first``: the block's first layer, whose
+    detached input needs no QKV input gradient (blocks.py:277-278)."""
+    T, D, F = spec.tokens, spec.dim, spec.mlp
+    fwd = 2.0 * T * (4 * D * D + 2 * D * F) + 4.0 * T * T * D
+    return 3.0 * fwd - (2.0 * T * D * 3 * D if first else 0.0)
+
+
+def balanced_vit_depths(spec: "VitSpec", s: int, d_prime: int, n: int,
+                        layer_cost: float | None = None, aux_cost: float | None = None,
+                        embed_cost: float | None = None) -> list:
+    """Contiguous split of the ``depth`` layers into ``s`` blocks minimising
+    the most expensive STAGE, each stage charged for its block layers, its
+    aux head (aux_depth(j, d', n) transformer layers, none on the final
+    stage, blocks.py:99-106,218-229) and the patch embedding on stage 0.
+    ``balanced_depths`` splits by depth only, which leaves the final stage
+    (no aux head) idle for a third of every cycle at d'=1; this split is what
+    the one-stage-per-GPU pipeline needs for an idle fraction under 10 %.
+
+    Like ``partition`` (blocks.py:75-96) it enumerates the cut positions in
+    ``itertools.combinations`` order and keeps the first strict minimum, so
+    ties go to the earliest cuts.  Costs default to the analytic training
+    FLOPs per image; pass measured ones (``calibrate``) to override."""
+    import itertools
+    if s < 1 or s > spec.depth:
+        raise ConfigMismatch(f"cannot split depth {spec.depth} into {s} blocks")
+    full = vit_layer_cost(spec) if layer_cost is None else layer_cost
+    first_saving = (vit_layer_cost(spec) - vit_layer_cost(spec, first=True)) * full \
+        / vit_layer_cost(spec)
+    aux = full if aux_cost is None else aux_cost
+    emb = (3.0 * 2.0 * spec.n_patches * spec.patch_dim * spec.dim
+           if embed_cost is None else embed_cost)
+
+    def stage_cost(j, n_layers):
+        c = n_layers * full - first_saving + (emb if j == 0 else 0.0)
+        if j < s - 1:
+            c += aux_depth(j, d_prime, n) * aux
+        return c
+
+    L = spec.depth
+    best, best_load = None, math.inf
+    for cuts in itertools.combinations(range(1, L), s - 1):
+        edges = (0,) + cuts + (L,)
+        load = max(stage_cost(j, b - a) for j, (a, b) in enumerate(zip(edges, edges[1:])))
+        if load < best_load * (1 - 1e-12):
+            best, best_load = edges, load
+    return [b - a for a, b in zip(best, best[1:])]
+
+
+def vit_stage_costs(spec: "VitSpec", depths: Sequence[int], d_prime: int, n: int) -> list:
+    """The analytic per-stage cost ``balanced_vit_depths`` minimises."""
+    s = len(depths)
+    full = vit_layer_cost(spec)
+    out = []
+    for j, dj in enumerate(depths):
+        c = (dj - 1) * full + vit_layer_cost(spec, first=True)
+        if j == 0:
+            c += 3.0 * 2.0 * spec.n_patches * spec.patch_dim * spec.dim
+        if j < s - 1:
+            c += aux_depth(j, d_prime, n) * full
+        out.append(c)
+    return out
+
+
 class VitLocalModule(LocalModule):
     """One ViT stage: [patch embed] + block layers + aux layers + head."""
 
@@ -247,7 +312,7 @@ def build_vit_modules(spec: VitSpec, depths: Sequence[int], d_prime: int, n: int
         flat = {"theta": theta, "mom": mom, "grad": grad, "theta_lp": theta_lp,
                 "offsets": native_offs, "lr": lr_table(sched, device),
                 "state": torch.zeros(4, dtype=torch.int32, device=device),
-                "loss": torch.zeros(hyper.total_steps + 1, dtype=torch.float32, device=device)}
+                "loss": torch.zeros(hyper.total_steps + 2, dtype=torch.float32, device=device)}
         groups, moms = [], []
         for (g, k, a), o in zip(host, offsets):
             view = theta[o:o + a.size].view(a.shape)

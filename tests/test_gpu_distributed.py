@@ -29,7 +29,7 @@ def _build(only=None, precision="bf16"):
     return lp.build_vit_modules(spec, [1, 1, 1, 1], 1, 2, hyper, only=only)
 
 
-def _rank(rank, world, port, precision, q):
+def _rank(rank, world, port, precision, q, chunks=(N_BATCHES,)):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     from paper_2411_12780_b200.distributed import (DistributedPipeline, gather_metrics,
@@ -41,8 +41,19 @@ def _rank(rank, world, port, precision, q):
         mine = [j for j in range(4) if placement[j] == rank]
         mods = _build(only=mine, precision=precision)
         pipe = DistributedPipeline(mods, placement, rank, None, capacity=2, max_batch=B)
-        res = pipe.run(iter(_data()) if rank == 0 else None, N_BATCHES, B)
-        met = gather_metrics(res, 4, N_BATCHES, N_BATCHES * B, None)
+        data = iter(_data())
+        hist = [[] for _ in range(4)]
+        errs = {}
+        # several run() calls continue one batch sequence (flags
+        # and credits carry over; 3 + 2 + 2 with M = 2 also shifts the slots)
+        for n in chunks:
+            res = pipe.run(data if rank == 0 else None, n, B)
+            met = gather_metrics(res, 4, n, n * B, None)
+            for j in range(4):
+                hist[j] += met.loss_history[j]
+            errs.update({k: errs.get(k, 0) | v for k, v in res["errors"].items()})
+        met.loss_history = hist
+        res = {"errors": errs}
         flat = {m.stage_index: np.concatenate([p.data.ravel() for p in m.parameters()])
                 for m in mods}
         q.put((rank, met.loss_history, flat, res["errors"]))
@@ -52,8 +63,9 @@ def _rank(rank, world, port, precision, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp32"])
-def test_two_process_ipc_pipeline_bitwise_equals_single_process(precision):
+@pytest.mark.parametrize("precision,chunks", [("bf16", (N_BATCHES,)), ("fp32", (N_BATCHES,)),
+                                              ("bf16", (3, 2, 2))])
+def test_two_process_ipc_pipeline_bitwise_equals_single_process(precision, chunks):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2411_12780_b200 as lp
@@ -64,8 +76,8 @@ def test_two_process_ipc_pipeline_bitwise_equals_single_process(precision):
                 for r in ref}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + os.getpid() % 500 + (7 if precision == "fp32" else 0)
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, precision, q)) for r in range(2)]
+    port = 29600 + os.getpid() % 500 + (7 if precision == "fp32" else 0) + 13 * len(chunks)
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, precision, q, chunks)) for r in range(2)]
     for p in procs:
         p.start()
     out = {}

@@ -1,0 +1,81 @@
+"""The torch-CPU restatement (oracle/torch_cpu.py, the ViT/ResNet CPU baseline
+of BASELINE.md §3) against the float64 numpy oracles: autograd vs the manual
+backward, same init, same step order — float64 to 1e-9, float32 to fp32
+rounding."""
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import ppll_oracle as orc
+import resnet_oracle as ro
+import torch_cpu as tc
+import vit_oracle as vo
+
+HP = (0.05, 0.001, 10, 0.9, 1e-4)
+
+
+def _run(stages, tstages, xs, ys, steps):
+    out = []
+    for t in range(steps):
+        h, ht = xs[t], xs[t]
+        for st, ts in zip(stages, tstages):
+            if isinstance(st, orc.OracleStage):
+                lo, h, _ = orc.local_step(st, h, ys[t], *HP)
+            elif isinstance(st, vo.VitStage):
+                lo, h, _ = vo.local_step(st, h, ys[t], *HP)
+            else:
+                lo, h, _ = ro.local_step(st, h, ys[t], *HP)
+            lt, ht, _ = tc.local_step(ts, ht, ys[t], *HP)
+            out.append((lo, lt, h, ht.numpy()))
+    return out
+
+
+def _check(stages, tstages, rtol):
+    for st, ts in zip(stages, tstages):
+        for p, q in zip(st.params(), ts.params):
+            q = q.detach().numpy()
+            assert p.shape == q.shape
+            assert np.max(np.abs(p - q)) <= rtol * max(1e-3, np.max(np.abs(p)))
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-9), (torch.float32, 2e-4)])
+def test_vit_restatement(dtype, tol):
+    spec = vo.VitSpec(image=8, channels=3, patch=4, dim=16, heads=2, mlp=32, depth=3, classes=5)
+    stages = vo.build_vit_stages(spec, [2, 1], 2, 1, 42)
+    tst = [tc.from_vit(copy.deepcopy(s), dtype) for s in stages]
+    rng = np.random.default_rng(0)
+    xs = rng.standard_normal((3, 4, 3, 8, 8))
+    ys = rng.integers(0, 5, (3, 4))
+    for lo, lt, h, ht in _run(stages, tst, xs, ys, 3):
+        assert abs(lo - lt) <= tol * max(1.0, abs(lo))
+        assert np.max(np.abs(h - ht)) <= tol * max(1.0, np.max(np.abs(h)))
+    _check(stages, tst, tol)
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-9), (torch.float32, 5e-4)])
+def test_resnet_restatement(dtype, tol):
+    spec = ro.ResNetSpec(n=1, image=8, channels=3, widths=(4, 8, 8), classes=5)
+    stages = ro.build_resnet_stages(spec, 2, 2, 1, 42, split=[[0, 1], [2]])
+    tst = [tc.from_resnet(copy.deepcopy(s), dtype) for s in stages]
+    rng = np.random.default_rng(1)
+    xs = rng.standard_normal((3, 4, 8, 8, 3))
+    ys = rng.integers(0, 5, (3, 4))
+    for lo, lt, h, ht in _run(stages, tst, xs, ys, 3):
+        assert abs(lo - lt) <= tol * max(1.0, abs(lo))
+        assert np.max(np.abs(h - ht)) <= tol * max(1.0, np.max(np.abs(h)))
+    _check(stages, tst, tol)
+
+
+def test_mlp_restatement():
+    dims = (12, 10, 9, 8, 5)
+    stages = orc.build_stages(dims, orc.partition(dims, 2), 2, 3, 42)
+    tst = [tc.from_mlp(copy.deepcopy(s), torch.float64) for s in stages]
+    rng = np.random.default_rng(2)
+    xs = rng.standard_normal((4, 6, 12))
+    ys = rng.integers(0, 5, (4, 6))
+    for lo, lt, h, ht in _run(stages, tst, xs, ys, 4):
+        assert abs(lo - lt) <= 1e-12
+        np.testing.assert_allclose(h, ht, rtol=0, atol=1e-12)
+    _check(stages, tst, 1e-12)
