@@ -131,6 +131,14 @@ double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps);
  * stride-1 convolutions (the extension family; no reference counterpart). */
 int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x, const void* w,
                       void* y, int dgrad, void* stream);
+/* The same convolution with the ResNet stage's fused epilogue:
+ * y = (conv + res) ⊙ [mask > 0] — res (same shape as y) and mask (the
+ * producing ReLU's output, same shape as y) may be NULL.  With dgrad = 1 this
+ * is the basic block's input-gradient epilogue: the shortcut gradient added
+ * and the previous ReLU's mask applied (blocks.py's backward of relu(bn(conv))
+ * + residual; resnet_stage.cu conv_bn_bwd). */
+int ppll_conv3x3_bf16_ex(int N, int H, int W, int Cin, int Cout, const void* x, const void* w,
+                         void* y, int dgrad, const void* res, const void* mask, void* stream);
 
 /* ---- data path / evaluation -------------------------------------------- */
 /* dst[r,:] = cast(src[idx[r],:]) for r < n (fp32 rows of `width` features,

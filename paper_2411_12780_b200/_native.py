@@ -39,6 +39,7 @@ SIGNATURES = {
     "ppll_cosine_lr": (_d, [_i, _d, _d, _i]),
     "ppll_cast": (_i, [_i64, _vp, _i, _vp, _i, _vp]),
     "ppll_conv3x3_bf16": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
+    "ppll_conv3x3_bf16_ex": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_gather_rows": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_gather_rows_u8": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_events_elapsed": (_i, [_i, _vp, C.c_uint64, _vp]),

@@ -347,14 +347,25 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
 
 }  // namespace ppll
 
-extern "C" int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x,
-                                 const void* w, void* y, int dgrad, void* stream) {
+extern "C" int ppll_conv3x3_bf16_ex(int N, int H, int W, int Cin, int Cout, const void* x,
+                                    const void* w, void* y, int dgrad, const void* res,
+                                    const void* mask, void* stream) {
   using namespace ppll;
   Epilogue<__nv_bfloat16> e;
   const int co = dgrad ? Cin : Cout, ci = dgrad ? Cout : Cin;
   e.C = (__nv_bfloat16*)y;
   e.ldc = co;
+  e.res = (const __nv_bfloat16*)res;
+  e.ldres = co;
+  e.mask = (const __nv_bfloat16*)mask;
+  e.ldmask = co;
+  e.mask_mode = mask ? kMaskRelu : kMaskNone;
   epilogue_finalize(e, co);
   return launch_conv3x3_tc(N, H, W, ci, co, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w,
                            dgrad != 0, e, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x,
+                                 const void* w, void* y, int dgrad, void* stream) {
+  return ppll_conv3x3_bf16_ex(N, H, W, Cin, Cout, x, w, y, dgrad, nullptr, nullptr, stream);
 }
