@@ -42,6 +42,8 @@ enum { PPLL_F32 = 0, PPLL_BF16 = 1 };
 #define PPLL_ERRBIT_LOSS 2    /* NonFiniteError   tensor.py:227     */
 #define PPLL_ERRBIT_PARAM 4   /* NonFiniteError   tensor.py:41-43   */
 #define PPLL_ERRBIT_STEP 8    /* StepOutOfRange   optim.py:41-42    */
+#define PPLL_ERRBIT_GRAD 16   /* NonFiniteError   tensor.py:41-43: a non-finite gradient;
+                                 the update is skipped (all-or-nothing) */
 
 /* GEMM engine selection for the bf16 path (PPLL_GEMM_AUTO picks tcgen05 when
  * the shape/alignment allows, else the SIMT kernel for skinny shapes). */
@@ -80,6 +82,21 @@ int ppll_linear_dgrad(int M, int K, int N, const void* dY, int lddy, const void*
  * adjoint g.sum(axis=0) (tensor.py:179). */
 int ppll_linear_wgrad(int M, int K, int N, const void* X, int ldx, const void* dY,
                       int lddy, float* dW, float* db, int dtype, void* stream);
+
+/* Tape primitives (the device GradTape of tensor.py; not the fused hot path).
+ * op 0 relu      out = max(a, 0)                 replaces relu      tensor.py:153-157
+ * op 1 relu_bwd  out = a · [b > 0] (g, x)        its adjoint (subgradient 0 at 0)
+ * op 2 bias_add  out[r,c] = a[r,c] + b[c]        replaces bias_add  tensor.py:170-180
+ * op 3 axpby     out = alpha·a + b (b nullable)  add :160-167, scale :183-191, _accumulate :128-132
+ * op 4 broadcast out[i] = alpha·a[0]             sum_all adjoint    tensor.py:194-198
+ * a/b/out are [rows, cols] of `dtype`; a non-finite output sets
+ * PPLL_ERRBIT_PARAM in *err (nullable) — _ensure_finite, tensor.py:41-43. */
+int ppll_ew(int op, int64_t rows, int64_t cols, const void* a, const void* b, float alpha,
+            void* out, int dtype, int* err, void* stream);
+/* out[c] = Σ_r g[r, c] in fp32 (the bias_add adjoint g.sum(axis=0), tensor.py:179) */
+int ppll_colsum(int rows, int cols, const void* g, float* out, int dtype, void* stream);
+/* *out = Σ x (fp32 result, fixed-order reduction): sum_all, tensor.py:194-198 */
+int ppll_sum_all(int64_t n, const void* x, float* out, int dtype, int* err, void* stream);
 
 /* Extended fused epilogues (the transformer-layer forms; same engines):
  *   fwd:   Y = act(X·W + b [+ R]);  act 0 none, 1 ReLU, 2 GELU(erf),

@@ -26,6 +26,8 @@ from .blocks import (
 )
 from .errors import (
     BadMagic,
+    EmptyTape,
+    NotScalar,
     ConfigMismatch,
     CountMismatch,
     DimensionMismatch,
@@ -59,7 +61,8 @@ from .runtime import (
     run_epoch,
     throughput,
 )
-from .tensor import Tensor, matmul, softmax_xent
+from .tensor import (GradTape, Tensor, active_tape, add, backward, backward_from, bias_add,
+                     matmul, relu, scale, softmax_xent, sum_all)
 from .data import (BatchIterator, Dataset, DeviceDataset, IdxDataset, batches, gen_blobs,
                    gen_spirals, load_idx, spiral_reference)
 from .costs import (

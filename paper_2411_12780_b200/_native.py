@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("PPLL_LIB") or os.path.join(_HERE, "lib", "libppll_b20
 
 PPLL_OK, PPLL_ERR_ARG, PPLL_ERR_CUDA, PPLL_ERR_UNSUPPORTED, PPLL_ERR_CLOSED = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1
-ERRBIT_LABEL, ERRBIT_LOSS, ERRBIT_PARAM, ERRBIT_STEP = 1, 2, 4, 8
+ERRBIT_LABEL, ERRBIT_LOSS, ERRBIT_PARAM, ERRBIT_STEP, ERRBIT_GRAD = 1, 2, 4, 8, 16
 GEMM_AUTO, GEMM_SIMT, GEMM_TCGEN05 = 0, 1, 2
 
 _vp, _i, _i64, _f, _d, _u64 = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_double, C.c_uint64
@@ -38,6 +38,9 @@ SIGNATURES = {
     "ppll_nesterov_step": (_i, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _i, _f, _f, _f, _vp, _vp]),
     "ppll_cosine_lr": (_d, [_i, _d, _d, _i]),
     "ppll_cast": (_i, [_i64, _vp, _i, _vp, _i, _vp]),
+    "ppll_ew": (_i, [_i, _i64, _i64, _vp, _vp, _f, _vp, _i, _vp, _vp]),
+    "ppll_colsum": (_i, [_i, _i, _vp, _vp, _i, _vp]),
+    "ppll_sum_all": (_i, [_i64, _vp, _vp, _i, _vp, _vp]),
     "ppll_conv3x3_bf16": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
     "ppll_conv3x3_bf16_ex": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_gather_rows": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),

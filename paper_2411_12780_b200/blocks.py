@@ -306,7 +306,7 @@ class LocalModule:
         self.clear_error()
         if e & N.ERRBIT_LABEL:
             exc = LabelOutOfRange("labels must lie in [0, num_classes)")
-        elif e & (N.ERRBIT_LOSS | N.ERRBIT_PARAM):
+        elif e & (N.ERRBIT_LOSS | N.ERRBIT_PARAM | N.ERRBIT_GRAD):
             exc = NonFiniteError("local step produced non-finite values")
         else:
             exc = StepOutOfRange(f"step outside [0, {self.schedule.total_steps}]")

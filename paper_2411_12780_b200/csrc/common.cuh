@@ -16,6 +16,7 @@ enum ErrBits : int {
   kErrLossNonFinite = PPLL_ERRBIT_LOSS,   // NonFiniteError    (tensor.py:227)
   kErrParamNonFinite = PPLL_ERRBIT_PARAM, // NonFiniteError    (tensor.py:41-43)
   kErrStep = PPLL_ERRBIT_STEP,            // StepOutOfRange    (optim.py:41-42)
+  kErrGradNonFinite = PPLL_ERRBIT_GRAD,   // NonFiniteError    (tensor.py:41-43, pre-update)
 };
 
 void set_error(const char* fmt, ...);

@@ -505,7 +505,7 @@ nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const flo
   if (threadIdx.x == 0) {
     int e = err ? *(volatile int*)err : 0;
     int st = step ? *(volatile int*)step : 0;
-    int skip = (e & (kErrLabel | kErrLossNonFinite)) ? 1 : 0;
+    int skip = (e & (kErrLabel | kErrLossNonFinite | kErrGradNonFinite)) ? 1 : 0;
     if (step && (st < 0 || st > max_step)) {
       skip = 1;
       if (err) atomicOr(err, kErrStep);
@@ -566,6 +566,28 @@ nesterov_kernel(long n, float* __restrict__ th, float* __restrict__ v, const flo
   }
 }
 
+// All-or-nothing guard in front of the update: the reference raises
+// NonFiniteError inside the forward/backward (tensor.py:41-43, called from
+// every primitive) BEFORE sgd_nesterov_step runs, so a non-finite value never
+// reaches the parameters.  The device step cannot raise mid-graph; instead one
+// pass over the gradient sets PPLL_ERRBIT_GRAD and the Nesterov kernel skips
+// the whole update (a NaN input can be squashed by ReLU = fmaxf on the way to
+// the loss, but it always reaches dW = Xᵀ·G).
+__global__ void __launch_bounds__(256)
+grad_finite_kernel(long n, const float* __restrict__ g, int* err) {
+  pdl_entry();
+  bool bad = false;
+  const long n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    const float4 q = g4[i];
+    bad |= !(isfinite(q.x) & isfinite(q.y) & isfinite(q.z) & isfinite(q.w));
+  }
+  for (long i = n4 * 4 + (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    bad |= !isfinite(g[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, kErrGradNonFinite);
+}
+
 int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* th_lp,
                     const float* lr_table, int* step, int max_step, float lr_host, float mu,
                     float wd, int* err, cudaStream_t s, bool advance) {
@@ -580,6 +602,11 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
   }
   // step points to two int32 words: [step_count, block-completion scratch]
   unsigned int* done = step ? reinterpret_cast<unsigned int*>(step + 1) : nullptr;
+  if (err && step && n > 0) {
+    launch_k(grad_finite_kernel, blocks, 256, 0, s, n, g, err);
+    note_launch();
+    PPLL_LAUNCH_CHECK();
+  }
   launch_k(nesterov_kernel, blocks, 256, 0, s, n, th, v, g, th_lp, lr_table, step, max_step, lr_host,
                                          mu, wd, err, done, advance ? 1 : 0);
   note_launch();

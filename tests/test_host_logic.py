@@ -188,3 +188,26 @@ def test_balanced_resnet_split_is_contiguous_and_minimax():
         assert all(len(blk) >= 1 for blk in b[1:])
     # the high-resolution early blocks are spread thinner than the even split
     assert len(balanced_resnet_split(ResNetSpec(), 4, 1, 3)[0]) < len(resnet_split(ResNetSpec(), 4)[0])
+
+
+def test_balanced_vit_depths_minimax_earliest_cut_and_idle():
+    """Cost-balanced ViT split: brute-force minimax over
+    every contiguous split, earliest cut on ties, and the predicted
+    one-stage-per-GPU idle fraction < 10 % for the bench configs at d'=1."""
+    import itertools
+    from paper_2411_12780_b200.vit import VitSpec, balanced_vit_depths, vit_stage_costs
+    vit_s = VitSpec()
+    vit_b = VitSpec(image=96, patch=16, dim=768, heads=12, mlp=3072, depth=12)
+    for spec, s in ((vit_s, 4), (vit_b, 8), (vit_s, 2), (vit_b, 4)):
+        for d in (1, 2, 4):
+            got = balanced_vit_depths(spec, s, d, 3)
+            assert sum(got) == spec.depth and min(got) >= 1
+            best = min(max(vit_stage_costs(spec, [b - a for a, b in zip((0,) + c, c + (spec.depth,))],
+                                           d, 3))
+                       for c in itertools.combinations(range(1, spec.depth), s - 1))
+            assert max(vit_stage_costs(spec, got, d, 3)) <= best * (1 + 1e-9)
+    for spec, s, want in ((vit_s, 4, [1, 2, 2, 3]), (vit_b, 8, [1, 1, 1, 1, 2, 2, 2, 2])):
+        got = balanced_vit_depths(spec, s, 1, 3)
+        assert got == want
+        c = vit_stage_costs(spec, got, 1, 3)
+        assert sum(1 - x / max(c) for x in c) / s < 0.10
