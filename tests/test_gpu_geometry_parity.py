@@ -21,8 +21,14 @@ unstepped one, because 3 steps move the weights by only ~4 % of max|W|):
 * x_out (the pushed boundary activation), max-abs error over max|ref| (XOUT_TOL).
 
 Tolerances: bf16 tensor-core operands (8-bit mantissa, 2^-9 relative
-rounding) with fp32 accumulation, bf16-stored activations; the bars below are
-~3x the errors measured on a B200 (profiles/r02_geometry_parity.json).
+rounding) with fp32 accumulation, bf16-stored activations.  ViT: the bars are
+~3x the errors measured on a B200 (profiles/r02_geometry_parity.json: loss
+2e-3, x_out 1.1e-2, dθ 0.7 % per stage).  ResNet: train-mode BatchNorm makes
+bf16 rounding grow with depth (the 12-conv final stage's dθ is ~11 % off the
+float64 update, the BN γ/β updates 20-25 %), so the bar is the bf16 NOISE
+FLOOR itself: the same 5 steps in torch-CPU with bf16 autocast (convs in bf16,
+BN/loss/update in fp32) give the same errors against float64, and the device
+must stay within 1.3x of that floor (+0.01) on every stage.
 """
 import copy
 import json
@@ -41,10 +47,10 @@ pytestmark = pytest.mark.gpu
 
 STEPS = 5
 HP = dict(lr0=0.05, lr_min=0.001)
-LOSS_TOL = 5e-3
+LOSS_TOL = 6e-3
 XOUT_TOL = 3e-2
-DTHETA_TOL = 6e-2
-DTHETA_TENSOR_TOL = 0.15
+DTHETA_TOL = 2.5e-2
+DTHETA_TENSOR_TOL = 4e-2
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
 
 
@@ -64,8 +70,11 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def _run(mods, tstages, xs, ys, tag):
-    """5 teacher-forced bf16 steps; returns the measured error summary."""
+def _run(mods, tstages, xs, ys, tag, emulated=None, tol=None):
+    """5 teacher-forced bf16 steps; returns the measured error summary.
+    ``emulated``: fp32 TorchStages stepped under bf16 autocast on the same
+    inputs (the bf16 noise floor, see the module docstring)."""
+    tol = tol or {}
     th0_dev = [_dev_params(m) for m in mods]
     th0_ref = [[p.detach().numpy().copy() for p in ts.params] for ts in tstages]
     for a, b in zip(th0_dev, th0_ref):               # same init (fp32 rounding)
@@ -80,6 +89,10 @@ def _run(mods, tstages, xs, ys, tag):
             loss, h = lp.local_loss_and_update(m, h, ys[t])
             ref, hr, _ = tc.local_step(ts, torch.as_tensor(x_ref, dtype=torch.float64), ys[t],
                                        HP["lr0"], HP["lr_min"], STEPS, 0.9, 1e-4)
+            if emulated is not None:
+                with torch.autocast("cpu", dtype=torch.bfloat16):
+                    tc.local_step(emulated[j], torch.as_tensor(x_ref, dtype=torch.float32), ys[t],
+                                  HP["lr0"], HP["lr_min"], STEPS, 0.9, 1e-4)
             hd = h.data.astype(np.float64)
             rep["loss_rel"].append(abs(loss - ref) / abs(ref))
             rep["xout_rel"].append(float(np.abs(hd - hr.numpy()).max() / np.abs(hr.numpy()).max()))
@@ -89,6 +102,9 @@ def _run(mods, tstages, xs, ys, tag):
         d_ref = [p.detach().numpy() - a for a, p in zip(th0_ref[j], ts.params)]
         cat = lambda L: np.concatenate([x.ravel() for x in L])  # noqa: E731
         rep["dtheta_stage"].append(_rel(cat(d_dev), cat(d_ref)))
+        if emulated is not None:
+            d_emu = [p.detach().double().numpy() - a for a, p in zip(th0_ref[j], emulated[j].params)]
+            rep.setdefault("dtheta_bf16_floor", []).append(_rel(cat(d_emu), cat(d_ref)))
         moved = [(_rel(a, b), np.linalg.norm(b)) for a, b in zip(d_dev, d_ref)]
         big = max(n for _, n in moved)
         rep["dtheta_worst_tensor"].append(max(r for r, n in moved if n > 1e-3 * big))
@@ -97,10 +113,14 @@ def _run(mods, tstages, xs, ys, tag):
     data = json.load(open(path)) if os.path.exists(path) else {}
     data[tag] = {k: (max(v) if v else None) for k, v in rep.items()} | {"per_stage": rep}
     json.dump(data, open(path, "w"), indent=1)
-    assert max(rep["loss_rel"]) <= LOSS_TOL, rep["loss_rel"]
-    assert max(rep["xout_rel"]) <= XOUT_TOL, rep["xout_rel"]
-    assert max(rep["dtheta_stage"]) <= DTHETA_TOL, rep["dtheta_stage"]
-    assert max(rep["dtheta_worst_tensor"]) <= DTHETA_TENSOR_TOL, rep["dtheta_worst_tensor"]
+    assert max(rep["loss_rel"]) <= tol.get("loss", LOSS_TOL), rep["loss_rel"]
+    assert max(rep["xout_rel"]) <= tol.get("xout", XOUT_TOL), rep["xout_rel"]
+    assert max(rep["dtheta_stage"]) <= tol.get("dtheta", DTHETA_TOL), rep["dtheta_stage"]
+    assert max(rep["dtheta_worst_tensor"]) <= tol.get("tensor", DTHETA_TENSOR_TOL), \
+        rep["dtheta_worst_tensor"]
+    if emulated is not None:
+        for got, floor in zip(rep["dtheta_stage"], rep["dtheta_bf16_floor"]):
+            assert got <= 1.3 * floor + 0.01, (rep["dtheta_stage"], rep["dtheta_bf16_floor"])
     # the update is real: every stage moved and the check would catch "no step"
     assert all(r < 0.5 for r in rep["dtheta_stage"])
 
@@ -129,12 +149,14 @@ def test_resnet32_bench_config_bf16_update_parity():
     hyper = lp.Hyperparams(total_steps=STEPS, seed=42, precision="bf16", **HP)
     mods = lp.build_resnet_modules(spec, 4, 1, 3, hyper, split=split)
     stages = ro.build_resnet_stages(ro.ResNetSpec(**kw), 4, 1, 3, 42, split=split)
-    tst = [tc.from_resnet(s, torch.float64) for s in stages]
+    tst = [tc.from_resnet(copy.deepcopy(s), torch.float64) for s in stages]
+    emu = [tc.from_resnet(copy.deepcopy(s), torch.float32) for s in stages]
     rng = np.random.default_rng(12)
     B = 128
     xs = rng.standard_normal((STEPS, B, 32, 32, 3)).astype(np.float32)
     ys = rng.integers(0, 10, (STEPS, B))
-    _run(mods, tst, xs, ys, "resnet32_b128_bf16")
+    _run(mods, tst, xs, ys, "resnet32_b128_bf16", emulated=emu,
+         tol={"loss": 2e-3, "xout": 6e-2, "dtheta": 0.15, "tensor": 0.35})
 
 
 @pytest.mark.parametrize("C", [16, 32, 64])
@@ -218,3 +240,30 @@ def test_nan_input_raises_nonfinite_and_skips_update(family):
         lp.run_epoch(lp.RunMode.PPLL, mods, iter([(x, y), (bad, y)]),
                      lp.RunConfig(buffer_capacity=2))
     assert ei.value.stage_index == 0
+
+
+@pytest.mark.parametrize("family", ["vit", "resnet"])
+def test_bench_config_fp32_update_parity(family):
+    """The same 5 steps in the fp32 parity mode: with no bf16 rounding the
+    device update matches the float64 one to fp32 precision at the full
+    geometry — the algorithm (not just its bf16 noise) is the reference's."""
+    rng = np.random.default_rng(13)
+    hyper = lp.Hyperparams(total_steps=STEPS, seed=42, precision="fp32", **HP)
+    if family == "vit":
+        kw = dict(image=32, channels=3, patch=4, dim=384, heads=6, mlp=1536, depth=8, classes=10)
+        depths = lp.balanced_vit_depths(lp.VitSpec(**kw), 4, 1, 3)
+        mods = lp.build_vit_modules(lp.VitSpec(**kw), depths, 1, 3, hyper)
+        tst = [tc.from_vit(s, torch.float64)
+               for s in vo.build_vit_stages(vo.VitSpec(**kw), depths, 1, 3, 42)]
+        xs = rng.standard_normal((STEPS, 128, 3, 32, 32)).astype(np.float32)
+    else:
+        from paper_2411_12780_b200.resnet import balanced_resnet_split
+        kw = dict(n=5, image=32, channels=3, widths=(16, 32, 64), classes=10)
+        split = balanced_resnet_split(lp.ResNetSpec(**kw), 4, 1, 3)
+        mods = lp.build_resnet_modules(lp.ResNetSpec(**kw), 4, 1, 3, hyper, split=split)
+        tst = [tc.from_resnet(s, torch.float64)
+               for s in ro.build_resnet_stages(ro.ResNetSpec(**kw), 4, 1, 3, 42, split=split)]
+        xs = rng.standard_normal((STEPS, 128, 32, 32, 3)).astype(np.float32)
+    ys = rng.integers(0, 10, (STEPS, 128))
+    _run(mods, tst, xs, ys, f"{family}_b128_fp32",
+         tol={"loss": 1e-5, "xout": 1e-4, "dtheta": 2e-3, "tensor": 1e-2})
