@@ -413,14 +413,19 @@ def run_sharded(args, wl, rank, world, local, dev):
     e2e_dt = max(dts)
     launch_counts = [None] * world
     dist.all_gather_object(launch_counts, launches)
+    xfer = _guard("boundary_transfer", boundary_transfer, pipe, mods, placement, rank, world, B,
+                  dev)
+    seq = None
+    if rank == 0:
+        seq = _guard("sequential_same_split", sequential_same_split, args, wl, s, dev, 40)
     roof = None
     if rank == 0:   # the dominant kernel, timed alone on rank 0's GPU (same as N = 1)
         hbm, tf_burst, _, peak_kind = peaks()
         if wl["kind"] == "vit":
-            roof = roofline_gemm(wl, tf_burst, hbm, dev)
+            roof = _guard("roofline_gemm", roofline_gemm, wl, tf_burst, hbm, dev)
         elif wl["kind"] == "resnet" and args.precision == "bf16":
-            roof = roofline_conv(wl, tf_burst, hbm, dev)
-        if roof is not None:
+            roof = _guard("roofline_conv", roofline_conv, wl, tf_burst, hbm, dev)
+        if isinstance(roof, dict):
             roof["peak_kind"] = peak_kind
     if rank == 0:
         line = {
@@ -431,7 +436,7 @@ def run_sharded(args, wl, rank, world, local, dev):
             "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (seeded N(0,1) CIFAR-shaped inputs, uniform labels; "
                     "random-init weights drawn like the reference)",
-            "config": cfg_dict(wl, args) | {
+            "config": cfg_dict(dict(wl, s=s), args) | {
                 "global_batch": B, "stages": s, "placement": f"stage->rank {placement}",
                 "parallelism": f"pp{world} (PPLL stages sharded over GPUs; CUDA-IPC rings, "
                                f"producer epilogue stores over NVLink)"},
@@ -442,6 +447,8 @@ def run_sharded(args, wl, rank, world, local, dev):
                     "d2h_bytes_per_step": 4 * s,
                     "api": "DistributedPipeline.run on pinned host batches (rank 0 H2D)"},
             "roofline": roof, "cpu_baseline": None,
+            "sequential_same_split": seq,
+            "boundary_transfer": xfer,
             "gpu_launches": int(sum(launch_counts)),
             "clocks": clk.summary(),
             "stage_errors": errs,
@@ -451,6 +458,130 @@ def run_sharded(args, wl, rank, world, local, dev):
     dist.barrier()
     pipe.close()
     dist.destroy_process_group()
+
+
+def boundary_transfer(pipe, mods, placement, rank, world, B, dev, reps=50):
+    """Queue-transfer evidence for the N > 1 line (north_star: "NVLink GB/s for
+    queue transfers"; SURVEY §8e baseline "ncclSend/ncclRecv on a comm
+    stream").  For every cross-rank boundary j -> j+1 the producer moves one
+    ring slot's payload (B x features activation + B int64 labels) to the
+    consumer's ring, all boundaries concurrently, ``reps`` times:
+      * ``p2p_ring``: a copy into the consumer's CUDA-IPC-mapped slot (the
+        path the pipeline's fused epilogue stores take, over NVLink);
+      * ``nccl``: torch.distributed NCCL isend/irecv of the same bytes (the
+        baseline), through a separate NCCL group.
+    Device-timed with CUDA events, max over ranks; GB/s per boundary."""
+    import torch
+    import torch.distributed as dist
+    from paper_2411_12780_b200 import _native as N
+    lib = N.load()
+    s = len(placement)
+    cross = [j for j in range(s - 1) if placement[j] != placement[j + 1]]
+    if not cross:
+        return None
+    feat = {}
+    for j in cross:
+        if placement[j] == rank:
+            feat[j] = mods_by_stage(mods)[j].out_features
+    sizes = [None] * world
+    dist.all_gather_object(sizes, feat)
+    allfeat = {}
+    for d in sizes:
+        allfeat.update(d)
+    esz = 2 if mods[0].precision == "bf16" else 4
+    nbytes = {j: B * allfeat[j] * esz + 8 * B for j in cross}
+    out = {"boundaries": cross, "bytes_per_boundary": nbytes, "reps": reps}
+    st = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        fn()                                                  # warm-up
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        b.synchronize()
+        t = [None] * world
+        dist.all_gather_object(t, a.elapsed_time(b) / 1e3)
+        return max(t)
+
+    # (1) the IPC ring: producer copies into the peer-mapped slot
+    src = {j: torch.empty(nbytes[j], dtype=torch.uint8, device=dev)
+           for j in cross if placement[j] == rank}
+
+    def p2p():
+        for j, buf in src.items():
+            N.check(lib.ppll_copy_async(pipe.x_peer[j + 1], buf.data_ptr(), nbytes[j],
+                                        st.cuda_stream), "p2p copy")
+    try:
+        t = timed(p2p)
+        out["p2p_ring"] = {"seconds": t, "GBps_per_boundary": {
+            str(j): nbytes[j] * reps / t / 1e9 for j in cross},
+            "path": "cudaMemcpyAsync into the consumer's CUDA-IPC-mapped ring slot"}
+    except Exception as e:                                     # noqa: BLE001
+        out["p2p_ring"] = {"error": f"{type(e).__name__}: {e}"}
+    # (2) the NCCL baseline
+    try:
+        g = dist.new_group(backend="nccl")
+        dst = {j: torch.empty(nbytes[j], dtype=torch.uint8, device=dev)
+               for j in cross if placement[j + 1] == rank}
+
+        def nccl():
+            ops = []
+            for j in cross:
+                if placement[j] == rank:
+                    ops.append(dist.P2POp(dist.isend, src[j], placement[j + 1], g))
+                if placement[j + 1] == rank:
+                    ops.append(dist.P2POp(dist.irecv, dst[j], placement[j], g))
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+        t = timed(nccl)
+        out["nccl_sendrecv"] = {"seconds": t, "GBps_per_boundary": {
+            str(j): nbytes[j] * reps / t / 1e9 for j in cross},
+            "path": "torch.distributed batch_isend_irecv over an NCCL group"}
+    except Exception as e:                                     # noqa: BLE001
+        out["nccl_sendrecv"] = {"error": f"{type(e).__name__}: {e}"}
+    return out
+
+
+def mods_by_stage(mods):
+    return {m.stage_index: m for m in mods}
+
+
+def sequential_same_split(args, wl, s, dev, steps):
+    """The paper's S=1 reference for the SAME s-stage split the sharded run
+    uses (all stages on one stream of rank 0's GPU): the speed-up at N GPUs is
+    value / this, model split held fixed (an s=8 sequential
+    baseline whenever N=8 switches to LPP)."""
+    import torch
+    import paper_2411_12780_b200 as lp
+    wl_s = dict(wl, s=s)
+    mods = build(wl_s, args.precision, dev, steps + 16)
+    B = wl["batch"]
+    in_shape = tuple(mods[0].in_shape)
+    gen = torch.Generator(device=dev).manual_seed(99)
+    pool_x = torch.randn((8, B) + in_shape, device=dev, generator=gen)
+    pool_y = torch.randint(0, mods[-1].num_classes, (8, B), device=dev, generator=gen)
+    seq = lp.DevicePipeline(mods, lp.RunConfig(buffer_capacity=args.capacity,
+                                               use_graphs=not args.no_graphs, timing=False))
+    cur = torch.cuda.current_stream(dev)
+    seq.streams = [cur] * len(mods)
+    seq.src_stream = cur
+    seq.run((pool_x[i % 8], pool_y[i % 8]) for i in range(3))
+    torch.cuda.synchronize(dev)
+    n = max(10, steps - 3)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    seq.run((pool_x[i % 8], pool_y[i % 8]) for i in range(n))
+    b.record()
+    b.synchronize()
+    for m in mods:
+        m.close()
+    return {"images_per_s": n * B / (a.elapsed_time(b) * 1e-3), "stages": s,
+            "placement": "all stages on one stream of rank 0's GPU"}
 
 
 def _time_kernel(fn, dev, reps=20):

@@ -93,3 +93,26 @@ def test_two_process_ipc_pipeline_bitwise_equals_single_process(precision, chunk
         assert all(e == 0 for e in out[r][2].values())
         for j, f in out[r][1].items():
             assert np.array_equal(f, ref_flat[j]), (r, j)
+
+
+def test_single_process_pipeline_across_two_devices_bitwise():
+    """DevicePipeline with stages on cuda:0 and cuda:1 (peer access, the
+    producer's epilogue storing into the peer's ring slot, cross-device
+    events) equals the one-device pipeline bitwise.  Needs two GPUs; gpurun
+    boxes have one, the driver's 8-GPU node runs it."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two CUDA devices")
+    import paper_2411_12780_b200 as lp
+    spec = lp.VitSpec(**SPEC)
+
+    def build(devs):
+        hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=20, seed=3, precision="bf16")
+        return lp.build_vit_modules(spec, [1, 1, 1, 1], 1, 2, hyper, devices=devs)
+    one = build(["cuda:0"] * 4)
+    two = build(["cuda:0", "cuda:0", "cuda:1", "cuda:1"])
+    m1 = lp.run_epoch(lp.RunMode.PPLL, one, iter(_data()), lp.RunConfig(buffer_capacity=2))
+    m2 = lp.run_epoch(lp.RunMode.PPLL, two, iter(_data()), lp.RunConfig(buffer_capacity=2))
+    assert m1.loss_history == m2.loss_history
+    for a, b in zip(one, two):
+        assert np.array_equal(np.concatenate([p.data.ravel() for p in a.parameters()]),
+                              np.concatenate([p.data.ravel() for p in b.parameters()]))
