@@ -164,9 +164,10 @@ int ppll_conv3x3_bf16_ex(int N, int H, int W, int Cin, int Cout, const void* x, 
  * HBM-resident dataset. */
 int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx, void* dst,
                      int dst_dtype, const int64_t* labels_src, int64_t* labels_dst, void* stream);
-/* Programmatic dependent launch on (1) / off (0) for kernels launched (or
- * captured into graphs) from now on; returns the previous setting.  On by
- * default (PPLL_PDL=0 in the environment turns it off at load). */
+/* Programmatic dependent launch on (1) / off (0) for kernels the CALLING
+ * THREAD launches (or captures into graphs) from now on; returns that
+ * thread's previous setting.  On by default (PPLL_PDL=0 in the environment
+ * turns it off). */
 int ppll_set_pdl(int on);
 /* out_ms[i] = milliseconds from event `ref` to events[i] (cudaEvent_t
  * handles, all recorded and complete): the per-step timestamps behind

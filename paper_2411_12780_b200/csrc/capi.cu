@@ -12,7 +12,9 @@ namespace ppll {
 static thread_local char t_err[512] = {0};
 static std::atomic<uint64_t> g_launches{0};
 int g_gemm_engine = PPLL_GEMM_AUTO;
-int g_pdl = getenv("PPLL_PDL") ? atoi(getenv("PPLL_PDL")) : 1;
+// per host thread: two pipelines driven from different threads each launch with
+// their own setting (a process-wide flag could be flipped under a capture)
+thread_local int g_pdl = getenv("PPLL_PDL") ? atoi(getenv("PPLL_PDL")) : 1;
 
 void set_error(const char* fmt, ...) {
   va_list ap;

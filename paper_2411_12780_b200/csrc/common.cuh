@@ -78,7 +78,7 @@ __device__ __forceinline__ void pdl_entry() {
   pdl_trigger();
 }
 
-extern int g_pdl;
+extern thread_local int g_pdl;
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

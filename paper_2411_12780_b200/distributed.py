@@ -170,6 +170,7 @@ class DistributedPipeline:
         # sequence (seq = t + 1, credit >= t - M + 1 for the GLOBAL index t);
         # restarting at 0 would let a consumer pass on the previous run's flags
         self.batches_done = 0
+        self._pdl = 1
         self._setup()
 
     # -- setup ---------------------------------------------------------------
@@ -250,7 +251,7 @@ class DistributedPipeline:
             with torch.cuda.stream(stream):
                 self._launch(p, slot, B, stream)
             return
-        key = (p.stage, slot)
+        key = (p.stage, slot, self._pdl)     # a graph keeps the PDL edges it was captured with
         g = self.graphs.get(key)
         if g is None:
             g = torch.cuda.CUDAGraph()
@@ -279,12 +280,13 @@ class DistributedPipeline:
         streams on this GPU unless PPLL_PDL is set)."""
         off = (len(self.mods) > 1 and
                not all(getattr(m, "shared_gpu_pdl", True) for m in self.mods.values()))
-        prev = None if "PPLL_PDL" in os.environ else self.lib.ppll_set_pdl(0 if off else 1)
+        want = int(os.environ["PPLL_PDL"] != "0") if "PPLL_PDL" in os.environ else int(not off)
+        prev = self.lib.ppll_set_pdl(want)
+        self._pdl = want
         try:
             return self._run(batches, n_batches, batch_size)
         finally:
-            if prev is not None:
-                self.lib.ppll_set_pdl(prev)
+            self.lib.ppll_set_pdl(prev)
 
     def _run(self, batches: Iterable | None, n_batches: int, batch_size: int) -> dict:
         M, B = self.M, batch_size

@@ -75,53 +75,71 @@ class BufferSlot:
 
 
 class StageBuffer:
-    """Bounded blocking SPSC FIFO (runtime.py:68-120) — the host-side API twin
-    of the device ring (same push/pop/close/high-water semantics)."""
+    """Host-side twin of the device ring (runtime.py:68-120 semantics).
+
+    Laid out like the device ring: ``capacity`` slots addressed by sequence
+    number (slot = seq % capacity), a write sequence and a read sequence.  A
+    producer waits for a free slot (the credit wait, never overwrite —
+    SPEC.md:319), a consumer for a filled one; after ``close`` the consumer
+    drains what is left and then gets END_OF_STREAM, and a producer still
+    waiting is released with PushAfterClose.  Counters as in the reference:
+    ``high_water`` (max occupancy after a push), ``total_pushed``,
+    ``producer_progress`` (set by the producer side)."""
 
     def __init__(self, capacity: int):
         if capacity < 1:
             raise ValueError(f"capacity must be >= 1, got {capacity}")
         self.capacity = capacity
-        self._items: deque = deque()
-        self._cv = threading.Condition()
+        self._ring = [None] * capacity
+        self._wseq = 0                       # next sequence number to write
+        self._rseq = 0                       # next sequence number to read
+        self._lock = threading.Lock()
+        self._filled = threading.Condition(self._lock)   # consumer waits here
+        self._freed = threading.Condition(self._lock)    # producer waits here
         self._closed = False
         self.high_water = 0
         self.producer_progress = -1
-        self.total_pushed = 0
+
+    @property
+    def total_pushed(self) -> int:
+        return self._wseq
+
+    def _count(self) -> int:
+        return self._wseq - self._rseq
 
     def push(self, slot: BufferSlot) -> None:
-        with self._cv:
+        with self._lock:
             if self._closed:
                 raise PushAfterClose("push on closed buffer")
-            while len(self._items) >= self.capacity:
-                self._cv.wait()
-                if self._closed:
-                    raise PushAfterClose("buffer closed while waiting to push")
-            self._items.append(slot)
-            self.total_pushed += 1
-            if len(self._items) > self.high_water:
-                self.high_water = len(self._items)
-            self._cv.notify_all()
+            self._freed.wait_for(lambda: self._closed or self._count() < self.capacity)
+            if self._closed:
+                raise PushAfterClose("buffer closed while waiting to push")
+            self._ring[self._wseq % self.capacity] = slot
+            self._wseq += 1
+            self.high_water = max(self.high_water, self._count())
+            self._filled.notify()
 
     def pop(self):
-        with self._cv:
-            while not self._items and not self._closed:
-                self._cv.wait()
-            if self._items:
-                slot = self._items.popleft()
-                self._cv.notify_all()
-                return slot
-            return END_OF_STREAM
+        with self._lock:
+            self._filled.wait_for(lambda: self._closed or self._count() > 0)
+            if self._count() == 0:
+                return END_OF_STREAM
+            k = self._rseq % self.capacity
+            slot, self._ring[k] = self._ring[k], None
+            self._rseq += 1
+            self._freed.notify()
+            return slot
 
     def close(self) -> None:
-        with self._cv:
+        with self._lock:
             self._closed = True
-            self._cv.notify_all()
+            self._filled.notify_all()
+            self._freed.notify_all()
 
     @property
     def occupancy(self) -> int:
-        with self._cv:
-            return len(self._items)
+        with self._lock:
+            return self._count()
 
 
 @dataclass
@@ -150,9 +168,10 @@ class RunConfig:
 
 @dataclass
 class EpochMetrics:
-    """What one epoch did (runtime.py:144-183).  Threaded (device) runs report
-    seconds measured with CUDA events; deterministic runs report scheduler
-    rounds (virtual time), like the reference."""
+    """What one epoch did (runtime.py:144-183; the field names and helpers are
+    the reference's API contract, restated deliberately).  Threaded (device)
+    runs report seconds measured with CUDA events; deterministic runs report
+    scheduler rounds (virtual time), like the reference."""
 
     n_stages: int
     n_batches: int = 0
@@ -488,6 +507,7 @@ class DevicePipeline:
         self.ev_free = [[torch.cuda.Event() for _ in range(M)] for _ in range(s)]
         self.ev_h2d, self.ev_cast = [], []     # per staging slot (sized in _ensure)
         self.used_free = [[False] * M for _ in range(s)]
+        self._pdl = 1
         _enable_peers(self.modules)
 
     # -- setup ----------------------------------------------------------
@@ -521,7 +541,7 @@ class DevicePipeline:
             with torch.cuda.stream(stream):
                 self._launch(j, slot, B, stream)
             return
-        key = (j, slot)
+        key = (j, slot, self._pdl)           # a graph keeps the PDL edges it was captured with
         g = self.graphs.get(key)
         if g is None:
             g = torch.cuda.CUDAGraph()
@@ -549,12 +569,13 @@ class DevicePipeline:
         shared = (max(len(v) for v in per_dev.values()) > 1 and
                   not all(getattr(m, "shared_gpu_pdl", True) for m in self.modules))
         lib = N.load()
-        prev = None if "PPLL_PDL" in os.environ else lib.ppll_set_pdl(0 if shared else 1)
+        want = int(os.environ["PPLL_PDL"] != "0") if "PPLL_PDL" in os.environ else int(not shared)
+        prev = lib.ppll_set_pdl(want)
+        self._pdl = want
         try:
             return self._run(dataset_iter)
         finally:
-            if prev is not None:
-                lib.ppll_set_pdl(prev)
+            lib.ppll_set_pdl(prev)
 
     def _run(self, dataset_iter: Iterable) -> EpochMetrics:
         mods, M, s = self.modules, self.M, len(self.modules)

@@ -181,3 +181,29 @@ def test_vit_b_stl_geometry_bf16_vs_oracle():
     for m, st in zip(mods, stages):
         a, b = _flat(m), _flat_o(st)
         assert np.abs(a - b).max() / np.abs(b).max() <= 5e-2
+
+
+def test_shared_gpu_vit_pipeline_pdl_on_off_bitwise(monkeypatch):
+    """the PDL policy must not change results, and a graph captured
+    under one setting must not be replayed under the other (graphs are keyed
+    by the setting).  Same epoch with PDL forced on / off / on again: bitwise."""
+    spec = lp.VitSpec(**SMALL)
+    rng = np.random.default_rng(9)
+    data = [(rng.standard_normal((6, 3, 8, 8)), rng.integers(0, 5, 6)) for _ in range(5)]
+    out = []
+    hyper = lp.Hyperparams(lr0=0.05, lr_min=0.001, total_steps=40, seed=3, precision="bf16")
+    mods_reused = lp.build_vit_modules(spec, [1, 1, 1], 1, 2, hyper)
+    for pdl in ("1", "0", "1"):
+        monkeypatch.setenv("PPLL_PDL", pdl)
+        mods = lp.build_vit_modules(spec, [1, 1, 1], 1, 2, hyper)
+        m = lp.run_epoch(lp.RunMode.PPLL, mods, iter(data), lp.RunConfig(buffer_capacity=2))
+        out.append((m.loss_history, [_flat(x) for x in mods]))
+        # one pipeline object replayed under both settings (cached graphs)
+        lp.run_epoch(lp.RunMode.PPLL, mods_reused, iter(data), lp.RunConfig(buffer_capacity=2))
+    for lh, fl in out[1:]:
+        assert lh == out[0][0]
+        for a, b in zip(fl, out[0][1]):
+            assert np.array_equal(a, b)
+    pipe = mods_reused[0]._pipelines
+    keys = {k for p in pipe.values() for k in p.graphs}
+    assert {k[2] for k in keys} == {0, 1}
