@@ -135,6 +135,17 @@ int ppll_nesterov_step(int64_t n, float* theta, float* v, const float* g, void* 
                        const float* lr_table, int* step, int max_step, float lr_host,
                        float mu, float wd, int* err, void* stream);
 
+/* The local optimizer of the stage whose flat parameter buffer is `theta`:
+ * kind 0 = Nesterov-SGD (the reference's, optim.py:71-89; the default),
+ * kind 1 = AdamW (north_star's "local SGD/Adam update"; no reference
+ * counterpart — torch.optim.AdamW semantics: decoupled weight decay
+ * θ -= lr·wd·θ, bias-corrected moments, t = step + 1).  m2 (second moment,
+ * same length as theta) is owned by the caller; the first moment is the
+ * buffer passed as `v`.  Every later update of that buffer — the fused stage
+ * steps and ppll_nesterov_step — applies the registered rule. */
+int ppll_set_local_optimizer(const float* theta, int kind, float* m2, float beta1, float beta2,
+                             float eps);
+
 /* cosine_lr (optim.py:39-44), fp64 on the host; returns NaN if out of range */
 double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps);
 

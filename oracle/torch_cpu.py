@@ -189,8 +189,13 @@ def from_mlp(st, dtype=torch.float32) -> TorchStage:
 # the local step (blocks.py:266-289)
 # --------------------------------------------------------------------------
 
-def local_step(ts: TorchStage, x_in, y, lr0, lr_min, total_steps, mu, wd):
-    """One local step; returns (loss, x_out detached, logits detached)."""
+def local_step(ts: TorchStage, x_in, y, lr0, lr_min, total_steps, mu, wd, opt="nesterov",
+               betas=(0.9, 0.999), eps=1e-8):
+    """One local step; returns (loss, x_out detached, logits detached).
+    ``opt="adamw"``: torch.optim.AdamW's rule (decoupled weight decay,
+    bias-corrected moments, t = step_count + 1) instead of the reference's
+    Nesterov — the checker of the device's AdamW local update (north_star's
+    "local SGD/Adam update"; the reference has no Adam)."""
     x_in = torch.as_tensor(x_in).to(ts.dtype).detach()
     y = torch.as_tensor(np.asarray(y)).long()
     P = ts.params
@@ -200,6 +205,19 @@ def local_step(ts: TorchStage, x_in, y, lr0, lr_min, total_steps, mu, wd):
     loss = F.cross_entropy(logits, y)        # mean over the batch
     grads = torch.autograd.grad(loss, P)
     lr = cosine_lr(ts.step_count, lr0, lr_min, total_steps)
+    if opt == "adamw":
+        if not hasattr(ts, "momenta2"):
+            ts.momenta2 = [torch.zeros_like(p, requires_grad=False) for p in P]
+        b1, b2 = betas
+        t = ts.step_count + 1
+        with torch.no_grad():
+            for p, m, v, g in zip(P, ts.momenta, ts.momenta2, grads):
+                p.mul_(1.0 - lr * wd)
+                m.mul_(b1).add_(g, alpha=1.0 - b1)
+                v.mul_(b2).addcmul_(g, g, value=1.0 - b2)
+                p.sub_(lr * (m / (1.0 - b1 ** t)) / ((v / (1.0 - b2 ** t)).sqrt() + eps))
+        ts.step_count += 1
+        return float(loss.detach()), x_out, logits.detach()
     with torch.no_grad():
         for p, v, g in zip(P, ts.momenta, grads):
             if wd != 0.0:

@@ -37,6 +37,7 @@ SIGNATURES = {
     "ppll_softmax_xent": (_i, [_i, _i, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp]),
     "ppll_nesterov_step": (_i, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _i, _f, _f, _f, _vp, _vp]),
     "ppll_cosine_lr": (_d, [_i, _d, _d, _i]),
+    "ppll_set_local_optimizer": (_i, [_vp, _i, _vp, _f, _f, _f]),
     "ppll_cast": (_i, [_i64, _vp, _i, _vp, _i, _vp]),
     "ppll_ew": (_i, [_i, _i64, _i64, _vp, _vp, _f, _vp, _i, _vp, _vp]),
     "ppll_colsum": (_i, [_i, _i, _vp, _vp, _i, _vp]),

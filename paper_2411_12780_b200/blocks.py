@@ -140,10 +140,35 @@ class Hyperparams:
     seed: int = 42
     aux_hidden_width: int | None = None
     precision: str = "fp32"
+    # the local optimizer: "nesterov" (the reference's, optim.py:71-89) or
+    # "adamw" (north_star's "local SGD/Adam update"; torch.optim.AdamW rule,
+    # ``weight_decay`` decoupled, ``momentum`` unused)
+    optimizer: str = "nesterov"
+    betas: tuple = (0.9, 0.999)
+    eps: float = 1e-8
 
     def __post_init__(self):
         if self.precision not in ("fp32", "bf16"):
             raise ValueError(f"precision must be 'fp32' or 'bf16', got {self.precision!r}")
+        if self.optimizer not in ("nesterov", "adamw"):
+            raise ValueError(f"optimizer must be 'nesterov' or 'adamw', got {self.optimizer!r}")
+
+
+def attach_local_optimizer(flat: dict, hyper: "Hyperparams") -> None:
+    """Register the stage's update rule with the library (keyed by its flat θ
+    buffer; ppll_set_local_optimizer).  AdamW needs a second-moment buffer
+    (``flat["mom2"]``; the first moment is ``flat["mom"]``).  The registration
+    is dropped when θ is freed, before its memory can be reused."""
+    if hyper.optimizer != "adamw":
+        return
+    import weakref
+    theta = flat["theta"]
+    flat["mom2"] = torch.zeros_like(theta)
+    lib = N.load()
+    b1, b2 = (float(b) for b in hyper.betas)
+    N.check(lib.ppll_set_local_optimizer(theta.data_ptr(), 1, flat["mom2"].data_ptr(), b1, b2,
+                                         float(hyper.eps)), "set_local_optimizer")
+    weakref.finalize(theta, lib.ppll_set_local_optimizer, theta.data_ptr(), 0, None, 0.0, 0.0, 0.0)
 
 
 class LocalModule:
@@ -397,6 +422,7 @@ def _materialise(j, host, n_block, assigned, hidden, hyper, device):
         "state": torch.zeros(4, dtype=torch.int32, device=device),
         "loss": torch.zeros(hyper.total_steps + 2, dtype=torch.float32, device=device),
     }
+    attach_local_optimizer(flat, hyper)
     layers, params, moms = [], [], []
     k = 0
     for W, b, relu_after in host:

@@ -210,6 +210,11 @@ int ppll_nesterov_step(int64_t n, float* theta, float* v, const float* g, void* 
                          wd, err, S(stream));
 }
 
+int ppll_set_local_optimizer(const float* theta, int kind, float* m2, float beta1, float beta2,
+                             float eps) {
+  return set_local_optimizer(theta, kind, m2, beta1, beta2, eps);
+}
+
 double ppll_cosine_lr(int step, double lr0, double lr_min, int total_steps) {
   if (step < 0 || step > total_steps || total_steps < 1) return NAN;
   double span = lr0 - lr_min;

@@ -12,6 +12,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace ppll {
 
 // ------------------------------------------------------------------------
@@ -588,6 +591,101 @@ grad_finite_kernel(long n, const float* __restrict__ g, int* err) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, kErrGradNonFinite);
 }
 
+// ------------------------------------------------------------------------
+// AdamW over one flat buffer — the "local SGD/Adam update" of north_star.
+// The reference has only Nesterov (optim.py:71-89); the Adam variant follows
+// torch.optim.AdamW (decoupled weight decay, bias-corrected moments):
+//   θ -= lr·wd·θ ; m = β1·m + (1-β1)·g ; v = β2·v + (1-β2)·g²
+//   θ -= lr · (m / (1-β1^t)) / (sqrt(v / (1-β2^t)) + eps),  t = step + 1
+// with the same device step counter, cosine-LR table, all-or-nothing skip and
+// step advance as nesterov_kernel.  28 B/param (+2 for the bf16 shadow).
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+adamw_kernel(long n, float* __restrict__ th, float* __restrict__ m1, float* __restrict__ m2,
+             const float* __restrict__ g, __nv_bfloat16* __restrict__ th_lp,
+             const float* __restrict__ lr_table, int* step, int max_step, float lr_host,
+             float beta1, float beta2, float eps, float wd, int* err, unsigned int* done,
+             int advance) {
+  pdl_entry();
+  __shared__ int s_skip;
+  __shared__ float s_lr, s_c1, s_c2;
+  if (threadIdx.x == 0) {
+    int e = err ? *(volatile int*)err : 0;
+    int st = step ? *(volatile int*)step : 0;
+    int skip = (e & (kErrLabel | kErrLossNonFinite | kErrGradNonFinite)) ? 1 : 0;
+    if (step && (st < 0 || st > max_step)) {
+      skip = 1;
+      if (err) atomicOr(err, kErrStep);
+    }
+    s_skip = skip;
+    s_lr = step ? lr_table[min(max(st, 0), max_step)] : lr_host;
+    const float t = (float)(max(st, 0) + 1);
+    s_c1 = 1.0f / (1.0f - powf(beta1, t));
+    s_c2 = 1.0f / (1.0f - powf(beta2, t));
+  }
+  __syncthreads();
+  bool bad = false;
+  if (!s_skip) {
+    const float lr = s_lr, c1 = s_c1, c2 = s_c2, decay = 1.0f - s_lr * wd;
+    const float ob1 = 1.0f - beta1, ob2 = 1.0f - beta2;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+      const float gi = g[i];
+      const float a = fmaf(beta1, m1[i], ob1 * gi);
+      const float b = fmaf(beta2, m2[i], ob2 * gi * gi);
+      const float t = th[i] * decay - lr * (a * c1) / (sqrtf(b * c2) + eps);
+      m1[i] = a;
+      m2[i] = b;
+      th[i] = t;
+      if (th_lp) th_lp[i] = __float2bfloat16_rn(t);
+      bad |= !isfinite(t);
+    }
+  }
+  if (bad && err) atomicOr(err, kErrParamNonFinite);
+  if (step && advance) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned int prev = atomicAdd(done, 1u);
+      if (prev == gridDim.x - 1) {
+        if (!s_skip) atomicAdd(step, 1);
+        *done = 0u;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// Per-flat-buffer optimizer choice: a stage whose θ buffer was registered
+// with ppll_set_local_optimizer(AdamW) is updated by adamw_kernel wherever
+// the stage executors call launch_nesterov (one switch for all families).
+struct AdamCfg { float* m2; float beta1, beta2, eps; };
+static std::mutex g_opt_mu;
+static std::unordered_map<const float*, AdamCfg> g_opt;
+
+int set_local_optimizer(const float* theta, int kind, float* m2, float beta1, float beta2,
+                        float eps) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  if (kind == 0) {
+    g_opt.erase(theta);
+    return PPLL_OK;
+  }
+  if (kind != 1 || !m2 || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) ||
+      !(eps > 0.f)) {
+    set_error("set_local_optimizer: bad arguments");
+    return PPLL_ERR_ARG;
+  }
+  g_opt[theta] = AdamCfg{m2, beta1, beta2, eps};
+  return PPLL_OK;
+}
+
+static bool adam_for(const float* theta, AdamCfg* out) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  auto it = g_opt.find(theta);
+  if (it == g_opt.end()) return false;
+  *out = it->second;
+  return true;
+}
+
 int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* th_lp,
                     const float* lr_table, int* step, int max_step, float lr_host, float mu,
                     float wd, int* err, cudaStream_t s, bool advance) {
@@ -607,8 +705,13 @@ int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* 
     note_launch();
     PPLL_LAUNCH_CHECK();
   }
-  launch_k(nesterov_kernel, blocks, 256, 0, s, n, th, v, g, th_lp, lr_table, step, max_step, lr_host,
-                                         mu, wd, err, done, advance ? 1 : 0);
+  AdamCfg ad;
+  if (adam_for(th, &ad))
+    launch_k(adamw_kernel, blocks, 256, 0, s, n, th, v, ad.m2, g, th_lp, lr_table, step, max_step,
+             lr_host, ad.beta1, ad.beta2, ad.eps, wd, err, done, advance ? 1 : 0);
+  else
+    launch_k(nesterov_kernel, blocks, 256, 0, s, n, th, v, g, th_lp, lr_table, step, max_step,
+             lr_host, mu, wd, err, done, advance ? 1 : 0);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;

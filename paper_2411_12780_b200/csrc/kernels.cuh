@@ -842,6 +842,8 @@ int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* 
 
 // advance = false: update only (the step counter is advanced by the step's
 // last launch, after every range has read it)
+int set_local_optimizer(const float* theta, int kind, float* m2, float beta1, float beta2,
+                        float eps);
 int launch_nesterov(long n, float* th, float* v, const float* g, __nv_bfloat16* th_lp,
                     const float* lr_table, int* step, int max_step, float lr_host, float mu,
                     float wd, int* err, cudaStream_t s, bool advance = true);

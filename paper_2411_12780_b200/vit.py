@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .blocks import Hyperparams, LocalModule, aux_depth
+from .blocks import Hyperparams, LocalModule, attach_local_optimizer, aux_depth
 from .errors import ConfigMismatch
 from .optim import LrSchedule, OptimizerState, lr_table
 from .tensor import Tensor, default_device
@@ -313,6 +313,7 @@ def build_vit_modules(spec: VitSpec, depths: Sequence[int], d_prime: int, n: int
                 "offsets": native_offs, "lr": lr_table(sched, device),
                 "state": torch.zeros(4, dtype=torch.int32, device=device),
                 "loss": torch.zeros(hyper.total_steps + 2, dtype=torch.float32, device=device)}
+        attach_local_optimizer(flat, hyper)
         groups, moms = [], []
         for (g, k, a), o in zip(host, offsets):
             view = theta[o:o + a.size].view(a.shape)

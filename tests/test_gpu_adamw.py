@@ -1,0 +1,75 @@
+"""The AdamW local update (north_star: "local SGD/Adam update"; no reference
+counterpart, torch.optim.AdamW semantics — checked against torch.optim.AdamW in
+tests/test_torch_cpu.py) in the fused stage step of every family, fp32 parity
+mode, against the float64 restatement (oracle/torch_cpu.py, opt="adamw"):
+losses 1e-5 relative, parameters after 4 steps 1e-4 of max|θ|."""
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2411_12780_b200 as lp
+import ppll_oracle as orc
+import resnet_oracle as ro
+import torch_cpu as tc
+import vit_oracle as vo
+
+pytestmark = pytest.mark.gpu
+STEPS = 4
+WD = 1e-2
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("family", ["mlp", "vit", "resnet"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_adamw_stage_step_matches_restatement(family, precision):
+    hyper = lp.Hyperparams(lr0=0.01, lr_min=0.001, total_steps=STEPS, seed=5, precision=precision,
+                           optimizer="adamw", weight_decay=WD)
+    rng = np.random.default_rng(0)
+    if family == "mlp":
+        dims = (48, 32, 32, 24, 10)
+        plan = lp.partition(lp.NetworkSpec(dims), 2)
+        mods = lp.build_modules(lp.NetworkSpec(dims), plan, 2, 3, hyper)
+        ref = [tc.from_mlp(s, torch.float64)
+               for s in orc.build_stages(dims, plan.boundaries, 2, 3, 5)]
+        xs = rng.standard_normal((STEPS, 16, 48))
+    elif family == "vit":
+        kw = dict(image=8, channels=3, patch=4, dim=128, heads=2, mlp=256, depth=2, classes=10)
+        mods = lp.build_vit_modules(lp.VitSpec(**kw), [1, 1], 1, 3, hyper)
+        ref = [tc.from_vit(s, torch.float64)
+               for s in vo.build_vit_stages(vo.VitSpec(**kw), [1, 1], 1, 3, 5)]
+        xs = rng.standard_normal((STEPS, 8, 3, 8, 8))
+    else:
+        kw = dict(n=1, image=8, channels=3, widths=(16, 32, 64), classes=10)
+        mods = lp.build_resnet_modules(lp.ResNetSpec(**kw), 2, 1, 3, hyper)
+        ref = [tc.from_resnet(s, torch.float64)
+               for s in ro.build_resnet_stages(ro.ResNetSpec(**kw), 2, 1, 3, 5)]
+        xs = rng.standard_normal((STEPS, 16, 8, 8, 3))
+    ys = rng.integers(0, 10, (STEPS, xs.shape[1]))
+    th0 = [np.concatenate([p.data.ravel() for p in m.parameters()]) for m in mods]
+    ltol, wtol = (1e-5, 1e-4) if precision == "fp32" else (2e-2, 5e-2)
+    for t in range(STEPS):
+        h = lp.Tensor(xs[t])
+        x_ref = xs[t]
+        for m, r in zip(mods, ref):
+            loss, h = lp.local_loss_and_update(m, h, ys[t])
+            want, _, _ = tc.local_step(r, torch.tensor(x_ref), ys[t], 0.01, 0.001, STEPS, 0.9, WD,
+                                       opt="adamw")
+            assert abs(loss - want) <= ltol * max(1.0, abs(want)), (family, t, loss, want)
+            x_ref = h.data                 # teacher forcing: the device's x_out
+    for m, r, a0 in zip(mods, ref, th0):
+        got = np.concatenate([p.data.ravel() for p in m.parameters()])
+        want = np.concatenate([p.detach().numpy().ravel() for p in r.params])
+        assert np.abs(got - want).max() <= wtol * np.abs(want).max()
+        # AdamW moves every parameter by ~lr per step: the update is real
+        d_dev, d_ref = got - a0, want - a0
+        assert np.linalg.norm(d_dev - d_ref) <= (0.02 if precision == "fp32" else 0.25) * \
+            np.linalg.norm(d_ref)
+

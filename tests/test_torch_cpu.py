@@ -79,3 +79,34 @@ def test_mlp_restatement():
         assert abs(lo - lt) <= 1e-12
         np.testing.assert_allclose(h, ht, rtol=0, atol=1e-12)
     _check(stages, tst, 1e-12)
+
+
+def test_adamw_rule_matches_torch_optim_adamw():
+    """oracle/torch_cpu.py's AdamW branch == torch.optim.AdamW step for step."""
+    dims = (12, 10, 5)
+    stages = orc.build_stages(dims, orc.partition(dims, 1), 1, 3, 42)
+    ts = tc.from_mlp(copy.deepcopy(stages[0]), torch.float64)
+    ref = [torch.tensor(p, requires_grad=True) for p in stages[0].params()]
+    rng = np.random.default_rng(4)
+    for t in range(4):
+        x = rng.standard_normal((6, 12))
+        y = rng.integers(0, 5, 6)
+        lr = tc.cosine_lr(t, 0.05, 0.001, 10)
+        tc.local_step(ts, x, y, 0.05, 0.001, 10, 0.9, 1e-2, opt="adamw")
+        opt = torch.optim.AdamW(ref, lr=lr, betas=(0.9, 0.999), eps=1e-8, weight_decay=1e-2)
+        if t:
+            opt.load_state_dict(state)
+            for gr in opt.param_groups:
+                gr["lr"] = lr
+        h = torch.tensor(x)
+        for i, (W, b) in enumerate(zip(ref[0::2], ref[1::2])):
+            h = h @ W + b
+            if i < len(ref) // 2 - 1:
+                h = torch.relu(h)
+        loss = torch.nn.functional.cross_entropy(h, torch.tensor(y))
+        opt.zero_grad()
+        loss.backward()
+        opt.step()
+        state = opt.state_dict()
+    for p, q in zip(ts.params, ref):
+        np.testing.assert_allclose(p.detach().numpy(), q.detach().numpy(), rtol=1e-10, atol=1e-12)
