@@ -2,7 +2,11 @@
 counterpart, torch.optim.AdamW semantics — checked against torch.optim.AdamW in
 tests/test_torch_cpu.py) in the fused stage step of every family, fp32 parity
 mode, against the float64 restatement (oracle/torch_cpu.py, opt="adamw"):
-losses 1e-5 relative, parameters after 4 steps 1e-4 of max|θ|."""
+losses 1e-5 relative, the 4-step update dθ within 2 % (L2) of the float64
+one.  AdamW normalises every coordinate's step to ~lr, so a coordinate whose
+true gradient is at rounding level (1e-9) still moves by ~lr in a direction
+set by rounding noise; eps = 1e-6 (instead of torch's 1e-8 default) keeps
+such coordinates from dominating the comparison."""
 import copy
 
 import numpy as np
@@ -18,6 +22,7 @@ import vit_oracle as vo
 pytestmark = pytest.mark.gpu
 STEPS = 4
 WD = 1e-2
+EPS = 1e-6
 
 
 @pytest.fixture(autouse=True)
@@ -31,7 +36,7 @@ def _cuda():
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_adamw_stage_step_matches_restatement(family, precision):
     hyper = lp.Hyperparams(lr0=0.01, lr_min=0.001, total_steps=STEPS, seed=5, precision=precision,
-                           optimizer="adamw", weight_decay=WD)
+                           optimizer="adamw", weight_decay=WD, eps=EPS)
     rng = np.random.default_rng(0)
     if family == "mlp":
         dims = (48, 32, 32, 24, 10)
@@ -54,14 +59,14 @@ def test_adamw_stage_step_matches_restatement(family, precision):
         xs = rng.standard_normal((STEPS, 16, 8, 8, 3))
     ys = rng.integers(0, 10, (STEPS, xs.shape[1]))
     th0 = [np.concatenate([p.data.ravel() for p in m.parameters()]) for m in mods]
-    ltol, wtol = (1e-5, 1e-4) if precision == "fp32" else (2e-2, 5e-2)
+    ltol, wtol = (1e-5, 2e-3) if precision == "fp32" else (2e-2, 5e-2)
     for t in range(STEPS):
         h = lp.Tensor(xs[t])
         x_ref = xs[t]
         for m, r in zip(mods, ref):
             loss, h = lp.local_loss_and_update(m, h, ys[t])
             want, _, _ = tc.local_step(r, torch.tensor(x_ref), ys[t], 0.01, 0.001, STEPS, 0.9, WD,
-                                       opt="adamw")
+                                       opt="adamw", eps=EPS)
             assert abs(loss - want) <= ltol * max(1.0, abs(want)), (family, t, loss, want)
             x_ref = h.data                 # teacher forcing: the device's x_out
     for m, r, a0 in zip(mods, ref, th0):
