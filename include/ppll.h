@@ -261,6 +261,17 @@ int ppll_vit_stage_step(ppll_vit_stage* st, int B, const void* x_in, const int64
                         void* x_out, void* stream);
 int ppll_vit_stage_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_out,
                            void* logits, void* stream);
+/* The paper's E2E / naive-PP baselines for the ViT family (reference
+ * runtime.py:248-284 E2E, :359-382 NaivePP; the reference's own blocks are
+ * MLPs): block forward only (h_out != NULL: non-final stage, output stored
+ * there; h_out == NULL: final stage, block + task head), and backward from
+ * g_out = dLoss/d(block output) or, on the final stage, from the task loss
+ * (labels), with dLoss/d(block input) into g_in (NULL on stage 0), then the
+ * optimizer over the block parameters only. */
+int ppll_vit_stage_block_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_out,
+                                 void* stream);
+int ppll_vit_stage_block_backward(ppll_vit_stage* st, int B, const void* x_in, const void* g_out,
+                                  const int64_t* labels, void* g_in, void* stream);
 
 /* ---- one local step of a ResNet stage (CIFAR basic blocks, NHWC; no
  * reference implementation — parity pinned to oracle/resnet_oracle.py) ----
@@ -283,6 +294,13 @@ int ppll_resnet_stage_step(ppll_resnet_stage* st, int B, const void* x_in, const
                            void* x_out, void* stream);
 int ppll_resnet_stage_forward(ppll_resnet_stage* st, int B, const void* x_in, void* h_out,
                               void* logits, void* stream);
+/* E2E / naive-PP baselines for the ResNet family (same contract as the ViT
+ * pair above; runtime.py:248-284, 359-382). */
+int ppll_resnet_stage_block_forward(ppll_resnet_stage* st, int B, const void* x_in, void* h_out,
+                                    void* stream);
+int ppll_resnet_stage_block_backward(ppll_resnet_stage* st, int B, const void* x_in,
+                                     const void* g_out, const int64_t* labels, void* g_in,
+                                     void* stream);
 
 /* ---- stage-boundary ring (runtime.py:52-120 StageBuffer) ----------------
  * Device-resident flag words for an SPSC ring of `capacity` slots.  ready[i]

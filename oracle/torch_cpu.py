@@ -226,3 +226,42 @@ def local_step(ts: TorchStage, x_in, y, lr0, lr_min, total_steps, mu, wd, opt="n
             p.sub_(lr * (g + mu * v))
     ts.step_count += 1
     return float(loss.detach()), x_out, logits.detach()
+
+
+# --------------------------------------------------------------------------
+# the paper's E2E baseline (reference runtime.py:248-284)
+# --------------------------------------------------------------------------
+
+def e2e_step(stages, x_in, y, lr0, lr_min, total_steps, mu, wd):
+    """One end-to-end backprop step through every stage's BLOCK (aux heads
+    unused): the final stage's block ends in its task head (the final stage
+    has no aux layers, so ``head_fn`` is that head); the mean softmax-CE of
+    the final logits is differentiated w.r.t. every parameter on the path and
+    each stage takes the reference's L2-in-gradient Nesterov step on those
+    parameters only (runtime.py:276-281); parameters off the path (aux heads)
+    are left untouched.  Every stage's step counter advances.  Returns the
+    loss."""
+    x = torch.as_tensor(x_in).to(stages[0].dtype).detach()
+    y = torch.as_tensor(np.asarray(y)).long()
+    h = x
+    for ts in stages:
+        h = ts.block_fn(ts.params, h)
+    logits = stages[-1].head_fn(stages[-1].params, h)
+    loss = F.cross_entropy(logits, y)
+    allp = [p for ts in stages for p in ts.params]
+    grads = torch.autograd.grad(loss, allp, allow_unused=True)
+    k = 0
+    for ts in stages:
+        lr = cosine_lr(ts.step_count, lr0, lr_min, total_steps)
+        with torch.no_grad():
+            for p, v in zip(ts.params, ts.momenta):
+                g = grads[k]
+                k += 1
+                if g is None:
+                    continue
+                if wd != 0.0:
+                    g = g + wd * p
+                v.mul_(mu).add_(g)
+                p.sub_(lr * (g + mu * v))
+        ts.step_count += 1
+    return float(loss.detach())

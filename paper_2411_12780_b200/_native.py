@@ -60,11 +60,15 @@ SIGNATURES = {
     "ppll_vit_stage_destroy": (None, [_vp]),
     "ppll_vit_stage_step": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ppll_vit_stage_forward": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "ppll_vit_stage_block_forward": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "ppll_vit_stage_block_backward": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp]),
     "ppll_resnet_stage_create": (_vp, [_vp, _vp, _vp, _vp, _i64, _i, _vp, _vp, _vp, _vp, _vp,
                                        _vp, _i, _vp, _vp, _f, _f]),
     "ppll_resnet_stage_destroy": (None, [_vp]),
     "ppll_resnet_stage_step": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ppll_resnet_stage_forward": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "ppll_resnet_stage_block_forward": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "ppll_resnet_stage_block_backward": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp]),
     "ppll_ring_publish": (_i, [_vp, _i, _vp]),
     "ppll_ring_wait": (_i, [_vp, _i, _vp]),
     "ppll_ring_release": (_i, [_vp, _vp]),

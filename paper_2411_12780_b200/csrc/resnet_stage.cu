@@ -205,7 +205,7 @@ static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, 
 
 template <typename TT>
 static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_out, bool head,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool with_aux = true) {
   const void* x = x_in;
   int r;
   if (st->has_stem) {
@@ -249,6 +249,7 @@ static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_o
     PPLL_CUDA_CHECK(cudaMemcpyAsync(x_out, x, Pout * st->c_out * st->esz, cudaMemcpyDeviceToDevice, s));
   if (!head) return PPLL_OK;
   for (auto& a : st->aux) {
+    if (!with_aux) break;
     r = conv_bn_fwd<TT>(st, a.c, B, x, a.off[0], s);
     if (r) return r;
     r = launch_bn_apply<TT>(Pout, a.c.cout, (const TT*)a.c.z, a.c.mean, a.c.rstd, st->P(a.off[1]),
@@ -265,35 +266,44 @@ static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_o
                   st->logits, st->classes, st->dtype, st->ws, st->ws_elems, s);
 }
 
+// Backward from the loss through the head (labels != NULL; aux layers when
+// `with_aux`) or from `g_out` = dLoss/d(block output), through the blocks and
+// the stem; dLoss/d(stage input) into `g_in` (NULL: detached input).  Every
+// weight gradient has landed on `s` when this returns.
 template <typename TT>
-static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_t* labels,
-                    void* x_out, cudaStream_t s) {
-  int r = res_forward<TT>(st, B, x_in, x_out, true, s);
-  if (r) return r;
+static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, const void* g_out,
+                        void* g_in, bool with_aux, cudaStream_t s) {
   const int C = st->c_out, HW = st->h_out * st->h_out;
-  r = launch_softmax_xent<TT>(B, st->classes, (const TT*)st->logits, st->classes, labels,
-                              (TT*)st->dlog, st->classes, st->loss_hist, st->step, st->err, s);
-  if (r) return r;
+  int r;
   static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
   const bool side = side_on && st->side && st->dz2;
   BwdSide bs{SideFlow{s, side ? st->side : s, st->ev.data(), 0, (int)st->ev.size()},
              {st->dz, side ? st->dz2 : st->dz}};
   bs.wsw = side ? st->ws2 : st->ws;
-  // head
-  bs.sf.fork();
-  r = linear_wgrad(B, C, st->classes, st->pooled, C, st->dlog, st->classes, st->G(st->head_off[0]),
-                   st->G(st->head_off[1]), st->dtype, bs.wsw, st->ws_elems, bs.sf.ss);
-  if (r) return r;
-  LinOpts none;
-  r = gemm_dgrad(B, C, st->classes, st->dlog, st->classes, st->W(st->head_off[0]), none, st->dp,
-                 C, st->dtype, st->ws, st->ws_elems, s);
-  if (r) return r;
   char* dx = st->dxa;
   char* dx_next = st->dxb;
-  r = launch_gap_bwd<TT>(B, HW, C, (const TT*)st->dp, (TT*)dx, s);
-  if (r) return r;
+  if (!labels) {
+    PPLL_CUDA_CHECK(cudaMemcpyAsync(dx, g_out, (size_t)B * HW * C * st->esz,
+                                    cudaMemcpyDeviceToDevice, s));
+  } else {
+    r = launch_softmax_xent<TT>(B, st->classes, (const TT*)st->logits, st->classes, labels,
+                                (TT*)st->dlog, st->classes, st->loss_hist, st->step, st->err, s);
+    if (r) return r;
+    // head
+    bs.sf.fork();
+    r = linear_wgrad(B, C, st->classes, st->pooled, C, st->dlog, st->classes,
+                     st->G(st->head_off[0]), st->G(st->head_off[1]), st->dtype, bs.wsw,
+                     st->ws_elems, bs.sf.ss);
+    if (r) return r;
+    LinOpts none;
+    r = gemm_dgrad(B, C, st->classes, st->dlog, st->classes, st->W(st->head_off[0]), none,
+                   st->dp, C, st->dtype, st->ws, st->ws_elems, s);
+    if (r) return r;
+    r = launch_gap_bwd<TT>(B, HW, C, (const TT*)st->dp, (TT*)dx, s);
+    if (r) return r;
+  }
   // aux layers, last first (gradient w.r.t. each aux conv-BN-ReLU output)
-  for (int i = (int)st->aux.size() - 1; i >= 0; --i) {
+  for (int i = with_aux ? (int)st->aux.size() - 1 : -1; i >= 0; --i) {
     Aux& a = st->aux[i];
     r = launch_relu_mask<TT>((long)B * HW * C, (const TT*)dx, (const TT*)a.out, (TT*)st->dy, s);
     if (r) return r;
@@ -306,7 +316,9 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
   for (int i = (int)st->blocks.size() - 1; i >= 0; --i) {
     Block& b = st->blocks[i];
     const long P = (long)B * b.c1.h_out * b.c1.h_out;
-    const bool need_dx = i > 0 || st->has_stem;
+    const bool need_dx = i > 0 || st->has_stem || g_in;
+    // the stage input's gradient goes straight to g_in (no stem below)
+    char* dx_dst = (i == 0 && !st->has_stem) ? (char*)g_in : dx_next;
     r = launch_relu_mask<TT>(P * b.c2.cout, (const TT*)dx, (const TT*)b.out, (TT*)st->dsum, s);
     if (r) return r;
     // conv2: input gradient masked by the ReLU that produced a1 -> dy
@@ -324,7 +336,7 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
     }
     // conv1 (+ shortcut / identity gradient) -> gradient of the block input
     r = conv_bn_bwd<TT>(st, b.c1, B, st->dy, b.off[0], b.off[1], b.off[2],
-                        need_dx ? dx_next : nullptr, dres, nullptr, s, bs);
+                        need_dx ? dx_dst : nullptr, dres, nullptr, s, bs);
     if (r) return r;
     char* t = dx; dx = dx_next; dx_next = t;
   }
@@ -338,9 +350,24 @@ static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_
     if (r) return r;
   }
   bs.sf.join(bs.sf.mark());   // every weight gradient has landed
-  return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
+  return PPLL_OK;
+}
+
+// optimizer over the first `n` elements of the flat parameter buffer
+static int res_update(ppll_resnet_stage* st, int64_t n, cudaStream_t s) {
+  return launch_nesterov(n, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
                          st->max_step, 0.f, st->mu, st->wd, st->err, s);
+}
+
+template <typename TT>
+static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_t* labels,
+                    void* x_out, cudaStream_t s) {
+  int r = res_forward<TT>(st, B, x_in, x_out, true, s);
+  if (r) return r;
+  r = res_backward<TT>(st, B, labels, nullptr, nullptr, true, s);
+  if (r) return r;
+  return res_update(st, st->n_params, s);
 }
 
 extern "C" {
@@ -483,6 +510,42 @@ int ppll_resnet_stage_forward(ppll_resnet_stage* st, int B, const void* x_in, vo
   PPLL_CUDA_CHECK(cudaMemcpyAsync(logits, st->logits, (size_t)B * st->classes * st->esz,
                                   cudaMemcpyDeviceToDevice, s));
   return PPLL_OK;
+}
+
+// ---- the paper's baselines: E2E / naive PP (runtime.py:248-284, 359-382) ----
+// Block forward only (aux convs and aux classifier unused): h_out != NULL
+// receives the block output (non-final stage); h_out == NULL is the final
+// stage, whose block ends in the task head (GAP + classifier).
+int ppll_resnet_stage_block_forward(ppll_resnet_stage* st, int B, const void* x_in, void* h_out,
+                                    void* stream) {
+  if (!st || B < 1 || B > st->Bmax || !x_in || (!h_out && st->n_aux)) {
+    set_error("ppll_resnet_stage_block_forward: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool head = h_out == nullptr;
+  return st->dtype == PPLL_F32 ? res_forward<float>(st, B, x_in, h_out, head, s, false)
+                               : res_forward<__nv_bfloat16>(st, B, x_in, h_out, head, s, false);
+}
+
+// Backward through the block from `g_out` = dLoss/d(block output), or — final
+// stage, labels != NULL — from the task loss; dLoss/d(block input) into g_in
+// (NULL for stage 0); then the optimizer over the BLOCK parameters only (stem
+// + basic blocks; + the task head on the final stage).  The step advances.
+int ppll_resnet_stage_block_backward(ppll_resnet_stage* st, int B, const void* x_in,
+                                     const void* g_out, const int64_t* labels, void* g_in,
+                                     void* stream) {
+  if (!st || B < 1 || B > st->Bmax || !x_in || (!g_out && !labels) || (labels && st->n_aux)) {
+    set_error("ppll_resnet_stage_block_backward: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t nb = labels ? st->n_params
+                            : (st->aux.empty() ? st->head_off[0] : st->aux[0].off[0]);
+  int r = st->dtype == PPLL_F32 ? res_backward<float>(st, B, labels, g_out, g_in, false, s)
+                                : res_backward<__nv_bfloat16>(st, B, labels, g_out, g_in, false, s);
+  if (r) return r;
+  return res_update(st, nb, s);
 }
 
 }  // extern "C"

@@ -113,7 +113,8 @@ static int attn_bwd_any(int B, int T, int H, int dh, const TT* qkv, const TT* o,
 
 template <typename TT>
 static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out, bool head,
-                       cudaStream_t s) {
+                       cudaStream_t s, int nl = -1) {
+  if (nl < 0) nl = st->layers();
   const int T = st->T, D = st->D, F = st->F, H = st->H;
   const int M = B * T;
   const TT* xcur = reinterpret_cast<const TT*>(x_in);
@@ -132,7 +133,7 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     if (r) return r;
     xcur = (const TT*)st->x0;
   }
-  for (int l = 0; l < st->layers(); ++l) {
+  for (int l = 0; l < nl; ++l) {
     LayerBufs& b = st->L[l];
     r = launch_ln_fwd<TT>(M, D, xcur, D, st->P(st->po(l, kLn1g)), st->P(st->po(l, kLn1b)),
                           (TT*)b.xn1, D, b.mean1, b.rstd1, s);
@@ -186,35 +187,53 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
                   st->ws, st->ws_elems, s);
 }
 
+// Backward of the stage's first `nl` layers (+ head when `labels`), then the
+// patch embedding on stage 0.  The gradient entering the top layer's output is
+// either the task / aux loss through the head (labels != NULL) or `g_out`
+// (dLoss/d(block output) from the next stage: E2E / naive PP).  `g_in`
+// receives dLoss/d(stage input) (NULL: detached input, blocks.py:277-278).
+// Every weight gradient has landed on `s` when this returns.
 template <typename TT>
-static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
-                    void* x_out, cudaStream_t s) {
+static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
+                        const void* g_out, void* g_in, int nl, cudaStream_t s) {
   const int T = st->T, D = st->D, F = st->F, H = st->H, C = st->C;
   const int M = B * T;
   static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
   SideFlow sf{s, (side_on && st->side) ? st->side : s, st->ev.data(), 0, (int)st->ev.size()};
   float* wsw = sf.on() ? st->ws2 : st->ws;   // the weight gradients' workspace
-  int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
-  if (r) return r;
-  r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
-                              st->loss_hist, st->step, st->err, s);
-  if (r) return r;
-  const TT* xlast = (const TT*)st->L[st->layers() - 1].x2;
-  // ---- head backward ----
-  sf.fork();
-  r = linear_wgrad(B, D, C, st->zc, D, st->dlog, C, st->G(st->ho(2)), st->G(st->ho(3)), st->dtype,
-                   wsw, st->ws_elems, sf.ss);
-  if (r) return r;
+  int r;
   LinOpts none;
-  r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
-                 st->ws_elems, s);
-  if (r) return r;
-  r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, (long)T * D, st->meanf, st->rstdf,
-                        st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, st->ln_part,
-                        st->G(st->ho(0)), st->G(st->ho(1)), s);
-  if (r) return r;
-  r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)st->dxa, s);
-  if (r) return r;
+  if (labels) {
+    r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
+                                st->loss_hist, st->step, st->err, s);
+    if (r) return r;
+    const TT* xlast = (const TT*)st->L[nl - 1].x2;
+    // ---- head backward ----
+    sf.fork();
+    r = linear_wgrad(B, D, C, st->zc, D, st->dlog, C, st->G(st->ho(2)), st->G(st->ho(3)),
+                     st->dtype, wsw, st->ws_elems, sf.ss);
+    if (r) return r;
+    r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
+                   st->ws_elems, s);
+    if (r) return r;
+    r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, (long)T * D, st->meanf, st->rstdf,
+                          st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, st->ln_part,
+                          st->G(st->ho(0)), st->G(st->ho(1)), s);
+    if (r) return r;
+    r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)st->dxa, s);
+    if (r) return r;
+    // db2 of the top layer = Σ rows of its output gradient: only the cls rows
+    // are non-zero (Σ of dz over the batch)
+    r = launch_colsum<TT>(B, D, (const TT*)st->dzc, D, st->G(st->po(nl - 1, kB2)), s, st->ws,
+                          st->ws_elems);
+    if (r) return r;
+  } else {
+    PPLL_CUDA_CHECK(cudaMemcpyAsync(st->dxa, g_out, (size_t)M * D * st->esz,
+                                    cudaMemcpyDeviceToDevice, s));
+    r = launch_colsum<TT>(M, D, (const TT*)st->dxa, D, st->G(st->po(nl - 1, kB2)), s, st->ws,
+                          st->ws_elems);
+    if (r) return r;
+  }
   // ---- layers, last first ----
   char* dx2 = st->dxa;   // gradient w.r.t. the current layer's output
   char* dx1 = st->dxb;
@@ -222,19 +241,11 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   // side-stream completion of the previous (higher) layer's weight gradients:
   // the main stream waits on them before overwriting the buffers they read
   cudaEvent_t e_w2 = nullptr, e_w1 = nullptr, e_wo = nullptr, e_wqkv = nullptr;
-  for (int l = st->layers() - 1; l >= 0; --l) {
+  for (int l = nl - 1; l >= 0; --l) {
     LayerBufs& b = st->L[l];
     const void* xin_l = l > 0 ? (const void*)st->L[l - 1].x2
                               : (st->has_patch ? (const void*)st->x0 : x_in);
-    const bool top = l == st->layers() - 1;
-    // db2 = Σ rows of dx2: for the top layer only the cls rows are non-zero
-    // (Σ of dz over the batch); below, the LN1 backward of layer l+1 already
-    // produced it as a fused output
-    if (top) {
-      r = launch_colsum<TT>(B, D, (const TT*)st->dzc, D, st->G(st->po(l, kB2)), s, st->ws,
-                            st->ws_elems);
-      if (r) return r;
-    }
+    // (db2 of layer l < top: fused into the LN1 backward of layer l+1)
     sf.fork();
     r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, wsw,
                      st->ws_elems, sf.ss);
@@ -288,12 +299,14 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
     // LN1 backward (+ residual) -> gradient of the layer input; no gradient
     // into the detached stage input (blocks.py:277-278).  Its row sum is the
     // bias gradient db2 of the layer below (fused).
-    const bool need_dx = l > 0 || st->has_patch;
+    const bool need_dx = l > 0 || st->has_patch || g_in;
+    // the stage input's gradient goes straight to g_in (no patch embedding below)
+    TT* dx_dst = (l == 0 && !st->has_patch) ? (TT*)g_in : (TT*)dxn_out;
     sf.join(e_w2);   // dxn_out was the layer above's dx2, read by its W2 gradient
     e_w2 = n_w2;
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
                           st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
-                          need_dx ? (TT*)dxn_out : nullptr, D, st->ln_part,
+                          need_dx ? dx_dst : nullptr, D, st->ln_part,
                           st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s,
                           l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr);
     if (r) return r;
@@ -312,9 +325,27 @@ static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* 
   }
   // every weight gradient has landed before the optimizer reads them
   sf.join(sf.mark());
-  return launch_nesterov(st->n_params, st->theta, st->mom, st->grad,
+  return PPLL_OK;
+}
+
+// optimizer over the first `n` elements of the flat parameter buffer
+static int vit_update(ppll_vit_stage* st, int64_t n, cudaStream_t s) {
+  return launch_nesterov(n, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
                          st->max_step, 0.f, st->mu, st->wd, st->err, s);
+}
+
+// one PPLL local step: forward (block + aux + head, the last block epilogue
+// dual-stores the push), local loss, backward with no gradient into the
+// detached input, update of every stage parameter
+template <typename TT>
+static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
+                    void* x_out, cudaStream_t s) {
+  int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
+  if (r) return r;
+  r = vit_backward<TT>(st, B, x_in, labels, nullptr, nullptr, st->layers(), s);
+  if (r) return r;
+  return vit_update(st, st->n_params, s);
 }
 
 extern "C" {
@@ -427,6 +458,44 @@ int ppll_vit_stage_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_
   PPLL_CUDA_CHECK(cudaMemcpyAsync(logits, st->logits, (size_t)B * st->C * st->esz,
                                   cudaMemcpyDeviceToDevice, s));
   return PPLL_OK;
+}
+
+// ---- the paper's baselines: E2E / naive PP (runtime.py:248-284, 359-382) ----
+// Block forward only (aux layers and aux head unused).  h_out != NULL: the
+// block output is stored there (a non-final stage); h_out == NULL: the final
+// stage, whose block ends in the task head (LN on the cls row + classifier).
+int ppll_vit_stage_block_forward(ppll_vit_stage* st, int B, const void* x_in, void* h_out,
+                                 void* stream) {
+  if (!st || B < 1 || B > st->Bmax || !x_in || (!h_out && st->n_aux)) {
+    set_error("ppll_vit_stage_block_forward: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool head = h_out == nullptr;
+  return st->dtype == PPLL_F32
+             ? vit_forward<float>(st, B, x_in, h_out, head, s, st->n_block)
+             : vit_forward<__nv_bfloat16>(st, B, x_in, h_out, head, s, st->n_block);
+}
+
+// Backward through the block from dLoss/d(block output) `g_out`, or — final
+// stage, labels != NULL — from the task loss; dLoss/d(block input) into
+// `g_in` (NULL for stage 0); then the optimizer over the BLOCK parameters only
+// (patch embedding + block layers; + the task head on the final stage).  The
+// step counter advances.
+int ppll_vit_stage_block_backward(ppll_vit_stage* st, int B, const void* x_in, const void* g_out,
+                                  const int64_t* labels, void* g_in, void* stream) {
+  if (!st || B < 1 || B > st->Bmax || !x_in || (!g_out && !labels) || (labels && st->n_aux)) {
+    set_error("ppll_vit_stage_block_backward: invalid arguments (B=%d)", B);
+    return PPLL_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t nb = labels ? st->n_params
+                            : (st->n_aux ? st->po(st->n_block, 0) : st->ho(0));
+  int r = st->dtype == PPLL_F32
+              ? vit_backward<float>(st, B, x_in, labels, g_out, g_in, st->n_block, s)
+              : vit_backward<__nv_bfloat16>(st, B, x_in, labels, g_out, g_in, st->n_block, s);
+  if (r) return r;
+  return vit_update(st, nb, s);
 }
 
 }  // extern "C"

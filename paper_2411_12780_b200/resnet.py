@@ -230,6 +230,16 @@ class ResLocalModule(LocalModule):
         N.check(N.load().ppll_resnet_stage_forward(self.native(B), B, x_ptr, h_ptr, logits_ptr,
                                                    stream), f"resnet stage {self.stage_index} forward")
 
+    # -- the E2E / naive-PP baselines (runtime.py:248-284, 359-382) ---------
+    def launch_block_forward(self, B, x_ptr, h_ptr, stream) -> None:
+        N.check(N.load().ppll_resnet_stage_block_forward(self.native(B), B, x_ptr, h_ptr, stream),
+                f"resnet stage {self.stage_index} block forward")
+
+    def launch_block_backward(self, B, x_ptr, gout_ptr, y_ptr, gin_ptr, stream) -> None:
+        N.check(N.load().ppll_resnet_stage_block_backward(self.native(B), B, x_ptr, gout_ptr,
+                                                          y_ptr, gin_ptr, stream),
+                f"resnet stage {self.stage_index} block backward")
+
     def __repr__(self) -> str:
         return (f"ResLocalModule(stage={self.stage_index}, blocks={self.block_ids}, "
                 f"aux_convs={self.n_aux_convs}, precision={self.precision})")

@@ -287,8 +287,8 @@ def _run_backprop(modules, dataset_iter, config, pipelined: bool, virtual_time: 
     s = len(mods)
     for m in mods:
         if not getattr(m, "supports_e2e", False):
-            raise InvalidMode(f"E2E / NaivePP are built for the reference's MLP blocks; "
-                              f"{type(m).__name__} runs PPLL only")
+            raise InvalidMode(f"{type(m).__name__} has no block-only forward/backward; "
+                              f"it runs PPLL only")
     metrics = EpochMetrics(n_stages=s)
     step0 = [m.optimizer.step_count for m in mods]
     dev0 = mods[0].device

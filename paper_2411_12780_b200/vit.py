@@ -252,6 +252,16 @@ class VitLocalModule(LocalModule):
         N.check(N.load().ppll_vit_stage_forward(self.native(B), B, x_ptr, h_ptr, logits_ptr,
                                                 stream), f"vit stage {self.stage_index} forward")
 
+    # -- the E2E / naive-PP baselines (runtime.py:248-284, 359-382) ---------
+    def launch_block_forward(self, B, x_ptr, h_ptr, stream) -> None:
+        N.check(N.load().ppll_vit_stage_block_forward(self.native(B), B, x_ptr, h_ptr, stream),
+                f"vit stage {self.stage_index} block forward")
+
+    def launch_block_backward(self, B, x_ptr, gout_ptr, y_ptr, gin_ptr, stream) -> None:
+        N.check(N.load().ppll_vit_stage_block_backward(self.native(B), B, x_ptr, gout_ptr, y_ptr,
+                                                       gin_ptr, stream),
+                f"vit stage {self.stage_index} block backward")
+
     def __repr__(self) -> str:
         return (f"VitLocalModule(stage={self.stage_index}, layers={self.n_block_layers}, "
                 f"aux_layers={self.n_aux_layers}, precision={self.precision})")

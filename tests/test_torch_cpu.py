@@ -110,3 +110,44 @@ def test_adamw_rule_matches_torch_optim_adamw():
         state = opt.state_dict()
     for p, q in zip(ts.params, ref):
         np.testing.assert_allclose(p.detach().numpy(), q.detach().numpy(), rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("tag", ["s2", "s4", "s3"])
+def test_e2e_step_matches_reference_e2e(tag):
+    """tc.e2e_step (autograd through the chained blocks) against the
+    reference's own E2E / naive-PP runs (tests/golden/e2e_naive.npz, generated
+    by importing the reference): this pins the checker the ViT / ResNet E2E
+    GPU tests use."""
+    import os
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "e2e_naive.npz"))
+    dims = tuple(int(d) for d in z[f"{tag}_dims"])
+    s = int(z[f"{tag}_s"])
+    stages = orc.build_stages(dims, orc.partition(dims, s), 2, 3, 42)
+    tst = [tc.from_mlp(copy.deepcopy(st), torch.float64) for st in stages]
+    losses = [tc.e2e_step(tst, x, y, 0.05, 0.001, 10, 0.9, 1e-4)
+              for x, y in zip(z[f"{tag}_xs"], z[f"{tag}_ys"])]
+    np.testing.assert_allclose(losses, z[f"{tag}_losses"], rtol=0, atol=1e-12)
+    for j, ts in enumerate(tst):
+        f = np.concatenate([p.detach().numpy().ravel() for p in ts.params])
+        np.testing.assert_allclose(f, z[f"{tag}_final_{j}"], rtol=0, atol=1e-12)
+        assert ts.step_count == int(z[f"{tag}_step_{j}"])
+
+
+def test_e2e_step_vit_resnet_leave_aux_untouched():
+    """E2E through ViT / ResNet stages: aux parameters never move, block
+    parameters do."""
+    vspec = vo.VitSpec(image=8, channels=3, patch=4, dim=128, heads=2, mlp=256, depth=3, classes=5)
+    rspec = ro.ResNetSpec(n=1, image=8, channels=3, widths=(16, 32, 64), classes=5)
+    cases = [([tc.from_vit(s) for s in vo.build_vit_stages(vspec, [1, 1, 1], 1, 2, 7)],
+              np.random.default_rng(0).standard_normal((4, 3, 8, 8))),
+             ([tc.from_resnet(s) for s in ro.build_resnet_stages(rspec, 3, 1, 2, 7)],
+              np.random.default_rng(0).standard_normal((4, 8, 8, 3)))]
+    for tst, x in cases:
+        before = [[p.detach().clone() for p in ts.params] for ts in tst]
+        tc.e2e_step(tst, x, np.array([0, 1, 2, 3]), 0.05, 0.001, 4, 0.9, 1e-4)
+        for j, ts in enumerate(tst):
+            moved = [not torch.equal(a, b) for a, b in zip(before[j], ts.params)]
+            assert any(moved)
+            if j < len(tst) - 1:
+                assert not all(moved)          # aux head parameters are untouched
