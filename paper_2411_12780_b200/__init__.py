@@ -63,8 +63,9 @@ from .runtime import (
 )
 from .tensor import (GradTape, Tensor, active_tape, add, backward, backward_from, bias_add,
                      matmul, relu, scale, softmax_xent, sum_all)
-from .data import (BatchIterator, Dataset, DeviceDataset, IdxDataset, batches, gen_blobs,
-                   gen_spirals, load_idx, spiral_reference)
+from .data import (BatchIterator, Dataset, DeviceDataset, IdxDataset, ImageDataset, batches,
+                   gen_blobs, gen_spirals, load_cifar10, load_idx, load_stl10, load_svhn,
+                   spiral_reference)
 from .costs import (
     CommModel,
     CostEstimate,

@@ -1103,6 +1103,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   const bool plain = !ep.bias && ep.act == kActNone && ep.mask_mode == kMaskNone && !ep.res &&
                      !ep.pre && !ep.C2;
   int cl_bn = 0, cl_cs = 0;
+  static const double dsmem_bpc = getenv("PPLL_DSMEM_BPC") ? atof(getenv("PPLL_DSMEM_BPC")) : 24.0;
   if (plain && force_cl != 0 && K >= 8 * BK) {
     double cl_best = -1;
     const int cb[4] = {256, 192, 128, 64};
@@ -1116,7 +1117,9 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
         if (cap <= 0) continue;
         const double waves = (double)((tiles + cap - 1) / cap);
         const double kb = (double)ceil_div(K, cs * BK);
-        const double t_red = 128.0 * c * 4 / 64.0 + 128.0 * c * 4 / 128.0;   // cycles
+        // partial dump (st.shared, ~128 B/cycle) + the distributed reduction: every
+        // CTA reads one fp32 tile's worth over DSMEM, (cs-1)/cs of it remote
+        const double t_red = 128.0 * c * 4 * (cs - 1) / cs / dsmem_bpc + 128.0 * c * 4 / 128.0;
         const double cost = waves * ((kb * kblock_cycles(c) + t_red) / 1.9e9 + 1.5e-6);
         if (cl_best < 0 || cost < cl_best) { cl_best = cost; cl_bn = c; cl_cs = cs; }
       }

@@ -174,6 +174,99 @@ def load_idx(images_path, labels_path) -> IdxDataset:
     return IdxDataset(features, labels, int(labels.max()) + 1 if n_lbl else 0, pixels=pixels)
 
 
+# ---------------------------------------------------------------------------
+# the image datasets of the paper's configurations (BASELINE configs: CIFAR-10
+# 32x32, SVHN 32x32, STL-10 96x96) in their distribution formats.  The
+# reference ships only the IDX reader above; these follow the same contract
+# (uint8 pixels kept for the 1-B/feature HBM copy, features = pixels / 255 in
+# fp32 — the device's ppll_gather_rows_u8 rounding) and the same error
+# classes.  ``layout`` picks the feature order a family's stage 0 takes:
+# "nchw" (ViT patch embedding, VitLocalModule.in_shape) or "nhwc" (ResNet,
+# ResNetLocalModule.in_shape).
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ImageDataset(IdxDataset):
+    """An image dataset: ``pixels`` [N x C·H·W] uint8 in ``layout`` order."""
+
+    shape: tuple = (0, 0, 0)          # (C, H, W)
+    layout: str = "nchw"
+
+
+def _image_dataset(chw: np.ndarray, labels: np.ndarray, classes: int, layout: str) -> ImageDataset:
+    """chw: uint8 [N, C, H, W] -> ImageDataset in the requested layout."""
+    if layout not in ("nchw", "nhwc"):
+        raise InvalidArg(f"layout must be 'nchw' or 'nhwc', got {layout!r}")
+    n, c, h, w = chw.shape
+    arr = chw if layout == "nchw" else chw.transpose(0, 2, 3, 1)
+    pixels = np.ascontiguousarray(arr).reshape(n, c * h * w)
+    features = (pixels.astype(np.float64) / 255.0).astype(np.float32)
+    return ImageDataset(features, labels.astype(np.int64), classes, pixels=pixels,
+                        shape=(c, h, w), layout=layout)
+
+
+def load_cifar10(paths, layout: str = "nchw", cifar100: bool = False) -> ImageDataset:
+    """CIFAR-10 (or -100) binary batches (``data_batch_*.bin`` /
+    ``test_batch.bin``): records of a label byte (CIFAR-100: coarse + fine,
+    the fine label is used) followed by 3072 bytes — the red, green and blue
+    32x32 planes, row-major.  ``paths``: one file or a list (concatenated)."""
+    if isinstance(paths, (str, Path)):
+        paths = [paths]
+    lb = 2 if cifar100 else 1
+    rec = lb + 3072
+    imgs, labels = [], []
+    for p in paths:
+        raw = Path(p).read_bytes()
+        if len(raw) == 0 or len(raw) % rec:
+            raise TruncatedFile(f"{p}: {len(raw)} bytes is not a whole number of "
+                                f"{rec}-byte records")
+        a = np.frombuffer(raw, dtype=np.uint8).reshape(-1, rec)
+        labels.append(a[:, lb - 1])
+        imgs.append(a[:, lb:].reshape(-1, 3, 32, 32))
+    y = np.concatenate(labels)
+    classes = 100 if cifar100 else 10
+    if y.max() >= classes:
+        raise InvalidArg(f"label {int(y.max())} outside [0, {classes})")
+    return _image_dataset(np.concatenate(imgs), y, classes, layout)
+
+
+def load_svhn(path, layout: str = "nchw") -> ImageDataset:
+    """SVHN cropped digits (``train_32x32.mat`` / ``test_32x32.mat``, MATLAB
+    v5): ``X`` uint8 [32, 32, 3, N], ``y`` [N, 1] with the digit 0 stored as
+    label 10 (mapped back to 0)."""
+    from scipy.io import loadmat
+    try:
+        m = loadmat(str(path))
+    except (ValueError, TypeError, OSError) as e:
+        raise TruncatedFile(f"{path}: not a readable MATLAB v5 file ({e})") from e
+    if "X" not in m or "y" not in m:
+        raise InvalidArg(f"{path}: expected variables X and y")
+    x, y = np.asarray(m["X"]), np.asarray(m["y"]).reshape(-1).astype(np.int64)
+    if x.ndim != 4 or x.shape[2] != 3 or x.shape[3] != y.size:
+        raise CountMismatch(f"{path}: X {x.shape} does not match {y.size} labels")
+    y = np.where(y == 10, 0, y)
+    if y.min() < 0 or y.max() > 9:
+        raise InvalidArg(f"{path}: labels outside [1, 10]")
+    return _image_dataset(np.ascontiguousarray(x.transpose(3, 2, 0, 1)), y, 10, layout)
+
+
+def load_stl10(x_path, y_path, layout: str = "nchw") -> ImageDataset:
+    """STL-10 binary (``train_X.bin`` / ``train_y.bin``): images uint8
+    [N, 3, 96, 96] with each channel plane stored column-major, labels 1..10
+    (mapped to 0..9)."""
+    raw = Path(x_path).read_bytes()
+    per = 3 * 96 * 96
+    if len(raw) == 0 or len(raw) % per:
+        raise TruncatedFile(f"{x_path}: {len(raw)} bytes is not a whole number of images")
+    x = np.frombuffer(raw, dtype=np.uint8).reshape(-1, 3, 96, 96).transpose(0, 1, 3, 2)
+    y = np.frombuffer(Path(y_path).read_bytes(), dtype=np.uint8).astype(np.int64)
+    if y.size != x.shape[0]:
+        raise CountMismatch(f"{x.shape[0]} images but {y.size} labels")
+    if y.size and (y.min() < 1 or y.max() > 10):
+        raise InvalidArg(f"{y_path}: labels outside [1, 10]")
+    return _image_dataset(np.ascontiguousarray(x), y - 1, 10, layout)
+
+
 def _order(n: int, shuffle: bool, seed: int) -> np.ndarray:
     """The epoch's row order (data.py:155-158)."""
     return np.random.default_rng(seed).permutation(n) if shuffle else np.arange(n)
