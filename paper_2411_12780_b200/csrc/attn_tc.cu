@@ -18,77 +18,23 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "vit.cuh"
+#include "ptx.cuh"
 
 namespace ppll {
 namespace atc {
 
 constexpr int kDh = 64;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                            int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
+using namespace ptx;
 __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
+  return umma_desc_sw128(saddr, lbo, sbo);
 }
 __device__ __forceinline__ uint32_t idesc(int M, int N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
+  return umma_idesc_bf16(M, N, a_mn, b_mn);
 }
 __device__ __forceinline__ void ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  tmem_ld16(taddr, r);
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
@@ -235,8 +181,8 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     const uint32_t id = idesc(128, NK, false, false);
     const uint32_t aq = smem_u32(sQ), ak = smem_u32(sK);
 #pragma unroll
-    for (int j = 0; j < kDh / 16; ++j) mma(tm, kmaj_tile(aq, j), kmaj_tile(ak, j), id, j > 0);
-    commit(&bar[1]);
+    for (int j = 0; j < kDh / 16; ++j) mma_bf16(tm, kmaj_tile(aq, j), kmaj_tile(ak, j), id, j > 0);
+    mma_commit(&bar[1]);
   }
   mbar_wait(&bar[1], 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -274,8 +220,8 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t id = idesc(128, kDh, false, true);
     const uint32_t ap = smem_u32(sP), av = smem_u32(sV);
-    for (int j = 0; j < NK / 16; ++j) mma(tm, kmaj_keys(ap, j), mnmaj_tile(av, j), id, j > 0);
-    commit(&bar[1]);
+    for (int j = 0; j < NK / 16; ++j) mma_bf16(tm, kmaj_keys(ap, j), mnmaj_tile(av, j), id, j > 0);
+    mma_commit(&bar[1]);
   }
   mbar_wait(&bar[1], 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -355,10 +301,10 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     const uint32_t id = idesc(128, NK, false, false);
     const uint32_t aq = smem_u32(sQ), ak = smem_u32(sK), av = smem_u32(sV), ad = smem_u32(sdO);
 #pragma unroll
-    for (int j = 0; j < kDh / 16; ++j) mma(tm, kmaj_tile(aq, j), kmaj_tile(ak, j), id, j > 0);
+    for (int j = 0; j < kDh / 16; ++j) mma_bf16(tm, kmaj_tile(aq, j), kmaj_tile(ak, j), id, j > 0);
 #pragma unroll
-    for (int j = 0; j < kDh / 16; ++j) mma(tm + 128, kmaj_tile(ad, j), kmaj_tile(av, j), id, j > 0);
-    commit(&bar[1]);
+    for (int j = 0; j < kDh / 16; ++j) mma_bf16(tm + 128, kmaj_tile(ad, j), kmaj_tile(av, j), id, j > 0);
+    mma_commit(&bar[1]);
   }
   // D_i = rowsum(dO ⊙ O) from global rows while the MMAs run
   const int r = tid;
@@ -404,13 +350,13 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     const uint32_t aq = smem_u32(sQ), ak = smem_u32(sK), ad = smem_u32(sdO);
     const uint32_t id_mn = idesc(128, kDh, true, true);
     // dV = Pᵀ·dO  (M = keys, K = queries)
-    for (int j = 0; j < 8; ++j) mma(tm + 0, mnmaj_rows(ap, j), mnmaj_tile(ad, j), id_mn, j > 0);
+    for (int j = 0; j < 8; ++j) mma_bf16(tm + 0, mnmaj_rows(ap, j), mnmaj_tile(ad, j), id_mn, j > 0);
     // dK = dSᵀ·Q
-    for (int j = 0; j < 8; ++j) mma(tm + 64, mnmaj_rows(as, j), mnmaj_tile(aq, j), id_mn, j > 0);
+    for (int j = 0; j < 8; ++j) mma_bf16(tm + 64, mnmaj_rows(as, j), mnmaj_tile(aq, j), id_mn, j > 0);
     // dQ = dS·K   (M = queries, K = keys)
     const uint32_t id_k = idesc(128, kDh, false, true);
-    for (int j = 0; j < NK / 16; ++j) mma(tm + 128, kmaj_keys(as, j), mnmaj_tile(ak, j), id_k, j > 0);
-    commit(&bar[1]);
+    for (int j = 0; j < NK / 16; ++j) mma_bf16(tm + 128, kmaj_keys(as, j), mnmaj_tile(ak, j), id_k, j > 0);
+    mma_commit(&bar[1]);
   }
   mbar_wait(&bar[1], 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
