@@ -371,7 +371,8 @@ template <typename TO, bool A_K, bool B_K, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ CUtensorMap map_b, int M, int N, int K, int mt,
-                       int kps, TO* __restrict__ C, long ldc, int vec, float* __restrict__ db) {
+                       int kps, TO* __restrict__ C, long ldc, int vec, float* __restrict__ db,
+                       unsigned long long* __restrict__ tl) {
   using L = Smem<BN>;
   constexpr int S = L::STAGES;
   static_assert(S * L::STAGE >= BM * BN * 4, "reduction buffer must fit in the operand ring");
@@ -419,6 +420,10 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
   const uint32_t tmem = *tmem_slot;
   // prologue (barriers, TMEM, tensor-map prefetch) overlaps the predecessor's tail
   pdl_entry();
+  // timeline probe (PPLL_GEMM_TIMELINE): per CTA, %globaltimer at start / first
+  // operands landed / mainloop done / partial dumped + cluster barrier /
+  // reduction done / exit
+  if (tl && threadIdx.x == 0) tl[blockIdx.x * 8 + 0] = gtimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -454,6 +459,7 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
       for (int k0 = kbeg; k0 < kend; k0 += BK, ++kb) {
         const int st = kb % S;
         mbar_wait(&full[st], (kb / S) & 1);
+        if (tl && kb == 0) tl[blockIdx.x * 8 + 1] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sa = smem_u32(smem + st * L::STAGE);
         const uint32_t sb = sa + L::A_BYTES;
@@ -515,6 +521,7 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
     // free and becomes this CTA's fp32 partial tile
     const int q = warp & 3, grp = (warp - 2) >> 2;
     mbar_wait(&tfull[0], 0);
+    if (tl && warp == 2 && lane == 0) tl[blockIdx.x * 8 + 2] = gtimer();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int r = q * 32 + lane;
     float* row = red + (long)r * BN;
@@ -532,6 +539,7 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();
+  if (tl && threadIdx.x == 0) tl[blockIdx.x * 8 + 3] = gtimer();
   // ---- distributed reduction: this CTA owns rows [rank·R, rank·R + R) ----
   {
     const int R = (BM + CS - 1) / CS;
@@ -577,7 +585,9 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
         if (n0 + 4 * c + j < N) db[n0 + 4 * c + j] = e[j];
     }
   }
+  if (tl && threadIdx.x == 0) tl[blockIdx.x * 8 + 4] = gtimer();
   cluster_sync();   // peers may still be reading this CTA's partial until here
+  if (tl && threadIdx.x == 0) tl[blockIdx.x * 8 + 5] = gtimer();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
@@ -587,6 +597,7 @@ gemm_tc_cluster_kernel(const __grid_constant__ CUtensorMap map_a,
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+static unsigned long long* cluster_tl();
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -827,7 +838,7 @@ static int run_cluster(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = cluster_cfg<TO, A_K, B_K, BN>(tiles * cs, cs, s, at);
   PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_cluster_kernel<TO, A_K, B_K, BN>, ma, mb, M, N,
-                                     K, mt, kps, C, ldc, vec, db));
+                                     K, mt, kps, C, ldc, vec, db, cluster_tl()));
   note_launch();
   return PPLL_OK;
 }
@@ -859,6 +870,11 @@ static int capacity_any(bool ak, bool bk, int bn, int cs) {
   return cluster_capacity_bn<TO, false, true>(bn, cs);
 }
 
+unsigned long long* timeline_buffer();
+static unsigned long long* cluster_tl() {
+  static const int on = getenv("PPLL_GEMM_TIMELINE") ? 1 : 0;
+  return on ? timeline_buffer() : nullptr;
+}
 unsigned long long* timeline_buffer() {
   static unsigned long long* buf = nullptr;
   if (!buf && cudaMalloc(&buf, kNumSMs * 4 * 4 * 8) != cudaSuccess) buf = nullptr;
