@@ -56,6 +56,15 @@ uint64_t ppll_launch_count(void);
 void ppll_set_gemm_engine(int engine);
 /* ViT attention engine: 0 = tcgen05 when supported (bf16, T <= 128), 1 = SIMT */
 void ppll_set_attn_engine(int engine);
+/* Multi-head self-attention of the ViT blocks (no reference counterpart; the
+ * reference's blocks are MLPs): qkv [B*T, 3*H*64] bf16 (q | k | v column
+ * blocks), o [B*T, H*64] bf16, lse [B*H*T] fp32 (row log-sum-exp kept for the
+ * backward).  Backward: dqkv [B*T, 3*H*64] from dout; bias_part (optional,
+ * fp32 [B, 3*H*64]) receives the per-image column sums of dqkv (the qkv bias
+ * gradient before the sum over images).  tcgen05 kernels, T <= 128. */
+int ppll_attn_fwd_bf16(int B, int T, int H, const void* qkv, void* o, float* lse, void* stream);
+int ppll_attn_bwd_bf16(int B, int T, int H, const void* qkv, const void* o, const void* dout,
+                       const float* lse, void* dqkv, float* bias_part, void* stream);
 /* profiling hook: device buffer of the GEMM timeline probe (PPLL_GEMM_TIMELINE
  * set): 148 CTAs x 4 tiles x {MMA start, MMA done, epilogue done, -} u64 ns */
 void* ppll_gemm_timeline(void);

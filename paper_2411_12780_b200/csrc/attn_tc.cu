@@ -71,56 +71,6 @@ __device__ __forceinline__ void store_chunk16(uint8_t* buf, int r, int c16, cons
   }
 }
 
-// Warp transpose-reduce of 64 per-lane values: after 5 halving rounds lane L
-// holds the warp-wide sums of columns col_of_lane(L) and col_of_lane(L) + 1.
-__device__ __forceinline__ int col_of_lane(int L) {
-  return ((L >> 4) & 1) * 32 + ((L >> 3) & 1) * 16 + ((L >> 2) & 1) * 8 + ((L >> 1) & 1) * 4 +
-         (L & 1) * 2;
-}
-__device__ __forceinline__ float2 warp_colsum64(const float (&v)[64], int lane) {
-  float a[32];
-  {
-    const bool hi = lane & 16;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float keep = hi ? v[j + 32] : v[j], send = hi ? v[j] : v[j + 32];
-      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-  }
-  float b[16];
-  {
-    const bool hi = lane & 8;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float keep = hi ? a[j + 16] : a[j], send = hi ? a[j] : a[j + 16];
-      b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-  }
-  float c[8];
-  {
-    const bool hi = lane & 4;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float keep = hi ? b[j + 8] : b[j], send = hi ? b[j] : b[j + 8];
-      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-  }
-  float d[4];
-  {
-    const bool hi = lane & 2;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float keep = hi ? c[j + 4] : c[j], send = hi ? c[j] : c[j + 4];
-      d[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-  }
-  const bool hi = lane & 1;
-  const float k0 = hi ? d[2] : d[0], s0 = hi ? d[0] : d[2];
-  const float k1 = hi ? d[3] : d[1], s1 = hi ? d[1] : d[3];
-  return make_float2(k0 + __shfl_xor_sync(0xffffffffu, s0, 1),
-                     k1 + __shfl_xor_sync(0xffffffffu, s1, 1));
-}
-
 struct Maps {
   CUtensorMap qkv128;   // box {64, 128} over [tokens, 3D]
   CUtensorMap qkvK;     // box {64, NK}
@@ -247,16 +197,66 @@ attn_tc_fwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
 }
 
 // ----------------------------------------------------------------- backward
-__global__ void __launch_bounds__(128, 2)
+// Warp transpose-reduce of 32 per-lane values: lane L ends with the warp-wide
+// sum of column L (five halving rounds, fixed order).
+__device__ __forceinline__ float warp_colsum32(const float (&v)[32], int lane) {
+  float a[16];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float keep = hi ? v[j + 16] : v[j], send = hi ? v[j] : v[j + 16];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  float b[8];
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float keep = hi ? a[j + 8] : a[j], send = hi ? a[j] : a[j + 8];
+      b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  float c[4];
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float keep = hi ? b[j + 4] : b[j], send = hi ? b[j] : b[j + 4];
+      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  float d[2];
+  {
+    const bool hi = lane & 2;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float keep = hi ? c[j + 2] : c[j], send = hi ? c[j] : c[j + 2];
+      d[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+  }
+  const bool hi = lane & 1;
+  return (hi ? d[1] : d[0]) + __shfl_xor_sync(0xffffffffu, hi ? d[0] : d[1], 1);
+}
+
+// 256 threads: two warps per TMEM lane quadrant (warps w and w + 4 own the
+// same 32 query / key rows) split the columns of every per-row phase — the
+// D_i dot product, the P / dS chunks, the dQ / dK / dV read-out and stores and
+// the fused bias sums — so each row's serial work is halved and an SM holds
+// 16 warps (two CTAs) to hide the TMA / MMA / TMEM latencies.
+constexpr int kBwdThreads = 256;
+__global__ void __launch_bounds__(kBwdThreads, 2)
 attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
-                   const __grid_constant__ CUtensorMap mdo, int Tn, int H, int NK,
+                   const __grid_constant__ CUtensorMap mdo, const __grid_constant__ CUtensorMap mo,
+                   int Tn, int H, int NK,
                    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                    const float* __restrict__ lse, __nv_bfloat16* __restrict__ dqkv, float scale,
                    float* __restrict__ bias_part) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base0 = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + ((1024 - (base0 & 1023)) & 1023);
-  // ~107 KB so two CTAs share an SM: K holds only its NK rows, and V (dead
+  // ~108 KB so two CTAs share an SM: K holds only its NK rows, and V (dead
   // once dP = dO·Vᵀ has retired) lives in dS's second 64-key atom, which is
   // written only after that MMA completes.
   const int kbytes = (NK * 128 + 1023) & ~1023;
@@ -268,7 +268,9 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   uint8_t* sV = sdS + 16384;        // NK rows, aliases dS keys 64..127
   uint64_t* bar = reinterpret_cast<uint64_t*>(sdS + 32768);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  float* scr = reinterpret_cast<float*>(sdS + 32768 + 64);   // [2][128] D_i halves
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int half = warp >> 2;
   const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int D = H * kDh;
   if (tid == 0) {
@@ -290,12 +292,16 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   pdl_entry();
   const int row0 = b * Tn;
   // TMEM columns: S [0,128), dP [128,256); later dV [0,64), dK [64,128), dQ [128,192)
+  // O arrives by TMA too, into the P buffer (P is written only after the
+  // D_i pass below has read O and every thread has passed a barrier)
+  uint8_t* sO = sP;
   if (tid == 0) {
-    mbar_expect_tx(&bar[0], 2 * 16384 + 2 * NK * 128);
+    mbar_expect_tx(&bar[0], 3 * 16384 + 2 * NK * 128);
     tma_load_2d(&mq, &bar[0], sQ, h * kDh, row0);
     tma_load_2d(&mk, &bar[0], sK, D + h * kDh, row0);
     tma_load_2d(&mk, &bar[0], sV, 2 * D + h * kDh, row0);
     tma_load_2d(&mdo, &bar[0], sdO, h * kDh, row0);
+    tma_load_2d(&mo, &bar[0], sO, h * kDh, row0);
     mbar_wait(&bar[0], 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t id = idesc(128, NK, false, false);
@@ -306,31 +312,52 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
     for (int j = 0; j < kDh / 16; ++j) mma_bf16(tm + 128, kmaj_tile(ad, j), kmaj_tile(av, j), id, j > 0);
     mma_commit(&bar[1]);
   }
-  // D_i = rowsum(dO ⊙ O) from global rows while the MMAs run
-  const int r = tid;
-  float Di = 0.f;
-  if (r < Tn) {
-    const __nv_bfloat16* orow = o + (long)(row0 + r) * D + h * kDh;
-    const __nv_bfloat16* grow = dout + (long)(row0 + r) * D + h * kDh;
-    float a[32], g[32];
+  // D_i = rowsum(dO ⊙ O) from the swizzled smem tiles while the MMAs run;
+  // each half of the CTA sums 32 of the 64 columns (four 16-B chunks), the
+  // halves are added in fixed order
+  const int r = (warp & 3) * 32 + lane;
+  const bool live = r < Tn;
+  const float lr = live ? lse[(long)blockIdx.x * Tn + r] : 0.f;
+  mbar_wait(&bar[0], 0);
+  {
+    float part = 0.f;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      ld_row32<__nv_bfloat16>(orow + 32 * half, true, 32, a);
-      ld_row32<__nv_bfloat16>(grow + 32 * half, true, 32, g);
+    for (int j = 0; j < 4; ++j) {
+      const int off = r * 128 + (((4 * half + j) ^ (r & 7)) << 4);
+      const uint4 qo = *reinterpret_cast<const uint4*>(sO + off);
+      const uint4 qd = *reinterpret_cast<const uint4*>(sdO + off);
+      const __nv_bfloat162* ho = reinterpret_cast<const __nv_bfloat162*>(&qo);
+      const __nv_bfloat162* hd = reinterpret_cast<const __nv_bfloat162*>(&qd);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) Di = fmaf(a[i], g[i], Di);
+      for (int e = 0; e < 4; ++e) {
+        const float2 a = __bfloat1622float2(ho[e]), g = __bfloat1622float2(hd[e]);
+        part = fmaf(a.x, g.x, part);
+        part = fmaf(a.y, g.y, part);
+      }
     }
+    scr[half * 128 + r] = live ? part : 0.f;
   }
-  const float lr = r < Tn ? lse[(long)blockIdx.x * Tn + r] : 0.f;
+  __syncthreads();
+  const float Di = scr[r] + scr[128 + r];
   mbar_wait(&bar[1], 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t lane_base = tm + ((uint32_t)(warp * 32) << 16);
-  const bool live = r < Tn;
-  for (int c = 0; c < 128; c += 16) {
+  const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16);
+  // P / dS chunks of 16 keys, interleaved between the halves
+  for (int c = 16 * half; c < 128; c += 32) {
     float p[16], ds[16];
     if (c < NK) {
-      ld16(lane_base + c, p);
-      ld16(lane_base + 128 + c, ds);
+      uint32_t rp[16], rd[16];
+      tmem_ld16_nw(lane_base + c, rp);
+      tmem_ld16_nw(lane_base + 128 + c, rd);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        p[i] = __uint_as_float(rp[i]);
+        ds[i] = __uint_as_float(rd[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) p[i] = ds[i] = 0.f;
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -361,40 +388,38 @@ attn_tc_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant
   mbar_wait(&bar[1], 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const long ld = 3L * D;
-  float v[64];
-  // lane r holds: dV[key r], dK[key r], dQ[query r]
+  float* red = reinterpret_cast<float*>(sP);   // P is dead: bias-sum scratch [8 warps][32]
+  // lane r holds: dV[key r], dK[key r], dQ[query r]; this half: columns 32·half ..
 #pragma unroll
   for (int part = 0; part < 3; ++part) {
-    const uint32_t col = part == 0 ? 0u : (part == 1 ? 64u : 128u);
+    const uint32_t col = (part == 0 ? 0u : (part == 1 ? 64u : 128u)) + 32u * half;
+    float v[32];
+    {
+      uint32_t ra[16], rb[16];
+      tmem_ld16_nw(lane_base + col, ra);
+      tmem_ld16_nw(lane_base + col + 16, rb);
+      tmem_wait_ld();
+      const float sc = part == 0 ? 1.f : scale;
 #pragma unroll
-    for (int c = 0; c < 64; c += 16) ld16(lane_base + col + c, v + c);
-    const float sc = part == 0 ? 1.f : scale;
-    const int off = part == 0 ? 2 * D : (part == 1 ? D : 0);
-#pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = r < Tn ? v[i] * sc : 0.f;
-    if (r < Tn) {
-      __nv_bfloat16* dst = dqkv + (long)(row0 + r) * ld + off + h * kDh;
-      float v32[32];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v32[i] = v[32 * hh + i];
-        st_row32<__nv_bfloat16>(dst + 32 * hh, true, 32, v32);
+      for (int i = 0; i < 16; ++i) {
+        v[i] = live ? __uint_as_float(ra[i]) * sc : 0.f;
+        v[16 + i] = live ? __uint_as_float(rb[i]) * sc : 0.f;
       }
     }
+    const int off = (part == 0 ? 2 * D : (part == 1 ? D : 0)) + h * kDh + 32 * half;
+    if (live) st_row32<__nv_bfloat16>(dqkv + (long)(row0 + r) * ld + off, true, 32, v);
     if (bias_part) {
-      // fused bias gradient: Σ over this image's rows of the 64 columns, as a
-      // warp transpose-reduce (lane keeps 2 columns) then a fixed-order sum of
-      // the 4 warps; partial row b of a [batch, 3D] matrix
-      float2 cs = warp_colsum64(v, r & 31);
-      float* red = reinterpret_cast<float*>(sP);
-      const int cb = col_of_lane(r & 31);
-      red[warp * 64 + cb] = cs.x;
-      red[warp * 64 + cb + 1] = cs.y;
+      // fused bias gradient: Σ over this image's rows of the 32 columns, as a
+      // warp transpose-reduce (lane = column) then a fixed-order sum over the
+      // four row quadrants; partial row b of a [batch, 3D] matrix
+      red[warp * 32 + lane] = warp_colsum32(v, lane);
       __syncthreads();
-      if (tid < 64)
-        bias_part[(long)b * ld + off + h * kDh + tid] =
-            ((red[tid] + red[64 + tid]) + red[128 + tid]) + red[192 + tid];
+      if (warp == 0 || warp == 4) {
+        const int w0 = warp;   // quadrants w0 .. w0 + 3 of this half
+        bias_part[(long)b * ld + off + lane] =
+            ((red[w0 * 32 + lane] + red[(w0 + 1) * 32 + lane]) + red[(w0 + 2) * 32 + lane]) +
+            red[(w0 + 3) * 32 + lane];
+      }
       __syncthreads();
     }
   }
@@ -434,8 +459,10 @@ constexpr int kFwdSmem = 16384 * 2 + 32768 + 1024 + 64;   // upper bound (NK = 1
 inline int fwd_smem(int NK) {
   return (NK <= 64 ? 16384 : 32768) + 2 * ((NK * 128 + 1023) & ~1023) + 1024 + 64;
 }
-constexpr int kBwdSmem = 16384 * 3 + 32768 * 2 + 1024 + 64;   // upper bound (NK = 128)
-inline int bwd_smem(int NK) { return 16384 * 2 + ((NK * 128 + 1023) & ~1023) + 32768 * 2 + 1024 + 64; }
+constexpr int kBwdSmem = 16384 * 3 + 32768 * 2 + 1024 + 64 + 1024;   // upper bound (NK = 128)
+inline int bwd_smem(int NK) {
+  return 16384 * 2 + ((NK * 128 + 1023) & ~1023) + 32768 * 2 + 1024 + 64 + 1024;
+}
 
 }  // namespace atc
 
@@ -471,10 +498,11 @@ int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __n
                        cudaStream_t s, float* bias_part) {
   using namespace atc;
   const int D = H * kDh, NK = (Tn + 15) / 16 * 16;
-  CUtensorMap mq, mk, md;
+  CUtensorMap mq, mk, md, mo;
   if (!map2d(&mq, qkv, 3L * D, (long)B * Tn, 3L * D, 128) ||
       !map2d(&mk, qkv, 3L * D, (long)B * Tn, 3L * D, NK) ||
-      !map2d(&md, dout, (long)D, (long)B * Tn, (long)D, 128)) {
+      !map2d(&md, dout, (long)D, (long)B * Tn, (long)D, 128) ||
+      !map2d(&mo, o, (long)D, (long)B * Tn, (long)D, 128)) {
     set_error("attention: tensor map encode failed");
     return PPLL_ERR_CUDA;
   }
@@ -484,7 +512,7 @@ int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __n
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
     set = true;
   }
-  launch_k(attn_tc_bwd_kernel, B * H, 128, bwd_smem(NK), s, mq, mk, md, Tn, H, NK, o, dout, lse, dqkv,
+  launch_k(attn_tc_bwd_kernel, B * H, kBwdThreads, bwd_smem(NK), s, mq, mk, md, mo, Tn, H, NK, o, dout, lse, dqkv,
                                                   1.0f / sqrtf((float)kDh), bias_part);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -494,3 +522,25 @@ int launch_attn_tc_bwd(int B, int Tn, int H, const __nv_bfloat16* qkv, const __n
 }  // namespace ppll
 
 extern "C" void ppll_set_attn_engine(int engine) { ppll::g_attn_engine = engine; }
+
+extern "C" int ppll_attn_fwd_bf16(int B, int T, int H, const void* qkv, void* o, float* lse,
+                                  void* stream) {
+  if (B < 1 || H < 1 || !ppll::attn_tc_supported(T, 64) || !qkv || !o || !lse) {
+    ppll::set_error("ppll_attn_fwd_bf16: unsupported arguments (B=%d T=%d H=%d)", B, T, H);
+    return PPLL_ERR_ARG;
+  }
+  return ppll::launch_attn_tc_fwd(B, T, H, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
+                                  (cudaStream_t)stream);
+}
+
+extern "C" int ppll_attn_bwd_bf16(int B, int T, int H, const void* qkv, const void* o,
+                                  const void* dout, const float* lse, void* dqkv,
+                                  float* bias_part, void* stream) {
+  if (B < 1 || H < 1 || !ppll::attn_tc_supported(T, 64) || !qkv || !o || !dout || !lse || !dqkv) {
+    ppll::set_error("ppll_attn_bwd_bf16: unsupported arguments (B=%d T=%d H=%d)", B, T, H);
+    return PPLL_ERR_ARG;
+  }
+  return ppll::launch_attn_tc_bwd(B, T, H, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)o,
+                                  (const __nv_bfloat16*)dout, lse, (__nv_bfloat16*)dqkv,
+                                  (cudaStream_t)stream, bias_part);
+}
