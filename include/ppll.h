@@ -322,6 +322,14 @@ int ppll_ring_publish(int* ready_word, int seq, void* stream);
 int ppll_ring_wait(const int* ready_word, int seq, void* stream);
 int ppll_ring_release(int* credit_word, void* stream);
 int ppll_ring_wait_credit(const int* credit_word, int need, void* stream);
+/* Ring watchdog (no reference counterpart: the reference's threaded queues
+ * poll a stop flag, runtime.py:411-418): a wait that sees no progress for the
+ * timeout (default 30 s, PPLL_RING_TIMEOUT_MS; <= 0 disables) gives up instead
+ * of hanging the GPU and records the first stall.  ppll_ring_stall returns
+ * 1 if a wait timed out, with out4 = {1, wanted, seen, kind (0 ready, 1
+ * credit)}; clear != 0 re-arms it. */
+void ppll_set_ring_timeout_ms(long long ms);
+int ppll_ring_stall(int* out4, int clear);
 
 /* ---- P2P / IPC plumbing for the multi-GPU ring -------------------------- */
 int ppll_ipc_get_handle(void* dev_ptr, void* handle_out /* 64 bytes */);

@@ -60,6 +60,8 @@ SIGNATURES = {
     "ppll_vit_stage_destroy": (None, [_vp]),
     "ppll_vit_stage_step": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ppll_vit_stage_forward": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "ppll_set_ring_timeout_ms": (None, [C.c_longlong]),
+    "ppll_ring_stall": (_i, [_vp, _i]),
     "ppll_attn_fwd_bf16": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "ppll_attn_bwd_bf16": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ppll_vit_stage_block_forward": (_i, [_vp, _i, _vp, _vp, _vp]),

@@ -287,8 +287,10 @@ int ppll_ring_release(int* credit_word, void* stream) {
   return launch_ring_release(credit_word, S(stream));
 }
 int ppll_ring_wait_credit(const int* credit_word, int need, void* stream) {
-  return launch_ring_wait(credit_word, need, S(stream));
+  return launch_ring_wait(credit_word, need, S(stream), 1);
 }
+void ppll_set_ring_timeout_ms(long long ms) { g_ring_timeout_ns = ms > 0 ? ms * 1000000LL : 0; }
+int ppll_ring_stall(int* out4, int clear) { return ring_stall_read(out4, clear != 0); }
 
 int ppll_ipc_get_handle(void* dev_ptr, void* handle_out) {
   cudaIpcMemHandle_t h;

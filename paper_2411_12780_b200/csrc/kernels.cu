@@ -924,11 +924,37 @@ __global__ void ring_publish_kernel(int* w, int seq) {
   __threadfence_system();
   st_release_sys(w, seq);
 }
-__global__ void ring_wait_kernel(const int* w, int seq) {
+// Watchdog (SURVEY §5 "host watchdog on flag progress"): a wait that sees no
+// progress for `timeout_ns` (%globaltimer) gives up instead of hanging the GPU,
+// and records {stalled, wanted, seen, kind} once in g_ring_stall, which the
+// host reads with ppll_ring_stall() and maps to WorkerPanic.  kind: 0 = ready
+// flag (pop), 1 = credit (backpressure).
+__device__ int g_ring_stall[4];
+__global__ void ring_wait_kernel(const int* w, int seq, long long timeout_ns, int kind) {
   pdl_entry();
-  while (ld_acquire_sys(w) < seq) __nanosleep(64);
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  int v;
+  while ((v = ld_acquire_sys(w)) < seq) {
+    __nanosleep(64);
+    if (timeout_ns > 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if ((long long)(t - t0) > timeout_ns) {
+        if (atomicCAS(&g_ring_stall[0], 0, 1) == 0) {
+          g_ring_stall[1] = seq;
+          g_ring_stall[2] = v;
+          g_ring_stall[3] = kind;
+        }
+        break;
+      }
+    }
+  }
   __threadfence_system();
 }
+long long g_ring_timeout_ns = getenv("PPLL_RING_TIMEOUT_MS")
+                                  ? (long long)atoll(getenv("PPLL_RING_TIMEOUT_MS")) * 1000000LL
+                                  : 30000000000LL;
 __global__ void ring_release_kernel(int* w) {
   pdl_entry();
   __threadfence_system();
@@ -941,8 +967,8 @@ int launch_ring_publish(int* w, int seq, cudaStream_t s) {
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
-int launch_ring_wait(const int* w, int seq, cudaStream_t s) {
-  launch_k(ring_wait_kernel, 1, 1, 0, s, w, seq);
+int launch_ring_wait(const int* w, int seq, cudaStream_t s, int kind) {
+  launch_k(ring_wait_kernel, 1, 1, 0, s, w, seq, g_ring_timeout_ns, kind);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -952,6 +978,17 @@ int launch_ring_release(int* w, cudaStream_t s) {
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
+}
+
+int ring_stall_read(int* out4, bool clear) {
+  int h[4];
+  PPLL_CUDA_CHECK(cudaMemcpyFromSymbol(h, g_ring_stall, sizeof(h)));
+  if (out4) memcpy(out4, h, sizeof(h));
+  if (clear && h[0]) {
+    const int z[4] = {0, 0, 0, 0};
+    PPLL_CUDA_CHECK(cudaMemcpyToSymbol(g_ring_stall, z, sizeof(z)));
+  }
+  return h[0];
 }
 
 }  // namespace ppll

@@ -857,7 +857,11 @@ int launch_count_correct(int B, int C, const void* z, long ldz, int dtype, const
                          unsigned long long* count, cudaStream_t s);
 int launch_relu_mask(long n, const void* g, const void* act, void* out, int dtype, cudaStream_t s);
 int launch_ring_publish(int* w, int seq, cudaStream_t s);
-int launch_ring_wait(const int* w, int seq, cudaStream_t s);
+int launch_ring_wait(const int* w, int seq, cudaStream_t s, int kind = 0);
+// ring-wait watchdog: timeout of every later wait (ns; <= 0 disables) and the
+// first recorded stall {stalled, wanted, seen, kind}
+extern long long g_ring_timeout_ns;
+int ring_stall_read(int* out4, bool clear);
 int launch_ring_release(int* w, cudaStream_t s);
 
 // Host-side description of a fused linear epilogue (see Epilogue).

@@ -364,6 +364,14 @@ class DistributedPipeline:
                 self.mods[j].optimizer.step_count += 1
             self.batches_done = t + 1
         self._drain()
+        stall = (C.c_int * 4)()
+        if lib.ppll_ring_stall(stall, 1):
+            # the device watchdog gave up on a ring wait (a peer stopped
+            # producing or consuming): the same surface as a dead worker
+            # thread in the reference (runtime.py:400-402)
+            what = "ready flag (pop)" if stall[3] == 0 else "credit (backpressure)"
+            raise WorkerPanic(min(self.mods), f"ring wait timed out on the {what}: wanted "
+                                               f"{stall[1]}, saw {stall[2]}")
         out = {"wall": 0.0, "busy": {}, "loss": {}, "errors": {}}
         for j, m in self.mods.items():
             out["errors"][j] = m.error_word()
