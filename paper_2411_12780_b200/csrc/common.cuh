@@ -7,6 +7,7 @@
 
 #include "../../include/ppll.h"
 
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges are no-ops unless a tool attaches
 namespace ppll {
 
 // Sticky per-stage error word bits (checked asynchronously by the host;
@@ -104,6 +105,15 @@ namespace ppll {
 // stream and the calls are no-ops.  The last event is reserved: if a step
 // ever needs more events than the pool holds, the side work is joined and the
 // rest of the step runs on the main stream (always correct, just serial).
+// NVTX range for the host-side enqueue phases of a stage step (visible in ncu
+// --nvtx / nsys timelines; free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct SideFlow {
   cudaStream_t s, ss;
   cudaEvent_t* ev;

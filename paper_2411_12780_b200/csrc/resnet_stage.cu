@@ -206,6 +206,7 @@ static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, 
 template <typename TT>
 static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_out, bool head,
                        cudaStream_t s, bool with_aux = true) {
+  NvtxRange nv("ppll.resnet.forward");
   const void* x = x_in;
   int r;
   if (st->has_stem) {
@@ -273,6 +274,7 @@ static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_o
 template <typename TT>
 static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, const void* g_out,
                         void* g_in, bool with_aux, cudaStream_t s) {
+  NvtxRange nv("ppll.resnet.backward");
   const int C = st->c_out, HW = st->h_out * st->h_out;
   int r;
   static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
@@ -355,6 +357,7 @@ static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, con
 
 // optimizer over the first `n` elements of the flat parameter buffer
 static int res_update(ppll_resnet_stage* st, int64_t n, cudaStream_t s) {
+  NvtxRange nv("ppll.resnet.update");
   return launch_nesterov(n, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
                          st->max_step, 0.f, st->mu, st->wd, st->err, s);

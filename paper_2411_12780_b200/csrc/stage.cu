@@ -157,6 +157,7 @@ static int forward_layers(ppll_stage* st, int B, const void* x_in, void* x_out, 
 
 int ppll_stage_step(ppll_stage* st, int B, const void* x_in, const int64_t* labels, void* x_out,
                     void* stream) {
+  NvtxRange nv("ppll.mlp.step");
   if (!st || B < 1 || B > st->max_batch || !x_in || !labels) {
     set_error("ppll_stage_step: invalid arguments (B=%d)", B);
     return PPLL_ERR_ARG;

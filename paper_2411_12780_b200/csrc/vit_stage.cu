@@ -114,6 +114,7 @@ static int attn_bwd_any(int B, int T, int H, int dh, const TT* qkv, const TT* o,
 template <typename TT>
 static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out, bool head,
                        cudaStream_t s, int nl = -1) {
+  NvtxRange nv("ppll.vit.forward");
   if (nl < 0) nl = st->layers();
   const int T = st->T, D = st->D, F = st->F, H = st->H;
   const int M = B * T;
@@ -196,6 +197,7 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
 template <typename TT>
 static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
                         const void* g_out, void* g_in, int nl, cudaStream_t s) {
+  NvtxRange nv("ppll.vit.backward");
   const int T = st->T, D = st->D, F = st->F, H = st->H, C = st->C;
   const int M = B * T;
   static const bool side_on = !(getenv("PPLL_SIDE_WGRAD") && atoi(getenv("PPLL_SIDE_WGRAD")) == 0);
@@ -330,6 +332,7 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
 
 // optimizer over the first `n` elements of the flat parameter buffer
 static int vit_update(ppll_vit_stage* st, int64_t n, cudaStream_t s) {
+  NvtxRange nv("ppll.vit.update");
   return launch_nesterov(n, st->theta, st->mom, st->grad,
                          reinterpret_cast<__nv_bfloat16*>(st->theta_lp), st->lr_table, st->step,
                          st->max_step, 0.f, st->mu, st->wd, st->err, s);
