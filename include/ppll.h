@@ -322,6 +322,32 @@ int ppll_ring_publish(int* ready_word, int seq, void* stream);
 int ppll_ring_wait(const int* ready_word, int seq, void* stream);
 int ppll_ring_release(int* credit_word, void* stream);
 int ppll_ring_wait_credit(const int* credit_word, int need, void* stream);
+/* ---- normalisation kernels of the extension families (no reference: its
+ * blocks are MLPs, blocks.py:240-255; SURVEY §8b lists them below the
+ * boundary).  Row-major [rows, features], dtype PPLL_F32 or PPLL_BF16;
+ * statistics, gamma / beta and their gradients are fp32.
+ * LayerNorm (eps 1e-5): mean / rstd per row.  Backward: dx (nullable) =
+ * LN-backward(dy) [+ dres]; dg / db (nullable) the gamma / beta gradients;
+ * dxsum (nullable) = Σ_rows dx (the fused bias gradient of the layer below);
+ * ws: ppll_layernorm_bwd_ws_floats(M, D) floats.
+ * BatchNorm (train mode, biased variance, eps 1e-5) over the rows of an NHWC
+ * [P, C] tensor: forward = batch statistics + apply (+ res, + ReLU);
+ * backward from dy to dz with dg / db; ws: ppll_batchnorm_ws_floats(P, C). */
+long ppll_layernorm_bwd_ws_floats(int M, int D);
+int ppll_layernorm_fwd(int M, int D, const void* x, long ldx, const float* g, const float* b,
+                       void* y, long ldy, float* mean, float* rstd, int dtype, void* stream);
+int ppll_layernorm_bwd(int M, int D, const void* dy, long lddy, const void* x, long ldx,
+                       const float* mean, const float* rstd, const float* g, const void* dres,
+                       long ldres, void* dx, long lddx, float* dg, float* db, float* dxsum,
+                       float* ws, long ws_floats, int dtype, void* stream);
+long ppll_batchnorm_ws_floats(int P, int C);
+int ppll_batchnorm_fwd(int P, int C, const void* z, const float* g, const float* b,
+                       const void* res, int relu, void* y, float* mean, float* rstd, float* ws,
+                       long ws_floats, int dtype, void* stream);
+int ppll_batchnorm_bwd(int P, int C, const void* dy, const void* z, const float* mean,
+                       const float* rstd, const float* g, float* dg, float* db, void* dz,
+                       float* ws, long ws_floats, int dtype, void* stream);
+
 /* Ring watchdog (no reference counterpart: the reference's threaded queues
  * poll a stop flag, runtime.py:411-418): a wait that sees no progress for the
  * timeout (default 30 s, PPLL_RING_TIMEOUT_MS; <= 0 disables) gives up instead

@@ -60,6 +60,15 @@ SIGNATURES = {
     "ppll_vit_stage_destroy": (None, [_vp]),
     "ppll_vit_stage_step": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ppll_vit_stage_forward": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "ppll_layernorm_bwd_ws_floats": (C.c_long, [_i, _i]),
+    "ppll_layernorm_fwd": (_i, [_i, _i, _vp, C.c_long, _vp, _vp, _vp, C.c_long, _vp, _vp, _i, _vp]),
+    "ppll_layernorm_bwd": (_i, [_i, _i, _vp, C.c_long, _vp, C.c_long, _vp, _vp, _vp, _vp, C.c_long,
+                                _vp, C.c_long, _vp, _vp, _vp, _vp, C.c_long, _i, _vp]),
+    "ppll_batchnorm_ws_floats": (C.c_long, [_i, _i]),
+    "ppll_batchnorm_fwd": (_i, [_i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, C.c_long, _i,
+                                _vp]),
+    "ppll_batchnorm_bwd": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_long, _i,
+                                _vp]),
     "ppll_set_ring_timeout_ms": (None, [C.c_longlong]),
     "ppll_ring_stall": (_i, [_vp, _i]),
     "ppll_attn_fwd_bf16": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
