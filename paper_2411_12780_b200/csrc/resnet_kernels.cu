@@ -337,20 +337,30 @@ bn_stats_part_vkernel(int P, int C, const __nv_bfloat16* __restrict__ z, int rpc
   int n = 0;
 #pragma unroll
   for (int e = 0; e < 8; ++e) K[e] = sm[e] = sq[e] = 0.f;
-  for (int r = r0 + ro; r < r1; r += RB) {
-    float v[8];
-    unpack8(*reinterpret_cast<const uint4*>(z + (long)r * C + vc * 8), v);
-    if (n == 0) {
+  // four rows' loads in flight per thread before any is consumed (same
+  // accumulation order as one row at a time)
+  for (int rb = r0 + ro; rb < r1; rb += 4 * RB) {
+    uint4 q[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) K[e] = v[e];
-    }
+    for (int u = 0; u < 4; ++u)
+      if (rb + u * RB < r1) q[u] = *reinterpret_cast<const uint4*>(z + (long)(rb + u * RB) * C + vc * 8);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float d = v[e] - K[e];
-      sm[e] += d;
-      sq[e] = fmaf(d, d, sq[e]);
+    for (int u = 0; u < 4; ++u) {
+      if (rb + u * RB >= r1) break;
+      float v[8];
+      unpack8(q[u], v);
+      if (n == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) K[e] = v[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = v[e] - K[e];
+        sm[e] += d;
+        sq[e] = fmaf(d, d, sq[e]);
+      }
+      ++n;
     }
-    ++n;
   }
   const float fn = (float)n;
 #pragma unroll
@@ -391,14 +401,25 @@ bn_bwd_part_vkernel(int P, int C, const __nv_bfloat16* __restrict__ dy,
     rs[e] = rstd[vc * 8 + e];
     sg[e] = sb[e] = 0.f;
   }
-  for (int r = r0 + ro; r < r1; r += RB) {
-    float d[8], x[8];
-    unpack8(*reinterpret_cast<const uint4*>(dy + (long)r * C + vc * 8), d);
-    unpack8(*reinterpret_cast<const uint4*>(z + (long)r * C + vc * 8), x);
+  for (int rb = r0 + ro; rb < r1; rb += 4 * RB) {
+    uint4 qd[4], qz[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      sg[e] = fmaf(d[e], (x[e] - mu[e]) * rs[e], sg[e]);
-      sb[e] += d[e];
+    for (int u = 0; u < 4; ++u)
+      if (rb + u * RB < r1) {
+        qd[u] = *reinterpret_cast<const uint4*>(dy + (long)(rb + u * RB) * C + vc * 8);
+        qz[u] = *reinterpret_cast<const uint4*>(z + (long)(rb + u * RB) * C + vc * 8);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (rb + u * RB >= r1) break;
+      float d[8], x[8];
+      unpack8(qd[u], d);
+      unpack8(qz[u], x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        sg[e] = fmaf(d[e], (x[e] - mu[e]) * rs[e], sg[e]);
+        sb[e] += d[e];
+      }
     }
   }
 #pragma unroll
