@@ -116,13 +116,36 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __re
 // in shared memory in chunks of 4096 / NP rows (16 KB), so the inner loop
 // streams only A.
 
+// Stage a [kc x NP] chunk of B (rows k0.., columns >= N zero) in shared
+// memory; every thread has eight independent loads in flight before it stores
+// (one memory latency per eight elements instead of one per element).
+template <int NP, int LD, typename TI>
+__device__ __forceinline__ void stage_b(float* bs, const TI* __restrict__ Bm, int k0, int kc, int N,
+                                        long b_rs, long b_cs) {
+  const int total = kc * NP;
+  for (int i0 = threadIdx.x; i0 < total; i0 += 8 * blockDim.x) {
+    float t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x, kk = i / NP, n = i % NP;
+      t[u] = (i < total && n < N) ? to_f(Bm[(long)(k0 + kk) * b_rs + (long)n * b_cs]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < total) bs[(i / NP) * LD + i % NP] = t[u];
+    }
+  }
+}
+
 template <typename TI, typename TO, int NP>
 __global__ void __launch_bounds__(256)
 gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
                     const TI* __restrict__ Bm, long b_rs, long b_cs, Epilogue<TO> ep) {
   pdl_entry();
   constexpr int kSkK = 4096 / NP;
-  __shared__ float bs[kSkK * NP];
+  constexpr int LD = NP + 1;   // lanes read different K rows: odd stride, no bank conflicts
+  __shared__ float bs[kSkK * LD];
   const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const bool live = m < M;
@@ -141,17 +164,14 @@ gemm_rowwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_rs,
       av[j] = (live && kk < kc) ? to_f(ar[k0 + kk]) : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kc * NP; i += blockDim.x) {
-      const int kk = i / NP, n = i % NP;
-      bs[i] = n < N ? to_f(Bm[(long)(k0 + kk) * b_rs + (long)n * b_cs]) : 0.f;
-    }
+    stage_b<NP, LD>(bs, Bm, k0, kc, N, b_rs, b_cs);
     __syncthreads();
     if (live) {
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
         const int kk = lane + 32 * j;
         if (kk < kc) {
-          const float* br = bs + kk * NP;
+          const float* br = bs + kk * LD;
 #pragma unroll
           for (int n = 0; n < NP; ++n) acc[n] = fmaf(av[j], br[n], acc[n]);
         }
@@ -183,17 +203,22 @@ gemm_colwarp_kernel(int M, int N, int K, const TI* __restrict__ A, long a_cs,
   for (int k0 = 0; k0 < K; k0 += kSkK) {
     const int kc = min(kSkK, K - k0);
     __syncthreads();
-    for (int i = threadIdx.x; i < kc * NP; i += blockDim.x) {
-      const int kk = i / NP, n = i % NP;
-      bs[i] = n < N ? to_f(Bm[(long)(k0 + kk) * b_rs + (long)n * b_cs]) : 0.f;
-    }
+    stage_b<NP, NP>(bs, Bm, k0, kc, N, b_rs, b_cs);
     __syncthreads();
     if (live) {
-      for (int kk = w; kk < kc; kk += 8) {
-        const float a = to_f(A[(long)(k0 + kk) * a_cs + m]);
-        const float* br = bs + kk * NP;
+      // A elements of four K rows loaded before they are consumed (same order)
+      for (int kb = w; kb < kc; kb += 32) {
+        float a[4];
 #pragma unroll
-        for (int n = 0; n < NP; ++n) acc[n] = fmaf(a, br[n], acc[n]);
+        for (int u = 0; u < 4; ++u)
+          a[u] = kb + 8 * u < kc ? to_f(A[(long)(k0 + kb + 8 * u) * a_cs + m]) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (kb + 8 * u >= kc) break;
+          const float* br = bs + (kb + 8 * u) * NP;
+#pragma unroll
+          for (int n = 0; n < NP; ++n) acc[n] = fmaf(a[u], br[n], acc[n]);
+        }
       }
     }
   }
