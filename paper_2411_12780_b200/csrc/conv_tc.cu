@@ -118,15 +118,23 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
       const uint4 q = *reinterpret_cast<const uint4*>(wg + ((long)(8 - tap) * CO + co) * CI + 8 * j);
       *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = q;
     }
-  } else {       // W row (tap, ci) holds co contiguous: scatter into [co][ci]
-    for (int i = threadIdx.x; i < 9 * CI * (CO / 8); i += kThreads) {
-      const int j = i % (CO / 8), ci = (i / (CO / 8)) % CI, tap = i / (CO / 8) / CI;
-      const uint4 q = *reinterpret_cast<const uint4*>(wg + ((long)tap * CI + ci) * CO + 8 * j);
-      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&q);
+  } else {       // W row (tap, ci) holds co contiguous: transpose into [co][ci]
+    // through the (still idle) operand ring: coalesced 16-B copies of W first,
+    // then each thread gathers the 8 ci values of one (tap, co) 16-B chunk and
+    // stores it whole (the element-wise scatter was 4 us of a 64->64 launch)
+    static_assert(9 * CI * CO * 2 <= S * L::A_BYTES, "weight transpose buffer");
+    uint4* tmp4 = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < 9 * CI * CO / 8; i += kThreads)
+      tmp4[i] = reinterpret_cast<const uint4*>(wg)[i];
+    __syncthreads();
+    const __nv_bfloat16* tmp = reinterpret_cast<const __nv_bfloat16*>(smem);
+    for (int i = threadIdx.x; i < 9 * CO * (CI / 8); i += kThreads) {
+      const int co = i % CO, j = (i / CO) % (CI / 8), tap = i / CO / (CI / 8);
+      uint4 q;
+      __nv_bfloat16* e = reinterpret_cast<__nv_bfloat16*>(&q);
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
-        *reinterpret_cast<__nv_bfloat16*>(sw + tap * CO * RB + swz<RB>(8 * j + t, ci >> 3) +
-                                          (ci & 7) * 2) = e[t];
+      for (int t = 0; t < 8; ++t) e[t] = tmp[((long)tap * CI + 8 * j + t) * CO + co];
+      *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = q;
     }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
