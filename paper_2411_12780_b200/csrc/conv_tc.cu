@@ -58,12 +58,23 @@ __device__ __forceinline__ int swz(int r, int j) {
   const int f = RB == 128 ? (r & 7) : (RB == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
   return r * RB + ((j ^ f) * 16);
 }
-template <int CI, int CO>
+// HALO: a pixel tile covers whole rows of ONE image (W >= 16); instead of nine
+// shifted 128-pixel windows the producer loads three column-shifted copies
+// (dx = -1, 0, +1) of the tile's rows plus one halo row above and below, and
+// tap (dy, dx) is copy dx read from row dy + 1 on: a constant row offset of
+// W·RB bytes, a whole number of swizzle atoms.  Same MMA sequence (bitwise
+// identical result), 2-3x fewer TMA rows and shared-memory bytes per tile, so
+// more tiles are in flight.
+template <int CI, int CO, bool HALO = false>
 struct ConvSmem {
   static constexpr int RB = CI * 2;                  // A / B row bytes (K = CI)
-  static constexpr int A_BYTES = 128 * RB;           // one tap of a pixel tile
+  // one slot: a 128-pixel tap window, or (HALO) one shifted copy of up to
+  // 192 pixels ((rows + 2)·W: 6 x 32 or 10 x 16)
+  static constexpr int A_BYTES = (HALO ? 192 : 128) * RB;
   static constexpr int W_BYTES = 9 * CO * RB;        // nine [CO x CI] weight tiles
-  static constexpr int STAGES = CI == 64 ? 6 : 18;   // tap slots (two pixel tiles below CI = 64)
+  // tap slots (two pixel tiles below CI = 64) / HALO copy slots (four tiles
+  // at CI = 16, three at 32, two at 64)
+  static constexpr int STAGES = HALO ? (CI == 64 ? 4 : (CI == 32 ? 9 : 12)) : (CI == 64 ? 6 : 18);
   static constexpr int STG = epi_warps<CO>() * 1024;
   static constexpr int TOTAL = STAGES * A_BYTES + W_BYTES + STG + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = 2 * CO <= 32 ? 32 : (2 * CO <= 64 ? 64 : 128);
@@ -72,11 +83,11 @@ struct ConvSmem {
 // W (global, bf16) is the GEMM weight [k·k·Cin (padded), Cout], row (tap·Cin + ci).
 // fwd:   Wtap[co][ci] = W[(tap·CI + ci)·CO + co]             (CI = Cin, CO = Cout)
 // dgrad: Wtap[co][ci] = W[((8 − tap)·CO + co)·CI + ci]       (CI = Cout, CO = Cin)
-template <int CI, int CO>
+template <int CI, int CO, bool HALO>
 __global__ void __launch_bounds__(conv_threads<CO>(), 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ wg,
                   int dgrad, int P, int H, int Wd, int rows, int imgs, Epilogue<__nv_bfloat16> ep) {
-  using L = ConvSmem<CI, CO>;
+  using L = ConvSmem<CI, CO, HALO>;
   constexpr int S = L::STAGES, RB = L::RB;
   constexpr int kEpiWarps = epi_warps<CO>(), kThreads = conv_threads<CO>();
   extern __shared__ uint8_t smem_raw[];
@@ -148,8 +159,18 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
       int kb = 0;
+      const uint32_t copy_bytes = (uint32_t)((rows + 2) * Wd * RB);
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int p0 = t * 128, n0 = p0 / HWp, h0 = (p0 % HWp) / Wd;
+        if constexpr (HALO) {   // three column-shifted copies with a halo row each side
+          for (int dx = 0; dx < 3; ++dx, ++kb) {
+            const int st = kb % S;
+            mbar_wait(&empty[st], ((kb / S) & 1) ^ 1);
+            mbar_expect_tx(&full[st], copy_bytes);
+            tma_load_4d(&xmap, &full[st], smem + st * L::A_BYTES, 0, dx - 1, h0 - 1, n0);
+          }
+          continue;
+        }
         for (int tap = 0; tap < 9; ++tap, ++kb) {
           const int st = kb % S;
           mbar_wait(&empty[st], ((kb / S) & 1) ^ 1);
@@ -169,6 +190,23 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if constexpr (HALO) {
+          for (int dx = 0; dx < 3; ++dx) mbar_wait(&full[(kb + dx) % S], ((kb + dx) / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          for (int tap = 0; tap < 9; ++tap) {
+            const int st = (kb + tap % 3) % S;
+            const uint32_t sa = smem_u32(smem + st * L::A_BYTES) + (uint32_t)((tap / 3) * Wd * RB);
+            const uint32_t sb = smem_u32(sw + tap * CO * RB);
+#pragma unroll
+            for (int k = 0; k < CI / 16; ++k)
+              mma_bf16(tmem + (uint32_t)(acc * CO), kdesc<RB>(sa + 32 * k), kdesc<RB>(sb + 32 * k),
+                       idesc, (tap | k) ? 1u : 0u);
+          }
+          for (int dx = 0; dx < 3; ++dx) mma_commit(&empty[(kb + dx) % S]);
+          kb += 3;
+          mma_commit(&tfull[acc]);
+          continue;
+        }
         for (int tap = 0; tap < 9; ++tap, ++kb) {
           const int st = kb % S;
           mbar_wait(&full[st], (kb / S) & 1);
@@ -232,11 +270,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-template <int CI, int CO>
+template <int CI, int CO, bool HALO>
 static int run(const CUtensorMap& xm, const __nv_bfloat16* w, int dgrad, int P, int H, int Wd,
                int rows, int imgs, const Epilogue<__nv_bfloat16>& ep, cudaStream_t s) {
-  auto kern = conv3x3_tc_kernel<CI, CO>;
-  constexpr int smem = ConvSmem<CI, CO>::TOTAL;
+  auto kern = conv3x3_tc_kernel<CI, CO, HALO>;
+  constexpr int smem = ConvSmem<CI, CO, HALO>::TOTAL;
   static bool attr = false;
   if (!attr) {
     PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -282,7 +320,11 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
   CUtensorMap xm;
   cuuint64_t dims[4] = {(cuuint64_t)CI, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
   cuuint64_t strides[3] = {(cuuint64_t)CI * 2, (cuuint64_t)W * CI * 2, (cuuint64_t)H * W * CI * 2};
-  cuuint32_t box[4] = {(cuuint32_t)CI, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs};
+  // whole rows of one image per tile: the halo form (three shifted copies)
+  static const int halo_env = getenv("PPLL_CONV_HALO") ? atoi(getenv("PPLL_CONV_HALO")) : 1;
+  const bool halo = halo_env && imgs == 1 && (rows + 2) * W <= 192;
+  cuuint32_t box[4] = {(cuuint32_t)CI, (cuuint32_t)W, (cuuint32_t)(halo ? rows + 2 : rows),
+                       (cuuint32_t)imgs};
   cuuint32_t es[4] = {1, 1, 1, 1};
   const CUtensorMapSwizzle sz = CI == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
                                 : (CI == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
@@ -292,8 +334,10 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
     return PPLL_ERR_UNSUPPORTED;
   Epilogue<__nv_bfloat16> e = ep;
   const int d = dgrad ? 1 : 0, Pi = (int)P;
-#define CONV_CASE(A, B) \
-  if (CI == A && CO == B) return run<A, B>(xm, w, d, Pi, H, W, rows, imgs, e, s);
+#define CONV_CASE(A, B)                                                             \
+  if (CI == A && CO == B)                                                           \
+    return halo ? run<A, B, true>(xm, w, d, Pi, H, W, rows, imgs, e, s)             \
+                : run<A, B, false>(xm, w, d, Pi, H, W, rows, imgs, e, s);
   CONV_CASE(16, 16) CONV_CASE(32, 32) CONV_CASE(64, 64)
   CONV_CASE(16, 32) CONV_CASE(32, 16) CONV_CASE(32, 64) CONV_CASE(64, 32)
 #undef CONV_CASE
