@@ -71,6 +71,10 @@ int ppll_batchnorm_fwd(int P, int C, const void* z, const float* g, const float*
                                   nullptr, nullptr, nullptr, (const float*)res, relu, (float*)y, s);
   }
   using B16 = __nv_bfloat16;
+  // one fused cluster launch where it applies (bn_cluster.cu), else stats + apply
+  r = launch_bn_fwd_fused(P, C, (const B16*)z, g, b, mean, rstd, nullptr, nullptr, nullptr,
+                          nullptr, nullptr, (const B16*)res, relu, (B16*)y, s);
+  if (r != PPLL_ERR_UNSUPPORTED) return r;
   r = launch_bn_stats<B16>(P, C, (const B16*)z, ws, mean, rstd, s);
   if (r) return r;
   return launch_bn_apply<B16>(P, C, (const B16*)z, mean, rstd, g, b, nullptr, nullptr, nullptr,
@@ -91,6 +95,10 @@ int ppll_batchnorm_bwd(int P, int C, const void* dy, const void* z, const float*
     return launch_bn_bwd<float>(P, C, (const float*)dy, (const float*)z, mean, rstd, g, ws, dg, db,
                                 (float*)dz, s);
   using B16 = __nv_bfloat16;
+  const int r = launch_bn_bwd_fused(P, C, (const B16*)dy, nullptr, nullptr, (const B16*)z, mean,
+                                    rstd, g, dg, db, (B16*)dz, nullptr, nullptr, nullptr, nullptr,
+                                    nullptr, nullptr, nullptr, s);
+  if (r != PPLL_ERR_UNSUPPORTED) return r;
   return launch_bn_bwd<B16>(P, C, (const B16*)dy, (const B16*)z, mean, rstd, g, ws, dg, db,
                             (B16*)dz, s);
 }

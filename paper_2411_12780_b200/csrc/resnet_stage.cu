@@ -114,12 +114,12 @@ static bool use_implicit(const ppll_resnet_stage* st, const ConvBN& c) {
   return !off && st->dtype == PPLL_BF16 && c.k == 3 && c.stride == 1;
 }
 
-// conv → BN statistics; returns z in c.z.  3x3 stride-1 convolutions run as
-// the implicit-GEMM kernel (conv_tc.cu, TMA gathers the shifted windows);
-// the rest as im2col · W on the GEMM engine
+// conv; returns z in c.z (BN follows in bn_act).  3x3 stride-1 convolutions
+// run as the implicit-GEMM kernel (conv_tc.cu, TMA gathers the shifted
+// windows); the rest as im2col · W on the GEMM engine
 template <typename TT>
-static int conv_bn_fwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* x, int64_t w_off,
-                       cudaStream_t s) {
+static int conv_fwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* x, int64_t w_off,
+                    cudaStream_t s) {
   const int P = B * c.h_out * c.h_out;
   int r = PPLL_ERR_UNSUPPORTED;
   c.implicit = false;
@@ -141,36 +141,96 @@ static int conv_bn_fwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* x, i
     LinOpts o;
     r = gemm_fwd(P, c.kp, c.cout, c.col, c.kp, st->W(w_off), o, c.z, c.cout, st->dtype, st->ws,
                  st->ws_elems, s);
-    if (r) return r;
   }
-  return launch_bn_stats<TT>(P, c.cout, (const TT*)c.z, st->bn_part, c.mean, c.rstd, s);
+  return r;
 }
 
-// given dy (gradient w.r.t. the BN output, ReLU already applied): BN backward,
-// weight gradient, and (if dx) the input gradient (+dres, ⊙mask): the
-// transposed implicit convolution, or col2im(dZ·Wᵀ)
-// side-stream state of one backward pass: convs alternate between the two dz
-// buffers; dz_done[i] = completion of the weight gradient that last read dz[i]
+// y = ReLU(BN(c.z) [+ BN2(c2.z) | + res]) with batch statistics (into c.mean /
+// c.rstd): one single-cluster launch for bf16 (bn_cluster.cu), else the
+// statistics kernels of each BN + the apply kernel.  g/b (g2/b2): parameter
+// offsets of the affine terms.
+template <typename TT>
+static int bn_act(ppll_resnet_stage* st, int P, ConvBN& c, int64_t g, int64_t b, ConvBN* c2,
+                  int64_t g2, int64_t b2, const void* res, void* y, cudaStream_t s) {
+  if (st->dtype == PPLL_BF16) {
+    const int r = launch_bn_fwd_fused(
+        P, c.cout, (const __nv_bfloat16*)c.z, st->P(g), st->P(b), c.mean, c.rstd,
+        c2 ? (const __nv_bfloat16*)c2->z : nullptr, c2 ? st->P(g2) : nullptr,
+        c2 ? st->P(b2) : nullptr, c2 ? c2->mean : nullptr, c2 ? c2->rstd : nullptr,
+        (const __nv_bfloat16*)res, 1, (__nv_bfloat16*)y, s);
+    if (r != PPLL_ERR_UNSUPPORTED) return r;
+  }
+  int r = launch_bn_stats<TT>(P, c.cout, (const TT*)c.z, st->bn_part, c.mean, c.rstd, s);
+  if (r) return r;
+  if (c2) {
+    r = launch_bn_stats<TT>(P, c2->cout, (const TT*)c2->z, st->bn_part, c2->mean, c2->rstd, s);
+    if (r) return r;
+  }
+  return launch_bn_apply<TT>(P, c.cout, (const TT*)c.z, c.mean, c.rstd, st->P(g), st->P(b),
+                             c2 ? (const TT*)c2->z : nullptr, c2 ? c2->mean : nullptr,
+                             c2 ? c2->rstd : nullptr, c2 ? st->P(g2) : nullptr,
+                             c2 ? st->P(b2) : nullptr, (const TT*)res, 1, (TT*)y, s);
+}
+
+// side-stream state of one backward pass: BN-backward outputs alternate
+// between the two dz buffers; dz_done[i] = completion of the weight gradient
+// that last read dz[i]
 struct BwdSide {
   SideFlow sf;
   char* dz[2];
   cudaEvent_t dz_done[2] = {nullptr, nullptr};
   int k = 0;
   float* wsw;
+  int take() {                   // next dz buffer, once its last reader is done
+    const int slot = k++ & 1;
+    sf.join(dz_done[slot]);
+    return slot;
+  }
 };
 
+// BatchNorm backward of c (and of c2, which shares dy — the projection
+// shortcut): dy = dout ⊙ [out > 0] when out != NULL (the ReLU after the add),
+// else dout; dγ/dβ into the gradient buffer, dz (dz2).  bf16: one fused
+// cluster launch (the masked dy stored only when keep_dy); else ReLU mask into
+// `scratch` + the three-kernel BN backward per BN.
 template <typename TT>
-static int conv_bn_bwd(ppll_resnet_stage* st, ConvBN& c, int B, const void* dy, int64_t w_off,
-                       int64_t g_off, int64_t b_off, void* dx, const void* dres,
-                       const void* mask, cudaStream_t s, BwdSide& bs) {
+static int bn_bwd(ppll_resnet_stage* st, int P, ConvBN& c, int64_t g, int64_t b, ConvBN* c2,
+                  int64_t g2, int64_t b2, const void* dout, const void* out, char* scratch,
+                  bool keep_dy, char* dz, char* dz2, cudaStream_t s) {
+  if (st->dtype == PPLL_BF16) {
+    const int r = launch_bn_bwd_fused(
+        P, c.cout, (const __nv_bfloat16*)dout, (const __nv_bfloat16*)out,
+        keep_dy ? (__nv_bfloat16*)scratch : nullptr, (const __nv_bfloat16*)c.z, c.mean, c.rstd,
+        st->P(g), st->G(g), st->G(b), (__nv_bfloat16*)dz,
+        c2 ? (const __nv_bfloat16*)c2->z : nullptr, c2 ? c2->mean : nullptr,
+        c2 ? c2->rstd : nullptr, c2 ? st->P(g2) : nullptr, c2 ? st->G(g2) : nullptr,
+        c2 ? st->G(b2) : nullptr, (__nv_bfloat16*)dz2, s);
+    if (r != PPLL_ERR_UNSUPPORTED) return r;
+  }
+  const void* dy = dout;
+  int r;
+  if (out) {
+    r = launch_relu_mask<TT>((long)P * c.cout, (const TT*)dout, (const TT*)out, (TT*)scratch, s);
+    if (r) return r;
+    dy = scratch;
+  }
+  r = launch_bn_bwd<TT>(P, c.cout, (const TT*)dy, (const TT*)c.z, c.mean, c.rstd, st->P(g),
+                        st->bn_part, st->G(g), st->G(b), (TT*)dz, s);
+  if (r || !c2) return r;
+  return launch_bn_bwd<TT>(P, c2->cout, (const TT*)dy, (const TT*)c2->z, c2->mean, c2->rstd,
+                           st->P(g2), st->bn_part, st->G(g2), st->G(b2), (TT*)dz2, s);
+}
+
+// given dz (gradient w.r.t. the conv output, in bs.dz[slot]): the weight
+// gradient on the side stream and (if dx) the input gradient (+dres, ⊙mask):
+// the transposed implicit convolution, or col2im(dZ·Wᵀ)
+template <typename TT>
+static int conv_bwd(ppll_resnet_stage* st, ConvBN& c, int B, int slot, int64_t w_off, void* dx,
+                    const void* dres, const void* mask, cudaStream_t s, BwdSide& bs) {
   const int P = B * c.h_out * c.h_out;
-  const int slot = bs.k++ & 1;
   char* dz = bs.dz[slot];
-  bs.sf.join(bs.dz_done[slot]);   // the weight gradient two convs back read this buffer
-  int r = launch_bn_bwd<TT>(P, c.cout, (const TT*)dy, (const TT*)c.z, c.mean, c.rstd,
-                            st->P(g_off), st->bn_part, st->G(g_off), st->G(b_off), (TT*)dz, s);
-  if (r) return r;
   bs.sf.fork();
+  int r;
   if (c.implicit) {   // the weight gradient still contracts over the im2col'd input
     r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)c.x_in,
                           (TT*)c.col, bs.sf.ss);
@@ -211,36 +271,28 @@ static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_o
   int r;
   if (st->has_stem) {
     ConvBN& c = st->stem;
-    r = conv_bn_fwd<TT>(st, c, B, x, st->stem_off[0], s);
+    r = conv_fwd<TT>(st, c, B, x, st->stem_off[0], s);
     if (r) return r;
-    r = launch_bn_apply<TT>((long)B * c.h_out * c.h_out, c.cout, (const TT*)c.z, c.mean, c.rstd,
-                            st->P(st->stem_off[1]), st->P(st->stem_off[2]), nullptr, nullptr,
-                            nullptr, nullptr, nullptr, nullptr, 1, (TT*)st->stem_out, s);
+    r = bn_act<TT>(st, B * c.h_out * c.h_out, c, st->stem_off[1], st->stem_off[2], nullptr, 0, 0,
+                   nullptr, st->stem_out, s);
     if (r) return r;
     x = st->stem_out;
   }
   for (size_t i = 0; i < st->blocks.size(); ++i) {
     Block& b = st->blocks[i];
-    const long P = (long)B * b.c1.h_out * b.c1.h_out;
-    r = conv_bn_fwd<TT>(st, b.c1, B, x, b.off[0], s);
+    const int P = B * b.c1.h_out * b.c1.h_out;
+    r = conv_fwd<TT>(st, b.c1, B, x, b.off[0], s);
     if (r) return r;
-    r = launch_bn_apply<TT>(P, b.c1.cout, (const TT*)b.c1.z, b.c1.mean, b.c1.rstd, st->P(b.off[1]),
-                            st->P(b.off[2]), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                            1, (TT*)b.a1, s);
+    r = bn_act<TT>(st, P, b.c1, b.off[1], b.off[2], nullptr, 0, 0, nullptr, b.a1, s);
     if (r) return r;
-    r = conv_bn_fwd<TT>(st, b.c2, B, b.a1, b.off[3], s);
+    r = conv_fwd<TT>(st, b.c2, B, b.a1, b.off[3], s);
     if (r) return r;
     if (b.has_sc) {
-      r = conv_bn_fwd<TT>(st, b.sc, B, x, b.off[6], s);
+      r = conv_fwd<TT>(st, b.sc, B, x, b.off[6], s);
       if (r) return r;
-      r = launch_bn_apply<TT>(P, b.c2.cout, (const TT*)b.c2.z, b.c2.mean, b.c2.rstd,
-                              st->P(b.off[4]), st->P(b.off[5]), (const TT*)b.sc.z, b.sc.mean,
-                              b.sc.rstd, st->P(b.off[7]), st->P(b.off[8]), nullptr, 1,
-                              (TT*)b.out, s);
+      r = bn_act<TT>(st, P, b.c2, b.off[4], b.off[5], &b.sc, b.off[7], b.off[8], nullptr, b.out, s);
     } else {
-      r = launch_bn_apply<TT>(P, b.c2.cout, (const TT*)b.c2.z, b.c2.mean, b.c2.rstd,
-                              st->P(b.off[4]), st->P(b.off[5]), nullptr, nullptr, nullptr, nullptr,
-                              nullptr, (const TT*)x, 1, (TT*)b.out, s);
+      r = bn_act<TT>(st, P, b.c2, b.off[4], b.off[5], nullptr, 0, 0, x, b.out, s);
     }
     if (r) return r;
     x = b.out;
@@ -251,11 +303,9 @@ static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_o
   if (!head) return PPLL_OK;
   for (auto& a : st->aux) {
     if (!with_aux) break;
-    r = conv_bn_fwd<TT>(st, a.c, B, x, a.off[0], s);
+    r = conv_fwd<TT>(st, a.c, B, x, a.off[0], s);
     if (r) return r;
-    r = launch_bn_apply<TT>(Pout, a.c.cout, (const TT*)a.c.z, a.c.mean, a.c.rstd, st->P(a.off[1]),
-                            st->P(a.off[2]), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                            1, (TT*)a.out, s);
+    r = bn_act<TT>(st, (int)Pout, a.c, a.off[1], a.off[2], nullptr, 0, 0, nullptr, a.out, s);
     if (r) return r;
     x = a.out;
   }
@@ -282,6 +332,9 @@ static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, con
   BwdSide bs{SideFlow{s, side ? st->side : s, st->ev.data(), 0, (int)st->ev.size()},
              {st->dz, side ? st->dz2 : st->dz}};
   bs.wsw = side ? st->ws2 : st->ws;
+  // without a side stream both "buffers" alias: the projection shortcut's two
+  // BN gradients then need distinct storage
+  char* dz_sc_alias = side ? nullptr : st->dtmp;
   char* dx = st->dxa;
   char* dx_next = st->dxb;
   if (!labels) {
@@ -307,48 +360,66 @@ static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, con
   // aux layers, last first (gradient w.r.t. each aux conv-BN-ReLU output)
   for (int i = with_aux ? (int)st->aux.size() - 1 : -1; i >= 0; --i) {
     Aux& a = st->aux[i];
-    r = launch_relu_mask<TT>((long)B * HW * C, (const TT*)dx, (const TT*)a.out, (TT*)st->dy, s);
+    const int sl = bs.take();
+    r = bn_bwd<TT>(st, B * HW, a.c, a.off[1], a.off[2], nullptr, 0, 0, dx, a.out, st->dy, false,
+                   bs.dz[sl], nullptr, s);
     if (r) return r;
-    r = conv_bn_bwd<TT>(st, a.c, B, st->dy, a.off[0], a.off[1], a.off[2], dx_next, nullptr, nullptr,
-                        s, bs);
+    r = conv_bwd<TT>(st, a.c, B, sl, a.off[0], dx_next, nullptr, nullptr, s, bs);
     if (r) return r;
     char* t = dx; dx = dx_next; dx_next = t;
   }
   // blocks, last first
   for (int i = (int)st->blocks.size() - 1; i >= 0; --i) {
     Block& b = st->blocks[i];
-    const long P = (long)B * b.c1.h_out * b.c1.h_out;
+    const int P = B * b.c1.h_out * b.c1.h_out;
     const bool need_dx = i > 0 || st->has_stem || g_in;
     // the stage input's gradient goes straight to g_in (no stem below)
     char* dx_dst = (i == 0 && !st->has_stem) ? (char*)g_in : dx_next;
-    r = launch_relu_mask<TT>(P * b.c2.cout, (const TT*)dx, (const TT*)b.out, (TT*)st->dsum, s);
-    if (r) return r;
-    // conv2: input gradient masked by the ReLU that produced a1 -> dy
-    r = conv_bn_bwd<TT>(st, b.c2, B, st->dsum, b.off[3], b.off[4], b.off[5], st->dy, nullptr, b.a1,
-                        s, bs);
-    if (r) return r;
     const void* dres = nullptr;
     if (b.has_sc) {
-      r = conv_bn_bwd<TT>(st, b.sc, B, st->dsum, b.off[6], b.off[7], b.off[8],
-                          need_dx ? st->dtmp : nullptr, nullptr, nullptr, s, bs);
+      // BN2 and the shortcut BN share dy = dx ⊙ [out > 0]: one backward launch
+      const int sa = bs.take();
+      int sb = bs.take();
+      char* dz_sc = dz_sc_alias ? dz_sc_alias : bs.dz[sb];
+      r = bn_bwd<TT>(st, P, b.c2, b.off[4], b.off[5], &b.sc, b.off[7], b.off[8], dx, b.out,
+                     st->dsum, false, bs.dz[sa], dz_sc, s);
+      if (r) return r;
+      // conv2: input gradient masked by the ReLU that produced a1 -> dy
+      r = conv_bwd<TT>(st, b.c2, B, sa, b.off[3], st->dy, nullptr, b.a1, s, bs);
+      if (r) return r;
+      if (dz_sc_alias) {   // single stream: dz_sc lives in dtmp, copy it into the slot
+        PPLL_CUDA_CHECK(cudaMemcpyAsync(bs.dz[sb], dz_sc, (size_t)P * b.sc.cout * st->esz,
+                                        cudaMemcpyDeviceToDevice, s));
+      }
+      r = conv_bwd<TT>(st, b.sc, B, sb, b.off[6], need_dx ? st->dtmp : nullptr, nullptr, nullptr,
+                       s, bs);
       if (r) return r;
       dres = st->dtmp;
     } else {
+      const int sa = bs.take();
+      r = bn_bwd<TT>(st, P, b.c2, b.off[4], b.off[5], nullptr, 0, 0, dx, b.out, st->dsum, true,
+                     bs.dz[sa], nullptr, s);
+      if (r) return r;
+      r = conv_bwd<TT>(st, b.c2, B, sa, b.off[3], st->dy, nullptr, b.a1, s, bs);
+      if (r) return r;
       dres = st->dsum;
     }
     // conv1 (+ shortcut / identity gradient) -> gradient of the block input
-    r = conv_bn_bwd<TT>(st, b.c1, B, st->dy, b.off[0], b.off[1], b.off[2],
-                        need_dx ? dx_dst : nullptr, dres, nullptr, s, bs);
+    const int s1 = bs.take();
+    r = bn_bwd<TT>(st, P, b.c1, b.off[1], b.off[2], nullptr, 0, 0, st->dy, nullptr, nullptr,
+                   false, bs.dz[s1], nullptr, s);
+    if (r) return r;
+    r = conv_bwd<TT>(st, b.c1, B, s1, b.off[0], need_dx ? dx_dst : nullptr, dres, nullptr, s, bs);
     if (r) return r;
     char* t = dx; dx = dx_next; dx_next = t;
   }
   if (st->has_stem) {
     ConvBN& c = st->stem;
-    const long P = (long)B * c.h_out * c.h_out;
-    r = launch_relu_mask<TT>(P * c.cout, (const TT*)dx, (const TT*)st->stem_out, (TT*)st->dy, s);
+    const int sl = bs.take();
+    r = bn_bwd<TT>(st, B * c.h_out * c.h_out, c, st->stem_off[1], st->stem_off[2], nullptr, 0, 0,
+                   dx, st->stem_out, st->dy, false, bs.dz[sl], nullptr, s);
     if (r) return r;
-    r = conv_bn_bwd<TT>(st, c, B, st->dy, st->stem_off[0], st->stem_off[1], st->stem_off[2],
-                        nullptr, nullptr, nullptr, s, bs);
+    r = conv_bwd<TT>(st, c, B, sl, st->stem_off[0], nullptr, nullptr, nullptr, s, bs);
     if (r) return r;
   }
   bs.sf.join(bs.sf.mark());   // every weight gradient has landed

@@ -50,5 +50,5 @@ def bnorm(P, C):
 
 
 ln(8320, 384)
-for P, C in ((131072, 16), (32768, 32), (8192, 64)):
+for P, C in ((131072, 16), (32768, 32), (8192, 64), (262144, 16), (524288, 16)):
     bnorm(P, C)
