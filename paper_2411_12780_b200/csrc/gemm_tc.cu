@@ -877,7 +877,7 @@ static unsigned long long* cluster_tl() {
 }
 unsigned long long* timeline_buffer() {
   static unsigned long long* buf = nullptr;
-  if (!buf && cudaMalloc(&buf, kNumSMs * 4 * 4 * 8) != cudaSuccess) buf = nullptr;
+  if (!buf && cudaMalloc(&buf, 65536 * 8) != cudaSuccess) buf = nullptr;   // 64 Ki stamps
   return buf;
 }
 
