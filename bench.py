@@ -683,6 +683,87 @@ def roofline_nesterov(mods, hbm, dev):
             "launch_us": dt * 1e6}
 
 
+def roofline_attention(wl, hbm, dev, sets=4, reps=5):
+    """Second roofline entry of the ViT line: the tcgen05 attention kernels
+    (attn_tc_fwd_kernel / the persistent attn_tc_bwd_kernel) at the workload's
+    geometry.  `sets` independent input/output sets (~45 MB each for the
+    backward, > L2 together) are cycled by back-to-back launches captured in a
+    CUDA graph (PDL edges, as in the stage graphs), so every launch reads
+    inputs the previous launches did not leave in L2; per-launch time = graph
+    time / launches.  HBM-bound: algorithmic bytes = qkv read + o (+ lse)
+    written (forward); qkv, o, dO (+ lse) read + dqkv (+ the fused bias
+    partials) written (backward)."""
+    import torch
+    from paper_2411_12780_b200 import _native as N
+    sp = wl["spec"]
+    B, T = wl["batch"], (sp["image"] // sp["patch"]) ** 2 + 1
+    H = sp["heads"]
+    D = 64 * H
+    M = B * T
+    lib = N.load()
+    bufs = []
+    for _ in range(sets):
+        qkv = (torch.randn(M, 3 * D, device=dev) * 0.5).bfloat16()
+        bufs.append(dict(qkv=qkv, dout=(torch.randn(M, D, device=dev) * 0.5).bfloat16(),
+                         o=torch.empty(M, D, device=dev, dtype=torch.bfloat16),
+                         lse=torch.empty(B * H * T, device=dev), dqkv=torch.empty_like(qkv),
+                         bias=torch.empty(B, 3 * D, device=dev)))
+    st = torch.cuda.Stream(dev)
+
+    def fwd(bf, s):
+        lib.ppll_attn_fwd_bf16(B, T, H, bf["qkv"].data_ptr(), bf["o"].data_ptr(),
+                               bf["lse"].data_ptr(), s)
+
+    def bwd(bf, s):
+        lib.ppll_attn_bwd_bf16(B, T, H, bf["qkv"].data_ptr(), bf["o"].data_ptr(),
+                               bf["dout"].data_ptr(), bf["lse"].data_ptr(), bf["dqkv"].data_ptr(),
+                               bf["bias"].data_ptr(), s)
+
+    def per_launch(fn):
+        with torch.cuda.stream(st):
+            for bf in bufs:
+                fn(bf, st.cuda_stream)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(reps):
+                for bf in bufs:
+                    fn(bf, st.cuda_stream)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        best = float("inf")
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g.replay()
+            b.record(st)
+            b.synchronize()
+            best = min(best, a.elapsed_time(b) * 1e-3 / (reps * sets))
+        return best
+
+    t_f = per_launch(fwd)
+    t_b = per_launch(bwd)
+    # the same launches on one resident input set (inputs in L2, as when the
+    # attention directly follows the GEMM that produced its inputs)
+    bufs = bufs[:1]
+    w_f, w_b = per_launch(fwd), per_launch(bwd)
+    by_f = 2 * M * 3 * D + 2 * M * D + 4 * B * H * T
+    by_b = 2 * M * 3 * D + 2 * 2 * M * D + 4 * B * H * T + 2 * M * 3 * D + 4 * B * 3 * D
+    return {"kernel": "attn_tc_bwd_kernel (persistent, one CTA per resident slot; the ViT "
+                      "layer's attention backward), back-to-back launches over "
+                      f"{sets} input sets (> L2) from one CUDA graph",
+            "bound": "hbm", "achieved": by_b / t_b / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": by_b / t_b / 1e9 / hbm, "traffic": None,
+            "algorithmic_bytes_per_launch": by_b, "launch_us": t_b * 1e6,
+            "geometry": {"batch": B, "tokens": T, "heads": H, "head_dim": 64},
+            "forward": {"kernel": "attn_tc_fwd_kernel", "achieved": by_f / t_f / 1e9,
+                        "frac": by_f / t_f / 1e9 / hbm, "algorithmic_bytes_per_launch": by_f,
+                        "launch_us": t_f * 1e6},
+            "warm_l2": {"how": "same graph on one input set (L2-resident inputs)",
+                        "bwd_launch_us": w_b * 1e6, "bwd_frac": by_b / w_b / 1e9 / hbm,
+                        "fwd_launch_us": w_f * 1e6, "fwd_frac": by_f / w_f / 1e9 / hbm}}
+
+
 def vit_layer_gemms(wl, dev):
     """The 12 tcgen05 GEMM launches of one ViT transformer layer's local step
     (vit_stage.cu: forward QKV / proj / FC1 / FC2, dgrad and wgrad of each) at
@@ -822,6 +903,51 @@ def gemm_sequence(gemms, dev, reps=20):
     return full, marginal
 
 
+def gemm_sequence_step_streams(gemms, dev, reps=20):
+    """The same 12 launches with the stage step's stream structure
+    (vit_stage.cu): forward and the data-gradient chain on the step's stream,
+    each weight gradient forked onto the stage's side stream when its input
+    gradient is ready (events, captured as graph edges) and joined before the
+    optimizer.  Returns the mean time of one layer's 12 GEMMs as the step
+    executes them."""
+    import torch
+    st, side = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def enqueue():
+        for i in (0, 1, 2, 3):
+            gemms[i][3](st.cuda_stream)
+        for dg, wg in ((4, 8), (5, 9), (6, 10), (7, 11)):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            side.wait_event(ev)
+            gemms[wg][3](side.cuda_stream)
+            gemms[dg][3](st.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        st.wait_event(ev)
+
+    with torch.cuda.stream(st):
+        enqueue()
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        enqueue()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize(dev)
+    best = float("inf")
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            a.record(st)
+            for _ in range(reps):
+                g.replay()
+            b.record(st)
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) / reps * 1e-3)
+    return best
+
+
 def roofline_gemm(wl, tf_burst, hbm, dev):
     """The dominant kernel of the ViT step: the tcgen05 GEMM engine
     (gemm_tc_kernel / gemm_tc_cluster_kernel, ~55 % of the step in the ncu
@@ -845,6 +971,11 @@ def roofline_gemm(wl, tf_burst, hbm, dev):
     seq_t, marg = gemm_sequence(gemms, dev)
     for i, row in enumerate(table):
         row["us_in_sequence"] = round(marg[i] * 1e6, 2)
+    try:
+        step_t = gemm_sequence_step_streams(gemms, dev)
+    except Exception as e:  # noqa: BLE001 — auxiliary figure
+        step_t = None
+        print(f"[bench] step-stream GEMM sequence failed: {e}", file=sys.stderr)
     del keep
     traffic = _ncu_traffic("vit_layer")
     return {"kernel": "gemm_tc (tcgen05 engine): the 12 GEMM launches of one ViT-S layer's "
@@ -853,6 +984,11 @@ def roofline_gemm(wl, tf_burst, hbm, dev):
             "bound": "tensor", "achieved": tot_fl / seq_t / 1e12, "peak": tf_burst,
             "unit": "TFLOP/s", "frac": tot_fl / seq_t / 1e12 / tf_burst,
             "launch_us_in_sequence": seq_t / len(table) * 1e6,
+            "in_step_streams": None if step_t is None else {
+                "how": "the same 12 launches with the step's streams: forward + dgrad chain on "
+                       "the step stream, each wgrad forked to the side stream (vit_stage.cu)",
+                "achieved": tot_fl / step_t / 1e12, "frac": tot_fl / step_t / 1e12 / tf_burst,
+                "layer_us": step_t * 1e6},
             "cold_alone": {"how": "each launch alone after a clean 512 MB L2 flush (round-1 "
                                   "method)", "achieved": tot_fl / tot_t / 1e12,
                            "frac": tot_fl / tot_t / 1e12 / tf_burst,
@@ -1067,9 +1203,11 @@ def main():
     used = [m.optimizer.step_count for m in mods]
     assert max(used) <= step_budget(ph), (used, ph)
 
+    roof_attn = None
     if wl["kind"] == "vit":
         roof = _guard("roofline_gemm", roofline_gemm, wl, tf_burst, hbm, dev)
         roof_extra = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
+        roof_attn = _guard("roofline_attention", roofline_attention, wl, hbm, dev)
     elif wl["kind"] == "resnet" and args.precision == "bf16":
         roof = _guard("roofline_conv", roofline_conv, wl, tf_burst, hbm, dev)
         roof_extra = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
@@ -1101,6 +1239,7 @@ def main():
         "sequential_schedule_images_per_s": seq_ips,
         "backprop_baselines": bp,
         "e2e": e2e, "roofline": roof, "roofline_optimizer": roof_extra,
+        "roofline_attention": roof_attn,
         "cpu_baseline": cpu,
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk.summary(),

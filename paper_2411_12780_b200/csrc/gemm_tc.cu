@@ -59,6 +59,7 @@ struct Sched {
   // takes Sched as a __grid_constant__ parameter so the maps live in param space
   CUtensorMap st_c, st_p;
   int tma_st;
+  int drain_full;   // PPLL_GEMM_DRAIN_FULL=1: wait for the bulk stores' writes at exit
   int mt, nt, tiles, splits, kps, items;
   int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores,
               // 2 = bias+GELU math only, 3 = stores only (interior tiles)
@@ -338,7 +339,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
       if (sc.tl && it < 4 && lane == 0) atomicMax(&sc.tl[(blockIdx.x * 4 + it) * 4 + 2], gtimer());
     }
-    if (F != kEFGeneric && sc.tma_st) tma_store_drain(lane);
+    if (F != kEFGeneric && sc.tma_st) tma_store_drain(lane, sc.drain_full);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -974,6 +975,8 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   }
   Sched sc;
   sc.tma_st = 0;
+  static const int drain_full = getenv("PPLL_GEMM_DRAIN_FULL") ? atoi(getenv("PPLL_GEMM_DRAIN_FULL")) : 0;
+  sc.drain_full = drain_full;
   sc.mt = mt;
   sc.nt = ceil_div(N, bn);
   sc.tiles = sc.mt * sc.nt;

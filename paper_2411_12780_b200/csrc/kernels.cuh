@@ -334,8 +334,15 @@ __device__ __forceinline__ void warp_store_tma16(const void* map, int row0, int 
     }
   }
 }
-__device__ __forceinline__ void tma_store_drain(int lane) {
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+// at exit only the shared-memory source must have been read (the CTA's smem
+// is released); the global writes complete with the grid, before any
+// dependent grid passes griddepcontrol.wait or the stream moves on
+// (PPLL_GEMM_DRAIN_FULL=1 restores the full wait_group 0)
+__device__ __forceinline__ void tma_store_drain(int lane, int full = 0) {
+  if (lane == 0) {
+    if (full) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
   __syncwarp();
 }
 

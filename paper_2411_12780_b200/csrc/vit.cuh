@@ -16,7 +16,23 @@ int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const floa
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
                   const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
-                  float* part, float* dg, float* db, cudaStream_t s, float* dxsum = nullptr);
+                  float* part, float* dg, float* db, cudaStream_t s, float* dxsum = nullptr,
+                  struct LnDefer* defer = nullptr);
+// Deferred LayerNorm parameter reductions: a stage's backward records each
+// LN backward's per-block partials (dγ, dβ and the fused Σ-rows bias gradient)
+// instead of reducing them right away, and one batched launch reduces them all
+// before the optimizer (same fixed summation order: bitwise identical).
+struct LnReduceTask {
+  const float* part;
+  float *o0, *o1, *o2;
+  int nblk, D, NS, blk0;   // blk0: first block of this task in the batched grid
+};
+struct LnDefer {
+  static constexpr int kMax = 24;
+  LnReduceTask t[kMax];
+  int n = 0, blocks = 0;
+};
+int launch_ln_reduce_deferred(const LnDefer& d, cudaStream_t s);
 int ln_bwd_blocks(int M);
 template <typename T>
 int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse, cudaStream_t s);

@@ -448,10 +448,47 @@ int launch_ln_fwd(int M, int D, const T* x, long ldx, const float* g, const floa
 int ln_bwd_blocks(int M) { return M < 148 * 8 ? ceil_div(M, 8) : min(ceil_div(M, 16), 148 * 2); }
 static int ln_bwd_vblocks(int M, int rpb) { return min(ceil_div(M, rpb), 148); }
 
+// batched form of ln_param_reduce_kernel over the deferred tasks of a stage
+// backward: block b belongs to the task whose [blk0, blk0 + ceil(NS·D/32)) holds
+// it; per column the same fixed-order sum
+__global__ void __launch_bounds__(1024)
+ln_param_reduce_batch_kernel(const __grid_constant__ LnDefer d) {
+  pdl_entry();
+  __shared__ float red[32][33];
+  int k = 0;
+  while (k + 1 < d.n && (int)blockIdx.x >= d.t[k + 1].blk0) ++k;
+  const LnReduceTask& t = d.t[k];
+  const int NS = t.NS, D = t.D;
+  const int c = ((int)blockIdx.x - t.blk0) * 32 + threadIdx.x;
+  float s = 0.f;
+  if (c < NS * D) {
+#pragma unroll 4
+    for (int j = threadIdx.y; j < t.nblk; j += 32) s += t.part[(long)j * NS * D + c];
+  }
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < NS * D) {
+    float u = 0.f;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) u += red[r][threadIdx.x];
+    const int kk = c / D, cc = c % D;
+    float* o = kk == 0 ? t.o0 : (kk == 1 ? t.o1 : t.o2);
+    if (o) o[cc] = u;
+  }
+}
+
+int launch_ln_reduce_deferred(const LnDefer& d, cudaStream_t s) {
+  if (d.n == 0) return PPLL_OK;
+  launch_k(ln_param_reduce_batch_kernel, d.blocks, dim3(32, 32), 0, s, d);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
 template <typename T>
 int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, const float* mean,
                   const float* rstd, const float* g, const T* dres, long ldres, T* dx, long lddx,
-                  float* part, float* dg, float* db, cudaStream_t s, float* dxsum) {
+                  float* part, float* dg, float* db, cudaStream_t s, float* dxsum, LnDefer* defer) {
   if (D % 32 || D > 1024) { set_error("layernorm: D=%d unsupported", D); return PPLL_ERR_ARG; }
   int nblk = ln_bwd_blocks(M);
   const int rpb = ceil_div(M, nblk);
@@ -493,7 +530,11 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
   }
   note_launch();
   PPLL_LAUNCH_CHECK();
-  if (part && (dg || (vec && dxsum))) {
+  if (part && (dg || (vec && dxsum)) && defer && defer->n < LnDefer::kMax) {
+    LnReduceTask& t = defer->t[defer->n++];
+    t = LnReduceTask{part, dg, db, vec ? dxsum : nullptr, nblk, D, NS, defer->blocks};
+    defer->blocks += ceil_div(NS * D, 32);
+  } else if (part && (dg || (vec && dxsum))) {
     launch_k(ln_param_reduce_kernel, ceil_div(NS * D, 32), dim3(32, 32), 0, s, nblk, D, NS, part, dg, db,
                                                                         vec ? dxsum : nullptr);
     note_launch();
@@ -857,7 +898,7 @@ int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s)
                                 float*, float*, cudaStream_t);                                   \
   template int launch_ln_bwd<T>(int, int, const T*, long, const T*, long, const float*,          \
                                 const float*, const float*, const T*, long, T*, long, float*,    \
-                                float*, float*, cudaStream_t, float*);                           \
+                                float*, float*, cudaStream_t, float*, LnDefer*);                 \
   template int launch_attn_fwd<T>(int, int, int, int, const T*, T*, float*, cudaStream_t);      \
   template int launch_attn_bwd<T>(int, int, int, int, const T*, const T*, const T*,             \
                                   const float*, T*, cudaStream_t);                               \

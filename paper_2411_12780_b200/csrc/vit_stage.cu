@@ -51,6 +51,8 @@ struct ppll_vit_stage {
   char *dxa = nullptr, *dxb = nullptr, *dxc = nullptr, *dbig = nullptr, *dxn = nullptr,
        *dqkv = nullptr, *dO = nullptr, *dtok = nullptr;
   float* ln_part = nullptr;
+  float* ln_parts = nullptr;   // [2·layers + 1][ln_slab] deferred LN partials
+  size_t ln_slab = 0;
   float* cs_part = nullptr;       // fused bias-gradient column partials [ceil(M/32), F]
   size_t cs_part_elems = 0;
   float* attn_bpart = nullptr;
@@ -205,6 +207,11 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
   float* wsw = sf.on() ? st->ws2 : st->ws;   // the weight gradients' workspace
   int r;
   LinOpts none;
+  // LN parameter (and fused bias) reductions are deferred to one batched
+  // launch at the end of the backward; each LN backward gets its own slab
+  LnDefer dfr;
+  int nslab = 0;
+  auto slab = [&]() { return st->ln_parts + st->ln_slab * (size_t)(nslab++); };
   if (labels) {
     r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
                                 st->loss_hist, st->step, st->err, s);
@@ -219,8 +226,8 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
                    st->ws_elems, s);
     if (r) return r;
     r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, (long)T * D, st->meanf, st->rstdf,
-                          st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, st->ln_part,
-                          st->G(st->ho(0)), st->G(st->ho(1)), s);
+                          st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, slab(),
+                          st->G(st->ho(0)), st->G(st->ho(1)), s, nullptr, &dfr);
     if (r) return r;
     r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)st->dxa, s);
     if (r) return r;
@@ -273,9 +280,9 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     // LN2 backward (+ residual) -> dx1, with dbo = Σ rows dx1 fused
     sf.join(e_wo);   // dx1 is still read by the layer above's Wo gradient
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
-                          st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, st->ln_part,
+                          st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, slab(),
                           st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s,
-                          st->G(st->po(l, kBo)));
+                          st->G(st->po(l, kBo)), &dfr);
     if (r) return r;
     sf.fork();
     r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, wsw,
@@ -308,9 +315,9 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     e_w2 = n_w2;
     r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
                           st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
-                          need_dx ? dx_dst : nullptr, D, st->ln_part,
+                          need_dx ? dx_dst : nullptr, D, slab(),
                           st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s,
-                          l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr);
+                          l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr, &dfr);
     if (r) return r;
     char* t = dx2;
     dx2 = dxn_out;
@@ -325,6 +332,8 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
                      st->G(st->off[1]), st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
   }
+  r = launch_ln_reduce_deferred(dfr, s);
+  if (r) return r;
   // every weight gradient has landed before the optimizer reads them
   sf.join(sf.mark());
   return PPLL_OK;
@@ -405,6 +414,10 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
   st->dbig = A(M * F * e); st->dxn = A(M * D * e); st->dqkv = A(M * 3 * D * e);
   st->dO = A(M * D * e);
   st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 3 * D * 4);
+  // deferred LN reductions: one partial slab per LN backward of a step
+  // (head LN + two per layer), reduced in one batched launch before the update
+  st->ln_slab = (size_t)ln_bwd_blocks((int)M) * 3 * D;
+  st->ln_parts = (float*)A(st->ln_slab * (2 * st->L.size() + 1) * 4);
   st->cs_part_elems = (size_t)ceil_div((long)M, 32) * st->F;
   st->cs_part = (float*)A(st->cs_part_elems * 4);
   st->attn_bpart = (float*)A((size_t)st->Bmax * 3 * D * 4);
