@@ -176,6 +176,15 @@ int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x, con
  * + residual; resnet_stage.cu conv_bn_bwd). */
 int ppll_conv3x3_bf16_ex(int N, int H, int W, int Cin, int Cout, const void* x, const void* w,
                          void* y, int dgrad, const void* res, const void* mask, void* stream);
+/* Weight gradient of the same convolution as an implicit GEMM (the matmul
+ * adjoint dW = Xᵀ·dY of tensor.py:145-150 with X the im2col'd input, which is
+ * never materialised): dw [9·Cin, Cout] fp32 (the GEMM weight layout) from
+ * x [N,H,W,Cin] and dz = dLoss/dconv-output [N·H·W, Cout]; ws holds the
+ * split-K partials (at least ppll_conv3x3_wgrad_ws_floats floats).  Fixed-
+ * order reduction (deterministic).  Same shape range as ppll_conv3x3_bf16. */
+long ppll_conv3x3_wgrad_ws_floats(int N, int H, int W, int Cin, int Cout);
+int ppll_conv3x3_wgrad_bf16(int N, int H, int W, int Cin, int Cout, const void* x, const void* dz,
+                            float* dw, float* ws, long ws_floats, void* stream);
 
 /* ---- data path / evaluation -------------------------------------------- */
 /* dst[r,:] = cast(src[idx[r],:]) for r < n (fp32 rows of `width` features,

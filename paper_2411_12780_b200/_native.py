@@ -44,6 +44,8 @@ SIGNATURES = {
     "ppll_sum_all": (_i, [_i64, _vp, _vp, _i, _vp, _vp]),
     "ppll_conv3x3_bf16": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
     "ppll_conv3x3_bf16_ex": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "ppll_conv3x3_wgrad_ws_floats": (C.c_long, [_i, _i, _i, _i, _i]),
+    "ppll_conv3x3_wgrad_bf16": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, C.c_long, _vp]),
     "ppll_gather_rows": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_gather_rows_u8": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_events_elapsed": (_i, [_i, _vp, C.c_uint64, _vp]),

@@ -15,6 +15,7 @@ int g_gemm_engine = PPLL_GEMM_AUTO;
 // per host thread: two pipelines driven from different threads each launch with
 // their own setting (a process-wide flag could be flipped under a capture)
 thread_local int g_pdl = getenv("PPLL_PDL") ? atoi(getenv("PPLL_PDL")) : 1;
+thread_local int g_gemm_cap = 0, g_wgrad_cap = 0;
 
 void set_error(const char* fmt, ...) {
   va_list ap;

@@ -80,6 +80,10 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 extern thread_local int g_pdl;
+// SM budget of the tcgen05 GEMM launches issued by this host thread (0 = the
+// whole GPU): a stage step caps its data-gradient GEMMs / cluster weight
+// gradients so the two streams' kernels can be resident side by side
+extern thread_local int g_gemm_cap, g_wgrad_cap;
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

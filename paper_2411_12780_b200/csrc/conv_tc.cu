@@ -21,6 +21,7 @@
 // col2im gather of the explicit path disappear (its residual-add and ReLU
 // mask ride in the epilogue).
 #include <cuda.h>
+#include <stdlib.h>
 #include <cudaTypedefs.h>
 #include "common.cuh"
 #include "kernels.cuh"
@@ -258,6 +259,170 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Implicit-GEMM weight gradient of the same 3x3 / stride-1 convolution:
+//
+//   dW[tap·CI + ci, co] = Σ_p x[p + off(tap), ci] · dZ[p, co]
+//
+// K = pixels.  Per 128-pixel chunk the producer fetches the nine shifted input
+// windows exactly like the forward (one 4-D TMA box per tap, zero padding from
+// out-of-range boxes) into nine consecutive [128 px x CI] slots, plus the
+// [128 px x CO] dZ tile.  Read MN-major (rows = pixels = K, CI contiguous),
+// consecutive tap slots are consecutive MN atoms (descriptor LBO = slot
+// stride), so ONE M = 128 MMA covers 128 / CI taps: rows m = tap·CI + ci of
+// the accumulator are the rows of dW in the GEMM weight layout.  N = CO (dZ
+// tile, MN-major), K step = 16 pixels.  M-tiles past the ninth tap read the
+// next slots (other data, never-stored accumulator rows).  Each CTA sums its
+// chunks in TMEM and writes one fp32 partial [9·CI, CO]; the fixed-order
+// split-K reduction (splitk_reduce) sums the partials — deterministic, no
+// im2col matrix (which was P·9·CI bf16: 38 MB for a 32x32x16 layer at B=128).
+// ---------------------------------------------------------------------------
+template <int CI, int CO>
+struct WgSmem {
+  static constexpr int RB = CI * 2, RBO = CO * 2;
+  static constexpr int SLOT = 128 * RB;                     // one tap window
+  static constexpr int TAPS_PER_M = 128 / CI;               // taps per M = 128 tile
+  static constexpr int MT = (9 + TAPS_PER_M - 1) / TAPS_PER_M;
+  static constexpr int DZ = 128 * RBO;
+  static constexpr int BUF = 9 * SLOT + DZ;                 // one chunk
+  static constexpr int NB = CI == 16 ? 4 : (CI == 32 ? 2 : 1);
+  // the last M-tile reads up to MT·TAPS_PER_M − 9 slots past a buffer's ninth
+  static constexpr int PAD = (MT * TAPS_PER_M - 9) * SLOT;
+  static constexpr int TOTAL = NB * BUF + PAD + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = MT * CO <= 32 ? 32 : (MT * CO <= 64 ? 64 : (MT * CO <= 128 ? 128 : (MT * CO <= 256 ? 256 : 512)));
+};
+
+// MN-major swizzled operand descriptor: 8-row K groups of 8·RB bytes (SBO),
+// MN atoms of RB bytes' worth of elements `lbo` bytes apart
+template <int RB>
+__device__ __forceinline__ uint64_t mndesc(uint32_t saddr, uint32_t lbo) {
+  constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(((8 * RB) >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= layout << 61;
+  return d;
+}
+
+template <int CI, int CO>
+__global__ void __launch_bounds__(192, 1)
+conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
+                        const __grid_constant__ CUtensorMap dzmap, int P, int H, int Wd,
+                        float* __restrict__ part) {
+  using L = WgSmem<CI, CO>;
+  constexpr int NB = L::NB, RB = L::RB, RBO = L::RBO, MT = L::MT;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (base & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NB * L::BUF + L::PAD);
+  uint64_t* empty = full + NB;
+  uint64_t* done = empty + NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int chunks = P / 128;
+  // contiguous chunk range of this split (fixed assignment: deterministic)
+  const int per = (chunks + gridDim.x - 1) / gridDim.x;
+  const int c0 = blockIdx.x * per, c1 = min(chunks, c0 + per);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&dzmap)) : "memory");
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+  const int HWp = H * Wd;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int kb = 0;
+      for (int c = c0; c < c1; ++c, ++kb) {
+        const int b = kb % NB;
+        mbar_wait(&empty[b], ((kb / NB) & 1) ^ 1);
+        uint8_t* buf = smem + b * L::BUF;
+        mbar_expect_tx(&full[b], 9 * L::SLOT + L::DZ);
+        const int p0 = c * 128, n0 = p0 / HWp, h0 = (p0 % HWp) / Wd;
+        for (int tap = 0; tap < 9; ++tap)
+          tma_load_4d(&xmap, &full[b], buf + tap * L::SLOT, 0, tap % 3 - 1, h0 + tap / 3 - 1, n0);
+        tma_load_2d(&dzmap, &full[b], buf + 9 * L::SLOT, 0, p0);
+      }
+    }
+  } else if (warp == 1) {
+    // M = 128 rows (tap, ci), N = CO, both operands MN-major
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                           ((uint32_t)(CO >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    if (lane == 0) {
+      int kb = 0;
+      for (int c = c0; c < c1; ++c, ++kb) {
+        const int b = kb % NB;
+        mbar_wait(&full[b], (kb / NB) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sbuf = smem_u32(smem + b * L::BUF);
+        const uint32_t sdz = sbuf + 9 * L::SLOT;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const uint32_t sa = sbuf + (uint32_t)(mt * L::TAPS_PER_M * L::SLOT);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)   // 16 pixels per MMA = two 8-row groups
+            mma_bf16(tmem + (uint32_t)(mt * CO), mndesc<RB>(sa + k * 16 * RB, L::SLOT),
+                     mndesc<RBO>(sdz + k * 16 * RBO, 128 * RBO), idesc,
+                     (c > c0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[b]);
+      }
+      mma_commit(done);
+    }
+    __syncwarp();
+  } else {
+    // warps 2..5: one TMEM lane quadrant each; row r of M-tile mt is dW row mt·128 + r
+    const int q = warp & 3;
+    if (c1 > c0) {
+      mbar_wait(done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    float* dst = part + (long)blockIdx.x * 9 * CI * CO;
+#pragma unroll 1
+    for (int mt = 0; mt < MT; ++mt) {
+      const int row = mt * 128 + q * 32 + lane;
+#pragma unroll 1
+      for (int cc = 0; cc < CO; cc += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * CO + cc), r);
+        if (row < 9 * CI) {
+          float4* o = reinterpret_cast<float4*>(dst + (long)row * CO + cc);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            o[j] = c1 > c0 ? make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -344,6 +509,92 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
   return PPLL_ERR_UNSUPPORTED;
 }
 
+// dW[9·CI, CO] (fp32, the GEMM weight layout) of conv3x3(x) given dZ [P, CO]:
+// implicit-GEMM partials (conv3x3_wgrad_tc_kernel) + the fixed-order split-K
+// reduction.  ws must hold splits·9·CI·CO floats.  PPLL_ERR_UNSUPPORTED for
+// shapes outside the kernel (the caller keeps im2col + GEMM).
+int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* x,
+                            const __nv_bfloat16* dz, float* dw, float* ws, size_t ws_elems,
+                            cudaStream_t s) {
+  using namespace cv;
+  static const int off = getenv("PPLL_CONV_WGRAD_IMPLICIT") ? !atoi(getenv("PPLL_CONV_WGRAD_IMPLICIT")) : 0;
+  if (off) return PPLL_ERR_UNSUPPORTED;
+  const long P = (long)N * H * W;
+  if (CI % 16 || CO % 16 || CI > 64 || CO > 64 || P % 128 || !ws) return PPLL_ERR_UNSUPPORTED;
+  int rows, imgs;
+  if (W > 128 || 128 % W) return PPLL_ERR_UNSUPPORTED;
+  if (128 / W <= H) {
+    rows = 128 / W;
+    imgs = 1;
+    if (H % rows) return PPLL_ERR_UNSUPPORTED;
+  } else {
+    if (128 % (H * W)) return PPLL_ERR_UNSUPPORTED;
+    rows = H;
+    imgs = 128 / (H * W);
+  }
+  if (((uintptr_t)x & 15) || ((uintptr_t)dz & 15) || ((uintptr_t)dw & 15)) return PPLL_ERR_UNSUPPORTED;
+  auto enc = encoder();
+  if (!enc) return PPLL_ERR_UNSUPPORTED;
+  CUtensorMap xm, dm;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)CI, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)CI * 2, (cuuint64_t)W * CI * 2, (cuuint64_t)H * W * CI * 2};
+    cuuint32_t box[4] = {(cuuint32_t)CI, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle sz = CI == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : (CI == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    if (enc(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<__nv_bfloat16*>(x), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return PPLL_ERR_UNSUPPORTED;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)CO, (cuuint64_t)P};
+    cuuint64_t strides[1] = {(cuuint64_t)CO * 2};
+    cuuint32_t box[2] = {(cuuint32_t)CO, 128};
+    cuuint32_t es[2] = {1, 1};
+    const CUtensorMapSwizzle sz = CO == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : (CO == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    if (enc(&dm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(dz), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return PPLL_ERR_UNSUPPORTED;
+  }
+  // splits: at least two chunks per CTA where the CTA double-buffers its
+  // chunks (CI < 64), one otherwise; the partials must fit the workspace
+  const int chunks = (int)(P / 128);
+  static const int minc_env = getenv("PPLL_CONV_WGRAD_MINC") ? atoi(getenv("PPLL_CONV_WGRAD_MINC")) : 0;
+  const int minc = minc_env > 0 ? minc_env : (CI == 64 ? 1 : 2);
+  int splits = chunks / minc < kNumSMs ? chunks / minc : kNumSMs;
+  if (splits < 1) splits = 1;
+  while (splits > 1 && (size_t)splits * 9 * CI * CO > ws_elems) --splits;
+  if ((size_t)splits * 9 * CI * CO > ws_elems) return PPLL_ERR_UNSUPPORTED;
+  const int per = (chunks + splits - 1) / splits;
+  splits = (chunks + per - 1) / per;   // every split owns >= 1 chunk
+  const int Pi = (int)P;
+#define WG_CASE(A, B)                                                                        \
+  if (CI == A && CO == B) {                                                                  \
+    auto kern = conv3x3_wgrad_tc_kernel<A, B>;                                               \
+    constexpr int smem = WgSmem<A, B>::TOTAL;                                                \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      attr = true;                                                                           \
+    }                                                                                        \
+    launch_k(kern, splits, 192, smem, s, xm, dm, Pi, H, W, ws);                              \
+    note_launch();                                                                           \
+    PPLL_LAUNCH_CHECK();                                                                     \
+  } else
+  WG_CASE(16, 16) WG_CASE(32, 32) WG_CASE(64, 64) WG_CASE(16, 32) WG_CASE(32, 16)
+  WG_CASE(32, 64) WG_CASE(64, 32) { return PPLL_ERR_UNSUPPORTED; }
+#undef WG_CASE
+  Epilogue<float> e;
+  e.C = dw;
+  e.ldc = CO;
+  epilogue_finalize(e, CO);
+  return launch_splitk_reduce<float>(9 * CI, CO, splits, ws, e, s);
+}
+
 }  // namespace ppll
 
 extern "C" int ppll_conv3x3_bf16_ex(int N, int H, int W, int Cin, int Cout, const void* x,
@@ -367,4 +618,24 @@ extern "C" int ppll_conv3x3_bf16_ex(int N, int H, int W, int Cin, int Cout, cons
 extern "C" int ppll_conv3x3_bf16(int N, int H, int W, int Cin, int Cout, const void* x,
                                  const void* w, void* y, int dgrad, void* stream) {
   return ppll_conv3x3_bf16_ex(N, H, W, Cin, Cout, x, w, y, dgrad, nullptr, nullptr, stream);
+}
+
+// dW (fp32 [9·Cin, Cout], the GEMM weight layout) of the 3x3 / stride-1 conv
+// of x [N,H,W,Cin] given dz = dLoss/dconv-output [N·H·W, Cout]; ws: split-K
+// partials (ppll_conv3x3_wgrad_ws_floats)
+extern "C" long ppll_conv3x3_wgrad_ws_floats(int N, int H, int W, int Cin, int Cout) {
+  (void)N; (void)H; (void)W;
+  return 148L * 9 * Cin * Cout;
+}
+extern "C" int ppll_conv3x3_wgrad_bf16(int N, int H, int W, int Cin, int Cout, const void* x,
+                                       const void* dz, float* dw, float* ws, long ws_floats,
+                                       void* stream) {
+  using namespace ppll;
+  if (N < 1 || H < 1 || W < 1 || !x || !dz || !dw || !ws || ws_floats < 1) {
+    set_error("ppll_conv3x3_wgrad_bf16: invalid arguments");
+    return PPLL_ERR_ARG;
+  }
+  return launch_conv3x3_wgrad_tc(N, H, W, Cin, Cout, (const __nv_bfloat16*)x,
+                                 (const __nv_bfloat16*)dz, dw, ws, (size_t)ws_floats,
+                                 reinterpret_cast<cudaStream_t>(stream));
 }

@@ -657,7 +657,8 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
     PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  const int grid = sc.items < kNumSMs ? sc.items : kNumSMs;
+  const int lim = (g_gemm_cap > 0 && g_gemm_cap < kNumSMs) ? g_gemm_cap : kNumSMs;
+  const int grid = sc.items < lim ? sc.items : lim;
   launch_k(kern, grid, kThreads, smem, s, ma, mb, M, N, K, sc, ep, part);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -949,7 +950,8 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
       const long tiles = (long)mt * ceil_div(N, c);
       for (int cs = 2; cs <= 8; ++cs) {
         if (K < cs * 4 * BK) break;
-        const int cap = capacity_any<TO>(a_kmajor, b_kmajor, c, cs);
+        int cap = capacity_any<TO>(a_kmajor, b_kmajor, c, cs);
+        if (g_wgrad_cap > 0 && cap > g_wgrad_cap / cs) cap = g_wgrad_cap / cs;
         if (cap <= 0) continue;
         const double waves = (double)((tiles + cap - 1) / cap);
         const double kb = (double)ceil_div(K, cs * BK);

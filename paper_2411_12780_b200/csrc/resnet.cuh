@@ -52,5 +52,12 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
                       cudaStream_t s);
 template <typename T>
 int launch_gap_bwd(int N, int HW, int C, const T* dp, T* dx, cudaStream_t s);
+// implicit-GEMM weight gradient of the 3x3 / stride-1 convolution (conv_tc.cu):
+// dw [9·CI, CO] fp32 (the GEMM weight layout) from x [N,H,W,CI] and dz [P,CO];
+// ws: split-K partials (splits·9·CI·CO floats).  PPLL_ERR_UNSUPPORTED outside
+// the kernel's shapes.
+int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* x,
+                            const __nv_bfloat16* dz, float* dw, float* ws, size_t ws_elems,
+                            cudaStream_t s);
 
 }  // namespace ppll

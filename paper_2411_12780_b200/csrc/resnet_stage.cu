@@ -230,15 +230,25 @@ static int conv_bwd(ppll_resnet_stage* st, ConvBN& c, int B, int slot, int64_t w
   const int P = B * c.h_out * c.h_out;
   char* dz = bs.dz[slot];
   bs.sf.fork();
-  int r;
-  if (c.implicit) {   // the weight gradient still contracts over the im2col'd input
-    r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)c.x_in,
-                          (TT*)c.col, bs.sf.ss);
+  int r = PPLL_ERR_UNSUPPORTED;
+  if (c.implicit) {
+    // implicit-GEMM weight gradient: tap windows gathered by TMA, no im2col
+    r = launch_conv3x3_wgrad_tc(B, c.h_in, c.h_in, c.cin, c.cout,
+                                (const __nv_bfloat16*)c.x_in, (const __nv_bfloat16*)dz,
+                                st->G(w_off), bs.wsw, st->ws_elems, bs.sf.ss);
+    if (r != PPLL_OK && r != PPLL_ERR_UNSUPPORTED) return r;
+    if (r == PPLL_ERR_UNSUPPORTED) {   // the GEMM still contracts over the im2col'd input
+      r = launch_im2col<TT>(B, c.h_in, c.h_in, c.cin, c.k, c.stride, c.kp, (const TT*)c.x_in,
+                            (TT*)c.col, bs.sf.ss);
+      if (r) return r;
+      r = PPLL_ERR_UNSUPPORTED;
+    }
+  }
+  if (r == PPLL_ERR_UNSUPPORTED) {
+    r = linear_wgrad(P, c.kp, c.cout, c.col, c.kp, dz, c.cout, st->G(w_off), nullptr,
+                     st->dtype, bs.wsw, st->ws_elems, bs.sf.ss);
     if (r) return r;
   }
-  r = linear_wgrad(P, c.kp, c.cout, c.col, c.kp, dz, c.cout, st->G(w_off), nullptr,
-                   st->dtype, bs.wsw, st->ws_elems, bs.sf.ss);
-  if (r) return r;
   bs.dz_done[slot] = bs.sf.mark();
   if (!dx) return r;
   if (c.implicit) {

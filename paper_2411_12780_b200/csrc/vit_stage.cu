@@ -211,6 +211,18 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
   // launch at the end of the backward; each LN backward gets its own slab
   LnDefer dfr;
   int nslab = 0;
+  // SM budgets (experiment, PPLL_DGRAD_CAP / PPLL_WGRAD_CAP): with the weight
+  // gradients on the side stream, cap the data-gradient chain's GEMM grid and
+  // the cluster wgrads' footprint so both streams' kernels can co-reside
+  static const int dcap = getenv("PPLL_DGRAD_CAP") ? atoi(getenv("PPLL_DGRAD_CAP")) : 0;
+  static const int wcap = getenv("PPLL_WGRAD_CAP") ? atoi(getenv("PPLL_WGRAD_CAP")) : 0;
+  struct CapScope {
+    int g0, w0;
+    CapScope(bool on, int d, int w) : g0(g_gemm_cap), w0(g_wgrad_cap) {
+      if (on) { g_gemm_cap = d; g_wgrad_cap = w; }
+    }
+    ~CapScope() { g_gemm_cap = g0; g_wgrad_cap = w0; }
+  } caps(sf.on(), dcap, wcap);
   auto slab = [&]() { return st->ln_parts + st->ln_slab * (size_t)(nslab++); };
   if (labels) {
     r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,

@@ -104,6 +104,42 @@ def test_resnet_pipeline_bitwise_equals_roundrobin(precision):
 
 
 @pytest.mark.parametrize("N,H,Cin,Cout", [(4, 32, 16, 16), (2, 16, 32, 32), (4, 8, 64, 64),
+                                          (2, 16, 16, 32), (6, 8, 64, 32), (128, 32, 16, 16),
+                                          (128, 16, 32, 32), (128, 8, 64, 64), (16, 8, 32, 64)])
+def test_implicit_conv3x3_wgrad_matches_torch(N, H, Cin, Cout):
+    """The implicit-GEMM weight gradient (TMA tap windows read MN-major, taps
+    stacked along M, split-K partials reduced in fixed order) against the
+    float64 torch weight gradient of conv2d on the same bf16 values, in the
+    GEMM weight layout [9·Cin, Cout]; deterministic across runs.  Includes the
+    ResNet-32 bench geometries at batch 128."""
+    import torch.nn.functional as Fn
+    from paper_2411_12780_b200 import _native as N_
+    g = torch.Generator(device="cuda").manual_seed(7 * N + H + Cin)
+    x = torch.randn(N, H, H, Cin, device="cuda", generator=g).bfloat16()
+    dz = torch.randn(N, H, H, Cout, device="cuda", generator=g).bfloat16()
+    lib = N_.load()
+    s = torch.cuda.current_stream().cuda_stream
+    nws = lib.ppll_conv3x3_wgrad_ws_floats(N, H, H, Cin, Cout)
+    ws = torch.empty(nws, device="cuda")
+    outs = []
+    for _ in range(2):
+        dw = torch.full((9 * Cin, Cout), float("nan"), device="cuda")
+        N_.check(lib.ppll_conv3x3_wgrad_bf16(N, H, H, Cin, Cout, x.data_ptr(), dz.data_ptr(),
+                                             dw.data_ptr(), ws.data_ptr(), nws, s), "conv wgrad")
+        torch.cuda.synchronize()
+        outs.append(dw.clone())
+    assert torch.equal(outs[0], outs[1])
+    xr = x.double().permute(0, 3, 1, 2)
+    wt = torch.zeros(Cout, Cin, 3, 3, dtype=torch.float64, device="cuda", requires_grad=True)
+    y = Fn.conv2d(xr, wt, padding=1)
+    y.backward(dz.double().permute(0, 3, 1, 2))
+    # [Cout, Cin, 3, 3] -> GEMM layout [(3r+s)·Cin + ci, co]
+    ref = wt.grad.permute(2, 3, 1, 0).reshape(9 * Cin, Cout)
+    err = (outs[0].double() - ref).abs().max().item() / (ref.abs().max().item() + 1e-12)
+    assert err < 1e-4, err
+
+
+@pytest.mark.parametrize("N,H,Cin,Cout", [(4, 32, 16, 16), (2, 16, 32, 32), (4, 8, 64, 64),
                                           (2, 16, 16, 32), (6, 8, 64, 32)])
 def test_implicit_conv3x3_matches_torch(N, H, Cin, Cout):
     """The implicit-GEMM conv (TMA 4-D window gathers, SW32/64/128 K-major
