@@ -44,6 +44,9 @@ enum { PPLL_F32 = 0, PPLL_BF16 = 1 };
 #define PPLL_ERRBIT_STEP 8    /* StepOutOfRange   optim.py:41-42    */
 #define PPLL_ERRBIT_GRAD 16   /* NonFiniteError   tensor.py:41-43: a non-finite gradient;
                                  the update is skipped (all-or-nothing) */
+#define PPLL_ERRBIT_SYNC 32   /* a device-side grid barrier gave up (watchdog): the stage's
+                                 results are invalid — a worker failure, WorkerPanic
+                                 (runtime.py:383-386) */
 
 /* GEMM engine selection for the bf16 path (PPLL_GEMM_AUTO picks tcgen05 when
  * the shape/alignment allows, else the SIMT kernel for skinny shapes). */
@@ -198,6 +201,12 @@ int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx,
  * thread's previous setting.  On by default (PPLL_PDL=0 in the environment
  * turns it off). */
 int ppll_set_pdl(int on);
+/* 1 (default; PPLL_GPU_EXCLUSIVE=0 in the environment flips it): the stage
+ * steps the CALLING THREAD launches own their GPU, so full-GPU cooperative
+ * kernels (the grid form of the fused BatchNorm) may be used; 0: several stage
+ * streams share the GPU (the single-GPU pipeline) and only kernels that leave
+ * SMs to the other streams are launched.  Returns the previous setting. */
+int ppll_set_gpu_exclusive(int on);
 /* out_ms[i] = milliseconds from event `ref` to events[i] (cudaEvent_t
  * handles, all recorded and complete): the per-step timestamps behind
  * EpochMetrics busy / wall time (runtime.py:340-354, 383-406), read in one

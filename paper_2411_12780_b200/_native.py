@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("PPLL_LIB") or os.path.join(_HERE, "lib", "libppll_b20
 PPLL_OK, PPLL_ERR_ARG, PPLL_ERR_CUDA, PPLL_ERR_UNSUPPORTED, PPLL_ERR_CLOSED = 0, 1, 2, 3, 4
 F32, BF16 = 0, 1
 ERRBIT_LABEL, ERRBIT_LOSS, ERRBIT_PARAM, ERRBIT_STEP, ERRBIT_GRAD = 1, 2, 4, 8, 16
+ERRBIT_SYNC = 32
 GEMM_AUTO, GEMM_SIMT, GEMM_TCGEN05 = 0, 1, 2
 
 _vp, _i, _i64, _f, _d, _u64 = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_double, C.c_uint64
@@ -50,6 +51,7 @@ SIGNATURES = {
     "ppll_gather_rows_u8": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "ppll_events_elapsed": (_i, [_i, _vp, C.c_uint64, _vp]),
     "ppll_set_pdl": (_i, [_i]),
+    "ppll_set_gpu_exclusive": (_i, [_i]),
     "ppll_count_correct": (_i, [_i, _i, _vp, _i, _i, _vp, _vp, _vp]),
     "ppll_stage_create": (_vp, [_i, _i, _vp, _vp, _vp, _vp, _i64, _i, _i, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _i, _vp, _vp, _f, _f]),

@@ -333,6 +333,8 @@ class LocalModule:
             exc = LabelOutOfRange("labels must lie in [0, num_classes)")
         elif e & (N.ERRBIT_LOSS | N.ERRBIT_PARAM | N.ERRBIT_GRAD):
             exc = NonFiniteError("local step produced non-finite values")
+        elif e & N.ERRBIT_SYNC:
+            exc = TimeoutError("a device grid barrier timed out (stage results invalid)")
         else:
             exc = StepOutOfRange(f"step outside [0, {self.schedule.total_steps}]")
         if stage is None:

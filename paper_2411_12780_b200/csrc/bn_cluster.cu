@@ -61,6 +61,9 @@ struct FwdArgs {
   int relu;
   __nv_bfloat16* y;
   unsigned long long* tl;             // PPLL_BN_TIMELINE probe: per CTA 8 %globaltimer stamps
+  float4* gpart;                      // grid form: per-CTA partials [grid][C]
+  unsigned* gbar;                     // grid form: {arrivals, generation}
+  int* err;                           // grid form: sticky error word (watchdog: kErrSync)
 };
 
 struct BwdArgs {
@@ -78,6 +81,9 @@ struct BwdArgs {
   float *dg2, *db2;
   __nv_bfloat16* dz2;
   unsigned long long* tl;
+  float4* gpart;
+  unsigned* gbar;
+  int* err;
 };
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
@@ -187,6 +193,86 @@ __device__ __forceinline__ float lanes_sum(float v, int V) {
   return v;
 }
 
+
+// ---- cross-CTA merge of the per-channel partials (cpart[c], c < C) ----------
+// CLUSTER: read the CS peers' partials over DSMEM in rank order.
+// GRID (cooperative launch, every CTA co-resident): publish the partial to
+// global memory, meet at a self-resetting grid barrier (arrival count +
+// generation word; a watchdog gives up after ~0.5 s and raises the flag word
+// instead of hanging), then sum the grid's partials in a fixed decomposition
+// (512/C strided groups in ascending CTA order, groups combined in order).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int* err) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const unsigned long long t0 = gtimer();
+      while (*vgen == g) {
+        if (gtimer() - t0 > 500000000ull) {
+          if (err) atomicOr(err, kErrSync);
+          break;
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+template <bool GRID>
+__device__ __forceinline__ float4 merge_partials(const float4* cpart, float4* scratch, int C,
+                                                 float4* gpart, unsigned* gbar, int* err) {
+  const int t = threadIdx.x;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if constexpr (!GRID) {
+    cluster_sync();   // every CTA's partial sums are in its shared memory
+    if (t < C) {
+      const int CS = (int)cluster_nctarank();
+      const uint32_t la = smem_u32(&cpart[t]);
+      float4 q[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (r < CS) q[r] = ld_dsmem_f4(la, (uint32_t)r);
+      acc = q[0];
+#pragma unroll
+      for (int r = 1; r < 16; ++r)
+        if (r < CS) { acc.x += q[r].x; acc.y += q[r].y; acc.z += q[r].z; acc.w += q[r].w; }
+    }
+  } else {
+    if (t < C) gpart[(long)blockIdx.x * C + t] = cpart[t];
+    __threadfence();
+    grid_barrier(gbar, err);
+    const int G = kThreads / C, g = t / C, c = t % C;
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g < G)
+      for (int r0 = g; r0 < (int)gridDim.x; r0 += 8 * G) {   // eight loads in flight
+        float4 q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r0 + u * G;
+          q[u] = r < (int)gridDim.x ? __ldcg(&gpart[(long)r * C + c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { s4.x += q[u].x; s4.y += q[u].y; s4.z += q[u].z; s4.w += q[u].w; }
+      }
+    if (g < G) scratch[g * C + c] = s4;
+    __syncthreads();
+    if (t < C) {
+      acc = scratch[t];
+      for (int k = 1; k < G; ++k) {
+        const float4 q = scratch[k * C + t];
+        acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+      }
+    }
+  }
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // forward: per channel, with one shift K = z[0, c] for the whole cluster,
 //   S1 = Σ (z − K), S2 = Σ (z − K)²   (plain fixed-order sums, no divisions)
@@ -194,7 +280,7 @@ __device__ __forceinline__ float lanes_sum(float v, int V) {
 //   y = act( z·s + t  [+ z2·s2 + t2 | + res] ),  s = γ·rstd, t = β − mean·s
 // RESIDENT: the whole slice (incl. res) fits in the ring: one HBM read.
 // ---------------------------------------------------------------------------
-template <bool TWO, bool RES, bool RESIDENT>
+template <bool TWO, bool RES, bool RESIDENT, bool GRID = false>
 __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __grid_constant__ FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -204,7 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int C = a.C, V = C >> 3, vc = t % V;
-  const int CS = (int)cluster_nctarank(), rank = (int)cluster_ctarank();
+  const int CS = GRID ? (int)gridDim.x : (int)cluster_nctarank();
+  const int rank = GRID ? (int)blockIdx.x : (int)cluster_ctarank();
   const int rpc = (a.P + CS - 1) / CS;
   const int r0 = min(a.P, rank * rpc), r1 = min(a.P, r0 + rpc);
   const long bytes = (long)(r1 - r0) * C * 2, o = (long)r0 * C;
@@ -295,17 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
     cpart[t] = sacc;
   }
   BN_TL(3)
-  cluster_sync();   // every CTA's partial sums are in its shared memory
+  const float4 sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
   if (t < C) {
-    const uint32_t la = smem_u32(&cpart[t]);
-    float4 q[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (r < CS) q[r] = ld_dsmem_f4(la, (uint32_t)r);
-    float4 sacc = q[0];
-#pragma unroll
-    for (int r = 1; r < 16; ++r)
-      if (r < CS) { sacc.x += q[r].x; sacc.y += q[r].y; sacc.z += q[r].z; sacc.w += q[r].w; }
     const float invP = 1.f / (float)a.P;
     {
       const float m1 = sacc.x * invP;
@@ -326,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
       if (rank == 0) { a.mean2[t] = mean; a.rstd2[t] = rstd; }
     }
   }
-  cluster_arrive();   // done reading the peers' partials
+  if constexpr (!GRID) cluster_arrive();   // done reading the peers' partials
   __syncthreads();
   BN_TL(4)
 
@@ -374,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
     }
   }
   BN_TL(5)
-  cluster_wait();     // no CTA leaves while a peer may still read its partial
+  if constexpr (!GRID) cluster_wait();   // no CTA leaves while a peer may still read its partial
   BN_TL(6)
 }
 
@@ -382,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
 // backward: dy = dout [⊙ (out > 0)];  dγ = Σ dy·x̂, dβ = Σ dy (cluster-merged);
 //   dz = γ·rstd·(dy − (dβ + x̂·dγ)/P) = A·dy + B·z + D   [dz2 likewise]
 // ---------------------------------------------------------------------------
-template <bool MASK, bool TWO, bool RESIDENT>
+template <bool MASK, bool TWO, bool RESIDENT, bool GRID = false>
 __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __grid_constant__ BwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -392,7 +470,8 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int C = a.C, V = C >> 3, vc = t % V;
-  const int CS = (int)cluster_nctarank(), rank = (int)cluster_ctarank();
+  const int CS = GRID ? (int)gridDim.x : (int)cluster_nctarank();
+  const int rank = GRID ? (int)blockIdx.x : (int)cluster_ctarank();
   const int rpc = (a.P + CS - 1) / CS;
   const int r0 = min(a.P, rank * rpc), r1 = min(a.P, r0 + rpc);
   const long bytes = (long)(r1 - r0) * C * 2, o = (long)r0 * C;
@@ -476,17 +555,8 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
     cpart[t] = sacc;
   }
   BN_TL(3)
-  cluster_sync();
+  const float4 sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
   if (t < C) {
-    const uint32_t la = smem_u32(&cpart[t]);
-    float4 q[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (r < CS) q[r] = ld_dsmem_f4(la, (uint32_t)r);
-    float4 sacc = q[0];
-#pragma unroll
-    for (int r = 1; r < 16; ++r)
-      if (r < CS) { sacc.x += q[r].x; sacc.y += q[r].y; sacc.z += q[r].z; }
     // dz = k1·(dy − db/P − x̂·dg/P) = A·dy + B·z + D
     const float k1 = pg * pr;
     const float Bc = -k1 * pr * sacc.x * a.invP;
@@ -509,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
       }
     }
   }
-  cluster_arrive();
+  if constexpr (!GRID) cluster_arrive();
   __syncthreads();
   BN_TL(4)
 
@@ -559,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
     }
   }
   BN_TL(5)
-  cluster_wait();
+  if constexpr (!GRID) cluster_wait();
   BN_TL(6)
 }
 
@@ -602,6 +672,46 @@ static int cluster_size_for(K kern) {
   return 0;
 }
 
+// grid form: every CTA co-resident (cooperative launch), one CTA per SM
+template <typename K, typename A>
+static int launch_grid(K kern, const A& args, cudaStream_t s) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  static const void* keys[32];
+  static int vals[32];
+  static int n = 0;
+  int grid = -1;
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == (const void*)kern) grid = vals[i];
+  if (grid < 0) {
+    int occ = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, kSmem) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 0;
+    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = occ > 0 ? sms : 0;   // one CTA per SM (the ring takes ~200 KB)
+    if (n < 32) { keys[n] = (const void*)kern; vals[n++] = grid; }
+  }
+  if (grid <= 0) return PPLL_ERR_UNSUPPORTED;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, args));
+  note_launch();
+  return PPLL_OK;
+}
+
 template <typename K, typename A>
 static int launch_cluster(K kern, int cs, const A& args, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -629,12 +739,15 @@ static int launch_cluster(K kern, int cs, const A& args, cudaStream_t s) {
 // so it is used where it is measured faster (tools/ab_bn.sh): forward up to
 // PPLL_BN_FWD_MAX_MB (default 2.5) MB per tensor, backward up to
 // PPLL_BN_BWD_MAX_MB (default 1.2).
-static bool fused_ok(long P, int C, bool bwd) {
+static int fused_mode(long P, int C, bool bwd, bool grid_ok) {
   static const int off = getenv("PPLL_BN_FUSED") ? !atoi(getenv("PPLL_BN_FUSED")) : 0;
   static const double fwd_mb = getenv("PPLL_BN_FWD_MAX_MB") ? atof(getenv("PPLL_BN_FWD_MAX_MB")) : 2.5;
   static const double bwd_mb = getenv("PPLL_BN_BWD_MAX_MB") ? atof(getenv("PPLL_BN_BWD_MAX_MB")) : 1.2;
-  if (off || C % 8 || C > kMaxC || kThreads % (C / 8) || P < 1 || P > (1L << 30) / C) return false;
-  return (double)P * C * 2 <= (bwd ? bwd_mb : fwd_mb) * 1048576.0;
+  static const double grid_mb = getenv("PPLL_BN_GRID_MAX_MB") ? atof(getenv("PPLL_BN_GRID_MAX_MB")) : 64.0;
+  if (off || C % 8 || C > kMaxC || kThreads % (C / 8) || P < 1 || P > (1L << 30) / C) return 0;
+  const double mb = (double)P * C * 2 / 1048576.0;
+  if (mb <= (bwd ? bwd_mb : fwd_mb)) return 1;
+  return (grid_ok && g_gpu_excl && mb <= grid_mb) ? 2 : 0;
 }
 
 // cluster size + launch of one kernel instantiation; `resident` picks the
@@ -662,26 +775,39 @@ static int run_fused(K kern_stream, K kern_resident, long P, int C, const A& arg
   const bool res = (slice + Ring<NT>::PIECE - 1) / Ring<NT>::PIECE <= Ring<NT>::NS;
   return res ? launch_cluster(kern_resident, cs_r, args, s) : launch_cluster(kern_stream, cs, args, s);
 }
+template <int NT, typename K, typename A>
+static int run_grid(K kern_stream, K kern_resident, long P, int C, const A& args, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long slice = (P + sms - 1) / sms * C * 2;
+  const bool res = (slice + Ring<NT>::PIECE - 1) / Ring<NT>::PIECE <= Ring<NT>::NS;
+  return launch_grid(res ? kern_resident : kern_stream, args, s);
+}
 
 }  // namespace bnc
 
 int launch_bn_fwd_fused(int P, int C, const __nv_bfloat16* z, const float* g, const float* b,
                         float* mean, float* rstd, const __nv_bfloat16* z2, const float* g2,
                         const float* b2, float* mean2, float* rstd2, const __nv_bfloat16* res,
-                        int relu, __nv_bfloat16* y, cudaStream_t s) {
+                        int relu, __nv_bfloat16* y, cudaStream_t s, const BnGrid* grid) {
   using namespace bnc;
-  if (!fused_ok(P, C, false) || !aligned16(z) || !aligned16(z2) || !aligned16(res) || !aligned16(y))
+  const int mode = fused_mode(P, C, false, grid && grid->part && grid->bar);
+  if (!mode || !aligned16(z) || !aligned16(z2) || !aligned16(res) || !aligned16(y))
     return PPLL_ERR_UNSUPPORTED;
   if (z2 && res) return PPLL_ERR_UNSUPPORTED;
-  FwdArgs a{P, C, z, g, b, mean, rstd, z2, g2, b2, mean2, rstd2, res, relu, y, bn_tl()};
-  if (z2)
-    return run_fused<2>(bn_fwd_cluster_kernel<true, false, false>,
-                        bn_fwd_cluster_kernel<true, false, true>, P, C, a, s);
-  if (res)
-    return run_fused<2>(bn_fwd_cluster_kernel<false, true, false>,
-                        bn_fwd_cluster_kernel<false, true, true>, P, C, a, s);
-  return run_fused<1>(bn_fwd_cluster_kernel<false, false, false>,
-                      bn_fwd_cluster_kernel<false, false, true>, P, C, a, s);
+  FwdArgs a{P, C, z, g, b, mean, rstd, z2, g2, b2, mean2, rstd2, res, relu, y, bn_tl(),
+            mode == 2 ? (float4*)grid->part : nullptr, mode == 2 ? grid->bar : nullptr,
+            mode == 2 ? grid->err : nullptr};
+#define PPLL_BN_FWD(NT_, T_, R_)                                                                 \
+  return mode == 2 ? run_grid<NT_>(bn_fwd_cluster_kernel<T_, R_, false, true>,                   \
+                                   bn_fwd_cluster_kernel<T_, R_, true, true>, P, C, a, s)        \
+                   : run_fused<NT_>(bn_fwd_cluster_kernel<T_, R_, false>,                        \
+                                    bn_fwd_cluster_kernel<T_, R_, true>, P, C, a, s);
+  if (z2) { PPLL_BN_FWD(2, true, false) }
+  if (res) { PPLL_BN_FWD(2, false, true) }
+  PPLL_BN_FWD(1, false, false)
+#undef PPLL_BN_FWD
 }
 
 int launch_bn_bwd_fused(int P, int C, const __nv_bfloat16* dout, const __nv_bfloat16* out,
@@ -689,24 +815,26 @@ int launch_bn_bwd_fused(int P, int C, const __nv_bfloat16* dout, const __nv_bflo
                         const float* rstd, const float* g, float* dg, float* db, __nv_bfloat16* dz,
                         const __nv_bfloat16* z2, const float* mean2, const float* rstd2,
                         const float* g2, float* dg2, float* db2, __nv_bfloat16* dz2,
-                        cudaStream_t s) {
+                        cudaStream_t s, const BnGrid* grid) {
   using namespace bnc;
-  if (!fused_ok(P, C, true) || !aligned16(dout) || !aligned16(out) || !aligned16(dy_store) ||
-      !aligned16(z) || !aligned16(dz) || !aligned16(z2) || !aligned16(dz2))
+  const int mode = fused_mode(P, C, true, grid && grid->part && grid->bar);
+  if (!mode || !aligned16(dout) || !aligned16(out) || !aligned16(dy_store) || !aligned16(z) ||
+      !aligned16(dz) || !aligned16(z2) || !aligned16(dz2))
     return PPLL_ERR_UNSUPPORTED;
   BwdArgs a{P, C, 1.f / (float)P, dout, out, out ? dy_store : nullptr, z, mean, rstd, g, dg, db, dz,
-            z2, mean2, rstd2, g2, dg2, db2, dz2, bn_tl()};
-  if (out && z2)
-    return run_fused<4>(bn_bwd_cluster_kernel<true, true, false>,
-                        bn_bwd_cluster_kernel<true, true, true>, P, C, a, s);
-  if (out)
-    return run_fused<3>(bn_bwd_cluster_kernel<true, false, false>,
-                        bn_bwd_cluster_kernel<true, false, true>, P, C, a, s);
-  if (z2)
-    return run_fused<3>(bn_bwd_cluster_kernel<false, true, false>,
-                        bn_bwd_cluster_kernel<false, true, true>, P, C, a, s);
-  return run_fused<2>(bn_bwd_cluster_kernel<false, false, false>,
-                      bn_bwd_cluster_kernel<false, false, true>, P, C, a, s);
+            z2, mean2, rstd2, g2, dg2, db2, dz2, bn_tl(),
+            mode == 2 ? (float4*)grid->part : nullptr, mode == 2 ? grid->bar : nullptr,
+            mode == 2 ? grid->err : nullptr};
+#define PPLL_BN_BWD(NT_, M_, T_)                                                                 \
+  return mode == 2 ? run_grid<NT_>(bn_bwd_cluster_kernel<M_, T_, false, true>,                   \
+                                   bn_bwd_cluster_kernel<M_, T_, true, true>, P, C, a, s)        \
+                   : run_fused<NT_>(bn_bwd_cluster_kernel<M_, T_, false>,                        \
+                                    bn_bwd_cluster_kernel<M_, T_, true>, P, C, a, s);
+  if (out && z2) { PPLL_BN_BWD(4, true, true) }
+  if (out) { PPLL_BN_BWD(3, true, false) }
+  if (z2) { PPLL_BN_BWD(3, false, true) }
+  PPLL_BN_BWD(2, false, false)
+#undef PPLL_BN_BWD
 }
 
 }  // namespace ppll

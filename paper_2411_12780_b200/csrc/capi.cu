@@ -16,6 +16,7 @@ int g_gemm_engine = PPLL_GEMM_AUTO;
 // their own setting (a process-wide flag could be flipped under a capture)
 thread_local int g_pdl = getenv("PPLL_PDL") ? atoi(getenv("PPLL_PDL")) : 1;
 thread_local int g_gemm_cap = 0, g_wgrad_cap = 0;
+thread_local int g_gpu_excl = getenv("PPLL_GPU_EXCLUSIVE") ? atoi(getenv("PPLL_GPU_EXCLUSIVE")) : 1;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -234,6 +235,12 @@ int ppll_gather_rows(int n, int64_t width, const float* src, const int64_t* idx,
 int ppll_set_pdl(int on) {
   const int prev = g_pdl;
   g_pdl = on ? 1 : 0;
+  return prev;
+}
+
+int ppll_set_gpu_exclusive(int on) {
+  const int prev = g_gpu_excl;
+  g_gpu_excl = on ? 1 : 0;
   return prev;
 }
 

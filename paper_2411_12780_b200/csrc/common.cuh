@@ -18,6 +18,7 @@ enum ErrBits : int {
   kErrParamNonFinite = PPLL_ERRBIT_PARAM, // NonFiniteError    (tensor.py:41-43)
   kErrStep = PPLL_ERRBIT_STEP,            // StepOutOfRange    (optim.py:41-42)
   kErrGradNonFinite = PPLL_ERRBIT_GRAD,   // NonFiniteError    (tensor.py:41-43, pre-update)
+  kErrSync = PPLL_ERRBIT_SYNC,            // WorkerPanic       (a grid barrier watchdog fired)
 };
 
 void set_error(const char* fmt, ...);
@@ -84,6 +85,11 @@ extern thread_local int g_pdl;
 // whole GPU): a stage step caps its data-gradient GEMMs / cluster weight
 // gradients so the two streams' kernels can be resident side by side
 extern thread_local int g_gemm_cap, g_wgrad_cap;
+// 1 when the kernels this host thread launches own their GPU (one stage
+// stream): full-GPU cooperative kernels (the grid-form fused BN) are allowed.
+// A pipeline that puts several stage streams on one GPU sets 0 — a
+// cooperative grid needs every SM at once and would serialise the streams.
+extern thread_local int g_gpu_excl;
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

@@ -49,6 +49,26 @@ int ppll_layernorm_bwd(int M, int D, const void* dy, long lddy, const void* x, l
                             (const B16*)dres, ldres, (B16*)dx, lddx, ws, dg, db, s, dxsum);
 }
 
+// scratch of the grid-form fused BN for the C-ABI entry points (one set per
+// process: these entry points are not meant for concurrent streams)
+static const BnGrid* capi_bn_grid() {
+  static BnGrid g{nullptr, nullptr, nullptr};
+  static bool init = false;
+  if (!init) {
+    init = true;
+    void* p = nullptr;
+    unsigned* b = nullptr;
+    if (cudaMalloc(&p, 256 * 128 * 16) == cudaSuccess && cudaMalloc(&b, 256) == cudaSuccess &&
+        cudaMemset(b, 0, 256) == cudaSuccess) {
+      g.part = p;
+      g.bar = b;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  return g.part ? &g : nullptr;
+}
+
 long ppll_batchnorm_ws_floats(int P, int C) { return (long)bn_chunks(P) * 3 * C; }
 
 // train-mode BatchNorm over the rows of an NHWC [P, C] tensor: batch
@@ -71,9 +91,10 @@ int ppll_batchnorm_fwd(int P, int C, const void* z, const float* g, const float*
                                   nullptr, nullptr, nullptr, (const float*)res, relu, (float*)y, s);
   }
   using B16 = __nv_bfloat16;
-  // one fused cluster launch where it applies (bn_cluster.cu), else stats + apply
+  // one fused launch where it applies (bn_cluster.cu: one cluster, or the
+  // whole GPU for large tensors), else stats + apply
   r = launch_bn_fwd_fused(P, C, (const B16*)z, g, b, mean, rstd, nullptr, nullptr, nullptr,
-                          nullptr, nullptr, (const B16*)res, relu, (B16*)y, s);
+                          nullptr, nullptr, (const B16*)res, relu, (B16*)y, s, capi_bn_grid());
   if (r != PPLL_ERR_UNSUPPORTED) return r;
   r = launch_bn_stats<B16>(P, C, (const B16*)z, ws, mean, rstd, s);
   if (r) return r;
@@ -97,7 +118,7 @@ int ppll_batchnorm_bwd(int P, int C, const void* dy, const void* z, const float*
   using B16 = __nv_bfloat16;
   const int r = launch_bn_bwd_fused(P, C, (const B16*)dy, nullptr, nullptr, (const B16*)z, mean,
                                     rstd, g, dg, db, (B16*)dz, nullptr, nullptr, nullptr, nullptr,
-                                    nullptr, nullptr, nullptr, s);
+                                    nullptr, nullptr, nullptr, s, capi_bn_grid());
   if (r != PPLL_ERR_UNSUPPORTED) return r;
   return launch_bn_bwd<B16>(P, C, (const B16*)dy, (const B16*)z, mean, rstd, g, ws, dg, db,
                             (B16*)dz, s);

@@ -30,16 +30,26 @@ int launch_bn_bwd(int P, int C, const T* dy, const T* z, const float* mean, cons
 // (masked by out > 0 when out != NULL; the masked dy stored when dy_store !=
 // NULL) to dz (and dz2 of a second BN sharing dy).  PPLL_ERR_UNSUPPORTED when
 // the shape / size is outside the fused kernel's range.
+// Tensors past the single-cluster range use the GRID form when the caller
+// provides its scratch (one co-resident CTA per SM, cooperative launch;
+// per-CTA partials + a self-resetting barrier {arrivals, generation}, zeroed
+// once; a watchdog sets kErrSync in *err instead of hanging).  One BnGrid per
+// stream of concurrently running BN launches.
+struct BnGrid {
+  void* part;      // >= 148 * 128 float4
+  unsigned* bar;   // 2 words, zero-initialised
+  int* err;        // sticky error word (nullable)
+};
 int launch_bn_fwd_fused(int P, int C, const __nv_bfloat16* z, const float* g, const float* b,
                         float* mean, float* rstd, const __nv_bfloat16* z2, const float* g2,
                         const float* b2, float* mean2, float* rstd2, const __nv_bfloat16* res,
-                        int relu, __nv_bfloat16* y, cudaStream_t s);
+                        int relu, __nv_bfloat16* y, cudaStream_t s, const BnGrid* grid = nullptr);
 int launch_bn_bwd_fused(int P, int C, const __nv_bfloat16* dout, const __nv_bfloat16* out,
                         __nv_bfloat16* dy_store, const __nv_bfloat16* z, const float* mean,
                         const float* rstd, const float* g, float* dg, float* db, __nv_bfloat16* dz,
                         const __nv_bfloat16* z2, const float* mean2, const float* rstd2,
                         const float* g2, float* dg2, float* db2, __nv_bfloat16* dz2,
-                        cudaStream_t s);
+                        cudaStream_t s, const BnGrid* grid = nullptr);
 template <typename T>
 int launch_gap(int N, int HW, int C, const T* x, T* out, cudaStream_t s);
 

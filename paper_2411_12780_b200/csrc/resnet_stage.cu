@@ -67,6 +67,7 @@ struct ppll_resnet_stage {
   char *dsum = nullptr, *dz = nullptr, *dy = nullptr, *dcol = nullptr, *dxa = nullptr,
        *dxb = nullptr, *dtmp = nullptr;
   float* bn_part = nullptr;
+  ppll::BnGrid bng{nullptr, nullptr, nullptr};   // scratch of the grid-form fused BN (main stream)
   float* ws = nullptr;
   size_t ws_elems = 0;
   // weight gradients (im2col + GEMM) on a side stream; the BN-backward output
@@ -157,7 +158,7 @@ static int bn_act(ppll_resnet_stage* st, int P, ConvBN& c, int64_t g, int64_t b,
         P, c.cout, (const __nv_bfloat16*)c.z, st->P(g), st->P(b), c.mean, c.rstd,
         c2 ? (const __nv_bfloat16*)c2->z : nullptr, c2 ? st->P(g2) : nullptr,
         c2 ? st->P(b2) : nullptr, c2 ? c2->mean : nullptr, c2 ? c2->rstd : nullptr,
-        (const __nv_bfloat16*)res, 1, (__nv_bfloat16*)y, s);
+        (const __nv_bfloat16*)res, 1, (__nv_bfloat16*)y, s, &st->bng);
     if (r != PPLL_ERR_UNSUPPORTED) return r;
   }
   int r = launch_bn_stats<TT>(P, c.cout, (const TT*)c.z, st->bn_part, c.mean, c.rstd, s);
@@ -204,7 +205,7 @@ static int bn_bwd(ppll_resnet_stage* st, int P, ConvBN& c, int64_t g, int64_t b,
         st->P(g), st->G(g), st->G(b), (__nv_bfloat16*)dz,
         c2 ? (const __nv_bfloat16*)c2->z : nullptr, c2 ? c2->mean : nullptr,
         c2 ? c2->rstd : nullptr, c2 ? st->P(g2) : nullptr, c2 ? st->G(g2) : nullptr,
-        c2 ? st->G(b2) : nullptr, (__nv_bfloat16*)dz2, s);
+        c2 ? st->G(b2) : nullptr, (__nv_bfloat16*)dz2, s, &st->bng);
     if (r != PPLL_ERR_UNSUPPORTED) return r;
   }
   const void* dy = dout;
@@ -534,6 +535,10 @@ ppll_resnet_stage* ppll_resnet_stage_create(const int* cfg, const int* geo, cons
   st->dxa = st->alloc(maxPC * e); st->dxb = st->alloc(maxPC * e); st->dtmp = st->alloc(maxPC * e);
   st->dcol = st->alloc(maxPK * e);
   st->bn_part = (float*)st->alloc((size_t)256 * 3 * maxC * 4);     // bn_chunks() <= 256
+  st->bng.part = st->alloc((size_t)256 * 128 * 16);
+  st->bng.bar = (unsigned*)st->alloc(256);
+  st->bng.err = st->err;
+  if (st->bng.bar) cudaMemset(st->bng.bar, 0, 256);
   // split-K partials of the largest weight gradient ([9·C, C]) for up to 160 splits
   st->ws_elems = std::max((size_t)1 << 22, (size_t)160 * 9 * maxC * maxC);
   st->ws = (float*)st->alloc(st->ws_elems * 4);

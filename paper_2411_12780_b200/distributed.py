@@ -251,7 +251,8 @@ class DistributedPipeline:
             with torch.cuda.stream(stream):
                 self._launch(p, slot, B, stream)
             return
-        key = (p.stage, slot, self._pdl)     # a graph keeps the PDL edges it was captured with
+        # a graph keeps the PDL edges / kernel forms it was captured with
+        key = (p.stage, slot, self._pdl, getattr(self, "_excl", 1))
         g = self.graphs.get(key)
         if g is None:
             g = torch.cuda.CUDAGraph()
@@ -283,10 +284,15 @@ class DistributedPipeline:
         want = int(os.environ["PPLL_PDL"] != "0") if "PPLL_PDL" in os.environ else int(not off)
         prev = self.lib.ppll_set_pdl(want)
         self._pdl = want
+        # several stages on this rank's GPU: no full-GPU cooperative kernels
+        excl = int(len(self.mods) == 1)
+        prev_excl = self.lib.ppll_set_gpu_exclusive(excl)
+        self._excl = excl
         try:
             return self._run(batches, n_batches, batch_size)
         finally:
             self.lib.ppll_set_pdl(prev)
+            self.lib.ppll_set_gpu_exclusive(prev_excl)
 
     def _run(self, batches: Iterable | None, n_batches: int, batch_size: int) -> dict:
         M, B = self.M, batch_size

@@ -294,6 +294,20 @@ def _run_backprop(modules, dataset_iter, config, pipelined: bool, virtual_time: 
     dev0 = mods[0].device
     streams = ([torch.cuda.Stream(device=m.device) for m in mods] if pipelined
                else [torch.cuda.Stream(device=dev0)] * s)
+    # stage streams sharing a GPU: no full-GPU cooperative kernels
+    shared_dev = pipelined and len({str(m.device) for m in mods}) < s
+    lib = N.load()
+    prev_excl = lib.ppll_set_gpu_exclusive(int(not shared_dev))
+    try:
+        return _run_backprop_body(mods, dataset_iter, config, pipelined, virtual_time, metrics,
+                                  step0, dev0, streams)
+    finally:
+        lib.ppll_set_gpu_exclusive(prev_excl)
+
+
+def _run_backprop_body(mods, dataset_iter, config, pipelined, virtual_time, metrics, step0, dev0,
+                       streams):
+    s = len(mods)
     src = torch.cuda.Stream(device=dev0)
     _enable_peers(mods)
     timing = config.timing and not virtual_time
@@ -541,7 +555,8 @@ class DevicePipeline:
             with torch.cuda.stream(stream):
                 self._launch(j, slot, B, stream)
             return
-        key = (j, slot, self._pdl)           # a graph keeps the PDL edges it was captured with
+        # a graph keeps the PDL edges / kernel forms it was captured with
+        key = (j, slot, self._pdl, getattr(self, "_excl", 1))
         g = self.graphs.get(key)
         if g is None:
             g = torch.cuda.CUDAGraph()
@@ -572,10 +587,15 @@ class DevicePipeline:
         want = int(os.environ["PPLL_PDL"] != "0") if "PPLL_PDL" in os.environ else int(not shared)
         prev = lib.ppll_set_pdl(want)
         self._pdl = want
+        # several stage streams on one GPU: no full-GPU cooperative kernels
+        excl = int(max(len(v) for v in per_dev.values()) == 1)
+        prev_excl = lib.ppll_set_gpu_exclusive(excl)
+        self._excl = excl
         try:
             return self._run(dataset_iter)
         finally:
             lib.ppll_set_pdl(prev)
+            lib.ppll_set_gpu_exclusive(prev_excl)
 
     def _run(self, dataset_iter: Iterable) -> EpochMetrics:
         mods, M, s = self.modules, self.M, len(self.modules)

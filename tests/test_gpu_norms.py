@@ -70,7 +70,8 @@ def test_layernorm_matches_torch(precision, M, D):
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("P,C,res", [(131072, 16, False), (8192, 64, True), (2048, 32, True),
-                                     (300, 24, False)])
+                                     (300, 24, False), (131072, 16, True), (262144, 32, False),
+                                     (524288, 16, True), (1048576, 16, False)])
 def test_batchnorm_matches_torch(precision, P, C, res):
     dt = torch.float32 if precision == "fp32" else torch.bfloat16
     code = N.F32 if precision == "fp32" else N.BF16
