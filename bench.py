@@ -729,16 +729,18 @@ def roofline_attention(wl, hbm, dev, sets=4, reps=5):
             for _ in range(reps):
                 for bf in bufs:
                     fn(bf, st.cuda_stream)
-        g.replay()
+        with torch.cuda.stream(st):
+            g.replay()
         torch.cuda.synchronize(dev)
         best = float("inf")
         for _ in range(3):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(st)
-            g.replay()
-            b.record(st)
+            with torch.cuda.stream(st):      # replay on the stream the events bracket
+                a.record(st)
+                g.replay()
+                b.record(st)
             b.synchronize()
-            best = min(best, a.elapsed_time(b) * 1e-3 / (reps * sets))
+            best = min(best, a.elapsed_time(b) * 1e-3 / (reps * len(bufs)))
         return best
 
     t_f = per_launch(fwd)
