@@ -50,7 +50,7 @@ struct Smem {
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 192 ? 4 : 6);
   static constexpr int EPI = 2 * BN * 4;          // bias slice per accumulator buffer
   static constexpr int STG = kEpiWarps * 1024;    // per-warp store-transpose buffers
-  static constexpr int TOTAL = STAGES * STAGE + EPI + STG + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TOTAL = STAGES * STAGE + EPI + STG + 1024 /*align*/ + 512 /*barriers, work ring*/;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
 
@@ -60,6 +60,7 @@ struct Sched {
   CUtensorMap st_c, st_p;
   int tma_st;
   int drain_full;   // PPLL_GEMM_DRAIN_FULL=1: wait for the bulk stores' writes at exit
+  int clc;          // dynamic tile scheduling (grid = items, CLC try_cancel work stealing)
   int mt, nt, tiles, splits, kps, items;
   int probe;   // profiling probe (PPLL_GEMM_PROBE): 1 = skip the epilogue math/stores,
               // 2 = bias+GELU math only, 3 = stores only (interior tiles)
@@ -67,6 +68,34 @@ struct Sched {
   // MMA start / MMA done (tfull observed) / epilogue done, 4 tiles max
   unsigned long long* tl;
 };
+
+// Dynamic tile scheduling (Sched::clc): the grid has one CTA per work item;
+// a running CTA first takes its own item, then steals the items of CTAs the
+// hardware has not launched yet with clusterlaunchcontrol.try_cancel — so when
+// other streams' kernels hold some SMs, the CTAs that do run take more tiles
+// instead of leaving a static 1/148 share to CTAs that start late.  The TMA
+// producer thread owns the sequence and hands each item id to the MMA and
+// epilogue warps through a 4-deep shared-memory ring (full / empty mbarriers).
+__device__ __forceinline__ void clc_try_cancel(uint32_t resp, uint64_t* bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+      ::"r"(resp), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ int clc_decode(uint32_t resp) {
+  uint32_t x = 0, valid = 0;
+  asm volatile(
+      "{\n\t.reg .pred p1;\n\t.reg .b128 r;\n\t"
+      "ld.shared.b128 r, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p1, r;\n\t"
+      "selp.u32 %1, 1, 0, p1;\n\t"
+      "@p1 clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %0, r;\n\t}"
+      : "=r"(x), "=r"(valid)
+      : "r"(resp)
+      : "memory");
+  return valid ? (int)x : -1;
+}
+constexpr int kWorkRing = 4;
 
 // MC: CTA pair (cta_group::2, 2-CTA cluster): the pair computes one 256 x BN
 // tile — each CTA loads its 128 rows of A and BN/2 rows of B, the leader
@@ -94,7 +123,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;      // [2]
   uint64_t* tempty = tfull + 2;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wfull = tempty + 2;     // [kWorkRing] dynamic-schedule work ring
+  uint64_t* wempty = wfull + kWorkRing;
+  uint64_t* clc_bar = wempty + kWorkRing;
+  int* wq = reinterpret_cast<int*>(clc_bar + 1);                   // [kWorkRing]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wq + kWorkRing);
+  uint8_t* clc_resp = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tmem_slot) + 16 + 15) & ~uintptr_t(15));   // 16-B aligned
+  const bool clc = !MC && sc.clc;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
@@ -109,6 +145,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], MC ? 2 * kEpiWarps : kEpiWarps);   // pair: both CTAs' warps
     }
+    for (int i = 0; i < kWorkRing; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&wempty[i], 1 + kEpiWarps);                     // MMA warp + epilogue warps
+    }
+    mbar_init(clc_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -144,7 +185,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // ------------------------- TMA producer -------------------------
     if (lane == 0) {
       int kb_total = 0;
-      for (int w = wid0; w < items_w; w += wstride) {
+      int w = wid0;
+      for (int n = 0;; ++n) {
+        if (clc) {   // publish this item (or the end) to the MMA / epilogue warps
+          const int ws = n % kWorkRing;
+          mbar_wait(&wempty[ws], ((n / kWorkRing) & 1) ^ 1);
+          wq[ws] = w;
+          mbar_arrive(&wfull[ws]);
+          if (w < 0) break;
+          // ask for the next item while this one's operands stream in
+          mbar_expect_tx(clc_bar, 16);
+          clc_try_cancel(smem_u32(clc_resp), clc_bar);
+        } else {
+          if (n > 0) w += wstride;
+          if (w >= items_w) break;
+        }
         const int tile = w % tiles_w, z = MC ? 0 : w / sc.tiles;
         const int m0 = ((tile % mtw) * (MC ? 2 : 1) + rank) * BM, n0 = (tile / mtw) * BN;
         const int kbeg = z * sc.kps, kend = min(K, kbeg + sc.kps);
@@ -191,6 +246,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
               tma_load_2d(&map_b, &full[st], sb + i * 8192, n0 + 64 * i, k0);
           }
         }
+        if (clc) {
+          mbar_wait(clc_bar, n & 1);
+          w = clc_decode(smem_u32(clc_resp));
+        }
       }
     }
   } else if (warp == 1) {
@@ -200,7 +259,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                            ((uint32_t)((MC ? 2 * BM : BM) >> 4) << 24);
     if (lane == 0 && rank == 0) {   // pair: the leader issues for both CTAs
       int kb_total = 0, it = 0;
-      for (int w = wid0; w < items_w; w += wstride, ++it) {
+      int w = wid0;
+      for (int n = 0;; ++n, ++it) {
+        if (clc) {
+          const int ws = n % kWorkRing;
+          mbar_wait(&wfull[ws], (n / kWorkRing) & 1);
+          w = wq[ws];
+          mbar_arrive(&wempty[ws]);
+          if (w < 0) break;
+        } else {
+          if (n > 0) w += wstride;
+          if (w >= items_w) break;
+        }
         const int z = MC ? 0 : w / sc.tiles;
         const int kbeg = z * sc.kps, kend = min(K, kbeg + sc.kps);
         const int acc = it & 1;
@@ -243,7 +313,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int grp = (warp - 2) >> 2;
     uint8_t* stg = stg_all + (warp - 2) * 1024;
     int it = 0;
-    for (int w = wid0; w < items_w; w += wstride, ++it) {
+    int w = wid0;
+    for (int n = 0;; ++n, ++it) {
+      if (clc) {
+        const int ws = n % kWorkRing;
+        mbar_wait(&wfull[ws], (n / kWorkRing) & 1);
+        w = wq[ws];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wempty[ws]);
+        if (w < 0) break;
+      } else {
+        if (n > 0) w += wstride;
+        if (w >= items_w) break;
+      }
       const int tile = w % tiles_w, z = MC ? 0 : w / sc.tiles;
       const int m0 = ((tile % mtw) * (MC ? 2 : 1) + rank) * BM, n0 = (tile / mtw) * BN;
       const int acc = it & 1;
@@ -658,7 +740,8 @@ static int run(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K
     attr_set = true;
   }
   const int lim = (g_gemm_cap > 0 && g_gemm_cap < kNumSMs) ? g_gemm_cap : kNumSMs;
-  const int grid = sc.items < lim ? sc.items : lim;
+  // dynamic scheduling: one CTA per item, running CTAs steal unlaunched ones
+  const int grid = sc.clc ? sc.items : (sc.items < lim ? sc.items : lim);
   launch_k(kern, grid, kThreads, smem, s, ma, mb, M, N, K, sc, ep, part);
   note_launch();
   PPLL_LAUNCH_CHECK();
@@ -979,6 +1062,8 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
   sc.tma_st = 0;
   static const int drain_full = getenv("PPLL_GEMM_DRAIN_FULL") ? atoi(getenv("PPLL_GEMM_DRAIN_FULL")) : 0;
   sc.drain_full = drain_full;
+  static const int clc_env = getenv("PPLL_GEMM_CLC") ? atoi(getenv("PPLL_GEMM_CLC")) : 1;
+  sc.clc = clc_env && g_gemm_cap == 0;
   sc.mt = mt;
   sc.nt = ceil_div(N, bn);
   sc.tiles = sc.mt * sc.nt;
