@@ -306,7 +306,13 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t saddr, uint32_t lbo) {
   return d;
 }
 
-template <int CI, int CO>
+// CLUSTER form (one thread-block cluster of CS CTAs, no workspace): each CTA
+// dumps its TMEM partial into its idle operand ring, the cluster synchronises
+// once and CTA r sums rows [r·R, r·R + R) of dW over the CS partials through
+// distributed shared memory in rank order, writing dW directly.  Uses CS SMs
+// for the whole weight gradient — the form for stage streams sharing a GPU
+// (one launch, ~1/9 of the SM-time of the wide form + reduction).
+template <int CI, int CO, bool CLUSTER = false>
 __global__ void __launch_bounds__(192, 1)
 conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                         const __grid_constant__ CUtensorMap dzmap, int P, int H, int Wd,
@@ -395,7 +401,9 @@ conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
       mbar_wait(done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    float* dst = part + (long)blockIdx.x * 9 * CI * CO;
+    // the wide form writes its partial to the workspace; the cluster form to
+    // its own (now idle) operand ring, row-major [9·CI][CO]
+    float* dst = CLUSTER ? reinterpret_cast<float*>(smem) : part + (long)blockIdx.x * 9 * CI * CO;
 #pragma unroll 1
     for (int mt = 0; mt < MT; ++mt) {
       const int row = mt * 128 + q * 32 + lane;
@@ -413,6 +421,27 @@ conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         }
       }
     }
+  }
+  if constexpr (CLUSTER) {
+    // ---- distributed reduction: CTA `rank` owns rows [rank·R, rank·R + R) ----
+    static_assert(9 * CI * CO * 4 <= L::NB * L::BUF + L::PAD, "partial must fit the ring");
+    cluster_sync();
+    const int CS = (int)cluster_nctarank(), rank = (int)cluster_ctarank();
+    const int R = (9 * CI + CS - 1) / CS;
+    const int r0 = rank * R, r1 = min(9 * CI, r0 + R);
+    constexpr int C4 = CO / 4;
+    const uint32_t base_s = smem_u32(smem);
+    for (int idx = threadIdx.x; idx < (r1 - r0) * C4; idx += 192) {
+      const int row = r0 + idx / C4, c4 = idx % C4;
+      const uint32_t a = base_s + (uint32_t)((row * CO + 4 * c4) * 4);
+      float4 acc = ld_dsmem_f4(a, 0);
+      for (int src = 1; src < CS; ++src) {
+        const float4 t = ld_dsmem_f4(a, (uint32_t)src);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      reinterpret_cast<float4*>(part)[(long)row * C4 + c4] = acc;   // part = dW here
+    }
+    cluster_sync();   // peers may still read this CTA's partial until here
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -572,6 +601,56 @@ int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bflo
   const int per = (chunks + splits - 1) / splits;
   splits = (chunks + per - 1) / per;   // every split owns >= 1 chunk
   const int Pi = (int)P;
+  // stage streams sharing the GPU (g_gpu_excl == 0): one cluster, in-kernel
+  // DSMEM reduction, dW written directly (PPLL_CONV_WGRAD_CLUSTER=0|1 forces)
+  static const int cl_env = getenv("PPLL_CONV_WGRAD_CLUSTER") ? atoi(getenv("PPLL_CONV_WGRAD_CLUSTER")) : -1;
+  const bool cl = cl_env >= 0 ? cl_env != 0 : !g_gpu_excl;
+  if (cl) {
+#define WGC_CASE(A, B)                                                                       \
+    if (CI == A && CO == B) {                                                                \
+      auto kern = conv3x3_wgrad_tc_kernel<A, B, true>;                                       \
+      constexpr int smem = WgSmem<A, B>::TOTAL;                                              \
+      static int cs = -1;                                                                    \
+      if (cs < 0) {                                                                          \
+        cs = 0;                                                                              \
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == \
+                cudaSuccess &&                                                               \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == \
+                cudaSuccess) {                                                               \
+          for (int c : {16, 8}) {                                                            \
+            cudaLaunchConfig_t q = {};                                                       \
+            q.gridDim = dim3(c); q.blockDim = dim3(192); q.dynamicSmemBytes = smem;          \
+            cudaLaunchAttribute qa[1];                                                       \
+            qa[0].id = cudaLaunchAttributeClusterDimension;                                  \
+            qa[0].val.clusterDim.x = c; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1; \
+            q.attrs = qa; q.numAttrs = 1;                                                    \
+            int nc = 0;                                                                      \
+            if (cudaOccupancyMaxActiveClusters(&nc, kern, &q) == cudaSuccess && nc > 0) { cs = c; break; } \
+            cudaGetLastError();                                                              \
+          }                                                                                  \
+        } else {                                                                             \
+          cudaGetLastError();                                                                \
+        }                                                                                    \
+      }                                                                                      \
+      if (cs > 0 && chunks >= cs) {                                                          \
+        cudaLaunchConfig_t cfg = {};                                                         \
+        cfg.gridDim = dim3(cs); cfg.blockDim = dim3(192); cfg.dynamicSmemBytes = smem;       \
+        cfg.stream = s;                                                                      \
+        cudaLaunchAttribute at[2];                                                           \
+        at[0].id = cudaLaunchAttributeClusterDimension;                                      \
+        at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1; \
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;                       \
+        at[1].val.programmaticStreamSerializationAllowed = g_pdl;                            \
+        cfg.attrs = at; cfg.numAttrs = 2;                                                    \
+        PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, xm, dm, Pi, H, W, dw));               \
+        note_launch();                                                                       \
+        return PPLL_OK;                                                                      \
+      }                                                                                      \
+    }
+    WGC_CASE(16, 16) WGC_CASE(32, 32) WGC_CASE(64, 64) WGC_CASE(16, 32) WGC_CASE(32, 16)
+    WGC_CASE(32, 64) WGC_CASE(64, 32)
+#undef WGC_CASE
+  }
 #define WG_CASE(A, B)                                                                        \
   if (CI == A && CO == B) {                                                                  \
     auto kern = conv3x3_wgrad_tc_kernel<A, B>;                                               \

@@ -121,22 +121,30 @@ def test_implicit_conv3x3_wgrad_matches_torch(N, H, Cin, Cout):
     s = torch.cuda.current_stream().cuda_stream
     nws = lib.ppll_conv3x3_wgrad_ws_floats(N, H, H, Cin, Cout)
     ws = torch.empty(nws, device="cuda")
-    outs = []
-    for _ in range(2):
-        dw = torch.full((9 * Cin, Cout), float("nan"), device="cuda")
-        N_.check(lib.ppll_conv3x3_wgrad_bf16(N, H, H, Cin, Cout, x.data_ptr(), dz.data_ptr(),
-                                             dw.data_ptr(), ws.data_ptr(), nws, s), "conv wgrad")
-        torch.cuda.synchronize()
-        outs.append(dw.clone())
-    assert torch.equal(outs[0], outs[1])
     xr = x.double().permute(0, 3, 1, 2)
     wt = torch.zeros(Cout, Cin, 3, 3, dtype=torch.float64, device="cuda", requires_grad=True)
     y = Fn.conv2d(xr, wt, padding=1)
     y.backward(dz.double().permute(0, 3, 1, 2))
     # [Cout, Cin, 3, 3] -> GEMM layout [(3r+s)·Cin + ci, co]
     ref = wt.grad.permute(2, 3, 1, 0).reshape(9 * Cin, Cout)
-    err = (outs[0].double() - ref).abs().max().item() / (ref.abs().max().item() + 1e-12)
-    assert err < 1e-4, err
+    # exclusive GPU: the wide split-K form; shared GPU: one cluster with the
+    # DSMEM reduction in-kernel
+    for exclusive in (1, 0):
+        prev = lib.ppll_set_gpu_exclusive(exclusive)
+        try:
+            outs = []
+            for _ in range(2):
+                dw = torch.full((9 * Cin, Cout), float("nan"), device="cuda")
+                N_.check(lib.ppll_conv3x3_wgrad_bf16(N, H, H, Cin, Cout, x.data_ptr(),
+                                                     dz.data_ptr(), dw.data_ptr(), ws.data_ptr(),
+                                                     nws, s), "conv wgrad")
+                torch.cuda.synchronize()
+                outs.append(dw.clone())
+        finally:
+            lib.ppll_set_gpu_exclusive(prev)
+        assert torch.equal(outs[0], outs[1]), exclusive
+        err = (outs[0].double() - ref).abs().max().item() / (ref.abs().max().item() + 1e-12)
+        assert err < 1e-4, (exclusive, err)
 
 
 @pytest.mark.parametrize("N,H,Cin,Cout", [(4, 32, 16, 16), (2, 16, 32, 32), (4, 8, 64, 64),
