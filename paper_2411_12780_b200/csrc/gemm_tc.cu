@@ -1024,6 +1024,14 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
                      !ep.pre && !ep.C2;
   int cl_bn = 0, cl_cs = 0;
   static const double dsmem_bpc = getenv("PPLL_DSMEM_BPC") ? atof(getenv("PPLL_DSMEM_BPC")) : 24.0;
+  // (experiment, PPLL_WGRAD_SHARED_CS=k) with stage streams sharing the GPU,
+  // fix the K-split of the cluster weight gradients at k: fewer SMs for longer,
+  // ~1/3 of the SM-time of the 6-8-way split.  Measured: ViT-S pipeline
+  // 53.1k -> 47.3k (k=2) / 48.0k (k=3) / 45.0k (k=4) img/s — the longer
+  // side-stream gradients delay each stage's update more than the freed SMs
+  // help the other streams — so it is off by default.
+  static const int shared_cs = getenv("PPLL_WGRAD_SHARED_CS") ? atoi(getenv("PPLL_WGRAD_SHARED_CS")) : 0;
+  const int cs_fixed = (!g_gpu_excl && shared_cs >= 2) ? shared_cs : 0;
   if (plain && force_cl != 0 && K >= 8 * BK) {
     double cl_best = -1;
     const int cb[4] = {256, 192, 128, 64};
@@ -1031,7 +1039,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
       const int c = cb[i];
       if (c > 64 && N <= c / 2) continue;
       const long tiles = (long)mt * ceil_div(N, c);
-      for (int cs = 2; cs <= 8; ++cs) {
+      for (int cs = cs_fixed ? cs_fixed : 2; cs <= (cs_fixed ? cs_fixed : 8); ++cs) {
         if (K < cs * 4 * BK) break;
         int cap = capacity_any<TO>(a_kmajor, b_kmajor, c, cs);
         if (g_wgrad_cap > 0 && cap > g_wgrad_cap / cs) cap = g_wgrad_cap / cs;
@@ -1045,7 +1053,7 @@ int launch_gemm_tc(int M, int N, int K, const __nv_bfloat16* A, long lda, bool a
         if (cl_best < 0 || cost < cl_best) { cl_best = cost; cl_bn = c; cl_cs = cs; }
       }
     }
-    if (cl_bn && (force_cl == 1 || cl_best < best)) {
+    if (cl_bn && (force_cl == 1 || cs_fixed || cl_best < best)) {
       bn = cl_bn;
     } else {
       cl_bn = 0;
