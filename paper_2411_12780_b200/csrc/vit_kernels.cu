@@ -5,6 +5,7 @@
 // The GEMM-shaped work of the layer (QKV, projection, MLP) runs on the
 // tcgen05 engine (gemm_tc.cu); see vit_stage.cu for the step schedule.
 #include <math.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "kernels.cuh"
 #include "vit.cuh"
@@ -252,6 +253,121 @@ ln_bwd_vkernel(int M, const __nv_bfloat16* __restrict__ dy, long lddy,
     part[(long)blockIdx.x * NS * D + c] = t;
   }
 }
+// LayerNorm backward, round-2 form (D = 32·CPL, CPL % 4 == 0, D <= 512): one
+// warp per row, lane owns the 4-element groups at columns 4·lane + 128·k
+// (8-B vectors, a warp moves 256 contiguous bytes per access); three rows'
+// dy / x / residual loads in flight per warp before the first is reduced;
+// the parameter-gradient sums (dγ, dβ and the fused Σ dx) accumulate in
+// registers (the row loop is over the warp's own rows), then a fixed-order
+// sum over the block's warps writes one [NS][D] partial per block.  Two
+// 256-thread blocks per SM (≤ 128 registers): 16 warps x 3 rows ≈ 110 KB of
+// loads in flight per SM, against 8 warps of 255-register threads before.
+template <int CPL, int NS>
+__global__ void __launch_bounds__(256, 2)
+ln_bwd_w_kernel(int M, const __nv_bfloat16* __restrict__ dy, long lddy,
+                const __nv_bfloat16* __restrict__ x, long ldx, const float* __restrict__ mean,
+                const float* __restrict__ rstd, const float* __restrict__ g,
+                const __nv_bfloat16* __restrict__ dres, long ldres, __nv_bfloat16* __restrict__ dx,
+                long lddx, float* __restrict__ part) {
+  pdl_entry();
+  constexpr int D = 32 * CPL, NV = CPL / 4, PF = 3;
+  extern __shared__ float gsm[];                     // gamma [D] | warp partials [8][NS][D]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = threadIdx.x; c < D; c += 256) gsm[c] = g[c];
+  __syncthreads();
+  const int nw = gridDim.x * 8, gw = blockIdx.x * 8 + w;
+  float acc[NS][CPL];
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[k][i] = 0.f;
+  uint2 qd[PF][NV], qx[PF][NV], qr[PF][NV];
+  float mu[PF], rs[PF];
+  auto load = [&](int slot, int row) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = 4 * lane + 128 * v;
+      qd[slot][v] = *reinterpret_cast<const uint2*>(dy + (long)row * lddy + c);
+      qx[slot][v] = *reinterpret_cast<const uint2*>(x + (long)row * ldx + c);
+      if (dres) qr[slot][v] = *reinterpret_cast<const uint2*>(dres + (long)row * ldres + c);
+    }
+    mu[slot] = mean[row];
+    rs[slot] = rstd[row];
+  };
+#pragma unroll
+  for (int k = 0; k < PF; ++k)
+    if (gw + k * nw < M) load(k, gw + k * nw);
+  for (int row = gw, it = 0; row < M; row += nw, ++it) {
+    const int slot = it % PF;
+    float d[CPL], xh[CPL], o[CPL];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qd[slot][v].x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qd[slot][v].y));
+      d[4 * v] = a.x; d[4 * v + 1] = a.y; d[4 * v + 2] = b.x; d[4 * v + 3] = b.y;
+      const float2 e = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qx[slot][v].x));
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qx[slot][v].y));
+      xh[4 * v] = e.x; xh[4 * v + 1] = e.y; xh[4 * v + 2] = f.x; xh[4 * v + 3] = f.y;
+      if (dres) {
+        const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qr[slot][v].x));
+        const float2 q = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qr[slot][v].y));
+        o[4 * v] = p.x; o[4 * v + 1] = p.y; o[4 * v + 2] = q.x; o[4 * v + 3] = q.y;
+      }
+    }
+    const float cmu = mu[slot], crs = rs[slot];
+    if (row + PF * nw < M) load(slot, row + PF * nw);   // refill this slot PF rows ahead
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = 4 * v + j;
+        xh[i] = (xh[i] - cmu) * crs;
+        const float dxh = d[i] * gsm[4 * lane + 128 * v + j];
+        s1 += dxh;
+        s2 += dxh * xh[i];
+        acc[0][i] += d[i] * xh[i];
+        acc[1][i] += d[i];
+      }
+    s1 = warp_sum(s1) * (1.f / D);
+    s2 = warp_sum(s2) * (1.f / D);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = 4 * v + j;
+        const float u = crs * (d[i] * gsm[4 * lane + 128 * v + j] - s1 - xh[i] * s2);
+        t[j] = dres ? o[i] + u : u;
+        if (NS == 3) acc[NS - 1][i] += t[j];
+      }
+      if (dx) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(t[0], t[1]), h1 = __floats2bfloat162_rn(t[2], t[3]);
+        uint2 q;
+        q.x = *reinterpret_cast<uint32_t*>(&h0);
+        q.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(dx + (long)row * lddx + 4 * lane + 128 * v) = q;
+      }
+    }
+  }
+  if (!part) return;
+  // block partial: the 8 warps' sums in fixed order
+  float* wp = gsm + D;
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      *reinterpret_cast<float4*>(wp + ((long)w * NS + k) * D + 4 * lane + 128 * v) =
+          make_float4(acc[k][4 * v], acc[k][4 * v + 1], acc[k][4 * v + 2], acc[k][4 * v + 3]);
+  __syncthreads();
+  for (int c = threadIdx.x; c < NS * D; c += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += wp[(long)k * NS * D + c];
+    part[(long)blockIdx.x * NS * D + c] = t;
+  }
+}
+
 template <int EPL, int NS, int LPR>
 static void launch_ln_bwd_v(int nblk, cudaStream_t s, int M, const __nv_bfloat16* dy, long lddy,
                             const __nv_bfloat16* x, long ldx, const float* mean,
@@ -497,7 +613,36 @@ int launch_ln_bwd(int M, int D, const T* dy, long lddy, const T* x, long ldx, co
                    (!dx || vec_ok<T>(D, lddx)) && aligned16(dy) && aligned16(x) &&
                    (!dres || aligned16(dres)) && (!dx || aligned16(dx)) && aligned16(g);
   int NS = 2;
-  if (vec) {
+  // round-2 warp-per-row form for D = 128 .. 512 (PPLL_LN_BWD_W=0: the
+  // half-warp form below)
+  static const int w_env = getenv("PPLL_LN_BWD_W") ? atoi(getenv("PPLL_LN_BWD_W")) : 1;
+  if (vec && w_env && (D == 128 || D == 256 || D == 384 || D == 512)) {
+    NS = dxsum ? 3 : 2;
+    nblk = ln_bwd_blocks(M);   // <= 296 (two blocks per SM); the partial buffers hold this many
+    using B16 = __nv_bfloat16;
+    const B16 *dyb = (const B16*)dy, *xb = (const B16*)x, *rb = (const B16*)dres;
+    B16* dxb = (B16*)dx;
+#define LNW(CPLV, NSV)                                                                          \
+    {                                                                                           \
+      auto kern = ln_bwd_w_kernel<CPLV, NSV>;                                                   \
+      const int smem = (32 * CPLV + 8 * NSV * 32 * CPLV) * 4;                                   \
+      static bool attr = false;                                                                 \
+      if (!attr) {                                                                              \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
+        attr = true;                                                                            \
+      }                                                                                         \
+      launch_k(kern, nblk, 256, smem, s, M, dyb, lddy, xb, ldx, mean, rstd, g, rb, ldres, dxb,  \
+               lddx, part);                                                                     \
+    }
+    if (NS == 3) {
+      switch (D) { case 128: LNW(4, 3) break; case 256: LNW(8, 3) break;
+                   case 384: LNW(12, 3) break; default: LNW(16, 3) break; }
+    } else {
+      switch (D) { case 128: LNW(4, 2) break; case 256: LNW(8, 2) break;
+                   case 384: LNW(12, 2) break; default: LNW(16, 2) break; }
+    }
+#undef LNW
+  } else if (vec) {
     NS = dxsum ? 3 : 2;
     nblk = ln_bwd_vblocks(M, D == 768 || D == 512 ? 8 : 16);
     using B16 = __nv_bfloat16;
