@@ -75,7 +75,11 @@ struct ConvSmem {
   static constexpr int W_BYTES = 9 * CO * RB;        // nine [CO x CI] weight tiles
   // tap slots (two pixel tiles below CI = 64) / HALO copy slots (four tiles
   // at CI = 16, three at 32, two at 64)
-  static constexpr int STAGES = HALO ? (CI == 64 ? 4 : (CI == 32 ? 9 : 12)) : (CI == 64 ? 6 : 18);
+#ifndef PPLL_CONV_HALO_TILES
+#define PPLL_CONV_HALO_TILES 4
+#endif
+  // HALO: copy slots for PPLL_CONV_HALO_TILES pixel tiles at CI = 16 (fewer at 32 / 64)
+  static constexpr int STAGES = HALO ? (CI == 64 ? 4 : (CI == 32 ? 9 : 3 * PPLL_CONV_HALO_TILES)) : (CI == 64 ? 6 : 18);
   static constexpr int STG = epi_warps<CO>() * 1024;
   static constexpr int TOTAL = STAGES * A_BYTES + W_BYTES + STG + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = 2 * CO <= 32 ? 32 : (2 * CO <= 64 ? 64 : 128);
