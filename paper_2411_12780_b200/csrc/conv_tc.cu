@@ -59,6 +59,26 @@ __device__ __forceinline__ int swz(int r, int j) {
   const int f = RB == 128 ? (r & 7) : (RB == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
   return r * RB + ((j ^ f) * 16);
 }
+// MN-major swizzled operand descriptor: 8-row K groups of 8·RB bytes (SBO),
+// MN atoms of RB bytes' worth of elements `lbo` bytes apart
+template <int RB>
+__device__ __forceinline__ uint64_t mndesc(uint32_t saddr, uint32_t lbo) {
+  constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(((8 * RB) >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= layout << 61;
+  return d;
+}
+
+// CLUSTER form (one thread-block cluster of CS CTAs, no workspace): each CTA
+// dumps its TMEM partial into its idle operand ring, the cluster synchronises
+// once and CTA r sums rows [r·R, r·R + R) of dW over the CS partials through
+// distributed shared memory in rank order, writing dW directly.  Uses CS SMs
+// for the whole weight gradient — the form for stage streams sharing a GPU
+// (one launch, ~1/9 of the SM-time of the wide form + reduction).
 // HALO: a pixel tile covers whole rows of ONE image (W >= 16); instead of nine
 // shifted 128-pixel windows the producer loads three column-shifted copies
 // (dx = -1, 0, +1) of the tile's rows plus one halo row above and below, and
@@ -81,17 +101,23 @@ struct ConvSmem {
   // HALO: copy slots for PPLL_CONV_HALO_TILES pixel tiles at CI = 16 (fewer at 32 / 64)
   static constexpr int STAGES = HALO ? (CI == 64 ? 4 : (CI == 32 ? 9 : 3 * PPLL_CONV_HALO_TILES)) : (CI == 64 ? 6 : 18);
   static constexpr int STG = epi_warps<CO>() * 1024;
-  static constexpr int TOTAL = STAGES * A_BYTES + W_BYTES + STG + 1024 + 256;
+  static constexpr int TOTAL = STAGES * A_BYTES + W_BYTES + STG + 1024 /*align*/ + (2 * STAGES + 8) * 8 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * CO <= 32 ? 32 : (2 * CO <= 64 ? 64 : 128);
 };
 
 // W (global, bf16) is the GEMM weight [k·k·Cin (padded), Cout], row (tap·Cin + ci).
 // fwd:   Wtap[co][ci] = W[(tap·CI + ci)·CO + co]             (CI = Cin, CO = Cout)
 // dgrad: Wtap[co][ci] = W[((8 − tap)·CO + co)·CI + ci]       (CI = Cout, CO = Cin)
+// Forward weights: W rows (tap·CI + ci) hold co contiguous — exactly an
+// MN-major B operand (N = co contiguous, K = ci), so the nine [CI x CO] tap
+// tiles arrive by TMA (box {CO, CI}, swizzle of their 2·CO-byte rows) and the
+// MMA reads them MN-major: no transpose (it was ~1-2 µs of a 64->64 launch).
 template <int CI, int CO, bool HALO>
 __global__ void __launch_bounds__(conv_threads<CO>(), 1)
-conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ wg,
-                  int dgrad, int P, int H, int Wd, int rows, int imgs, Epilogue<__nv_bfloat16> ep) {
+conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                  const __nv_bfloat16* __restrict__ wg,
+                  int dgrad, int wtma, int P, int H, int Wd, int rows, int imgs,
+                  Epilogue<__nv_bfloat16> ep) {
   using L = ConvSmem<CI, CO, HALO>;
   constexpr int S = L::STAGES, RB = L::RB;
   constexpr int kEpiWarps = epi_warps<CO>(), kThreads = conv_threads<CO>();
@@ -104,7 +130,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles = P / 128;
 
@@ -118,13 +145,16 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps);
     }
+    mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)), "r"(L::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  __syncthreads();   // every thread sees the initialised barriers (wbar is waited on below)
   pdl_entry();   // the weights below are written by the predecessor (optimizer step)
   // stage the nine weight tiles, K-major and swizzled like the TMA'd A tiles,
   // reading the global weight rows as 16-B vectors
@@ -134,10 +164,13 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
       const uint4 q = *reinterpret_cast<const uint4*>(wg + ((long)(8 - tap) * CO + co) * CI + 8 * j);
       *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = q;
     }
-  } else {       // W row (tap, ci) holds co contiguous: transpose into [co][ci]
-    // through the (still idle) operand ring: coalesced 16-B copies of W first,
-    // then each thread gathers the 8 ci values of one (tap, co) 16-B chunk and
-    // stores it whole (the element-wise scatter was 4 us of a 64->64 launch)
+  } else if (wtma) {   // W row (tap, ci) holds co contiguous: nine MN-major [CI x CO] tiles by TMA
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(wbar, 9 * CI * CO * 2);
+      for (int tap = 0; tap < 9; ++tap) tma_load_2d(&wmap, wbar, sw + tap * CO * RB, 0, tap * CI);
+    }
+    mbar_wait(wbar, 0);
+  } else {       // (PPLL_CONV_WTMA=0) transpose into K-major [co][ci] through the idle ring
     static_assert(9 * CI * CO * 2 <= S * L::A_BYTES, "weight transpose buffer");
     uint4* tmp4 = reinterpret_cast<uint4*>(smem);
     for (int i = threadIdx.x; i < 9 * CI * CO / 8; i += kThreads)
@@ -187,8 +220,13 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
     }
   } else if (warp == 1) {
     // ------------------------- MMA issuer ---------------------------
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CO >> 3) << 17) |
-                           ((uint32_t)(128 >> 4) << 24);
+    // forward: B (weights) MN-major; input gradient: B K-major
+    const bool bmn = !dgrad && wtma;
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (bmn ? (1u << 16) : 0u) |
+                           ((uint32_t)(CO >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    auto bdesc = [&](uint32_t sb, int k) {
+      return bmn ? mndesc<2 * CO>(sb + k * 16 * 2 * CO, CI * 2 * CO) : kdesc<RB>(sb + 32 * k);
+    };
     if (lane == 0) {
       int kb = 0, it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
@@ -204,7 +242,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
             const uint32_t sb = smem_u32(sw + tap * CO * RB);
 #pragma unroll
             for (int k = 0; k < CI / 16; ++k)
-              mma_bf16(tmem + (uint32_t)(acc * CO), kdesc<RB>(sa + 32 * k), kdesc<RB>(sb + 32 * k),
+              mma_bf16(tmem + (uint32_t)(acc * CO), kdesc<RB>(sa + 32 * k), bdesc(sb, k),
                        idesc, (tap | k) ? 1u : 0u);
           }
           for (int dx = 0; dx < 3; ++dx) mma_commit(&empty[(kb + dx) % S]);
@@ -220,7 +258,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16*
           const uint32_t sb = smem_u32(sw + tap * CO * RB);
 #pragma unroll
           for (int k = 0; k < CI / 16; ++k)
-            mma_bf16(tmem + (uint32_t)(acc * CO), kdesc<RB>(sa + 32 * k), kdesc<RB>(sb + 32 * k),
+            mma_bf16(tmem + (uint32_t)(acc * CO), kdesc<RB>(sa + 32 * k), bdesc(sb, k),
                      idesc, (tap | k) ? 1u : 0u);
           mma_commit(&empty[st]);
         }
@@ -296,26 +334,6 @@ struct WgSmem {
   static constexpr uint32_t TMEM_COLS = MT * CO <= 32 ? 32 : (MT * CO <= 64 ? 64 : (MT * CO <= 128 ? 128 : (MT * CO <= 256 ? 256 : 512)));
 };
 
-// MN-major swizzled operand descriptor: 8-row K groups of 8·RB bytes (SBO),
-// MN atoms of RB bytes' worth of elements `lbo` bytes apart
-template <int RB>
-__device__ __forceinline__ uint64_t mndesc(uint32_t saddr, uint32_t lbo) {
-  constexpr uint64_t layout = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)(((8 * RB) >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= layout << 61;
-  return d;
-}
-
-// CLUSTER form (one thread-block cluster of CS CTAs, no workspace): each CTA
-// dumps its TMEM partial into its idle operand ring, the cluster synchronises
-// once and CTA r sums rows [r·R, r·R + R) of dW over the CS partials through
-// distributed shared memory in rank order, writing dW directly.  Uses CS SMs
-// for the whole weight gradient — the form for stage streams sharing a GPU
-// (one launch, ~1/9 of the SM-time of the wide form + reduction).
 template <int CI, int CO, bool CLUSTER = false>
 __global__ void __launch_bounds__(192, 1)
 conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
@@ -469,8 +487,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }
 
 template <int CI, int CO, bool HALO>
-static int run(const CUtensorMap& xm, const __nv_bfloat16* w, int dgrad, int P, int H, int Wd,
-               int rows, int imgs, const Epilogue<__nv_bfloat16>& ep, cudaStream_t s) {
+static int run(const CUtensorMap& xm, const CUtensorMap& wm, const __nv_bfloat16* w, int dgrad,
+               int P, int H, int Wd, int rows, int imgs, const Epilogue<__nv_bfloat16>& ep,
+               cudaStream_t s) {
   auto kern = conv3x3_tc_kernel<CI, CO, HALO>;
   constexpr int smem = ConvSmem<CI, CO, HALO>::TOTAL;
   static bool attr = false;
@@ -483,7 +502,8 @@ static int run(const CUtensorMap& xm, const __nv_bfloat16* w, int dgrad, int P, 
   PPLL_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, conv_threads<CO>(),
                                                                 smem));
   const int grid = tiles < kNumSMs * per_sm ? tiles : kNumSMs * (per_sm > 0 ? per_sm : 1);
-  launch_k(kern, grid, conv_threads<CO>(), smem, s, xm, w, dgrad, P, H, Wd, rows, imgs, ep);
+  static const int wtma = getenv("PPLL_CONV_WTMA") ? atoi(getenv("PPLL_CONV_WTMA")) : 1;
+  launch_k(kern, grid, conv_threads<CO>(), smem, s, xm, wm, w, dgrad, wtma, P, H, Wd, rows, imgs, ep);
   note_launch();
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
@@ -530,12 +550,26 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return PPLL_ERR_UNSUPPORTED;
+  // forward weights as MN-major B tiles: W viewed as [9·CI rows][CO], box {CO, CI}
+  CUtensorMap wm = xm;
+  if (!dgrad) {
+    cuuint64_t dims[2] = {(cuuint64_t)CO, (cuuint64_t)(9 * CI)};
+    cuuint64_t strides[1] = {(cuuint64_t)CO * 2};
+    cuuint32_t box[2] = {(cuuint32_t)CO, (cuuint32_t)CI};
+    cuuint32_t es2[2] = {1, 1};
+    const CUtensorMapSwizzle wsz = CO == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : (CO == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    if (enc(&wm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(w), dims, strides,
+            box, es2, CU_TENSOR_MAP_INTERLEAVE_NONE, wsz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return PPLL_ERR_UNSUPPORTED;
+  }
   Epilogue<__nv_bfloat16> e = ep;
   const int d = dgrad ? 1 : 0, Pi = (int)P;
 #define CONV_CASE(A, B)                                                             \
   if (CI == A && CO == B)                                                           \
-    return halo ? run<A, B, true>(xm, w, d, Pi, H, W, rows, imgs, e, s)             \
-                : run<A, B, false>(xm, w, d, Pi, H, W, rows, imgs, e, s);
+    return halo ? run<A, B, true>(xm, wm, w, d, Pi, H, W, rows, imgs, e, s)         \
+                : run<A, B, false>(xm, wm, w, d, Pi, H, W, rows, imgs, e, s);
   CONV_CASE(16, 16) CONV_CASE(32, 32) CONV_CASE(64, 64)
   CONV_CASE(16, 32) CONV_CASE(32, 16) CONV_CASE(32, 64) CONV_CASE(64, 32)
 #undef CONV_CASE
