@@ -158,18 +158,25 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
   pdl_entry();   // the weights below are written by the predecessor (optimizer step)
   // stage the nine weight tiles, K-major and swizzled like the TMA'd A tiles,
   // reading the global weight rows as 16-B vectors
-  if (dgrad) {   // Wtap[co][ci..ci+7] is contiguous in W
+  // weights by TMA: issued here, awaited only by the MMA issuer, so the first
+  // activation windows stream in alongside them
+  if (dgrad && wtma) {   // Wtap[co][ci] = W row (8 - tap)·CO + co: K-major tiles
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(wbar, 9 * CI * CO * 2);
+      for (int tap = 0; tap < 9; ++tap)
+        tma_load_2d(&wmap, wbar, sw + tap * CO * RB, 0, (8 - tap) * CO);
+    }
+  } else if (dgrad) {   // Wtap[co][ci..ci+7] is contiguous in W
     for (int i = threadIdx.x; i < 9 * CO * (CI / 8); i += kThreads) {
       const int j = i % (CI / 8), co = (i / (CI / 8)) % CO, tap = i / (CI / 8) / CO;
       const uint4 q = *reinterpret_cast<const uint4*>(wg + ((long)(8 - tap) * CO + co) * CI + 8 * j);
       *reinterpret_cast<uint4*>(sw + tap * CO * RB + swz<RB>(co, j)) = q;
     }
-  } else if (wtma) {   // W row (tap, ci) holds co contiguous: nine MN-major [CI x CO] tiles by TMA
+  } else if (wtma) {   // W row (tap, ci) holds co contiguous: nine MN-major [CI x CO] tiles
     if (threadIdx.x == 0) {
       mbar_expect_tx(wbar, 9 * CI * CO * 2);
       for (int tap = 0; tap < 9; ++tap) tma_load_2d(&wmap, wbar, sw + tap * CO * RB, 0, tap * CI);
     }
-    mbar_wait(wbar, 0);
   } else {       // (PPLL_CONV_WTMA=0) transpose into K-major [co][ci] through the idle ring
     static_assert(9 * CI * CO * 2 <= S * L::A_BYTES, "weight transpose buffer");
     uint4* tmp4 = reinterpret_cast<uint4*>(smem);
@@ -228,6 +235,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
       return bmn ? mndesc<2 * CO>(sb + k * 16 * 2 * CO, CI * 2 * CO) : kdesc<RB>(sb + 32 * k);
     };
     if (lane == 0) {
+      if (wtma) mbar_wait(wbar, 0);   // the weight tiles have landed
       int kb = 0, it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
@@ -550,9 +558,22 @@ int launch_conv3x3_tc(int N, int H, int W, int CI, int CO, const __nv_bfloat16* 
           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return PPLL_ERR_UNSUPPORTED;
-  // forward weights as MN-major B tiles: W viewed as [9·CI rows][CO], box {CO, CI}
+  // forward weights as MN-major B tiles: W viewed as [9·CI rows][CO], box {CO, CI};
+  // input gradient: W viewed as [9·CO rows][CI] (CI = the forward's Cout), box
+  // {CI, CO}, landing K-major like the activation tiles
   CUtensorMap wm = xm;
-  if (!dgrad) {
+  if (dgrad) {
+    cuuint64_t dims[2] = {(cuuint64_t)CI, (cuuint64_t)(9 * CO)};
+    cuuint64_t strides[1] = {(cuuint64_t)CI * 2};
+    cuuint32_t box[2] = {(cuuint32_t)CI, (cuuint32_t)CO};
+    cuuint32_t es2[2] = {1, 1};
+    const CUtensorMapSwizzle wsz = CI == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                   : (CI == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    if (enc(&wm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(w), dims, strides,
+            box, es2, CU_TENSOR_MAP_INTERLEAVE_NONE, wsz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return PPLL_ERR_UNSUPPORTED;
+  } else {
     cuuint64_t dims[2] = {(cuuint64_t)CO, (cuuint64_t)(9 * CI)};
     cuuint64_t strides[1] = {(cuuint64_t)CO * 2};
     cuuint32_t box[2] = {(cuuint32_t)CO, (cuuint32_t)CI};
