@@ -75,12 +75,15 @@ ln_fwd_vkernel(int M, const T* __restrict__ x, long ldx, const float* __restrict
   const int row = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + (lane >> 4);
   const bool live = row < M;
   const int c0 = hl * EPL;
-  float v[EPL];
+  float v[EPL], gg[EPL], bb[EPL];
   if (live) ldv<EPL>(x + (long)row * ldx + c0, v);
   else {
 #pragma unroll
     for (int i = 0; i < EPL; ++i) v[i] = 0.f;
   }
+  // γ / β loads issued with the row's, not after the two reductions
+  ldv<EPL>(g + c0, gg);
+  ldv<EPL>(b + c0, bb);
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < EPL; ++i) s += v[i];
@@ -93,9 +96,6 @@ ln_fwd_vkernel(int M, const T* __restrict__ x, long ldx, const float* __restrict
   }
   const float rs = rsqrtf(half_sum(q) * (1.f / D) + kLnEps);
   if (!live) return;
-  float gg[EPL], bb[EPL];
-  ldv<EPL>(g + c0, gg);
-  ldv<EPL>(b + c0, bb);
 #pragma unroll
   for (int i = 0; i < EPL; ++i) v[i] = (v[i] - mu) * rs * gg[i] + bb[i];
   stv<EPL>(y + (long)row * ldy + c0, v);
