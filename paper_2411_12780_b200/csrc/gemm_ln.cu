@@ -1,0 +1,363 @@
+// LayerNorm backward fused into the epilogue of the GEMM that produces its
+// input gradient (the ViT layer's FC1 and QKV data gradients, D = 384):
+//
+//   dxn = dY · Wᵀ                       (tcgen05, fp32 in TMEM, never stored)
+//   dx  = rstd·(γ·dxn − mean_row(γ·dxn) − x̂·mean_row(γ·dxn·x̂)) + dres
+//   dγ += Σ_rows dxn·x̂,  dβ += Σ_rows dxn,  Σ_rows dx  (next bias gradient)
+//
+// One CTA per 128-row tile and the WHOLE row (N = 384 = two N = 192 MMAs per
+// K step into TMEM columns [0,192) / [192,384)), so the epilogue has complete
+// rows: pass 1 reads the accumulator chunk by chunk with x̂ for the two row
+// sums (the four warps sharing a TMEM lane quadrant meet at a named barrier),
+// pass 2 re-reads it, writes dx and folds the three column sums (warp
+// transpose-reduce, fixed quadrant order) into one per-CTA partial that the
+// stage's deferred LN reduction sums (vit_kernels.cu).  Replaces the GEMM's
+// dxn store + the LN-backward kernel's re-read of it (12.8 MB and one launch
+// per LayerNorm) — tensor.py:137-150 matmul adjoint + the LN adjoint of the
+// ViT extension (oracle/vit_oracle.py).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+#include "vit.cuh"
+
+namespace ppll {
+namespace tc { unsigned long long* timeline_buffer(); }
+namespace gln {
+using namespace ptx;
+
+constexpr int BM = 128, BK = 64, D = 384, NH = 192;
+constexpr int kEpiWarps = 16, kThreads = 64 + 32 * kEpiWarps;
+constexpr int STAGES = 3;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KB
+constexpr int BH_BYTES = NH * BK * 2;           // 24 KB per N half
+constexpr int STAGE = A_BYTES + 2 * BH_BYTES;   // 64 KB
+constexpr int kGamOff = STAGES * STAGE;         // γ [D] f32
+constexpr int kRedOff = kGamOff + D * 4;        // [2][4][BM] f32 row partial sums
+constexpr int kCpartOff = kRedOff + 2 * 4 * BM * 4;   // [4 quadrants][3][D] f32
+constexpr int kBarOff = kCpartOff + 4 * 3 * D * 4;
+constexpr int kSmem = kBarOff + 256 + 1024;
+
+struct Args {
+  int M, K;
+  const __nv_bfloat16* x;      // LN input [M, D]
+  const float *mean, *rstd;    // [M]
+  const float* g;              // γ [D]
+  const __nv_bfloat16* dres;   // residual gradient added to dx [M, D] (nullable)
+  __nv_bfloat16* dx;           // [M, D] (nullable: parameter gradients only)
+  float* part;                 // [gridDim][3][D] per-CTA column partials
+  unsigned long long* tl;      // PPLL_GEMM_LN_TIMELINE: per CTA 8 %globaltimer stamps
+};
+#define GLN_TL(k) \
+  if (a.tl && threadIdx.x == 64) a.tl[blockIdx.x * 8 + (k)] = gtimer();
+
+// warp transpose-reduce of 32 per-lane values: lane L ends with Σ_lanes v[L]
+__device__ __forceinline__ float colsum32(const float (&v)[32], int lane) {
+  float a[16];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float keep = hi ? v[j + 16] : v[j], send = hi ? v[j] : v[j + 16];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  float b[8];
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float keep = hi ? a[j + 8] : a[j], send = hi ? a[j] : a[j + 8];
+      b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  float c[4];
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float keep = hi ? b[j + 4] : b[j], send = hi ? b[j] : b[j + 4];
+      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  float d[2];
+  {
+    const bool hi = lane & 2;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float keep = hi ? c[j + 2] : c[j], send = hi ? c[j] : c[j + 2];
+      d[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+  }
+  const bool hi = lane & 1;
+  return (hi ? d[1] : d[0]) + __shfl_xor_sync(0xffffffffu, hi ? d[0] : d[1], 1);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_r,
+                   const __grid_constant__ Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  float* gam = reinterpret_cast<float*>(smem + kGamOff);
+  float* red = reinterpret_cast<float*>(smem + kRedOff);
+  float* cpart = reinterpret_cast<float*>(smem + kCpartOff);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* xfull = tfull + 1;     // x / dres tiles landed in the (freed) operand ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.x * BM;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(xfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+  GLN_TL(0)
+
+  const int nkb = a.K / BK;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % STAGES;
+        mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + st * STAGE;
+        mbar_expect_tx(&full[st], STAGE);
+        tma_load_2d(&map_a, &full[st], sa, kb * BK, m0);
+        tma_load_2d(&map_b, &full[st], sa + A_BYTES, kb * BK, 0);
+        tma_load_2d(&map_b, &full[st], sa + A_BYTES + BH_BYTES, kb * BK, NH);
+      }
+      // every MMA retired => the ring is free: the epilogue's x and dres tiles
+      // (six 64-column SW128 boxes each, 96 KB per tensor) arrive in it
+      mbar_wait(tfull, 0);
+      mbar_expect_tx(xfull, (a.dres ? 2 : 1) * BM * D * 2);
+      for (int b = 0; b < D / 64; ++b) {
+        tma_load_2d(&map_x, xfull, smem + b * 16384, 64 * b, m0);
+        if (a.dres) tma_load_2d(&map_r, xfull, smem + 6 * 16384 + b * 16384, 64 * b, m0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BM, NH, false, false);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % STAGES;
+        mbar_wait(&full[st], (kb / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(smem + st * STAGE);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            mma_bf16(tmem + (uint32_t)(h * NH),
+                     ad, umma_desc_sw128(sa + A_BYTES + h * BH_BYTES + k * 32, 16, 1024), idesc,
+                     (kb | k) ? 1u : 0u);
+        }
+        mma_commit(&empty[st]);
+      }
+      mma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------- LN-backward epilogue ----------------------------
+    const int q = warp & 3, grp = (warp - 2) >> 2;       // lane quadrant, column group
+    const int r = q * 32 + lane, row = m0 + r;
+    const bool live = row < a.M;
+    const float mu = live ? a.mean[row] : 0.f, rs = live ? a.rstd[row] : 0.f;
+    for (int c = threadIdx.x - 64; c < D; c += 32 * kEpiWarps) gam[c] = a.g[c];
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+    mbar_wait(tfull, 0);
+    GLN_TL(1)
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    mbar_wait(xfull, 0);
+    GLN_TL(2)
+    // 16 columns c.. of this thread's row from a swizzled [128][64] box set
+    auto ld16s = [&](int tensor, int c, float (&v)[16]) {
+      const uint8_t* box = smem + (tensor * 6 + c / 64) * 16384 + r * 128;
+      const int j0 = (c % 64) / 8;
+      const uint4 q0 = *reinterpret_cast<const uint4*>(box + (((j0) ^ (r & 7)) << 4));
+      const uint4 q1 = *reinterpret_cast<const uint4*>(box + (((j0 + 1) ^ (r & 7)) << 4));
+      const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&q0);
+      const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x0 = __bfloat1622float2(h0[e]), x1 = __bfloat1622float2(h1[e]);
+        v[2 * e] = x0.x; v[2 * e + 1] = x0.y; v[8 + 2 * e] = x1.x; v[8 + 2 * e + 1] = x1.y;
+      }
+    };
+    // pass 1: this warp's six 16-column chunks -> partial row sums
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 1
+    for (int j = 0; j < 6; ++j) {
+      const int c = 16 * grp + 64 * j;
+      uint32_t u[16];
+      tmem_ld16(tbase + (uint32_t)c, u);
+      float x[16];
+      ld16s(0, c, x);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float dxh = __uint_as_float(u[i]) * gam[c + i];
+        s1 += dxh;
+        s2 += dxh * ((x[i] - mu) * rs);
+      }
+    }
+    red[(0 * 4 + grp) * BM + r] = s1;
+    red[(1 * 4 + grp) * BM + r] = s2;
+    asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");   // the quadrant's four warps
+    GLN_TL(3)
+    const float m1 = (((red[0 * BM + r] + red[1 * BM + r]) + red[2 * BM + r]) + red[3 * BM + r]) *
+                     (1.f / D);
+    const float m2 = (((red[4 * BM + r] + red[5 * BM + r]) + red[6 * BM + r]) + red[7 * BM + r]) *
+                     (1.f / D);
+    // pass 2: dx, and the column sums dγ (dxn·x̂), dβ (dxn), Σ dx
+    __nv_bfloat16* orow = a.dx ? a.dx + (long)row * D : nullptr;
+    float* cp = cpart + (long)q * 3 * D;
+#pragma unroll 1
+    for (int j = 0; j < 6; ++j) {
+      const int c = 16 * grp + 64 * j;
+      uint32_t u[16];
+      tmem_ld16(tbase + (uint32_t)c, u);
+      float x[16], rv[16];
+      ld16s(0, c, x);
+      if (a.dres) {
+        ld16s(1, c, rv);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) rv[i] = 0.f;
+      }
+      float va[32], vd[32], o[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float dy = live ? __uint_as_float(u[i]) : 0.f;
+        const float xh = (x[i] - mu) * rs;
+        o[i] = rs * (dy * gam[c + i] - m1 - xh * m2) + rv[i];
+        va[i] = dy * xh;          // dγ
+        va[16 + i] = dy;          // dβ
+        vd[i] = live ? o[i] : 0.f;
+        vd[16 + i] = 0.f;
+      }
+      if (orow && live) {
+        uint4 q0, q1;
+        __nv_bfloat162* h0 = reinterpret_cast<__nv_bfloat162*>(&q0);
+        __nv_bfloat162* h1 = reinterpret_cast<__nv_bfloat162*>(&q1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          h0[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+          h1[e] = __floats2bfloat162_rn(o[8 + 2 * e], o[8 + 2 * e + 1]);
+        }
+        reinterpret_cast<uint4*>(orow + c)[0] = q0;
+        reinterpret_cast<uint4*>(orow + c)[1] = q1;
+      }
+      const float sa = colsum32(va, lane), sd = colsum32(vd, lane);
+      if (lane < 16) {
+        cp[0 * D + c + lane] = sa;          // dγ chunk
+        cp[2 * D + c + lane] = sd;          // Σ dx chunk
+      } else {
+        cp[1 * D + c + lane - 16] = sa;     // dβ chunk
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+    GLN_TL(4)
+    // per-CTA partial: the four lane quadrants (row blocks) in fixed order
+    for (int i = threadIdx.x - 64; i < 3 * D; i += 32 * kEpiWarps)
+      a.part[(long)blockIdx.x * 3 * D + i] =
+          ((cpart[i] + cpart[3 * D + i]) + cpart[6 * D + i]) + cpart[9 * D + i];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// 2-D K-major bf16 operand map: inner extent K (contiguous), `rows` rows of
+// pitch ld elements, box {64, box_rows}, 128-B swizzle
+static bool kmap(CUtensorMap* m, const void* p, long K, long rows, long ld, int box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace gln
+
+// dx = LN_backward(dY · Wᵀ) for D = 384 (bf16): dY [M, K] (ld K), W [384, K]
+// (the linear weight [in, out] = [D, K], ld K), x / dres / dx [M, 384].
+// The per-CTA column partials go to `part` ([ceil(M/128)][3][384]) and are
+// recorded in `defer` for the stage's batched reduction into dg, db and
+// dxsum (each nullable).  PPLL_ERR_UNSUPPORTED outside the fused shape range
+// (the caller keeps GEMM + LN-backward kernel).
+int launch_gemm_ln_bwd(int M, int K, const __nv_bfloat16* dY, const __nv_bfloat16* W,
+                       const __nv_bfloat16* x, const float* mean, const float* rstd,
+                       const float* g, const __nv_bfloat16* dres, __nv_bfloat16* dx, float* part,
+                       float* dg, float* db, float* dxsum, LnDefer* defer, cudaStream_t s) {
+  using namespace gln;
+  static const int on = getenv("PPLL_GEMM_LN") ? atoi(getenv("PPLL_GEMM_LN")) : 1;
+  if (!on || M < 1 || K % BK || K < BK || !defer || defer->n >= LnDefer::kMax || !part)
+    return PPLL_ERR_UNSUPPORTED;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al(dY) || !al(W) || !al(x) || !al(dres) || !al(dx)) return PPLL_ERR_UNSUPPORTED;
+  CUtensorMap ma, mb, mx, mr;
+  if (!kmap(&ma, dY, K, M, K, BM) || !kmap(&mb, W, K, D, K, NH) || !kmap(&mx, x, D, M, D, BM))
+    return PPLL_ERR_UNSUPPORTED;
+  if (dres ? !kmap(&mr, dres, D, M, D, BM) : false) return PPLL_ERR_UNSUPPORTED;
+  if (!dres) mr = mx;
+  static bool attr = false;
+  if (!attr) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(gemm_ln_bwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  const int grid = (M + BM - 1) / BM;
+  static unsigned long long* tl =
+      getenv("PPLL_GEMM_LN_TIMELINE") ? tc::timeline_buffer() : nullptr;
+  Args a{M, K, x, mean, rstd, g, dres, dx, part, tl};
+  launch_k(gemm_ln_bwd_kernel, grid, kThreads, kSmem, s, ma, mb, mx, mr, a);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  LnReduceTask& t = defer->t[defer->n++];
+  t = LnReduceTask{part, dg, db, dxsum, grid, D, 3, defer->blocks};
+  defer->blocks += (3 * D + 31) / 32;
+  return PPLL_OK;
+}
+
+}  // namespace ppll

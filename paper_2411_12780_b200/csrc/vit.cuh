@@ -33,6 +33,13 @@ struct LnDefer {
   int n = 0, blocks = 0;
 };
 int launch_ln_reduce_deferred(const LnDefer& d, cudaStream_t s);
+// LayerNorm backward fused into the data-gradient GEMM that feeds it
+// (gemm_ln.cu, D = 384): dx = LN_bwd(dY·Wᵀ) (+ dres), column partials recorded
+// in `defer`; PPLL_ERR_UNSUPPORTED outside its range.
+int launch_gemm_ln_bwd(int M, int K, const __nv_bfloat16* dY, const __nv_bfloat16* W,
+                       const __nv_bfloat16* x, const float* mean, const float* rstd,
+                       const float* g, const __nv_bfloat16* dres, __nv_bfloat16* dx, float* part,
+                       float* dg, float* db, float* dxsum, LnDefer* defer, cudaStream_t s);
 int ln_bwd_blocks(int M);
 template <typename T>
 int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse, cudaStream_t s);

@@ -286,16 +286,29 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
                      st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_w1 = sf.mark();
-    r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
-                   st->ws, st->ws_elems, s);
-    if (r) return r;
-    // LN2 backward (+ residual) -> dx1, with dbo = Σ rows dx1 fused
+    // FC1 data gradient + LN2 backward (+ residual) -> dx1, with dbo = Σ rows
+    // dx1: one fused launch for bf16 D = 384 (gemm_ln.cu), else GEMM + LN kernel
     sf.join(e_wo);   // dx1 is still read by the layer above's Wo gradient
-    r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
-                          st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, slab(),
-                          st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s,
-                          st->G(st->po(l, kBo)), &dfr);
-    if (r) return r;
+    r = PPLL_ERR_UNSUPPORTED;
+    float* part2 = slab();   // this LayerNorm's partial slab (fused or not)
+    if (st->dtype == PPLL_BF16 && D == 384)
+      r = launch_gemm_ln_bwd(M, F, (const __nv_bfloat16*)st->dbig,
+                             (const __nv_bfloat16*)st->W(st->po(l, kW1)),
+                             (const __nv_bfloat16*)b.x1, b.mean2, b.rstd2, st->P(st->po(l, kLn2g)),
+                             (const __nv_bfloat16*)dx2, (__nv_bfloat16*)dx1, part2,
+                             st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)),
+                             st->G(st->po(l, kBo)), &dfr, s);
+    if (r != PPLL_OK && r != PPLL_ERR_UNSUPPORTED) return r;
+    if (r == PPLL_ERR_UNSUPPORTED) {
+      r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
+                     st->ws, st->ws_elems, s);
+      if (r) return r;
+      r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
+                            st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, part2,
+                            st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s,
+                            st->G(st->po(l, kBo)), &dfr);
+      if (r) return r;
+    }
     sf.fork();
     r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, wsw,
                      st->ws_elems, sf.ss);
@@ -314,23 +327,35 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
                      st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_wqkv = sf.mark();
-    r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
-                   st->dtype, st->ws, st->ws_elems, s);
-    if (r) return r;
-    // LN1 backward (+ residual) -> gradient of the layer input; no gradient
-    // into the detached stage input (blocks.py:277-278).  Its row sum is the
-    // bias gradient db2 of the layer below (fused).
+    // QKV data gradient + LN1 backward (+ residual) -> gradient of the layer
+    // input; no gradient into the detached stage input (blocks.py:277-278).
+    // Its row sum is the bias gradient db2 of the layer below (fused).
     const bool need_dx = l > 0 || st->has_patch || g_in;
     // the stage input's gradient goes straight to g_in (no patch embedding below)
     TT* dx_dst = (l == 0 && !st->has_patch) ? (TT*)g_in : (TT*)dxn_out;
     sf.join(e_w2);   // dxn_out was the layer above's dx2, read by its W2 gradient
     e_w2 = n_w2;
-    r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
-                          st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
-                          need_dx ? dx_dst : nullptr, D, slab(),
-                          st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s,
-                          l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr, &dfr);
-    if (r) return r;
+    r = PPLL_ERR_UNSUPPORTED;
+    float* part1 = slab();
+    if (st->dtype == PPLL_BF16 && D == 384)
+      r = launch_gemm_ln_bwd(M, 3 * D, (const __nv_bfloat16*)st->dqkv,
+                             (const __nv_bfloat16*)st->W(st->po(l, kWqkv)),
+                             (const __nv_bfloat16*)xin_l, b.mean1, b.rstd1, st->P(st->po(l, kLn1g)),
+                             (const __nv_bfloat16*)dx1, need_dx ? (__nv_bfloat16*)dx_dst : nullptr,
+                             part1, st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)),
+                             l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr, &dfr, s);
+    if (r != PPLL_OK && r != PPLL_ERR_UNSUPPORTED) return r;
+    if (r == PPLL_ERR_UNSUPPORTED) {
+      r = gemm_dgrad(M, D, 3 * D, st->dqkv, 3 * D, st->W(st->po(l, kWqkv)), none, st->dxn, D,
+                     st->dtype, st->ws, st->ws_elems, s);
+      if (r) return r;
+      r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)xin_l, D, b.mean1, b.rstd1,
+                            st->P(st->po(l, kLn1g)), (const TT*)dx1, D,
+                            need_dx ? dx_dst : nullptr, D, part1,
+                            st->G(st->po(l, kLn1g)), st->G(st->po(l, kLn1b)), s,
+                            l > 0 ? st->G(st->po(l - 1, kB2)) : nullptr, &dfr);
+      if (r) return r;
+    }
     char* t = dx2;
     dx2 = dxn_out;
     dxn_out = t;
