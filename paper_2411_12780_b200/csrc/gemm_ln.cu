@@ -28,16 +28,20 @@ namespace tc { unsigned long long* timeline_buffer(); }
 namespace gln {
 using namespace ptx;
 
+// A 2-CTA cluster owns a 128-row tile: CTA rank h computes columns
+// [192h, 192h + 192) (one N = 192 MMA per K step) and the two CTAs exchange
+// their halves of the row sums over DSMEM — 130 CTAs for M = 8320 instead of 65.
 constexpr int BM = 128, BK = 64, D = 384, NH = 192;
 constexpr int kEpiWarps = 16, kThreads = 64 + 32 * kEpiWarps;
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
-constexpr int BH_BYTES = NH * BK * 2;           // 24 KB per N half
-constexpr int STAGE = A_BYTES + 2 * BH_BYTES;   // 64 KB
-constexpr int kGamOff = STAGES * STAGE;         // γ [D] f32
-constexpr int kRedOff = kGamOff + D * 4;        // [2][4][BM] f32 row partial sums
-constexpr int kCpartOff = kRedOff + 2 * 4 * BM * 4;   // [4 quadrants][3][D] f32
-constexpr int kBarOff = kCpartOff + 4 * 3 * D * 4;
+constexpr int BH_BYTES = NH * BK * 2;           // 24 KB (this CTA's N half)
+constexpr int STAGE = A_BYTES + BH_BYTES;       // 40 KB
+constexpr int kGamOff = STAGES * STAGE;         // γ of this half [NH] f32
+constexpr int kRedOff = kGamOff + NH * 4;       // [2][4][BM] f32 quadrant row partial sums
+constexpr int kRowOff = kRedOff + 2 * 4 * BM * 4;     // [2][BM] this CTA's row sums (DSMEM)
+constexpr int kCpartOff = kRowOff + 2 * BM * 4;       // [4 quadrants][3][NH] f32
+constexpr int kBarOff = kCpartOff + 4 * 3 * NH * 4;
 constexpr int kSmem = kBarOff + 256 + 1024;
 
 struct Args {
@@ -103,14 +107,17 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float* gam = reinterpret_cast<float*>(smem + kGamOff);
   float* red = reinterpret_cast<float*>(smem + kRedOff);
+  float* rows_s = reinterpret_cast<float*>(smem + kRowOff);
   float* cpart = reinterpret_cast<float*>(smem + kCpartOff);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* xfull = tfull + 1;     // x / dres tiles landed in the (freed) operand ring
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+  uint64_t* xch = xfull + 1;       // the peer half's row sums are ready (remote arrive)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xch + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * BM;
+  const int half = (int)cluster_ctarank(), tile = blockIdx.x / 2;
+  const int m0 = tile * BM, n0 = half * NH;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -121,16 +128,18 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
     }
     mbar_init(tfull, 1);
     mbar_init(xfull, 1);
+    mbar_init(xch, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
         smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  cluster_sync();   // the peer's barriers are initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   pdl_entry();
@@ -145,16 +154,15 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
         uint8_t* sa = smem + st * STAGE;
         mbar_expect_tx(&full[st], STAGE);
         tma_load_2d(&map_a, &full[st], sa, kb * BK, m0);
-        tma_load_2d(&map_b, &full[st], sa + A_BYTES, kb * BK, 0);
-        tma_load_2d(&map_b, &full[st], sa + A_BYTES + BH_BYTES, kb * BK, NH);
+        tma_load_2d(&map_b, &full[st], sa + A_BYTES, kb * BK, n0);
       }
-      // every MMA retired => the ring is free: the epilogue's x and dres tiles
-      // (six 64-column SW128 boxes each, 96 KB per tensor) arrive in it
+      // every MMA retired => the ring is free: this half's x and dres columns
+      // (three 64-column SW128 boxes each, 48 KB per tensor) arrive in it
       mbar_wait(tfull, 0);
-      mbar_expect_tx(xfull, (a.dres ? 2 : 1) * BM * D * 2);
-      for (int b = 0; b < D / 64; ++b) {
-        tma_load_2d(&map_x, xfull, smem + b * 16384, 64 * b, m0);
-        if (a.dres) tma_load_2d(&map_r, xfull, smem + 6 * 16384 + b * 16384, 64 * b, m0);
+      mbar_expect_tx(xfull, (a.dres ? 2 : 1) * BM * NH * 2);
+      for (int b = 0; b < NH / 64; ++b) {
+        tma_load_2d(&map_x, xfull, smem + b * 16384, n0 + 64 * b, m0);
+        if (a.dres) tma_load_2d(&map_r, xfull, smem + 3 * 16384 + b * 16384, n0 + 64 * b, m0);
       }
     }
   } else if (warp == 1) {
@@ -166,14 +174,9 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sa = smem_u32(smem + st * STAGE);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = umma_desc_sw128(sa + k * 32, 16, 1024);
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            mma_bf16(tmem + (uint32_t)(h * NH),
-                     ad, umma_desc_sw128(sa + A_BYTES + h * BH_BYTES + k * 32, 16, 1024), idesc,
-                     (kb | k) ? 1u : 0u);
-        }
+        for (int k = 0; k < BK / 16; ++k)
+          mma_bf16(tmem, umma_desc_sw128(sa + k * 32, 16, 1024),
+                   umma_desc_sw128(sa + A_BYTES + k * 32, 16, 1024), idesc, (kb | k) ? 1u : 0u);
         mma_commit(&empty[st]);
       }
       mma_commit(tfull);
@@ -185,7 +188,7 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
     const int r = q * 32 + lane, row = m0 + r;
     const bool live = row < a.M;
     const float mu = live ? a.mean[row] : 0.f, rs = live ? a.rstd[row] : 0.f;
-    for (int c = threadIdx.x - 64; c < D; c += 32 * kEpiWarps) gam[c] = a.g[c];
+    for (int c = threadIdx.x - 64; c < NH; c += 32 * kEpiWarps) gam[c] = a.g[n0 + c];
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     mbar_wait(tfull, 0);
     GLN_TL(1)
@@ -193,9 +196,9 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
     mbar_wait(xfull, 0);
     GLN_TL(2)
-    // 16 columns c.. of this thread's row from a swizzled [128][64] box set
+    // 16 columns c.. (of this half) of this thread's row from a swizzled [128][64] box set
     auto ld16s = [&](int tensor, int c, float (&v)[16]) {
-      const uint8_t* box = smem + (tensor * 6 + c / 64) * 16384 + r * 128;
+      const uint8_t* box = smem + (tensor * 3 + c / 64) * 16384 + r * 128;
       const int j0 = (c % 64) / 8;
       const uint4 q0 = *reinterpret_cast<const uint4*>(box + (((j0) ^ (r & 7)) << 4));
       const uint4 q1 = *reinterpret_cast<const uint4*>(box + (((j0 + 1) ^ (r & 7)) << 4));
@@ -207,10 +210,10 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
         v[2 * e] = x0.x; v[2 * e + 1] = x0.y; v[8 + 2 * e] = x1.x; v[8 + 2 * e + 1] = x1.y;
       }
     };
-    // pass 1: this warp's six 16-column chunks -> partial row sums
+    // pass 1: this warp's three 16-column chunks -> partial row sums
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
-    for (int j = 0; j < 6; ++j) {
+    for (int j = 0; j < 3; ++j) {
       const int c = 16 * grp + 64 * j;
       uint32_t u[16];
       tmem_ld16(tbase + (uint32_t)c, u);
@@ -226,16 +229,34 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
     red[(0 * 4 + grp) * BM + r] = s1;
     red[(1 * 4 + grp) * BM + r] = s2;
     asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");   // the quadrant's four warps
+    // this half's row sums -> shared memory; the peer reads them over DSMEM
+    if (grp == 0) {
+      rows_s[r] = ((red[0 * BM + r] + red[1 * BM + r]) + red[2 * BM + r]) + red[3 * BM + r];
+      rows_s[BM + r] = ((red[4 * BM + r] + red[5 * BM + r]) + red[6 * BM + r]) + red[7 * BM + r];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+    if (threadIdx.x == 64) mbar_arrive_cluster(mapa_shared(smem_u32(xch), (uint32_t)(half ^ 1)));
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tXW_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra XW_%=;\n\t}" ::"r"(smem_u32(xch))
+        : "memory");
     GLN_TL(3)
-    const float m1 = (((red[0 * BM + r] + red[1 * BM + r]) + red[2 * BM + r]) + red[3 * BM + r]) *
-                     (1.f / D);
-    const float m2 = (((red[4 * BM + r] + red[5 * BM + r]) + red[6 * BM + r]) + red[7 * BM + r]) *
-                     (1.f / D);
+    float p1, p2;   // the peer half's sums of this row
+    {
+      const uint32_t ra = mapa_shared(smem_u32(rows_s + r), (uint32_t)(half ^ 1));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p1) : "r"(ra) : "memory");
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p2) : "r"(ra + 4 * BM) : "memory");
+    }
+    const float o1 = rows_s[r], o2 = rows_s[BM + r];
+    // fixed order: columns [0,192) first
+    const float m1 = (half == 0 ? o1 + p1 : p1 + o1) * (1.f / D);
+    const float m2 = (half == 0 ? o2 + p2 : p2 + o2) * (1.f / D);
     // pass 2: dx, and the column sums dγ (dxn·x̂), dβ (dxn), Σ dx
-    __nv_bfloat16* orow = a.dx ? a.dx + (long)row * D : nullptr;
-    float* cp = cpart + (long)q * 3 * D;
+    __nv_bfloat16* orow = a.dx ? a.dx + (long)row * D + n0 : nullptr;
+    float* cp = cpart + (long)q * 3 * NH;
 #pragma unroll 1
-    for (int j = 0; j < 6; ++j) {
+    for (int j = 0; j < 3; ++j) {
       const int c = 16 * grp + 64 * j;
       uint32_t u[16];
       tmem_ld16(tbase + (uint32_t)c, u);
@@ -272,24 +293,27 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
       }
       const float sa = colsum32(va, lane), sd = colsum32(vd, lane);
       if (lane < 16) {
-        cp[0 * D + c + lane] = sa;          // dγ chunk
-        cp[2 * D + c + lane] = sd;          // Σ dx chunk
+        cp[0 * NH + c + lane] = sa;          // dγ chunk
+        cp[2 * NH + c + lane] = sd;          // Σ dx chunk
       } else {
-        cp[1 * D + c + lane - 16] = sa;     // dβ chunk
+        cp[1 * NH + c + lane - 16] = sa;     // dβ chunk
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     GLN_TL(4)
-    // per-CTA partial: the four lane quadrants (row blocks) in fixed order
-    for (int i = threadIdx.x - 64; i < 3 * D; i += 32 * kEpiWarps)
-      a.part[(long)blockIdx.x * 3 * D + i] =
-          ((cpart[i] + cpart[3 * D + i]) + cpart[6 * D + i]) + cpart[9 * D + i];
+    // this half's columns of the tile's partial: the four lane quadrants in fixed order
+    for (int i = threadIdx.x - 64; i < 3 * NH; i += 32 * kEpiWarps) {
+      const int st = i / NH, c = i % NH;
+      a.part[((long)tile * 3 + st) * D + n0 + c] =
+          ((cpart[i] + cpart[3 * NH + i]) + cpart[6 * NH + i]) + cpart[9 * NH + i];
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  cluster_sync();   // the peer has read this CTA's row sums
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
   }
 }
 
@@ -347,13 +371,26 @@ int launch_gemm_ln_bwd(int M, int K, const __nv_bfloat16* dY, const __nv_bfloat1
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr = true;
   }
-  const int grid = (M + BM - 1) / BM;
+  const int tiles = (M + BM - 1) / BM, grid = tiles;
   static unsigned long long* tl =
       getenv("PPLL_GEMM_LN_TIMELINE") ? tc::timeline_buffer() : nullptr;
   Args a{M, K, x, mean, rstd, g, dres, dx, part, tl};
-  launch_k(gemm_ln_bwd_kernel, grid, kThreads, kSmem, s, ma, mb, mx, mr, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * tiles);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_ln_bwd_kernel, ma, mb, mx, mr, a));
   note_launch();
-  PPLL_LAUNCH_CHECK();
   LnReduceTask& t = defer->t[defer->n++];
   t = LnReduceTask{part, dg, db, dxsum, grid, D, 3, defer->blocks};
   defer->blocks += (3 * D + 31) / 32;

@@ -31,9 +31,9 @@ torch.cuda.synchronize()
 rt.cudaMemset(buf, 0, 65536 * 8)
 m.launch_step(B, x.data_ptr(), y.data_ptr(), out.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
-host = np.zeros(65 * 8, dtype=np.uint64)
+host = np.zeros(130 * 8, dtype=np.uint64)
 rt.cudaMemcpy(host.ctypes.data, buf, host.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
-a = host.reshape(65, 8)[:, :5].astype(np.float64)
+a = host.reshape(130, 8)[:, :5].astype(np.float64)
 a = a[a[:, 0] > 0]
 rel = (a - a[:, 0].min()) / 1e3
 names = ["start", "mma done", "x/dres", "row sums", "col sums"]
