@@ -317,6 +317,209 @@ gemm_ln_bwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_const
   }
 }
 
+// ---------------------------------------------------------------------------
+// Forward counterpart: x1 = res + A·W + bias and xn = LN(x1) (the ViT proj
+// GEMM followed by LN2), one 2-CTA cluster per 128-row tile, N half per CTA
+// (W read MN-major, as the forward GEMMs do).  The residual columns arrive by
+// TMA in the freed ring; the epilogue keeps its 48 values per row in registers:
+// pass A stores x1 (bf16) and sums its rounded values, the halves exchange the
+// row sums (DSMEM) -> mean; pass B sums (x1 − mean)², second exchange -> rstd;
+// pass C stores xn.  Same two-pass statistics as ln_fwd_vkernel.
+// ---------------------------------------------------------------------------
+struct FwdArgs {
+  int M, K;
+  const float* bias;            // [D]
+  const float *g, *b;           // LN γ, β [D]
+  __nv_bfloat16 *x1, *xn;       // [M, D]
+  float *mean, *rstd;           // [M]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_ln_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_r, const __grid_constant__ FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  float* prm = reinterpret_cast<float*>(smem + kGamOff);       // reuses γ slot: [3][NH] below
+  float* red = reinterpret_cast<float*>(smem + kRedOff);       // [4][BM]
+  float* rows_s = reinterpret_cast<float*>(smem + kRowOff);    // [2][BM]: mean / var partials
+  float* pb = reinterpret_cast<float*>(smem + kCpartOff);      // bias, γ, β of this half [3][NH]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* xfull = tfull + 1;
+  uint64_t* xch = xfull + 1;       // [2] the peer's mean / variance partials are ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xch + 2);
+  (void)prm;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int half = (int)cluster_ctarank(), tile = blockIdx.x / 2;
+  const int m0 = tile * BM, n0 = half * NH;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(xfull, 1);
+    mbar_init(&xch[0], 1);
+    mbar_init(&xch[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+  const int nkb = a.K / BK;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % STAGES;
+        mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + st * STAGE;
+        mbar_expect_tx(&full[st], STAGE);
+        tma_load_2d(&map_a, &full[st], sa, kb * BK, m0);
+#pragma unroll
+        for (int i = 0; i < NH / 64; ++i)   // W [K, N] MN-major: 64-column boxes 8 KB apart
+          tma_load_2d(&map_b, &full[st], sa + A_BYTES + i * 8192, n0 + 64 * i, kb * BK);
+      }
+      mbar_wait(tfull, 0);
+      mbar_expect_tx(xfull, BM * NH * 2);
+      for (int b = 0; b < NH / 64; ++b)
+        tma_load_2d(&map_r, xfull, smem + b * 16384, n0 + 64 * b, m0);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BM, NH, false, true);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % STAGES;
+        mbar_wait(&full[st], (kb / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(smem + st * STAGE);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          mma_bf16(tmem, umma_desc_sw128(sa + k * 32, 16, 1024),
+                   umma_desc_sw128(sa + A_BYTES + k * 2048, 8192, 1024), idesc,
+                   (kb | k) ? 1u : 0u);
+        mma_commit(&empty[st]);
+      }
+      mma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3, grp = (warp - 2) >> 2;
+    const int r = q * 32 + lane, row = m0 + r;
+    const bool live = row < a.M;
+    for (int c = threadIdx.x - 64; c < NH; c += 32 * kEpiWarps) {
+      pb[c] = a.bias[n0 + c];
+      pb[NH + c] = a.g[n0 + c];
+      pb[2 * NH + c] = a.b[n0 + c];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    mbar_wait(xfull, 0);
+    auto st16 = [&](__nv_bfloat16* dst, const float (&o)[16]) {
+      uint4 q0, q1;
+      __nv_bfloat162* h0 = reinterpret_cast<__nv_bfloat162*>(&q0);
+      __nv_bfloat162* h1 = reinterpret_cast<__nv_bfloat162*>(&q1);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        h0[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+        h1[e] = __floats2bfloat162_rn(o[8 + 2 * e], o[8 + 2 * e + 1]);
+      }
+      reinterpret_cast<uint4*>(dst)[0] = q0;
+      reinterpret_cast<uint4*>(dst)[1] = q1;
+    };
+    // row-sum exchange k (0: Σ x1, 1: Σ (x1 − mean)²) with the peer half
+    auto exchange = [&](float part, int k) -> float {
+      red[grp * BM + r] = part;
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");
+      if (grp == 0)
+        rows_s[k * BM + r] = ((red[r] + red[BM + r]) + red[2 * BM + r]) + red[3 * BM + r];
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (threadIdx.x == 64) mbar_arrive_cluster(mapa_shared(smem_u32(&xch[k]), (uint32_t)(half ^ 1)));
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tXF_%=:\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n\t"
+          "@!p bra XF_%=;\n\t}" ::"r"(smem_u32(&xch[k]))
+          : "memory");
+      float peer;
+      const uint32_t ra = mapa_shared(smem_u32(rows_s + k * BM + r), (uint32_t)(half ^ 1));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer) : "r"(ra) : "memory");
+      const float own = rows_s[k * BM + r];
+      return half == 0 ? own + peer : peer + own;
+    };
+    float v[3][16];
+    float s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = 16 * grp + 64 * j;
+      uint32_t u[16];
+      tmem_ld16(tbase + (uint32_t)c, u);
+      const uint8_t* box = smem + (c / 64) * 16384 + r * 128;
+      const int j0 = (c % 64) / 8;
+      const uint4 q0 = *reinterpret_cast<const uint4*>(box + ((j0 ^ (r & 7)) << 4));
+      const uint4 q1 = *reinterpret_cast<const uint4*>(box + (((j0 + 1) ^ (r & 7)) << 4));
+      const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&q0);
+      const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
+      float o[16];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 r0 = __bfloat1622float2(h0[e]), r1 = __bfloat1622float2(h1[e]);
+        o[2 * e] = __uint_as_float(u[2 * e]) + pb[c + 2 * e] + r0.x;
+        o[2 * e + 1] = __uint_as_float(u[2 * e + 1]) + pb[c + 2 * e + 1] + r0.y;
+        o[8 + 2 * e] = __uint_as_float(u[8 + 2 * e]) + pb[c + 8 + 2 * e] + r1.x;
+        o[8 + 2 * e + 1] = __uint_as_float(u[8 + 2 * e + 1]) + pb[c + 8 + 2 * e + 1] + r1.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {   // the statistics see the stored (rounded) x1
+        v[j][i] = __bfloat162float(__float2bfloat16_rn(o[i]));
+        s1 += live ? v[j][i] : 0.f;
+      }
+      if (live) st16(a.x1 + (long)row * D + n0 + c, o);
+    }
+    const float mean = exchange(s1, 0) * (1.f / D);
+    float s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float d = v[j][i] - mean;
+        s2 += live ? d * d : 0.f;
+      }
+    const float rstd = rsqrtf(exchange(s2, 1) * (1.f / D) + kLnEps);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = 16 * grp + 64 * j;
+      float o[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] = (v[j][i] - mean) * rstd * pb[NH + c + i] + pb[2 * NH + c + i];
+      if (live) st16(a.xn + (long)row * D + n0 + c, o);
+    }
+    if (live && half == 0 && grp == 0) {
+      a.mean[row] = mean;
+      a.rstd[row] = rstd;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -397,4 +600,50 @@ int launch_gemm_ln_bwd(int M, int K, const __nv_bfloat16* dY, const __nv_bfloat1
   return PPLL_OK;
 }
 
+}  // namespace ppll
+
+namespace ppll {
+// x1 = res + A·W + bias, xn = LN(x1)·γ + β with mean / rstd per row (bf16,
+// D = 384): A [M, K] (ld K), W [K, 384] (ld 384), res / x1 / xn [M, 384].
+// PPLL_ERR_UNSUPPORTED outside the fused range.
+int launch_gemm_ln_fwd(int M, int K, const __nv_bfloat16* A, const __nv_bfloat16* W,
+                       const float* bias, const __nv_bfloat16* res, const float* g, const float* b,
+                       __nv_bfloat16* x1, __nv_bfloat16* xn, float* mean, float* rstd,
+                       cudaStream_t s) {
+  using namespace gln;
+  // off by default: measured ViT-S pipeline 55.0k -> 54.1k img/s (the 148-CTA proj GEMM + LN
+  // kernel beat the 130-CTA fused form with its two DSMEM exchanges); PPLL_GEMM_LN_FWD=1 enables
+  static const int on = getenv("PPLL_GEMM_LN_FWD") ? atoi(getenv("PPLL_GEMM_LN_FWD")) : 0;
+  if (!on || M < 1 || K % BK || K < BK || !bias || !res) return PPLL_ERR_UNSUPPORTED;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al(A) || !al(W) || !al(res) || !al(x1) || !al(xn)) return PPLL_ERR_UNSUPPORTED;
+  CUtensorMap ma, mb, mr;
+  if (!kmap(&ma, A, K, M, K, BM) || !kmap(&mb, W, D, K, D, 64) || !kmap(&mr, res, D, M, D, BM))
+    return PPLL_ERR_UNSUPPORTED;
+  static bool attr = false;
+  if (!attr) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(gemm_ln_fwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  const int tiles = (M + BM - 1) / BM;
+  FwdArgs a{M, K, bias, g, b, x1, xn, mean, rstd};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * tiles);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_ln_fwd_kernel, ma, mb, mr, a));
+  note_launch();
+  return PPLL_OK;
+}
 }  // namespace ppll

@@ -36,6 +36,10 @@ int launch_ln_reduce_deferred(const LnDefer& d, cudaStream_t s);
 // LayerNorm backward fused into the data-gradient GEMM that feeds it
 // (gemm_ln.cu, D = 384): dx = LN_bwd(dY·Wᵀ) (+ dres), column partials recorded
 // in `defer`; PPLL_ERR_UNSUPPORTED outside its range.
+int launch_gemm_ln_fwd(int M, int K, const __nv_bfloat16* A, const __nv_bfloat16* W,
+                       const float* bias, const __nv_bfloat16* res, const float* g, const float* b,
+                       __nv_bfloat16* x1, __nv_bfloat16* xn, float* mean, float* rstd,
+                       cudaStream_t s);
 int launch_gemm_ln_bwd(int M, int K, const __nv_bfloat16* dY, const __nv_bfloat16* W,
                        const __nv_bfloat16* x, const float* mean, const float* rstd,
                        const float* g, const __nv_bfloat16* dres, __nv_bfloat16* dx, float* part,

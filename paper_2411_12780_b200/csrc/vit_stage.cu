@@ -148,16 +148,28 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     if (r) return r;
     r = attn_fwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
     if (r) return r;
-    LinOpts o2;
-    o2.bias = st->P(st->po(l, kBo));
-    o2.res = xcur;
-    o2.ldres = D;
-    r = gemm_fwd(M, D, D, b.o, D, st->W(st->po(l, kWo)), o2, b.x1, D, st->dtype, st->ws,
-                 st->ws_elems, s);
-    if (r) return r;
-    r = launch_ln_fwd<TT>(M, D, (const TT*)b.x1, D, st->P(st->po(l, kLn2g)),
-                          st->P(st->po(l, kLn2b)), (TT*)b.xn2, D, b.mean2, b.rstd2, s);
-    if (r) return r;
+    // proj (+bias, +residual) -> x1 and LN2 -> xn2: one fused launch for bf16
+    // D = 384 (gemm_ln.cu), else the GEMM with its residual epilogue + LN kernel
+    r = PPLL_ERR_UNSUPPORTED;
+    if (st->dtype == PPLL_BF16 && D == 384)
+      r = launch_gemm_ln_fwd(M, D, (const __nv_bfloat16*)b.o,
+                             (const __nv_bfloat16*)st->W(st->po(l, kWo)), st->P(st->po(l, kBo)),
+                             (const __nv_bfloat16*)xcur, st->P(st->po(l, kLn2g)),
+                             st->P(st->po(l, kLn2b)), (__nv_bfloat16*)b.x1, (__nv_bfloat16*)b.xn2,
+                             b.mean2, b.rstd2, s);
+    if (r != PPLL_OK && r != PPLL_ERR_UNSUPPORTED) return r;
+    if (r == PPLL_ERR_UNSUPPORTED) {
+      LinOpts o2;
+      o2.bias = st->P(st->po(l, kBo));
+      o2.res = xcur;
+      o2.ldres = D;
+      r = gemm_fwd(M, D, D, b.o, D, st->W(st->po(l, kWo)), o2, b.x1, D, st->dtype, st->ws,
+                   st->ws_elems, s);
+      if (r) return r;
+      r = launch_ln_fwd<TT>(M, D, (const TT*)b.x1, D, st->P(st->po(l, kLn2g)),
+                            st->P(st->po(l, kLn2b)), (TT*)b.xn2, D, b.mean2, b.rstd2, s);
+      if (r) return r;
+    }
     LinOpts o3;
     o3.bias = st->P(st->po(l, kB1));
     o3.act = kActGeluD;   // b.u <- gelu'(pre-activation)
