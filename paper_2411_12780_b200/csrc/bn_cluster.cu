@@ -64,6 +64,7 @@ struct FwdArgs {
   float4* gpart;                      // grid form: per-CTA partials [grid][C]
   unsigned* gbar;                     // grid form: {arrivals, generation}
   int* err;                           // grid form: sticky error word (watchdog: kErrSync)
+  int ncl;                            // split form: cluster partials written by launch A
 };
 
 struct BwdArgs {
@@ -84,6 +85,7 @@ struct BwdArgs {
   float4* gpart;
   unsigned* gbar;
   int* err;
+  int ncl;
 };
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
@@ -273,6 +275,28 @@ __device__ __forceinline__ float4 merge_partials(const float4* cpart, float4* sc
   return acc;
 }
 
+// SPLIT form (stage streams sharing the GPU, tensors past the one-cluster
+// range): launch A (SPLIT = 1) = statistics over the whole grid, merged per
+// 8-CTA cluster over DSMEM, rank 0 writing the cluster's partial to
+// gpart[cluster]; launch B (SPLIT = 2, plain grid) = every CTA sums the ncl
+// cluster partials in ascending order, then applies.  No grid barrier (the
+// kernel boundary orders A before B), two launches instead of three / four.
+__device__ __forceinline__ float4 split_partial_out(const float4* cpart, int C, float4* gpart) {
+  const float4 acc = merge_partials<false>(cpart, nullptr, C, nullptr, nullptr, nullptr);
+  if (threadIdx.x < C && cluster_ctarank() == 0)
+    gpart[(long)(blockIdx.x / cluster_nctarank()) * C + threadIdx.x] = acc;
+  return acc;
+}
+__device__ __forceinline__ float4 split_partial_in(int C, const float4* gpart, int ncl) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x < C)
+    for (int k = 0; k < ncl; ++k) {
+      const float4 q = __ldcg(&gpart[(long)k * C + threadIdx.x]);
+      acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+    }
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // forward: per channel, with one shift K = z[0, c] for the whole cluster,
 //   S1 = Σ (z − K), S2 = Σ (z − K)²   (plain fixed-order sums, no divisions)
@@ -280,7 +304,7 @@ __device__ __forceinline__ float4 merge_partials(const float4* cpart, float4* sc
 //   y = act( z·s + t  [+ z2·s2 + t2 | + res] ),  s = γ·rstd, t = β − mean·s
 // RESIDENT: the whole slice (incl. res) fits in the ring: one HBM read.
 // ---------------------------------------------------------------------------
-template <bool TWO, bool RES, bool RESIDENT, bool GRID = false>
+template <bool TWO, bool RES, bool RESIDENT, bool GRID = false, int SPLIT = 0>
 __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __grid_constant__ FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -290,8 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int C = a.C, V = C >> 3, vc = t % V;
-  const int CS = GRID ? (int)gridDim.x : (int)cluster_nctarank();
-  const int rank = GRID ? (int)blockIdx.x : (int)cluster_ctarank();
+  // row slice of this CTA: over the cluster (one-cluster form) or over the grid
+  const int CS = (GRID || SPLIT) ? (int)gridDim.x : (int)cluster_nctarank();
+  const int rank = (GRID || SPLIT) ? (int)blockIdx.x : (int)cluster_ctarank();
   const int rpc = (a.P + CS - 1) / CS;
   const int r0 = min(a.P, rank * rpc), r1 = min(a.P, r0 + rpc);
   const long bytes = (long)(r1 - r0) * C * 2, o = (long)r0 * C;
@@ -301,12 +326,13 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
   BN_TL(1)
 
   constexpr int NT1 = 1 + (TWO ? 1 : 0) + (RES && RESIDENT ? 1 : 0);
+  static_assert(SPLIT != 2 || !RESIDENT, "the apply-only launch streams its slice");
   Ring<NT1> r1g;
   r1g.init(smem, bars, bytes);
   r1g.src[0] = reinterpret_cast<const uint8_t*>(a.z + o);
   if constexpr (TWO) r1g.src[1] = reinterpret_cast<const uint8_t*>(a.z2 + o);
   if constexpr (RES && RESIDENT) r1g.src[NT1 - 1] = reinterpret_cast<const uint8_t*>(a.res + o);
-  r1g.start();
+  if constexpr (SPLIT != 2) r1g.start();
 
   // the cluster-wide shift: row 0 of the tensor (a sample of every channel)
   float2 nk[4], s1[4], s2[4], nk2[4], u1[4], u2[4];
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
       s1[p] = s2[p] = u1[p] = u2[p] = make_float2(0.f, 0.f);
     }
   }
-  for (long i = 0; i < r1g.nch; ++i) {
+  for (long i = 0; i < (SPLIT == 2 ? 0 : r1g.nch); ++i) {
     const uint8_t* sl = r1g.wait(i);
     const int nv = r1g.nvec(i);
     for (int v = t; v < nv; v += kThreads) {
@@ -382,7 +408,17 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
     cpart[t] = sacc;
   }
   BN_TL(3)
-  const float4 sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
+  float4 sacc;
+  if constexpr (SPLIT == 1) {
+    split_partial_out(cpart, C, a.gpart);
+    cluster_arrive();
+    cluster_wait();
+    return;
+  } else if constexpr (SPLIT == 2) {
+    sacc = split_partial_in(C, a.gpart, a.ncl);
+  } else {
+    sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
+  }
   if (t < C) {
     const float invP = 1.f / (float)a.P;
     {
@@ -404,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
       if (rank == 0) { a.mean2[t] = mean; a.rstd2[t] = rstd; }
     }
   }
-  if constexpr (!GRID) cluster_arrive();   // done reading the peers' partials
+  if constexpr (!GRID && !SPLIT) cluster_arrive();   // done reading the peers' partials
   __syncthreads();
   BN_TL(4)
 
@@ -452,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
     }
   }
   BN_TL(5)
-  if constexpr (!GRID) cluster_wait();   // no CTA leaves while a peer may still read its partial
+  if constexpr (!GRID && !SPLIT) cluster_wait();   // no CTA leaves while a peer may still read its partial
   BN_TL(6)
 }
 
@@ -460,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
 // backward: dy = dout [⊙ (out > 0)];  dγ = Σ dy·x̂, dβ = Σ dy (cluster-merged);
 //   dz = γ·rstd·(dy − (dβ + x̂·dγ)/P) = A·dy + B·z + D   [dz2 likewise]
 // ---------------------------------------------------------------------------
-template <bool MASK, bool TWO, bool RESIDENT, bool GRID = false>
+template <bool MASK, bool TWO, bool RESIDENT, bool GRID = false, int SPLIT = 0>
 __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __grid_constant__ BwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -470,8 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int C = a.C, V = C >> 3, vc = t % V;
-  const int CS = GRID ? (int)gridDim.x : (int)cluster_nctarank();
-  const int rank = GRID ? (int)blockIdx.x : (int)cluster_ctarank();
+  const int CS = (GRID || SPLIT) ? (int)gridDim.x : (int)cluster_nctarank();
+  const int rank = (GRID || SPLIT) ? (int)blockIdx.x : (int)cluster_ctarank();
   const int rpc = (a.P + CS - 1) / CS;
   const int r0 = min(a.P, rank * rpc), r1 = min(a.P, r0 + rpc);
   const long bytes = (long)(r1 - r0) * C * 2, o = (long)r0 * C;
@@ -488,7 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
   if constexpr (MASK) rg.src[kOut] = reinterpret_cast<const uint8_t*>(a.out + o);
   rg.src[kZ] = reinterpret_cast<const uint8_t*>(a.z + o);
   if constexpr (TWO) rg.src[kZ2] = reinterpret_cast<const uint8_t*>(a.z2 + o);
-  rg.start();
+  static_assert(SPLIT != 2 || !RESIDENT, "the apply-only launch streams its slice");
+  if constexpr (SPLIT != 2) rg.start();
 
   // x̂ = z·rstd − mean·rstd
   float2 rs[4], nm[4], rs2[4], nm2[4], sg[4], sb[4], sg2[4];
@@ -501,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
     nm2[p] = TWO ? make_float2(-a.mean2[c] * rs2[p].x, -a.mean2[c + 1] * rs2[p].y) : nm[p];
     sg[p] = sb[p] = sg2[p] = make_float2(0.f, 0.f);
   }
-  for (long i = 0; i < rg.nch; ++i) {
+  for (long i = 0; i < (SPLIT == 2 ? 0 : rg.nch); ++i) {
     const uint8_t* sl = rg.wait(i);
     const int nv = rg.nvec(i);
     for (int v = t; v < nv; v += kThreads) {
@@ -555,7 +592,17 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
     cpart[t] = sacc;
   }
   BN_TL(3)
-  const float4 sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
+  float4 sacc;
+  if constexpr (SPLIT == 1) {
+    split_partial_out(cpart, C, a.gpart);
+    cluster_arrive();
+    cluster_wait();
+    return;
+  } else if constexpr (SPLIT == 2) {
+    sacc = split_partial_in(C, a.gpart, a.ncl);
+  } else {
+    sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
+  }
   if (t < C) {
     // dz = k1·(dy − db/P − x̂·dg/P) = A·dy + B·z + D
     const float k1 = pg * pr;
@@ -579,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
       }
     }
   }
-  if constexpr (!GRID) cluster_arrive();
+  if constexpr (!GRID && !SPLIT) cluster_arrive();
   __syncthreads();
   BN_TL(4)
 
@@ -629,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_bwd_cluster_kernel(const __gri
     }
   }
   BN_TL(5)
-  if constexpr (!GRID) cluster_wait();
+  if constexpr (!GRID && !SPLIT) cluster_wait();
   BN_TL(6)
 }
 
@@ -746,8 +793,12 @@ static int fused_mode(long P, int C, bool bwd, bool grid_ok) {
   static const double grid_mb = getenv("PPLL_BN_GRID_MAX_MB") ? atof(getenv("PPLL_BN_GRID_MAX_MB")) : 64.0;
   if (off || C % 8 || C > kMaxC || kThreads % (C / 8) || P < 1 || P > (1L << 30) / C) return 0;
   const double mb = (double)P * C * 2 / 1048576.0;
+  // split form off by default: its 144 one-per-SM CTAs (~200 KB smem) crowd out the other
+  // stage streams — ResNet-32 pipeline 132.8k -> 111.3k img/s (PPLL_BN_SPLIT=1 enables)
+  static const int split_on = getenv("PPLL_BN_SPLIT") ? atoi(getenv("PPLL_BN_SPLIT")) : 0;
   if (mb <= (bwd ? bwd_mb : fwd_mb)) return 1;
-  return (grid_ok && g_gpu_excl && mb <= grid_mb) ? 2 : 0;
+  if (!grid_ok || mb > grid_mb) return 0;
+  return g_gpu_excl ? 2 : (split_on ? 3 : 0);
 }
 
 // cluster size + launch of one kernel instantiation; `resident` picks the
@@ -775,6 +826,50 @@ static int run_fused(K kern_stream, K kern_resident, long P, int C, const A& arg
   const bool res = (slice + Ring<NT>::PIECE - 1) / Ring<NT>::PIECE <= Ring<NT>::NS;
   return res ? launch_cluster(kern_resident, cs_r, args, s) : launch_cluster(kern_stream, cs, args, s);
 }
+// split form: launch A = 8-CTA clusters over the grid (statistics, one partial
+// per cluster), launch B = a plain grid that merges them and applies
+template <typename K, typename A>
+static int run_split(K kern_a, K kern_b, A args, cudaStream_t s) {
+  constexpr int kCl = 8, kNcl = 18;   // 144 CTAs: one per SM, whole clusters
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  static const void* keys[32];
+  static int n = 0;
+  bool seen = false;
+  for (int i = 0; i < n; ++i) seen |= keys[i] == (const void*)kern_a;
+  if (!seen) {
+    if (cudaFuncSetAttribute(kern_a, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(kern_b, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess) {
+      cudaGetLastError();
+      return PPLL_ERR_UNSUPPORTED;
+    }
+    if (n < 32) keys[n++] = (const void*)kern_a;
+  }
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kCl * kNcl);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = g_pdl;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern_a, args));
+    note_launch();
+  }
+  args.ncl = kNcl;
+  launch_k(kern_b, kCl * kNcl, kThreads, kSmem, s, args);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+
 template <int NT, typename K, typename A>
 static int run_grid(K kern_stream, K kern_resident, long P, int C, const A& args, cudaStream_t s) {
   int dev = 0, sms = 148;
@@ -797,10 +892,12 @@ int launch_bn_fwd_fused(int P, int C, const __nv_bfloat16* z, const float* g, co
     return PPLL_ERR_UNSUPPORTED;
   if (z2 && res) return PPLL_ERR_UNSUPPORTED;
   FwdArgs a{P, C, z, g, b, mean, rstd, z2, g2, b2, mean2, rstd2, res, relu, y, bn_tl(),
-            mode == 2 ? (float4*)grid->part : nullptr, mode == 2 ? grid->bar : nullptr,
-            mode == 2 ? grid->err : nullptr};
+            mode >= 2 ? (float4*)grid->part : nullptr, mode == 2 ? grid->bar : nullptr,
+            mode == 2 ? grid->err : nullptr, 0};
 #define PPLL_BN_FWD(NT_, T_, R_)                                                                 \
-  return mode == 2 ? run_grid<NT_>(bn_fwd_cluster_kernel<T_, R_, false, true>,                   \
+  return mode == 3 ? run_split(bn_fwd_cluster_kernel<T_, R_, false, false, 1>,                   \
+                               bn_fwd_cluster_kernel<T_, R_, false, false, 2>, a, s)             \
+       : mode == 2 ? run_grid<NT_>(bn_fwd_cluster_kernel<T_, R_, false, true>,                   \
                                    bn_fwd_cluster_kernel<T_, R_, true, true>, P, C, a, s)        \
                    : run_fused<NT_>(bn_fwd_cluster_kernel<T_, R_, false>,                        \
                                     bn_fwd_cluster_kernel<T_, R_, true>, P, C, a, s);
@@ -823,10 +920,12 @@ int launch_bn_bwd_fused(int P, int C, const __nv_bfloat16* dout, const __nv_bflo
     return PPLL_ERR_UNSUPPORTED;
   BwdArgs a{P, C, 1.f / (float)P, dout, out, out ? dy_store : nullptr, z, mean, rstd, g, dg, db, dz,
             z2, mean2, rstd2, g2, dg2, db2, dz2, bn_tl(),
-            mode == 2 ? (float4*)grid->part : nullptr, mode == 2 ? grid->bar : nullptr,
-            mode == 2 ? grid->err : nullptr};
+            mode >= 2 ? (float4*)grid->part : nullptr, mode == 2 ? grid->bar : nullptr,
+            mode == 2 ? grid->err : nullptr, 0};
 #define PPLL_BN_BWD(NT_, M_, T_)                                                                 \
-  return mode == 2 ? run_grid<NT_>(bn_bwd_cluster_kernel<M_, T_, false, true>,                   \
+  return mode == 3 ? run_split(bn_bwd_cluster_kernel<M_, T_, false, false, 1>,                   \
+                               bn_bwd_cluster_kernel<M_, T_, false, false, 2>, a, s)             \
+       : mode == 2 ? run_grid<NT_>(bn_bwd_cluster_kernel<M_, T_, false, true>,                   \
                                    bn_bwd_cluster_kernel<M_, T_, true, true>, P, C, a, s)        \
                    : run_fused<NT_>(bn_bwd_cluster_kernel<M_, T_, false>,                        \
                                     bn_bwd_cluster_kernel<M_, T_, true>, P, C, a, s);

@@ -68,11 +68,22 @@ def test_layernorm_matches_torch(precision, M, D):
     assert _rel(dxs, dx.double().sum(0) if precision == "fp32" else ref_dx.sum(0)) < tp
 
 
+@pytest.mark.parametrize("exclusive", [1, 0])
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("P,C,res", [(131072, 16, False), (8192, 64, True), (2048, 32, True),
                                      (300, 24, False), (131072, 16, True), (262144, 32, False),
                                      (524288, 16, True), (1048576, 16, False)])
-def test_batchnorm_matches_torch(precision, P, C, res):
+def test_batchnorm_matches_torch(precision, P, C, res, exclusive):
+    """exclusive = 1: large bf16 tensors take the cooperative full-GPU form;
+    0 (stage streams sharing the GPU): the two-launch split form."""
+    prev = N.load().ppll_set_gpu_exclusive(exclusive)
+    try:
+        _batchnorm_case(precision, P, C, res)
+    finally:
+        N.load().ppll_set_gpu_exclusive(prev)
+
+
+def _batchnorm_case(precision, P, C, res):
     dt = torch.float32 if precision == "fp32" else torch.bfloat16
     code = N.F32 if precision == "fp32" else N.BF16
     g = torch.Generator(device="cuda").manual_seed(P + C)
