@@ -1,3 +1,4 @@
+# NOTE: the light GEMM form was reverted after this A/B ("tried"); PPLL_GEMM_LIGHT is a no-op on the current tree
 # light GEMM form (8 epilogue warps, 2 stages, one TMEM accumulator, 2 CTAs/SM) for
 # stage streams sharing the GPU: parity with the light form forced on, then the
 # ViT-S / ResNet-32 / ViT-B pipeline benches with and without it
