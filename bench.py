@@ -979,8 +979,12 @@ def roofline_gemm(wl, tf_burst, hbm, dev):
         step_t = None
         print(f"[bench] step-stream GEMM sequence failed: {e}", file=sys.stderr)
     del keep
-    traffic = _ncu_traffic("vit_layer")
-    return {"kernel": "gemm_tc (tcgen05 engine): the 12 GEMM launches of one ViT-S layer's "
+    sp = wl["spec"]
+    is_vit_s = sp["dim"] == 384 and sp["image"] == 32
+    # the committed ncu capture is of the ViT-S layer; other geometries get null
+    traffic = _ncu_traffic("vit_layer") if is_vit_s else None
+    label = "ViT-S" if is_vit_s else f"ViT (D={sp['dim']}, {sp['image']}px/{sp['patch']})"
+    return {"kernel": f"gemm_tc (tcgen05 engine): the 12 GEMM launches of one {label} layer's "
                       "local step with the step's fused epilogues, in step order, replayed back "
                       "to back from one CUDA graph (PDL edges; inputs larger than L2, no flush)",
             "bound": "tensor", "achieved": tot_fl / seq_t / 1e12, "peak": tf_burst,
