@@ -19,4 +19,5 @@ for name in sys.argv[1:] or ["vit_s"]:
     print(f"{name}: engine {r['achieved']:.1f} TF/s frac {r['frac']:.3f}  "
           f"mean launch {r['launch_us']:.2f} us")
     for g in r["per_gemm"]:
-        print(f"  {g['us']:7.2f} us {g['tflops']:7.1f} TF/s  {g['gemm']}")
+        print(f"  {g['us']:7.2f} us alone {g.get('us_in_sequence', 0):7.2f} us in seq "
+              f"{g['tflops']:7.1f} TF/s  {g['gemm']}")
