@@ -327,27 +327,37 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
 // split-K reduction (splitk_reduce) sums the partials — deterministic, no
 // im2col matrix (which was P·9·CI bf16: 38 MB for a 32x32x16 layer at B=128).
 // ---------------------------------------------------------------------------
-template <int CI, int CO>
+// HALO (chunks of whole rows of one image, CI <= 32): the chunk's input is
+// three column-shifted copies (dx = -1, 0, +1) of its rows plus a halo row on
+// each side, as in the forward; M-tile dx stacks the taps dy = -1, 0, +1 of
+// copy dx along M at a stride of one image row (LBO = W·RB, whole swizzle
+// atoms), the remaining 128/CI − 3 atoms of the tile read further rows and
+// their (discarded) dW rows are never stored.  3·(rows + 2)/rows instead of
+// 9 windows of TMA rows per chunk, so twice as many chunks are in flight.
+template <int CI, int CO, bool HALO = false>
 struct WgSmem {
   static constexpr int RB = CI * 2, RBO = CO * 2;
-  static constexpr int SLOT = 128 * RB;                     // one tap window
-  static constexpr int TAPS_PER_M = 128 / CI;               // taps per M = 128 tile
-  static constexpr int MT = (9 + TAPS_PER_M - 1) / TAPS_PER_M;
+  static constexpr int SLOT = (HALO ? 192 : 128) * RB;      // a tap window / a shifted copy
+  static constexpr int TAPS_PER_M = 128 / CI;               // taps (atoms) per M = 128 tile
+  static constexpr int MT = HALO ? 3 : (9 + TAPS_PER_M - 1) / TAPS_PER_M;
   static constexpr int DZ = 128 * RBO;
-  static constexpr int BUF = 9 * SLOT + DZ;                 // one chunk
-  static constexpr int NB = CI == 16 ? 4 : (CI == 32 ? 2 : 1);
-  // the last M-tile reads up to MT·TAPS_PER_M − 9 slots past a buffer's ninth
-  static constexpr int PAD = (MT * TAPS_PER_M - 9) * SLOT;
+  static constexpr int BUF = (HALO ? 3 : 9) * SLOT + DZ;    // one chunk
+  static constexpr int NB = HALO ? (204800 / BUF < 8 ? 204800 / BUF : 8)
+                                : (CI == 16 ? 4 : (CI == 32 ? 2 : 1));
+  // the last M-tile reads up to MT·TAPS_PER_M − 9 slots past a buffer's ninth;
+  // (HALO) copy dx = +1 of the last buffer read up to TAPS_PER_M − 1 rows (≤ 8 KB
+  // at W·RB ≤ 1 KB) plus a window past its start
+  static constexpr int PAD = HALO ? 8192 : (MT * TAPS_PER_M - 9) * SLOT;
   static constexpr int TOTAL = NB * BUF + PAD + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = MT * CO <= 32 ? 32 : (MT * CO <= 64 ? 64 : (MT * CO <= 128 ? 128 : (MT * CO <= 256 ? 256 : 512)));
 };
 
-template <int CI, int CO, bool CLUSTER = false>
+template <int CI, int CO, bool CLUSTER = false, bool HALO = false>
 __global__ void __launch_bounds__(192, 1)
 conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                         const __grid_constant__ CUtensorMap dzmap, int P, int H, int Wd,
                         float* __restrict__ part) {
-  using L = WgSmem<CI, CO>;
+  using L = WgSmem<CI, CO, HALO>;
   constexpr int NB = L::NB, RB = L::RB, RBO = L::RBO, MT = L::MT;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
@@ -391,8 +401,15 @@ conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         const int b = kb % NB;
         mbar_wait(&empty[b], ((kb / NB) & 1) ^ 1);
         uint8_t* buf = smem + b * L::BUF;
-        mbar_expect_tx(&full[b], 9 * L::SLOT + L::DZ);
         const int p0 = c * 128, n0 = p0 / HWp, h0 = (p0 % HWp) / Wd;
+        if constexpr (HALO) {
+          mbar_expect_tx(&full[b], 3 * (128 + 2 * Wd) * RB + L::DZ);
+          for (int dx = 0; dx < 3; ++dx)
+            tma_load_4d(&xmap, &full[b], buf + dx * L::SLOT, 0, dx - 1, h0 - 1, n0);
+          tma_load_2d(&dzmap, &full[b], buf + 3 * L::SLOT, 0, p0);
+          continue;
+        }
+        mbar_expect_tx(&full[b], 9 * L::SLOT + L::DZ);
         for (int tap = 0; tap < 9; ++tap)
           tma_load_4d(&xmap, &full[b], buf + tap * L::SLOT, 0, tap % 3 - 1, h0 + tap / 3 - 1, n0);
         tma_load_2d(&dzmap, &full[b], buf + 9 * L::SLOT, 0, p0);
@@ -409,13 +426,15 @@ conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         mbar_wait(&full[b], (kb / NB) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sbuf = smem_u32(smem + b * L::BUF);
-        const uint32_t sdz = sbuf + 9 * L::SLOT;
+        const uint32_t sdz = sbuf + (HALO ? 3 : 9) * L::SLOT;
+        // M-tile stride between taps: a window (SLOT) / an image row (HALO)
+        const uint32_t lbo = HALO ? (uint32_t)(Wd * RB) : (uint32_t)L::SLOT;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const uint32_t sa = sbuf + (uint32_t)(mt * L::TAPS_PER_M * L::SLOT);
+          const uint32_t sa = sbuf + (uint32_t)(mt * (HALO ? 1 : L::TAPS_PER_M) * L::SLOT);
 #pragma unroll
           for (int k = 0; k < 8; ++k)   // 16 pixels per MMA = two 8-row groups
-            mma_bf16(tmem + (uint32_t)(mt * CO), mndesc<RB>(sa + k * 16 * RB, L::SLOT),
+            mma_bf16(tmem + (uint32_t)(mt * CO), mndesc<RB>(sa + k * 16 * RB, lbo),
                      mndesc<RBO>(sdz + k * 16 * RBO, 128 * RBO), idesc,
                      (c > c0 || k > 0) ? 1u : 0u);
         }
@@ -436,7 +455,11 @@ conv3x3_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     float* dst = CLUSTER ? reinterpret_cast<float*>(smem) : part + (long)blockIdx.x * 9 * CI * CO;
 #pragma unroll 1
     for (int mt = 0; mt < MT; ++mt) {
-      const int row = mt * 128 + q * 32 + lane;
+      // dW row (tap·CI + ci) of TMEM lane q·32 + lane: HALO tile dx holds tap
+      // (dy, dx) = atom dy (< 3), ci at lane % CI
+      const int lr = q * 32 + lane;
+      const int row = HALO ? ((lr / CI) < 3 ? ((lr / CI) * 3 + mt) * CI + lr % CI : 1 << 20)
+                           : mt * 128 + lr;
 #pragma unroll 1
       for (int cc = 0; cc < CO; cc += 16) {
         uint32_t r[16];
@@ -623,11 +646,24 @@ int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bflo
   if (((uintptr_t)x & 15) || ((uintptr_t)dz & 15) || ((uintptr_t)dw & 15)) return PPLL_ERR_UNSUPPORTED;
   auto enc = encoder();
   if (!enc) return PPLL_ERR_UNSUPPORTED;
+  // whole rows of one image per chunk: the halo form (PPLL_CONV_WGRAD_HALO=0 never,
+  // 1 where it measured faster, 2 always)
+  // (read per call: the parity tests switch it)
+  const char* halo_s = getenv("PPLL_CONV_WGRAD_HALO");
+  const int halo_env = halo_s ? atoi(halo_s) : 1;
+  // Measured (tools/ab_wgrad_halo.sh): faster in the wide form (16->16 15.0 -> 13.5 us,
+  // 32->32 11.2 -> 10.5 us) and the one-cluster form at CI = 32; the one-cluster
+  // 16->16 form is held by its MMA count (24 vs 16 per chunk: 48.8 -> 57 us)
+  static const int wcl_env = getenv("PPLL_CONV_WGRAD_CLUSTER") ? atoi(getenv("PPLL_CONV_WGRAD_CLUSTER")) : -1;
+  const bool will_cluster = wcl_env >= 0 ? wcl_env != 0 : !g_gpu_excl;
+  const bool halo = CI <= 32 && imgs == 1 && (rows + 2) * W <= 192 && W >= 16 &&
+                    (halo_env == 2 || (halo_env == 1 && (!will_cluster || CI == 32)));
   CUtensorMap xm, dm;
   {
     cuuint64_t dims[4] = {(cuuint64_t)CI, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)CI * 2, (cuuint64_t)W * CI * 2, (cuuint64_t)H * W * CI * 2};
-    cuuint32_t box[4] = {(cuuint32_t)CI, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs};
+    cuuint32_t box[4] = {(cuuint32_t)CI, (cuuint32_t)W, (cuuint32_t)(halo ? rows + 2 : rows),
+                         (cuuint32_t)imgs};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sz = CI == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : (CI == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
@@ -662,13 +698,12 @@ int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bflo
   const int Pi = (int)P;
   // stage streams sharing the GPU (g_gpu_excl == 0): one cluster, in-kernel
   // DSMEM reduction, dW written directly (PPLL_CONV_WGRAD_CLUSTER=0|1 forces)
-  static const int cl_env = getenv("PPLL_CONV_WGRAD_CLUSTER") ? atoi(getenv("PPLL_CONV_WGRAD_CLUSTER")) : -1;
-  const bool cl = cl_env >= 0 ? cl_env != 0 : !g_gpu_excl;
+  const bool cl = will_cluster;
   if (cl) {
-#define WGC_CASE(A, B)                                                                       \
-    if (CI == A && CO == B) {                                                                \
-      auto kern = conv3x3_wgrad_tc_kernel<A, B, true>;                                       \
-      constexpr int smem = WgSmem<A, B>::TOTAL;                                              \
+#define WGC_CASE(A, B, HL)                                                                   \
+    if (CI == A && CO == B && halo == HL) {                                                  \
+      auto kern = conv3x3_wgrad_tc_kernel<A, B, true, HL>;                                   \
+      constexpr int smem = WgSmem<A, B, HL>::TOTAL;                                          \
       static int cs = -1;                                                                    \
       if (cs < 0) {                                                                          \
         cs = 0;                                                                              \
@@ -706,14 +741,16 @@ int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bflo
         return PPLL_OK;                                                                      \
       }                                                                                      \
     }
-    WGC_CASE(16, 16) WGC_CASE(32, 32) WGC_CASE(64, 64) WGC_CASE(16, 32) WGC_CASE(32, 16)
-    WGC_CASE(32, 64) WGC_CASE(64, 32)
+    WGC_CASE(16, 16, true) WGC_CASE(32, 32, true) WGC_CASE(16, 32, true) WGC_CASE(32, 16, true)
+    WGC_CASE(32, 64, true)
+    WGC_CASE(16, 16, false) WGC_CASE(32, 32, false) WGC_CASE(64, 64, false) WGC_CASE(16, 32, false)
+    WGC_CASE(32, 16, false) WGC_CASE(32, 64, false) WGC_CASE(64, 32, false)
 #undef WGC_CASE
   }
-#define WG_CASE(A, B)                                                                        \
-  if (CI == A && CO == B) {                                                                  \
-    auto kern = conv3x3_wgrad_tc_kernel<A, B>;                                               \
-    constexpr int smem = WgSmem<A, B>::TOTAL;                                                \
+#define WG_CASE(A, B, HL)                                                                    \
+  if (CI == A && CO == B && halo == HL) {                                                    \
+    auto kern = conv3x3_wgrad_tc_kernel<A, B, false, HL>;                                    \
+    constexpr int smem = WgSmem<A, B, HL>::TOTAL;                                            \
     static bool attr = false;                                                                \
     if (!attr) {                                                                             \
       PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
@@ -723,8 +760,10 @@ int launch_conv3x3_wgrad_tc(int N, int H, int W, int CI, int CO, const __nv_bflo
     note_launch();                                                                           \
     PPLL_LAUNCH_CHECK();                                                                     \
   } else
-  WG_CASE(16, 16) WG_CASE(32, 32) WG_CASE(64, 64) WG_CASE(16, 32) WG_CASE(32, 16)
-  WG_CASE(32, 64) WG_CASE(64, 32) { return PPLL_ERR_UNSUPPORTED; }
+  WG_CASE(16, 16, true) WG_CASE(32, 32, true) WG_CASE(16, 32, true) WG_CASE(32, 16, true)
+  WG_CASE(32, 64, true)
+  WG_CASE(16, 16, false) WG_CASE(32, 32, false) WG_CASE(64, 64, false) WG_CASE(16, 32, false)
+  WG_CASE(32, 16, false) WG_CASE(32, 64, false) WG_CASE(64, 32, false) { return PPLL_ERR_UNSUPPORTED; }
 #undef WG_CASE
   Epilogue<float> e;
   e.C = dw;

@@ -6,6 +6,8 @@ Tolerances: fp32 parity mode — per-step loss |Δ| <= 2e-4·max(1,|loss|),
 x_out max|Δ|/max|ref| <= 2e-4, weights max|ΔW|/max|W| <= 2e-3; bf16 mode
 — loss 5e-2 relative, x_out 8e-2, weights 8e-2 (BatchNorm over bf16
 activations).  Pipeline vs round-robin: bitwise."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -105,10 +107,13 @@ def test_resnet_pipeline_bitwise_equals_roundrobin(precision):
 
 @pytest.mark.parametrize("N,H,Cin,Cout", [(4, 32, 16, 16), (2, 16, 32, 32), (4, 8, 64, 64),
                                           (2, 16, 16, 32), (6, 8, 64, 32), (128, 32, 16, 16),
-                                          (128, 16, 32, 32), (128, 8, 64, 64), (16, 8, 32, 64)])
+                                          (128, 16, 32, 32), (128, 8, 64, 64), (16, 8, 32, 64),
+                                          (4, 32, 32, 16), (2, 16, 32, 64)])
 def test_implicit_conv3x3_wgrad_matches_torch(N, H, Cin, Cout):
     """The implicit-GEMM weight gradient (TMA tap windows read MN-major, taps
-    stacked along M, split-K partials reduced in fixed order) against the
+    stacked along M — or, for chunks of whole rows at Cin <= 32 and W >= 16, the
+    halo form: three shifted copies, taps one image row apart — split-K
+    partials reduced in fixed order) against the
     float64 torch weight gradient of conv2d on the same bf16 values, in the
     GEMM weight layout [9·Cin, Cout]; deterministic across runs.  Includes the
     ResNet-32 bench geometries at batch 128."""
@@ -129,22 +134,33 @@ def test_implicit_conv3x3_wgrad_matches_torch(N, H, Cin, Cout):
     ref = wt.grad.permute(2, 3, 1, 0).reshape(9 * Cin, Cout)
     # exclusive GPU: the wide split-K form; shared GPU: one cluster with the
     # DSMEM reduction in-kernel
-    for exclusive in (1, 0):
-        prev = lib.ppll_set_gpu_exclusive(exclusive)
-        try:
-            outs = []
-            for _ in range(2):
-                dw = torch.full((9 * Cin, Cout), float("nan"), device="cuda")
-                N_.check(lib.ppll_conv3x3_wgrad_bf16(N, H, H, Cin, Cout, x.data_ptr(),
-                                                     dz.data_ptr(), dw.data_ptr(), ws.data_ptr(),
-                                                     nws, s), "conv wgrad")
-                torch.cuda.synchronize()
-                outs.append(dw.clone())
-        finally:
-            lib.ppll_set_gpu_exclusive(prev)
-        assert torch.equal(outs[0], outs[1]), exclusive
-        err = (outs[0].double() - ref).abs().max().item() / (ref.abs().max().item() + 1e-12)
-        assert err < 1e-4, (exclusive, err)
+    # PPLL_CONV_WGRAD_HALO: 0 tap windows, 2 halo copies wherever the shape allows
+    # (the default, 1, picks per form); read by the library on every call
+    old_env = os.environ.get("PPLL_CONV_WGRAD_HALO")
+    try:
+        for halo in ("0", "2"):
+            os.environ["PPLL_CONV_WGRAD_HALO"] = halo
+            for exclusive in (1, 0):
+                prev = lib.ppll_set_gpu_exclusive(exclusive)
+                try:
+                    outs = []
+                    for _ in range(2):
+                        dw = torch.full((9 * Cin, Cout), float("nan"), device="cuda")
+                        N_.check(lib.ppll_conv3x3_wgrad_bf16(N, H, H, Cin, Cout, x.data_ptr(),
+                                                             dz.data_ptr(), dw.data_ptr(),
+                                                             ws.data_ptr(), nws, s), "conv wgrad")
+                        torch.cuda.synchronize()
+                        outs.append(dw.clone())
+                finally:
+                    lib.ppll_set_gpu_exclusive(prev)
+                assert torch.equal(outs[0], outs[1]), (halo, exclusive)
+                err = (outs[0].double() - ref).abs().max().item() / (ref.abs().max().item() + 1e-12)
+                assert err < 1e-4, (halo, exclusive, err)
+    finally:
+        if old_env is None:
+            os.environ.pop("PPLL_CONV_WGRAD_HALO", None)
+        else:
+            os.environ["PPLL_CONV_WGRAD_HALO"] = old_env
 
 
 @pytest.mark.parametrize("N,H,Cin,Cout", [(4, 32, 16, 16), (2, 16, 32, 32), (4, 8, 64, 64),
