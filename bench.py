@@ -1268,7 +1268,10 @@ def main():
     if wl["kind"] == "vit":
         roof = _guard("roofline_gemm", roofline_gemm, wl, tf_burst, hbm, dev)
         roof_extra = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
-        roof_attn = _guard("roofline_attention", roofline_attention, wl, hbm, dev)
+        with ClockSampler(local) as clk_attn:   # the attention entry is latency-bound: clock-sensitive
+            roof_attn = _guard("roofline_attention", roofline_attention, wl, hbm, dev)
+        if isinstance(roof_attn, dict):
+            roof_attn["clocks"] = clk_attn.summary()
     elif wl["kind"] == "resnet" and args.precision == "bf16":
         roof = _guard("roofline_conv", roofline_conv, wl, tf_burst, hbm, dev)
         roof_extra = _guard("roofline_nesterov", roofline_nesterov, mods, hbm, dev)
