@@ -678,7 +678,9 @@ def roofline_nesterov(mods, hbm, dev):
     per = 20 + (2 if lpb is not None else 0)
     return {"kernel": "nesterov_kernel (fused Nesterov-SGD over the largest stage's flat "
                       "parameter buffer)", "bound": "hbm", "achieved": n * per / dt / 1e9,
-            "peak": hbm, "unit": "GB/s", "frac": n * per / dt / 1e9 / hbm, "traffic": None,
+            "peak": hbm, "unit": "GB/s", "frac": n * per / dt / 1e9 / hbm,
+            # the committed capture is of ResNet-32's largest stage (373,056 params)
+            "traffic": _traffic_of("nesterov_kernel") if (n == 373056 and lpb is not None) else None,
             "algorithmic_bytes_per_launch": n * per, "params": n, "bytes_per_param": per,
             "launch_us": dt * 1e6}
 
@@ -700,6 +702,7 @@ def roofline_attention(wl, hbm, dev, sets=4, reps=5):
     H = sp["heads"]
     D = 64 * H
     M = B * T
+    geo_vit_s = (B, T, H) == (128, 65, 6)   # the geometry of profiles/r02_ncu_traffic.csv
     lib = N.load()
     bufs = []
     for _ in range(sets):
@@ -755,11 +758,14 @@ def roofline_attention(wl, hbm, dev, sets=4, reps=5):
                       "layer's attention backward), back-to-back launches over "
                       f"{sets} input sets (> L2) from one CUDA graph",
             "bound": "hbm", "achieved": by_b / t_b / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": by_b / t_b / 1e9 / hbm, "traffic": None,
+            "frac": by_b / t_b / 1e9 / hbm,
+            "traffic": _traffic_of("attn_tc_bwd") if geo_vit_s else None,
+            "traffic_source": "profiles/r02_ncu_traffic.csv (ViT-S geometry only)",
             "algorithmic_bytes_per_launch": by_b, "launch_us": t_b * 1e6,
             "geometry": {"batch": B, "tokens": T, "heads": H, "head_dim": 64},
             "forward": {"kernel": "attn_tc_fwd_kernel", "achieved": by_f / t_f / 1e9,
                         "frac": by_f / t_f / 1e9 / hbm, "algorithmic_bytes_per_launch": by_f,
+                        "traffic": _traffic_of("attn_tc_fwd") if geo_vit_s else None,
                         "launch_us": t_f * 1e6},
             "warm_l2": {"how": "same graph on one input set (L2-resident inputs)",
                         "bwd_launch_us": w_b * 1e6, "bwd_frac": by_b / w_b / 1e9 / hbm,
@@ -855,6 +861,43 @@ def _ncu_traffic(tag):
         return [vals[k] for k in sorted(vals)]
     except Exception:
         return None
+
+
+def _ncu_launch_traffic(fname="r02_ncu_traffic.csv"):
+    """[(kernel name, dram read + write bytes)] per launch, in launch order, from
+    a committed `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` CSV
+    (profiles/r02_ncu_traffic.csv: tools/traffic_probe.py, one launch of each
+    roofline kernel at the bench geometry, caches flushed before each)."""
+    path = os.path.join(ROOT, "profiles", fname)
+    try:
+        import csv
+        rows = [r for r in csv.reader(open(path)) if len(r) > 12]
+        hdr = next(r for r in rows if "Metric Name" in r)
+        vals, names = {}, {}
+        for r in rows:
+            if r is hdr:
+                continue
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                continue
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(d["Metric Unit"], 1)
+            key = int(d["ID"])
+            names[key] = d.get("Kernel Name", "")
+            vals[key] = vals.get(key, 0.0) + float(d["Metric Value"].replace(",", "")) * scale
+        return [(names[k], vals[k]) for k in sorted(vals)]
+    except Exception:
+        return []
+
+
+def _traffic_of(substr, nth=None):
+    """Traffic of the launches whose kernel name contains `substr` (the nth, or
+    the mean over all of them); None when the capture holds none."""
+    hits = [b for n, b in _ncu_launch_traffic() if substr in n]
+    if not hits:
+        return None
+    if nth is not None:
+        return hits[nth] if nth < len(hits) else None
+    return sum(hits) / len(hits)
 
 
 def gemm_sequence(gemms, dev, reps=20):
@@ -1056,6 +1099,7 @@ def roofline_conv(wl, tf_burst, hbm, dev):
     B = wl["batch"]
     table, tot_t, tot_b, tot_f = [], 0.0, 0.0, 0.0
     wg_t, wg_b = 0.0, 0.0
+    trs = []
     nws = lib.ppll_conv3x3_wgrad_ws_floats(B, 32, 32, 64, 64)
     ws = torch.empty(nws, device=dev)
     for C, H in zip(wl["spec"]["widths"], (32, 16, 8)):
@@ -1075,7 +1119,11 @@ def roofline_conv(wl, tf_burst, hbm, dev):
         dtw = _graph_per_launch(wgr, dev)
         fl, by = 2.0 * P * 9 * C * C, 2.0 * (2 * P * C + 9 * C * C)
         byw = 2.0 * 2 * P * C + 4.0 * 9 * C * C
+        # ncu DRAM bytes of this shape (tools/traffic_probe.py captures batch 128)
+        tr = _traffic_of("conv3x3_tc_kernel", len(table)) if B == 128 else None
+        trs.append(tr)
         table.append({"conv": f"{C}->{C} 3x3 @ {H}x{H}, batch {B}", "us": round(dt * 1e6, 2),
+                      "traffic": tr, "algorithmic_bytes": by,
                       "gbs": round(by / dt / 1e9, 1), "tflops": round(fl / dt / 1e12, 1),
                       "hbm_frac": round(by / dt / 1e9 / hbm, 3),
                       "wgrad_us": round(dtw * 1e6, 2), "wgrad_gbs": round(byw / dtw / 1e9, 1),
@@ -1089,7 +1137,10 @@ def roofline_conv(wl, tf_burst, hbm, dev):
     return {"kernel": "conv3x3_tc_kernel (implicit-GEMM tcgen05 conv, TMA 4-D window gathers), "
                       "the three CIFAR stage resolutions, back-to-back launches from HBM",
             "bound": "hbm", "achieved": tot_b / tot_t / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": tot_b / tot_t / 1e9 / hbm, "traffic": None,
+            "frac": tot_b / tot_t / 1e9 / hbm,
+            "traffic": (sum(trs) / len(trs) if trs and all(t is not None for t in trs) else None),
+            "traffic_source": "profiles/r02_ncu_traffic.csv (ncu dram__bytes_read.sum + "
+                              "dram__bytes_write.sum per launch, caches flushed; batch 128)",
             "algorithmic_bytes_per_launch": tot_b / 3, "algorithmic_flops_per_launch": tot_f / 3,
             "tflops": tot_f / tot_t / 1e12, "launch_us": tot_t / 3 * 1e6, "per_conv": table,
             "weight_gradient": {"kernel": "conv3x3_wgrad_tc_kernel (implicit GEMM, wide split-K "
