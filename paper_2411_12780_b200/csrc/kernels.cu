@@ -517,6 +517,243 @@ template int launch_softmax_xent<float>(int, int, const float*, int, const int64
 template int launch_softmax_xent<__nv_bfloat16>(int, int, const __nv_bfloat16*, int, const int64_t*, __nv_bfloat16*, int, float*, const int*, int*, cudaStream_t);
 
 // ------------------------------------------------------------------------
+// Fused classifier head of a local step (blocks.py:280-285 for the head's
+// Linear + softmax_xent, tensor.py:137-150 / 201-234), one warp per row:
+//   logits = z·W + b            (the rowwarp GEMM's arithmetic and order:
+//                                lane-strided K, fmaf, xor-tree warp sum)
+//   loss, dlog = softmax_xent   (the softmax_xent kernel's arithmetic on the
+//                                stored logits; same fixed-order batch mean)
+//   dz = dlog·Wᵀ                (the gemm_dot kernel's four FMA chains)
+// so logits, dlog, dz and the loss are bitwise what the three separate
+// launches produce, with two launches and their dependent latencies off the
+// critical path of every stage step.  One 8-CTA cluster (rows split over the
+// CTAs, 16 warps each): every CTA stages W [K, C] (the reference's (fan_in,
+// fan_out) layout) in shared memory as fp32 [K][NP+1] with 16-B loads while
+// its warps' row loads (all of a row's lane-strided elements, issued at once)
+// are in flight; the row losses stay in each CTA's shared memory and rank 0
+// gathers them over DSMEM in the fixed order of the batch mean.
+// ------------------------------------------------------------------------
+constexpr int kHeadCluster = 8, kHeadWarps = 16, kHeadMaxT = 24;   // K <= 768 in registers
+
+__device__ __forceinline__ float ld_dsmem_f32(const float* p, uint32_t rank) {
+  uint32_t ra, a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+  return v;
+}
+__device__ __forceinline__ void head_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+template <typename T, int NP>
+__global__ void __launch_bounds__(kHeadWarps * 32)
+head_xent_kernel(int B, int K, int C, const T* __restrict__ z, int ldz, const T* __restrict__ W,
+                 const float* __restrict__ bias, const int64_t* __restrict__ y,
+                 T* __restrict__ logits, T* __restrict__ dlog, T* __restrict__ dz, int lddz,
+                 float* loss_hist, const int* step, int* err) {
+  constexpr int LD = NP + 1;
+  extern __shared__ float hsm[];
+  const int rank = (int)(blockIdx.x % kHeadCluster);
+  const int rpc = (B + kHeadCluster - 1) / kHeadCluster;   // rows of this CTA: [rank·rpc, +rpc)
+  float* ws = hsm;                                          // [K][LD]
+  float* row_loss = ws + (size_t)K * LD;                    // [rpc]
+  T* rowbuf = reinterpret_cast<T*>(row_loss + rpc);         // per warp: logits[32] | dlog[32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r0 = rank * rpc, r1 = min(B, r0 + rpc);
+  pdl_entry();
+  // first row of this warp: every lane-strided element loaded before W is staged
+  int r = r0 + w;
+  float av[kHeadMaxT];
+  auto load_row = [&](int row) {
+    const T* zr = z + (long)row * ldz;
+#pragma unroll
+    for (int t = 0; t < kHeadMaxT; ++t) {
+      const int k = lane + 32 * t;
+      av[t] = (row < r1 && k < K) ? to_f(zr[k]) : 0.f;
+    }
+  };
+  load_row(r);
+  // W [K, C] contiguous: 16-B vectors when aligned, scattered into [K][LD]
+  const long nW = (long)K * C;
+  constexpr int V = 16 / sizeof(T);
+  if ((reinterpret_cast<uintptr_t>(W) & 15) == 0 && nW % V == 0) {
+    for (long v = threadIdx.x; v < nW / V; v += blockDim.x) {
+      const uint4 q = reinterpret_cast<const uint4*>(W)[v];
+      const T* e = reinterpret_cast<const T*>(&q);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const long idx = v * V + i;
+        ws[(idx / C) * LD + idx % C] = to_f(e[i]);
+      }
+    }
+  } else {
+    for (long idx = threadIdx.x; idx < nW; idx += blockDim.x) ws[(idx / C) * LD + idx % C] = to_f(W[idx]);
+  }
+  if (C < NP)
+    for (int i = threadIdx.x; i < K * (NP - C); i += blockDim.x)
+      ws[(i / (NP - C)) * LD + C + i % (NP - C)] = 0.f;
+  __syncthreads();
+  T* lg = rowbuf + w * 64;
+  T* dl = lg + 32;
+  const float invB = 1.0f / (float)B;
+  const int sl = lane & 15, seg = lane >> 4;
+  for (; r < r1; r += kHeadWarps) {
+    // ---- logits row r ----
+    float acc[NP];
+#pragma unroll
+    for (int n = 0; n < NP; ++n) acc[n] = 0.f;
+#pragma unroll
+    for (int t = 0; t < kHeadMaxT; ++t) {
+      const int k = lane + 32 * t;
+      if (k < K) {
+        const float* br = ws + k * LD;
+#pragma unroll
+        for (int n = 0; n < NP; ++n) acc[n] = fmaf(av[t], br[n], acc[n]);
+      }
+    }
+    for (int k = lane + 32 * kHeadMaxT; k < K; k += 32) {   // K > 768: the rest streamed
+      const float a = to_f(z[(long)r * ldz + k]);
+      const float* br = ws + k * LD;
+#pragma unroll
+      for (int n = 0; n < NP; ++n) acc[n] = fmaf(a, br[n], acc[n]);
+    }
+    if (r + kHeadWarps < r1) load_row(r + kHeadWarps);   // next row's loads under this row's math
+#pragma unroll
+    for (int n = 0; n < NP; ++n) acc[n] = warp_sum(acc[n]);
+    float mine = 0.f;
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+      if (lane == n) mine = acc[n];
+    if (lane < C) {
+      float v = mine;
+      if (bias) v += bias[lane];
+      DT<T>::st(lg + lane, v);
+      DT<T>::st(logits + (long)r * C + lane, v);
+    }
+    __syncwarp();
+    // ---- softmax_xent on the stored row (half-warp arithmetic of softmax_xent_kernel;
+    //      both halves evaluate the row, the lower half writes) ----
+    const long lab = y[r];
+    const bool bad = (lab < 0 || lab >= C);
+    float mx = -INFINITY;
+    for (int c = sl; c < C; c += 16) mx = fmaxf(mx, to_f(lg[c]));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.f, zl = 0.f;
+    for (int c = sl; c < C; c += 16) {
+      const float v = to_f(lg[c]);
+      se += __expf(v - mx);
+      if (c == lab) zl = v;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      se += __shfl_xor_sync(0xffffffffu, se, o);
+      zl += __shfl_xor_sync(0xffffffffu, zl, o);
+    }
+    const float inv = 1.0f / se;
+    if (seg == 0) {
+      for (int c = sl; c < C; c += 16) {
+        const float p = __expf(to_f(lg[c]) - mx) * inv;
+        const float g = bad ? 0.f : (p - (c == lab ? 1.f : 0.f)) * invB;
+        DT<T>::st(dl + c, g);
+        DT<T>::st(dlog + (long)r * C + c, g);
+      }
+      if (sl == 0) {
+        row_loss[r - r0] = bad ? 0.f : -((zl - mx) - logf(se));
+        if (bad && err) atomicOr(err, kErrLabel);
+      }
+    }
+    __syncwarp();
+    // ---- dz row r = dlog[r]·Wᵀ (gemm_dot's chains: k ≡ 0,1,2,3 mod 4) ----
+    T* dzr = dz + (long)r * lddz;
+    for (int n = lane; n < K; n += 32) {
+      const float* wr = ws + n * LD;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      int k = 0;
+      for (; k + 4 <= C; k += 4) {
+        a0 = fmaf(to_f(dl[k]), wr[k], a0);
+        a1 = fmaf(to_f(dl[k + 1]), wr[k + 1], a1);
+        a2 = fmaf(to_f(dl[k + 2]), wr[k + 2], a2);
+        a3 = fmaf(to_f(dl[k + 3]), wr[k + 3], a3);
+      }
+      for (; k < C; ++k) a0 = fmaf(to_f(dl[k]), wr[k], a0);
+      DT<T>::st(dzr + n, (a0 + a1) + (a2 + a3));
+    }
+    __syncwarp();
+  }
+  head_cluster_sync();   // every CTA's row losses are in its shared memory
+  if (rank == 0 && w == 0) {   // the softmax_xent kernel's fixed-order batch mean
+    double s = 0.0;
+    for (int q = lane; q < B; q += 32) s += (double)ld_dsmem_f32(row_loss + q % rpc, q / rpc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const float loss = (float)(s / (double)B);
+      loss_hist[step ? *step : 0] = loss;
+      if (!isfinite(loss) && err) atomicOr(err, kErrLossNonFinite);
+    }
+  }
+  head_cluster_sync();   // peers keep their shared memory until rank 0 has read it
+}
+
+static size_t head_xent_smem(int B, int K, int np, size_t esz) {
+  const int rpc = (B + kHeadCluster - 1) / kHeadCluster;
+  return sizeof(float) * ((size_t)K * (np + 1) + (size_t)rpc) + kHeadWarps * 64 * esz;
+}
+
+bool head_xent_fusable(int B, int K, int C, size_t esz) {
+  static const int on = getenv("PPLL_HEAD_FUSED") ? atoi(getenv("PPLL_HEAD_FUSED")) : 1;
+  return on && C >= 1 && C <= 32 && K >= 64 && B >= 1 &&
+         head_xent_smem(B, K, C <= 16 ? 16 : 32, esz) <= 200 * 1024;
+}
+
+template <typename T, int NP>
+static int head_xent_go(int B, int K, int C, const T* z, int ldz, const T* W, const float* bias,
+                        const int64_t* y, T* logits, T* dlog, T* dz, int lddz, float* loss_hist,
+                        const int* step, int* err, cudaStream_t s) {
+  auto kern = head_xent_kernel<T, NP>;
+  static bool set = false;
+  if (!set) {
+    PPLL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kHeadCluster);
+  cfg.blockDim = dim3(kHeadWarps * 32);
+  cfg.dynamicSmemBytes = head_xent_smem(B, K, NP, sizeof(T));
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kHeadCluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  PPLL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, B, K, C, z, ldz, W, bias, y, logits, dlog, dz,
+                                     lddz, loss_hist, step, err));
+  return PPLL_OK;
+}
+
+template <typename T>
+int launch_head_xent(int B, int K, int C, const T* z, int ldz, const T* W, const float* bias,
+                     const int64_t* y, T* logits, T* dlog, T* dz, int lddz, float* loss_hist,
+                     const int* step, int* err, cudaStream_t s) {
+  if (!head_xent_fusable(B, K, C, sizeof(T))) return PPLL_ERR_UNSUPPORTED;
+  const int r = C <= 16 ? head_xent_go<T, 16>(B, K, C, z, ldz, W, bias, y, logits, dlog, dz, lddz,
+                                              loss_hist, step, err, s)
+                        : head_xent_go<T, 32>(B, K, C, z, ldz, W, bias, y, logits, dlog, dz, lddz,
+                                              loss_hist, step, err, s);
+  if (r) return r;
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template int launch_head_xent<float>(int, int, int, const float*, int, const float*, const float*, const int64_t*, float*, float*, float*, int, float*, const int*, int*, cudaStream_t);
+template int launch_head_xent<__nv_bfloat16>(int, int, int, const __nv_bfloat16*, int, const __nv_bfloat16*, const float*, const int64_t*, __nv_bfloat16*, __nv_bfloat16*, __nv_bfloat16*, int, float*, const int*, int*, cudaStream_t);
+
+// ------------------------------------------------------------------------
 // Nesterov-SGD over one flat buffer (optim.py:81-88):
 //   g' = g + wd·θ ; v = μv + g' ; θ -= lr·(g' + μv)
 // 20 B/param algorithmic (read θ,v,g; write θ,v) + 2 B for the bf16 shadow.

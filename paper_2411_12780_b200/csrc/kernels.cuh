@@ -847,6 +847,15 @@ template <typename T>
 int launch_softmax_xent(int B, int C, const T* z, int ldz, const int64_t* y, T* dz, int lddz,
                         float* loss_hist, const int* step, int* err, cudaStream_t s);
 
+// fused classifier head of a local step: logits = z·W + b, softmax_xent
+// (loss, dlog) and dz = dlog·Wᵀ in one launch, bitwise equal to the three
+// separate kernels; PPLL_ERR_UNSUPPORTED outside C <= 32, K >= 64
+bool head_xent_fusable(int B, int K, int C, size_t esz);
+template <typename T>
+int launch_head_xent(int B, int K, int C, const T* z, int ldz, const T* W, const float* bias,
+                     const int64_t* y, T* logits, T* dlog, T* dz, int lddz, float* loss_hist,
+                     const int* step, int* err, cudaStream_t s);
+
 // advance = false: update only (the step counter is advanced by the step's
 // last launch, after every range has read it)
 int set_local_optimizer(const float* theta, int kind, float* m2, float beta1, float beta2,

@@ -276,7 +276,7 @@ static int conv_bwd(ppll_resnet_stage* st, ConvBN& c, int B, int slot, int64_t w
 
 template <typename TT>
 static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_out, bool head,
-                       cudaStream_t s, bool with_aux = true) {
+                       cudaStream_t s, bool with_aux = true, bool defer_logits = false) {
   NvtxRange nv("ppll.resnet.forward");
   const void* x = x_in;
   int r;
@@ -322,6 +322,8 @@ static int res_forward(ppll_resnet_stage* st, int B, const void* x_in, void* x_o
   }
   r = launch_gap<TT>(B, st->h_out * st->h_out, st->c_out, (const TT*)x, (TT*)st->pooled, s);
   if (r) return r;
+  // a backward follows: the fused head kernel computes the logits there
+  if (defer_logits && head_xent_fusable(B, st->c_out, st->classes, st->esz)) return PPLL_OK;
   LinOpts oh;
   oh.bias = st->P(st->head_off[1]);
   return gemm_fwd(B, st->c_out, st->classes, st->pooled, st->c_out, st->W(st->head_off[0]), oh,
@@ -352,8 +354,16 @@ static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, con
     PPLL_CUDA_CHECK(cudaMemcpyAsync(dx, g_out, (size_t)B * HW * C * st->esz,
                                     cudaMemcpyDeviceToDevice, s));
   } else {
-    r = launch_softmax_xent<TT>(B, st->classes, (const TT*)st->logits, st->classes, labels,
-                                (TT*)st->dlog, st->classes, st->loss_hist, st->step, st->err, s);
+    const bool fused = head_xent_fusable(B, C, st->classes, st->esz);
+    if (fused) {   // logits + softmax_xent + dp in one launch (the forward deferred the logits)
+      r = launch_head_xent<TT>(B, C, st->classes, (const TT*)st->pooled, C,
+                               (const TT*)st->W(st->head_off[0]), st->P(st->head_off[1]), labels,
+                               (TT*)st->logits, (TT*)st->dlog, (TT*)st->dp, C, st->loss_hist,
+                               st->step, st->err, s);
+    } else {
+      r = launch_softmax_xent<TT>(B, st->classes, (const TT*)st->logits, st->classes, labels,
+                                  (TT*)st->dlog, st->classes, st->loss_hist, st->step, st->err, s);
+    }
     if (r) return r;
     // head
     bs.sf.fork();
@@ -362,9 +372,11 @@ static int res_backward(ppll_resnet_stage* st, int B, const int64_t* labels, con
                      st->ws_elems, bs.sf.ss);
     if (r) return r;
     LinOpts none;
-    r = gemm_dgrad(B, C, st->classes, st->dlog, st->classes, st->W(st->head_off[0]), none,
-                   st->dp, C, st->dtype, st->ws, st->ws_elems, s);
-    if (r) return r;
+    if (!fused) {
+      r = gemm_dgrad(B, C, st->classes, st->dlog, st->classes, st->W(st->head_off[0]), none,
+                     st->dp, C, st->dtype, st->ws, st->ws_elems, s);
+      if (r) return r;
+    }
     r = launch_gap_bwd<TT>(B, HW, C, (const TT*)st->dp, (TT*)dx, s);
     if (r) return r;
   }
@@ -448,7 +460,7 @@ static int res_update(ppll_resnet_stage* st, int64_t n, cudaStream_t s) {
 template <typename TT>
 static int res_step(ppll_resnet_stage* st, int B, const void* x_in, const int64_t* labels,
                     void* x_out, cudaStream_t s) {
-  int r = res_forward<TT>(st, B, x_in, x_out, true, s);
+  int r = res_forward<TT>(st, B, x_in, x_out, true, s, true, true);
   if (r) return r;
   r = res_backward<TT>(st, B, labels, nullptr, nullptr, true, s);
   if (r) return r;
@@ -613,8 +625,8 @@ int ppll_resnet_stage_block_forward(ppll_resnet_stage* st, int B, const void* x_
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool head = h_out == nullptr;
-  return st->dtype == PPLL_F32 ? res_forward<float>(st, B, x_in, h_out, head, s, false)
-                               : res_forward<__nv_bfloat16>(st, B, x_in, h_out, head, s, false);
+  return st->dtype == PPLL_F32 ? res_forward<float>(st, B, x_in, h_out, head, s, false, true)
+                               : res_forward<__nv_bfloat16>(st, B, x_in, h_out, head, s, false, true);
 }
 
 // Backward through the block from `g_out` = dLoss/d(block output), or — final

@@ -115,7 +115,7 @@ static int attn_bwd_any(int B, int T, int H, int dh, const TT* qkv, const TT* o,
 
 template <typename TT>
 static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out, bool head,
-                       cudaStream_t s, int nl = -1) {
+                       cudaStream_t s, int nl = -1, bool defer_logits = false) {
   NvtxRange nv("ppll.vit.forward");
   if (nl < 0) nl = st->layers();
   const int T = st->T, D = st->D, F = st->F, H = st->H;
@@ -196,6 +196,9 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
   r = launch_ln_fwd<TT>(B, D, xcur, (long)T * D, st->P(st->ho(0)), st->P(st->ho(1)), (TT*)st->zc,
                         D, st->meanf, st->rstdf, s);
   if (r) return r;
+  // a backward follows (local step / E2E final stage): the fused head kernel
+  // computes the logits there, together with the loss and dz
+  if (defer_logits && head_xent_fusable(B, D, st->C, st->esz)) return PPLL_OK;
   LinOpts oh;
   oh.bias = st->P(st->ho(3));
   return gemm_fwd(B, D, st->C, st->zc, D, st->W(st->ho(2)), oh, st->logits, st->C, st->dtype,
@@ -237,8 +240,16 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
   } caps(sf.on(), dcap, wcap);
   auto slab = [&]() { return st->ln_parts + st->ln_slab * (size_t)(nslab++); };
   if (labels) {
-    r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
-                                st->loss_hist, st->step, st->err, s);
+    // logits + softmax_xent + dz in one launch (the forward deferred the logits)
+    const bool fused = head_xent_fusable(B, D, C, st->esz);
+    if (fused) {
+      r = launch_head_xent<TT>(B, D, C, (const TT*)st->zc, D, (const TT*)st->W(st->ho(2)),
+                               st->P(st->ho(3)), labels, (TT*)st->logits, (TT*)st->dlog,
+                               (TT*)st->dz, D, st->loss_hist, st->step, st->err, s);
+    } else {
+      r = launch_softmax_xent<TT>(B, C, (const TT*)st->logits, C, labels, (TT*)st->dlog, C,
+                                  st->loss_hist, st->step, st->err, s);
+    }
     if (r) return r;
     const TT* xlast = (const TT*)st->L[nl - 1].x2;
     // ---- head backward ----
@@ -246,9 +257,11 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     r = linear_wgrad(B, D, C, st->zc, D, st->dlog, C, st->G(st->ho(2)), st->G(st->ho(3)),
                      st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
-    r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
-                   st->ws_elems, s);
-    if (r) return r;
+    if (!fused) {
+      r = gemm_dgrad(B, D, C, st->dlog, C, st->W(st->ho(2)), none, st->dz, D, st->dtype, st->ws,
+                     st->ws_elems, s);
+      if (r) return r;
+    }
     r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, (long)T * D, st->meanf, st->rstdf,
                           st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, slab(),
                           st->G(st->ho(0)), st->G(st->ho(1)), s, nullptr, &dfr);
@@ -402,7 +415,7 @@ static int vit_update(ppll_vit_stage* st, int64_t n, cudaStream_t s) {
 template <typename TT>
 static int vit_step(ppll_vit_stage* st, int B, const void* x_in, const int64_t* labels,
                     void* x_out, cudaStream_t s) {
-  int r = vit_forward<TT>(st, B, x_in, x_out, true, s);
+  int r = vit_forward<TT>(st, B, x_in, x_out, true, s, -1, true);
   if (r) return r;
   r = vit_backward<TT>(st, B, x_in, labels, nullptr, nullptr, st->layers(), s);
   if (r) return r;
@@ -538,8 +551,8 @@ int ppll_vit_stage_block_forward(ppll_vit_stage* st, int B, const void* x_in, vo
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool head = h_out == nullptr;
   return st->dtype == PPLL_F32
-             ? vit_forward<float>(st, B, x_in, h_out, head, s, st->n_block)
-             : vit_forward<__nv_bfloat16>(st, B, x_in, h_out, head, s, st->n_block);
+             ? vit_forward<float>(st, B, x_in, h_out, head, s, st->n_block, true)
+             : vit_forward<__nv_bfloat16>(st, B, x_in, h_out, head, s, st->n_block, true);
 }
 
 // Backward through the block from dLoss/d(block output) `g_out`, or — final
