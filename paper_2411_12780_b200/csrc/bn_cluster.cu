@@ -228,11 +228,13 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* err) {
 }
 template <bool GRID>
 __device__ __forceinline__ float4 merge_partials(const float4* cpart, float4* scratch, int C,
-                                                 float4* gpart, unsigned* gbar, int* err) {
+                                                 float4* gpart, unsigned* gbar, int* err,
+                                                 unsigned long long* tl = nullptr) {
   const int t = threadIdx.x;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if constexpr (!GRID) {
     cluster_sync();   // every CTA's partial sums are in its shared memory
+    if (tl && t == 0) tl[blockIdx.x * 8 + 7] = gtimer();
     if (t < C) {
       const int CS = (int)cluster_nctarank();
       const uint32_t la = smem_u32(&cpart[t]);
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) bn_fwd_cluster_kernel(const __gri
   } else if constexpr (SPLIT == 2) {
     sacc = split_partial_in(C, a.gpart, a.ncl);
   } else {
-    sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err);
+    sacc = merge_partials<GRID>(cpart, wred, C, a.gpart, a.gbar, a.err, a.tl);
   }
   if (t < C) {
     const float invP = 1.f / (float)a.P;
@@ -792,7 +794,14 @@ static int fused_mode(long P, int C, bool bwd, bool grid_ok) {
   static const double bwd_mb = getenv("PPLL_BN_BWD_MAX_MB") ? atof(getenv("PPLL_BN_BWD_MAX_MB")) : 1.2;
   static const double grid_mb = getenv("PPLL_BN_GRID_MAX_MB") ? atof(getenv("PPLL_BN_GRID_MAX_MB")) : 64.0;
   if (off || C % 8 || C > kMaxC || kThreads % (C / 8) || P < 1 || P > (1L << 30) / C) return 0;
+  // a stage that owns its GPU: the full-GPU grid form beats the 16-SM cluster
+  // form above ~1 MB (ResNet-32 stage steps 472 -> 462 / 392 -> 376 µs with the
+  // forward threshold at 1.0 MB, tools/prof_gaps.py; 0.5 MB and below slower)
+  static const double excl_mb = getenv("PPLL_BN_EXCL_MAX_MB") ? atof(getenv("PPLL_BN_EXCL_MAX_MB")) : 1.0;
   const double mb = (double)P * C * 2 / 1048576.0;
+  // (explicit PPLL_BN_FWD_MAX_MB / PPLL_BN_BWD_MAX_MB keep the old thresholds)
+  static const bool thr_env = getenv("PPLL_BN_FWD_MAX_MB") || getenv("PPLL_BN_BWD_MAX_MB");
+  if (!thr_env && g_gpu_excl && grid_ok && mb > excl_mb && mb <= grid_mb) return 2;
   // split form off by default: its 144 one-per-SM CTAs (~200 KB smem) crowd out the other
   // stage streams — ResNet-32 pipeline 132.8k -> 111.3k img/s (PPLL_BN_SPLIT=1 enables)
   static const int split_on = getenv("PPLL_BN_SPLIT") ? atoi(getenv("PPLL_BN_SPLIT")) : 0;

@@ -21,7 +21,7 @@ ws = torch.empty(lib.ppll_batchnorm_ws_floats(P, C), device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 lib.ppll_gemm_timeline.restype = ctypes.c_void_p
 buf = lib.ppll_gemm_timeline()
-names = ["entry", "pdl", "stats", "cta-merge", "cl-merge", "apply", "exit"]
+names = ["entry", "pdl", "stats", "cta-merge", "cl-merge", "apply", "exit", "cl-sync"]
 for which in ("fwd", "bwd"):
     for it in range(3):
         if which == "fwd":
@@ -39,7 +39,7 @@ for which in ("fwd", "bwd"):
     host = np.zeros(16 * 8, dtype=np.uint64)
     import cuda.bindings.runtime as rt  # noqa
     rt.cudaMemcpy(host.ctypes.data, buf, host.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
-    a = host.reshape(16, 8)[:, :7].astype(np.float64)
+    a = host.reshape(16, 8)[:, :8].astype(np.float64)
     a = a[a[:, 0] > 0]
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3

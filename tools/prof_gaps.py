@@ -69,3 +69,8 @@ print(f"{fam} stage {j}: graph replay {step_ms * 1e3:.1f} us/step (events), {len
       f"(median {np.median(gaps):.2f} us)")
 for k, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1])[:25]:
     print(f"{t / busy * 100:5.1f}%  {c:4d}  {t / c:7.2f} us  {k}")
+if os.environ.get("TIMELINE"):   # every kernel of the middle replay: start / end offsets
+    t0 = ev[0].time_range.start
+    for e in ev:
+        print(f"  {e.time_range.start - t0:8.1f} {e.time_range.end - t0:8.1f} "
+              f"{e.time_range.elapsed_us():7.1f}  {e.name.split('(')[0][:60]}")
