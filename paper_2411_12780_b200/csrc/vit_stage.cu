@@ -64,6 +64,8 @@ struct ppll_vit_stage {
   std::vector<cudaEvent_t> ev;
   float* ws2 = nullptr;
   std::vector<void*> allocs;
+  // the last forward ran its top layer on the cls rows only (see vit_forward)
+  bool cls_top = false;
 
   int layers() const { return n_block + n_aux; }
   int64_t po(int layer, int k) const { return off[4 + layer * kLayerParams + k]; }
@@ -122,6 +124,18 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
   const int M = B * T;
   const TT* xcur = reinterpret_cast<const TT*>(x_in);
   int r;
+  // Top layer on the cls rows only: when the stage's last layer feeds nothing
+  // but the head (an aux stack's last layer, or the final stage's last block
+  // layer — not a layer whose output is pushed), only its cls rows reach the
+  // loss.  Its LN1 / QKV / attention still run over every token (the cls
+  // query attends to all keys and values), but the proj, LN2, FC1 and FC2
+  // work — and their backward — is needed for the B cls rows alone; the other
+  // rows' contributions to the loss and to every gradient are exactly zero.
+  // Same values for everything the step produces, ~80 % of the layer's GEMM
+  // work gone.  PPLL_VIT_CLS_TOP=0 runs the layer over all rows.
+  static const int cls_env = getenv("PPLL_VIT_CLS_TOP") ? atoi(getenv("PPLL_VIT_CLS_TOP")) : 1;
+  const bool cls_top = cls_env && head && nl >= 1 && !(nl - 1 == st->n_block - 1 && x_out);
+  st->cls_top = cls_top;
   if (st->has_patch) {
     const int P = T - 1, pd = st->img_c * st->patch * st->patch;
     r = launch_patchify<TT>(B, st->img_c, st->img_hw, st->patch, (const TT*)x_in, (TT*)st->patches, s);
@@ -148,6 +162,38 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     if (r) return r;
     r = attn_fwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
     if (r) return r;
+    if (cls_top && l == nl - 1) {
+      // cls rows only (row stride T·D in o and in the residual); x1, xn2, u,
+      // h, x2 hold B compact rows
+      const long ldt = (long)T * D;
+      LinOpts o2;
+      o2.bias = st->P(st->po(l, kBo));
+      o2.res = xcur;
+      o2.ldres = ldt;
+      r = gemm_fwd(B, D, D, b.o, ldt, st->W(st->po(l, kWo)), o2, b.x1, D, st->dtype, st->ws,
+                   st->ws_elems, s);
+      if (r) return r;
+      r = launch_ln_fwd<TT>(B, D, (const TT*)b.x1, D, st->P(st->po(l, kLn2g)),
+                            st->P(st->po(l, kLn2b)), (TT*)b.xn2, D, b.mean2, b.rstd2, s);
+      if (r) return r;
+      LinOpts o3;
+      o3.bias = st->P(st->po(l, kB1));
+      o3.act = kActGeluD;
+      o3.pre = b.u;
+      o3.ldpre = F;
+      r = gemm_fwd(B, D, F, b.xn2, D, st->W(st->po(l, kW1)), o3, b.h, F, st->dtype, st->ws,
+                   st->ws_elems, s);
+      if (r) return r;
+      LinOpts o4;
+      o4.bias = st->P(st->po(l, kB2));
+      o4.res = b.x1;
+      o4.ldres = D;
+      r = gemm_fwd(B, F, D, b.h, F, st->W(st->po(l, kW2)), o4, b.x2, D, st->dtype, st->ws,
+                   st->ws_elems, s);
+      if (r) return r;
+      xcur = (const TT*)b.x2;
+      continue;
+    }
     // proj (+bias, +residual) -> x1 and LN2 -> xn2: one fused launch for bf16
     // D = 384 (gemm_ln.cu), else the GEMM with its residual epilogue + LN kernel
     r = PPLL_ERR_UNSUPPORTED;
@@ -192,9 +238,10 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     xcur = (const TT*)b.x2;
   }
   if (!head) return PPLL_OK;
-  // head: LayerNorm on the cls rows (row stride T·D) + classifier
-  r = launch_ln_fwd<TT>(B, D, xcur, (long)T * D, st->P(st->ho(0)), st->P(st->ho(1)), (TT*)st->zc,
-                        D, st->meanf, st->rstdf, s);
+  // head: LayerNorm on the cls rows (row stride T·D; compact after a cls-only
+  // top layer) + classifier
+  r = launch_ln_fwd<TT>(B, D, xcur, cls_top ? (long)D : (long)T * D, st->P(st->ho(0)),
+                        st->P(st->ho(1)), (TT*)st->zc, D, st->meanf, st->rstdf, s);
   if (r) return r;
   // a backward follows (local step / E2E final stage): the fused head kernel
   // computes the logits there, together with the loss and dz
@@ -239,6 +286,7 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     ~CapScope() { g_gemm_cap = g0; g_wgrad_cap = w0; }
   } caps(sf.on(), dcap, wcap);
   auto slab = [&]() { return st->ln_parts + st->ln_slab * (size_t)(nslab++); };
+  const bool cls_top = labels && st->cls_top;   // the forward's choice
   if (labels) {
     // logits + softmax_xent + dz in one launch (the forward deferred the logits)
     const bool fused = head_xent_fusable(B, D, C, st->esz);
@@ -262,15 +310,20 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
                      st->ws_elems, s);
       if (r) return r;
     }
-    r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, (long)T * D, st->meanf, st->rstdf,
-                          st->P(st->ho(0)), nullptr, 0, (TT*)st->dzc, D, slab(),
-                          st->G(st->ho(0)), st->G(st->ho(1)), s, nullptr, &dfr);
+    // cls-only top layer: the head's input gradient IS the top layer's
+    // (compact, B rows) output gradient; else it is scattered to the cls rows
+    char* dhead = cls_top ? st->dxa : st->dzc;
+    r = launch_ln_bwd<TT>(B, D, (const TT*)st->dz, D, xlast, cls_top ? (long)D : (long)T * D,
+                          st->meanf, st->rstdf, st->P(st->ho(0)), nullptr, 0, (TT*)dhead, D,
+                          slab(), st->G(st->ho(0)), st->G(st->ho(1)), s, nullptr, &dfr);
     if (r) return r;
-    r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)st->dxa, s);
-    if (r) return r;
+    if (!cls_top) {
+      r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)st->dxa, s);
+      if (r) return r;
+    }
     // db2 of the top layer = Σ rows of its output gradient: only the cls rows
     // are non-zero (Σ of dz over the batch)
-    r = launch_colsum<TT>(B, D, (const TT*)st->dzc, D, st->G(st->po(nl - 1, kB2)), s, st->ws,
+    r = launch_colsum<TT>(B, D, (const TT*)dhead, D, st->G(st->po(nl - 1, kB2)), s, st->ws,
                           st->ws_elems);
     if (r) return r;
   } else {
@@ -292,8 +345,11 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     const void* xin_l = l > 0 ? (const void*)st->L[l - 1].x2
                               : (st->has_patch ? (const void*)st->x0 : x_in);
     // (db2 of layer l < top: fused into the LN1 backward of layer l+1)
+    // cls-only top layer: FC2 / FC1 / LN2 / proj over the B compact cls rows
+    const bool cls = cls_top && l == nl - 1;
+    const int Mr = cls ? B : M;
     sf.fork();
-    r = linear_wgrad(M, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, wsw,
+    r = linear_wgrad(Mr, F, D, b.h, F, dx2, D, st->G(st->po(l, kW2)), nullptr, st->dtype, wsw,
                      st->ws_elems, sf.ss);
     if (r) return r;
     const cudaEvent_t n_w2 = sf.mark();
@@ -302,12 +358,12 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     og.mask = b.u;
     og.ldmask = F;
     og.mask_mode = kMaskMul;
-    r = gemm_dgrad(M, F, D, dx2, D, st->W(st->po(l, kW2)), og, st->dbig, F, st->dtype, st->ws,
+    r = gemm_dgrad(Mr, F, D, dx2, D, st->W(st->po(l, kW2)), og, st->dbig, F, st->dtype, st->ws,
                    st->ws_elems, s);
     if (r) return r;
     // db1 = Σ rows dU: summed from the dU tiles in smem by the cluster wgrad
     sf.fork();
-    r = linear_wgrad(M, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
+    r = linear_wgrad(Mr, D, F, b.xn2, D, st->dbig, F, st->G(st->po(l, kW1)), st->G(st->po(l, kB1)),
                      st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_w1 = sf.mark();
@@ -316,32 +372,41 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
     sf.join(e_wo);   // dx1 is still read by the layer above's Wo gradient
     r = PPLL_ERR_UNSUPPORTED;
     float* part2 = slab();   // this LayerNorm's partial slab (fused or not)
+    // cls-only: the compact dx1 goes to dzc (free after the head), then is
+    // scattered to the cls rows of dx1 (the residual input of the LN1 backward)
+    char* dx1w = cls ? st->dzc : dx1;
     if (st->dtype == PPLL_BF16 && D == 384)
-      r = launch_gemm_ln_bwd(M, F, (const __nv_bfloat16*)st->dbig,
+      r = launch_gemm_ln_bwd(Mr, F, (const __nv_bfloat16*)st->dbig,
                              (const __nv_bfloat16*)st->W(st->po(l, kW1)),
                              (const __nv_bfloat16*)b.x1, b.mean2, b.rstd2, st->P(st->po(l, kLn2g)),
-                             (const __nv_bfloat16*)dx2, (__nv_bfloat16*)dx1, part2,
+                             (const __nv_bfloat16*)dx2, (__nv_bfloat16*)dx1w, part2,
                              st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)),
                              st->G(st->po(l, kBo)), &dfr, s);
     if (r != PPLL_OK && r != PPLL_ERR_UNSUPPORTED) return r;
     if (r == PPLL_ERR_UNSUPPORTED) {
-      r = gemm_dgrad(M, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
+      r = gemm_dgrad(Mr, D, F, st->dbig, F, st->W(st->po(l, kW1)), none, st->dxn, D, st->dtype,
                      st->ws, st->ws_elems, s);
       if (r) return r;
-      r = launch_ln_bwd<TT>(M, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
-                            st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1, D, part2,
+      r = launch_ln_bwd<TT>(Mr, D, (const TT*)st->dxn, D, (const TT*)b.x1, D, b.mean2, b.rstd2,
+                            st->P(st->po(l, kLn2g)), (const TT*)dx2, D, (TT*)dx1w, D, part2,
                             st->G(st->po(l, kLn2g)), st->G(st->po(l, kLn2b)), s,
                             st->G(st->po(l, kBo)), &dfr);
       if (r) return r;
     }
     sf.fork();
-    r = linear_wgrad(M, D, D, b.o, D, dx1, D, st->G(st->po(l, kWo)), nullptr, st->dtype, wsw,
-                     st->ws_elems, sf.ss);
+    r = linear_wgrad(Mr, D, D, b.o, cls ? T * D : D, dx1w, D, st->G(st->po(l, kWo)), nullptr,
+                     st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_wo = sf.mark();
-    r = gemm_dgrad(M, D, D, dx1, D, st->W(st->po(l, kWo)), none, st->dO, D, st->dtype, st->ws,
-                   st->ws_elems, s);
+    r = gemm_dgrad(Mr, D, D, dx1w, D, st->W(st->po(l, kWo)), none, cls ? st->dz : st->dO, D,
+                   st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
+    if (cls) {   // dO and the residual gradient: zero except on the cls rows
+      r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dz, (TT*)st->dO, s);
+      if (r) return r;
+      r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)dx1, s);
+      if (r) return r;
+    }
     sf.join(e_wqkv);   // dqkv is still read by the layer above's Wqkv gradient
     r = attn_bwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
                          b.lse, (TT*)st->dqkv, st->G(st->po(l, kBqkv)), st->attn_bpart, st->ws,
