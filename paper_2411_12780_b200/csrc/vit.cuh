@@ -47,6 +47,14 @@ int launch_gemm_ln_bwd(int M, int K, const __nv_bfloat16* dY, const __nv_bfloat1
 int ln_bwd_blocks(int M);
 template <typename T>
 int launch_attn_fwd(int B, int Tn, int H, int dh, const T* qkv, T* o, float* lse, cudaStream_t s);
+// attention of the cls query alone (head_dim 64): o [B, D] compact, lse [B·H];
+// backward writes the full dqkv (zero Q rows past the cls row) and the
+// per-image column sums of dqkv into bpart [B, 3D] (nullable)
+template <typename T>
+int launch_cls_attn_fwd(int B, int Tn, int H, const T* qkv, T* o, float* lse, cudaStream_t s);
+template <typename T>
+int launch_cls_attn_bwd(int B, int Tn, int H, const T* qkv, const T* o, const T* dout,
+                        const float* lse, T* dqkv, float* bpart, cudaStream_t s);
 template <typename T>
 int launch_attn_bwd(int B, int Tn, int H, int dh, const T* qkv, const T* o, const T* dout,
                     const float* lse, T* dqkv, cudaStream_t s);

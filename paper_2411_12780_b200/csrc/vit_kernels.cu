@@ -1026,6 +1026,179 @@ int launch_embed_bwd(int B, int P, int D, const T* dx, T* dtok, float* dcls, flo
   PPLL_LAUNCH_CHECK();
   return PPLL_OK;
 }
+// ---------------------------------------------------------------------------
+// Attention of the cls query alone (the cls-only top layer of a stage, see
+// vit_stage.cu): per (image, head) one block —
+//   forward   s_j = scale·q₀·k_j, p = softmax(s), o₀ = Σ_j p_j v_j, lse₀;
+//   backward  with dO non-zero on the cls row only: dP_j = dO₀·v_j,
+//             Dsum = dO₀·o₀, dS_j = p_j (dP_j − Dsum),
+//             dV_j = p_j dO₀, dK_j = scale·dS_j q₀, dQ₀ = scale·Σ_j dS_j k_j,
+//             dQ_j = 0 (j > 0); per-image column sums of dqkv into bpart.
+// fp32 arithmetic from T inputs; head_dim 64; any T.  Phase 1: thread = key
+// (dot products over the 64 dims, 16-B loads); phase 2: thread = (dim, key
+// half), fixed-order combination of the halves.
+// ---------------------------------------------------------------------------
+constexpr int kClsThreads = 128;
+
+template <typename T>
+__device__ __forceinline__ float dot64(const T* __restrict__ row, const float* q) {
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < 64; c += 8) {
+    float v[8];
+    ldv<8>(row + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc = fmaf(v[i], q[c + i], acc);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ float block_max128(float v, float* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const float r = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ float block_sum128(float v, float* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const float r = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kClsThreads)
+cls_attn_fwd_kernel(int Tn, int H, const T* __restrict__ qkv, T* __restrict__ o,
+                    float* __restrict__ lse, float scale) {
+  pdl_entry();
+  extern __shared__ float csm[];
+  float* q = csm;              // [64]
+  float* p = q + 64;           // [Tn]
+  float* red = p + Tn;         // [4]
+  float* half = red + 4;       // [64]
+  const int bh = blockIdx.x, b = bh / H, h = bh % H, t = threadIdx.x;
+  const int D = H * 64, D3 = 3 * D;
+  const T* base = qkv + (long)b * Tn * D3;
+  if (t < 64) q[t] = to_f(base[h * 64 + t]) * scale;
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int j = t; j < Tn; j += kClsThreads) {
+    const float sj = dot64(base + (long)j * D3 + D + h * 64, q);
+    p[j] = sj;
+    mx = fmaxf(mx, sj);
+  }
+  mx = block_max128(mx, red);
+  float sum = 0.f;
+  for (int j = t; j < Tn; j += kClsThreads) {
+    const float e = __expf(p[j] - mx);
+    p[j] = e;
+    sum += e;
+  }
+  sum = block_sum128(sum, red);   // (barrier inside: p complete)
+  const float inv = 1.f / sum;
+  const int d = t & 63, hf = t >> 6;
+  const int jm = (Tn + 1) / 2, j0 = hf ? jm : 0, j1 = hf ? Tn : jm;
+  float acc = 0.f;
+  for (int j = j0; j < j1; ++j) acc = fmaf(p[j], to_f(base[(long)j * D3 + 2 * D + h * 64 + d]), acc);
+  if (hf) half[d] = acc;
+  __syncthreads();
+  if (!hf) {
+    DT<T>::st(o + (long)b * D + h * 64 + d, (acc + half[d]) * inv);
+    if (d == 0) lse[bh] = mx + logf(sum);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kClsThreads)
+cls_attn_bwd_kernel(int Tn, int H, const T* __restrict__ qkv, const T* __restrict__ o,
+                    const T* __restrict__ dout, const float* __restrict__ lse,
+                    T* __restrict__ dqkv, float* __restrict__ bpart, float scale) {
+  pdl_entry();
+  extern __shared__ float csm[];
+  float* q = csm;               // [64]  scale·q₀
+  float* g = q + 64;            // [64]  dO₀
+  float* p = g + 64;            // [Tn]
+  float* ds = p + Tn;           // [Tn]
+  float* red = ds + Tn;         // [4]
+  float* hq = red + 4;          // [64] second-half partials: dQ
+  float* hk = hq + 64;          // [64] Σ dK
+  float* hv = hk + 64;          // [64] Σ dV
+  const int bh = blockIdx.x, b = bh / H, h = bh % H, t = threadIdx.x;
+  const int D = H * 64, D3 = 3 * D;
+  const T* base = qkv + (long)b * Tn * D3;
+  float dsum = 0.f;
+  if (t < 64) {
+    q[t] = to_f(base[h * 64 + t]) * scale;
+    const float gd = to_f(dout[(long)b * D + h * 64 + t]);
+    g[t] = gd;
+    dsum = gd * to_f(o[(long)b * D + h * 64 + t]);
+  }
+  dsum = block_sum128(dsum, red);   // Dsum = dO₀·o₀ (barrier inside: q, g complete)
+  const float l0 = lse[bh];
+  for (int j = t; j < Tn; j += kClsThreads) {
+    const T* kr = base + (long)j * D3 + D + h * 64;
+    const float pj = __expf(dot64(kr, q) - l0);
+    const float dpj = dot64(kr + D, g);          // v_j (the V block is D further on)
+    p[j] = pj;
+    ds[j] = pj * (dpj - dsum);
+  }
+  __syncthreads();
+  const int d = t & 63, hf = t >> 6;
+  const int jm = (Tn + 1) / 2, j0 = hf ? jm : 0, j1 = hf ? Tn : jm;
+  const float qd = q[d], gd = g[d];   // q already carries the scale
+  float aq = 0.f, ak = 0.f, av = 0.f;
+  for (int j = j0; j < j1; ++j) {
+    T* row = dqkv + ((long)b * Tn + j) * D3 + h * 64 + d;
+    const float kd = to_f(base[(long)j * D3 + D + h * 64 + d]);
+    aq = fmaf(ds[j], kd, aq);
+    const float dk = ds[j] * qd, dv = p[j] * gd;
+    ak += dk;
+    av += dv;
+    if (j > 0) DT<T>::st(row, 0.f);
+    DT<T>::st(row + D, dk);
+    DT<T>::st(row + 2 * D, dv);
+  }
+  if (hf) { hq[d] = aq; hk[d] = ak; hv[d] = av; }
+  __syncthreads();
+  if (!hf) {
+    const float dq = (aq + hq[d]) * scale;
+    DT<T>::st(dqkv + (long)b * Tn * D3 + h * 64 + d, dq);
+    if (bpart) {
+      float* bp = bpart + (long)b * D3 + h * 64 + d;
+      bp[0] = dq;
+      bp[D] = ak + hk[d];
+      bp[2 * D] = av + hv[d];
+    }
+  }
+}
+
+template <typename T>
+int launch_cls_attn_fwd(int B, int Tn, int H, const T* qkv, T* o, float* lse, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (64 + Tn + 4 + 64);
+  launch_k(cls_attn_fwd_kernel<T>, B * H, kClsThreads, smem, s, Tn, H, qkv, o, lse, 0.125f);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template <typename T>
+int launch_cls_attn_bwd(int B, int Tn, int H, const T* qkv, const T* o, const T* dout,
+                        const float* lse, T* dqkv, float* bpart, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (128 + 2 * Tn + 4 + 192);
+  launch_k(cls_attn_bwd_kernel<T>, B * H, kClsThreads, smem, s, Tn, H, qkv, o, dout, lse, dqkv,
+           bpart, 0.125f);
+  note_launch();
+  PPLL_LAUNCH_CHECK();
+  return PPLL_OK;
+}
+template int launch_cls_attn_fwd<float>(int, int, int, const float*, float*, float*, cudaStream_t);
+template int launch_cls_attn_fwd<__nv_bfloat16>(int, int, int, const __nv_bfloat16*, __nv_bfloat16*, float*, cudaStream_t);
+template int launch_cls_attn_bwd<float>(int, int, int, const float*, const float*, const float*, const float*, float*, float*, cudaStream_t);
+template int launch_cls_attn_bwd<__nv_bfloat16>(int, int, int, const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*, const float*, __nv_bfloat16*, float*, cudaStream_t);
+
 template <typename T>
 int launch_scatter_cls(int B, int Tn, int D, const T* dz, T* dx, cudaStream_t s) {
   const bool v8 = sizeof(T) == 2 && D % 8 == 0 && ((uintptr_t)dz & 15) == 0 && ((uintptr_t)dx & 15) == 0;

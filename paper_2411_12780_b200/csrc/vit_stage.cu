@@ -160,17 +160,17 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
     r = gemm_fwd(M, D, 3 * D, b.xn1, D, st->W(st->po(l, kWqkv)), o1, b.qkv, 3 * D, st->dtype,
                  st->ws, st->ws_elems, s);
     if (r) return r;
-    r = attn_fwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
-    if (r) return r;
     if (cls_top && l == nl - 1) {
-      // cls rows only (row stride T·D in o and in the residual); x1, xn2, u,
-      // h, x2 hold B compact rows
-      const long ldt = (long)T * D;
+      // cls rows only: the cls query's attention (o, lse compact: B rows /
+      // B·H entries), then proj (+ the residual's cls rows, row stride T·D),
+      // LN2, FC1, FC2 on B compact rows
+      r = launch_cls_attn_fwd<TT>(B, T, H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
+      if (r) return r;
       LinOpts o2;
       o2.bias = st->P(st->po(l, kBo));
       o2.res = xcur;
-      o2.ldres = ldt;
-      r = gemm_fwd(B, D, D, b.o, ldt, st->W(st->po(l, kWo)), o2, b.x1, D, st->dtype, st->ws,
+      o2.ldres = (long)T * D;
+      r = gemm_fwd(B, D, D, b.o, D, st->W(st->po(l, kWo)), o2, b.x1, D, st->dtype, st->ws,
                    st->ws_elems, s);
       if (r) return r;
       r = launch_ln_fwd<TT>(B, D, (const TT*)b.x1, D, st->P(st->po(l, kLn2g)),
@@ -194,6 +194,8 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
       xcur = (const TT*)b.x2;
       continue;
     }
+    r = attn_fwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (TT*)b.o, b.lse, s);
+    if (r) return r;
     // proj (+bias, +residual) -> x1 and LN2 -> xn2: one fused launch for bf16
     // D = 384 (gemm_ln.cu), else the GEMM with its residual epilogue + LN kernel
     r = PPLL_ERR_UNSUPPORTED;
@@ -394,23 +396,29 @@ static int vit_backward(ppll_vit_stage* st, int B, const void* x_in, const int64
       if (r) return r;
     }
     sf.fork();
-    r = linear_wgrad(Mr, D, D, b.o, cls ? T * D : D, dx1w, D, st->G(st->po(l, kWo)), nullptr,
+    r = linear_wgrad(Mr, D, D, b.o, D, dx1w, D, st->G(st->po(l, kWo)), nullptr,
                      st->dtype, wsw, st->ws_elems, sf.ss);
     if (r) return r;
     e_wo = sf.mark();
     r = gemm_dgrad(Mr, D, D, dx1w, D, st->W(st->po(l, kWo)), none, cls ? st->dz : st->dO, D,
                    st->dtype, st->ws, st->ws_elems, s);
     if (r) return r;
-    if (cls) {   // dO and the residual gradient: zero except on the cls rows
-      r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dz, (TT*)st->dO, s);
-      if (r) return r;
+    if (cls) {   // the residual gradient: zero except on the cls rows
       r = launch_scatter_cls<TT>(B, T, D, (const TT*)st->dzc, (TT*)dx1, s);
       if (r) return r;
     }
     sf.join(e_wqkv);   // dqkv is still read by the layer above's Wqkv gradient
-    r = attn_bwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
-                         b.lse, (TT*)st->dqkv, st->G(st->po(l, kBqkv)), st->attn_bpart, st->ws,
-                         st->ws_elems, s);
+    if (cls) {   // dO is non-zero on the cls rows only (compact in st->dz)
+      r = launch_cls_attn_bwd<TT>(B, T, H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dz,
+                                  b.lse, (TT*)st->dqkv, st->attn_bpart, s);
+      if (r) return r;
+      r = launch_colsum<float>(B, 3 * D, st->attn_bpart, 3 * D, st->G(st->po(l, kBqkv)), s,
+                               st->ws, st->ws_elems);
+    } else {
+      r = attn_bwd_any<TT>(B, T, H, D / H, (const TT*)b.qkv, (const TT*)b.o, (const TT*)st->dO,
+                           b.lse, (TT*)st->dqkv, st->G(st->po(l, kBqkv)), st->attn_bpart, st->ws,
+                           st->ws_elems, s);
+    }
     if (r) return r;
     sf.fork();
     r = linear_wgrad(M, D, 3 * D, b.xn1, D, st->dqkv, 3 * D, st->G(st->po(l, kWqkv)), nullptr,
