@@ -11,6 +11,7 @@
 #include <math.h>
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 #include <mutex>
 #include <unordered_map>
@@ -535,17 +536,6 @@ template int launch_softmax_xent<__nv_bfloat16>(int, int, const __nv_bfloat16*, 
 // ------------------------------------------------------------------------
 constexpr int kHeadCluster = 8, kHeadWarps = 16, kHeadMaxT = 24;   // K <= 768 in registers
 
-__device__ __forceinline__ float ld_dsmem_f32(const float* p, uint32_t rank) {
-  uint32_t ra, a = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
-  return v;
-}
-__device__ __forceinline__ void head_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
-               ::: "memory");
-}
 
 template <typename T, int NP>
 __global__ void __launch_bounds__(kHeadWarps * 32)
@@ -683,10 +673,10 @@ head_xent_kernel(int B, int K, int C, const T* __restrict__ z, int ldz, const T*
     }
     __syncwarp();
   }
-  head_cluster_sync();   // every CTA's row losses are in its shared memory
+  ptx::cluster_sync();   // every CTA's row losses are in its shared memory
   if (rank == 0 && w == 0) {   // the softmax_xent kernel's fixed-order batch mean
     double s = 0.0;
-    for (int q = lane; q < B; q += 32) s += (double)ld_dsmem_f32(row_loss + q % rpc, q / rpc);
+    for (int q = lane; q < B; q += 32) s += (double)ptx::ld_dsmem_f32(ptx::smem_u32(row_loss + q % rpc), q / rpc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
@@ -695,7 +685,7 @@ head_xent_kernel(int B, int K, int C, const T* __restrict__ z, int ldz, const T*
       if (!isfinite(loss) && err) atomicOr(err, kErrLossNonFinite);
     }
   }
-  head_cluster_sync();   // peers keep their shared memory until rank 0 has read it
+  ptx::cluster_sync();   // peers keep their shared memory until rank 0 has read it
 }
 
 static size_t head_xent_smem(int B, int K, int np, size_t esz) {
