@@ -16,6 +16,7 @@
 // Every tensor is [rows, features] row-major with rows = batch·tokens; the
 // per-layer activations needed by the backward are kept in a workspace sized
 // once for max_batch.
+#include <algorithm>
 #include <type_traits>
 #include <vector>
 #include "common.cuh"
@@ -551,7 +552,10 @@ ppll_vit_stage* ppll_vit_stage_create(const int* cfg, const int64_t* offsets, in
   st->ln_part = (float*)A((size_t)ln_bwd_blocks((int)M) * 3 * D * 4);
   // deferred LN reductions: one partial slab per LN backward of a step
   // (head LN + two per layer), reduced in one batched launch before the update
-  st->ln_slab = (size_t)ln_bwd_blocks((int)M) * 3 * D;
+  // one slab holds the partials of either LN backward form: the persistent
+  // kernel's blocks or the fused GEMM + LN kernel's 128-row tiles (more than
+  // the former past ~37k rows, e.g. ViT-S at batch 1024)
+  st->ln_slab = (size_t)std::max(ln_bwd_blocks((int)M), (int)((M + 127) / 128)) * 3 * D;
   st->ln_parts = (float*)A(st->ln_slab * (2 * st->L.size() + 1) * 4);
   st->cs_part_elems = (size_t)ceil_div((long)M, 32) * st->F;
   st->cs_part = (float*)A(st->cs_part_elems * 4);
