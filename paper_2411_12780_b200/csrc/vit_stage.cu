@@ -131,9 +131,10 @@ static int vit_forward(ppll_vit_stage* st, int B, const void* x_in, void* x_out,
   // loss.  Its LN1 / QKV / attention still run over every token (the cls
   // query attends to all keys and values), but the proj, LN2, FC1 and FC2
   // work — and their backward — is needed for the B cls rows alone; the other
-  // rows' contributions to the loss and to every gradient are exactly zero.
-  // Same values for everything the step produces, ~80 % of the layer's GEMM
-  // work gone.  PPLL_VIT_CLS_TOP=0 runs the layer over all rows.
+  // rows' contributions to the loss and to every gradient are exactly zero:
+  // the same math for everything the step produces (the cls-query attention
+  // rounds in fp32 where the tcgen05 tiles round P to bf16), ~80 % of the
+  // layer's GEMM work gone.  PPLL_VIT_CLS_TOP=0 runs the layer over all rows.
   static const int cls_env = getenv("PPLL_VIT_CLS_TOP") ? atoi(getenv("PPLL_VIT_CLS_TOP")) : 1;
   const bool cls_top = cls_env && head && nl >= 1 && !(nl - 1 == st->n_block - 1 && x_out);
   st->cls_top = cls_top;
