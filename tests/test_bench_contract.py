@@ -64,3 +64,25 @@ def test_reference_arm_line_reports_the_real_batch():
     assert line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["value"] > 0
+
+
+def test_roofline_traffic_capture_is_committed_and_parsed():
+    """The `traffic` of the attention / conv / optimizer roofline entries comes
+    from the committed ncu capture (profiles/r02_ncu_traffic.csv,
+    tools/traffic_probe.py): one DRAM-bytes figure per roofline kernel, equal to
+    the kernel's algorithmic reads (no HBM re-reads) within 2 %."""
+    rows = bench._ncu_launch_traffic()
+    names = [n for n, _ in rows]
+    assert any("attn_tc_fwd" in n for n in names) and any("attn_tc_bwd" in n for n in names)
+    assert sum("conv3x3_tc_kernel" in n for n in names) == 3
+    assert any("nesterov_kernel" in n for n in names)
+    B, T, D = 128, 65, 384
+    M = B * T
+    fwd_reads = 2 * M * 3 * D                                   # qkv
+    bwd_reads = 2 * M * 3 * D + 2 * 2 * M * D + 4 * B * 6 * T   # qkv, o, dO, lse
+    assert abs(bench._traffic_of("attn_tc_fwd") / fwd_reads - 1) < 0.02
+    assert abs(bench._traffic_of("attn_tc_bwd") / bwd_reads - 1) < 0.02
+    for i, (C, H) in enumerate(((16, 32), (32, 16), (64, 8))):
+        x_bytes = 2 * 128 * H * H * C
+        assert abs(bench._traffic_of("conv3x3_tc_kernel", i) / x_bytes - 1) < 0.12
+    assert abs(bench._traffic_of("nesterov_kernel") / (3 * 4 * 373056) - 1) < 0.02
