@@ -1040,16 +1040,19 @@ int launch_embed_bwd(int B, int P, int D, const T* dx, T* dtok, float* dcls, flo
 // ---------------------------------------------------------------------------
 constexpr int kClsThreads = 128;
 
+// dot product of a 64-element row with q (shared memory), eight lanes per row:
+// lane g of the group loads dims [8g, 8g + 8) as one 16-B (bf16) vector — the
+// group reads the row as one coalesced 128-B segment — and the group sums over
+// xor shuffles (offsets 1, 2, 4); every lane of the group returns the sum
 template <typename T>
-__device__ __forceinline__ float dot64(const T* __restrict__ row, const float* q) {
+__device__ __forceinline__ float dot64_g8(const T* __restrict__ row, const float* q, int g) {
+  float v[8];
+  ldv<8>(row + 8 * g, v);
   float acc = 0.f;
 #pragma unroll
-  for (int c = 0; c < 64; c += 8) {
-    float v[8];
-    ldv<8>(row + c, v);
+  for (int i = 0; i < 8; ++i) acc = fmaf(v[i], q[8 * g + i], acc);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc = fmaf(v[i], q[c + i], acc);
-  }
+  for (int o = 1; o < 8; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
 
@@ -1086,12 +1089,18 @@ cls_attn_fwd_kernel(int Tn, int H, const T* __restrict__ qkv, T* __restrict__ o,
   if (t < 64) q[t] = to_f(base[h * 64 + t]) * scale;
   __syncthreads();
   float mx = -INFINITY;
-  for (int j = t; j < Tn; j += kClsThreads) {
-    const float sj = dot64(base + (long)j * D3 + D + h * 64, q);
-    p[j] = sj;
-    mx = fmaxf(mx, sj);
+  {
+    const int g = t & 7, kr = t >> 3;   // 16 keys per pass, eight lanes each
+    for (int j0 = 0; j0 < Tn; j0 += kClsThreads / 8) {
+      const int j = j0 + kr;
+      const float sj = dot64_g8(base + (long)min(j, Tn - 1) * D3 + D + h * 64, q, g);
+      if (j < Tn) {
+        if (g == 0) p[j] = sj;
+        mx = fmaxf(mx, sj);
+      }
+    }
   }
-  mx = block_max128(mx, red);
+  mx = block_max128(mx, red);   // (barrier inside: p complete)
   float sum = 0.f;
   for (int j = t; j < Tn; j += kClsThreads) {
     const float e = __expf(p[j] - mx);
@@ -1139,12 +1148,18 @@ cls_attn_bwd_kernel(int Tn, int H, const T* __restrict__ qkv, const T* __restric
   }
   dsum = block_sum128(dsum, red);   // Dsum = dO₀·o₀ (barrier inside: q, g complete)
   const float l0 = lse[bh];
-  for (int j = t; j < Tn; j += kClsThreads) {
-    const T* kr = base + (long)j * D3 + D + h * 64;
-    const float pj = __expf(dot64(kr, q) - l0);
-    const float dpj = dot64(kr + D, g);          // v_j (the V block is D further on)
-    p[j] = pj;
-    ds[j] = pj * (dpj - dsum);
+  {
+    const int gl = t & 7, kq = t >> 3;   // 16 keys per pass, eight lanes each
+    for (int j0 = 0; j0 < Tn; j0 += kClsThreads / 8) {
+      const int j = j0 + kq;
+      const T* kr = base + (long)min(j, Tn - 1) * D3 + D + h * 64;
+      const float pj = __expf(dot64_g8(kr, q, gl) - l0);
+      const float dpj = dot64_g8(kr + D, g, gl);   // v_j (the V block is D further on)
+      if (j < Tn && gl == 0) {
+        p[j] = pj;
+        ds[j] = pj * (dpj - dsum);
+      }
+    }
   }
   __syncthreads();
   const int d = t & 63, hf = t >> 6;
